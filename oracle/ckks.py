@@ -1,0 +1,643 @@
+"""Oracle RNS-CKKS + SecPE Argmax -- TEST INFRASTRUCTURE ONLY.
+
+Python orchestration over the plain-C core ``ckks_oracle.c``.  Only tests/,
+__graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
+import this module.  Shares no code with paper_2502_00847_b200/.
+
+What each part follows (PAPER.md line numbers; readings R* are listed in DESIGN.md sec. 3):
+  Params / primes ........ PAPER.md:89-93 (R_Q, Q = prod q_i), reading R1
+  encode / decode ........ PAPER.md:98 (SIMD packing), reading R5 (slot j <-> zeta^{5^j})
+  sampler / keygen ....... reading R6/R7 (BASELINE configs[0]: Gaussian sigma=3.2, ternary secret)
+  encrypt / decrypt ...... PAPER.md:139, :143 (Steps 1 and 4)
+  add / sub / mul / rot .. PAPER.md:101-105
+  scale planning ......... reading R9
+  Sign plan .............. PAPER.md:189-195 (Eq. 4 composite, BSGS), reading R13
+  Max .................... PAPER.md:208-210 (Eq. 6)
+  Argmax ................. PAPER.md:214-235 (Algorithm 1), :141 (aggregation), :197-204 (Eq. 5),
+                           :239 (2n slots per argmax)
+"""
+import ctypes
+import math
+import os
+import struct
+import subprocess
+from decimal import Decimal, getcontext
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "ckks_oracle.c")
+
+u64p = ctypes.POINTER(ctypes.c_uint64)
+i64p = ctypes.POINTER(ctypes.c_int64)
+intp = ctypes.POINTER(ctypes.c_int)
+
+
+def build():
+    """Compile the oracle core (plain C, -O2, no fast-math)."""
+    if os.path.exists(_SO) and os.path.getmtime(_SO) >= os.path.getmtime(_SRC):
+        return _SO
+    cmd = ["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC",
+           "-o", _SO, _SRC]
+    subprocess.check_call(cmd)
+    return _SO
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_SO)
+        U, I = ctypes.c_uint64, ctypes.c_int
+        sig = {
+            "o_is_prime": (I, [U]),
+            "o_gen_primes": (I, [I, I, U, I, u64p, I, u64p]),
+            "o_find_psi": (U, [U, I]),
+            "o_mulmod": (U, [U, U, U]),
+            "o_powmod": (U, [U, U, U]),
+            "o_ntt": (None, [u64p, I, U, U]),
+            "o_intt": (None, [u64p, I, U, U]),
+            "o_ntt_naive": (None, [u64p, u64p, I, U, U]),
+            "o_ntt_limbs": (None, [u64p, I, I, u64p, u64p, intp]),
+            "o_intt_limbs": (None, [u64p, I, I, u64p, u64p, intp]),
+            "o_draw": (U, [U, U, U]),
+            "o_tag": (U, [U, U, U]),
+            "o_uniform": (U, [U, U, U, U, I, U]),
+            "o_sample_uniform": (None, [U, U, I, I, u64p, intp, u64p]),
+            "o_sample_ternary": (None, [U, U, I, i64p]),
+            "o_sample_gauss": (None, [U, U, I, u64p, I, i64p]),
+            "o_int_to_ntt": (None, [ctypes.c_void_p, i64p, I, intp, u64p]),
+            "o_keygen_pk": (None, [ctypes.c_void_p, U, u64p, u64p, I, u64p]),
+            "o_keygen_swk": (None, [ctypes.c_void_p, U, U, u64p, u64p, u64p, I, u64p]),
+            "o_encrypt": (None, [ctypes.c_void_p, U, u64p, i64p, I, u64p, I, u64p]),
+            "o_decrypt_residues": (None, [ctypes.c_void_p, u64p, u64p, I, u64p]),
+            "o_add": (None, [ctypes.c_void_p, u64p, u64p, I, I, u64p]),
+            "o_sub": (None, [ctypes.c_void_p, u64p, u64p, I, I, u64p]),
+            "o_mul_int": (None, [ctypes.c_void_p, u64p, I, ctypes.c_int64, u64p]),
+            "o_add_int": (None, [ctypes.c_void_p, u64p, I, ctypes.c_int64, u64p]),
+            "o_mul_plain": (None, [ctypes.c_void_p, u64p, I, u64p, u64p]),
+            "o_tensor": (None, [ctypes.c_void_p, u64p, u64p, I, u64p]),
+            "o_keyswitch": (None, [ctypes.c_void_p, u64p, I, u64p, u64p]),
+            "o_rescale": (None, [ctypes.c_void_p, u64p, I, u64p]),
+            "o_mul_vec": (None, [u64p, u64p, U, U, u64p]),
+            "o_automorph": (None, [ctypes.c_void_p, u64p, I, I, U, u64p]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def P(a):
+    """numpy uint64 array -> pointer (array must be C-contiguous)."""
+    assert a.flags["C_CONTIGUOUS"]
+    if a.dtype == np.uint64:
+        return a.ctypes.data_as(u64p)
+    if a.dtype == np.int64:
+        return a.ctypes.data_as(i64p)
+    if a.dtype == np.int32:
+        return a.ctypes.data_as(intp)
+    raise TypeError(a.dtype)
+
+
+class _OCtx(ctypes.Structure):
+    _fields_ = [("logn", ctypes.c_int), ("nq", ctypes.c_int), ("np", ctypes.c_int),
+                ("alpha", ctypes.c_int), ("primes", u64p), ("psi", u64p)]
+
+
+# ---------------------------------------------------------------------------
+# exact rounding helpers
+# ---------------------------------------------------------------------------
+def round_half_away(x):
+    """Exact round-half-away-from-zero of a Python float -> int."""
+    a = abs(x)
+    f = math.floor(a)
+    r = f + (1 if a - f >= 0.5 else 0)  # a - f is exact (Sterbenz)
+    return int(r) if x >= 0 else -int(r)
+
+
+def round_half_away_np(x):
+    a = np.abs(x)
+    f = np.floor(a)
+    r = f + (a - f >= 0.5)
+    return np.where(x >= 0, r, -r)
+
+
+def dbits(x):
+    """IEEE-754 bit pattern of a double as 16 hex digits (used in op logs)."""
+    return "%016x" % struct.unpack("<Q", struct.pack("<d", float(x)))[0]
+
+
+# ---------------------------------------------------------------------------
+# Parameters (reading R1: prime chains; O-3 psi)
+# ---------------------------------------------------------------------------
+def gen_primes(bits, count, logn, mode, exclude=()):
+    ex = np.array(list(exclude) or [0], dtype=np.uint64)
+    out = np.zeros(count, dtype=np.uint64)
+    got = lib().o_gen_primes(bits, count, 2 << logn, 0 if mode == "nearest" else 1, P(ex),
+                             len(exclude), P(out))
+    if got != count:
+        raise RuntimeError("prime generation failed")
+    return [int(v) for v in out]
+
+
+def cdt_table(sigma=Decimal("3.2"), tail=19):
+    """CDT thresholds T[m] = floor(2^63 F(m)), F = CDF of |X|, X ~ D_{Z,sigma} cut at |X| <= tail.
+    Computed with 60-digit decimal arithmetic (reading R6)."""
+    getcontext().prec = 60
+    sigma = Decimal(sigma)
+    rho = [(-(Decimal(j * j)) / (2 * sigma * sigma)).exp() for j in range(tail + 1)]
+    tot = rho[0] + 2 * sum(rho[1:])
+    out, acc = [], rho[0]
+    two63 = Decimal(2) ** 63
+    for m in range(tail + 1):
+        if m > 0:
+            acc += 2 * rho[m]
+        out.append(int((two63 * acc / tot).to_integral_value(rounding="ROUND_FLOOR")))
+    out[-1] = 1 << 63
+    return np.array(out, dtype=np.uint64)
+
+
+class Params:
+    """RNS-CKKS parameters: ring degree N = 2^logn, chain q_0..q_L, special primes p, digit size alpha."""
+
+    def __init__(self, desc):
+        self.desc = desc
+        self.logn = desc["logn"]
+        self.N = 1 << self.logn
+        primes = []
+        for mode, bits, cnt in desc["q"]:
+            primes += gen_primes(bits, cnt, self.logn, mode, primes)
+        self.nq = len(primes)
+        for mode, bits, cnt in desc["p"]:
+            primes += gen_primes(bits, cnt, self.logn, mode, primes)
+        self.np_ = len(primes) - self.nq
+        self.primes = primes
+        self.q = primes[: self.nq]
+        self.p = primes[self.nq:]
+        self.alpha = desc["alpha"]
+        self.scale = float(2 ** desc["log_scale"])
+        self.psi = [int(lib().o_find_psi(q, self.logn)) for q in primes]
+        self.primes_np = np.array(primes, dtype=np.uint64)
+        self.psi_np = np.array(self.psi, dtype=np.uint64)
+        self.cdt = cdt_table()
+        self._c = _OCtx(self.logn, self.nq, self.np_, self.alpha, P(self.primes_np), P(self.psi_np))
+        self.cptr = ctypes.cast(ctypes.pointer(self._c), ctypes.c_void_p)
+
+    @property
+    def L(self):
+        return self.nq - 1
+
+    def beta(self, level):
+        return (level + 1 + self.alpha - 1) // self.alpha
+
+
+# ---------------------------------------------------------------------------
+# NTT helpers
+# ---------------------------------------------------------------------------
+def ntt(a, q, psi, logn):
+    a = np.ascontiguousarray(a, dtype=np.uint64).copy()
+    lib().o_ntt(P(a), logn, q, psi)
+    return a
+
+
+def intt(a, q, psi, logn):
+    a = np.ascontiguousarray(a, dtype=np.uint64).copy()
+    lib().o_intt(P(a), logn, q, psi)
+    return a
+
+
+def ntt_limbs(a, prm, pids, inverse=False):
+    """In-place-free batched NTT of array [..., nl, N] with limb l under prime index pids[l]."""
+    a = np.ascontiguousarray(a, dtype=np.uint64).copy()
+    nl = a.shape[-2]
+    flat = a.reshape(-1, nl, prm.N)
+    ids = np.array(pids, dtype=np.int32)
+    f = lib().o_intt_limbs if inverse else lib().o_ntt_limbs
+    for b in range(flat.shape[0]):
+        blk = np.ascontiguousarray(flat[b])
+        f(P(blk), prm.logn, nl, P(prm.primes_np), P(prm.psi_np), P(ids))
+        flat[b] = blk
+    return flat.reshape(a.shape)
+
+
+# ---------------------------------------------------------------------------
+# Encoding (reading R5): slot j <-> evaluation at zeta^{5^j mod 2N}, zeta = e^{i pi / N}
+# m_k = round_half_away((2 Delta / N) Re sum_j z_j zeta^{-5^j k})
+# ---------------------------------------------------------------------------
+def _rot_group(N):
+    e = np.empty(N // 2, dtype=np.int64)
+    v = 1
+    for j in range(N // 2):
+        e[j] = v
+        v = (v * 5) % (2 * N)
+    return e
+
+
+def encode_real(prm, z, scale):
+    """Real coefficients (before rounding) of the scaled encoding, via numpy's FFT (a library step)."""
+    N = prm.N
+    z = np.zeros(N // 2, dtype=np.complex128) if z is None else np.asarray(z, dtype=np.complex128)
+    zz = np.zeros(N // 2, dtype=np.complex128)
+    zz[: len(z)] = z
+    e = _rot_group(N)
+    w = np.zeros(2 * N, dtype=np.complex128)
+    w[e] = zz
+    w[(2 * N - e) % (2 * N)] = np.conj(zz)
+    W = w[1::2]  # W[t] = w[2t+1]
+    k = np.arange(N)
+    zeta_mk = np.exp(-1j * np.pi * k / N)
+    m = zeta_mk * np.fft.fft(W) / N
+    return m.real * scale
+
+
+def encode(prm, z, scale):
+    """Integer plaintext coefficients (int64) of slot vector z at the given scale."""
+    r = round_half_away_np(encode_real(prm, z, scale))
+    if np.max(np.abs(r)) >= 2.0 ** 62:
+        raise OverflowError("encoded coefficient exceeds 2^62")
+    return r.astype(np.int64)
+
+
+def encode_naive(prm, z, scale):
+    """O(N^2) evaluation of the encoding definition (pins only, small N)."""
+    N = prm.N
+    zz = np.zeros(N // 2, dtype=np.complex128)
+    zz[: len(z)] = z
+    e = _rot_group(N)
+    k = np.arange(N)
+    M = np.exp(-1j * np.pi * np.outer(e, k) / N)  # zeta^{-5^j k}
+    s = (zz[:, None] * M).sum(axis=0)
+    return round_half_away_np(2.0 * scale / N * s.real).astype(np.int64)
+
+
+def decode(prm, m, scale):
+    """z_j = (1/scale) sum_k m_k zeta^{5^j k}; m real/integer coefficients (float array)."""
+    N = prm.N
+    m = np.asarray(m, dtype=np.float64)
+    k = np.arange(N)
+    v = np.fft.ifft(m * np.exp(1j * np.pi * k / N)) * N  # v[t] = sum_k m_k zeta^k omega^{tk}
+    e = _rot_group(N)
+    return v[(e - 1) // 2] / scale
+
+
+def mask_coeffs(prm, mask_slots, delta_m, quant_bits=24):
+    """Quantised plaintext-mask encoding (reading R16): M_k = rha(delta_m * rha(m_k 2^24) / 2^24),
+    m_k the unit-scale real coefficients of the mask."""
+    mk = encode_real(prm, mask_slots, 1.0)
+    qk = round_half_away_np(mk * float(2 ** quant_bits)) / float(2 ** quant_bits)
+    return round_half_away_np(delta_m * qk).astype(np.int64)
+
+
+# ---------------------------------------------------------------------------
+# CRT (O-4): centered lift of residues [nl][N]
+# ---------------------------------------------------------------------------
+def crt_centered(res, primes):
+    nl = res.shape[0]
+    Q = 1
+    for q in primes[:nl]:
+        Q *= q
+    acc = np.zeros(res.shape[1], dtype=object)
+    for i in range(nl):
+        qi = primes[i]
+        Qi = Q // qi
+        c = pow(Qi % qi, -1, qi)
+        r = res[i].astype(object)
+        acc = acc + ((r * c) % qi) * Qi
+    acc = acc % Q
+    return np.where(acc > Q // 2, acc - Q, acc)
+
+
+# ---------------------------------------------------------------------------
+# Ciphertexts and keys
+# ---------------------------------------------------------------------------
+class Ct:
+    __slots__ = ("data", "scale")
+
+    def __init__(self, data, scale):
+        self.data = np.ascontiguousarray(data, dtype=np.uint64)
+        self.scale = float(scale)
+
+    @property
+    def level(self):
+        return self.data.shape[1] - 1
+
+    def copy(self):
+        return Ct(self.data.copy(), self.scale)
+
+
+def galois_elt(prm, steps):
+    """RotL(s): g = 5^s mod 2N; RotR(s) = RotL(N/2 - s) (reading R2)."""
+    N = prm.N
+    s = steps % (N // 2)
+    return pow(5, s, 2 * N)
+
+
+class Keys:
+    pass
+
+
+class Oracle:
+    """Oracle evaluator: plain CKKS ops on Ct objects (every op logged for plan comparison)."""
+
+    def __init__(self, prm):
+        self.prm = prm
+        self.log = []
+        self.counts = {}
+
+    # ---- keys ----------------------------------------------------------------
+    def keygen(self, seed, rot_steps=()):
+        prm = self.prm
+        L = lib()
+        N, ne = prm.N, prm.nq + prm.np_
+        k = Keys()
+        k.seed = seed
+        s = np.zeros(N, dtype=np.int64)
+        L.o_sample_ternary(seed, L.o_tag(1, 0, 0), prm.logn, P(s))
+        k.s = s
+        k.s_ntt = np.zeros((ne, N), dtype=np.uint64)
+        L.o_int_to_ntt(prm.cptr, P(s), ne, P(np.arange(ne, dtype=np.int32)), P(k.s_ntt))
+        k.pk = np.zeros((2, prm.nq, N), dtype=np.uint64)
+        L.o_keygen_pk(prm.cptr, seed, P(k.s_ntt), P(prm.cdt), len(prm.cdt), P(k.pk))
+        # relinearisation key: s' = s^2
+        s2 = np.zeros((prm.nq, N), dtype=np.uint64)
+        for t in range(prm.nq):
+            q = prm.primes[t]
+            lib().o_mul_vec(P(np.ascontiguousarray(k.s_ntt[t])), P(np.ascontiguousarray(k.s_ntt[t])), N, q, P(s2[t]))
+        k.rlk = self._swk(seed, 0, k.s_ntt, s2)
+        k.gk = {}
+        for st in rot_steps:
+            g = galois_elt(prm, st)
+            if g in k.gk:
+                continue
+            sg = self.automorph_poly(k.s_ntt[: prm.nq], g)
+            k.gk[g] = self._swk(seed, g, k.s_ntt, sg)
+        return k
+
+    def _swk(self, seed, g, s_ntt, sp_ntt):
+        prm = self.prm
+        beta = prm.beta(prm.L)
+        out = np.zeros((beta, 2, prm.nq + prm.np_, prm.N), dtype=np.uint64)
+        sp = np.ascontiguousarray(sp_ntt, dtype=np.uint64)
+        lib().o_keygen_swk(prm.cptr, seed, g, P(s_ntt), P(sp), P(prm.cdt), len(prm.cdt), P(out))
+        return out
+
+    def automorph_poly(self, poly_ntt, g):
+        """sigma_g of a single polynomial [nl][N] in NTT form (via the coefficient domain)."""
+        nl = poly_ntt.shape[0]
+        src = np.ascontiguousarray(poly_ntt[None], dtype=np.uint64)
+        out = np.zeros_like(src)
+        lib().o_automorph(self.prm.cptr, P(src), nl, 1, g, P(out))
+        return out[0]
+
+    # ---- encrypt / decrypt -----------------------------------------------------
+    def encrypt_int(self, keys, m, level, scale, seed):
+        prm = self.prm
+        m = np.ascontiguousarray(m, dtype=np.int64)
+        ct = np.zeros((2, level + 1, prm.N), dtype=np.uint64)
+        lib().o_encrypt(prm.cptr, seed, P(keys.pk), P(m), level, P(prm.cdt), len(prm.cdt), P(ct))
+        return Ct(ct, scale)
+
+    def encrypt(self, keys, z, scale, seed, level=None):
+        level = self.prm.L if level is None else level
+        return self.encrypt_int(keys, encode(self.prm, z, scale), level, scale, seed)
+
+    def decrypt_int(self, keys, ct):
+        """Centered integer coefficients of c0 + c1 s mod Q_level (Python ints)."""
+        prm = self.prm
+        out = np.zeros((ct.level + 1, prm.N), dtype=np.uint64)
+        lib().o_decrypt_residues(prm.cptr, P(keys.s_ntt), P(ct.data), ct.level, P(out))
+        return crt_centered(out, prm.primes)
+
+    def decrypt(self, keys, ct):
+        m = self.decrypt_int(keys, ct)
+        return decode(self.prm, np.array([float(v) for v in m]), ct.scale)
+
+    # ---- logging ------------------------------------------------------------------
+    def _log(self, kind, lin, lout, scale, extra=""):
+        self.log.append("%s %d %d %s %s" % (kind, lin, lout, dbits(scale), extra))
+        self.counts[kind] = self.counts.get(kind, 0) + 1
+
+    # ---- primitive ops (no logging; used by the planned ops below and by tests) ----------
+    def drop(self, ct, level):
+        if level > ct.level:
+            raise ValueError("cannot raise level")
+        return Ct(ct.data[:, : level + 1].copy(), ct.scale)
+
+    def _align(self, a, b):
+        lv = min(a.level, b.level)
+        if a.scale != b.scale:
+            raise ValueError("scale mismatch %r vs %r" % (a.scale, b.scale))
+        return self.drop(a, lv), self.drop(b, lv)
+
+    def add_raw(self, a, b):
+        a, b = self._align(a, b)
+        out = np.zeros_like(a.data)
+        lib().o_add(self.prm.cptr, P(a.data), P(b.data), a.level + 1, 2, P(out))
+        return Ct(out, a.scale)
+
+    def sub_raw(self, a, b):
+        a, b = self._align(a, b)
+        out = np.zeros_like(a.data)
+        lib().o_sub(self.prm.cptr, P(a.data), P(b.data), a.level + 1, 2, P(out))
+        return Ct(out, a.scale)
+
+    def mul_int_raw(self, a, C):
+        out = np.zeros_like(a.data)
+        lib().o_mul_int(self.prm.cptr, P(a.data), a.level + 1, int(C), P(out))
+        return out
+
+    def add_int_raw(self, a, C):
+        out = np.zeros_like(a.data)
+        lib().o_add_int(self.prm.cptr, P(a.data), a.level + 1, int(C), P(out))
+        return out
+
+    def mul_plain_raw(self, a, pt_ntt):
+        out = np.zeros_like(a.data)
+        pt = np.ascontiguousarray(pt_ntt[: a.level + 1])
+        lib().o_mul_plain(self.prm.cptr, P(a.data), a.level + 1, P(pt), P(out))
+        return out
+
+    def tensor(self, a, b):
+        nl = a.level + 1
+        d = np.zeros((3, nl, self.prm.N), dtype=np.uint64)
+        lib().o_tensor(self.prm.cptr, P(a.data), P(b.data), nl, P(d))
+        return d
+
+    def keyswitch(self, d, swk):
+        nl = d.shape[0]
+        ks = np.zeros((2, nl, self.prm.N), dtype=np.uint64)
+        dd = np.ascontiguousarray(d)
+        lib().o_keyswitch(self.prm.cptr, P(dd), nl, P(swk), P(ks))
+        return ks
+
+    def mul_relin(self, keys, a, b):
+        """ct x ct -> tensor -> relinearise (no rescale); scale S_a S_b."""
+        if a.level != b.level:
+            raise ValueError("level mismatch")
+        d = self.tensor(a, b)
+        ks = self.keyswitch(d[2], keys.rlk)
+        out = np.zeros((2, a.level + 1, self.prm.N), dtype=np.uint64)
+        lib().o_add(self.prm.cptr, P(np.ascontiguousarray(d[:2])), P(ks), a.level + 1, 2, P(out))
+        return Ct(out, a.scale * b.scale)
+
+    def rescale(self, ct, new_scale=None):
+        nl = ct.level + 1
+        out = np.zeros((2, nl - 1, self.prm.N), dtype=np.uint64)
+        lib().o_rescale(self.prm.cptr, P(ct.data), nl, P(out))
+        s = ct.scale / float(self.prm.primes[ct.level]) if new_scale is None else new_scale
+        return Ct(out, s)
+
+    def rotate_raw(self, keys, ct, steps):
+        g = galois_elt(self.prm, steps)
+        if g == 1:
+            return ct.copy()
+        if g not in keys.gk:
+            raise KeyError("no Galois key for step %d" % steps)
+        nl = ct.level + 1
+        sig = np.zeros_like(ct.data)
+        lib().o_automorph(self.prm.cptr, P(ct.data), nl, 2, g, P(sig))
+        ks = self.keyswitch(np.ascontiguousarray(sig[1]), keys.gk[g])
+        out = np.zeros_like(ct.data)
+        o0 = np.zeros((nl, self.prm.N), dtype=np.uint64)
+        lib().o_add(self.prm.cptr, P(np.ascontiguousarray(sig[0])), P(np.ascontiguousarray(ks[0])), nl, 1, P(o0))
+        out[0] = o0
+        out[1] = ks[1]
+        return Ct(out, ct.scale)
+
+    # ---- planned ops (logged; reading R9 scale planning) ------------------------------------
+    def rot(self, keys, x, steps):
+        g = galois_elt(self.prm, steps)
+        out = self.rotate_raw(keys, x, steps)
+        self._log("ROT", x.level, out.level, out.scale, str(g))
+        return out
+
+    def add(self, a, b):
+        out = self.add_raw(a, b)
+        self._log("ADD", max(a.level, b.level), out.level, out.scale)
+        return out
+
+    def sub(self, a, b):
+        out = self.sub_raw(a, b)
+        self._log("SUB", max(a.level, b.level), out.level, out.scale)
+        return out
+
+    def mul_const(self, x, c, target_scale, target_level):
+        """c * x landing at (target_scale, target_level): drop x to target_level + 1,
+        Delta_c = (S_t * q_{l}) / S_x, C = rha(c * Delta_c), multiply, rescale, scale := S_t."""
+        lv = target_level + 1
+        x = self.drop(x, lv)
+        dc = (target_scale * float(self.prm.primes[lv])) / x.scale
+        C = round_half_away(c * dc)
+        if abs(C) >= 2 ** 62:
+            raise OverflowError("constant too large")
+        y = Ct(self.mul_int_raw(x, C), x.scale * dc)
+        out = self.rescale(y, target_scale)
+        self._log("MULC", lv, target_level, target_scale, str(C))
+        return out
+
+    def mul_ct(self, keys, a, b, target_scale, target_level):
+        """a (x) b: drop both to target_level + 1, tensor + relinearise + rescale.
+        Output scale := target_scale if given else (S_a * S_b) / q_l."""
+        lv = target_level + 1
+        a = self.drop(a, lv)
+        b = self.drop(b, lv)
+        prod = self.mul_relin(keys, a, b)
+        s = (a.scale * b.scale) / float(self.prm.primes[lv]) if target_scale is None else target_scale
+        out = self.rescale(prod, s)
+        self._log("MULCT", lv, target_level, s)
+        return out
+
+    def mul_mask(self, x, mask_slots, target_scale):
+        """x * mask (plaintext), Delta_m = (S_t * q_l) / S_x, quantised encoding (R16), rescale."""
+        prm = self.prm
+        lv = x.level
+        dm = (target_scale * float(prm.primes[lv])) / x.scale
+        M = mask_coeffs(prm, mask_slots, dm)
+        pt = np.zeros((lv + 1, prm.N), dtype=np.uint64)
+        lib().o_int_to_ntt(prm.cptr, P(M), lv + 1, P(np.arange(lv + 1, dtype=np.int32)), P(pt))
+        y = Ct(self.mul_plain_raw(x, pt), x.scale * dm)
+        out = self.rescale(y, target_scale)
+        self._log("MULP", lv, lv - 1, target_scale, dbits(dm))
+        return out
+
+    def add_const(self, x, c):
+        C = round_half_away(c * x.scale)
+        out = Ct(self.add_int_raw(x, C), x.scale)
+        self._log("ADDC", x.level, x.level, x.scale, str(C))
+        return out
+
+
+# ---------------------------------------------------------------------------
+# Plaintext mirror: the same planned ops on float slot vectors (O-16)
+# ---------------------------------------------------------------------------
+class MirrorCt:
+    __slots__ = ("v", "level", "scale")
+
+    def __init__(self, v, level, scale):
+        self.v, self.level, self.scale = v, level, scale
+
+
+class Mirror:
+    """Executes the plan on doubles with identical level/scale bookkeeping; exact slot semantics."""
+
+    def __init__(self, prm):
+        self.prm = prm
+        self.log = []
+        self.counts = {}
+
+    _log = Oracle._log
+
+    def _check(self, a, b):
+        if a.scale != b.scale:
+            raise ValueError("scale mismatch")
+        return min(a.level, b.level)
+
+    def rot(self, keys, x, steps):
+        out = MirrorCt(np.roll(x.v, -steps), x.level, x.scale)
+        self._log("ROT", x.level, x.level, x.scale, str(galois_elt(self.prm, steps)))
+        return out
+
+    def add(self, a, b):
+        lv = self._check(a, b)
+        self._log("ADD", max(a.level, b.level), lv, a.scale)
+        return MirrorCt(a.v + b.v, lv, a.scale)
+
+    def sub(self, a, b):
+        lv = self._check(a, b)
+        self._log("SUB", max(a.level, b.level), lv, a.scale)
+        return MirrorCt(a.v - b.v, lv, a.scale)
+
+    def mul_const(self, x, c, target_scale, target_level):
+        lv = target_level + 1
+        if x.level < lv:
+            raise ValueError("level")
+        dc = (target_scale * float(self.prm.primes[lv])) / x.scale
+        C = round_half_away(c * dc)
+        self._log("MULC", lv, target_level, target_scale, str(C))
+        return MirrorCt(c * x.v, target_level, target_scale)
+
+    def mul_ct(self, keys, a, b, target_scale, target_level):
+        lv = target_level + 1
+        if a.level < lv or b.level < lv:
+            raise ValueError("level")
+        s = (a.scale * b.scale) / float(self.prm.primes[lv]) if target_scale is None else target_scale
+        self._log("MULCT", lv, target_level, s)
+        return MirrorCt(a.v * b.v, target_level, s)
+
+    def mul_mask(self, x, mask_slots, target_scale):
+        lv = x.level
+        dm = (target_scale * float(self.prm.primes[lv])) / x.scale
+        self._log("MULP", lv, lv - 1, target_scale, dbits(dm))
+        return MirrorCt(x.v * mask_slots, lv - 1, target_scale)
+
+    def add_const(self, x, c):
+        C = round_half_away(c * x.scale)
+        self._log("ADDC", x.level, x.level, x.scale, str(C))
+        return MirrorCt(x.v + c, x.level, x.scale)

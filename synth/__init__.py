@@ -1,0 +1,87 @@
+"""Seeded synthetic workloads shared by the oracle tests, the CUDA parity tests and bench.py.
+
+This module holds NO arithmetic of the method: only workload shapes (BASELINE.json
+configs, restated as data) and numpy PCG64 random draws.  Prime chains, NTT tables,
+encodings, packing and every homomorphic step are implemented separately by
+``oracle/`` and by ``paper_2502_00847_b200/``.
+
+Recipe: per-prompt logits ~ N(0, sigma=2) iid per
+(query, prompt, class), softmax over classes -> scores in [0, 1]; the toy config draws
+scores ~ U[0,1] and keeps a query only if its mean-over-prompts top-1 gap is >= 0.1.
+"""
+import numpy as np
+
+# Parameter sets.  Prime segments: (mode, bits, count); mode "nearest" = primes == 1 mod 2N
+# closest to 2^bits alternating above/below; "below" = largest primes below 2^bits,
+# descending.  Every segment excludes the primes generated before it (q first, then p).
+PARAM_SETS = {
+    # BASELINE configs[0]: 8 x 40-bit primes + 1 special 50-bit prime, scale 2^40, N = 2^12.
+    "toy": dict(logn=12, q=[("nearest", 40, 8)], p=[("below", 50, 1)], alpha=1, log_scale=40),
+    # Same ring with a 17-prime chain for the end-to-end toy argmax (reading R20).
+    "toy_argmax": dict(logn=12, q=[("nearest", 40, 17)], p=[("below", 50, 1)], alpha=1, log_scale=40),
+    # Tiny ring for fast CPU pins of every primitive (not a BASELINE config).
+    "tiny": dict(logn=6, q=[("nearest", 30, 4)], p=[("below", 31, 2)], alpha=2, log_scale=25),
+    "tiny_deep": dict(logn=8, q=[("below", 60, 1), ("nearest", 40, 16)], p=[("below", 61, 2)],
+                      alpha=3, log_scale=40),
+    # configs[4]'s prime structure on a 2^12 ring: CPU-sized check of the (7,15,15) circuit numerics.
+    "argmax_small": dict(logn=12, q=[("below", 60, 1), ("nearest", 45, 29)], p=[("below", 60, 8)],
+                         alpha=10, log_scale=45),
+    # BASELINE configs[1]: NTT microbench, 24 x 60-bit primes, N = 2^16.
+    "ntt": dict(logn=16, q=[("below", 60, 24)], p=[], alpha=24, log_scale=50),
+    # BASELINE configs[2]/[3]: 24 x 60-bit q, dnum = 3 -> alpha = 8, 8 special 60-bit primes, scale 2^50.
+    "ks": dict(logn=16, q=[("below", 60, 24)], p=[("below", 60, 8)], alpha=8, log_scale=50),
+    # BASELINE configs[4]: q_0 60-bit, q_1..q_29 ~ 2^45, 8 x 60-bit special, dnum = 3 (alpha = 10), scale 2^45.
+    "argmax": dict(logn=16, q=[("below", 60, 1), ("nearest", 45, 29)], p=[("below", 60, 8)],
+                   alpha=10, log_scale=45),
+}
+
+# SecPE layouts ("2n slots per argmax"; BASELINE configs[4]):
+# query q, prompt p, class k -> slot q*block + p*K + k.
+LAYOUTS = {
+    "toy": dict(queries=1, prompts=4, classes=4, block=16),
+    "argmax_k2": dict(queries=2048, prompts=8, classes=2, block=16),
+    "argmax_k16": dict(queries=256, prompts=8, classes=16, block=128),
+    "argmax_small_k2": dict(queries=128, prompts=8, classes=2, block=16),
+}
+
+KEY_SEED_BASE = 0x5EC9E000
+
+
+def rng(seed):
+    return np.random.Generator(np.random.PCG64(seed))
+
+
+def softmax_scores(seed, queries, prompts, classes, sigma=2.0):
+    """Per-prompt class scores: logits ~ N(0, sigma) iid, softmax over classes. Shape (q, P, K)."""
+    g = rng(seed)
+    logits = g.normal(0.0, sigma, size=(queries, prompts, classes))
+    e = np.exp(logits - logits.max(axis=2, keepdims=True))
+    return e / e.sum(axis=2, keepdims=True)
+
+
+def toy_scores(seed, queries, prompts, classes, gap=0.1):
+    """Scores ~ U[0,1]; keep a query only if its mean-over-prompts top-1 gap >= gap (rejection)."""
+    g = rng(seed)
+    out = np.empty((queries, prompts, classes))
+    i = 0
+    while i < queries:
+        s = g.uniform(0.0, 1.0, size=(prompts, classes))
+        m = np.sort(s.mean(axis=0))
+        if m[-1] - m[-2] >= gap:
+            out[i] = s
+            i += 1
+    return out
+
+
+def uniform_residues(seed, primes, n_polys, logn):
+    """uint64 array (n_polys, len(primes), 2^logn), limb l uniform in [0, primes[l])."""
+    g = rng(seed)
+    n = 1 << logn
+    out = np.empty((n_polys, len(primes), n), dtype=np.uint64)
+    for l, q in enumerate(primes):
+        out[:, l, :] = g.integers(0, int(q), size=(n_polys, n), dtype=np.uint64)
+    return out
+
+
+def uniform_slots(seed, n, lo=-1.0, hi=1.0):
+    return rng(seed).uniform(lo, hi, size=n)

@@ -1,0 +1,534 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix (no GPU needed).
+
+Every check here recomputes the expected value by an independent route (Python big integers,
+sympy/mpmath, schoolbook products, closed forms, brute force on tiny inputs) -- never by
+re-calling the oracle routine under test.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import sympy
+import mpmath
+
+import synth
+from oracle import ckks, plan
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_examples.json")))
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    return ckks.Params(synth.PARAM_SETS["tiny"])
+
+
+@pytest.fixture(scope="module")
+def toy():
+    return ckks.Params(synth.PARAM_SETS["toy"])
+
+
+def brv(x, bits):
+    return int(format(x, "0%db" % bits)[::-1], 2)
+
+
+# ---------------------------------------------------------------------------------------------
+# O-1 primes, O-3 psi
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["tiny", "toy", "toy_argmax", "ks", "argmax"])
+def test_prime_chain(name):
+    d = synth.PARAM_SETS[name]
+    logn = d["logn"]
+    two_n = 2 << logn
+    primes = []
+    for segs in (d["q"], d["p"]):
+        for mode, bits, cnt in segs:
+            # independent walk with sympy primality
+            base, got, k = 1 << bits, [], 0
+            while len(got) < cnt:
+                cands = [base + 1 + k * two_n, base + 1 - (k + 1) * two_n] if mode == "nearest" else \
+                        [base + 1 - (k + 1) * two_n]
+                for c in cands:
+                    if len(got) < cnt and sympy.isprime(c) and c not in primes and c not in got:
+                        got.append(c)
+                k += 1
+            primes += got
+    assert ckks.Params(d).primes == primes
+    for q in primes:
+        assert q % two_n == 1 and q < 2 ** 62
+
+
+@pytest.mark.parametrize("q,logn", [(7681, 8), (12289, 10), (257, 7), (65537, 12)])
+def test_psi_is_smallest_root_bruteforce(q, logn):
+    n = 1 << logn
+    want = min(x for x in range(2, q) if pow(x, n, q) == q - 1)
+    assert ckks.lib().o_find_psi(q, logn) == want
+
+
+def test_psi_real_primes(toy):
+    for q, psi in zip(toy.primes[:3], toy.psi[:3]):
+        n = toy.N
+        assert pow(psi, n, q) == q - 1
+        g = sympy.primitive_root(q)
+        r = pow(g, (q - 1) // (2 * n), q)
+        r2 = r * r % q
+        roots, cur = [], r
+        for _ in range(n):
+            roots.append(cur)
+            cur = cur * r2 % q
+        assert psi == min(roots)
+
+
+# ---------------------------------------------------------------------------------------------
+# O-3 NTT
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("logn", [3, 4, 6])
+def test_ntt_definition_bigint(logn):
+    q = 7681 if logn <= 7 else 12289
+    n = 1 << logn
+    psi = ckks.lib().o_find_psi(q, logn)
+    a = np.random.default_rng(logn).integers(0, q, n).astype(np.uint64)
+    want = [sum(int(a[k]) * pow(psi, (2 * brv(i, logn) + 1) * k, q) for k in range(n)) % q for i in range(n)]
+    assert [int(v) for v in ckks.ntt(a, q, psi, logn)] == want
+
+
+def test_ntt_roundtrip_and_convolution(toy):
+    rng = np.random.default_rng(5)
+    for logn, q in [(6, 7681), (8, 7681)]:
+        n = 1 << logn
+        psi = ckks.lib().o_find_psi(q, logn)
+        a = rng.integers(0, q, n).astype(np.uint64)
+        b = rng.integers(0, q, n).astype(np.uint64)
+        assert np.array_equal(ckks.intt(ckks.ntt(a, q, psi, logn), q, psi, logn), a)
+        # schoolbook negacyclic product mod (X^N + 1, q)
+        c = [0] * n
+        for i in range(n):
+            for j in range(n):
+                v = int(a[i]) * int(b[j])
+                if i + j < n:
+                    c[i + j] += v
+                else:
+                    c[i + j - n] -= v
+        c = [x % q for x in c]
+        A, B = ckks.ntt(a, q, psi, logn), ckks.ntt(b, q, psi, logn)
+        prod = np.array([(int(x) * int(y)) % q for x, y in zip(A, B)], dtype=np.uint64)
+        assert [int(v) for v in ckks.intt(prod, q, psi, logn)] == c
+    # full-size round trip on a 40-bit toy prime
+    q, psi = toy.primes[0], toy.psi[0]
+    a = rng.integers(0, q, toy.N).astype(np.uint64)
+    assert np.array_equal(ckks.intt(ckks.ntt(a, q, psi, toy.logn), q, psi, toy.logn), a)
+
+
+# ---------------------------------------------------------------------------------------------
+# O-6 sampler
+# ---------------------------------------------------------------------------------------------
+def test_splitmix_stream_matches_sequential_generator():
+    # the counter form equals the sequential SplitMix64 recurrence started at s0
+    M = (1 << 64) - 1
+    G = 0x9E3779B97F4A7C15
+
+    def mix(z):
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        return z ^ (z >> 31)
+
+    seed, tag = 12345, ckks.lib().o_tag(4, 5, 2)
+    assert tag == (4 << 48) ^ (5 << 8) ^ 2
+    state = mix(seed ^ mix((tag + G) & M))
+    for ctr in range(6):
+        state = (state + G) & M
+        assert ckks.lib().o_draw(seed, tag, ctr) == mix(state)
+
+
+def test_cdt_table_mpmath():
+    mpmath.mp.prec = 200
+    sigma = mpmath.mpf(16) / 5
+    rho = [mpmath.exp(-mpmath.mpf(j * j) / (2 * sigma ** 2)) for j in range(20)]
+    tot = rho[0] + 2 * sum(rho[1:])
+    acc, want = mpmath.mpf(0), []
+    for m in range(20):
+        acc += rho[m] if m == 0 else 2 * rho[m]
+        want.append(int(mpmath.floor(mpmath.mpf(2) ** 63 * acc / tot)))
+    want[-1] = 1 << 63
+    assert [int(v) for v in ckks.cdt_table()] == want
+
+
+def test_sampler_moments(toy):
+    L = ckks.lib()
+    n = 1 << 16
+    t = np.zeros(n, dtype=np.int64)
+    L.o_sample_ternary(7, 99, 16, ckks.P(t))
+    counts = np.bincount(t + 1, minlength=3)
+    chi2 = ((counts - n / 3) ** 2 / (n / 3)).sum()
+    assert set(np.unique(t)) <= {-1, 0, 1} and chi2 < 20
+    e = np.zeros(n, dtype=np.int64)
+    L.o_sample_gauss(7, 98, 16, ckks.P(toy.cdt), len(toy.cdt), ckks.P(e))
+    assert abs(e.mean()) < 0.05 and abs(e.std() - 3.2) < 0.05 and np.abs(e).max() <= 19
+    # exact discrete Gaussian pmf vs histogram (chi^2 over |e| <= 8)
+    rho = np.exp(-np.arange(-19, 20) ** 2 / (2 * 3.2 ** 2))
+    p = rho / rho.sum()
+    hist = np.array([(e == v).sum() for v in range(-8, 9)])
+    exp = n * p[19 - 8: 19 + 9]
+    assert ((hist - exp) ** 2 / exp).sum() < 60
+    # uniform mod q: mean and bucket chi^2
+    q = toy.primes[0]
+    u = np.array([L.o_uniform(3, 5, 0, k, 12, q) for k in range(4096)], dtype=np.float64)
+    assert u.max() < q and abs(u.mean() / q - 0.5) < 0.02
+    h = np.histogram(u / q, bins=16, range=(0, 1))[0]
+    assert ((h - 256) ** 2 / 256).sum() < 45
+
+
+# ---------------------------------------------------------------------------------------------
+# O-7 keys, O-8 encryption
+# ---------------------------------------------------------------------------------------------
+def ntt_def(vals, q, psi, logn):
+    n = 1 << logn
+    return [sum(int(vals[k]) * pow(psi, (2 * brv(i, logn) + 1) * k, q) for k in range(n)) % q for i in range(n)]
+
+
+def test_switching_key_gadget_identity(tiny):
+    """b_j + a_j s - e_j == [P]_t s' [t in D_j]   (Python big ints, NTT by definition)."""
+    prm, ev = tiny, ckks.Oracle(tiny)
+    keys = ev.keygen(11, [1])
+    L = ckks.lib()
+    N, ne = prm.N, prm.nq + prm.np_
+    # the secret itself: ternary stream, NTT by definition
+    s = np.zeros(N, dtype=np.int64)
+    L.o_sample_ternary(11, L.o_tag(1, 0, 0), prm.logn, ckks.P(s))
+    for t in range(ne):
+        q = prm.primes[t]
+        assert [int(v) for v in keys.s_ntt[t]] == ntt_def([int(x) % q for x in s], q, prm.psi[t], prm.logn)
+    P_ = 1
+    for p in prm.p:
+        P_ *= p
+    for j in range(prm.beta(prm.L)):
+        e = np.zeros(N, dtype=np.int64)
+        L.o_sample_gauss(11, L.o_tag(5, 0, j), prm.logn, ckks.P(prm.cdt), len(prm.cdt), ckks.P(e))
+        for t in range(ne):
+            q = prm.primes[t]
+            en = ntt_def([int(x) % q for x in e], q, prm.psi[t], prm.logn)
+            b, a = keys.rlk[j, 0, t], keys.rlk[j, 1, t]
+            lhs = [(int(b[k]) + int(a[k]) * int(keys.s_ntt[t, k]) - en[k]) % q for k in range(N)]
+            in_digit = t < prm.nq and t // prm.alpha == j
+            rhs = [((P_ % q) * int(keys.s_ntt[t, k]) ** 2) % q if in_digit else 0 for k in range(N)]
+            assert lhs == rhs
+
+
+def test_encrypt_decrypt(toy):
+    ev = ckks.Oracle(toy)
+    keys = ev.keygen(3)
+    z = synth.uniform_slots(1, toy.N // 2)
+    ct = ev.encrypt(keys, z, toy.scale, 9)
+    assert np.abs(ev.decrypt(keys, ct).real - z).max() < 2 ** -20
+    # bit-level: decrypt_int - m is the small encryption noise
+    m = ckks.encode(toy, z, toy.scale)
+    noise = ev.decrypt_int(keys, ct) - m.astype(object)
+    assert max(abs(int(v)) for v in noise) < 2 ** 14
+
+
+# ---------------------------------------------------------------------------------------------
+# O-9..O-12 homomorphic ops
+# ---------------------------------------------------------------------------------------------
+def test_rescale_exact_bigint(tiny):
+    prm = tiny
+    rng = np.random.default_rng(2)
+    nl = prm.nq
+    data = np.stack([np.stack([rng.integers(0, q, prm.N).astype(np.uint64) for q in prm.q]) for _ in range(2)])
+    ct = ckks.Ct(data, 1.0)
+    out = ckks.Oracle(prm).rescale(ct)
+    ids = list(range(nl))
+    coef = ckks.ntt_limbs(data, prm, ids, inverse=True)
+    coef_out = ckks.ntt_limbs(out.data, prm, ids[:-1], inverse=True)
+    Q = 1
+    for q in prm.q:
+        Q *= q
+    ql = prm.q[-1]
+    Qd = Q // ql
+    for b in range(2):
+        for k in range(prm.N):
+            c = 0
+            for i in range(nl):  # CRT, independent of the oracle's crt_centered
+                Qi = Q // prm.q[i]
+                c += int(coef[b, i, k]) * Qi * pow(Qi, -1, prm.q[i])
+            c %= Q
+            want = ((c + ql // 2) // ql) % Qd
+            for i in range(nl - 1):
+                assert int(coef_out[b, i, k]) == want % prm.q[i]
+
+
+def _centered(x, Q):
+    x %= Q
+    return x - Q if x > Q // 2 else x
+
+
+def test_keyswitch_bigint_bound(tiny):
+    """<KS(d), (1, s)> - d s^2 is small mod Q_l (reading R10/R11), checked with big ints."""
+    prm, ev = tiny, ckks.Oracle(tiny)
+    keys = ev.keygen(4)
+    rng = np.random.default_rng(8)
+    for level in (prm.L, prm.L - 1):
+        nl = level + 1
+        d = np.stack([rng.integers(0, q, prm.N).astype(np.uint64) for q in prm.q[:nl]])
+        ks = ev.keyswitch(d, keys.rlk)
+        Q = 1
+        for q in prm.q[:nl]:
+            Q *= q
+        ids = list(range(nl))
+        # err = ks0 + ks1 s - d s^2  in NTT form, then back to coefficients
+        err = np.zeros((nl, prm.N), dtype=np.uint64)
+        for i, q in enumerate(prm.q[:nl]):
+            s = [int(v) for v in keys.s_ntt[i]]
+            err[i] = [(int(ks[0, i, k]) + int(ks[1, i, k]) * s[k] - int(d[i, k]) * s[k] * s[k]) % q
+                      for k in range(prm.N)]
+        ec = ckks.ntt_limbs(err, prm, ids, inverse=True)
+        for k in range(prm.N):
+            x = 0
+            for i in range(nl):
+                Qi = Q // prm.q[i]
+                x += int(ec[i, k]) * Qi * pow(Qi, -1, prm.q[i])
+            assert abs(_centered(x, Q)) < 2 ** 20
+
+
+def test_ops_against_slots(toy):
+    ev = ckks.Oracle(toy)
+    keys = ev.keygen(5, [1, -1, 3])
+    z1 = synth.uniform_slots(11, toy.N // 2)
+    z2 = synth.uniform_slots(12, toy.N // 2)
+    a = ev.encrypt(keys, z1, toy.scale, 1)
+    b = ev.encrypt(keys, z2, toy.scale, 2)
+    tol = 2 ** -10
+    assert np.abs(ev.decrypt(keys, ev.add_raw(a, b)).real - (z1 + z2)).max() < tol
+    assert np.abs(ev.decrypt(keys, ev.sub_raw(a, b)).real - (z1 - z2)).max() < tol
+    m = ev.rescale(ev.mul_relin(keys, a, b))
+    assert np.abs(ev.decrypt(keys, m).real - z1 * z2).max() < tol
+    for s in (1, -1, 3):
+        r = ev.rotate_raw(keys, a, s)
+        assert np.abs(ev.decrypt(keys, r).real - np.roll(z1, -s)).max() < tol
+    # RotL o RotR = id and additive composition RotL(RotL(a,1),... )
+    back = ev.rotate_raw(keys, ev.rotate_raw(keys, a, 1), -1)
+    assert np.abs(ev.decrypt(keys, back).real - z1).max() < tol
+    # golden: RotL([a0..a3], 1) = [a1, a2, a3, a0]
+    g = GOLD["rotation_direction"]
+    v = np.zeros(toy.N // 2)
+    v[:4] = g["vector"]
+    v[4:] = 0
+    v4 = np.array(g["vector"], dtype=float)
+    full = np.tile(v4, toy.N // 8)
+    r = ev.rotate_raw(keys, ev.encrypt(keys, full, toy.scale, 3), g["steps"])
+    assert np.allclose(ev.decrypt(keys, r).real[:4], g["rotl"], atol=tol)
+    # planned ops: mul_const lands exactly on the target scale and level
+    y = ev.mul_const(a, 0.75, toy.scale, a.level - 2)
+    assert y.level == a.level - 2 and y.scale == toy.scale
+    assert np.abs(ev.decrypt(keys, y).real - 0.75 * z1).max() < tol
+    w = ev.add_const(a, -0.5)
+    assert np.abs(ev.decrypt(keys, w).real - (z1 - 0.5)).max() < tol
+
+
+def test_automorph_is_sigma_g(tiny):
+    """o_automorph == coefficient map X^k -> X^{gk} applied by definition (Python)."""
+    prm, ev = tiny, ckks.Oracle(tiny)
+    rng = np.random.default_rng(1)
+    nl = prm.nq
+    data = np.stack([np.stack([rng.integers(0, q, prm.N).astype(np.uint64) for q in prm.q]) for _ in range(2)])
+    g = ckks.galois_elt(prm, 3)
+    out = ev.automorph_poly(data[0], g)
+    coef = ckks.ntt_limbs(data[0], prm, list(range(nl)), inverse=True)
+    for i, q in enumerate(prm.q):
+        want = [0] * prm.N
+        for k in range(prm.N):
+            e = k * g % (2 * prm.N)
+            if e < prm.N:
+                want[e] = int(coef[i, k])
+            else:
+                want[e - prm.N] = (q - int(coef[i, k])) % q
+        assert [int(v) for v in ntt_def(want, q, prm.psi[i], prm.logn)] == [int(v) for v in out[i]]
+
+
+# ---------------------------------------------------------------------------------------------
+# O-5 encoding
+# ---------------------------------------------------------------------------------------------
+def test_encode_fft_vs_definition(toy):
+    z = synth.uniform_slots(4, toy.N // 2)
+    a = ckks.encode(toy, z, toy.scale)
+    b = ckks.encode_naive(toy, z, toy.scale)
+    assert np.abs(a - b).max() <= 1
+    assert np.abs(ckks.decode(toy, a.astype(float), toy.scale).real - z).max() < 2 ** -25
+
+
+def test_mask_encoding_quantised(toy):
+    lay = synth.LAYOUTS["toy"]
+    m = plan.mask_slots(lay, toy.N // 2)
+    M = ckks.mask_coeffs(toy, m, 2.0 ** 40)
+    back = ckks.decode(toy, M.astype(float), 2.0 ** 40).real
+    assert np.abs(back - m).max() < 2 ** -14
+
+
+# ---------------------------------------------------------------------------------------------
+# O-13 sign plan, O-14 argmax (plaintext mirror)
+# ---------------------------------------------------------------------------------------------
+def load_sign(name):
+    d = json.load(open(os.path.join(os.path.dirname(__file__), "..", "data", name)))
+    return [list(map(float, c)) for c in d["coeffs"]]
+
+
+def horner(stages, x):
+    for c in stages:
+        y = np.zeros_like(x)
+        for cf in reversed(c):
+            y = y * x + cf
+        x = y
+    return x
+
+
+class _Flat:
+    """Mirror inputs at a given level/scale."""
+
+
+@pytest.mark.parametrize("sname", ["sign_7_15_15.json", "sign_f1_f1.json"])
+def test_sign_plan_equals_horner(sname):
+    prm = ckks.Params(synth.PARAM_SETS["argmax"]) if sname.startswith("sign_7") else \
+        ckks.Params(synth.PARAM_SETS["toy_argmax"])
+    st = load_sign(sname)
+    mir = ckks.Mirror(prm)
+    x = np.linspace(-1, 1, 2001)
+    out = plan.sign(mir, None, ckks.MirrorCt(x, prm.L, prm.scale), st, prm.scale)
+    assert np.abs(out.v - horner(st, x)).max() < 1e-9
+    assert out.level == prm.L - plan.sign_depth(st)  # depth law sum ceil(log2(d+1))
+    assert plan.sign_depth(st) == sum(math.ceil(math.log2(len(c))) for c in st)
+    # odd symmetry S(-x) = -S(x)
+    assert np.abs(horner(st, -x) + horner(st, x)).max() < 1e-9
+    # every planned addition saw identical scales, constants fit 62 bits
+    assert all(abs(int(l.split()[4])) < 2 ** 62 for l in mir.log if l.startswith("MULC "))
+
+
+def test_sign_certificate_7_15_15():
+    """Certifier: max |1 - S| over >= 10^6 grid points on [2^-7, 1] (+1e5 random)."""
+    st = load_sign("sign_7_15_15.json")
+    x = np.concatenate([np.linspace(2.0 ** -7, 1, 1_000_001),
+                        np.random.default_rng(0).uniform(2.0 ** -7, 1, 100_000)])
+    err = np.abs(1 - horner(st, x)).max()
+    assert err < 1.2e-4
+    # range preservation on [-1, 1]
+    assert np.abs(horner(st, np.linspace(-1, 1, 200001))).max() < 1 + 1.2e-4
+
+
+def test_paper_layout_and_op_law():
+    g = GOLD["batching"]
+    assert g["slots"] // (2 * g["n"]) == g["argmax_per_ct"]
+    lay = dict(queries=g["argmax_per_ct"], prompts=1, classes=g["n"], block=2 * g["n"])
+    plan.check_layout(lay, g["slots"])
+    # op-count law through the mirror: log n + 1 Sign, log n + 1 rotations
+    prm = ckks.Params(synth.PARAM_SETS["argmax"])
+    for n in (2, 4, 16, 256):
+        mir = ckks.Mirror(prm)
+        lay = dict(queries=1, prompts=1, classes=n, block=2 * n)
+        calls = {"sign": 0}
+        orig = plan.sign
+
+        def counting(ev, keys, x, stages, s):
+            calls["sign"] += 1
+            return orig(ev, keys, x, stages, s)
+
+        plan.sign = counting
+        try:
+            # a 1-stage degree-3 sign keeps the depth within the 30-level chain for n <= 256
+            st = [[0.0, 1.5, 0.0, -0.5]]
+            plan.argmax(mir, None, ckks.MirrorCt(np.zeros(prm.N // 2), prm.L, prm.scale), lay, st)
+        except ValueError:
+            pass
+        finally:
+            plan.sign = orig
+        if n <= 4:
+            assert calls["sign"] == int(math.log2(n)) + 1
+            assert mir.counts["ROT"] == int(math.log2(n)) + 1
+    assert GOLD["op_law"]["sign_ops"] == int(math.log2(GOLD["op_law"]["n"])) + 1
+
+
+def test_argmax_mirror_examples():
+    """SPEC.md:246, :259-260, :326 examples through the planned circuit on doubles."""
+    prm = ckks.Params(synth.PARAM_SETS["argmax"])
+    st = load_sign("sign_7_15_15.json")
+    mir = ckks.Mirror(prm)
+    # Eq. 6 example Max(0.2, 0.8) = 0.8
+    g = GOLD["max_example"]
+    r = ckks.MirrorCt(np.full(4, g["a"]), prm.L, prm.scale)
+    y = ckks.MirrorCt(np.full(4, g["b"]), prm.L, prm.scale)
+    assert abs(plan.hom_max(mir, None, r, y, st).v[0] - g["max"]) < 1e-3
+    for key in ("argmax_window", "argmax_ties"):
+        g = GOLD[key]
+        lay = dict(queries=1, prompts=1, classes=4, block=8)
+        z = np.zeros(prm.N // 2)
+        z[:4] = g["window"]
+        out = plan.argmax(ckks.Mirror(prm), None, ckks.MirrorCt(z, prm.L, prm.scale), lay, st)
+        # the polynomial Sign is not exact: y_max undershoots the max by ~|S - 1| |a - b| / 2,
+        # which the steep Sign near 0 turns into a ~1e-2 deficit on the winning slot
+        assert np.abs(out.v[:4] - np.array(g["one_hot"])).max() < 2e-2
+    # vote example: 3 prompts is not a power of two -> pad prompts with zeros (reading R17)
+    g = GOLD["vote_example"]
+    logits = np.array(g["logits"], dtype=float)
+    norm = (logits - g["d_min"]) / (g["d_max"] - g["d_min"])  # Eq. 5
+    scores = np.zeros((1, 4, 2))
+    scores[0, :3] = norm
+    lay = dict(queries=1, prompts=4, classes=2, block=8)
+    z = plan.pack(scores, lay, prm.N // 2)
+    out = plan.argmax(ckks.Mirror(prm), None, ckks.MirrorCt(z, prm.L, prm.scale), lay, st)
+    assert plan.labels(out.v, lay)[0] == g["label"]
+    assert np.allclose(logits.mean(axis=0), g["mean"])
+
+
+def test_argmax_mirror_random_labels():
+    prm = ckks.Params(synth.PARAM_SETS["argmax"])
+    st = load_sign("sign_7_15_15.json")
+    lay = synth.LAYOUTS["argmax_k2"]
+    scores = synth.softmax_scores(1000 * 5 + 1, lay["queries"], lay["prompts"], lay["classes"])
+    z = plan.pack(scores, lay, prm.N // 2)
+    out = plan.argmax(ckks.Mirror(prm), None, ckks.MirrorCt(z, prm.L, prm.scale), lay, st)
+    mean = scores.mean(axis=1)
+    gap = np.abs(mean[:, 0] - mean[:, 1])
+    ok = gap >= 2.0 ** -7
+    assert (plan.labels(out.v, lay)[ok] == plan.true_labels(scores)[ok]).all()
+    assert out.level == prm.L - plan.argmax_depth(lay, st) == 5
+
+
+@pytest.mark.slow
+def test_toy_argmax_end_to_end_oracle():
+    """Full toy argmax on oracle ciphertexts: labels exact, values within 2^-10 of the mirror."""
+    prm = ckks.Params(synth.PARAM_SETS["toy_argmax"])
+    st = load_sign("sign_f1_f1.json")
+    lay = dict(synth.LAYOUTS["toy"])
+    lay["queries"] = 8
+    scores = synth.toy_scores(1001, lay["queries"], lay["prompts"], lay["classes"])
+    z = plan.pack(scores, lay, prm.N // 2)
+    ev = ckks.Oracle(prm)
+    keys = ev.keygen(synth.KEY_SEED_BASE + 1, plan.argmax_rotations(lay))
+    ct = ev.encrypt(keys, z, prm.scale, 77)
+    out = plan.argmax(ev, keys, ct, lay, st)
+    mir = ckks.Mirror(prm)
+    ref = plan.argmax(mir, None, ckks.MirrorCt(z, prm.L, prm.scale), lay, st)
+    assert ev.log == mir.log
+    dec = ev.decrypt(keys, out).real
+    assert np.abs(dec - ref.v).max() < 2 ** -10
+    assert (plan.labels(dec, lay) == plan.true_labels(scores)).all()
+
+
+@pytest.mark.slow
+def test_argmax_small_ring_7_15_15_oracle():
+    """configs[4] circuit (q0 60-bit, 29 x 45-bit, dnum 3, (7,15,15) Sign, K=2, P=8) on a 2^12 ring."""
+    prm = ckks.Params(synth.PARAM_SETS["argmax_small"])
+    st = load_sign("sign_7_15_15.json")
+    lay = synth.LAYOUTS["argmax_small_k2"]
+    scores = synth.softmax_scores(5001, lay["queries"], lay["prompts"], lay["classes"])
+    z = plan.pack(scores, lay, prm.N // 2)
+    ev = ckks.Oracle(prm)
+    keys = ev.keygen(synth.KEY_SEED_BASE + 5, plan.argmax_rotations(lay))
+    ct = ev.encrypt(keys, z, prm.scale, 55)
+    out = plan.argmax(ev, keys, ct, lay, st)
+    mir = ckks.Mirror(prm)
+    ref = plan.argmax(mir, None, ckks.MirrorCt(z, prm.L, prm.scale), lay, st)
+    assert ev.log == mir.log and out.level == 5
+    dec = ev.decrypt(keys, out).real
+    assert np.abs(dec - ref.v).max() < 2 ** -10
+    mean = scores.mean(axis=1)
+    ok = np.abs(mean[:, 0] - mean[:, 1]) >= 2.0 ** -7
+    assert (plan.labels(dec, lay)[ok] == plan.true_labels(scores)[ok]).all()
