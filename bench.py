@@ -1,0 +1,289 @@
+#!/usr/bin/env python
+"""SecPE encrypted aggregate-then-Argmax benchmark on B200 (BASELINE.json metric and configs[4]).
+
+One step = the whole hot path (prompt aggregation, mask/normalise, duplicate, QuickMax, final Sign + 1;
+SURVEY.md 8(a) H1-H6, i.e. PAPER.md:141-142 + Algorithm 1) over a batch of B packed ciphertexts,
+each holding 2048 queries x P=8 prompts x K=2 classes at N = 2^16 (30 limbs, scale 2^45, dnum 3).
+value = query-argmax/s over all ranks (weak scaling: B ciphertexts per rank, no data-path collective).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl secpe|reference]
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "encrypted argmax/s at N=2^16; NTT & key-switch HBM GB/s vs peak"
+UNIT = "query-argmax/s"
+WORKLOAD = "configs[4]: SecPE encrypted prompt-ensemble aggregation + Argmax, N=2^16, L=30 (q0 60-bit + 29x45-bit), " \
+           "scale 2^45, dnum=3 (8x60-bit special), 2048 queries x P=8 x K=2 per ciphertext, Sign (7,15,15) eps=2^-7"
+
+
+def peaks():
+    try:
+        m = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(m["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_sign(name):
+    d = json.load(open(os.path.join(ROOT, "data", name)))
+    return [list(map(float, c)) for c in d["coeffs"]]
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.p = index, None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        rows = [l.split(",") for l in out.strip().splitlines() if l.count(",") >= 6]
+        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[3 + i] and "Not" not in r[3 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------------------------------------
+# reference arm / cpu baseline: the CPU oracle as it stands
+# ------------------------------------------------------------------------------------------------
+def oracle_argmax_once(seed_base=1):
+    """Full oracle argmax of ONE configs[4] ciphertext (2048 queries).  Returns (seconds, queries, threads)."""
+    import synth
+    from oracle import ckks, plan
+    prm = ckks.Params(synth.PARAM_SETS["argmax"])
+    lay = synth.LAYOUTS["argmax_k2"]
+    st = load_sign("sign_7_15_15.json")
+    ev = ckks.Oracle(prm)
+    keys = ev.keygen(synth.KEY_SEED_BASE + 5, plan.argmax_rotations(lay))
+    scores = synth.softmax_scores(1000 * 5 + seed_base, lay["queries"], lay["prompts"], lay["classes"])
+    ct = ev.encrypt(keys, plan.pack(scores, lay, prm.N // 2), prm.scale, 11)
+    t0 = time.perf_counter()
+    plan.argmax(ev, keys, ct, lay, st)
+    dt = time.perf_counter() - t0
+    return dt, lay["queries"], int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+
+
+def run_reference(a):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    for _ in range(a.warmup if a.ref_warmup else 0):
+        oracle_argmax_once()
+    times, q = [], 0
+    for _ in range(a.steps):
+        dt, q, cores = oracle_argmax_once()
+        times.append(dt)
+    T = sum(times)
+    v = q * a.steps / T
+    sample = "1 ciphertext (2048 queries x P=8 x K=2, full argmax circuit) per step; warm-up steps %s" % (
+        "run" if a.ref_warmup else "skipped (CPU oracle has no warm-up state)")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": 1000 * T / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64 (RNS residues)", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "batch_per_step": 1},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------------
+def run_secpe(a):
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2502_00847_b200 import build, secpe
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    build.build()
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    desc = synth.PARAM_SETS["argmax"]
+    lay = synth.LAYOUTS["argmax_k2"]
+    st = load_sign("sign_7_15_15.json")
+    ctx = secpe.Context(desc, stream=stream.cuda_stream)
+    steps_rot = secpe.argmax_rotations(lay)
+    # evaluation keys: every rank derives the same keys from the same client seed (replicated, no transfer)
+    keys = ctx.keygen(synth.KEY_SEED_BASE + 5, steps_rot)
+    B = a.batch
+    L = ctx.L
+    inp = ctx.new_ct(L, B)
+    for i in range(B):
+        scores = synth.softmax_scores(1000 * 5 + 100 * rank + i, lay["queries"], lay["prompts"], lay["classes"])
+        z = secpe.pack(scores, lay, ctx.N // 2)
+        m = ctx.encode(z, ctx.scale)
+        c = secpe.Ct(inp.t[i:i + 1], L, ctx.scale)
+        ctx.encrypt_coeffs(keys, m, L, ctx.scale, 700 + i, out=c)
+    inp.level, inp.scale = L, ctx.scale
+    ol, _ = ctx.argmax_info(lay, st, L)
+    out = ctx.new_ct(ol, B)
+    torch.cuda.synchronize()
+
+    def step():
+        ctx.enc_argmax(keys, inp, lay, st, out=out)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    ctx.opcounts(reset=True)
+    ctx.profile_begin()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    prof = ctx.profile_end()
+    counts = ctx.opcounts(reset=True)
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    queries = lay["queries"] * B * ws * a.steps
+    value = queries / (ms / 1000.0)
+
+    # end to end through the public API with host buffers (pinned), copies inside the timed region
+    h_in = inp.t.cpu().pin_memory()
+    h_out = torch.empty(out.t.shape, dtype=torch.uint64).pin_memory()
+    d_in = secpe.Ct(torch.empty_like(inp.t), L, ctx.scale)
+    for _ in range(max(1, a.warmup // 2)):
+        d_in.t.copy_(h_in, non_blocking=True)
+        ctx.enc_argmax(keys, d_in, lay, st, out=out)
+        h_out.copy_(out.t, non_blocking=True)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(a.steps):
+        d_in.t.copy_(h_in, non_blocking=True)
+        ctx.enc_argmax(keys, d_in, lay, st, out=out)
+        h_out.copy_(out.t, non_blocking=True)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = f0.elapsed_time(f1)
+    if ws > 1:
+        t = torch.tensor([ms_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    e2e = queries / (ms_e2e / 1000.0)
+
+    if rank != 0:
+        if ws > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = peaks()
+    ntt = prof["ntt"]
+    ks = prof["keyswitch"]
+    ach = ntt["bytes"] / (ntt["ms"] / 1000.0) / 1e9 if ntt["ms"] > 0 else 0.0
+    ks_ach = ks["bytes"] / (ks["ms"] / 1000.0) / 1e9 if ks["ms"] > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ntt_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_limb_transform")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64 (RNS residues mod 45/60-bit primes)", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "ciphertexts_per_rank_per_step": B, "queries_per_ciphertext": lay["queries"],
+                   "parallelism": "ciphertexts sharded over ranks (replicated keys)" if ws > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (%.0f MB ciphertexts + %.0f MB keys per rank)" % (
+                       B * inp.t[0].numel() * 8 / 1e6, 6 * 119.5)},
+        "roofline": {"bound": "hbm", "kernel": "ntt (forward+inverse, all launches in the timed region)",
+                     "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
+                     "peak_source": peak_src,
+                     "algorithmic_bytes_per_limb_transform": 16 * ctx.N,
+                     "ntt_share_of_step": ntt["ms"] / ms if ms else None,
+                     "keyswitch": {"achieved": ks_ach, "frac": ks_ach / peak, "share_of_step": ks["ms"] / ms,
+                                   "unit": "GB/s"},
+                     "rescale_share_of_step": prof["rescale"]["ms"] / ms},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h_in.numel() * 8),
+                "d2h_bytes_per_step": int(h_out.numel() * 8)},
+        "gpu_launches": int(counts["launches"]),
+        "op_counts_per_step": {k: v / a.steps for k, v in counts.items()},
+        "clocks": clk,
+    }
+    if ws == 1 and not a.no_cpu_baseline:
+        dt, q, cores = oracle_argmax_once()
+        line["cpu_baseline"] = {"value": q / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                "sample": "1 ciphertext of the same workload (2048 queries, full argmax circuit), "
+                                          "%.1f s" % dt}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=8, help="ciphertexts per rank per step")
+    ap.add_argument("--impl", default="secpe", choices=["secpe", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-warmup", action="store_true", help="also run oracle warm-up steps (reference arm)")
+    a = ap.parse_args()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_secpe(a)
+
+
+if __name__ == "__main__":
+    main()

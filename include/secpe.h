@@ -1,0 +1,211 @@
+/*
+ * secpe.h -- C ABI of the B200-native SecPE private-voting library (libsecpe.so).
+ *
+ * SecPE (arXiv 2502.00847): the server aggregates encrypted per-prompt class scores and
+ * evaluates an encrypted Argmax (Sec. 3.1; Algorithm 1)
+ * over packed RNS-CKKS ciphertexts (Sec. 2.2).  Every homomorphic step
+ * runs in hand-written sm_100a CUDA kernels on the stream given to secpe_ctx_create /
+ * secpe_set_stream.  There is no CPU fallback: without a CUDA device every call that
+ * computes returns SECPE_ECUDA.
+ *
+ * Conventions (DESIGN.md sections 3 and 5):
+ *  - N = 2^log_n; a polynomial limb is N uint64 residues in [0, q); a ciphertext at level l
+ *    is uint64[2][l+1][N] (c0 limbs then c1 limbs), limb i under prime q_i, NTT (evaluation)
+ *    form, NTT(a)[i] = sum_k a_k psi^{(2 brv(i)+1) k}, psi the smallest primitive 2N-th root.
+ *  - Slots: N/2 complex slots, slot j <-> evaluation at zeta^{5^j mod 2N}; real scores use the
+ *    real parts (reading R5).  RotL(s) uses Galois element 5^s mod 2N and
+ *    RotR(s) = RotL(N/2 - s) (reading R2).
+ *  - Device pointers (marked "dev") are caller-owned, 16-byte aligned, and must stay valid
+ *    until the enqueued work completes.  Host pointers ("host") are read or written before
+ *    the call returns.  The library never frees caller memory.  Context and keys are
+ *    library-owned and immutable after creation (safe to share read-only across threads).
+ *  - Calls enqueue work on the context stream and return; secpe_decrypt*, secpe_key_export,
+ *    secpe_sync and the host-returning calls synchronise.
+ *  - Errors: a negative status; secpe_last_error() returns a thread-local message.
+ *    Nothing throws across the ABI.
+ */
+#ifndef SECPE_H
+#define SECPE_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    SECPE_OK = 0,
+    SECPE_EINVAL = -1,    /* bad argument / shape */
+    SECPE_ELEVEL = -2,    /* not enough levels left for the requested circuit */
+    SECPE_ESCALE = -3,    /* add/sub of ciphertexts whose scales are not bit-identical (reading R9) */
+    SECPE_ENOKEY = -4,    /* no Galois key generated for this rotation */
+    SECPE_ELAYOUT = -5,   /* slot layout does not fit / not a power of two */
+    SECPE_EOVERFLOW = -6, /* an encoded value does not fit the 62-bit integer range */
+    SECPE_ECUDA = -7,     /* CUDA error (including: no device) */
+    SECPE_ENOMEM = -8
+};
+
+typedef struct secpe_ctx secpe_ctx;   /* opaque: parameters + device tables + stream */
+typedef struct secpe_keys secpe_keys; /* opaque: secret/public/relinearisation/Galois keys (device) */
+
+/* RNS-CKKS parameters (R_Q = Z_Q[X]/(X^N+1), Q = prod q_i). */
+typedef struct {
+    uint32_t log_n;     /* 10..17 */
+    uint32_t n_q;       /* ciphertext primes q_0..q_L (L = n_q - 1), each < 2^62, == 1 mod 2N */
+    const uint64_t *q;  /* host[n_q] */
+    uint32_t n_p;       /* special primes for hybrid key switching (>= 1) */
+    const uint64_t *p;  /* host[n_p] */
+    uint32_t alpha;     /* primes per key-switching digit; dnum = ceil(n_q / alpha) */
+    double scale;       /* nominal scale Delta used by the planner for intermediate results */
+} secpe_params;
+
+/* A ciphertext: data = dev uint64[2][level+1][N] (NTT form), scale = its CKKS scale. */
+typedef struct {
+    uint64_t *data;
+    int32_t level;
+    double scale;
+} secpe_ct;
+
+/* Composite odd Sign approximation p_r o ... o p_1 (Eq. 4).
+ * degrees: host[n_stages], each 3, 7 or 15.  coeffs: host, concatenated power-basis
+ * coefficients c_0..c_d of every stage (even ones must be 0). */
+typedef struct {
+    int32_t n_stages;
+    const int32_t *degrees;
+    const double *coeffs;
+} secpe_sign_cfg;
+
+/* Packed slot layout: query q, prompt p, class k -> slot q*block + p*classes + k.
+ * prompts and classes powers of two; prompts*classes <= block; 2*classes <= block;
+ * queries*block <= N/2. */
+typedef struct {
+    int32_t queries;
+    int32_t prompts;
+    int32_t classes;
+    int32_t block;
+} secpe_layout;
+
+/* ---- context ------------------------------------------------------------------------- */
+const char *secpe_last_error(void);
+const char *secpe_version(void);
+
+/* Product-side prime chain generator (reading R1): primes == 1 mod 2^(log_n+1).
+ * mode 0: nearest to 2^bits, alternating above/below (closest first); mode 1: largest below
+ * 2^bits, descending.  Primes in exclude (host[n_exclude]) are skipped.  out: host[count]. */
+int secpe_gen_primes(uint32_t bits, uint32_t count, uint32_t log_n, int32_t mode,
+                     const uint64_t *exclude, uint32_t n_exclude, uint64_t *out);
+
+/* Build the context: twiddle/Shoup tables, CRT and base-conversion constants (device).
+ * stream: a cudaStream_t (NULL = legacy default stream). */
+int secpe_ctx_create(const secpe_params *prm, void *stream, secpe_ctx **out);
+void secpe_ctx_destroy(secpe_ctx *ctx);
+int secpe_set_stream(secpe_ctx *ctx, void *stream);
+int secpe_sync(secpe_ctx *ctx);
+/* host[n_q + n_p] copies of the primes and of psi (the NTT root per prime). */
+int secpe_ctx_info(const secpe_ctx *ctx, uint64_t *primes_out, uint64_t *psi_out);
+size_t secpe_ct_bytes(const secpe_ctx *ctx, int32_t level);
+
+/* ---- keys (client) ---------------------------------------------------------------------
+ * All randomness comes from counter-based SplitMix64 streams of `seed` (reading R6):
+ * ternary secret, public key, relinearisation key (s^2) and one Galois key per distinct
+ * rotation step in rot_steps (host[n_rot]; >0 RotL, <0 RotR).  Hybrid digits (reading R7). */
+int secpe_keygen(secpe_ctx *ctx, uint64_t seed, const int32_t *rot_steps, int32_t n_rot,
+                 secpe_keys **out);
+void secpe_keys_destroy(secpe_keys *keys);
+/* Copy key material to host (synchronises), for parity tests.
+ * which 0: secret s, NTT form over all n_q+n_p primes, uint64[n_q+n_p][N]
+ *       1: public key uint64[2][n_q][N]
+ *       2: relinearisation key uint64[dnum][2][n_q+n_p][N]
+ *       3: Galois key of element `galois` (same shape as 2)
+ * n_words must equal the shape's size. */
+int secpe_key_export(const secpe_ctx *ctx, const secpe_keys *keys, int32_t which, uint64_t galois,
+                     uint64_t *host_out, size_t n_words);
+
+/* ---- encoding / encryption (client, PAPER.md:139 Step 1 and :143 Step 4) ------------------ */
+/* Integer plaintext of host slots[n] (real parts, n <= N/2) at `scale`:
+ * m_k = round_half_away((2 scale / N) Re sum_j z_j zeta^{-5^j k}); host out int64[N]. */
+int secpe_encode(secpe_ctx *ctx, const double *slots, size_t n, double scale, int64_t *coeffs_out);
+/* Encrypt the integer plaintext host coeffs[N] at `level` with the public key; out->data must
+ * hold secpe_ct_bytes(level); out->level/scale are set. */
+int secpe_encrypt_coeffs(secpe_ctx *ctx, const secpe_keys *keys, const int64_t *coeffs,
+                         int32_t level, double scale, uint64_t seed, secpe_ct *out);
+int secpe_encrypt(secpe_ctx *ctx, const secpe_keys *keys, const double *slots, size_t n,
+                  int32_t level, double scale, uint64_t seed, secpe_ct *out);
+/* host out uint64[level+1][N]: residues of c0 + c1 s in coefficient form (synchronises). */
+int secpe_decrypt_residues(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *ct,
+                           uint64_t *host_out);
+/* host slots_out[n] (real parts) = decode(centered lift of c0 + c1 s) / scale (synchronises). */
+int secpe_decrypt(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *ct, double *slots_out,
+                  size_t n);
+
+/* ---- primitives (server; all device buffers) ---------------------------------------------- */
+/* In-place forward / inverse negacyclic NTT of polys dev uint64[n_polys][n_limbs][N];
+ * limb l uses prime index first_prime + l of the chain q_0..q_L, p_0..p_{k-1}. */
+int secpe_ntt(secpe_ctx *ctx, uint64_t *polys, int32_t n_polys, int32_t first_prime, int32_t n_limbs);
+int secpe_intt(secpe_ctx *ctx, uint64_t *polys, int32_t n_polys, int32_t first_prime, int32_t n_limbs);
+
+/* a (+) b, a (-) b.  Levels are aligned by dropping top limbs; scales must be
+ * bit-identical (SECPE_ESCALE).  out may alias a or b; out level = min level. */
+int secpe_add(secpe_ctx *ctx, const secpe_ct *a, const secpe_ct *b, secpe_ct *out);
+int secpe_sub(secpe_ctx *ctx, const secpe_ct *a, const secpe_ct *b, secpe_ct *out);
+/* Add the real constant c: round_half_away(c * scale) on every NTT point of c0. */
+int secpe_add_const(secpe_ctx *ctx, const secpe_ct *a, double c, secpe_ct *out);
+/* c * a landing at (target_scale, target_level) (reading R9): a is dropped to target_level+1,
+ * multiplied by C = round_half_away(c * Delta_c), Delta_c = target_scale * q_{l} / scale_a,
+ * then rescaled.  out level = target_level. */
+int secpe_mul_const(secpe_ctx *ctx, const secpe_ct *a, double c, double target_scale,
+                    int32_t target_level, secpe_ct *out);
+/* a * plaintext mask (host mask_slots[n] real), quantised encoding at
+ * Delta_m = target_scale * q_l / scale_a (reading R16), then rescale; out level = a.level-1. */
+int secpe_mul_mask(secpe_ctx *ctx, const secpe_ct *a, const double *mask_slots, size_t n,
+                   double target_scale, secpe_ct *out);
+/* Drop to a lower level (exact; scale unchanged). */
+int secpe_drop(secpe_ctx *ctx, const secpe_ct *a, int32_t level, secpe_ct *out);
+/* PAPER.md:103 a (x) b: tensor + relinearisation (hybrid key switching, reading R10/R11), no
+ * rescale.  Same level required; out scale = scale_a * scale_b.  out must not alias. */
+int secpe_mul_relin(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *a, const secpe_ct *b,
+                    secpe_ct *out);
+/* Rescale by q_level: round(c / q_l) (round half up, reading R12).  out level = in level - 1,
+ * out scale = scale / q_l.  out must not alias. */
+int secpe_rescale(secpe_ctx *ctx, const secpe_ct *in, secpe_ct *out);
+/* PAPER.md:104-105 RotL(a, steps) (steps < 0: RotR(a, -steps)).  out must not alias. */
+int secpe_rotate(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t steps,
+                 secpe_ct *out);
+
+/* ---- SecPE circuits --------------------------------------------------------------------- */
+/* Composite Sign (Eq. 3-4) with the fixed BSGS plan of reading R13;
+ * out level = in level - sum ceil(log2(d+1)); out scale = target_scale. */
+int secpe_sign_poly(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in,
+                    const secpe_sign_cfg *cfg, double target_scale, secpe_ct *out);
+/* Level and scale of secpe_enc_argmax's outputs for inputs at in_level. */
+int secpe_argmax_info(secpe_ctx *ctx, const secpe_layout *layout, const secpe_sign_cfg *cfg,
+                      int32_t in_level, int32_t *out_level, double *out_scale);
+/* SecPE private voting (PAPER.md:141-142 + Algorithm 1) on n_in packed ciphertexts:
+ * aggregate prompts by rotate-and-sum, mask/normalise (Eq. 5), duplicate, QuickMax with
+ * Eq. 6, Sign(y - y_max) + 1 (Eq. 2).  in: host[n_in] ciphertexts (same level and scale);
+ * out: host[n_in], out[i].data sized for the level secpe_argmax_info reports.  The batch is
+ * evaluated together so every key is read once per op for all n_in ciphertexts.
+ * No secret key is taken or needed. */
+int secpe_enc_argmax(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n_in,
+                     const secpe_layout *layout, const secpe_sign_cfg *cfg, secpe_ct *out);
+
+/* ---- instrumentation ---------------------------------------------------------------------- */
+/* Enable (1) / disable (0) the planned-op log; secpe_oplog_get copies it (NUL-terminated)
+ * into host buf[cap] and returns its full length; secpe_oplog_clear empties it. */
+int secpe_oplog_enable(secpe_ctx *ctx, int32_t on);
+int64_t secpe_oplog_get(secpe_ctx *ctx, char *buf, size_t cap);
+int secpe_oplog_clear(secpe_ctx *ctx);
+/* CUDA-event profile of the NTT, key-switch and rescale spans enqueued between begin and end
+ * (events recorded on the context stream around each span; end synchronises).  out[9]:
+ * per kind k (0 NTT, 1 key switch, 2 rescale): out[3k] total ms, out[3k+1] algorithmic bytes
+ * (NTT: 16 N per limb transform; key switch: (input + output limbs) per ciphertext + key once per
+ * batch; rescale: 2(l+1) + 2l limbs per ciphertext), out[3k+2] units (limb transforms / ciphertexts). */
+int secpe_profile_begin(secpe_ctx *ctx);
+int secpe_profile_end(secpe_ctx *ctx, double *out, int32_t n_out);
+/* host counts[8]: NTT limb-transforms, key switches, rescales, rotations, ct-ct products,
+ * constant products, kernel launches, Sign evaluations. */
+int secpe_opcounts(secpe_ctx *ctx, int64_t *counts, int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,62 @@
+"""Build libsecpe.so in-tree with nvcc for sm_100a (no JIT, no torch extension machinery).
+
+    python -m paper_2502_00847_b200.build          # incremental
+    python -m paper_2502_00847_b200.build --clean
+"""
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "build")
+LIB = os.path.join(HERE, "libsecpe.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-ffp-contract=off",
+         "-Xptxas", "-warn-spills"]
+SOURCES = ["ntt.cu", "ops.cu", "ks.cu", "sample.cu", "context.cu", "eval.cu", "plan.cu", "client.cu",
+           "encode.cpp", "abi.cpp"]
+
+
+def _headers_mtime():
+    hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    hs.append(os.path.join(HERE, "..", "include", "secpe.h"))
+    return max(os.path.getmtime(h) for h in hs)
+
+
+def _compile(src, hm):
+    s = os.path.join(CSRC, src)
+    o = os.path.join(OBJ, src + ".o")
+    if os.path.exists(o) and os.path.getmtime(o) >= max(os.path.getmtime(s), hm):
+        return o, None
+    cmd = [NVCC] + ARCH + FLAGS + ["-x", "cu", "-c", s, "-o", o]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        return o, "%s\n%s\n%s" % (" ".join(cmd), r.stdout, r.stderr)
+    if r.stderr.strip():
+        sys.stderr.write(r.stderr)
+    return o, None
+
+
+def build(clean=False, verbose=False):
+    if clean and os.path.isdir(OBJ):
+        shutil.rmtree(OBJ)
+    os.makedirs(OBJ, exist_ok=True)
+    hm = _headers_mtime()
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        res = list(ex.map(lambda s: _compile(s, hm), SOURCES))
+    errs = [e for _, e in res if e]
+    if errs:
+        raise RuntimeError("nvcc failed:\n" + "\n".join(errs))
+    objs = [o for o, _ in res]
+    if not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lquadmath", "-lcudart"]
+        subprocess.check_call(cmd)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(clean="--clean" in sys.argv))

@@ -1,0 +1,482 @@
+// abi.cpp -- extern "C" entry points of libsecpe.so (declared in include/secpe.h).
+// Exceptions never cross the boundary: every entry point maps them to a status code and a
+// thread-local message (secpe_last_error).
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "../../include/secpe.h"
+#include "context.h"
+
+Keys *keygen(Ctx &c, u64 seed, const int *rot, int n_rot);
+void encrypt_coeffs(Ctx &c, const Keys &k, const i64 *coeffs, int level, u64 seed, u64 *ct);
+void decrypt_residues(Ctx &c, const Keys &k, const CtView &ct, u64 *host_out);
+void decrypt_slots(Ctx &c, const Keys &k, const CtView &ct, double *slots, size_t n);
+
+struct secpe_ctx {
+    Ctx c;
+};
+struct secpe_keys {
+    Keys *k;
+};
+
+static thread_local std::string g_err;
+void set_error(const std::string &m) { g_err = m; }
+
+template <typename F>
+static int guard(F &&f) {
+    try {
+        f();
+        return SECPE_OK;
+    } catch (const SecpeError &e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc &) {
+        g_err = "out of host memory";
+        return SECPE_ENOMEM;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return SECPE_EINVAL;
+    }
+}
+#define REQUIRE(cond, code, msg) \
+    do {                         \
+        if (!(cond)) throw SecpeError{code, msg}; \
+    } while (0)
+
+static CtView view_of(const Ctx &c, const secpe_ct *ct) {
+    REQUIRE(ct && ct->data, SECPE_EINVAL, "null ciphertext");
+    REQUIRE(ct->level >= 0 && ct->level < c.nq, SECPE_EINVAL, "ciphertext level out of range");
+    return compact_view(c, ct->data, 1, ct->level, ct->scale);
+}
+static void set_out(secpe_ct *out, const CtView &v) {
+    out->level = v.level;
+    out->scale = v.scale;
+}
+static SignCfg sign_cfg(const secpe_sign_cfg *cfg) {
+    REQUIRE(cfg && cfg->n_stages > 0 && cfg->degrees && cfg->coeffs, SECPE_EINVAL, "bad sign config");
+    SignCfg s;
+    size_t off = 0;
+    for (int i = 0; i < cfg->n_stages; i++) {
+        const int d = cfg->degrees[i];
+        REQUIRE(d == 3 || d == 7 || d == 15, SECPE_EINVAL, "sign stage degree must be 3, 7 or 15");
+        std::vector<double> c(cfg->coeffs + off, cfg->coeffs + off + d + 1);
+        for (int e = 0; e <= d; e += 2) REQUIRE(c[e] == 0.0, SECPE_EINVAL, "sign polynomials must be odd");
+        s.stages.push_back(c);
+        off += d + 1;
+    }
+    return s;
+}
+static Layout layout_of(const Ctx &c, const secpe_layout *l) {
+    REQUIRE(l, SECPE_EINVAL, "null layout");
+    auto pow2 = [](int v) { return v >= 1 && (v & (v - 1)) == 0; };
+    REQUIRE(pow2(l->prompts) && pow2(l->classes), SECPE_ELAYOUT, "prompts and classes must be powers of two");
+    REQUIRE(l->queries >= 1 && l->prompts * l->classes <= l->block && 2 * l->classes <= l->block &&
+                (long)l->queries * l->block <= c.N / 2,
+            SECPE_ELAYOUT, "layout does not fit the slots");
+    return Layout{l->queries, l->prompts, l->classes, l->block};
+}
+
+extern "C" {
+
+const char *secpe_last_error(void) { return g_err.c_str(); }
+const char *secpe_version(void) { return "secpe-b200 0.1 (sm_100a)"; }
+
+int secpe_gen_primes(uint32_t bits, uint32_t count, uint32_t log_n, int32_t mode, const uint64_t *exclude,
+                     uint32_t n_exclude, uint64_t *out) {
+    return guard([&] {
+        REQUIRE(bits >= 20 && bits <= 62 && out && (mode == 0 || mode == 1), SECPE_EINVAL, "bad prime request");
+        const int got = h_gen_primes((int)bits, (int)count, (int)log_n, mode, exclude, (int)n_exclude, out);
+        REQUIRE(got == (int)count, SECPE_EINVAL, "not enough primes");
+    });
+}
+
+int secpe_ctx_create(const secpe_params *prm, void *stream, secpe_ctx **out) {
+    return guard([&] {
+        REQUIRE(prm && out && prm->q && prm->p, SECPE_EINVAL, "null argument");
+        REQUIRE(prm->log_n >= 11 && prm->log_n <= 17, SECPE_EINVAL, "log_n must be in [11, 17]");
+        REQUIRE(prm->n_q >= 1 && prm->n_p >= 1 && prm->n_q + prm->n_p <= MAXL, SECPE_EINVAL, "prime counts");
+        REQUIRE(prm->alpha >= 1 && prm->alpha <= 16 && (prm->n_q + prm->alpha - 1) / prm->alpha <= 16 &&
+                    prm->n_p <= 16,
+                SECPE_EINVAL, "alpha / dnum / special primes must be <= 16");
+        const u64 two_n = (u64)2 << prm->log_n;
+        for (uint32_t i = 0; i < prm->n_q + prm->n_p; i++) {
+            const u64 v = i < prm->n_q ? prm->q[i] : prm->p[i - prm->n_q];
+            REQUIRE(v > (1ULL << 32) && v < (1ULL << 62) && v % two_n == 1 && h_is_prime(v), SECPE_EINVAL,
+                    "primes must be NTT-friendly primes in (2^32, 2^62)");
+        }
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw SecpeError{SECPE_ECUDA, "no CUDA device: libsecpe has no CPU fallback"};
+        auto h = std::make_unique<secpe_ctx>();
+        h->c.st = (cudaStream_t)stream;
+        h->c.build(prm->q, (int)prm->n_q, prm->p, (int)prm->n_p, (int)prm->alpha, (int)prm->log_n, prm->scale);
+        *out = h.release();
+    });
+}
+void secpe_ctx_destroy(secpe_ctx *ctx) {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->c.st);
+    delete ctx;
+}
+int secpe_set_stream(secpe_ctx *ctx, void *stream) {
+    return guard([&] {
+        REQUIRE(ctx, SECPE_EINVAL, "null ctx");
+        CUDA_CHECK(cudaStreamSynchronize(ctx->c.st));
+        ctx->c.st = (cudaStream_t)stream;
+    });
+}
+int secpe_sync(secpe_ctx *ctx) {
+    return guard([&] {
+        REQUIRE(ctx, SECPE_EINVAL, "null ctx");
+        CUDA_CHECK(cudaStreamSynchronize(ctx->c.st));
+    });
+}
+int secpe_ctx_info(const secpe_ctx *ctx, uint64_t *primes_out, uint64_t *psi_out) {
+    return guard([&] {
+        REQUIRE(ctx, SECPE_EINVAL, "null ctx");
+        if (primes_out) std::memcpy(primes_out, ctx->c.primes.data(), ctx->c.primes.size() * 8);
+        if (psi_out) std::memcpy(psi_out, ctx->c.psi.data(), ctx->c.psi.size() * 8);
+    });
+}
+size_t secpe_ct_bytes(const secpe_ctx *ctx, int32_t level) {
+    if (!ctx || level < 0) return 0;
+    return (size_t)ctx->c.ct_words(level) * 8;
+}
+
+int secpe_keygen(secpe_ctx *ctx, uint64_t seed, const int32_t *rot_steps, int32_t n_rot, secpe_keys **out) {
+    return guard([&] {
+        REQUIRE(ctx && out && (n_rot == 0 || rot_steps), SECPE_EINVAL, "null argument");
+        auto h = std::make_unique<secpe_keys>();
+        h->k = keygen(ctx->c, seed, rot_steps, n_rot);
+        *out = h.release();
+    });
+}
+void secpe_keys_destroy(secpe_keys *keys) {
+    if (!keys) return;
+    delete keys->k;
+    delete keys;
+}
+int secpe_key_export(const secpe_ctx *ctx, const secpe_keys *keys, int32_t which, uint64_t galois, uint64_t *host_out,
+                     size_t n_words) {
+    return guard([&] {
+        REQUIRE(ctx && keys && host_out, SECPE_EINVAL, "null argument");
+        const Ctx &c = ctx->c;
+        const DevBuf *b = nullptr;
+        if (which == 0) b = &keys->k->s;
+        else if (which == 1) b = &keys->k->pk;
+        else if (which == 2) b = &keys->k->rlk;
+        else if (which == 3) {
+            auto it = keys->k->gk.find(galois);
+            REQUIRE(it != keys->k->gk.end(), SECPE_ENOKEY, "no Galois key for this element");
+            b = &it->second;
+        } else
+            throw SecpeError{SECPE_EINVAL, "bad key selector"};
+        REQUIRE(n_words == b->words, SECPE_EINVAL, "n_words does not match the key size");
+        CUDA_CHECK(cudaMemcpyAsync(host_out, b->p, n_words * 8, cudaMemcpyDeviceToHost, c.st));
+        CUDA_CHECK(cudaStreamSynchronize(c.st));
+    });
+}
+
+int secpe_encode(secpe_ctx *ctx, const double *slots, size_t n, double scale, int64_t *coeffs_out) {
+    return guard([&] {
+        REQUIRE(ctx && coeffs_out && (n == 0 || slots), SECPE_EINVAL, "null argument");
+        encode_int(ctx->c, slots, n, scale, coeffs_out);
+    });
+}
+int secpe_encrypt_coeffs(secpe_ctx *ctx, const secpe_keys *keys, const int64_t *coeffs, int32_t level, double scale,
+                         uint64_t seed, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && keys && coeffs && out && out->data, SECPE_EINVAL, "null argument");
+        REQUIRE(level >= 0 && level < ctx->c.nq, SECPE_EINVAL, "level out of range");
+        encrypt_coeffs(ctx->c, *keys->k, coeffs, level, seed, out->data);
+        out->level = level;
+        out->scale = scale;
+    });
+}
+int secpe_encrypt(secpe_ctx *ctx, const secpe_keys *keys, const double *slots, size_t n, int32_t level, double scale,
+                  uint64_t seed, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && keys && out && out->data && (n == 0 || slots), SECPE_EINVAL, "null argument");
+        REQUIRE(level >= 0 && level < ctx->c.nq, SECPE_EINVAL, "level out of range");
+        std::vector<i64> m(ctx->c.N);
+        encode_int(ctx->c, slots, n, scale, m.data());
+        encrypt_coeffs(ctx->c, *keys->k, m.data(), level, seed, out->data);
+        out->level = level;
+        out->scale = scale;
+    });
+}
+int secpe_decrypt_residues(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *ct, uint64_t *host_out) {
+    return guard([&] {
+        REQUIRE(ctx && keys && host_out, SECPE_EINVAL, "null argument");
+        decrypt_residues(ctx->c, *keys->k, view_of(ctx->c, ct), host_out);
+    });
+}
+int secpe_decrypt(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *ct, double *slots_out, size_t n) {
+    return guard([&] {
+        REQUIRE(ctx && keys && slots_out, SECPE_EINVAL, "null argument");
+        decrypt_slots(ctx->c, *keys->k, view_of(ctx->c, ct), slots_out, n);
+    });
+}
+
+static int ntt_common(secpe_ctx *ctx, uint64_t *polys, int32_t n_polys, int32_t first, int32_t n_limbs, bool inv) {
+    return guard([&] {
+        REQUIRE(ctx && polys, SECPE_EINVAL, "null argument");
+        Ctx &c = ctx->c;
+        REQUIRE(n_polys >= 0 && n_limbs >= 1 && first >= 0 && first + n_limbs <= c.nprimes(), SECPE_EINVAL,
+                "limb range out of the prime chain");
+        const long s = (long)n_limbs * c.N;
+        LimbMap lm{n_limbs, std::max(0, std::min(n_limbs, c.nq - first)), first, first <= c.nq ? c.nq : first};
+        if (first >= c.nq) lm = LimbMap{n_limbs, 0, 0, first};
+        ev_ntt(c, RowsArg{polys, 2 * s, s}, n_polys, lm, inv);
+    });
+}
+int secpe_ntt(secpe_ctx *ctx, uint64_t *polys, int32_t n_polys, int32_t first_prime, int32_t n_limbs) {
+    return ntt_common(ctx, polys, n_polys, first_prime, n_limbs, false);
+}
+int secpe_intt(secpe_ctx *ctx, uint64_t *polys, int32_t n_polys, int32_t first_prime, int32_t n_limbs) {
+    return ntt_common(ctx, polys, n_polys, first_prime, n_limbs, true);
+}
+
+int secpe_add(secpe_ctx *ctx, const secpe_ct *a, const secpe_ct *b, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && out && out->data, SECPE_EINVAL, "null argument");
+        CtView va = view_of(ctx->c, a), vb = view_of(ctx->c, b);
+        CtView vo = compact_view(ctx->c, out->data, 1, std::min(va.level, vb.level), va.scale);
+        ev_addsub(ctx->c, va, vb, vo, false);
+        set_out(out, vo);
+    });
+}
+int secpe_sub(secpe_ctx *ctx, const secpe_ct *a, const secpe_ct *b, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && out && out->data, SECPE_EINVAL, "null argument");
+        CtView va = view_of(ctx->c, a), vb = view_of(ctx->c, b);
+        CtView vo = compact_view(ctx->c, out->data, 1, std::min(va.level, vb.level), va.scale);
+        ev_addsub(ctx->c, va, vb, vo, true);
+        set_out(out, vo);
+    });
+}
+int secpe_add_const(secpe_ctx *ctx, const secpe_ct *a, double cval, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && out && out->data, SECPE_EINVAL, "null argument");
+        CtView va = view_of(ctx->c, a);
+        const double Cd = round_half_away(cval * va.scale);
+        REQUIRE(std::fabs(Cd) < 4611686018427387904.0, SECPE_EOVERFLOW, "constant exceeds 2^62");
+        CtView vo = compact_view(ctx->c, out->data, 1, va.level, va.scale);
+        ev_add_int(ctx->c, va, (i64)Cd, vo);
+        set_out(out, vo);
+    });
+}
+int secpe_mul_const(secpe_ctx *ctx, const secpe_ct *a, double cval, double target_scale, int32_t target_level,
+                    secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && out && out->data, SECPE_EINVAL, "null argument");
+        Ctx &c = ctx->c;
+        CtView va = view_of(c, a);
+        const int lv = target_level + 1;
+        REQUIRE(target_level >= 0 && lv <= va.level, SECPE_ELEVEL, "not enough levels");
+        va.level = lv;
+        const double dc = (target_scale * (double)c.primes[lv]) / va.scale;
+        const double Cd = round_half_away(cval * dc);
+        REQUIRE(std::fabs(Cd) < 4611686018427387904.0, SECPE_EOVERFLOW, "constant exceeds 2^62");
+        DevBuf tmp((size_t)c.ct_words(lv), c.st);
+        CtView vt = compact_view(c, tmp.p, 1, lv, va.scale * dc);
+        ev_mul_int(c, va, (i64)Cd, vt);
+        CtView vo = compact_view(c, out->data, 1, target_level, target_scale);
+        ev_rescale(c, vt, vo);
+        set_out(out, vo);
+    });
+}
+int secpe_mul_mask(secpe_ctx *ctx, const secpe_ct *a, const double *mask_slots, size_t n, double target_scale,
+                   secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && out && out->data && mask_slots, SECPE_EINVAL, "null argument");
+        Ctx &c = ctx->c;
+        CtView va = view_of(c, a);
+        const int lv = va.level;
+        REQUIRE(lv >= 1, SECPE_ELEVEL, "not enough levels");
+        const double dm = (target_scale * (double)c.primes[lv]) / va.scale;
+        std::vector<i64> M(c.N);
+        encode_mask(c, mask_slots, n, dm, M.data());
+        DevBuf mi(c.N, c.st), pt((size_t)(lv + 1) * c.N, c.st), tmp((size_t)c.ct_words(lv), c.st);
+        CUDA_CHECK(cudaMemcpyAsync(mi.p, M.data(), c.N * 8, cudaMemcpyHostToDevice, c.st));
+        k_int_to_rows(c.tab, c.logn, (const i64 *)mi.p, pt.p, LimbMap{lv + 1, lv + 1, 0, 0}, c.st);
+        ev_ntt(c, RowsArg{pt.p, 2L * (lv + 1) * c.N, (long)(lv + 1) * c.N}, 1, LimbMap{lv + 1, lv + 1, 0, 0}, false);
+        CtView vt = compact_view(c, tmp.p, 1, lv, va.scale * dm);
+        ev_mul_plain_ntt(c, va, pt.p, vt);
+        CtView vo = compact_view(c, out->data, 1, lv - 1, target_scale);
+        ev_rescale(c, vt, vo);
+        CUDA_CHECK(cudaStreamSynchronize(c.st));
+        set_out(out, vo);
+    });
+}
+int secpe_drop(secpe_ctx *ctx, const secpe_ct *a, int32_t level, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && out && out->data, SECPE_EINVAL, "null argument");
+        CtView va = view_of(ctx->c, a);
+        REQUIRE(level >= 0 && level <= va.level, SECPE_ELEVEL, "cannot raise the level");
+        REQUIRE(out->data != a->data || level == va.level, SECPE_EINVAL, "drop cannot alias");
+        CtView vo = compact_view(ctx->c, out->data, 1, level, va.scale);
+        ev_copy(ctx->c, va, vo);
+        set_out(out, vo);
+    });
+}
+int secpe_mul_relin(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *a, const secpe_ct *b, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && keys && out && out->data, SECPE_EINVAL, "null argument");
+        CtView va = view_of(ctx->c, a), vb = view_of(ctx->c, b);
+        REQUIRE(va.level == vb.level, SECPE_ELEVEL, "mul_relin needs equal levels");
+        CtView vo = compact_view(ctx->c, out->data, 1, va.level, va.scale * vb.scale);
+        ev_mul_relin(ctx->c, *keys->k, va, vb, vo);
+        set_out(out, vo);
+    });
+}
+int secpe_rescale(secpe_ctx *ctx, const secpe_ct *in, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && out && out->data, SECPE_EINVAL, "null argument");
+        CtView vi = view_of(ctx->c, in);
+        REQUIRE(vi.level >= 1, SECPE_ELEVEL, "no level left to rescale");
+        CtView vo = compact_view(ctx->c, out->data, 1, vi.level - 1, vi.scale / (double)ctx->c.primes[vi.level]);
+        ev_rescale(ctx->c, vi, vo);
+        set_out(out, vo);
+    });
+}
+int secpe_rotate(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t steps, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && keys && out && out->data, SECPE_EINVAL, "null argument");
+        CtView vi = view_of(ctx->c, in);
+        CtView vo = compact_view(ctx->c, out->data, 1, vi.level, vi.scale);
+        ev_rotate(ctx->c, *keys->k, vi, steps, vo);
+        set_out(out, vo);
+    });
+}
+
+int secpe_sign_poly(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const secpe_sign_cfg *cfg,
+                    double target_scale, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && keys && out && out->data, SECPE_EINVAL, "null argument");
+        SignCfg sc = sign_cfg(cfg);
+        CtView vi = view_of(ctx->c, in);
+        const int ol = vi.level - sign_depth(sc);
+        REQUIRE(ol >= 0, SECPE_ELEVEL, "not enough levels for the sign polynomial");
+        CtView vo = compact_view(ctx->c, out->data, 1, ol, target_scale);
+        run_sign(ctx->c, *keys->k, vi, sc, target_scale, vo);
+        set_out(out, vo);
+    });
+}
+int secpe_argmax_info(secpe_ctx *ctx, const secpe_layout *layout, const secpe_sign_cfg *cfg, int32_t in_level,
+                      int32_t *out_level, double *out_scale) {
+    return guard([&] {
+        REQUIRE(ctx && out_level && out_scale, SECPE_EINVAL, "null argument");
+        Layout lay = layout_of(ctx->c, layout);
+        SignCfg sc = sign_cfg(cfg);
+        const int ol = in_level - argmax_depth(lay, sc);
+        REQUIRE(ol >= 0, SECPE_ELEVEL, "not enough levels for the argmax circuit");
+        *out_level = ol;
+        *out_scale = ctx->c.scale;
+    });
+}
+int secpe_enc_argmax(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n_in,
+                     const secpe_layout *layout, const secpe_sign_cfg *cfg, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && keys && in && out && n_in >= 1, SECPE_EINVAL, "null argument");
+        Ctx &c = ctx->c;
+        Layout lay = layout_of(c, layout);
+        SignCfg sc = sign_cfg(cfg);
+        const int lv = in[0].level;
+        for (int i = 0; i < n_in; i++) {
+            REQUIRE(in[i].data && out[i].data, SECPE_EINVAL, "null ciphertext data");
+            REQUIRE(in[i].level == lv && in[i].scale == in[0].scale, SECPE_EINVAL,
+                    "batch inputs must share level and scale");
+        }
+        const int ol = lv - argmax_depth(lay, sc);
+        REQUIRE(ol >= 0, SECPE_ELEVEL, "not enough levels for the argmax circuit");
+        const long cw = c.ct_words(lv), ow = c.ct_words(ol);
+        // batch view: reuse the caller's memory if the inputs are laid out contiguously
+        bool contiguous = true;
+        for (int i = 1; i < n_in; i++) contiguous &= in[i].data == in[0].data + (long)i * cw;
+        DevBuf inb, outb;
+        CtView vin = compact_view(c, in[0].data, n_in, lv, in[0].scale);
+        if (!contiguous) {
+            inb = DevBuf((size_t)n_in * cw, c.st);
+            for (int i = 0; i < n_in; i++)
+                CUDA_CHECK(cudaMemcpyAsync(inb.p + (long)i * cw, in[i].data, cw * 8, cudaMemcpyDeviceToDevice, c.st));
+            vin.data = inb.p;
+        }
+        bool ocontig = true;
+        for (int i = 1; i < n_in; i++) ocontig &= out[i].data == out[0].data + (long)i * ow;
+        CtView vout = compact_view(c, out[0].data, n_in, ol, c.scale);
+        if (!ocontig) {
+            outb = DevBuf((size_t)n_in * ow, c.st);
+            vout.data = outb.p;
+        }
+        run_argmax(c, *keys->k, vin, lay, sc, vout);
+        if (!ocontig)
+            for (int i = 0; i < n_in; i++)
+                CUDA_CHECK(
+                    cudaMemcpyAsync(out[i].data, outb.p + (long)i * ow, ow * 8, cudaMemcpyDeviceToDevice, c.st));
+        for (int i = 0; i < n_in; i++) set_out(&out[i], vout);
+    });
+}
+
+int secpe_oplog_enable(secpe_ctx *ctx, int32_t on) {
+    return guard([&] {
+        REQUIRE(ctx, SECPE_EINVAL, "null ctx");
+        ctx->c.log_on = on != 0;
+    });
+}
+int64_t secpe_oplog_get(secpe_ctx *ctx, char *buf, size_t cap) {
+    if (!ctx) return -1;
+    const std::string &s = ctx->c.oplog;
+    if (buf && cap) {
+        const size_t n = std::min(cap - 1, s.size());
+        std::memcpy(buf, s.data(), n);
+        buf[n] = 0;
+    }
+    return (int64_t)s.size();
+}
+int secpe_oplog_clear(secpe_ctx *ctx) {
+    return guard([&] {
+        REQUIRE(ctx, SECPE_EINVAL, "null ctx");
+        ctx->c.oplog.clear();
+    });
+}
+int secpe_profile_begin(secpe_ctx *ctx) {
+    return guard([&] {
+        REQUIRE(ctx, SECPE_EINVAL, "null ctx");
+        Prof &p = ctx->c.prof;
+        CUDA_CHECK(cudaStreamSynchronize(ctx->c.st));
+        p.used = 0;
+        p.spans.clear();
+        p.on = true;
+    });
+}
+int secpe_profile_end(secpe_ctx *ctx, double *out, int32_t n_out) {
+    return guard([&] {
+        REQUIRE(ctx && out && n_out >= 9, SECPE_EINVAL, "need out[9]");
+        Prof &p = ctx->c.prof;
+        CUDA_CHECK(cudaStreamSynchronize(ctx->c.st));
+        p.on = false;
+        for (int i = 0; i < 9; i++) out[i] = 0;
+        for (const auto &s : p.spans) {
+            float ms = 0;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, p.pool[s.a], p.pool[s.b]));
+            out[3 * s.kind + 0] += ms;
+            out[3 * s.kind + 1] += s.bytes;
+            out[3 * s.kind + 2] += (double)s.units;
+        }
+        p.spans.clear();
+        p.used = 0;
+    });
+}
+int secpe_opcounts(secpe_ctx *ctx, int64_t *counts, int32_t reset) {
+    return guard([&] {
+        REQUIRE(ctx && counts, SECPE_EINVAL, "null argument");
+        Counters &k = ctx->c.cnt;
+        const long long v[8] = {k.ntt_limbs, k.keyswitch, k.rescale, k.rotate, k.mulct, k.mulconst, k.launches, k.sign};
+        for (int i = 0; i < 8; i++) counts[i] = v[i];
+        if (reset) k = Counters{};
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,328 @@
+// context.cu -- parameters, precomputed tables and per-level constants (host side of the product).
+//
+// Everything here is computed by the library itself (independent of oracle/): prime chains
+// (reading R1), psi = smallest primitive 2N-th root of unity (reading R4), twiddle tables with
+// Shoup companions, Barrett constants, CRT / fast-base-conversion constants for hybrid key
+// switching (R10, R11) and rescale (R12), and the Gaussian CDT in quad precision (R6).
+#include <quadmath.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "context.h"
+
+// ---------------------------------------------------------------------------------------------
+// device buffers
+// ---------------------------------------------------------------------------------------------
+DevBuf::DevBuf(size_t w, cudaStream_t s) : words(w), st(s) {
+    if (w) CUDA_CHECK(cudaMallocAsync((void **)&p, w * sizeof(u64), s));
+}
+DevBuf::~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+}
+DevBuf &DevBuf::operator=(DevBuf &&o) noexcept {
+    if (this != &o) {
+        if (p) cudaFreeAsync(p, st);
+        p = o.p;
+        words = o.words;
+        st = o.st;
+        o.p = nullptr;
+        o.words = 0;
+    }
+    return *this;
+}
+
+static DevBuf upload(const std::vector<u64> &h, cudaStream_t st) {
+    DevBuf b(std::max<size_t>(h.size(), 1), st);
+    if (!h.empty()) CUDA_CHECK(cudaMemcpyAsync(b.p, h.data(), h.size() * sizeof(u64), cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));  // h may be a temporary
+    return b;
+}
+
+// ---------------------------------------------------------------------------------------------
+// host modular arithmetic
+// ---------------------------------------------------------------------------------------------
+u64 h_mulmod(u64 a, u64 b, u64 q) { return (u64)((u128)a * b % q); }
+u64 h_powmod(u64 a, u64 e, u64 q) {
+    u64 r = 1 % q;
+    a %= q;
+    for (; e; e >>= 1) {
+        if (e & 1) r = h_mulmod(r, a, q);
+        a = h_mulmod(a, a, q);
+    }
+    return r;
+}
+u64 h_invmod(u64 a, u64 q) { return h_powmod(a % q, q - 2, q); }
+u64 h_shoup(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
+u64 h_smod(i64 v, u64 q) {
+    if (v >= 0) return (u64)v % q;
+    u64 m = (u64)(-(v + 1)) % q;  // (|v| - 1) mod q
+    m = (m + 1) % q;
+    return m ? q - m : 0;
+}
+
+bool h_is_prime(u64 n) {
+    if (n < 2) return false;
+    static const u64 small[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+    for (u64 p : small) {
+        if (n == p) return true;
+        if (n % p == 0) return false;
+    }
+    u64 d = n - 1;
+    int s = 0;
+    while (!(d & 1)) d >>= 1, s++;
+    for (u64 a : small) {
+        u64 x = h_powmod(a, d, n);
+        if (x == 1 || x == n - 1) continue;
+        bool witness = true;
+        for (int r = 1; r < s && witness; r++) {
+            x = h_mulmod(x, x, n);
+            if (x == n - 1) witness = false;
+        }
+        if (witness) return false;
+    }
+    return true;
+}
+
+// mode 0: candidates 2^b + 1 + k 2N ordered by distance to 2^b (k = 0, -1, 1, -2, 2, ...);
+// mode 1: largest below 2^b, descending.
+int h_gen_primes(int bits, int count, int logn, int mode, const u64 *ex, int nex, u64 *out) {
+    const u64 base = (u64)1 << bits, step = (u64)2 << logn;
+    int got = 0;
+    auto take = [&](u64 c) {
+        if (got < count && h_is_prime(c) && std::find(ex, ex + nex, c) == ex + nex) out[got++] = c;
+    };
+    for (u64 k = 0; got < count && k < ((u64)1 << 40); k++) {
+        if (mode == 0) {
+            take(base + 1 + k * step);
+            take(base + 1 - (k + 1) * step);
+        } else {
+            take(base + 1 - (k + 1) * step);
+        }
+    }
+    return got;
+}
+
+// psi: generator g of Z_q^* from the factorisation of q-1, psi0 = g^((q-1)/2N), then the minimum
+// over all primitive 2N-th roots psi0^(2j+1).
+u64 h_find_psi(u64 q, int logn) {
+    const u64 two_n = (u64)2 << logn;
+    std::vector<u64> f;
+    u64 m = q - 1;
+    for (u64 p = 2; p * p <= m; p += (p == 2 ? 1 : 2)) {
+        if (m % p == 0) {
+            f.push_back(p);
+            while (m % p == 0) m /= p;
+        }
+    }
+    if (m > 1) f.push_back(m);
+    u64 g = 2;
+    for (;; g++) {
+        bool gen = true;
+        for (u64 p : f)
+            if (h_powmod(g, (q - 1) / p, q) == 1) {
+                gen = false;
+                break;
+            }
+        if (gen) break;
+    }
+    const u64 psi0 = h_powmod(g, (q - 1) / two_n, q), psi2 = h_mulmod(psi0, psi0, q);
+    u64 best = psi0, cur = psi0;
+    for (u64 j = 0; j < two_n / 2; j++) {
+        best = std::min(best, cur);
+        cur = h_mulmod(cur, psi2, q);
+    }
+    return best;
+}
+
+// CDT over |e| <= 19, sigma = 3.2: T[m] = floor(2^63 F(m)), exp(-j^2 / (2 sigma^2)) = exp(-25 j^2 / 512)
+void h_cdt(u64 *out, int n) {
+    __float128 rho[32], tot = 0, acc = 0;
+    for (int j = 0; j < n; j++) {
+        rho[j] = expq(-(__float128)(25 * j * j) / 512);
+        tot += j ? 2 * rho[j] : rho[j];
+    }
+    const __float128 two63 = ldexpq(1, 63);
+    for (int m = 0; m < n; m++) {
+        acc += m ? 2 * rho[m] : rho[m];
+        out[m] = (u64)floorq(two63 * acc / tot);
+    }
+    out[n - 1] = (u64)1 << 63;
+}
+
+u64 galois_elt(const Ctx &c, int steps) {
+    const long half = c.N / 2;
+    long s = ((steps % half) + half) % half;
+    return h_powmod(5, (u64)s, (u64)(2 * c.N));
+}
+
+double round_half_away(double x) { return std::round(x); }
+
+static unsigned brv(unsigned x, int bits) {
+    unsigned r = 0;
+    for (int i = 0; i < bits; i++) r = (r << 1) | ((x >> i) & 1);
+    return r;
+}
+
+cudaEvent_t Prof::next() {
+    if (used == pool.size()) {
+        cudaEvent_t e;
+        CUDA_CHECK(cudaEventCreate(&e));
+        pool.push_back(e);
+    }
+    return pool[used++];
+}
+size_t Ctx::prof_begin(int) {
+    if (!prof.on) return 0;
+    const size_t a = prof.used;
+    CUDA_CHECK(cudaEventRecord(prof.next(), st));
+    return a;
+}
+void Ctx::prof_end(size_t a, int kind, double bytes, long long units) {
+    if (!prof.on) return;
+    const size_t b = prof.used;
+    CUDA_CHECK(cudaEventRecord(prof.next(), st));
+    prof.spans.push_back(Prof::Span{a, b, kind, bytes, units});
+}
+
+void Ctx::log(const char *kind, int lin, int lout, double s, const std::string &extra) {
+    if (!log_on) return;
+    u64 bits;
+    std::memcpy(&bits, &s, 8);
+    char buf[128];
+    snprintf(buf, sizeof buf, "%s %d %d %016llx %s\n", kind, lin, lout, (unsigned long long)bits, extra.c_str());
+    oplog += buf;
+}
+
+// ---------------------------------------------------------------------------------------------
+// context build
+// ---------------------------------------------------------------------------------------------
+void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int logn_, double scale_) {
+    logn = logn_;
+    N = 1L << logn;
+    nq = nq_;
+    np = np_;
+    alpha = alpha_;
+    scale = scale_;
+    primes.assign(q, q + nq);
+    primes.insert(primes.end(), p, p + np);
+    const int P = nprimes();
+    psi.resize(P);
+    std::vector<u64> hq(P), hr0(P), hr1(P), hni(P), hnish(P);
+    std::vector<u64> tw((size_t)P * N), twsh((size_t)P * N), itw((size_t)P * N), itwsh((size_t)P * N);
+    for (int i = 0; i < P; i++) {
+        const u64 qi = primes[i];
+        psi[i] = h_find_psi(qi, logn);
+        hq[i] = qi;
+        const u128 r = (~(u128)0) / qi;  // floor((2^128 - 1)/q) = floor(2^128/q) for odd q
+        hr0[i] = (u64)r;
+        hr1[i] = (u64)(r >> 64);
+        hni[i] = h_invmod((u64)N % qi, qi);
+        hnish[i] = h_shoup(hni[i], qi);
+        // powers psi^k and psi^-k, then bit-reversed tables
+        std::vector<u64> pw(N), ipw(N);
+        const u64 pinv = h_invmod(psi[i], qi);
+        pw[0] = ipw[0] = 1;
+        for (long k = 1; k < N; k++) {
+            pw[k] = h_mulmod(pw[k - 1], psi[i], qi);
+            ipw[k] = h_mulmod(ipw[k - 1], pinv, qi);
+        }
+        for (long k = 0; k < N; k++) {
+            const unsigned b = brv((unsigned)k, logn);
+            const size_t o = (size_t)i * N + k;
+            tw[o] = pw[b];
+            twsh[o] = h_shoup(pw[b], qi);
+            itw[o] = ipw[b];
+            itwsh[o] = h_shoup(ipw[b], qi);
+        }
+    }
+    h_br0 = hr0;
+    h_br1 = hr1;
+    d_q = upload(hq, st);
+    d_br0 = upload(hr0, st);
+    d_br1 = upload(hr1, st);
+    d_ninv = upload(hni, st);
+    d_ninvsh = upload(hnish, st);
+    d_tw = upload(tw, st);
+    d_twsh = upload(twsh, st);
+    d_itw = upload(itw, st);
+    d_itwsh = upload(itwsh, st);
+    tab = Tab{d_q.p, d_br0.p, d_br1.p, d_tw.p, d_twsh.p, d_itw.p, d_itwsh.p, d_ninv.p, d_ninvsh.p};
+
+    // ModDown constants: P = prod p
+    std::vector<u64> vihp(std::max(np, 1)), vihpsh(std::max(np, 1)), vhatp((size_t)std::max(np, 1) * nq),
+        vpinv(nq), vpinvsh(nq);
+    for (int a = 0; a < np; a++) {
+        const u64 pa = primes[nq + a];
+        u64 h = 1;
+        for (int b = 0; b < np; b++)
+            if (b != a) h = h_mulmod(h, primes[nq + b] % pa, pa);
+        vihp[a] = h_invmod(h, pa);
+        vihpsh[a] = h_shoup(vihp[a], pa);
+        for (int i = 0; i < nq; i++) {
+            u64 hq2 = 1;
+            for (int b = 0; b < np; b++)
+                if (b != a) hq2 = h_mulmod(hq2, primes[nq + b] % primes[i], primes[i]);
+            vhatp[(size_t)a * nq + i] = hq2;
+        }
+    }
+    for (int i = 0; i < nq; i++) {
+        u64 pp = 1;
+        for (int a = 0; a < np; a++) pp = h_mulmod(pp, primes[nq + a] % primes[i], primes[i]);
+        vpinv[i] = h_invmod(pp, primes[i]);
+        vpinvsh[i] = h_shoup(vpinv[i], primes[i]);
+    }
+    ihp = upload(vihp, st);
+    ihp_sh = upload(vihpsh, st);
+    hat_p = upload(vhatp, st);
+    pinv = upload(vpinv, st);
+    pinv_sh = upload(vpinvsh, st);
+
+    // per-level constants
+    lvl.clear();
+    for (int l = 0; l < nq; l++) {
+        auto lc = std::make_unique<LevelConsts>();
+        const int nl = l + 1, ne = nl + np, bt = beta(l);
+        lc->nl = nl;
+        lc->beta = bt;
+        std::vector<u64> ih(nl), ihs(nl), hat((size_t)bt * 16 * ne, 0);
+        for (int j = 0; j < bt; j++) {
+            const int i0 = j * alpha, i1 = std::min(i0 + alpha, nl);
+            for (int i = i0; i < i1; i++) {
+                u64 h = 1;
+                for (int i2 = i0; i2 < i1; i2++)
+                    if (i2 != i) h = h_mulmod(h, primes[i2] % primes[i], primes[i]);
+                ih[i] = h_invmod(h, primes[i]);
+                ihs[i] = h_shoup(ih[i], primes[i]);
+                for (int e = 0; e < ne; e++) {
+                    const u64 t = primes[e < nl ? e : nq + (e - nl)];
+                    u64 ht = 1;
+                    for (int i2 = i0; i2 < i1; i2++)
+                        if (i2 != i) ht = h_mulmod(ht, primes[i2] % t, t);
+                    hat[((size_t)j * 16 + (i - i0)) * ne + e] = ht;
+                }
+            }
+        }
+        lc->inv_hat = upload(ih, st);
+        lc->inv_hat_sh = upload(ihs, st);
+        lc->hat = upload(hat, st);
+        if (l >= 1) {
+            std::vector<u64> hf(l), qi(l), qis(l);
+            const u64 ql = primes[l];
+            for (int i = 0; i < l; i++) {
+                hf[i] = (ql >> 1) % primes[i];
+                qi[i] = h_invmod(ql % primes[i], primes[i]);
+                qis[i] = h_shoup(qi[i], primes[i]);
+            }
+            lc->half = upload(hf, st);
+            lc->qlinv = upload(qi, st);
+            lc->qlinv_sh = upload(qis, st);
+        }
+        lvl.push_back(std::move(lc));
+    }
+    u64 cdt[20];
+    h_cdt(cdt, 20);
+    set_cdt(cdt, 20);
+    CUDA_CHECK(cudaStreamSynchronize(st));
+}

@@ -1,0 +1,153 @@
+// context.h -- library context, keys, device buffers and the ciphertext evaluator.
+#pragma once
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+// RAII device buffer (stream-ordered allocation on the context stream)
+struct DevBuf {
+    u64 *p = nullptr;
+    size_t words = 0;
+    cudaStream_t st = nullptr;
+    DevBuf() = default;
+    DevBuf(size_t w, cudaStream_t s);
+    ~DevBuf();
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    DevBuf(DevBuf &&o) noexcept { *this = std::move(o); }
+    DevBuf &operator=(DevBuf &&o) noexcept;
+};
+
+// per-level key-switching / rescale constants (device)
+struct LevelConsts {
+    int nl, beta;
+    DevBuf inv_hat, inv_hat_sh;  // [nl]  (Q'_j / q_i)^{-1} mod q_i
+    DevBuf hat;                  // [beta][16][ne]  (Q'_j / q_i) mod t_e
+    DevBuf half, qlinv, qlinv_sh;  // rescale by q_{nl-1}: [nl-1]
+};
+
+// CUDA-event profiling of the dominant kernels inside a timed region (bench.py roofline)
+struct Prof {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    struct Span {
+        size_t a, b;
+        int kind;      // 0 NTT, 1 key switch, 2 rescale
+        double bytes;  // algorithmic bytes of the span
+        long long units;
+    };
+    std::vector<Span> spans;
+    cudaEvent_t next();
+};
+
+struct Counters {
+    long long ntt_limbs = 0, keyswitch = 0, rescale = 0, rotate = 0, mulct = 0, mulconst = 0, launches = 0,
+              sign = 0;
+};
+
+// Ciphertext batch view: n cts; ct c polynomial b limb i at data + c * stride + b * ps + i * N.
+// A view at a lower level than its storage is a zero-copy drop (limbs above `level` ignored).
+struct CtView {
+    u64 *data;
+    long stride;  // elements between ciphertexts
+    long ps;      // elements between c0 and c1 (= (storage level + 1) * N)
+    int n;
+    int level;
+    double scale;
+};
+
+struct Keys;
+
+struct Ctx {
+    int logn = 0;
+    long N = 0;
+    int nq = 0, np = 0, alpha = 1;
+    double scale = 0;
+    std::vector<u64> primes, psi;  // q_0..q_L, p_0..p_{k-1}
+    cudaStream_t st = nullptr;
+    // tables
+    DevBuf d_q, d_br0, d_br1, d_tw, d_twsh, d_itw, d_itwsh, d_ninv, d_ninvsh;
+    Tab tab{};
+    // ModDown constants
+    DevBuf ihp, ihp_sh, hat_p, pinv, pinv_sh;
+    std::vector<std::unique_ptr<LevelConsts>> lvl;  // index = level
+    // host copies used by planning
+    std::vector<u64> h_br0, h_br1;
+    // instrumentation
+    bool log_on = false;
+    std::string oplog;
+    Counters cnt;
+    Prof prof;
+    size_t prof_begin(int kind);
+    void prof_end(size_t a, int kind, double bytes, long long units);
+
+    int nprimes() const { return nq + np; }
+    int L() const { return nq - 1; }
+    int beta(int level) const { return (level + 1 + alpha - 1) / alpha; }
+    long ct_words(int level) const { return 2L * (level + 1) * N; }
+    void build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int logn_, double scale_);
+    const LevelConsts &level(int l) const { return *lvl[l]; }
+    void log(const char *kind, int lin, int lout, double s, const std::string &extra);
+};
+
+struct Keys {
+    DevBuf s;      // [nq+np][N] NTT
+    DevBuf pk;     // [2][nq][N]
+    DevBuf rlk;    // [beta_top][2][nq+np][N]
+    std::map<u64, DevBuf> gk;
+    std::vector<i64> s_coeff;  // not kept (client secret stays on device); unused
+};
+
+// host modular helpers (context.cu)
+u64 h_mulmod(u64 a, u64 b, u64 q);
+u64 h_powmod(u64 a, u64 e, u64 q);
+u64 h_invmod(u64 a, u64 q);
+u64 h_shoup(u64 w, u64 q);
+u64 h_smod(i64 v, u64 q);
+bool h_is_prime(u64 n);
+int h_gen_primes(int bits, int count, int logn, int mode, const u64 *ex, int nex, u64 *out);
+u64 h_find_psi(u64 q, int logn);
+void h_cdt(u64 *out, int n);  // 20-entry CDT (quad precision)
+u64 galois_elt(const Ctx &c, int steps);
+double round_half_away(double x);
+
+// evaluator primitives (eval.cu) -- all operate on batches of n ciphertexts
+// Outputs are compact views (stride = 2 (level+1) N, ps = (level+1) N) supplied by the caller.
+CtView compact_view(const Ctx &c, u64 *data, int n, int level, double scale);
+void ev_ntt(Ctx &c, RowsArg d, int n_polys, LimbMap lm, bool inverse);
+void ev_copy(Ctx &c, const CtView &a, const CtView &out);
+void ev_addsub(Ctx &c, const CtView &a, const CtView &b, const CtView &out, bool sub);
+void ev_mul_int(Ctx &c, const CtView &a, i64 C, const CtView &out);
+void ev_add_int(Ctx &c, const CtView &a, i64 C, const CtView &out);
+void ev_rescale(Ctx &c, const CtView &in, const CtView &out);
+void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, const u64 *add,
+                  long add_stride, int add_polys, u64 *out, long out_stride);
+void ev_mul_relin(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const CtView &out);
+void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView &out);
+void ev_mul_plain_ntt(Ctx &c, const CtView &a, const u64 *pt, const CtView &out);
+LimbConst limb_const(const Ctx &c, i64 C, int nl);
+
+// host encode/decode (encode.cpp)
+void encode_real(const Ctx &c, const double *slots, size_t n, double scale, std::vector<double> &coef);
+void encode_int(const Ctx &c, const double *slots, size_t n, double scale, i64 *out);
+void decode_real(const Ctx &c, const std::vector<double> &coef, double scale, double *slots, size_t n);
+void encode_mask(const Ctx &c, const double *slots, size_t n, double delta, i64 *out);
+
+// circuits (plan.cu)
+struct SignCfg {
+    std::vector<std::vector<double>> stages;
+};
+struct Layout {
+    int queries, prompts, classes, block;
+};
+struct Ev;  // planned evaluator (plan.cu)
+void run_sign(Ctx &c, const Keys &k, const CtView &in, const SignCfg &cfg, double target_scale, CtView &out);
+void run_argmax(Ctx &c, const Keys &k, const CtView &in, const Layout &lay, const SignCfg &cfg, CtView &out);
+int sign_depth(const SignCfg &cfg);
+int argmax_depth(const Layout &lay, const SignCfg &cfg);
+std::vector<int> argmax_rotations(const Layout &lay);

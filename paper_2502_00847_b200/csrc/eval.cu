@@ -1,0 +1,166 @@
+// eval.cu -- batched ciphertext primitives built from the kernels (server side).
+//
+//   add/sub, constant products, plaintext products, tensor + hybrid key switch
+//   (relinearisation), rotation = NTT-domain automorphism + key switch,
+//   rescale (leveled chain).  Readings R9-R12 of DESIGN.md fix the integers.
+// Every primitive works on a batch of n ciphertexts in one set of launches, so the switching key
+// is streamed once per op for the whole batch.
+#include "context.h"
+
+static inline RowsArg rows_of(const CtView &v) { return RowsArg{v.data, v.stride, v.ps}; }
+static inline CRows crows_of(const CtView &v) { return CRows{v.data, v.stride, v.ps}; }
+static inline LimbMap qmap(int nl) { return LimbMap{nl, nl, 0, 0}; }
+
+CtView compact_view(const Ctx &c, u64 *data, int n, int level, double scale) {
+    return CtView{data, 2L * (level + 1) * c.N, (long)(level + 1) * c.N, n, level, scale};
+}
+
+LimbConst limb_const(const Ctx &c, i64 C, int nl) {
+    LimbConst lc{};
+    for (int l = 0; l < nl; l++) {
+        const u64 q = c.primes[l];
+        lc.c[l] = h_smod(C, q);
+        lc.csh[l] = h_shoup(lc.c[l], q);
+    }
+    return lc;
+}
+
+void ev_ntt(Ctx &c, RowsArg d, int n_polys, LimbMap lm, bool inverse) {
+    const size_t pa = c.prof_begin(0);
+    if (inverse)
+        ntt_inverse(c.tab, c.logn, d, n_polys, lm, c.st);
+    else
+        ntt_forward(c.tab, c.logn, d, n_polys, lm, c.st);
+    c.cnt.ntt_limbs += (long long)n_polys * lm.nl;
+    c.cnt.launches += 2;
+    // algorithmic bytes: every limb read once and written once
+    c.prof_end(pa, 0, 16.0 * (double)n_polys * lm.nl * c.N, (long long)n_polys * lm.nl);
+}
+
+void ev_copy(Ctx &c, const CtView &a, const CtView &out) {
+    k_copy_rows(c.logn, crows_of(a), rows_of(out), 2 * a.n, out.level + 1, c.st);
+    c.cnt.launches++;
+}
+
+void ev_addsub(Ctx &c, const CtView &a, const CtView &b, const CtView &out, bool sub) {
+    if (a.scale != b.scale) throw SecpeError{-3, "add/sub: scales are not bit-identical"};
+    if (out.level > std::min(a.level, b.level)) throw SecpeError{-1, "add/sub: output level too high"};
+    k_addsub(c.tab, c.logn, crows_of(a), crows_of(b), rows_of(out), 2 * a.n, qmap(out.level + 1), sub, c.st);
+    c.cnt.launches++;
+}
+
+void ev_mul_int(Ctx &c, const CtView &a, i64 C, const CtView &out) {
+    const int nl = out.level + 1;
+    k_mul_const(c.tab, c.logn, crows_of(a), rows_of(out), 2 * a.n, qmap(nl), limb_const(c, C, nl), c.st);
+    c.cnt.launches++;
+}
+
+void ev_add_int(Ctx &c, const CtView &a, i64 C, const CtView &out) {
+    const int nl = out.level + 1;
+    // c0 rows of every ct (poly P = ct: cs = 2 * stride, ps = stride), then copy c1 if out != a
+    k_add_const(c.tab, c.logn, CRows{a.data, 2 * a.stride, a.stride}, RowsArg{out.data, 2 * out.stride, out.stride},
+                a.n, qmap(nl), limb_const(c, C, nl), c.st);
+    c.cnt.launches++;
+    if (out.data != a.data) {
+        k_copy_rows(c.logn, CRows{a.data + a.ps, 2 * a.stride, a.stride},
+                    RowsArg{out.data + out.ps, 2 * out.stride, out.stride}, a.n, nl, c.st);
+        c.cnt.launches++;
+    }
+}
+
+void ev_mul_plain_ntt(Ctx &c, const CtView &a, const u64 *pt, const CtView &out) {
+    const int nl = out.level + 1;
+    k_mul_poly(c.tab, c.logn, crows_of(a), pt, rows_of(out), 2 * a.n, qmap(nl), c.st);
+    c.cnt.launches++;
+}
+
+// O(rescale): r = [c_l + floor(q_l/2)]_{q_l} (coefficient form); c'_i = (c_i + [q_l/2]_{q_i} - [r]_{q_i}) q_l^{-1}
+void ev_rescale(Ctx &c, const CtView &in, const CtView &out) {
+    const size_t pa = c.prof_begin(2);
+    const int l = in.level;
+    if (l < 1) throw SecpeError{-2, "rescale: no level left"};
+    if (out.level != l - 1) throw SecpeError{-1, "rescale: bad output level"};
+    const long N = c.N;
+    const int n = in.n;
+    DevBuf last(2L * n * N, c.st), T(2L * n * l * N, c.st);
+    k_copy_rows(c.logn, CRows{in.data + l * N, in.stride, in.ps}, RowsArg{last.p, 2 * N, N}, 2 * n, 1, c.st);
+    ev_ntt(c, RowsArg{last.p, 2 * N, N}, 2 * n, LimbMap{1, 1, l, 0}, true);
+    k_rescale_bcast(c.tab, c.logn, last.p, 2 * N, T.p, 2L * l * N, n, l, c.st);
+    ev_ntt(c, RowsArg{T.p, 2L * l * N, (long)l * N}, 2 * n, qmap(l), false);
+    const LevelConsts &lc = c.level(l);
+    k_rescale_combine(c.tab, c.logn, crows_of(in), T.p, 2L * l * N, out.data, out.stride, n, l, lc.half.p, lc.qlinv.p,
+                      lc.qlinv_sh.p, c.st);
+    c.cnt.launches += 3;
+    c.cnt.rescale += n;
+    // algorithmic bytes: read 2(l+1) limbs, write 2l limbs per ciphertext
+    c.prof_end(pa, 2, 8.0 * (double)n * (2 * (l + 1) + 2 * l) * N, n);
+}
+
+// Hybrid key switching of d (NTT form; ct c at d + c * d_stride, level limbs), result added to
+// `add` (add_polys of 2 polynomials; compact, ct stride add_stride) and written compact to out.
+void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, const u64 *add,
+                  long add_stride, int add_polys, u64 *out, long out_stride) {
+    const long N = c.N;
+    const int nl = level + 1, np = c.np, ne = nl + np, bt = c.beta(level);
+    const LevelConsts &lc = c.level(level);
+    const size_t pa = c.prof_begin(1);
+    // 1. coefficient form of d
+    DevBuf dc((size_t)n * nl * N, c.st);
+    k_copy_rows(c.logn, CRows{d, 2 * d_stride, d_stride}, RowsArg{dc.p, 2L * nl * N, (long)nl * N}, n, nl, c.st);
+    ev_ntt(c, RowsArg{dc.p, 2L * nl * N, (long)nl * N}, n, qmap(nl), true);
+    // 2. ModUp into every digit's complement, then NTT of the converted limbs
+    const long exts = (long)bt * ne * N;
+    DevBuf ext((size_t)n * exts, c.st);
+    k_modup(c.tab, c.logn, dc.p, (long)nl * N, ext.p, exts, n, nl, np, c.nq, c.alpha, lc.inv_hat.p,
+            lc.inv_hat_sh.p, lc.hat.p, c.st);
+    for (int j = 0; j < bt; j++) {
+        const int i0 = j * c.alpha, i1 = std::min(i0 + c.alpha, nl);
+        if (i0 > 0) ev_ntt(c, RowsArg{ext.p + (long)j * ne * N, 2 * exts, exts}, n, LimbMap{i0, i0, 0, 0}, false);
+        ev_ntt(c, RowsArg{ext.p + ((long)j * ne + i1) * N, 2 * exts, exts}, n, LimbMap{ne - i1, nl - i1, i1, c.nq},
+               false);
+    }
+    // 3. inner product with the switching key
+    const long accs = 2L * ne * N;
+    DevBuf acc((size_t)n * accs, c.st);
+    k_ks_inner(c.tab, c.logn, d, d_stride, ext.p, exts, key, c.nq, np, acc.p, accs, n, nl, c.alpha, c.st);
+    // 4. ModDown: INTT of the special limbs, conversion to Q, NTT, subtract and scale by P^{-1}
+    ev_ntt(c, RowsArg{acc.p + (long)nl * N, accs, (long)ne * N}, 2 * n, LimbMap{np, 0, 0, c.nq}, true);
+    const long Ts = 2L * nl * N;
+    DevBuf T((size_t)n * Ts, c.st);
+    k_moddown_conv(c.tab, c.logn, acc.p, accs, T.p, Ts, n, nl, np, c.nq, c.ihp.p, c.ihp_sh.p, c.hat_p.p, c.st);
+    ev_ntt(c, RowsArg{T.p, Ts, (long)nl * N}, 2 * n, qmap(nl), false);
+    k_moddown_combine(c.tab, c.logn, acc.p, accs, T.p, Ts, add, add_stride, add_polys, out, out_stride, n, nl, ne,
+                      c.pinv.p, c.pinv_sh.p, c.st);
+    c.cnt.launches += 5;
+    c.cnt.keyswitch += n;
+    // algorithmic bytes: input limbs + output limbs per ciphertext + the key once per batch
+    c.prof_end(pa, 1, 8.0 * N * ((double)n * (nl + 2 * nl + add_polys * nl) + 2.0 * bt * ne), n);
+}
+
+void ev_mul_relin(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const CtView &out) {
+    const int l = out.level, nl = l + 1;
+    if (a.level < l || b.level < l) throw SecpeError{-1, "mul_relin: level"};
+    const long N = c.N, ds = 3L * nl * N;
+    DevBuf d((size_t)a.n * ds, c.st);
+    k_tensor(c.tab, c.logn, crows_of(a), crows_of(b), d.p, ds, a.n, nl, c.st);
+    c.cnt.launches++;
+    ev_keyswitch(c, d.p + 2L * nl * N, ds, a.n, l, k.rlk.p, d.p, ds, 2, out.data, out.stride);
+    c.cnt.mulct += a.n;
+}
+
+void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView &out) {
+    const u64 g = galois_elt(c, steps);
+    const int nl = out.level + 1;
+    if (g == 1) {
+        ev_copy(c, in, out);
+        return;
+    }
+    auto it = k.gk.find(g);
+    if (it == k.gk.end()) throw SecpeError{-4, "no Galois key for rotation step " + std::to_string(steps)};
+    const long N = c.N, ss = 2L * nl * N;
+    DevBuf sig((size_t)in.n * ss, c.st);
+    k_automorph(c.logn, crows_of(in), RowsArg{sig.p, ss, (long)nl * N}, 2 * in.n, nl, g, c.st);
+    c.cnt.launches++;
+    ev_keyswitch(c, sig.p + (long)nl * N, ss, in.n, out.level, it->second.p, sig.p, ss, 1, out.data, out.stride);
+    c.cnt.rotate += in.n;
+}

@@ -1,0 +1,96 @@
+// kernels.h -- launchers of the sm_100a kernels (all enqueue on the given stream).
+#pragma once
+#include "common.cuh"
+
+// ---- elementwise (ops.cu) -----------------------------------------------------------------
+// Polynomial P (of a batch) lives at p + (P >> 1) * cs + (P & 1) * ps: P = 2 * ct + b for
+// ciphertext batches (cs = ct stride, ps = c0 -> c1 offset); a plain array of polynomials with
+// stride s uses cs = 2 s, ps = s.  Row r = P * nl + limb; element (r, k) at poly + limb * N + k.
+struct RowsArg {
+    u64 *p;
+    long cs, ps;
+};
+struct CRows {
+    const u64 *p;
+    long cs, ps;
+};
+SECPE_HD long poly_off(long cs, long ps, int P) { return (long)(P >> 1) * cs + (long)(P & 1) * ps; }
+constexpr int MAXL = 64;  // max limbs per polynomial (n_q + n_p)
+struct LimbConst {
+    u64 c[MAXL];
+    u64 csh[MAXL];
+};
+
+// ---- NTT (ntt.cu) -------------------------------------------------------------------------
+// data: n_polys polynomials (RowsArg addressing) of lm.nl limbs each; in place.
+void ntt_forward(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st);
+void ntt_inverse(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st);
+
+void k_addsub(const Tab &tab, int logn, CRows a, CRows b, RowsArg out, int n_polys, LimbMap lm,
+              bool sub, cudaStream_t st);
+void k_copy_rows(int logn, CRows a, RowsArg out, int n_polys, int nl, cudaStream_t st);
+// out = a * c_l (Shoup, per-limb constant residues)
+void k_mul_const(const Tab &tab, int logn, CRows a, RowsArg out, int n_polys, LimbMap lm,
+                 const LimbConst &c, cudaStream_t st);
+// out = a + c_l (only the rows given)
+void k_add_const(const Tab &tab, int logn, CRows a, RowsArg out, int n_polys, LimbMap lm,
+                 const LimbConst &c, cudaStream_t st);
+// out[p][l] = a[p][l] * b[l]  (b one polynomial, broadcast over n_polys)
+void k_mul_poly(const Tab &tab, int logn, CRows a, const u64 *b, RowsArg out, int n_polys, LimbMap lm,
+                cudaStream_t st);
+// tensor: d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1 for n_ct ciphertexts (a, b: CRows views);
+// d compact: ct c, poly p at d + c*d_ct_stride + p*nl*N
+void k_tensor(const Tab &tab, int logn, CRows a, CRows b, u64 *d, long d_ct_stride, int n_ct, int nl,
+              cudaStream_t st);
+// automorphism in the NTT domain: out[i] = in[perm_g(i)]
+void k_automorph(int logn, CRows a, RowsArg out, int n_polys, int nl, u64 galois, cudaStream_t st);
+
+// ---- key switching (keyswitch.cu) ------------------------------------------------------------
+struct KsLevel;  // per-level constants (device pointers), see context.h
+// ModUp base conversion (coefficient domain): for every digit j and extended limb e not in I_j:
+//   ext[c][j][e] = sum_{i in I_j} [dc_i (Q'_j/q_i)^-1]_{q_i} [Q'_j/q_i]_{t_e}  mod t_e
+// dc: [n_ct][nl][N] coefficient form; ext: [n_ct][beta][ne][N]
+void k_modup(const Tab &tab, int logn, const u64 *dc, long dc_ct_stride, u64 *ext, long ext_ct_stride,
+             int n_ct, int nl, int np, int nq_total, int alpha, const u64 *inv_hat, const u64 *inv_hat_sh,
+             const u64 *hat, cudaStream_t st);
+// key inner product: acc[c][b][e] = sum_j X_j[e] * key_j[b][prime(e)], X_j[e] = d[c][e] if e in I_j else ext[c][j][e]
+void k_ks_inner(const Tab &tab, int logn, const u64 *d, long d_ct_stride, const u64 *ext, long ext_ct_stride,
+                const u64 *key, int nq_total, int np, u64 *acc, long acc_ct_stride, int n_ct, int nl,
+                int alpha, cudaStream_t st);
+// ModDown conversion: T[c][b][i] = sum_p [r_p (P/p)^-1]_p [P/p]_{q_i} mod q_i ; r = acc P-limbs (coeff form)
+void k_moddown_conv(const Tab &tab, int logn, const u64 *acc, long acc_ct_stride, u64 *T, long T_ct_stride,
+                    int n_ct, int nl, int np, int nq_total, const u64 *inv_hat_p, const u64 *inv_hat_p_sh,
+                    const u64 *hat_p, cudaStream_t st);
+// out[c][b][i] = addend[c][b][i] + (acc[c][b][i] - T[c][b][i]) * P^-1   (addend may be null for b)
+void k_moddown_combine(const Tab &tab, int logn, const u64 *acc, long acc_ct_stride, const u64 *T,
+                       long T_ct_stride, const u64 *addend, long add_ct_stride, int add_polys, u64 *out,
+                       long out_ct_stride, int n_ct, int nl, int ne, const u64 *pinv, const u64 *pinv_sh,
+                       cudaStream_t st);
+
+// ---- rescale (rescale.cu) --------------------------------------------------------------------
+// T[c][b][i] = ([r + half]_{q_l}) mod q_i for i < l, r = coeff-form last limb (tmp[c][b])
+void k_rescale_bcast(const Tab &tab, int logn, const u64 *last, long last_ct_stride, u64 *T, long T_ct_stride,
+                     int n_ct, int l, cudaStream_t st);
+// out[c][b][i] = (in[c][b][i] + half_i - T[c][b][i]) * q_l^{-1}
+void k_rescale_combine(const Tab &tab, int logn, CRows in, const u64 *T,
+                       long T_ct_stride, u64 *out, long out_ct_stride, int n_ct, int l, const u64 *half,
+                       const u64 *qlinv, const u64 *qlinv_sh, cudaStream_t st);
+
+// ---- sampling / keys (sample.cu) ----------------------------------------------------------------
+// uniform residues in the NTT domain: out[l][k] for prime ids map (formula lm), counter layout per R6
+void k_sample_uniform(const Tab &tab, int logn, u64 seed, u64 tag, u64 *out, LimbMap lm, cudaStream_t st);
+// signed small polynomial: kind 0 ternary, 1 Gaussian (cdt in constant memory)
+void k_sample_small(int logn, u64 seed, u64 tag, int kind, i64 *out, cudaStream_t st);
+void set_cdt(const u64 *cdt, int n);
+// residues of a signed int64 polynomial: out[l][k] = m[k] mod q_l (coefficient form)
+void k_int_to_rows(const Tab &tab, int logn, const i64 *m, u64 *out, LimbMap lm, cudaStream_t st);
+// out = -a*s + e  (+ gadget * sp on limbs with gadget flag) ; all NTT form, rows lm
+void k_key_combine(const Tab &tab, int logn, const u64 *a, const u64 *s, const u64 *e, const u64 *sp,
+                   const LimbConst *gadget, u64 *out, LimbMap lm, cudaStream_t st);
+// ct0 = v*pk0 + e0 + m, ct1 = v*pk1 + e1  (all NTT, nl limbs)
+void k_encrypt_combine(const Tab &tab, int logn, const u64 *v, const u64 *pk, long pk_stride, const u64 *e0,
+                       const u64 *e1, const u64 *m, u64 *ct, int nl, cudaStream_t st);
+// out = c0 + c1 * s
+void k_decrypt_combine(const Tab &tab, int logn, const u64 *ct, const u64 *s, u64 *out, int nl, cudaStream_t st);
+// elementwise square: out = a*a
+void k_square(const Tab &tab, int logn, const u64 *a, u64 *out, LimbMap lm, cudaStream_t st);

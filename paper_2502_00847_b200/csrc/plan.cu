@@ -1,0 +1,229 @@
+// plan.cu -- SecPE circuits on the GPU evaluator: composite Sign (Eq. 3-4 with
+// BSGS), homomorphic Max (Eq. 6) and Algorithm 1 Argmax with
+// prompt aggregation and Eq. 5 normalisation.
+//
+// Scale planning (R9): every sub-expression is requested at a target (scale, level);
+// constant products absorb all scale drift (Delta_c = S_t q_l / S_x), ct x ct products are
+// assigned their target scale after rescale, so every addition sees bit-identical scales.
+// BSGS plans (R13) for odd degrees 3, 7, 15; emission order "first operand first".
+#include <cmath>
+#include <cstring>
+
+#include "context.h"
+
+namespace {
+
+std::string dbits(double x) {
+    u64 b;
+    std::memcpy(&b, &x, 8);
+    char buf[24];
+    snprintf(buf, sizeof buf, "%016llx", (unsigned long long)b);
+    return buf;
+}
+
+struct Val {
+    std::shared_ptr<DevBuf> buf;
+    CtView v;
+    int level() const { return v.level; }
+    double scale() const { return v.scale; }
+};
+
+}  // namespace
+
+struct Ev {
+    Ctx &c;
+    const Keys &k;
+    int n;
+
+    double q(int l) const { return (double)c.primes[l]; }
+
+    Val fresh(int level, double scale) {
+        auto b = std::make_shared<DevBuf>((size_t)n * c.ct_words(level), c.st);
+        return Val{b, compact_view(c, b->p, n, level, scale)};
+    }
+    Val drop(const Val &x, int level) {
+        if (level > x.level()) throw SecpeError{-2, "not enough levels"};
+        Val y = x;
+        y.v.level = level;
+        return y;
+    }
+    Val add(const Val &a, const Val &b, bool sub = false) {
+        const int lv = std::min(a.level(), b.level());
+        Val out = fresh(lv, a.scale());
+        ev_addsub(c, a.v, b.v, out.v, sub);
+        c.log(sub ? "SUB" : "ADD", std::max(a.level(), b.level()), lv, out.scale(), "");
+        return out;
+    }
+    Val sub(const Val &a, const Val &b) { return add(a, b, true); }
+    Val rot(const Val &x, int steps) {
+        Val out = fresh(x.level(), x.scale());
+        ev_rotate(c, k, x.v, steps, out.v);
+        c.log("ROT", x.level(), x.level(), x.scale(), std::to_string(galois_elt(c, steps)));
+        return out;
+    }
+    Val mul_const(const Val &x, double cval, double St, int Lt) {
+        const int lv = Lt + 1;
+        if (lv < 1) throw SecpeError{-2, "mul_const: no level left"};
+        Val xd = drop(x, lv);
+        const double dc = (St * q(lv)) / x.scale();
+        const double Cd = round_half_away(cval * dc);
+        if (!(std::fabs(Cd) < 4611686018427387904.0)) throw SecpeError{-6, "constant exceeds 2^62"};
+        const i64 C = (i64)Cd;
+        Val tmp = fresh(lv, x.scale() * dc);
+        ev_mul_int(c, xd.v, C, tmp.v);
+        Val out = fresh(Lt, St);
+        ev_rescale(c, tmp.v, out.v);
+        c.cnt.mulconst += n;
+        c.log("MULC", lv, Lt, St, std::to_string((long long)C));
+        return out;
+    }
+    // St = NAN: natural scale (S_a S_b) / q_l
+    Val mul_ct(const Val &a, const Val &b, double St, int Lt) {
+        const int lv = Lt + 1;
+        if (lv < 1) throw SecpeError{-2, "mul_ct: no level left"};
+        Val ad = drop(a, lv), bd = drop(b, lv);
+        Val prod = fresh(lv, a.scale() * b.scale());
+        ev_mul_relin(c, k, ad.v, bd.v, prod.v);
+        const double s = std::isnan(St) ? (a.scale() * b.scale()) / q(lv) : St;
+        Val out = fresh(Lt, s);
+        ev_rescale(c, prod.v, out.v);
+        c.log("MULCT", lv, Lt, s, "");
+        return out;
+    }
+    Val mul_mask(const Val &x, const std::vector<double> &mask, double St) {
+        const int lv = x.level();
+        if (lv < 1) throw SecpeError{-2, "mul_mask: no level left"};
+        const double dm = (St * q(lv)) / x.scale();
+        const long N = c.N;
+        std::vector<i64> M(N);
+        encode_mask(c, mask.data(), mask.size(), dm, M.data());
+        DevBuf mi(N, c.st), pt((size_t)(lv + 1) * N, c.st);
+        CUDA_CHECK(cudaMemcpyAsync(mi.p, M.data(), N * 8, cudaMemcpyHostToDevice, c.st));
+        k_int_to_rows(c.tab, c.logn, (const i64 *)mi.p, pt.p, LimbMap{lv + 1, lv + 1, 0, 0}, c.st);
+        ev_ntt(c, RowsArg{pt.p, 2L * (lv + 1) * N, (long)(lv + 1) * N}, 1, LimbMap{lv + 1, lv + 1, 0, 0}, false);
+        Val tmp = fresh(lv, x.scale() * dm);
+        ev_mul_plain_ntt(c, x.v, pt.p, tmp.v);
+        Val out = fresh(lv - 1, St);
+        ev_rescale(c, tmp.v, out.v);
+        CUDA_CHECK(cudaStreamSynchronize(c.st));  // M is host memory of this frame
+        c.log("MULP", lv, lv - 1, St, dbits(dm));
+        return out;
+    }
+    Val add_const(const Val &x, double cval) {
+        const double Cd = round_half_away(cval * x.scale());
+        if (!(std::fabs(Cd) < 4611686018427387904.0)) throw SecpeError{-6, "constant exceeds 2^62"};
+        const i64 C = (i64)Cd;
+        Val out = fresh(x.level(), x.scale());
+        ev_add_int(c, x.v, C, out.v);
+        c.log("ADDC", x.level(), x.level(), x.scale(), std::to_string((long long)C));
+        return out;
+    }
+
+    // ---- composite sign --------------------------------------------------------------------
+    Val odd_poly(const Val &x, const std::vector<double> &cf, double T) {
+        const int deg = (int)cf.size() - 1;
+        const int l = x.level();
+        Val x2 = mul_ct(x, x, NAN, l - 1);
+        Val x4 = deg >= 7 ? mul_ct(x2, x2, NAN, l - 2) : Val{};
+        Val x8 = deg >= 15 ? mul_ct(x4, x4, NAN, l - 3) : Val{};
+        auto A = [&](int i, double S, int L) {
+            Val inner = mul_const(x, cf[4 * i + 3], (S * q(L + 1)) / x2.scale(), L + 1);
+            Val prod = mul_ct(inner, x2, S, L);
+            Val lin = mul_const(x, cf[4 * i + 1], S, L);
+            return add(prod, lin);
+        };
+        auto B = [&](int i, double S, int L) {
+            Val hi = A(2 * i + 1, (S * q(L + 1)) / x4.scale(), L + 1);
+            Val prod = mul_ct(hi, x4, S, L);
+            Val lo = A(2 * i, S, L);
+            return add(prod, lo);
+        };
+        if (deg == 3) return A(0, T, l - 2);
+        if (deg == 7) return B(0, T, l - 3);
+        const int L = l - 4;
+        Val hi = B(1, (T * q(L + 1)) / x8.scale(), L + 1);
+        Val prod = mul_ct(hi, x8, T, L);
+        Val lo = B(0, T, L);
+        return add(prod, lo);
+    }
+    Val sign(Val x, const SignCfg &cfg, double T) {
+        for (size_t i = 0; i < cfg.stages.size(); i++) {
+            const double s = (i + 1 == cfg.stages.size()) ? T : c.scale;
+            x = odd_poly(x, cfg.stages[i], s);
+        }
+        c.cnt.sign += n;
+        return x;
+    }
+    // Eq. 6: Max(r, y) = (r + y)/2 + (r - y)/2 * Sign(r - y); output scale = scale(y)
+    Val hom_max(const Val &r, const Val &y, const SignCfg &cfg) {
+        const double Sy = y.scale();
+        Val d = sub(r, y);
+        Val s = sign(d, cfg, c.scale);
+        const int Ls = s.level();
+        Val g = mul_const(d, 0.5, (Sy * q(Ls)) / s.scale(), Ls);
+        Val t2 = mul_ct(g, s, Sy, Ls - 1);
+        Val ry = add(r, y);
+        Val h = mul_const(ry, 0.5, Sy, Ls - 1);
+        return add(h, t2);
+    }
+    // Algorithm 1 with the H1..H6 steps of DESIGN.md section 2
+    Val argmax(const Val &in, const Layout &lay, const SignCfg &cfg) {
+        const int P = lay.prompts, K = lay.classes;
+        Val y = in;
+        for (int t = 0; (1 << t) < P; t++) y = add(y, rot(y, K << t));
+        std::vector<double> mask(c.N / 2, 0.0);
+        for (int qi = 0; qi < lay.queries; qi++)
+            for (int kk = 0; kk < K; kk++) mask[(size_t)qi * lay.block + kk] = 1.0 / P;
+        y = mul_mask(y, mask, c.scale);
+        y = add(y, rot(y, -K));
+        Val ydup = y;
+        for (int i = 0; (1 << i) < K; i++) y = hom_max(rot(y, 1 << i), y, cfg);
+        Val d = sub(ydup, y);
+        Val z = sign(d, cfg, c.scale);
+        return add_const(z, 1.0);
+    }
+};
+
+static int ilog2(int v) {
+    int r = 0;
+    while ((1 << r) < v) r++;
+    return r;
+}
+static int poly_depth(int deg) { return ilog2(deg + 1); }
+
+int sign_depth(const SignCfg &cfg) {
+    int d = 0;
+    for (auto &s : cfg.stages) d += poly_depth((int)s.size() - 1);
+    return d;
+}
+int argmax_depth(const Layout &lay, const SignCfg &cfg) {
+    return 1 + ilog2(lay.classes) * (sign_depth(cfg) + 1) + sign_depth(cfg);
+}
+std::vector<int> argmax_rotations(const Layout &lay) {
+    std::vector<int> r;
+    for (int t = 0; (1 << t) < lay.prompts; t++) r.push_back(lay.classes << t);
+    r.push_back(-lay.classes);
+    for (int i = 0; (1 << i) < lay.classes; i++) r.push_back(1 << i);
+    return r;
+}
+
+static void copy_in(Ctx &c, const CtView &src, const Val &dst) { ev_copy(c, src, dst.v); }
+
+void run_sign(Ctx &c, const Keys &k, const CtView &in, const SignCfg &cfg, double target_scale, CtView &out) {
+    Ev ev{c, k, in.n};
+    Val x{nullptr, in};
+    Val r = ev.sign(x, cfg, target_scale);
+    out.level = r.level();
+    out.scale = r.scale();
+    ev_copy(c, r.v, out);
+}
+
+void run_argmax(Ctx &c, const Keys &k, const CtView &in, const Layout &lay, const SignCfg &cfg, CtView &out) {
+    Ev ev{c, k, in.n};
+    Val x{nullptr, in};
+    Val r = ev.argmax(x, lay, cfg);
+    out.level = r.level();
+    out.scale = r.scale();
+    ev_copy(c, r.v, out);
+    (void)copy_in;
+}

@@ -1,0 +1,432 @@
+"""Thin ctypes binding of libsecpe.so (include/secpe.h).  Argument marshalling only: every
+homomorphic step runs in the library's sm_100a kernels.  PyTorch provides device memory and the
+stream.  There is no fallback: without the built library or a CUDA device, calls raise.
+"""
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsecpe.so")
+
+u64p = ctypes.POINTER(ctypes.c_uint64)
+i64p = ctypes.POINTER(ctypes.c_int64)
+i32p = ctypes.POINTER(ctypes.c_int32)
+f64p = ctypes.POINTER(ctypes.c_double)
+vp = ctypes.c_void_p
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("log_n", ctypes.c_uint32), ("n_q", ctypes.c_uint32), ("q", u64p), ("n_p", ctypes.c_uint32),
+                ("p", u64p), ("alpha", ctypes.c_uint32), ("scale", ctypes.c_double)]
+
+
+class CCt(ctypes.Structure):
+    _fields_ = [("data", u64p), ("level", ctypes.c_int32), ("scale", ctypes.c_double)]
+
+
+class SignCfg(ctypes.Structure):
+    _fields_ = [("n_stages", ctypes.c_int32), ("degrees", i32p), ("coeffs", f64p)]
+
+
+class Layout(ctypes.Structure):
+    _fields_ = [("queries", ctypes.c_int32), ("prompts", ctypes.c_int32), ("classes", ctypes.c_int32),
+                ("block", ctypes.c_int32)]
+
+
+_lib = None
+
+SIGS = {
+    "secpe_last_error": (ctypes.c_char_p, []),
+    "secpe_version": (ctypes.c_char_p, []),
+    "secpe_gen_primes": (ctypes.c_int, [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int32, u64p,
+                                        ctypes.c_uint32, u64p]),
+    "secpe_ctx_create": (ctypes.c_int, [ctypes.POINTER(Params), vp, ctypes.POINTER(vp)]),
+    "secpe_ctx_destroy": (None, [vp]),
+    "secpe_set_stream": (ctypes.c_int, [vp, vp]),
+    "secpe_sync": (ctypes.c_int, [vp]),
+    "secpe_ctx_info": (ctypes.c_int, [vp, u64p, u64p]),
+    "secpe_ct_bytes": (ctypes.c_size_t, [vp, ctypes.c_int32]),
+    "secpe_keygen": (ctypes.c_int, [vp, ctypes.c_uint64, i32p, ctypes.c_int32, ctypes.POINTER(vp)]),
+    "secpe_keys_destroy": (None, [vp]),
+    "secpe_key_export": (ctypes.c_int, [vp, vp, ctypes.c_int32, ctypes.c_uint64, u64p, ctypes.c_size_t]),
+    "secpe_encode": (ctypes.c_int, [vp, f64p, ctypes.c_size_t, ctypes.c_double, i64p]),
+    "secpe_encrypt_coeffs": (ctypes.c_int, [vp, vp, i64p, ctypes.c_int32, ctypes.c_double, ctypes.c_uint64,
+                                            ctypes.POINTER(CCt)]),
+    "secpe_encrypt": (ctypes.c_int, [vp, vp, f64p, ctypes.c_size_t, ctypes.c_int32, ctypes.c_double,
+                                     ctypes.c_uint64, ctypes.POINTER(CCt)]),
+    "secpe_decrypt_residues": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), u64p]),
+    "secpe_decrypt": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), f64p, ctypes.c_size_t]),
+    "secpe_ntt": (ctypes.c_int, [vp, u64p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
+    "secpe_intt": (ctypes.c_int, [vp, u64p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
+    "secpe_add": (ctypes.c_int, [vp, ctypes.POINTER(CCt), ctypes.POINTER(CCt), ctypes.POINTER(CCt)]),
+    "secpe_sub": (ctypes.c_int, [vp, ctypes.POINTER(CCt), ctypes.POINTER(CCt), ctypes.POINTER(CCt)]),
+    "secpe_add_const": (ctypes.c_int, [vp, ctypes.POINTER(CCt), ctypes.c_double, ctypes.POINTER(CCt)]),
+    "secpe_mul_const": (ctypes.c_int, [vp, ctypes.POINTER(CCt), ctypes.c_double, ctypes.c_double, ctypes.c_int32,
+                                       ctypes.POINTER(CCt)]),
+    "secpe_mul_mask": (ctypes.c_int, [vp, ctypes.POINTER(CCt), f64p, ctypes.c_size_t, ctypes.c_double,
+                                      ctypes.POINTER(CCt)]),
+    "secpe_drop": (ctypes.c_int, [vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.POINTER(CCt)]),
+    "secpe_mul_relin": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.POINTER(CCt), ctypes.POINTER(CCt)]),
+    "secpe_rescale": (ctypes.c_int, [vp, ctypes.POINTER(CCt), ctypes.POINTER(CCt)]),
+    "secpe_rotate": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.POINTER(CCt)]),
+    "secpe_sign_poly": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.POINTER(SignCfg), ctypes.c_double,
+                                       ctypes.POINTER(CCt)]),
+    "secpe_argmax_info": (ctypes.c_int, [vp, ctypes.POINTER(Layout), ctypes.POINTER(SignCfg), ctypes.c_int32,
+                                         i32p, f64p]),
+    "secpe_enc_argmax": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.POINTER(Layout),
+                                        ctypes.POINTER(SignCfg), ctypes.POINTER(CCt)]),
+    "secpe_oplog_enable": (ctypes.c_int, [vp, ctypes.c_int32]),
+    "secpe_oplog_get": (ctypes.c_int64, [vp, ctypes.c_char_p, ctypes.c_size_t]),
+    "secpe_oplog_clear": (ctypes.c_int, [vp]),
+    "secpe_opcounts": (ctypes.c_int, [vp, i64p, ctypes.c_int32]),
+    "secpe_profile_begin": (ctypes.c_int, [vp]),
+    "secpe_profile_end": (ctypes.c_int, [vp, f64p, ctypes.c_int32]),
+}
+EXPORTS = list(SIGS)
+
+
+def lib():
+    """Load libsecpe.so (built in-tree by paper_2502_00847_b200.build); raise if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError("libsecpe.so not built: run `python -m paper_2502_00847_b200.build` "
+                               "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+class SecpeError(RuntimeError):
+    pass
+
+
+def _chk(code):
+    if code != 0:
+        raise SecpeError("secpe error %d: %s" % (code, lib().secpe_last_error().decode()))
+
+
+def _u64(a):
+    a = np.ascontiguousarray(a, dtype=np.uint64)
+    return a, a.ctypes.data_as(u64p)
+
+
+def gen_primes(bits, count, logn, mode, exclude=()):
+    ex, exp_ = _u64(np.array(list(exclude) or [0], dtype=np.uint64))
+    out = np.zeros(count, dtype=np.uint64)
+    _chk(lib().secpe_gen_primes(bits, count, logn, 0 if mode == "nearest" else 1, exp_, len(exclude),
+                                out.ctypes.data_as(u64p)))
+    return [int(v) for v in out]
+
+
+def primes_for(desc):
+    """Prime chain of a parameter description (synth.PARAM_SETS entry), generated by the library."""
+    q = []
+    for mode, bits, cnt in desc["q"]:
+        q += gen_primes(bits, cnt, desc["logn"], mode, q)
+    p = []
+    for mode, bits, cnt in desc["p"]:
+        p += gen_primes(bits, cnt, desc["logn"], mode, q + p)
+    return q, p
+
+
+class Ct:
+    """A ciphertext (or a batch): torch uint64 tensor [n, 2, level+1, N] on the GPU + level + scale."""
+
+    def __init__(self, t, level, scale):
+        self.t, self.level, self.scale = t, level, scale
+
+    def c(self, i=0):
+        return CCt(ctypes.cast(self.t[i].data_ptr(), u64p), self.level, self.scale)
+
+    @property
+    def n(self):
+        return self.t.shape[0]
+
+
+def sign_cfg(stages):
+    deg = np.array([len(c) - 1 for c in stages], dtype=np.int32)
+    co = np.ascontiguousarray(np.concatenate([np.asarray(c, dtype=np.float64) for c in stages]))
+    cfg = SignCfg(len(stages), deg.ctypes.data_as(i32p), co.ctypes.data_as(f64p))
+    cfg._keep = (deg, co)
+    return cfg
+
+
+def layout(d):
+    return Layout(d["queries"], d["prompts"], d["classes"], d["block"])
+
+
+class Keys:
+    def __init__(self, ctx, handle):
+        self.ctx, self.h = ctx, handle
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.secpe_keys_destroy(self.h)
+            self.h = None
+
+    def export(self, which, galois=0):
+        cx = self.ctx
+        N, P = cx.N, cx.nq + cx.np_
+        beta = (cx.nq + cx.alpha - 1) // cx.alpha
+        shape = {0: (P, N), 1: (2, cx.nq, N), 2: (beta, 2, P, N), 3: (beta, 2, P, N)}[which]
+        out = np.zeros(shape, dtype=np.uint64)
+        _chk(lib().secpe_key_export(cx.h, self.h, which, galois, out.ctypes.data_as(u64p), out.size))
+        return out
+
+
+class Context:
+    """Parameters + device tables on the current torch CUDA stream."""
+
+    def __init__(self, desc=None, q=None, p=None, logn=None, alpha=None, scale=None, stream=None):
+        if desc is not None:
+            q, p = primes_for(desc)
+            logn, alpha, scale = desc["logn"], desc["alpha"], float(2 ** desc["log_scale"])
+        self.q, self.p = list(q), list(p)
+        self.logn, self.N = logn, 1 << logn
+        self.nq, self.np_, self.alpha, self.scale = len(q), len(p), alpha, scale
+        self._qa, qp = _u64(q)
+        self._pa, pp = _u64(p if p else [0])
+        prm = Params(logn, len(q), qp, len(p), pp, alpha, scale)
+        if stream is None:
+            stream = torch.cuda.current_stream().cuda_stream
+        h = vp()
+        _chk(lib().secpe_ctx_create(ctypes.byref(prm), vp(stream), ctypes.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.secpe_ctx_destroy(self.h)
+            self.h = None
+
+    @property
+    def L(self):
+        return self.nq - 1
+
+    def info(self):
+        P = self.nq + self.np_
+        pr, ps = np.zeros(P, dtype=np.uint64), np.zeros(P, dtype=np.uint64)
+        _chk(lib().secpe_ctx_info(self.h, pr.ctypes.data_as(u64p), ps.ctypes.data_as(u64p)))
+        return [int(v) for v in pr], [int(v) for v in ps]
+
+    def set_stream(self, stream):
+        _chk(lib().secpe_set_stream(self.h, vp(stream)))
+
+    def sync(self):
+        _chk(lib().secpe_sync(self.h))
+
+    # ---- memory -------------------------------------------------------------------------------
+    def alloc(self, level, n=1):
+        return torch.empty((n, 2, level + 1, self.N), dtype=torch.uint64, device="cuda")
+
+    def new_ct(self, level, n=1):
+        return Ct(self.alloc(level, n), level, 0.0)
+
+    # ---- keys / client ----------------------------------------------------------------------------
+    def keygen(self, seed, rot_steps=()):
+        r = np.array(list(rot_steps) or [0], dtype=np.int32)
+        h = vp()
+        _chk(lib().secpe_keygen(self.h, seed, r.ctypes.data_as(i32p), len(rot_steps), ctypes.byref(h)))
+        return Keys(self, h)
+
+    def encode(self, slots, scale):
+        z = np.ascontiguousarray(slots, dtype=np.float64)
+        out = np.zeros(self.N, dtype=np.int64)
+        _chk(lib().secpe_encode(self.h, z.ctypes.data_as(f64p), len(z), scale, out.ctypes.data_as(i64p)))
+        return out
+
+    def encrypt_coeffs(self, keys, coeffs, level, scale, seed, out=None):
+        m = np.ascontiguousarray(coeffs, dtype=np.int64)
+        ct = out if out is not None else self.new_ct(level)
+        cc = CCt(ctypes.cast(ct.t.data_ptr(), u64p), level, scale)
+        _chk(lib().secpe_encrypt_coeffs(self.h, keys.h, m.ctypes.data_as(i64p), level, scale, seed,
+                                        ctypes.byref(cc)))
+        ct.level, ct.scale = level, scale
+        return ct
+
+    def encrypt(self, keys, slots, level, scale, seed):
+        z = np.ascontiguousarray(slots, dtype=np.float64)
+        ct = self.new_ct(level)
+        cc = ct.c()
+        _chk(lib().secpe_encrypt(self.h, keys.h, z.ctypes.data_as(f64p), len(z), level, scale, seed,
+                                 ctypes.byref(cc)))
+        ct.level, ct.scale = level, scale
+        return ct
+
+    def decrypt_residues(self, keys, ct, i=0):
+        out = np.zeros((ct.level + 1, self.N), dtype=np.uint64)
+        cc = ct.c(i)
+        _chk(lib().secpe_decrypt_residues(self.h, keys.h, ctypes.byref(cc), out.ctypes.data_as(u64p)))
+        return out
+
+    def decrypt(self, keys, ct, i=0, n=None):
+        n = self.N // 2 if n is None else n
+        out = np.zeros(n, dtype=np.float64)
+        cc = ct.c(i)
+        _chk(lib().secpe_decrypt(self.h, keys.h, ctypes.byref(cc), out.ctypes.data_as(f64p), n))
+        return out
+
+    # ---- primitives -------------------------------------------------------------------------------
+    def ntt(self, polys, first_prime, n_limbs, inverse=False):
+        """In-place (I)NTT of a torch uint64 tensor [..., n_limbs, N] (contiguous)."""
+        assert polys.is_contiguous() and polys.dtype == torch.uint64
+        n_polys = polys.numel() // (n_limbs * self.N)
+        f = lib().secpe_intt if inverse else lib().secpe_ntt
+        _chk(f(self.h, ctypes.cast(polys.data_ptr(), u64p), n_polys, first_prime, n_limbs))
+        return polys
+
+    def _out(self, level):
+        return self.new_ct(level)
+
+    def _binary(self, fn, a, b):
+        out = self._out(min(a.level, b.level))
+        ca, cb, co = a.c(), b.c(), out.c()
+        _chk(fn(self.h, ctypes.byref(ca), ctypes.byref(cb), ctypes.byref(co)))
+        out.level, out.scale = co.level, co.scale
+        return out
+
+    def add(self, a, b):
+        return self._binary(lib().secpe_add, a, b)
+
+    def sub(self, a, b):
+        return self._binary(lib().secpe_sub, a, b)
+
+    def add_const(self, a, c):
+        out = self._out(a.level)
+        ca, co = a.c(), out.c()
+        _chk(lib().secpe_add_const(self.h, ctypes.byref(ca), c, ctypes.byref(co)))
+        out.level, out.scale = co.level, co.scale
+        return out
+
+    def mul_const(self, a, c, target_scale, target_level):
+        out = self._out(target_level)
+        ca, co = a.c(), out.c()
+        _chk(lib().secpe_mul_const(self.h, ctypes.byref(ca), c, target_scale, target_level, ctypes.byref(co)))
+        out.level, out.scale = co.level, co.scale
+        return out
+
+    def mul_mask(self, a, mask, target_scale):
+        m = np.ascontiguousarray(mask, dtype=np.float64)
+        out = self._out(a.level - 1)
+        ca, co = a.c(), out.c()
+        _chk(lib().secpe_mul_mask(self.h, ctypes.byref(ca), m.ctypes.data_as(f64p), len(m), target_scale,
+                                  ctypes.byref(co)))
+        out.level, out.scale = co.level, co.scale
+        return out
+
+    def drop(self, a, level):
+        out = self._out(level)
+        ca, co = a.c(), out.c()
+        _chk(lib().secpe_drop(self.h, ctypes.byref(ca), level, ctypes.byref(co)))
+        out.level, out.scale = co.level, co.scale
+        return out
+
+    def mul_relin(self, keys, a, b):
+        out = self._out(a.level)
+        ca, cb, co = a.c(), b.c(), out.c()
+        _chk(lib().secpe_mul_relin(self.h, keys.h, ctypes.byref(ca), ctypes.byref(cb), ctypes.byref(co)))
+        out.level, out.scale = co.level, co.scale
+        return out
+
+    def rescale(self, a):
+        out = self._out(a.level - 1)
+        ca, co = a.c(), out.c()
+        _chk(lib().secpe_rescale(self.h, ctypes.byref(ca), ctypes.byref(co)))
+        out.level, out.scale = co.level, co.scale
+        return out
+
+    def rotate(self, keys, a, steps):
+        out = self._out(a.level)
+        ca, co = a.c(), out.c()
+        _chk(lib().secpe_rotate(self.h, keys.h, ctypes.byref(ca), steps, ctypes.byref(co)))
+        out.level, out.scale = co.level, co.scale
+        return out
+
+    # ---- SecPE circuits ---------------------------------------------------------------------------
+    def sign_poly(self, keys, a, stages, target_scale):
+        cfg = sign_cfg(stages)
+        depth = sum(int(np.ceil(np.log2(len(c)))) for c in stages)
+        out = self._out(a.level - depth)
+        ca, co = a.c(), out.c()
+        _chk(lib().secpe_sign_poly(self.h, keys.h, ctypes.byref(ca), ctypes.byref(cfg), target_scale,
+                                   ctypes.byref(co)))
+        out.level, out.scale = co.level, co.scale
+        return out
+
+    def argmax_info(self, lay, stages, in_level):
+        cfg, ly = sign_cfg(stages), layout(lay)
+        ol, os_ = ctypes.c_int32(), ctypes.c_double()
+        _chk(lib().secpe_argmax_info(self.h, ctypes.byref(ly), ctypes.byref(cfg), in_level, ctypes.byref(ol),
+                                     ctypes.byref(os_)))
+        return ol.value, os_.value
+
+    def enc_argmax(self, keys, cts, lay, stages, out=None):
+        """SecPE private voting on a batch Ct (n ciphertexts, contiguous) -> batch Ct."""
+        cfg, ly = sign_cfg(stages), layout(lay)
+        ol, _ = self.argmax_info(lay, stages, cts.level)
+        if out is None:
+            out = self.new_ct(ol, cts.n)
+        ins = (CCt * cts.n)(*[cts.c(i) for i in range(cts.n)])
+        outs = (CCt * cts.n)(*[CCt(ctypes.cast(out.t[i].data_ptr(), u64p), ol, 0.0) for i in range(cts.n)])
+        _chk(lib().secpe_enc_argmax(self.h, keys.h, ins, cts.n, ctypes.byref(ly), ctypes.byref(cfg), outs))
+        out.level, out.scale = outs[0].level, outs[0].scale
+        return out
+
+    # ---- instrumentation --------------------------------------------------------------------------
+    def oplog(self, enable=None, clear=False):
+        if enable is not None:
+            _chk(lib().secpe_oplog_enable(self.h, 1 if enable else 0))
+        n = lib().secpe_oplog_get(self.h, None, 0)
+        buf = ctypes.create_string_buffer(n + 1)
+        lib().secpe_oplog_get(self.h, buf, n + 1)
+        if clear:
+            _chk(lib().secpe_oplog_clear(self.h))
+        return [l for l in buf.value.decode().split("\n") if l]
+
+    def profile_begin(self):
+        _chk(lib().secpe_profile_begin(self.h))
+
+    def profile_end(self):
+        o = np.zeros(9, dtype=np.float64)
+        _chk(lib().secpe_profile_end(self.h, o.ctypes.data_as(f64p), 9))
+        r = {}
+        for k, name in enumerate(("ntt", "keyswitch", "rescale")):
+            r[name] = dict(ms=float(o[3 * k]), bytes=float(o[3 * k + 1]), units=float(o[3 * k + 2]))
+        return r
+
+    def opcounts(self, reset=False):
+        c = np.zeros(8, dtype=np.int64)
+        _chk(lib().secpe_opcounts(self.h, c.ctypes.data_as(i64p), 1 if reset else 0))
+        keys = ["ntt_limbs", "keyswitch", "rescale", "rotate", "mulct", "mulconst", "launches", "sign"]
+        return dict(zip(keys, (int(v) for v in c)))
+
+
+def pack(scores, lay, n_slots):
+    """H0 client packing: score[q, p, k] -> slot q*block + p*K + k."""
+    P, K, b = lay["prompts"], lay["classes"], lay["block"]
+    z = np.zeros(n_slots)
+    q = scores.shape[0]
+    idx = (np.arange(q)[:, None, None] * b + np.arange(P)[None, :, None] * K + np.arange(K)[None, None, :])
+    z[idx.ravel()] = scores.ravel()
+    return z
+
+
+def argmax_rotations(lay):
+    """Rotation steps the argmax circuit uses (Galois keys to request from the client)."""
+    P, K = lay["prompts"], lay["classes"]
+    r = [K << t for t in range(P.bit_length() - 1)] + [-K] + [1 << i for i in range(K.bit_length() - 1)]
+    return sorted(set(r))
+
+
+def labels(z, lay):
+    """Client decode: argmax over each query's K window slots (first index on ties)."""
+    K, b, q = lay["classes"], lay["block"], lay["queries"]
+    w = np.asarray(z)[: q * b].reshape(q, b)[:, :K]
+    return np.argmax(w, axis=1)

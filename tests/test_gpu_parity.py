@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by element.
+
+Integer ciphertext arithmetic must be bit-exact (north_star); decrypted values within 2^-10 of
+the plaintext mirror; labels exact.  Inputs are seeded (synth) and shared as data; the oracle
+never consumes anything the CUDA path produced.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import ckks, plan
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def load_sign(name):
+    d = json.load(open(os.path.join(HERE, "..", "data", name)))
+    return [list(map(float, c)) for c in d["coeffs"]]
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2502_00847_b200 import build, secpe
+    build.build()
+    return secpe
+
+
+class Pair:
+    """Oracle params + GPU context for the same parameter description."""
+
+    def __init__(self, secpe, name):
+        self.desc = synth.PARAM_SETS[name]
+        self.prm = ckks.Params(self.desc)
+        self.gpu = secpe.Context(self.desc)
+        self.secpe = secpe
+
+    def up(self, ct):
+        """oracle Ct -> GPU Ct (upload of oracle data as an input)."""
+        t = torch.from_numpy(ct.data[None].copy()).cuda()
+        return self.secpe.Ct(t, ct.level, ct.scale)
+
+    @staticmethod
+    def down(ct, i=0):
+        torch.cuda.synchronize()
+        return ct.t[i].cpu().numpy()
+
+
+_pairs = {}
+
+
+def pair(S, name):
+    if name not in _pairs:
+        _pairs[name] = Pair(S, name)
+    return _pairs[name]
+
+
+# ---------------------------------------------------------------------------------------------
+def test_context_tables(S):
+    for name in ("toy", "argmax"):
+        P = pair(S, name)
+        primes, psi = P.gpu.info()
+        assert primes == P.prm.primes and psi == P.prm.psi
+
+
+@pytest.mark.parametrize("name,n_polys,first,n_limbs", [
+    ("toy", 1, 0, 8), ("toy", 3, 2, 5), ("toy", 2, 8, 1),       # ragged batch, offset limbs, special prime
+    ("ntt", 2, 0, 24), ("ntt", 1, 13, 11),                       # configs[1] primes at N = 2^16
+    ("argmax", 1, 25, 13),                                       # q tail + special primes
+])
+def test_ntt_bit_exact(S, name, n_polys, first, n_limbs):
+    P = pair(S, name)
+    prm = P.prm
+    primes = prm.primes[first:first + n_limbs]
+    x = synth.uniform_residues(100 + first, primes, n_polys, prm.logn)
+    t = torch.from_numpy(x.copy()).cuda()
+    P.gpu.ntt(t, first, n_limbs)
+    got = t.cpu().numpy()
+    # compare sampled limbs (oracle NTT is ~6 ms per 2^16 limb)
+    rng = np.random.default_rng(1)
+    for pi in range(n_polys):
+        for l in sorted(set(rng.integers(0, n_limbs, 3).tolist())):
+            want = ckks.ntt(x[pi, l], primes[l], prm.psi[first + l], prm.logn)
+            assert np.array_equal(got[pi, l], want), (pi, l)
+    P.gpu.ntt(t, first, n_limbs, inverse=True)
+    assert np.array_equal(t.cpu().numpy(), x)
+
+
+def test_ntt_edge_inputs(S):
+    P = pair(S, "toy")
+    prm = P.prm
+    for fill in ("zero", "max"):
+        x = np.zeros((1, 8, prm.N), dtype=np.uint64)
+        if fill == "max":
+            x[:] = np.array(prm.q, dtype=np.uint64)[None, :, None] - np.uint64(1)
+        t = torch.from_numpy(x.copy()).cuda()
+        P.gpu.ntt(t, 0, 8)
+        got = t.cpu().numpy()
+        for l in range(8):
+            assert np.array_equal(got[0, l], ckks.ntt(x[0, l], prm.q[l], prm.psi[l], prm.logn))
+
+
+def test_keys_bit_exact(S):
+    P = pair(S, "toy")
+    ev = ckks.Oracle(P.prm)
+    seed = synth.KEY_SEED_BASE + 1
+    ko = ev.keygen(seed, [1, -1, 4])
+    kg = P.gpu.keygen(seed, [1, -1, 4])
+    assert np.array_equal(kg.export(0), ko.s_ntt)
+    assert np.array_equal(kg.export(1), ko.pk)
+    assert np.array_equal(kg.export(2), ko.rlk)
+    for g, swk in ko.gk.items():
+        assert np.array_equal(kg.export(3, g), swk)
+
+
+@pytest.fixture(scope="module")
+def toy_env(S):
+    P = pair(S, "toy")
+    ev = ckks.Oracle(P.prm)
+    seed = synth.KEY_SEED_BASE + 1
+    steps = [1, -1, 3, 64]
+    return P, ev, ev.keygen(seed, steps), P.gpu.keygen(seed, steps)
+
+
+def test_encrypt_decrypt_bit_exact(toy_env):
+    P, ev, ko, kg = toy_env
+    prm = P.prm
+    z = synth.uniform_slots(7, prm.N // 2)
+    m = ckks.encode(prm, z, prm.scale)                      # oracle encoding = shared integer input
+    for level in (prm.L, 3, 0):
+        co = ev.encrypt_int(ko, m, level, prm.scale, 99)
+        cg = P.gpu.encrypt_coeffs(kg, m, level, prm.scale, 99)
+        assert np.array_equal(P.down(cg), co.data)
+        res = np.zeros((level + 1, prm.N), dtype=np.uint64)
+        ckks.lib().o_decrypt_residues(prm.cptr, ckks.P(ko.s_ntt), ckks.P(co.data), level, ckks.P(res))
+        assert np.array_equal(P.gpu.decrypt_residues(kg, cg), res)
+    # client encoders agree within +-1 per coefficient (reading R16) and decrypt is accurate
+    assert np.abs(P.gpu.encode(z, prm.scale) - m).max() <= 1
+    cg = P.gpu.encrypt(kg, z, prm.L, prm.scale, 5)
+    assert np.abs(P.gpu.decrypt(kg, cg) - z).max() < 2 ** -20
+
+
+def test_ops_bit_exact_toy(toy_env):
+    P, ev, ko, kg = toy_env
+    prm, g = P.prm, P.gpu
+    z1, z2 = synth.uniform_slots(1, prm.N // 2), synth.uniform_slots(2, prm.N // 2)
+    a = ev.encrypt(ko, z1, prm.scale, 1)
+    b = ev.encrypt(ko, z2, prm.scale, 2)
+    ga, gb = P.up(a), P.up(b)
+    b5 = ev.drop(b, 5)
+    chk = lambda gct, oct_: np.array_equal(P.down(gct), oct_.data)
+    assert chk(g.add(ga, gb), ev.add_raw(a, b))
+    assert chk(g.sub(ga, P.up(b5)), ev.sub_raw(a, b5))               # level alignment by drop
+    assert chk(g.add_const(ga, -0.3125), ckks.Ct(ev.add_int_raw(a, ckks.round_half_away(-0.3125 * a.scale)), 0))
+    assert chk(g.drop(ga, 2), ev.drop(a, 2))
+    r = g.rescale(ga)
+    ro = ev.rescale(a)
+    assert chk(r, ro) and r.scale == ro.scale
+    mr = g.mul_relin(kg, ga, gb)
+    assert chk(mr, ev.mul_relin(ko, a, b))
+    mc = g.mul_const(ga, 0.7, prm.scale, 4)
+    assert chk(mc, ev.mul_const(a, 0.7, prm.scale, 4))
+    for s in (1, -1, 3, 64):
+        assert chk(g.rotate(kg, ga, s), ev.rotate_raw(ko, a, s))
+    lay = dict(synth.LAYOUTS["toy"], queries=16)
+    mask = plan.mask_slots(lay, prm.N // 2)
+    assert chk(g.mul_mask(ga, mask, prm.scale), ev.mul_mask(a, mask, prm.scale))
+    with pytest.raises(P.secpe.SecpeError, match="scales"):
+        g.add(ga, g.rescale(gb))
+
+
+def test_ops_bit_exact_ks_config(S):
+    """configs[2]/[3] parameters (N = 2^16, 24 x 60-bit, dnum 3, 8 special primes)."""
+    P = pair(S, "ks")
+    prm, g = P.prm, P.gpu
+    ev = ckks.Oracle(prm)
+    seed = synth.KEY_SEED_BASE + 3
+    ko, kg = ev.keygen(seed, [1]), g.keygen(seed, [1])
+    z1, z2 = synth.uniform_slots(31, prm.N // 2), synth.uniform_slots(32, prm.N // 2)
+    a = ev.encrypt(ko, z1, prm.scale, 1)
+    b = ev.encrypt(ko, z2, prm.scale, 2)
+    ga, gb = P.up(a), P.up(b)
+    mo = ev.rescale(ev.mul_relin(ko, a, b))
+    mg = g.rescale(g.mul_relin(kg, ga, gb))
+    assert np.array_equal(P.down(mg), mo.data)
+    assert np.abs(P.gpu.decrypt(kg, mg) - z1 * z2).max() < 2 ** -10
+    ro = ev.rotate_raw(ko, a, 1)
+    assert np.array_equal(P.down(g.rotate(kg, ga, 1)), ro.data)
+
+
+def test_sign_poly_bit_exact(toy_env):
+    P, ev, ko, kg = toy_env
+    prm = P.prm
+    st = load_sign("sign_f1_f1.json")
+    x = synth.uniform_slots(9, prm.N // 2, -1, 1)
+    a = ev.encrypt(ko, x, prm.scale, 3)
+    so = plan.sign(ev, ko, a, st, prm.scale)
+    sg = P.gpu.sign_poly(kg, P.up(a), st, prm.scale)
+    assert np.array_equal(P.down(sg), so.data) and sg.scale == so.scale and sg.level == so.level
+
+
+def run_argmax_pair(S, pname, lname, sname, seed_in, n_ct=1, oracle_cts=1):
+    P = pair(S, pname)
+    prm, g = P.prm, P.gpu
+    st = load_sign(sname)
+    lay = synth.LAYOUTS[lname] if isinstance(lname, str) else lname
+    steps = plan.argmax_rotations(lay)
+    seed = synth.KEY_SEED_BASE + 7
+    ev = ckks.Oracle(prm)
+    ko, kg = ev.keygen(seed, steps), g.keygen(seed, steps)
+    gen = synth.toy_scores if pname.startswith("toy") else synth.softmax_scores
+    scores = [gen(seed_in + i, lay["queries"], lay["prompts"], lay["classes"]) for i in range(n_ct)]
+    cts = [ev.encrypt(ko, plan.pack(s, lay, prm.N // 2), prm.scale, 500 + i) for i, s in enumerate(scores)]
+    batch = S.Ct(torch.from_numpy(np.stack([c.data for c in cts])).cuda(), prm.L, prm.scale)
+    g.oplog(enable=True, clear=True)
+    out = g.enc_argmax(kg, batch, lay, st)
+    glog = g.oplog(enable=False, clear=True)
+    got = out.t.cpu().numpy()
+    mir = ckks.Mirror(prm)
+    for i in range(n_ct):
+        z = plan.pack(scores[i], lay, prm.N // 2)
+        ref = plan.argmax(ckks.Mirror(prm), None, ckks.MirrorCt(z, prm.L, prm.scale), lay, st)
+        dec = g.decrypt(kg, out, i)
+        assert np.abs(dec - ref.v).max() < 2 ** -10
+        mean = scores[i].mean(axis=1)
+        srt = np.sort(mean, axis=1)
+        ok = srt[:, -1] - srt[:, -2] >= 2.0 ** -7
+        assert (S.labels(dec, lay)[ok] == plan.true_labels(scores[i])[ok]).all()
+        if i < oracle_cts:
+            oo = plan.argmax(ev, ko, cts[i], lay, st)
+            assert np.array_equal(got[i], oo.data), "ciphertext %d differs from the oracle" % i
+            assert out.level == oo.level and out.scale == oo.scale
+    plan.argmax(mir, None, ckks.MirrorCt(np.zeros(prm.N // 2), prm.L, prm.scale), lay, st)
+    assert glog == mir.log  # identical planned op lists (reading R13)
+    return out
+
+
+def test_argmax_toy_bit_exact(S):
+    lay = dict(synth.LAYOUTS["toy"], queries=64)
+    run_argmax_pair(S, "toy_argmax", lay, "sign_f1_f1.json", 1001, n_ct=3, oracle_cts=3)
+
+
+def test_argmax_small_ring_bit_exact(S):
+    run_argmax_pair(S, "argmax_small", "argmax_small_k2", "sign_7_15_15.json", 5001, n_ct=2, oracle_cts=2)
+
+
+@pytest.mark.slow
+def test_argmax_config5_full(S):
+    """BASELINE configs[4] at full size (N = 2^16, 30 limbs, 2048 queries x P=8 x K=2), batch of 2 as bench:
+    ciphertext 0 bit-exact against the oracle, every query's label exact above the margin."""
+    run_argmax_pair(S, "argmax", "argmax_k2", "sign_7_15_15.json", 1000 * 5 + 1, n_ct=2, oracle_cts=1)
