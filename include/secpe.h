@@ -52,9 +52,10 @@ typedef struct {
     uint32_t log_n;     /* 10..17 */
     uint32_t n_q;       /* ciphertext primes q_0..q_L (L = n_q - 1), each < 2^62, == 1 mod 2N */
     const uint64_t *q;  /* host[n_q] */
-    uint32_t n_p;       /* special primes for hybrid key switching (>= 1) */
+    uint32_t n_p;       /* special primes for hybrid key switching (>= 1 for keys; 0 = NTT-only context) */
     const uint64_t *p;  /* host[n_p] */
-    uint32_t alpha;     /* primes per key-switching digit; dnum = ceil(n_q / alpha) */
+    uint32_t alpha;     /* primes per key-switching digit (<= 16); dnum = ceil(n_q / alpha) <= 32; the
+                           products of two primes times max(dnum, alpha, n_p) must stay < 2^125 */
     double scale;       /* nominal scale Delta used by the planner for intermediate results */
 } secpe_params;
 

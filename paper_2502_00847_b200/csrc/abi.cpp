@@ -1,6 +1,7 @@
 // abi.cpp -- extern "C" entry points of libsecpe.so (declared in include/secpe.h).
 // Exceptions never cross the boundary: every entry point maps them to a status code and a
 // thread-local message (secpe_last_error).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -93,13 +94,24 @@ int secpe_gen_primes(uint32_t bits, uint32_t count, uint32_t log_n, int32_t mode
 
 int secpe_ctx_create(const secpe_params *prm, void *stream, secpe_ctx **out) {
     return guard([&] {
-        REQUIRE(prm && out && prm->q && prm->p, SECPE_EINVAL, "null argument");
+        REQUIRE(prm && out && prm->q && (prm->p || prm->n_p == 0), SECPE_EINVAL, "null argument");
         REQUIRE(prm->log_n >= 11 && prm->log_n <= 17, SECPE_EINVAL, "log_n must be in [11, 17]");
-        REQUIRE(prm->n_q >= 1 && prm->n_p >= 1 && prm->n_q + prm->n_p <= MAXL, SECPE_EINVAL, "prime counts");
-        REQUIRE(prm->alpha >= 1 && prm->alpha <= 16 && (prm->n_q + prm->alpha - 1) / prm->alpha <= 16 &&
+        REQUIRE(prm->n_q >= 1 && prm->n_q + prm->n_p <= MAXL, SECPE_EINVAL, "prime counts");
+        REQUIRE(prm->alpha >= 1 && prm->alpha <= 16 && (prm->n_q + prm->alpha - 1) / prm->alpha <= 32 &&
                     prm->n_p <= 16,
-                SECPE_EINVAL, "alpha / dnum / special primes must be <= 16");
+                SECPE_EINVAL, "need alpha <= 16, dnum <= 32, special primes <= 16");
         const u64 two_n = (u64)2 << prm->log_n;
+        // lazy 128-bit accumulations (key inner product: dnum terms, ModUp: alpha terms, ModDown: n_p terms)
+        // must stay below 2^125 (Barrett input bound)
+        {
+            u64 mx = 0;
+            for (uint32_t i = 0; i < prm->n_q; i++) mx = std::max(mx, prm->q[i]);
+            for (uint32_t i = 0; i < prm->n_p; i++) mx = std::max(mx, prm->p[i]);
+            const double lg = 2.0 * std::log2((double)mx);
+            const int terms = (int)std::max({(prm->n_q + prm->alpha - 1) / prm->alpha, prm->alpha, prm->n_p});
+            REQUIRE(lg + std::log2((double)terms) < 124.9, SECPE_EINVAL,
+                    "prime sizes x dnum/alpha/n_p exceed the 128-bit lazy accumulation bound");
+        }
         for (uint32_t i = 0; i < prm->n_q + prm->n_p; i++) {
             const u64 v = i < prm->n_q ? prm->q[i] : prm->p[i - prm->n_q];
             REQUIRE(v > (1ULL << 32) && v < (1ULL << 62) && v % two_n == 1 && h_is_prime(v), SECPE_EINVAL,
@@ -147,6 +159,7 @@ size_t secpe_ct_bytes(const secpe_ctx *ctx, int32_t level) {
 int secpe_keygen(secpe_ctx *ctx, uint64_t seed, const int32_t *rot_steps, int32_t n_rot, secpe_keys **out) {
     return guard([&] {
         REQUIRE(ctx && out && (n_rot == 0 || rot_steps), SECPE_EINVAL, "null argument");
+        REQUIRE(ctx->c.np >= 1, SECPE_EINVAL, "key generation needs at least one special prime");
         auto h = std::make_unique<secpe_keys>();
         h->k = keygen(ctx->c, seed, rot_steps, n_rot);
         *out = h.release();

@@ -74,7 +74,8 @@ void ev_mul_plain_ntt(Ctx &c, const CtView &a, const u64 *pt, const CtView &out)
     c.cnt.launches++;
 }
 
-// O(rescale): r = [c_l + floor(q_l/2)]_{q_l} (coefficient form); c'_i = (c_i + [q_l/2]_{q_i} - [r]_{q_i}) q_l^{-1}
+// Rescale (R12): per coefficient r = [c_l + floor(q_l/2)]_{q_l}; c'_i = (c_i + [floor(q_l/2)]_{q_i} - [r]_{q_i}) q_l^{-1}.
+// The (half - r) polynomial is formed in the coefficient domain and NTT'd under each q_i.
 void ev_rescale(Ctx &c, const CtView &in, const CtView &out) {
     const size_t pa = c.prof_begin(2);
     const int l = in.level;
@@ -85,10 +86,10 @@ void ev_rescale(Ctx &c, const CtView &in, const CtView &out) {
     DevBuf last(2L * n * N, c.st), T(2L * n * l * N, c.st);
     k_copy_rows(c.logn, CRows{in.data + l * N, in.stride, in.ps}, RowsArg{last.p, 2 * N, N}, 2 * n, 1, c.st);
     ev_ntt(c, RowsArg{last.p, 2 * N, N}, 2 * n, LimbMap{1, 1, l, 0}, true);
-    k_rescale_bcast(c.tab, c.logn, last.p, 2 * N, T.p, 2L * l * N, n, l, c.st);
-    ev_ntt(c, RowsArg{T.p, 2L * l * N, (long)l * N}, 2 * n, qmap(l), false);
     const LevelConsts &lc = c.level(l);
-    k_rescale_combine(c.tab, c.logn, crows_of(in), T.p, 2L * l * N, out.data, out.stride, n, l, lc.half.p, lc.qlinv.p,
+    k_rescale_bcast(c.tab, c.logn, last.p, 2 * N, T.p, 2L * l * N, n, l, lc.half.p, c.st);
+    ev_ntt(c, RowsArg{T.p, 2L * l * N, (long)l * N}, 2 * n, qmap(l), false);
+    k_rescale_combine(c.tab, c.logn, crows_of(in), T.p, 2L * l * N, out.data, out.stride, n, l, lc.qlinv.p,
                       lc.qlinv_sh.p, c.st);
     c.cnt.launches += 3;
     c.cnt.rescale += n;

@@ -68,12 +68,12 @@ void k_moddown_combine(const Tab &tab, int logn, const u64 *acc, long acc_ct_str
                        cudaStream_t st);
 
 // ---- rescale (rescale.cu) --------------------------------------------------------------------
-// T[c][b][i] = ([r + half]_{q_l}) mod q_i for i < l, r = coeff-form last limb (tmp[c][b])
+// T[c][b][i] = [floor(q_l/2)]_{q_i} - ([r + floor(q_l/2)]_{q_l} mod q_i) for i < l, r = coeff-form last limb
 void k_rescale_bcast(const Tab &tab, int logn, const u64 *last, long last_ct_stride, u64 *T, long T_ct_stride,
-                     int n_ct, int l, cudaStream_t st);
-// out[c][b][i] = (in[c][b][i] + half_i - T[c][b][i]) * q_l^{-1}
+                     int n_ct, int l, const u64 *half, cudaStream_t st);
+// out[c][b][i] = (in[c][b][i] + NTT(T)[c][b][i]) * q_l^{-1}
 void k_rescale_combine(const Tab &tab, int logn, CRows in, const u64 *T,
-                       long T_ct_stride, u64 *out, long out_ct_stride, int n_ct, int l, const u64 *half,
+                       long T_ct_stride, u64 *out, long out_ct_stride, int n_ct, int l,
                        const u64 *qlinv, const u64 *qlinv_sh, cudaStream_t st);
 
 // ---- sampling / keys (sample.cu) ----------------------------------------------------------------

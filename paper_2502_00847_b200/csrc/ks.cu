@@ -43,7 +43,8 @@ __global__ void modup_kernel(Tab tab, int logn, const u64 *__restrict__ dc, long
 }
 
 // grid: x = coefficient chunks, y = extended limb e; loops over the n_ct ciphertexts so each key
-// word is read from HBM once per launch.
+// word is read from HBM once per launch (held in registers across the batch).  MAXB >= beta.
+template <int MAXB>
 __global__ void ks_inner_kernel(Tab tab, int logn, const u64 *__restrict__ d, long ds, const u64 *__restrict__ ext,
                                 long exts, const u64 *__restrict__ key, int nq_total, int np,
                                 u64 *__restrict__ acc, long accs, int n_ct, int nl, int alpha, int beta) {
@@ -53,9 +54,9 @@ __global__ void ks_inner_kernel(Tab tab, int logn, const u64 *__restrict__ d, lo
     const int ne = nl + np, nk = nq_total + np;
     const int pr = e < nl ? e : nq_total + (e - nl);
     const u64 q = tab.q[pr], r0 = tab.br0[pr], r1 = tab.br1[pr];
-    u64 kb[MAXA], ka[MAXA];
+    u64 kb[MAXB], ka[MAXB];
 #pragma unroll
-    for (int j = 0; j < MAXA; j++)
+    for (int j = 0; j < MAXB; j++)
         if (j < beta) {
             kb[j] = __ldg(key + (((long)j * 2 + 0) * nk + pr) * N + k);
             ka[j] = __ldg(key + (((long)j * 2 + 1) * nk + pr) * N + k);
@@ -64,7 +65,7 @@ __global__ void ks_inner_kernel(Tab tab, int logn, const u64 *__restrict__ d, lo
     for (int c = 0; c < n_ct; c++) {
         U128 s0{0, 0}, s1{0, 0};
 #pragma unroll
-        for (int j = 0; j < MAXA; j++)
+        for (int j = 0; j < MAXB; j++)
             if (j < beta) {
                 const u64 x = (j == jd) ? d[c * ds + e * N + k] : ext[c * exts + ((long)j * ne + e) * N + k];
                 mac_wide(s0, x, kb[j]);
@@ -118,23 +119,25 @@ __global__ void moddown_combine_kernel(Tab tab, int logn, const u64 *__restrict_
     out[ct * outs + ((long)b * nl + i) * N + k] = v;
 }
 
-// rescale, step 1: T[c][b][i] = ([r + half]_{q_l}) mod q_i, r = coefficient-form limb l
+// rescale, step 1 (coefficient domain): T[c][b][i] = [floor(q_l/2)]_{q_i} - [r]_{q_i} mod q_i with
+// r = [c_l + floor(q_l/2)]_{q_l} per coefficient (the half is added to every coefficient).
 // grid: y = (ct * 2 + b) * l + i
 __global__ void rescale_bcast_kernel(Tab tab, int logn, const u64 *__restrict__ last, long lasts,
-                                     u64 *__restrict__ T, long Ts, int l) {
+                                     u64 *__restrict__ T, long Ts, int l, const u64 *__restrict__ half) {
     const int row = blockIdx.y;
     const int i = row % l, b = (row / l) % 2, ct = row / (2 * l);
     const long N = 1L << logn;
     const long k = (long)blockIdx.x * TPB + threadIdx.x;
     const u64 ql = tab.q[l];
     const u64 r = csub(last[ct * lasts + (long)b * N + k] + (ql >> 1), ql);
-    T[ct * Ts + ((long)b * l + i) * N + k] = barrett128(U128{r, 0}, tab.q[i], tab.br0[i], tab.br1[i]);
+    const u64 qi = tab.q[i];
+    T[ct * Ts + ((long)b * l + i) * N + k] = submod(half[i], barrett128(U128{r, 0}, qi, tab.br0[i], tab.br1[i]), qi);
 }
 
-// rescale, step 2 (NTT domain): out = (in + half_i - T) * q_l^{-1}
+// rescale, step 2 (NTT domain): out = (in + NTT(T)) * q_l^{-1}
 __global__ void rescale_combine_kernel(Tab tab, int logn, CRows in,
                                        const u64 *__restrict__ T, long Ts, u64 *__restrict__ out, long outs, int l,
-                                       const u64 *__restrict__ half, const u64 *__restrict__ qlinv,
+                                       const u64 *__restrict__ qlinv,
                                        const u64 *__restrict__ qlinv_sh) {
     const int row = blockIdx.y;
     const int i = row % l, b = (row / l) % 2, ct = row / (2 * l);
@@ -143,7 +146,7 @@ __global__ void rescale_combine_kernel(Tab tab, int logn, CRows in,
     const u64 q = tab.q[i];
     const u64 x = in.p[poly_off(in.cs, in.ps, 2 * ct + b) + (long)i * N + k];
     const u64 t = T[ct * Ts + ((long)b * l + i) * N + k];
-    const u64 v = submod(addmod(x, half[i], q), t, q);
+    const u64 v = addmod(x, t, q);
     out[ct * outs + ((long)b * l + i) * N + k] = mul_shoup(v, qlinv[i], qlinv_sh[i], q);
 }
 }  // namespace
@@ -161,9 +164,23 @@ void k_modup(const Tab &tab, int logn, const u64 *dc, long dcs, u64 *ext, long e
 void k_ks_inner(const Tab &tab, int logn, const u64 *d, long ds, const u64 *ext, long exts, const u64 *key,
                 int nq_total, int np, u64 *acc, long accs, int n_ct, int nl, int alpha, cudaStream_t st) {
     const int beta = (nl + alpha - 1) / alpha;
-    if (beta > MAXA) throw SecpeError{-1, "dnum > 16 not supported"};
-    ks_inner_kernel<<<dim3(chunks(logn), nl + np), TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc,
-                                                                  accs, n_ct, nl, alpha, beta);
+    const dim3 grid(chunks(logn), nl + np);
+    // 128-bit accumulation of beta products < 2^124 each requires beta <= 16 per Barrett input bound
+    // (2^125); larger dnum only occurs with small primes (toy: 40-bit, products < 2^80).
+    if (beta <= 4)
+        ks_inner_kernel<4><<<grid, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, n_ct, nl,
+                                                 alpha, beta);
+    else if (beta <= 8)
+        ks_inner_kernel<8><<<grid, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, n_ct, nl,
+                                                 alpha, beta);
+    else if (beta <= 16)
+        ks_inner_kernel<16><<<grid, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, n_ct, nl,
+                                                  alpha, beta);
+    else if (beta <= 32)
+        ks_inner_kernel<32><<<grid, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, n_ct, nl,
+                                                  alpha, beta);
+    else
+        throw SecpeError{-1, "dnum > 32 not supported"};
     LAUNCH_CHECK();
 }
 void k_moddown_conv(const Tab &tab, int logn, const u64 *acc, long accs, u64 *T, long Ts, int n_ct, int nl, int np,
@@ -182,13 +199,13 @@ void k_moddown_combine(const Tab &tab, int logn, const u64 *acc, long accs, cons
     LAUNCH_CHECK();
 }
 void k_rescale_bcast(const Tab &tab, int logn, const u64 *last, long lasts, u64 *T, long Ts, int n_ct, int l,
-                     cudaStream_t st) {
-    rescale_bcast_kernel<<<dim3(chunks(logn), n_ct * 2 * l), TPB, 0, st>>>(tab, logn, last, lasts, T, Ts, l);
+                     const u64 *half, cudaStream_t st) {
+    rescale_bcast_kernel<<<dim3(chunks(logn), n_ct * 2 * l), TPB, 0, st>>>(tab, logn, last, lasts, T, Ts, l, half);
     LAUNCH_CHECK();
 }
 void k_rescale_combine(const Tab &tab, int logn, CRows in, const u64 *T, long Ts, u64 *out, long outs,
-                       int n_ct, int l, const u64 *half, const u64 *qlinv, const u64 *qlinv_sh, cudaStream_t st) {
+                       int n_ct, int l, const u64 *qlinv, const u64 *qlinv_sh, cudaStream_t st) {
     rescale_combine_kernel<<<dim3(chunks(logn), n_ct * 2 * l), TPB, 0, st>>>(tab, logn, in, T, Ts, out, outs, l,
-                                                                              half, qlinv, qlinv_sh);
+                                                                              qlinv, qlinv_sh);
     LAUNCH_CHECK();
 }

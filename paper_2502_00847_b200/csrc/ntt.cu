@@ -114,7 +114,7 @@ struct PassArgs {
 template <int S, bool INV>
 __global__ void __launch_bounds__(STRIDED_C *(1 << S) / 8)
     ntt_strided(PassArgs a) {
-    constexpr int G = 1 << S, TPG = G / 8, C = STRIDED_C;
+    constexpr int G = 1 << S, C = STRIDED_C;
     __shared__ u64 sm[G * C];
     const int nl = a.lm.nl;
     const int poly = blockIdx.y / nl, limb = blockIdx.y % nl;
