@@ -49,8 +49,9 @@ typedef struct secpe_keys secpe_keys; /* opaque: secret/public/relinearisation/G
 
 /* RNS-CKKS parameters (R_Q = Z_Q[X]/(X^N+1), Q = prod q_i). */
 typedef struct {
-    uint32_t log_n;     /* 10..17 */
-    uint32_t n_q;       /* ciphertext primes q_0..q_L (L = n_q - 1), each < 2^62, == 1 mod 2N */
+    uint32_t log_n;     /* 12..16 */
+    uint32_t n_q;       /* ciphertext primes q_0..q_L (L = n_q - 1), each in (2^32, 2^60), == 1 mod 2N (all primes,
+                           special ones included: the split-30 base-conversion MACs need < 2^60) */
     const uint64_t *q;  /* host[n_q] */
     uint32_t n_p;       /* special primes for hybrid key switching (>= 1 for keys; 0 = NTT-only context) */
     const uint64_t *p;  /* host[n_p] */

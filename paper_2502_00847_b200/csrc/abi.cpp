@@ -95,7 +95,7 @@ int secpe_gen_primes(uint32_t bits, uint32_t count, uint32_t log_n, int32_t mode
 int secpe_ctx_create(const secpe_params *prm, void *stream, secpe_ctx **out) {
     return guard([&] {
         REQUIRE(prm && out && prm->q && (prm->p || prm->n_p == 0), SECPE_EINVAL, "null argument");
-        REQUIRE(prm->log_n >= 11 && prm->log_n <= 17, SECPE_EINVAL, "log_n must be in [11, 17]");
+        REQUIRE(prm->log_n >= 12 && prm->log_n <= 16, SECPE_EINVAL, "log_n must be in [12, 16]");
         REQUIRE(prm->n_q >= 1 && prm->n_q + prm->n_p <= MAXL, SECPE_EINVAL, "prime counts");
         REQUIRE(prm->alpha >= 1 && prm->alpha <= 16 && (prm->n_q + prm->alpha - 1) / prm->alpha <= 32 &&
                     prm->n_p <= 16,
@@ -114,8 +114,8 @@ int secpe_ctx_create(const secpe_params *prm, void *stream, secpe_ctx **out) {
         }
         for (uint32_t i = 0; i < prm->n_q + prm->n_p; i++) {
             const u64 v = i < prm->n_q ? prm->q[i] : prm->p[i - prm->n_q];
-            REQUIRE(v > (1ULL << 32) && v < (1ULL << 62) && v % two_n == 1 && h_is_prime(v), SECPE_EINVAL,
-                    "primes must be NTT-friendly primes in (2^32, 2^62)");
+            REQUIRE(v > (1ULL << 32) && v < (1ULL << 60) && v % two_n == 1 && h_is_prime(v), SECPE_EINVAL,
+                    "primes must be NTT-friendly primes in (2^32, 2^60)");
         }
         int ndev = 0;
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)

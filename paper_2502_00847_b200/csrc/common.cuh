@@ -69,10 +69,8 @@ struct Tab {
     const u64 *q;      // [P]
     const u64 *br0;    // [P] Barrett floor(2^128/q) low word
     const u64 *br1;    // [P] high word
-    const u64 *tw;     // [P][N]  psi^{brv(i)}            (forward CT twiddles)
-    const u64 *twsh;   // [P][N]  Shoup companions
-    const u64 *itw;    // [P][N]  psi^{-brv(i)}           (inverse GS twiddles)
-    const u64 *itwsh;  // [P][N]
+    const ulonglong2 *tw2;   // [P][N] {psi^{brv(i)}, Shoup companion}   (forward CT twiddles)
+    const ulonglong2 *itw2;  // [P][N] {psi^{-brv(i)}, Shoup companion}  (inverse GS twiddles)
     const u64 *ninv;   // [P] N^{-1} mod q
     const u64 *ninvsh; // [P]
 };

@@ -33,6 +33,9 @@ DevBuf &DevBuf::operator=(DevBuf &&o) noexcept {
     return *this;
 }
 
+// split-30 packed constant for the base-conversion MACs (ks.cu): (c >> 30) << 32 | (c mod 2^30)
+static u64 pack30(u64 c) { return ((c >> 30) << 32) | (c & ((1ULL << 30) - 1)); }
+
 static DevBuf upload(const std::vector<u64> &h, cudaStream_t st) {
     DevBuf b(std::max<size_t>(h.size(), 1), st);
     if (!h.empty()) CUDA_CHECK(cudaMemcpyAsync(b.p, h.data(), h.size() * sizeof(u64), cudaMemcpyHostToDevice, st));
@@ -210,7 +213,7 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
     const int P = nprimes();
     psi.resize(P);
     std::vector<u64> hq(P), hr0(P), hr1(P), hni(P), hnish(P);
-    std::vector<u64> tw((size_t)P * N), twsh((size_t)P * N), itw((size_t)P * N), itwsh((size_t)P * N);
+    std::vector<u64> tw(2 * (size_t)P * N), itw(2 * (size_t)P * N);  // interleaved {w, w'}
     for (int i = 0; i < P; i++) {
         const u64 qi = primes[i];
         psi[i] = h_find_psi(qi, logn);
@@ -231,10 +234,10 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
         for (long k = 0; k < N; k++) {
             const unsigned b = brv((unsigned)k, logn);
             const size_t o = (size_t)i * N + k;
-            tw[o] = pw[b];
-            twsh[o] = h_shoup(pw[b], qi);
-            itw[o] = ipw[b];
-            itwsh[o] = h_shoup(ipw[b], qi);
+            tw[2 * o] = pw[b];
+            tw[2 * o + 1] = h_shoup(pw[b], qi);
+            itw[2 * o] = ipw[b];
+            itw[2 * o + 1] = h_shoup(ipw[b], qi);
         }
     }
     h_br0 = hr0;
@@ -245,10 +248,9 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
     d_ninv = upload(hni, st);
     d_ninvsh = upload(hnish, st);
     d_tw = upload(tw, st);
-    d_twsh = upload(twsh, st);
     d_itw = upload(itw, st);
-    d_itwsh = upload(itwsh, st);
-    tab = Tab{d_q.p, d_br0.p, d_br1.p, d_tw.p, d_twsh.p, d_itw.p, d_itwsh.p, d_ninv.p, d_ninvsh.p};
+    tab = Tab{d_q.p, d_br0.p, d_br1.p, reinterpret_cast<const ulonglong2 *>(d_tw.p),
+              reinterpret_cast<const ulonglong2 *>(d_itw.p), d_ninv.p, d_ninvsh.p};
 
     // ModDown constants: P = prod p
     std::vector<u64> vihp(std::max(np, 1)), vihpsh(std::max(np, 1)), vhatp((size_t)std::max(np, 1) * nq),
@@ -264,7 +266,7 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
             u64 hq2 = 1;
             for (int b = 0; b < np; b++)
                 if (b != a) hq2 = h_mulmod(hq2, primes[nq + b] % primes[i], primes[i]);
-            vhatp[(size_t)a * nq + i] = hq2;
+            vhatp[(size_t)a * nq + i] = pack30(hq2);
         }
     }
     for (int i = 0; i < nq; i++) {
@@ -275,6 +277,16 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
     }
     ihp = upload(vihp, st);
     ihp_sh = upload(vihpsh, st);
+    {
+        std::vector<u64> a(std::max(np, 1)), b(std::max(np, 1));
+        for (int i = 0; i < np; i++) {
+            const u64 pi = primes[nq + i];
+            a[i] = h_mulmod(vihp[i], h_invmod((u64)N % pi, pi), pi);
+            b[i] = h_shoup(a[i], pi);
+        }
+        ihp_ninv = upload(a, st);
+        ihp_ninv_sh = upload(b, st);
+    }
     hat_p = upload(vhatp, st);
     pinv = upload(vpinv, st);
     pinv_sh = upload(vpinvsh, st);
@@ -300,12 +312,21 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
                     u64 ht = 1;
                     for (int i2 = i0; i2 < i1; i2++)
                         if (i2 != i) ht = h_mulmod(ht, primes[i2] % t, t);
-                    hat[((size_t)j * 16 + (i - i0)) * ne + e] = ht;
+                    hat[((size_t)j * 16 + (i - i0)) * ne + e] = pack30(ht);
                 }
             }
         }
         lc->inv_hat = upload(ih, st);
         lc->inv_hat_sh = upload(ihs, st);
+        {
+            std::vector<u64> a(nl), b(nl);
+            for (int i = 0; i < nl; i++) {
+                a[i] = h_mulmod(ih[i], h_invmod((u64)N % primes[i], primes[i]), primes[i]);
+                b[i] = h_shoup(a[i], primes[i]);
+            }
+            lc->inv_hat_ninv = upload(a, st);
+            lc->inv_hat_ninv_sh = upload(b, st);
+        }
         lc->hat = upload(hat, st);
         if (l >= 1) {
             std::vector<u64> hf(l), qi(l), qis(l);

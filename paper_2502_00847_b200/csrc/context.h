@@ -26,7 +26,8 @@ struct DevBuf {
 struct LevelConsts {
     int nl, beta;
     DevBuf inv_hat, inv_hat_sh;  // [nl]  (Q'_j / q_i)^{-1} mod q_i
-    DevBuf hat;                  // [beta][16][ne]  (Q'_j / q_i) mod t_e
+    DevBuf inv_hat_ninv, inv_hat_ninv_sh;  // [nl]  N^{-1} (Q'_j / q_i)^{-1} mod q_i (folded into the INTT)
+    DevBuf hat;                  // [beta][16][ne]  (Q'_j / q_i) mod t_e, split-30 packed
     DevBuf half, qlinv, qlinv_sh;  // rescale by q_{nl-1}: [nl-1]
 };
 
@@ -71,10 +72,11 @@ struct Ctx {
     std::vector<u64> primes, psi;  // q_0..q_L, p_0..p_{k-1}
     cudaStream_t st = nullptr;
     // tables
-    DevBuf d_q, d_br0, d_br1, d_tw, d_twsh, d_itw, d_itwsh, d_ninv, d_ninvsh;
+    DevBuf d_q, d_br0, d_br1, d_tw, d_itw, d_ninv, d_ninvsh;
     Tab tab{};
     // ModDown constants
-    DevBuf ihp, ihp_sh, hat_p, pinv, pinv_sh;
+    DevBuf ihp, ihp_sh, hat_p, pinv, pinv_sh;  // hat_p split-30 packed
+    DevBuf ihp_ninv, ihp_ninv_sh;               // N^{-1} (P/p)^{-1} mod p (folded into the INTT)
     std::vector<std::unique_ptr<LevelConsts>> lvl;  // index = level
     // host copies used by planning
     std::vector<u64> h_br0, h_br1;
@@ -119,7 +121,7 @@ double round_half_away(double x);
 // evaluator primitives (eval.cu) -- all operate on batches of n ciphertexts
 // Outputs are compact views (stride = 2 (level+1) N, ps = (level+1) N) supplied by the caller.
 CtView compact_view(const Ctx &c, u64 *data, int n, int level, double scale);
-void ev_ntt(Ctx &c, RowsArg d, int n_polys, LimbMap lm, bool inverse);
+void ev_ntt(Ctx &c, RowsArg d, int n_polys, LimbMap lm, bool inverse, const NttFusion &f = NttFusion());
 void ev_copy(Ctx &c, const CtView &a, const CtView &out);
 void ev_addsub(Ctx &c, const CtView &a, const CtView &b, const CtView &out, bool sub);
 void ev_mul_int(Ctx &c, const CtView &a, i64 C, const CtView &out);

@@ -25,12 +25,12 @@ LimbConst limb_const(const Ctx &c, i64 C, int nl) {
     return lc;
 }
 
-void ev_ntt(Ctx &c, RowsArg d, int n_polys, LimbMap lm, bool inverse) {
+void ev_ntt(Ctx &c, RowsArg d, int n_polys, LimbMap lm, bool inverse, const NttFusion &f) {
     const size_t pa = c.prof_begin(0);
     if (inverse)
-        ntt_inverse(c.tab, c.logn, d, n_polys, lm, c.st);
+        ntt_inverse(c.tab, c.logn, d, n_polys, lm, c.st, f);
     else
-        ntt_forward(c.tab, c.logn, d, n_polys, lm, c.st);
+        ntt_forward(c.tab, c.logn, d, n_polys, lm, c.st, f);
     c.cnt.ntt_limbs += (long long)n_polys * lm.nl;
     c.cnt.launches += 2;
     // algorithmic bytes: every limb read once and written once
@@ -75,7 +75,8 @@ void ev_mul_plain_ntt(Ctx &c, const CtView &a, const u64 *pt, const CtView &out)
 }
 
 // Rescale (R12): per coefficient r = [c_l + floor(q_l/2)]_{q_l}; c'_i = (c_i + [floor(q_l/2)]_{q_i} - [r]_{q_i}) q_l^{-1}.
-// The (half - r) polynomial is formed in the coefficient domain and NTT'd under each q_i.
+// Two fused transforms: INTT of the last limb (copy fused into its first pass), then a forward NTT
+// whose first pass forms (half - r) under each q_i and whose last pass adds c_i and scales by q_l^{-1}.
 void ev_rescale(Ctx &c, const CtView &in, const CtView &out) {
     const size_t pa = c.prof_begin(2);
     const int l = in.level;
@@ -84,14 +85,22 @@ void ev_rescale(Ctx &c, const CtView &in, const CtView &out) {
     const long N = c.N;
     const int n = in.n;
     DevBuf last(2L * n * N, c.st), T(2L * n * l * N, c.st);
-    k_copy_rows(c.logn, CRows{in.data + l * N, in.stride, in.ps}, RowsArg{last.p, 2 * N, N}, 2 * n, 1, c.st);
-    ev_ntt(c, RowsArg{last.p, 2 * N, N}, 2 * n, LimbMap{1, 1, l, 0}, true);
+    NttFusion fi;
+    fi.in_mode = 1;
+    fi.src = CRows{in.data + l * N, in.stride, in.ps};
+    ev_ntt(c, RowsArg{last.p, 2 * N, N}, 2 * n, LimbMap{1, 1, l, 0}, true, fi);
     const LevelConsts &lc = c.level(l);
-    k_rescale_bcast(c.tab, c.logn, last.p, 2 * N, T.p, 2L * l * N, n, l, lc.half.p, c.st);
-    ev_ntt(c, RowsArg{T.p, 2L * l * N, (long)l * N}, 2 * n, qmap(l), false);
-    k_rescale_combine(c.tab, c.logn, crows_of(in), T.p, 2L * l * N, out.data, out.stride, n, l, lc.qlinv.p,
-                      lc.qlinv_sh.p, c.st);
-    c.cnt.launches += 3;
+    NttFusion ff;
+    ff.in_mode = 2;
+    ff.src = CRows{last.p, 2 * N, N};
+    ff.lp = l;
+    ff.half = lc.half.p;
+    ff.out_mode = 1;
+    ff.e1 = crows_of(in);
+    ff.out = rows_of(out);
+    ff.k = lc.qlinv.p;
+    ff.ksh = lc.qlinv_sh.p;
+    ev_ntt(c, RowsArg{T.p, 2L * l * N, (long)l * N}, 2 * n, qmap(l), false, ff);
     c.cnt.rescale += n;
     // algorithmic bytes: read 2(l+1) limbs, write 2l limbs per ciphertext
     c.prof_end(pa, 2, 8.0 * (double)n * (2 * (l + 1) + 2 * l) * N, n);
@@ -105,15 +114,19 @@ void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u
     const int nl = level + 1, np = c.np, ne = nl + np, bt = c.beta(level);
     const LevelConsts &lc = c.level(level);
     const size_t pa = c.prof_begin(1);
-    // 1. coefficient form of d
+    // 1. y_i = [INTT(d)_i (Q'_j/q_i)^{-1}]_{q_i}: copy and the ModUp factor fused into the INTT
     DevBuf dc((size_t)n * nl * N, c.st);
-    k_copy_rows(c.logn, CRows{d, 2 * d_stride, d_stride}, RowsArg{dc.p, 2L * nl * N, (long)nl * N}, n, nl, c.st);
-    ev_ntt(c, RowsArg{dc.p, 2L * nl * N, (long)nl * N}, n, qmap(nl), true);
+    NttFusion f1;
+    f1.in_mode = 1;
+    f1.src = CRows{d, 2 * d_stride, d_stride};
+    f1.k = lc.inv_hat_ninv.p;
+    f1.ksh = lc.inv_hat_ninv_sh.p;
+    ev_ntt(c, RowsArg{dc.p, 2L * nl * N, (long)nl * N}, n, qmap(nl), true, f1);
     // 2. ModUp into every digit's complement, then NTT of the converted limbs
     const long exts = (long)bt * ne * N;
     DevBuf ext((size_t)n * exts, c.st);
-    k_modup(c.tab, c.logn, dc.p, (long)nl * N, ext.p, exts, n, nl, np, c.nq, c.alpha, lc.inv_hat.p,
-            lc.inv_hat_sh.p, lc.hat.p, c.st);
+    k_modup(c.tab, c.logn, dc.p, (long)nl * N, ext.p, exts, n, nl, np, c.nq, c.alpha, nullptr, nullptr, lc.hat.p,
+            c.st);
     for (int j = 0; j < bt; j++) {
         const int i0 = j * c.alpha, i1 = std::min(i0 + c.alpha, nl);
         if (i0 > 0) ev_ntt(c, RowsArg{ext.p + (long)j * ne * N, 2 * exts, exts}, n, LimbMap{i0, i0, 0, 0}, false);
@@ -124,15 +137,25 @@ void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u
     const long accs = 2L * ne * N;
     DevBuf acc((size_t)n * accs, c.st);
     k_ks_inner(c.tab, c.logn, d, d_stride, ext.p, exts, key, c.nq, np, acc.p, accs, n, nl, c.alpha, c.st);
-    // 4. ModDown: INTT of the special limbs, conversion to Q, NTT, subtract and scale by P^{-1}
-    ev_ntt(c, RowsArg{acc.p + (long)nl * N, accs, (long)ne * N}, 2 * n, LimbMap{np, 0, 0, c.nq}, true);
+    // 4. ModDown: INTT of the special limbs (with (P/p)^{-1} folded in), conversion to Q, then an NTT
+    //    whose last pass forms (acc - T) P^{-1} + addend
+    NttFusion f4;
+    f4.k = c.ihp_ninv.p;
+    f4.ksh = c.ihp_ninv_sh.p;
+    ev_ntt(c, RowsArg{acc.p + (long)nl * N, accs, (long)ne * N}, 2 * n, LimbMap{np, 0, 0, c.nq}, true, f4);
     const long Ts = 2L * nl * N;
     DevBuf T((size_t)n * Ts, c.st);
-    k_moddown_conv(c.tab, c.logn, acc.p, accs, T.p, Ts, n, nl, np, c.nq, c.ihp.p, c.ihp_sh.p, c.hat_p.p, c.st);
-    ev_ntt(c, RowsArg{T.p, Ts, (long)nl * N}, 2 * n, qmap(nl), false);
-    k_moddown_combine(c.tab, c.logn, acc.p, accs, T.p, Ts, add, add_stride, add_polys, out, out_stride, n, nl, ne,
-                      c.pinv.p, c.pinv_sh.p, c.st);
-    c.cnt.launches += 5;
+    k_moddown_conv(c.tab, c.logn, acc.p, accs, T.p, Ts, n, nl, np, c.nq, nullptr, nullptr, c.hat_p.p, c.st);
+    NttFusion f6;
+    f6.out_mode = 2;
+    f6.e1 = CRows{acc.p, accs, (long)ne * N};
+    f6.e2 = CRows{add, add_stride, (long)nl * N};
+    f6.e2_polys = add ? add_polys : 0;
+    f6.out = RowsArg{out, out_stride, (long)nl * N};
+    f6.k = c.pinv.p;
+    f6.ksh = c.pinv_sh.p;
+    ev_ntt(c, RowsArg{T.p, Ts, (long)nl * N}, 2 * n, qmap(nl), false, f6);
+    c.cnt.launches += 3;
     c.cnt.keyswitch += n;
     // algorithmic bytes: input limbs + output limbs per ciphertext + the key once per batch
     c.prof_end(pa, 1, 8.0 * N * ((double)n * (nl + 2 * nl + add_polys * nl) + 2.0 * bt * ne), n);

@@ -22,9 +22,30 @@ struct LimbConst {
 };
 
 // ---- NTT (ntt.cu) -------------------------------------------------------------------------
-// data: n_polys polynomials (RowsArg addressing) of lm.nl limbs each; in place.
-void ntt_forward(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st);
-void ntt_inverse(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st);
+// data: n_polys polynomials (RowsArg addressing) of lm.nl limbs each; in place unless fused.
+// Fusions (all optional; the default is a plain in-place transform):
+//   in_mode  1 (inverse): the first pass reads polynomial P, limb i from src (copy fused in)
+//   in_mode  2 (forward): rescale broadcast (R12): the input of limb i is
+//            [floor(q_l/2)]_{q_i} - [[x + floor(q_l/2)]_{q_l}]_{q_i}, x = src row of polynomial P
+//            (one coefficient-form limb, prime lp); half[i] = [floor(q_l/2)]_{q_i}
+//   out_mode 1 (forward): out = (e1 + NTT(x)) * k[i]            (rescale: e1 = ciphertext, k = q_l^-1)
+//   out_mode 2 (forward): out = (e1 - NTT(x)) * k[i] (+ e2 for polys with (P & 1) < e2_polys)
+//            (ModDown R11: e1 = acc, k = P^-1, e2 = tensor / sigma(c0) addend)
+//   k/ksh on an inverse transform: per-limb final factor replacing N^{-1} (must include it)
+struct NttFusion {
+    int in_mode = 0, out_mode = 0;
+    CRows src{nullptr, 0, 0};
+    int lp = 0;
+    const u64 *half = nullptr;
+    CRows e1{nullptr, 0, 0}, e2{nullptr, 0, 0};
+    int e2_polys = 0;
+    RowsArg out{nullptr, 0, 0};
+    const u64 *k = nullptr, *ksh = nullptr;
+};
+void ntt_forward(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
+                 const NttFusion &f = NttFusion());
+void ntt_inverse(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
+                 const NttFusion &f = NttFusion());
 
 void k_addsub(const Tab &tab, int logn, CRows a, CRows b, RowsArg out, int n_polys, LimbMap lm,
               bool sub, cudaStream_t st);
@@ -49,7 +70,7 @@ void k_automorph(int logn, CRows a, RowsArg out, int n_polys, int nl, u64 galois
 struct KsLevel;  // per-level constants (device pointers), see context.h
 // ModUp base conversion (coefficient domain): for every digit j and extended limb e not in I_j:
 //   ext[c][j][e] = sum_{i in I_j} [dc_i (Q'_j/q_i)^-1]_{q_i} [Q'_j/q_i]_{t_e}  mod t_e
-// dc: [n_ct][nl][N] coefficient form; ext: [n_ct][beta][ne][N]
+// dc: [n_ct][nl][N] coefficient form (inv_hat == nullptr: dc already holds [dc_i (Q'_j/q_i)^-1]); ext: [n_ct][beta][ne][N]
 void k_modup(const Tab &tab, int logn, const u64 *dc, long dc_ct_stride, u64 *ext, long ext_ct_stride,
              int n_ct, int nl, int np, int nq_total, int alpha, const u64 *inv_hat, const u64 *inv_hat_sh,
              const u64 *hat, cudaStream_t st);
@@ -57,25 +78,11 @@ void k_modup(const Tab &tab, int logn, const u64 *dc, long dc_ct_stride, u64 *ex
 void k_ks_inner(const Tab &tab, int logn, const u64 *d, long d_ct_stride, const u64 *ext, long ext_ct_stride,
                 const u64 *key, int nq_total, int np, u64 *acc, long acc_ct_stride, int n_ct, int nl,
                 int alpha, cudaStream_t st);
-// ModDown conversion: T[c][b][i] = sum_p [r_p (P/p)^-1]_p [P/p]_{q_i} mod q_i ; r = acc P-limbs (coeff form)
+// ModDown conversion: T[c][b][i] = sum_p [r_p (P/p)^-1]_p [P/p]_{q_i} mod q_i ; r = acc P-limbs (coeff form);
+// inv_hat_p == nullptr: the P-limbs already hold [r_p (P/p)^-1]_p (factor folded into the INTT)
 void k_moddown_conv(const Tab &tab, int logn, const u64 *acc, long acc_ct_stride, u64 *T, long T_ct_stride,
                     int n_ct, int nl, int np, int nq_total, const u64 *inv_hat_p, const u64 *inv_hat_p_sh,
                     const u64 *hat_p, cudaStream_t st);
-// out[c][b][i] = addend[c][b][i] + (acc[c][b][i] - T[c][b][i]) * P^-1   (addend may be null for b)
-void k_moddown_combine(const Tab &tab, int logn, const u64 *acc, long acc_ct_stride, const u64 *T,
-                       long T_ct_stride, const u64 *addend, long add_ct_stride, int add_polys, u64 *out,
-                       long out_ct_stride, int n_ct, int nl, int ne, const u64 *pinv, const u64 *pinv_sh,
-                       cudaStream_t st);
-
-// ---- rescale (rescale.cu) --------------------------------------------------------------------
-// T[c][b][i] = [floor(q_l/2)]_{q_i} - ([r + floor(q_l/2)]_{q_l} mod q_i) for i < l, r = coeff-form last limb
-void k_rescale_bcast(const Tab &tab, int logn, const u64 *last, long last_ct_stride, u64 *T, long T_ct_stride,
-                     int n_ct, int l, const u64 *half, cudaStream_t st);
-// out[c][b][i] = (in[c][b][i] + NTT(T)[c][b][i]) * q_l^{-1}
-void k_rescale_combine(const Tab &tab, int logn, CRows in, const u64 *T,
-                       long T_ct_stride, u64 *out, long out_ct_stride, int n_ct, int l,
-                       const u64 *qlinv, const u64 *qlinv_sh, cudaStream_t st);
-
 // ---- sampling / keys (sample.cu) ----------------------------------------------------------------
 // uniform residues in the NTT domain: out[l][k] for prime ids map (formula lm), counter layout per R6
 void k_sample_uniform(const Tab &tab, int logn, u64 seed, u64 tag, u64 *out, LimbMap lm, cudaStream_t st);

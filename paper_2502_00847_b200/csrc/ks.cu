@@ -11,34 +11,87 @@ namespace {
 constexpr int TPB = 256;
 constexpr int MAXA = 16;  // max primes per digit / special primes
 
-// grid: x = coefficient chunks, y = ct * beta + j ; one coefficient per thread
-__global__ void modup_kernel(Tab tab, int logn, const u64 *__restrict__ dc, long dcs, u64 *__restrict__ ext,
-                             long exts, int nl, int np, int nq_total, int alpha, int beta,
-                             const u64 *__restrict__ inv_hat, const u64 *__restrict__ inv_hat_sh,
-                             const u64 *__restrict__ hat) {
+// Split-30 multiply-accumulate for base conversion.  Every residue is < 2^60, so writing
+// y = yh 2^30 + yl and c = ch 2^30 + cl (all halves < 2^30) gives four 32x32->64 partial products
+// < 2^60 each; up to 16 of them accumulate in a 64-bit register without overflow (IMAD.WIDE.U32 with
+// a 64-bit addend, one instruction each).  V = s3 2^60 + (s1 + s2) 2^30 + s0 < 2^125 is then reduced
+// once with Barrett.  Constants are stored packed as (ch << 32) | cl.
+struct Acc4 {
+    u64 s0, s1, s2, s3;
+};
+__device__ __forceinline__ void acc4_zero(Acc4 &a) { a.s0 = a.s1 = a.s2 = a.s3 = 0; }
+__device__ __forceinline__ void acc4_mac(Acc4 &a, uint32_t yl, uint32_t yh, u64 cpk) {
+    const uint32_t cl = (uint32_t)cpk, ch = (uint32_t)(cpk >> 32);
+    a.s0 += (u64)yl * cl;
+    a.s1 += (u64)yl * ch;
+    a.s2 += (u64)yh * cl;
+    a.s3 += (u64)yh * ch;
+}
+__device__ __forceinline__ u64 acc4_reduce(const Acc4 &a, u64 q, u64 r0, u64 r1) {
+    const u128 m = (u128)a.s1 + a.s2;
+    const u128 v = ((u128)a.s3 << 60) + (m << 30) + a.s0;
+    return barrett128(U128{(u64)v, (u64)(v >> 64)}, q, r0, r1);
+}
+constexpr uint32_t M30 = (1u << 30) - 1;
+
+__device__ __forceinline__ ulonglong2 ldv2(const u64 *p) { return *reinterpret_cast<const ulonglong2 *>(p); }
+__device__ __forceinline__ void stv2(u64 *p, u64 a, u64 b) { *reinterpret_cast<ulonglong2 *>(p) = make_ulonglong2(a, b); }
+
+// ModUp (R10).  grid: x = coefficient chunks (two coefficients per thread), y = ct * beta + j.
+// The digit's packed constants [Q'_j/q_i]_{t_e} sit in shared memory as sc[e][a] (A words per e).
+template <int A>
+__global__ void __launch_bounds__(TPB) modup_kernel(Tab tab, int logn, const u64 *__restrict__ dc, long dcs,
+                                                    u64 *__restrict__ ext, long exts, int nl, int np, int nq_total,
+                                                    int alpha, int beta, const u64 *__restrict__ inv_hat,
+                                                    const u64 *__restrict__ inv_hat_sh,
+                                                    const u64 *__restrict__ hatpk) {
+    static_assert(A % 2 == 0, "A even (16-byte constant pairs)");
+    __shared__ __align__(16) u64 sc[MAXL * A];
     const int ct = blockIdx.y / beta, j = blockIdx.y % beta;
     const long N = 1L << logn;
-    const long k = (long)blockIdx.x * TPB + threadIdx.x;
     const int i0 = j * alpha, i1 = min(i0 + alpha, nl), na = i1 - i0;
     const int ne = nl + np;
-    u64 y[MAXA];
+    for (int t = threadIdx.x; t < ne * A; t += TPB) {
+        const int e = t / A, a = t % A;
+        sc[t] = a < na ? hatpk[((long)j * MAXA + a) * ne + e] : 0;
+    }
+    const long k = 2L * ((long)blockIdx.x * TPB + threadIdx.x);
+    uint32_t yl[A][2], yh[A][2];
 #pragma unroll
-    for (int a = 0; a < MAXA; a++) {
+    for (int a = 0; a < A; a++) {
         if (a < na) {
             const int i = i0 + a;
-            y[a] = mul_shoup(dc[ct * dcs + i * N + k], inv_hat[i], inv_hat_sh[i], tab.q[i]);
+            const ulonglong2 x = ldv2(dc + ct * dcs + i * N + k);
+            // inv_hat == nullptr: the factor was folded into the INTT (input is already y)
+            const u64 y0 = inv_hat ? mul_shoup(x.x, inv_hat[i], inv_hat_sh[i], tab.q[i]) : x.x;
+            const u64 y1 = inv_hat ? mul_shoup(x.y, inv_hat[i], inv_hat_sh[i], tab.q[i]) : x.y;
+            yl[a][0] = (uint32_t)y0 & M30, yh[a][0] = (uint32_t)(y0 >> 30);
+            yl[a][1] = (uint32_t)y1 & M30, yh[a][1] = (uint32_t)(y1 >> 30);
+        } else {
+            yl[a][0] = yh[a][0] = yl[a][1] = yh[a][1] = 0;
         }
     }
-    const u64 *hj = hat + (long)j * MAXA * ne;  // hat[j][a][e]
+    __syncthreads();
     u64 *out = ext + ct * exts + (long)j * ne * N + k;
     for (int e = 0; e < ne; e++) {
         if (e >= i0 && e < i1) continue;
         const int pr = e < nl ? e : nq_total + (e - nl);
-        U128 acc{0, 0};
+        Acc4 s0, s1;
+        acc4_zero(s0);
+        acc4_zero(s1);
+        const ulonglong2 *cp = reinterpret_cast<const ulonglong2 *>(sc + e * A);
 #pragma unroll
-        for (int a = 0; a < MAXA; a++)
-            if (a < na) mac_wide(acc, y[a], __ldg(hj + a * ne + e));
-        out[e * N] = barrett128(acc, tab.q[pr], tab.br0[pr], tab.br1[pr]);
+        for (int a2 = 0; a2 < A / 2; a2++) {
+            if (2 * a2 < na) {
+                const ulonglong2 c = cp[a2];
+                acc4_mac(s0, yl[2 * a2][0], yh[2 * a2][0], c.x);
+                acc4_mac(s1, yl[2 * a2][1], yh[2 * a2][1], c.x);
+                acc4_mac(s0, yl[2 * a2 + 1][0], yh[2 * a2 + 1][0], c.y);
+                acc4_mac(s1, yl[2 * a2 + 1][1], yh[2 * a2 + 1][1], c.y);
+            }
+        }
+        const u64 q = tab.q[pr], r0 = tab.br0[pr], r1 = tab.br1[pr];
+        stv2(out + e * N, acc4_reduce(s0, q, r0, r1), acc4_reduce(s1, q, r0, r1));
     }
 }
 
@@ -76,89 +129,86 @@ __global__ void ks_inner_kernel(Tab tab, int logn, const u64 *__restrict__ d, lo
     }
 }
 
-// grid: x = coefficient chunks, y = ct * 2 + b
-__global__ void moddown_conv_kernel(Tab tab, int logn, const u64 *__restrict__ acc, long accs, u64 *__restrict__ T,
-                                    long Ts, int nl, int np, int nq_total, const u64 *__restrict__ ihp,
-                                    const u64 *__restrict__ ihp_sh, const u64 *__restrict__ hat_p) {
+// ModDown conversion (R11).  grid: x = coefficient chunks (two per thread), y = ct * 2 + b.
+// Packed constants [P/p]_{q_i} in shared memory as sc[i][p] (NP words per i).
+template <int NP>
+__global__ void __launch_bounds__(TPB) moddown_conv_kernel(Tab tab, int logn, const u64 *__restrict__ acc, long accs,
+                                                           u64 *__restrict__ T, long Ts, int nl, int np,
+                                                           int nq_total, const u64 *__restrict__ ihp,
+                                                           const u64 *__restrict__ ihp_sh,
+                                                           const u64 *__restrict__ hatpk) {
+    static_assert(NP % 2 == 0, "NP even");
+    __shared__ __align__(16) u64 sc[MAXL * NP];
     const int ct = blockIdx.y / 2, b = blockIdx.y % 2;
     const long N = 1L << logn;
-    const long k = (long)blockIdx.x * TPB + threadIdx.x;
     const int ne = nl + np;
+    for (int t = threadIdx.x; t < nl * NP; t += TPB) {
+        const int i = t / NP, p = t % NP;
+        sc[t] = p < np ? hatpk[(long)p * nq_total + i] : 0;
+    }
+    const long k = 2L * ((long)blockIdx.x * TPB + threadIdx.x);
     const u64 *src = acc + ct * accs + ((long)b * ne + nl) * N + k;
-    u64 y[MAXA];
+    uint32_t yl[NP][2], yh[NP][2];
 #pragma unroll
-    for (int p = 0; p < MAXA; p++)
+    for (int p = 0; p < NP; p++) {
         if (p < np) {
             const int pr = nq_total + p;
-            y[p] = mul_shoup(src[p * N], ihp[p], ihp_sh[p], tab.q[pr]);
+            const ulonglong2 x = ldv2(src + p * N);
+            // ihp == nullptr: the factor was folded into the INTT (input is already y)
+            const u64 y0 = ihp ? mul_shoup(x.x, ihp[p], ihp_sh[p], tab.q[pr]) : x.x;
+            const u64 y1 = ihp ? mul_shoup(x.y, ihp[p], ihp_sh[p], tab.q[pr]) : x.y;
+            yl[p][0] = (uint32_t)y0 & M30, yh[p][0] = (uint32_t)(y0 >> 30);
+            yl[p][1] = (uint32_t)y1 & M30, yh[p][1] = (uint32_t)(y1 >> 30);
+        } else {
+            yl[p][0] = yh[p][0] = yl[p][1] = yh[p][1] = 0;
         }
+    }
+    __syncthreads();
     u64 *dst = T + ct * Ts + (long)b * nl * N + k;
     for (int i = 0; i < nl; i++) {
-        U128 s{0, 0};
+        Acc4 s0, s1;
+        acc4_zero(s0);
+        acc4_zero(s1);
+        const ulonglong2 *cp = reinterpret_cast<const ulonglong2 *>(sc + i * NP);
 #pragma unroll
-        for (int p = 0; p < MAXA; p++)
-            if (p < np) mac_wide(s, y[p], __ldg(hat_p + (long)p * nq_total + i));
-        dst[i * N] = barrett128(s, tab.q[i], tab.br0[i], tab.br1[i]);
+        for (int p2 = 0; p2 < NP / 2; p2++) {
+            if (2 * p2 < np) {
+                const ulonglong2 c = cp[p2];
+                acc4_mac(s0, yl[2 * p2][0], yh[2 * p2][0], c.x);
+                acc4_mac(s1, yl[2 * p2][1], yh[2 * p2][1], c.x);
+                acc4_mac(s0, yl[2 * p2 + 1][0], yh[2 * p2 + 1][0], c.y);
+                acc4_mac(s1, yl[2 * p2 + 1][1], yh[2 * p2 + 1][1], c.y);
+            }
+        }
+        stv2(dst + i * N, acc4_reduce(s0, tab.q[i], tab.br0[i], tab.br1[i]),
+             acc4_reduce(s1, tab.q[i], tab.br0[i], tab.br1[i]));
     }
 }
 
-// grid: x = coefficient chunks, y = (ct * 2 + b) * nl + i
-__global__ void moddown_combine_kernel(Tab tab, int logn, const u64 *__restrict__ acc, long accs,
-                                       const u64 *__restrict__ T, long Ts, const u64 *__restrict__ add, long adds,
-                                       int add_polys, u64 *__restrict__ out, long outs, int nl, int ne,
-                                       const u64 *__restrict__ pinv, const u64 *__restrict__ pinv_sh) {
-    const int row = blockIdx.y;
-    const int i = row % nl, b = (row / nl) % 2, ct = row / (2 * nl);
-    const long N = 1L << logn;
-    const long k = (long)blockIdx.x * TPB + threadIdx.x;
-    const u64 q = tab.q[i];
-    const u64 a = acc[ct * accs + ((long)b * ne + i) * N + k];
-    const u64 t = T[ct * Ts + ((long)b * nl + i) * N + k];
-    u64 v = mul_shoup(submod(a, t, q), pinv[i], pinv_sh[i], q);
-    if (b < add_polys) v = addmod(v, add[ct * adds + ((long)b * nl + i) * N + k], q);
-    out[ct * outs + ((long)b * nl + i) * N + k] = v;
-}
-
-// rescale, step 1 (coefficient domain): T[c][b][i] = [floor(q_l/2)]_{q_i} - [r]_{q_i} mod q_i with
-// r = [c_l + floor(q_l/2)]_{q_l} per coefficient (the half is added to every coefficient).
-// grid: y = (ct * 2 + b) * l + i
-__global__ void rescale_bcast_kernel(Tab tab, int logn, const u64 *__restrict__ last, long lasts,
-                                     u64 *__restrict__ T, long Ts, int l, const u64 *__restrict__ half) {
-    const int row = blockIdx.y;
-    const int i = row % l, b = (row / l) % 2, ct = row / (2 * l);
-    const long N = 1L << logn;
-    const long k = (long)blockIdx.x * TPB + threadIdx.x;
-    const u64 ql = tab.q[l];
-    const u64 r = csub(last[ct * lasts + (long)b * N + k] + (ql >> 1), ql);
-    const u64 qi = tab.q[i];
-    T[ct * Ts + ((long)b * l + i) * N + k] = submod(half[i], barrett128(U128{r, 0}, qi, tab.br0[i], tab.br1[i]), qi);
-}
-
-// rescale, step 2 (NTT domain): out = (in + NTT(T)) * q_l^{-1}
-__global__ void rescale_combine_kernel(Tab tab, int logn, CRows in,
-                                       const u64 *__restrict__ T, long Ts, u64 *__restrict__ out, long outs, int l,
-                                       const u64 *__restrict__ qlinv,
-                                       const u64 *__restrict__ qlinv_sh) {
-    const int row = blockIdx.y;
-    const int i = row % l, b = (row / l) % 2, ct = row / (2 * l);
-    const long N = 1L << logn;
-    const long k = (long)blockIdx.x * TPB + threadIdx.x;
-    const u64 q = tab.q[i];
-    const u64 x = in.p[poly_off(in.cs, in.ps, 2 * ct + b) + (long)i * N + k];
-    const u64 t = T[ct * Ts + ((long)b * l + i) * N + k];
-    const u64 v = addmod(x, t, q);
-    out[ct * outs + ((long)b * l + i) * N + k] = mul_shoup(v, qlinv[i], qlinv_sh[i], q);
-}
 }  // namespace
 
 static inline unsigned chunks(int logn) { return (unsigned)((1L << logn) / TPB); }
+static inline unsigned chunks2(int logn) { return (unsigned)((1L << logn) / (2 * TPB)); }
 
 void k_modup(const Tab &tab, int logn, const u64 *dc, long dcs, u64 *ext, long exts, int n_ct, int nl, int np,
              int nq_total, int alpha, const u64 *inv_hat, const u64 *inv_hat_sh, const u64 *hat, cudaStream_t st) {
     const int beta = (nl + alpha - 1) / alpha;
     if (alpha > MAXA) throw SecpeError{-1, "alpha > 16 not supported"};
-    modup_kernel<<<dim3(chunks(logn), n_ct * beta), TPB, 0, st>>>(tab, logn, dc, dcs, ext, exts, nl, np, nq_total,
-                                                                   alpha, beta, inv_hat, inv_hat_sh, hat);
+    const dim3 grid(chunks2(logn), n_ct * beta);
+#define MODUP(A_)                                                                                          \
+    modup_kernel<A_><<<grid, TPB, 0, st>>>(tab, logn, dc, dcs, ext, exts, nl, np, nq_total, alpha, beta, inv_hat, \
+                                           inv_hat_sh, hat)
+    if (alpha <= 2)
+        MODUP(2);
+    else if (alpha <= 4)
+        MODUP(4);
+    else if (alpha <= 8)
+        MODUP(8);
+    else if (alpha <= 10)
+        MODUP(10);
+    else
+        MODUP(16);
+#undef MODUP
     LAUNCH_CHECK();
 }
 void k_ks_inner(const Tab &tab, int logn, const u64 *d, long ds, const u64 *ext, long exts, const u64 *key,
@@ -186,26 +236,17 @@ void k_ks_inner(const Tab &tab, int logn, const u64 *d, long ds, const u64 *ext,
 void k_moddown_conv(const Tab &tab, int logn, const u64 *acc, long accs, u64 *T, long Ts, int n_ct, int nl, int np,
                     int nq_total, const u64 *ihp, const u64 *ihp_sh, const u64 *hat_p, cudaStream_t st) {
     if (np > MAXA) throw SecpeError{-1, "more than 16 special primes not supported"};
-    moddown_conv_kernel<<<dim3(chunks(logn), n_ct * 2), TPB, 0, st>>>(tab, logn, acc, accs, T, Ts, nl, np, nq_total,
-                                                                       ihp, ihp_sh, hat_p);
-    LAUNCH_CHECK();
-}
-void k_moddown_combine(const Tab &tab, int logn, const u64 *acc, long accs, const u64 *T, long Ts, const u64 *add,
-                       long adds, int add_polys, u64 *out, long outs, int n_ct, int nl, int ne, const u64 *pinv,
-                       const u64 *pinv_sh, cudaStream_t st) {
-    moddown_combine_kernel<<<dim3(chunks(logn), n_ct * 2 * nl), TPB, 0, st>>>(tab, logn, acc, accs, T, Ts, add, adds,
-                                                                               add_polys, out, outs, nl, ne, pinv,
-                                                                               pinv_sh);
-    LAUNCH_CHECK();
-}
-void k_rescale_bcast(const Tab &tab, int logn, const u64 *last, long lasts, u64 *T, long Ts, int n_ct, int l,
-                     const u64 *half, cudaStream_t st) {
-    rescale_bcast_kernel<<<dim3(chunks(logn), n_ct * 2 * l), TPB, 0, st>>>(tab, logn, last, lasts, T, Ts, l, half);
-    LAUNCH_CHECK();
-}
-void k_rescale_combine(const Tab &tab, int logn, CRows in, const u64 *T, long Ts, u64 *out, long outs,
-                       int n_ct, int l, const u64 *qlinv, const u64 *qlinv_sh, cudaStream_t st) {
-    rescale_combine_kernel<<<dim3(chunks(logn), n_ct * 2 * l), TPB, 0, st>>>(tab, logn, in, T, Ts, out, outs, l,
-                                                                              qlinv, qlinv_sh);
+    const dim3 grid(chunks2(logn), n_ct * 2);
+#define MDC(P_)                                                                                                  \
+    moddown_conv_kernel<P_><<<grid, TPB, 0, st>>>(tab, logn, acc, accs, T, Ts, nl, np, nq_total, ihp, ihp_sh, hat_p)
+    if (np <= 2)
+        MDC(2);
+    else if (np <= 4)
+        MDC(4);
+    else if (np <= 8)
+        MDC(8);
+    else
+        MDC(16);
+#undef MDC
     LAUNCH_CHECK();
 }

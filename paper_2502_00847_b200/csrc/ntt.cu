@@ -3,25 +3,40 @@
 // Definition (R4): NTT(a)[i] = sum_k a_k psi^{(2 brv(i)+1) k} mod q, computed with the
 // merged Cooley-Tukey network (twiddle psi^{brv(m+i)} at stage m) and its Gentleman-Sande inverse.
 //
-// Decomposition: N = 2^logN = G1 * G2 (G = 2^S).  Each transform is two passes over HBM:
-//   forward : pass 1 = the first S1 stages on "columns" {c + (N/G1) r}  (strided groups)
-//             pass 2 = the last  S2 stages on contiguous blocks of G2
-//   inverse : pass A = the first S2 GS stages on contiguous blocks, pass B = the last S1 on columns
-// Within a pass a group of G elements is held by G/8 threads, 8 values per thread (radix-8 register
-// rounds of up to three butterfly stages), exchanging through shared memory between rounds.
-// Strided passes put 16 consecutive columns in one CTA so every global access is a full 128-byte
-// line; contiguous passes stage their loads/stores through shared memory with 16-byte vectors.
-// Arithmetic: Harvey lazy butterflies with Shoup twiddles; forward values stay in [0, 4q),
-// inverse in [0, 2q); the last pass reduces to [0, q) (and the inverse folds in N^{-1}).
+// Decomposition: N = 2^LOGN = G1 * G2 (G = 2^S, S1 = LOGN/2, S2 = LOGN - S1).  Two passes over a limb:
+//   forward : pass 1 = stages 0..S1-1 on "columns" {c + (N/G1) r}   (strided groups)
+//             pass 2 = stages S1..LOGN-1 on contiguous blocks of G2
+//   inverse : pass A = GS stages LOGN-1..S1 on contiguous blocks, pass B = stages S1-1..0 on columns
+// Radix-16 register rounds: a group of G elements is held by G/16 threads, 16 values each, so one
+// round runs four butterfly stages on registers (LOGN = 16: two rounds per pass, one shared-memory
+// exchange).  A round needs 1 + 2 + 4 + 8 = 15 distinct twiddles per thread, loaded once each as a
+// 16-byte {w, w'} pair (interleaved Shoup table).
+// Global access: strided passes put 16 consecutive columns in one CTA, so every load/store
+// instruction of a half-warp covers one full 128-byte line; contiguous passes read (forward) or
+// write (inverse) straight from registers in a lane-consecutive layout and stage the other side
+// through padded shared memory with 16-byte vectors.
+// Arithmetic: Harvey lazy butterflies with Shoup twiddles (all primes < 2^60); forward values stay
+// below 8q with a correction on every other stage only (bfly_ct), inverse in [0, 2q); the last pass
+// reduces to [0, q) (the inverse folds in N^{-1}).  Forward input may be any value < 4q.
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace {
 
-constexpr int STRIDED_C = 16;  // columns per CTA in strided passes (16 x 8 B = one 128-B line)
+constexpr int RB = 4;        // bits held per thread
+constexpr int NV = 1 << RB;  // values per thread
+constexpr int SC = 16;       // columns per CTA in strided passes (16 x 8 B = one 128-B line)
+constexpr int CT = 256;      // threads per CTA in contiguous passes
 
+// Forward CT butterfly, lazy every other stage: T = y w in [0, 2q); x' = X + T, y' = X - T + 2q.
+// Uncorrected stages (even global stage) take inputs < 6q (outputs < 8q); corrected stages (odd)
+// take inputs < 8q, fold X = x >= 4q ? x - 4q : x < 4q, outputs < 6q.  8q < 2^64 (q < 2^60).
+template <bool CORR>
 __device__ __forceinline__ void bfly_ct(u64 &x, u64 &y, u64 w, u64 wsh, u64 q, u64 q2) {
-    u64 X = x >= q2 ? x - q2 : x;
+    u64 X = x;
+    if (CORR) X = X >= 2 * q2 ? X - 2 * q2 : X;
     u64 T = mul_shoup_lazy(y, w, wsh, q);
     x = X + T;
     y = X - T + q2;
@@ -33,278 +48,341 @@ __device__ __forceinline__ void bfly_gs(u64 &x, u64 &y, u64 w, u64 wsh, u64 q, u
     y = mul_shoup_lazy(X - Y + q2, w, wsh, q);
 }
 
-// index of value v (3 bits) held by thread tau when the held bits start at LO
+// local index of held value v of thread tau when the held bits start at LO
 template <int LO>
-__device__ __forceinline__ int held_index(int tau, int v) {
-    return ((tau >> LO) << (LO + 3)) | (v << LO) | (tau & ((1 << LO) - 1));
+__device__ __forceinline__ int held(int tau, int v) {
+    return ((tau >> LO) << (LO + RB)) | (v << LO) | (tau & ((1 << LO) - 1));
 }
 
-// Rounds: forward round k pairs local bits hi = S-1-3k, hi-1, hi-2 (clipped at 0),
-// holding bits LO = max(hi-2, 0).  Inverse round k pairs bits lo = 3k .. min(lo+2, S-1),
-// holding LO = min(lo, S-3).
+// Round k of a pass of S stages.  Forward rounds pair local bits hi = S-1-4k downwards, inverse
+// rounds pair lo = 4k upwards; the held window [LO, LO+4) is clipped into [0, S).
 template <int S, bool INV>
-struct RoundInfo {
-    static constexpr int NR = (S + 2) / 3;
-    __host__ __device__ static constexpr int first_bit(int k) { return INV ? 3 * k : S - 1 - 3 * k; }
-    __host__ __device__ static constexpr int nbits(int k) {
-        return INV ? ((3 * k + 2 <= S - 1) ? 3 : S - 3 * k) : ((S - 1 - 3 * k - 2 >= 0) ? 3 : S - 3 * k);
+struct Rnd {
+    static constexpr int NR = (S + RB - 1) / RB;
+    __host__ __device__ static constexpr int first(int k) { return INV ? RB * k : S - 1 - RB * k; }
+    __host__ __device__ static constexpr int nb(int k) {
+        return INV ? (S - RB * k < RB ? S - RB * k : RB) : (S - RB * k < RB ? S - RB * k : RB);
     }
     __host__ __device__ static constexpr int lo(int k) {
-        return INV ? ((3 * k < S - 3) ? 3 * k : S - 3) : ((S - 1 - 3 * k - 2 > 0) ? S - 1 - 3 * k - 2 : 0);
+        return INV ? (RB * k < S - RB ? RB * k : S - RB) : (S - 1 - RB * k - (RB - 1) > 0 ? S - RB * k - RB : 0);
     }
 };
 
-// One round of butterflies on the 8 values held by this thread.
-// gidx(r) maps a local index to the global index within the limb.
-template <int S, bool INV, int K, typename GIdx>
-__device__ __forceinline__ void do_round(u64 (&v)[8], int tau, GIdx gidx, int logn, int sg0,
-                                         const u64 *__restrict__ tw, const u64 *__restrict__ twsh,
-                                         u64 q, u64 q2) {
-    using R = RoundInfo<S, INV>;
+// One round of butterflies on the 16 held values.  Twiddle of the pair whose lower element has
+// local index r, paired bit b: tw[2^sg + (g << (S-1-b)) + (r >> (b+1))] where sg is the global
+// stage (strided: S-1-b, g = 0; contiguous: LOGN-1-b, g = group).  It depends only on the held bits
+// above the paired one, so each distinct twiddle is loaded once.
+template <int S, bool INV, int K, bool CONTIG, int LOGN>
+__device__ __forceinline__ void do_round(u64 (&v)[NV], int tau, int g, const ulonglong2 *__restrict__ tw, u64 q,
+                                         u64 q2) {
+    using R = Rnd<S, INV>;
     constexpr int LO = R::lo(K);
-    constexpr int NB = R::nbits(K);
 #pragma unroll
-    for (int st = 0; st < NB; st++) {
-        const int b = INV ? R::first_bit(K) + st : R::first_bit(K) - st;  // local bit paired
+    for (int st = 0; st < R::nb(K); st++) {
+        const int b = INV ? R::first(K) + st : R::first(K) - st;
         const int vb = b - LO;
-        const int s_local = INV ? b : (S - 1 - b);
-        const int sg = INV ? sg0 - s_local : sg0 + s_local;  // global stage
-        const int shift = logn - sg;
+        const int sg = CONTIG ? LOGN - 1 - b : S - 1 - b;
+        const int gterm = CONTIG ? (g << (S - 1 - b)) : 0;
 #pragma unroll
-        for (int p = 0; p < 4; p++) {
-            // p enumerates the 4 pairs: insert a 0 bit at position vb
-            const int v0 = ((p >> vb) << (vb + 1)) | (p & ((1 << vb) - 1));
-            const int v1 = v0 | (1 << vb);
-            const int r0 = held_index<LO>(tau, v0);
-            const int j0 = gidx(r0);
-            const int ti = (1 << sg) + (j0 >> shift);
-            const u64 w = __ldg(tw + ti), wsh = __ldg(twsh + ti);
-            if (INV)
-                bfly_gs(v[v0], v[v1], w, wsh, q, q2);
-            else
-                bfly_ct(v[v0], v[v1], w, wsh, q, q2);
+        for (int u = 0; u < (1 << (RB - 1 - vb)); u++) {
+            const int v0b = u << (vb + 1);
+            const int r = held<LO>(tau, v0b);
+            const ulonglong2 w = __ldg(tw + ((1 << sg) + gterm + (r >> (b + 1))));
+#pragma unroll
+            for (int l = 0; l < (1 << vb); l++) {
+                const int i0 = v0b | l, i1 = i0 | (1 << vb);
+                if (INV)
+                    bfly_gs(v[i0], v[i1], w.x, w.y, q, q2);
+                else if (sg & 1)
+                    bfly_ct<true>(v[i0], v[i1], w.x, w.y, q, q2);
+                else
+                    bfly_ct<false>(v[i0], v[i1], w.x, w.y, q, q2);
+            }
         }
     }
 }
 
-template <int LO, typename Phys>
-__device__ __forceinline__ void smem_store(u64 *sm, const u64 (&v)[8], int tau, Phys phys) {
-#pragma unroll
-    for (int k = 0; k < 8; k++) sm[phys(held_index<LO>(tau, k))] = v[k];
-}
-template <int LO, typename Phys>
-__device__ __forceinline__ void smem_load(const u64 *sm, u64 (&v)[8], int tau, Phys phys) {
-#pragma unroll
-    for (int k = 0; k < 8; k++) v[k] = sm[phys(held_index<LO>(tau, k))];
-}
+// Fused prologue / epilogue modes (NttFusion in kernels.h)
+enum { IN_PLAIN = 0, IN_SRC = 1, IN_BCAST = 2 };
+enum { OUT_PLAIN = 0, OUT_RESCALE = 1, OUT_MODDOWN = 2 };
 
 struct PassArgs {
-    u64 *data;
-    long cs, ps;  // polynomial addressing (see RowsArg)
+    RowsArg d;  // transform buffer rows (row = poly * nl + limb)
     LimbMap lm;
     Tab tab;
-    int logn;
-    int sg0;     // global stage of local stage 0
-    int final_;  // last pass of the transform: reduce to [0, q) (inverse: also * N^{-1})
+    NttFusion f;
 };
 
 // ---------------------------------------------------------------------------------------------
-// strided pass: group = column c, elements c + stride * r, 16 columns per CTA
+// strided pass: group = column c, elements c + (N >> S) r, SC columns per CTA
+//   forward: stages 0..S-1 (first pass);  inverse: stages S-1..0 (last pass, * N^{-1})
 // ---------------------------------------------------------------------------------------------
-template <int S, bool INV>
-__global__ void __launch_bounds__(STRIDED_C *(1 << S) / 8)
+template <int LOGN, bool INV, int IN, int MINB>
+__global__ void __launch_bounds__(SC *(1 << (LOGN / 2 - RB)), MINB)
     ntt_strided(PassArgs a) {
-    constexpr int G = 1 << S, C = STRIDED_C;
-    __shared__ u64 sm[G * C];
+    constexpr int S = LOGN / 2, G = 1 << S;
+    constexpr long N = 1L << LOGN;
+    constexpr int STRIDE = (int)(N >> S);
+    using R = Rnd<S, INV>;
+    __shared__ u64 sm[G * SC];
     const int nl = a.lm.nl;
     const int poly = blockIdx.y / nl, limb = blockIdx.y % nl;
     const int prime = prime_of(a.lm, limb);
-    const long N = 1L << a.logn;
-    u64 *base = a.data + poly_off(a.cs, a.ps, poly) + limb * N;
+    const int cl = threadIdx.x % SC, tau = threadIdx.x / SC;
+    const int c = blockIdx.x * SC + cl;
+    u64 *base = a.d.p + poly_off(a.d.cs, a.d.ps, poly) + limb * N + c;
     const u64 q = a.tab.q[prime], q2 = 2 * q;
-    const u64 *tw = (INV ? a.tab.itw : a.tab.tw) + prime * N;
-    const u64 *twsh = (INV ? a.tab.itwsh : a.tab.twsh) + prime * N;
-    const int cl = threadIdx.x % C, tau = threadIdx.x / C;
-    const int c = blockIdx.x * C + cl;
-    const int stride = (int)(N >> S);
-    auto gidx = [&](int r) { return c + stride * r; };
-    auto phys = [&](int r) { return r * C + cl; };
-    using R = RoundInfo<S, INV>;
-    u64 v[8];
+    const ulonglong2 *tw = (INV ? a.tab.itw2 : a.tab.tw2) + prime * N;
+    u64 v[NV];
     constexpr int LO0 = R::lo(0);
+    if constexpr (IN == IN_BCAST) {
+        // rescale (R12): T_i = [floor(q_l/2)]_{q_i} - [r]_{q_i}, r = [c_l + floor(q_l/2)]_{q_l};
+        // the source row is the coefficient-form last limb of the same polynomial
+        const u64 *src = a.f.src.p + poly_off(a.f.src.cs, a.f.src.ps, poly) + c;
+        const u64 ql = a.tab.q[a.f.lp], hl = ql >> 1, hi = a.f.half[limb], one_sh = a.tab.br1[prime];
 #pragma unroll
-    for (int k = 0; k < 8; k++) v[k] = base[gidx(held_index<LO0>(tau, k))];
-    do_round<S, INV, 0>(v, tau, gidx, a.logn, a.sg0, tw, twsh, q, q2);
-    if constexpr (R::NR > 1) {
-        smem_store<R::lo(0)>(sm, v, tau, phys);
-        __syncthreads();
-        smem_load<R::lo(1)>(sm, v, tau, phys);
-        do_round<S, INV, 1>(v, tau, gidx, a.logn, a.sg0, tw, twsh, q, q2);
-    }
-    if constexpr (R::NR > 2) {
-        __syncthreads();
-        smem_store<R::lo(1)>(sm, v, tau, phys);
-        __syncthreads();
-        smem_load<R::lo(2)>(sm, v, tau, phys);
-        do_round<S, INV, 2>(v, tau, gidx, a.logn, a.sg0, tw, twsh, q, q2);
-    }
-    constexpr int LOL = R::lo(R::NR - 1);
-    if (a.final_) {
-        if (INV) {
-            const u64 ni = a.tab.ninv[prime], nish = a.tab.ninvsh[prime];
-#pragma unroll
-            for (int k = 0; k < 8; k++) v[k] = mul_shoup(v[k], ni, nish, q);
-        } else {
-#pragma unroll
-            for (int k = 0; k < 8; k++) v[k] = csub(csub(v[k], q2), q);
+        for (int k = 0; k < NV; k++) {
+            const u64 r = csub(src[STRIDE * held<LO0>(tau, k)] + hl, ql);
+            v[k] = submod(hi, mul_shoup(r, 1, one_sh, q), q);
         }
+    } else {
+#pragma unroll
+        for (int k = 0; k < NV; k++) v[k] = base[STRIDE * held<LO0>(tau, k)];
+    }
+    do_round<S, INV, 0, false, LOGN>(v, tau, 0, tw, q, q2);
+    if constexpr (R::NR > 1) {
+#pragma unroll
+        for (int k = 0; k < NV; k++) sm[held<R::lo(0)>(tau, k) * SC + cl] = v[k];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < NV; k++) v[k] = sm[held<R::lo(1)>(tau, k) * SC + cl];
+        do_round<S, INV, 1, false, LOGN>(v, tau, 0, tw, q, q2);
+    }
+    static_assert(R::NR <= 2, "strided pass: at most two rounds");
+    constexpr int LOL = R::lo(R::NR - 1);
+    if (INV) {
+        // last inverse pass: * N^{-1} (or a caller-supplied per-limb factor that includes it)
+        const u64 ni = a.f.k ? a.f.k[limb] : a.tab.ninv[prime];
+        const u64 nish = a.f.k ? a.f.ksh[limb] : a.tab.ninvsh[prime];
+#pragma unroll
+        for (int k = 0; k < NV; k++) v[k] = mul_shoup(v[k], ni, nish, q);
     }
 #pragma unroll
-    for (int k = 0; k < 8; k++) base[gidx(held_index<LOL>(tau, k))] = v[k];
+    for (int k = 0; k < NV; k++) base[STRIDE * held<LOL>(tau, k)] = v[k];
 }
 
 // ---------------------------------------------------------------------------------------------
-// contiguous pass: group = block of G consecutive elements, CG groups per CTA
+// contiguous pass: group = block of G consecutive elements, CT / (G/16) groups per CTA
+//   forward: stages S1..LOGN-1 (last pass, reduce to [0, q));  inverse: stages LOGN-1..S1 (first)
 // ---------------------------------------------------------------------------------------------
-template <int S>
+template <int LOGN>
 struct ContigCfg {
+    static constexpr int S = LOGN - LOGN / 2;
     static constexpr int G = 1 << S;
-    static constexpr int TPG = G / 8;
-    static constexpr int CG = (256 / TPG) > 0 ? 256 / TPG : 1;  // 256 threads per CTA
-    static constexpr int PITCH = G + G / 8;                     // padded group pitch in smem
+    static constexpr int TPG = G / NV;
+    static constexpr int CG = CT / TPG;
+    static constexpr int PITCH = G + G / 16;  // one pad word per 16: conflict-free both layouts
 };
+__device__ __forceinline__ int padr(int r) { return r + (r >> 4); }
 
-template <int S, bool INV>
-__global__ void __launch_bounds__(256) ntt_contig(PassArgs a) {
-    using CF = ContigCfg<S>;
-    constexpr int G = CF::G, TPG = CF::TPG, CG = CF::CG, PITCH = CF::PITCH;
+template <int LOGN, bool INV, int IO, int MINB>
+__global__ void __launch_bounds__(CT, MINB) ntt_contig(PassArgs a) {
+    // IO: inverse -> IN_PLAIN | IN_SRC (first pass reads f.src rows);  forward -> OUT_* epilogue
+    using CF = ContigCfg<LOGN>;
+    constexpr int S = CF::S, G = CF::G, TPG = CF::TPG, CG = CF::CG, PITCH = CF::PITCH;
+    constexpr long N = 1L << LOGN;
+    using R = Rnd<S, INV>;
+    static_assert(R::NR == 2, "contiguous pass: two rounds");
     __shared__ __align__(16) u64 sm[CG * PITCH];
     const int nl = a.lm.nl;
     const int poly = blockIdx.y / nl, limb = blockIdx.y % nl;
     const int prime = prime_of(a.lm, limb);
-    const long N = 1L << a.logn;
-    u64 *base = a.data + poly_off(a.cs, a.ps, poly) + limb * N + (long)blockIdx.x * CG * G;
+    const long boff = limb * N + (long)blockIdx.x * CG * G;  // tile offset inside the polynomial
+    u64 *blk = a.d.p + poly_off(a.d.cs, a.d.ps, poly) + boff;
     const u64 q = a.tab.q[prime], q2 = 2 * q;
-    const u64 *tw = (INV ? a.tab.itw : a.tab.tw) + prime * N;
-    const u64 *twsh = (INV ? a.tab.itwsh : a.tab.twsh) + prime * N;
+    const ulonglong2 *tw = (INV ? a.tab.itw2 : a.tab.tw2) + prime * N;
     const int gl = threadIdx.x / TPG, tau = threadIdx.x % TPG;
     const int g = blockIdx.x * CG + gl;
-    auto gidx = [&](int r) { return g * G + r; };
     u64 *smg = sm + gl * PITCH;
-    auto phys = [&](int r) { return r + (r >> 3); };
-    // coalesced load of CG*G elements (16-byte vectors) into padded smem
-    {
-        const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(base);
-        for (int i = threadIdx.x; i < CG * G / 2; i += 256) {
-            ulonglong2 x = src[i];
-            const int e = 2 * i, gg = e / G, r = e % G;
-            sm[gg * PITCH + phys(r)] = x.x;
-            sm[gg * PITCH + phys(r + 1)] = x.y;
-        }
-    }
-    __syncthreads();
-    using R = RoundInfo<S, INV>;
-    u64 v[8];
-    smem_load<R::lo(0)>(smg, v, tau, phys);
-    do_round<S, INV, 0>(v, tau, gidx, a.logn, a.sg0, tw, twsh, q, q2);
-    if constexpr (R::NR > 1) {
-        __syncthreads();
-        smem_store<R::lo(0)>(smg, v, tau, phys);
-        __syncthreads();
-        smem_load<R::lo(1)>(smg, v, tau, phys);
-        do_round<S, INV, 1>(v, tau, gidx, a.logn, a.sg0, tw, twsh, q, q2);
-    }
-    if constexpr (R::NR > 2) {
-        __syncthreads();
-        smem_store<R::lo(1)>(smg, v, tau, phys);
-        __syncthreads();
-        smem_load<R::lo(2)>(smg, v, tau, phys);
-        do_round<S, INV, 2>(v, tau, gidx, a.logn, a.sg0, tw, twsh, q, q2);
-    }
-    if (a.final_) {
-        if (INV) {
-            const u64 ni = a.tab.ninv[prime], nish = a.tab.ninvsh[prime];
+    u64 v[NV];
+    constexpr int LO0 = R::lo(0), LO1 = R::lo(1);
+    if (!INV) {
+        // forward round 0 holds r = 16 k + tau: lane-consecutive, load straight from global
+        const u64 *src = blk + gl * G;
 #pragma unroll
-            for (int k = 0; k < 8; k++) v[k] = mul_shoup(v[k], ni, nish, q);
+        for (int k = 0; k < NV; k++) v[k] = src[held<LO0>(tau, k)];
+    } else {
+        const u64 *sp = (IO == IN_SRC) ? a.f.src.p + poly_off(a.f.src.cs, a.f.src.ps, poly) + boff : blk;
+        const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(sp);
+#pragma unroll 4
+        for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
+            const ulonglong2 x = src[i];
+            const int e = 2 * i, gg = e / G, r = e % G;
+            sm[gg * PITCH + padr(r)] = x.x;
+            sm[gg * PITCH + padr(r + 1)] = x.y;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < NV; k++) v[k] = smg[padr(held<LO0>(tau, k))];
+        // no barrier: each thread rewrites exactly the words it just read (same layout)
+    }
+    do_round<S, INV, 0, true, LOGN>(v, tau, g, tw, q, q2);
+#pragma unroll
+    for (int k = 0; k < NV; k++) smg[padr(held<LO0>(tau, k))] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NV; k++) v[k] = smg[padr(held<LO1>(tau, k))];
+    do_round<S, INV, 1, true, LOGN>(v, tau, g, tw, q, q2);
+    if (!INV) {
+#pragma unroll
+        for (int k = 0; k < NV; k++) v[k] = csub(csub(csub(v[k], 2 * q2), q2), q);  // < 6q -> [0, q)
+        // no barrier: each thread rewrites exactly the words it read for round 1
+#pragma unroll
+        for (int k = 0; k < NV; k++) smg[padr(held<LO1>(tau, k))] = v[k];
+        __syncthreads();
+        // epilogue on 16-byte vectors; element e of the tile is at boff + e in its polynomial
+        const ulonglong2 *e1 = nullptr, *e2 = nullptr;
+        ulonglong2 *dst;
+        u64 kc = 0, kcsh = 0;
+        if (IO == OUT_PLAIN) {
+            dst = reinterpret_cast<ulonglong2 *>(blk);
         } else {
-#pragma unroll
-            for (int k = 0; k < 8; k++) v[k] = csub(csub(v[k], q2), q);
+            const int P = poly;
+            e1 = reinterpret_cast<const ulonglong2 *>(a.f.e1.p + poly_off(a.f.e1.cs, a.f.e1.ps, P) + boff);
+            if (IO == OUT_MODDOWN && (P & 1) < a.f.e2_polys)
+                e2 = reinterpret_cast<const ulonglong2 *>(a.f.e2.p + poly_off(a.f.e2.cs, a.f.e2.ps, P) + boff);
+            dst = reinterpret_cast<ulonglong2 *>(a.f.out.p + poly_off(a.f.out.cs, a.f.out.ps, P) + boff);
+            kc = a.f.k[limb];
+            kcsh = a.f.ksh[limb];
         }
-    }
-    __syncthreads();
-    smem_store<R::lo(R::NR - 1)>(smg, v, tau, phys);
-    __syncthreads();
-    {
-        ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(base);
-        for (int i = threadIdx.x; i < CG * G / 2; i += 256) {
+#pragma unroll 4
+        for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
             const int e = 2 * i, gg = e / G, r = e % G;
-            dst[i] = make_ulonglong2(sm[gg * PITCH + phys(r)], sm[gg * PITCH + phys(r + 1)]);
+            u64 x0 = sm[gg * PITCH + padr(r)], x1 = sm[gg * PITCH + padr(r + 1)];
+            if (IO == OUT_RESCALE) {
+                // (c_i + NTT(T)_i) * q_l^{-1}
+                const ulonglong2 c = e1[i];
+                x0 = mul_shoup(addmod(c.x, x0, q), kc, kcsh, q);
+                x1 = mul_shoup(addmod(c.y, x1, q), kc, kcsh, q);
+            } else if (IO == OUT_MODDOWN) {
+                // (acc_i - NTT(T)_i) * P^{-1} (+ addend)
+                const ulonglong2 c = e1[i];
+                x0 = mul_shoup(submod(c.x, x0, q), kc, kcsh, q);
+                x1 = mul_shoup(submod(c.y, x1, q), kc, kcsh, q);
+                if (e2) {
+                    const ulonglong2 d = e2[i];
+                    x0 = addmod(x0, d.x, q);
+                    x1 = addmod(x1, d.y, q);
+                }
+            }
+            dst[i] = make_ulonglong2(x0, x1);
         }
+    } else {
+        // inverse round 1 holds r = 16 k + tau (LO = S - 4): store straight to global
+        u64 *dst = blk + gl * G;
+#pragma unroll
+        for (int k = 0; k < NV; k++) dst[held<LO1>(tau, k)] = v[k];
     }
 }
 
-template <int S, bool INV>
-void launch_strided(const PassArgs &a, int n_rows, cudaStream_t st) {
-    const long N = 1L << a.logn;
-    const int ncols = (int)(N >> S);
-    dim3 grid(ncols / STRIDED_C, n_rows);
-    ntt_strided<S, INV><<<grid, STRIDED_C * (1 << S) / 8, 0, st>>>(a);
-}
-template <int S, bool INV>
-void launch_contig(const PassArgs &a, int n_rows, cudaStream_t st) {
-    const long N = 1L << a.logn;
-    const int nblocks = (int)(N >> S);
-    dim3 grid(nblocks / ContigCfg<S>::CG, n_rows);
-    ntt_contig<S, INV><<<grid, 256, 0, st>>>(a);
-}
-
-template <bool INV>
-void dispatch_strided(int S, const PassArgs &a, int rows, cudaStream_t st) {
-    switch (S) {
-        case 5: launch_strided<5, INV>(a, rows, st); break;
-        case 6: launch_strided<6, INV>(a, rows, st); break;
-        case 7: launch_strided<7, INV>(a, rows, st); break;
-        case 8: launch_strided<8, INV>(a, rows, st); break;
-        default: throw SecpeError{-1, "unsupported NTT split"};
+template <typename K>
+void max_smem_carveout(K kern) {
+    static bool done = false;  // per instantiation
+    if (!done) {
+        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        done = true;
     }
 }
-template <bool INV>
-void dispatch_contig(int S, const PassArgs &a, int rows, cudaStream_t st) {
-    switch (S) {
-        case 5: launch_contig<5, INV>(a, rows, st); break;
-        case 6: launch_contig<6, INV>(a, rows, st); break;
-        case 7: launch_contig<7, INV>(a, rows, st); break;
-        case 8: launch_contig<8, INV>(a, rows, st); break;
-        case 9: launch_contig<9, INV>(a, rows, st); break;
-        default: throw SecpeError{-1, "unsupported NTT split"};
+
+int g_minb = -1;  // occupancy target (development switch SECPE_NTT_MINB = 3 | 4)
+int minb() {
+    if (g_minb < 0) {
+        const char *e = getenv("SECPE_NTT_MINB");
+        g_minb = (e && atoi(e) == 3) ? 3 : 4;
+    }
+    return g_minb;
+}
+
+template <int LOGN, bool INV, int IN, int MINB>
+void launch_strided_m(const PassArgs &a, int rows, cudaStream_t st) {
+    constexpr int S = LOGN / 2;
+    max_smem_carveout(ntt_strided<LOGN, INV, IN, MINB>);
+    dim3 grid((unsigned)((1L << (LOGN - S)) / SC), rows);
+    ntt_strided<LOGN, INV, IN, MINB><<<grid, SC * (1 << (S - RB)), 0, st>>>(a);
+}
+template <int LOGN, bool INV, int IO, int MINB>
+void launch_contig_m(const PassArgs &a, int rows, cudaStream_t st) {
+    using CF = ContigCfg<LOGN>;
+    max_smem_carveout(ntt_contig<LOGN, INV, IO, MINB>);
+    dim3 grid((unsigned)((1L << (LOGN - CF::S)) / CF::CG), rows);
+    ntt_contig<LOGN, INV, IO, MINB><<<grid, CT, 0, st>>>(a);
+}
+template <int LOGN, bool INV, int IN>
+void launch_strided(const PassArgs &a, int rows, cudaStream_t st) {
+    if (minb() == 3)
+        launch_strided_m<LOGN, INV, IN, 3>(a, rows, st);
+    else
+        launch_strided_m<LOGN, INV, IN, 4>(a, rows, st);
+}
+template <int LOGN, bool INV, int IO>
+void launch_contig(const PassArgs &a, int rows, cudaStream_t st) {
+    if (minb() == 3)
+        launch_contig_m<LOGN, INV, IO, 3>(a, rows, st);
+    else
+        launch_contig_m<LOGN, INV, IO, 4>(a, rows, st);
+}
+
+template <int LOGN>
+void run(const PassArgs &a, int rows, bool inverse, cudaStream_t st) {
+    const NttFusion &f = a.f;
+    if (!inverse) {
+        if (f.in_mode == IN_BCAST)
+            launch_strided<LOGN, false, IN_BCAST>(a, rows, st);
+        else
+            launch_strided<LOGN, false, IN_PLAIN>(a, rows, st);
+        LAUNCH_CHECK();
+        if (f.out_mode == OUT_RESCALE)
+            launch_contig<LOGN, false, OUT_RESCALE>(a, rows, st);
+        else if (f.out_mode == OUT_MODDOWN)
+            launch_contig<LOGN, false, OUT_MODDOWN>(a, rows, st);
+        else
+            launch_contig<LOGN, false, OUT_PLAIN>(a, rows, st);
+        LAUNCH_CHECK();
+    } else {
+        if (f.in_mode == IN_SRC)
+            launch_contig<LOGN, true, IN_SRC>(a, rows, st);
+        else
+            launch_contig<LOGN, true, IN_PLAIN>(a, rows, st);
+        LAUNCH_CHECK();
+        launch_strided<LOGN, true, IN_PLAIN>(a, rows, st);
+        LAUNCH_CHECK();
+    }
+}
+
+void dispatch(int logn, const PassArgs &a, int rows, bool inverse, cudaStream_t st) {
+    switch (logn) {
+        case 12: run<12>(a, rows, inverse, st); break;
+        case 13: run<13>(a, rows, inverse, st); break;
+        case 14: run<14>(a, rows, inverse, st); break;
+        case 15: run<15>(a, rows, inverse, st); break;
+        case 16: run<16>(a, rows, inverse, st); break;
+        default: throw SecpeError{-1, "NTT: log N must be in [12, 16]"};
     }
 }
 
 }  // namespace
 
-// logN = S1 + S2 with S1 = logN / 2 (strided part), S2 = logN - S1 (contiguous part)
-void ntt_forward(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st) {
+void ntt_forward(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
+                 const NttFusion &f) {
     if (n_polys <= 0 || lm.nl <= 0) return;
-    const int S1 = logn / 2, S2 = logn - S1;
-    const int rows = n_polys * lm.nl;
-    PassArgs a{data.p, data.cs, data.ps, lm, tab, logn, 0, 0};
-    dispatch_strided<false>(S1, a, rows, st);
-    LAUNCH_CHECK();
-    a.sg0 = S1;
-    a.final_ = 1;
-    dispatch_contig<false>(S2, a, rows, st);
-    LAUNCH_CHECK();
+    if (f.in_mode != IN_PLAIN && f.in_mode != IN_BCAST) throw SecpeError{-1, "ntt_forward: bad input mode"};
+    dispatch(logn, PassArgs{data, lm, tab, f}, n_polys * lm.nl, false, st);
 }
 
-void ntt_inverse(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st) {
+void ntt_inverse(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
+                 const NttFusion &f) {
     if (n_polys <= 0 || lm.nl <= 0) return;
-    const int S1 = logn / 2, S2 = logn - S1;
-    const int rows = n_polys * lm.nl;
-    PassArgs a{data.p, data.cs, data.ps, lm, tab, logn, logn - 1, 0};
-    dispatch_contig<true>(S2, a, rows, st);
-    LAUNCH_CHECK();
-    a.sg0 = S1 - 1;
-    a.final_ = 1;
-    dispatch_strided<true>(S1, a, rows, st);
-    LAUNCH_CHECK();
+    if ((f.in_mode != IN_PLAIN && f.in_mode != IN_SRC) || f.out_mode != OUT_PLAIN)
+        throw SecpeError{-1, "ntt_inverse: bad fusion mode"};
+    dispatch(logn, PassArgs{data, lm, tab, f}, n_polys * lm.nl, true, st);
 }
