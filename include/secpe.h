@@ -166,6 +166,19 @@ int secpe_drop(secpe_ctx *ctx, const secpe_ct *a, int32_t level, secpe_ct *out);
  * rescale.  Same level required; out scale = scale_a * scale_b.  out must not alias. */
 int secpe_mul_relin(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *a, const secpe_ct *b,
                     secpe_ct *out);
+/* a (x) b relinearised and rescaled in ONE step for a batch of n pairs (the form the argmax circuit
+ * uses, reading R11b): the ModDown by P and the division by q_l are a single floor division by
+ * B = P q_l (fast base conversion from {q_l} u P).  Not bit-identical to secpe_mul_relin followed by
+ * secpe_rescale (different rounding, error <= n_p + 1 per coefficient).  a[i], b[i]: same level
+ * l >= 1 and scale within the batch; out[i]: level l - 1, scale (S_a S_b) / q_l, sized
+ * secpe_ct_bytes(l - 1), must not alias.  Contiguous batches (data[i] = data[0] + i * ct words)
+ * are used in place; others are staged.  The relinearisation key is streamed once per batch. */
+int secpe_mul_relin_rescale(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *a, const secpe_ct *b,
+                            int32_t n, secpe_ct *out);
+/* Batched secpe_rotate: n ciphertexts (same level and scale) rotated by the same step with one
+ * pass over the Galois key.  out[i] must not alias in[i]. */
+int secpe_rotate_batch(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n, int32_t steps,
+                       secpe_ct *out);
 /* Rescale by q_level: round(c / q_l) (round half up, reading R12).  out level = in level - 1,
  * out scale = scale / q_l.  out must not alias. */
 int secpe_rescale(secpe_ctx *ctx, const secpe_ct *in, secpe_ct *out);

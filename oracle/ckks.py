@@ -477,12 +477,14 @@ class Oracle:
         lib().o_keyswitch(self.prm.cptr, P(dd), nl, P(swk), P(ks))
         return ks
 
-    def mul_relin(self, keys, a, b):
-        """ct x ct -> tensor -> relinearise (no rescale); scale S_a S_b."""
+    def mul_relin(self, keys, a, b, d=None):
+        """ct x ct -> tensor -> relinearise (no rescale); scale S_a S_b.  d: a precomputed
+        (possibly augmented) tensor of a and b."""
         if a.level != b.level:
             raise ValueError("level mismatch")
-        d = self.tensor(a, b)
-        ks = self.keyswitch(d[2], keys.rlk)
+        if d is None:
+            d = self.tensor(a, b)
+        ks = self.keyswitch(np.ascontiguousarray(d[2]), keys.rlk)
         out = np.zeros((2, a.level + 1, self.prm.N), dtype=np.uint64)
         lib().o_add(self.prm.cptr, P(np.ascontiguousarray(d[:2])), P(ks), a.level + 1, 2, P(out))
         return Ct(out, a.scale * b.scale)
@@ -542,16 +544,30 @@ class Oracle:
         self._log("MULC", lv, target_level, target_scale, str(C))
         return out
 
-    def mul_ct(self, keys, a, b, target_scale, target_level):
-        """a (x) b: drop both to target_level + 1, tensor + relinearise + rescale.
-        Output scale := target_scale if given else (S_a * S_b) / q_l."""
+    def mul_ct(self, keys, a, b, target_scale, target_level, lin=None):
+        """a (x) b [+ c x]: drop the inputs to target_level + 1 = l, tensor, optionally add the constant
+        product C x to (d0, d1) with C = rha(c Delta_c), Delta_c = (S_t q_l) / S_x (lin = (x, c); R9,
+        R13), relinearise, rescale.  Output scale := target_scale if given else (S_a * S_b) / q_l."""
         lv = target_level + 1
         a = self.drop(a, lv)
         b = self.drop(b, lv)
-        prod = self.mul_relin(keys, a, b)
         s = (a.scale * b.scale) / float(self.prm.primes[lv]) if target_scale is None else target_scale
-        out = self.rescale(prod, s)
-        self._log("MULCT", lv, target_level, s)
+        d = self.tensor(a, b)
+        extra = ""
+        if lin is not None:
+            x, c = lin
+            x = self.drop(x, lv)
+            dc = (s * float(self.prm.primes[lv])) / x.scale
+            C = round_half_away(c * dc)
+            if abs(C) >= 2 ** 62:
+                raise OverflowError("constant too large")
+            cx = self.mul_int_raw(x, C)
+            d01 = np.zeros((2, lv + 1, self.prm.N), dtype=np.uint64)
+            lib().o_add(self.prm.cptr, P(np.ascontiguousarray(d[:2])), P(cx), lv + 1, 2, P(d01))
+            d[:2] = d01
+            extra = str(C)
+        out = self.rescale(self.mul_relin(keys, a, b, d), s)
+        self._log("MULCT", lv, target_level, s, extra)
         return out
 
     def mul_mask(self, x, mask_slots, target_scale):
@@ -623,13 +639,21 @@ class Mirror:
         self._log("MULC", lv, target_level, target_scale, str(C))
         return MirrorCt(c * x.v, target_level, target_scale)
 
-    def mul_ct(self, keys, a, b, target_scale, target_level):
+    def mul_ct(self, keys, a, b, target_scale, target_level, lin=None):
         lv = target_level + 1
         if a.level < lv or b.level < lv:
             raise ValueError("level")
         s = (a.scale * b.scale) / float(self.prm.primes[lv]) if target_scale is None else target_scale
-        self._log("MULCT", lv, target_level, s)
-        return MirrorCt(a.v * b.v, target_level, s)
+        v = a.v * b.v
+        extra = ""
+        if lin is not None:
+            x, c = lin
+            if x.level < lv:
+                raise ValueError("level")
+            extra = str(round_half_away(c * ((s * float(self.prm.primes[lv])) / x.scale)))
+            v = v + c * x.v
+        self._log("MULCT", lv, target_level, s, extra)
+        return MirrorCt(v, target_level, s)
 
     def mul_mask(self, x, mask_slots, target_scale):
         lv = x.level

@@ -484,9 +484,12 @@ void o_tensor(const OCtx *c, const u64 *a, const u64 *b, int nl, u64 *d) {
  *   inner  : acc_b[t] = sum_j ext_j[t] * swk_j[b][t]
  *   ModDown: r_p = INTT(acc_b[p]);  out_b,i = (acc_b,i - NTT(sum_p [r_p (P/p)^{-1}]_p [P/p]_{q_i})) [P^{-1}]_{q_i}
  */
-void o_keyswitch(const OCtx *c, const u64 *d, int nl, const u64 *swk, u64 *ks) {
+/* ModUp + key inner product of O-10: returns acc[2][ne][N] (NTT form over Q_level u P, extended
+ * index e < nl -> prime e, e >= nl -> special prime e - nl); *eid_out = extended index -> prime id */
+static u64 *ks_acc(const OCtx *c, const u64 *d, int nl, const u64 *swk, int **eid_out) {
     u64 n = NN(c);
     int nq = c->nq, np = c->np, ne = nl + np, nek = nq + np;
+    (void)nq;
     int beta = (nl + c->alpha - 1) / c->alpha;
     /* extended basis: ext index e < nl -> prime e; e >= nl -> prime nq + (e - nl) */
     int *eid = (int *)malloc(sizeof(int) * ne);
@@ -538,6 +541,16 @@ void o_keyswitch(const OCtx *c, const u64 *d, int nl, const u64 *swk, u64 *ks) {
             }
         }
     }
+    free(dc); free(ext);
+    *eid_out = eid;
+    return acc;
+}
+
+void o_keyswitch(const OCtx *c, const u64 *d, int nl, const u64 *swk, u64 *ks) {
+    u64 n = NN(c);
+    int nq = c->nq, np = c->np, ne = nl + np;
+    int *eid;
+    u64 *acc = ks_acc(c, d, nl, swk, &eid);
     /* ModDown */
     for (int b = 0; b < 2; b++) {
         u64 *ab = acc + (u64)b * ne * n;
@@ -576,7 +589,7 @@ void o_keyswitch(const OCtx *c, const u64 *d, int nl, const u64 *swk, u64 *ks) {
         }
         free(r);
     }
-    free(eid); free(dc); free(acc); free(ext);
+    free(eid); free(acc);
 }
 
 /*

@@ -5,7 +5,8 @@ executed by either ``ckks.Oracle`` (ciphertexts) or ``ckks.Mirror`` (plaintext d
 both log the same op list, which tests diff against the CUDA library's own planner.
 
 Reading R13: odd polynomials in the power basis, evaluated with the fixed
-BSGS plans below (degrees 3, 7, 15).  Every sub-expression is requested at a target
+BSGS plans below (degrees 3, 7, 15).  A linear term c x that is summed with a ct x ct
+product enters that product before its rescale (one rescale instead of two).  Every sub-expression is requested at a target
 (scale, level) and computed as low as possible: a constant product drops its input to
 target+1 first; a ct x ct product drops both inputs to target+1.  Emission order is
 "first operand first" exactly as written here.
@@ -41,11 +42,10 @@ def eval_odd_poly(ev, keys, x, coeffs, target_scale):
     x8 = ev.mul_ct(keys, x4, x4, None, l - 3) if deg >= 15 else None
 
     def A(i, S, L):
-        # A_i = c_{4i+1} x + (c_{4i+3} x) * x^2  at (S, L)
+        # A_i = (c_{4i+3} x) * x^2 + c_{4i+1} x  at (S, L); the linear term joins the product
+        # before its (fused) rescale (reading R13)
         inner = ev.mul_const(x, coeffs[4 * i + 3], (S * q(L + 1)) / x2.scale, L + 1)
-        prod = ev.mul_ct(keys, inner, x2, S, L)
-        lin = ev.mul_const(x, coeffs[4 * i + 1], S, L)
-        return ev.add(prod, lin)
+        return ev.mul_ct(keys, inner, x2, S, L, lin=(x, coeffs[4 * i + 1]))
 
     def B(i, S, L):
         # B_i = A_{2i} + x^4 A_{2i+1}  at (S, L)
@@ -86,10 +86,9 @@ def hom_max(ev, keys, r, y, stages):
     s = sign(ev, keys, d, stages, ev.prm.scale)
     Ls = s.level
     g = ev.mul_const(d, 0.5, (Sy * float(ev.prm.primes[Ls])) / s.scale, Ls)
-    t2 = ev.mul_ct(keys, g, s, Sy, Ls - 1)
     ry = ev.add(r, y)
-    h = ev.mul_const(ry, 0.5, Sy, Ls - 1)
-    return ev.add(h, t2)
+    # (r - y)/2 * Sign(r - y) + (r + y)/2: the half-sum joins the product before its rescale
+    return ev.mul_ct(keys, g, s, Sy, Ls - 1, lin=(ry, 0.5))
 
 
 def mask_slots(layout, n_slots):

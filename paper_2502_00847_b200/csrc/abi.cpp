@@ -50,6 +50,53 @@ static CtView view_of(const Ctx &c, const secpe_ct *ct) {
     REQUIRE(ct->level >= 0 && ct->level < c.nq, SECPE_EINVAL, "ciphertext level out of range");
     return compact_view(c, ct->data, 1, ct->level, ct->scale);
 }
+// A batch of n caller ciphertexts as one CtView: the caller's memory when the batch is contiguous
+// (data[i] = data[0] + i * ct_words), else a staged copy (`stage` receives the buffer).
+static CtView batch_in(Ctx &c, const secpe_ct *in, int n, DevBuf &stage) {
+    REQUIRE(in && n >= 1, SECPE_EINVAL, "empty batch");
+    const int lv = in[0].level;
+    REQUIRE(lv >= 0 && lv < c.nq, SECPE_EINVAL, "ciphertext level out of range");
+    for (int i = 0; i < n; i++) {
+        REQUIRE(in[i].data, SECPE_EINVAL, "null ciphertext data");
+        REQUIRE(in[i].level == lv && in[i].scale == in[0].scale, SECPE_EINVAL, "batch must share level and scale");
+    }
+    const long cw = c.ct_words(lv);
+    bool contiguous = true;
+    for (int i = 1; i < n; i++) contiguous &= in[i].data == in[0].data + (long)i * cw;
+    CtView v = compact_view(c, in[0].data, n, lv, in[0].scale);
+    if (!contiguous) {
+        stage = DevBuf((size_t)n * cw, c.st);
+        for (int i = 0; i < n; i++)
+            CUDA_CHECK(cudaMemcpyAsync(stage.p + (long)i * cw, in[i].data, cw * 8, cudaMemcpyDeviceToDevice, c.st));
+        v.data = stage.p;
+    }
+    return v;
+}
+// Output batch at `level`: the caller's memory when contiguous, else a staging buffer copied back by
+// batch_out_finish.
+static CtView batch_out(Ctx &c, secpe_ct *out, int n, int level, double scale, DevBuf &stage) {
+    const long ow = c.ct_words(level);
+    bool contiguous = true;
+    for (int i = 0; i < n; i++) REQUIRE(out[i].data, SECPE_EINVAL, "null output data");
+    for (int i = 1; i < n; i++) contiguous &= out[i].data == out[0].data + (long)i * ow;
+    CtView v = compact_view(c, out[0].data, n, level, scale);
+    if (!contiguous) {
+        stage = DevBuf((size_t)n * ow, c.st);
+        v.data = stage.p;
+    }
+    return v;
+}
+static void batch_out_finish(Ctx &c, secpe_ct *out, int n, const CtView &v, const DevBuf &stage) {
+    const long ow = c.ct_words(v.level);
+    if (stage.p)
+        for (int i = 0; i < n; i++)
+            CUDA_CHECK(cudaMemcpyAsync(out[i].data, stage.p + (long)i * ow, ow * 8, cudaMemcpyDeviceToDevice, c.st));
+    for (int i = 0; i < n; i++) {
+        out[i].level = v.level;
+        out[i].scale = v.scale;
+    }
+}
+
 static void set_out(secpe_ct *out, const CtView &v) {
     out->level = v.level;
     out->scale = v.scale;
@@ -122,6 +169,16 @@ int secpe_ctx_create(const secpe_params *prm, void *stream, secpe_ctx **out) {
             throw SecpeError{SECPE_ECUDA, "no CUDA device: libsecpe has no CPU fallback"};
         auto h = std::make_unique<secpe_ctx>();
         h->c.st = (cudaStream_t)stream;
+        {
+            // scratch comes from the device's stream-ordered pool: keep freed blocks cached instead of
+            // returning them to the driver at every synchronisation (hot-path allocations are then free)
+            int dev = 0;
+            CUDA_CHECK(cudaGetDevice(&dev));
+            cudaMemPool_t pool;
+            CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, dev));
+            uint64_t thr = ~0ULL;
+            CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        }
         h->c.build(prm->q, (int)prm->n_q, prm->p, (int)prm->n_p, (int)prm->alpha, (int)prm->log_n, prm->scale);
         *out = h.release();
     });
@@ -342,6 +399,35 @@ int secpe_mul_relin(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *a, c
         CtView vo = compact_view(ctx->c, out->data, 1, va.level, va.scale * vb.scale);
         ev_mul_relin(ctx->c, *keys->k, va, vb, vo);
         set_out(out, vo);
+    });
+}
+int secpe_mul_relin_rescale(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *a, const secpe_ct *b, int32_t n,
+                            secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && keys && a && b && out && n >= 1, SECPE_EINVAL, "null argument");
+        Ctx &c = ctx->c;
+        DevBuf sa, sb, so;
+        CtView va = batch_in(c, a, n, sa), vb = batch_in(c, b, n, sb);
+        REQUIRE(va.level == vb.level, SECPE_ELEVEL, "mul_relin_rescale needs equal levels");
+        REQUIRE(va.level >= 1, SECPE_ELEVEL, "no level left to rescale");
+        for (int i = 0; i < n; i++)
+            REQUIRE(out[i].data != a[i].data && out[i].data != b[i].data, SECPE_EINVAL, "out must not alias");
+        CtView vo = batch_out(c, out, n, va.level - 1, (va.scale * vb.scale) / (double)c.primes[va.level], so);
+        ev_mul_relin_rescale(c, *keys->k, va, vb, nullptr, 0, vo);
+        batch_out_finish(c, out, n, vo, so);
+    });
+}
+int secpe_rotate_batch(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n, int32_t steps,
+                       secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && keys && in && out && n >= 1, SECPE_EINVAL, "null argument");
+        Ctx &c = ctx->c;
+        DevBuf si, so;
+        CtView vi = batch_in(c, in, n, si);
+        for (int i = 0; i < n; i++) REQUIRE(out[i].data != in[i].data, SECPE_EINVAL, "out must not alias");
+        CtView vo = batch_out(c, out, n, vi.level, vi.scale, so);
+        ev_rotate(c, *keys->k, vi, steps, vo);
+        batch_out_finish(c, out, n, vo, so);
     });
 }
 int secpe_rescale(secpe_ctx *ctx, const secpe_ct *in, secpe_ct *out) {

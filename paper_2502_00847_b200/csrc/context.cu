@@ -290,6 +290,13 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
     hat_p = upload(vhatp, st);
     pinv = upload(vpinv, st);
     pinv_sh = upload(vpinvsh, st);
+    h_pinv = vpinv;
+    h_pinv_sh = vpinvsh;
+    {
+        std::vector<u64> pm(nq);
+        for (int i = 0; i < nq; i++) pm[i] = h_invmod(vpinv[i], primes[i]);  // P mod q_i
+        pmod = upload(pm, st);
+    }
 
     // per-level constants
     lvl.clear();
@@ -339,6 +346,45 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
             lc->half = upload(hf, st);
             lc->qlinv = upload(qi, st);
             lc->qlinv_sh = upload(qis, st);
+            // fused relinearise-and-rescale (bit-identical to ModDown then rescale, eval.cu):
+            //   rr_fold [np+1]: N^{-1} mod q_l, then N^{-1} (P/p)^{-1} mod p
+            //   rr_hl   [np]  : (P/p) mod q_l (split-30 packed)
+            //   rr_hat  [np+2][l]: (P/p) mod q_i, P mod q_i, -P floor(q_l/2) mod q_i (split-30 packed)
+            //   rr_binv [l]   : (P q_l)^{-1} mod q_i
+            std::vector<u64> fold(np + 1), foldsh(np + 1), hl(np), rhat((size_t)(np + 2) * l), binv(l), binvsh(l);
+            fold[0] = h_invmod((u64)N % ql, ql);
+            foldsh[0] = h_shoup(fold[0], ql);
+            for (int p2 = 0; p2 < np; p2++) {
+                const u64 pp = primes[nq + p2];
+                fold[1 + p2] = h_mulmod(vihp[p2], h_invmod((u64)N % pp, pp), pp);
+                foldsh[1 + p2] = h_shoup(fold[1 + p2], pp);
+                u64 h = 1;
+                for (int p3 = 0; p3 < np; p3++)
+                    if (p3 != p2) h = h_mulmod(h, primes[nq + p3] % ql, ql);
+                hl[p2] = pack30(h);
+            }
+            for (int i = 0; i < l; i++) {
+                const u64 qi2 = primes[i];
+                u64 Pm = 1;
+                for (int p2 = 0; p2 < np; p2++) {
+                    u64 h = 1;
+                    for (int p3 = 0; p3 < np; p3++)
+                        if (p3 != p2) h = h_mulmod(h, primes[nq + p3] % qi2, qi2);
+                    rhat[(size_t)p2 * l + i] = pack30(h);
+                    Pm = h_mulmod(Pm, primes[nq + p2] % qi2, qi2);
+                }
+                rhat[(size_t)np * l + i] = pack30(Pm);
+                const u64 ph = h_mulmod(Pm, (ql >> 1) % qi2, qi2);
+                rhat[(size_t)(np + 1) * l + i] = pack30(ph ? qi2 - ph : 0);
+                binv[i] = h_invmod(h_mulmod(Pm, ql % qi2, qi2), qi2);
+                binvsh[i] = h_shoup(binv[i], qi2);
+            }
+            lc->rr_hl = upload(hl, st);
+            lc->rr_fold = upload(fold, st);
+            lc->rr_fold_sh = upload(foldsh, st);
+            lc->rr_hat = upload(rhat, st);
+            lc->rr_binv = upload(binv, st);
+            lc->rr_binv_sh = upload(binvsh, st);
         }
         lvl.push_back(std::move(lc));
     }

@@ -29,6 +29,8 @@ struct LevelConsts {
     DevBuf inv_hat_ninv, inv_hat_ninv_sh;  // [nl]  N^{-1} (Q'_j / q_i)^{-1} mod q_i (folded into the INTT)
     DevBuf hat;                  // [beta][16][ne]  (Q'_j / q_i) mod t_e, split-30 packed
     DevBuf half, qlinv, qlinv_sh;  // rescale by q_{nl-1}: [nl-1]
+    // fused relinearise-and-rescale (ev_mul_relin_rescale), l = nl - 1 >= 1; see context.cu
+    DevBuf rr_fold, rr_fold_sh, rr_hl, rr_hat, rr_binv, rr_binv_sh;
 };
 
 // CUDA-event profiling of the dominant kernels inside a timed region (bench.py roofline)
@@ -77,9 +79,10 @@ struct Ctx {
     // ModDown constants
     DevBuf ihp, ihp_sh, hat_p, pinv, pinv_sh;  // hat_p split-30 packed
     DevBuf ihp_ninv, ihp_ninv_sh;               // N^{-1} (P/p)^{-1} mod p (folded into the INTT)
+    DevBuf pmod;                                // [nq] P mod q_i
     std::vector<std::unique_ptr<LevelConsts>> lvl;  // index = level
     // host copies used by planning
-    std::vector<u64> h_br0, h_br1;
+    std::vector<u64> h_br0, h_br1, h_pinv, h_pinv_sh;
     // instrumentation
     bool log_on = false;
     std::string oplog;
@@ -130,6 +133,10 @@ void ev_rescale(Ctx &c, const CtView &in, const CtView &out);
 void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, const u64 *add,
                   long add_stride, int add_polys, u64 *out, long out_stride);
 void ev_mul_relin(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const CtView &out);
+// a (x) b [+ C x] relinearised and rescaled by q_l in one pass (bit-identical to ev_mul_relin then
+// ev_rescale); out at level a.level - 1.  lin_x: optional linear term (nullptr: none), C its constant
+void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const CtView *lin_x, i64 C,
+                          const CtView &out);
 void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView &out);
 void ev_mul_plain_ntt(Ctx &c, const CtView &a, const u64 *pt, const CtView &out);
 LimbConst limb_const(const Ctx &c, i64 C, int nl);

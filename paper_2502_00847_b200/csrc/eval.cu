@@ -106,14 +106,13 @@ void ev_rescale(Ctx &c, const CtView &in, const CtView &out) {
     c.prof_end(pa, 2, 8.0 * (double)n * (2 * (l + 1) + 2 * l) * N, n);
 }
 
-// Hybrid key switching of d (NTT form; ct c at d + c * d_stride, level limbs), result added to
-// `add` (add_polys of 2 polynomials; compact, ct stride add_stride) and written compact to out.
-void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, const u64 *add,
-                  long add_stride, int add_polys, u64 *out, long out_stride) {
+// ModUp + key inner product (R10): acc[ct][b][ne][N] over Q_level u P (NTT form).  d01/d01s: optional
+// tensor (d0, d1) rows whose [P] multiple is added on the Q limbs (R11b).
+static void ks_modup_inner(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, DevBuf &acc,
+                           const u64 *d01 = nullptr, long d01s = 0) {
     const long N = c.N;
     const int nl = level + 1, np = c.np, ne = nl + np, bt = c.beta(level);
     const LevelConsts &lc = c.level(level);
-    const size_t pa = c.prof_begin(1);
     // 1. y_i = [INTT(d)_i (Q'_j/q_i)^{-1}]_{q_i}: copy and the ModUp factor fused into the INTT
     DevBuf dc((size_t)n * nl * N, c.st);
     NttFusion f1;
@@ -125,8 +124,7 @@ void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u
     // 2. ModUp into every digit's complement, then NTT of the converted limbs
     const long exts = (long)bt * ne * N;
     DevBuf ext((size_t)n * exts, c.st);
-    k_modup(c.tab, c.logn, dc.p, (long)nl * N, ext.p, exts, n, nl, np, c.nq, c.alpha, nullptr, nullptr, lc.hat.p,
-            c.st);
+    k_modup(c.tab, c.logn, dc.p, (long)nl * N, ext.p, exts, n, nl, np, c.nq, c.alpha, lc.hat.p, c.st);
     for (int j = 0; j < bt; j++) {
         const int i0 = j * c.alpha, i1 = std::min(i0 + c.alpha, nl);
         if (i0 > 0) ev_ntt(c, RowsArg{ext.p + (long)j * ne * N, 2 * exts, exts}, n, LimbMap{i0, i0, 0, 0}, false);
@@ -135,8 +133,22 @@ void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u
     }
     // 3. inner product with the switching key
     const long accs = 2L * ne * N;
-    DevBuf acc((size_t)n * accs, c.st);
-    k_ks_inner(c.tab, c.logn, d, d_stride, ext.p, exts, key, c.nq, np, acc.p, accs, n, nl, c.alpha, c.st);
+    acc = DevBuf((size_t)n * accs, c.st);
+    k_ks_inner(c.tab, c.logn, d, d_stride, ext.p, exts, key, c.nq, np, acc.p, accs, n, nl, c.alpha, c.st, d01, d01s,
+               c.pmod.p);
+    c.cnt.launches += 2;
+}
+
+// Hybrid key switching of d (NTT form; ct c at d + c * d_stride, level limbs), result added to
+// `add` (add_polys of 2 polynomials; compact, ct stride add_stride) and written compact to out.
+void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, const u64 *add,
+                  long add_stride, int add_polys, u64 *out, long out_stride) {
+    const long N = c.N;
+    const int nl = level + 1, np = c.np, ne = nl + np, bt = c.beta(level);
+    const size_t pa = c.prof_begin(1);
+    DevBuf acc;
+    ks_modup_inner(c, d, d_stride, n, level, key, acc);
+    const long accs = 2L * ne * N;
     // 4. ModDown: INTT of the special limbs (with (P/p)^{-1} folded in), conversion to Q, then an NTT
     //    whose last pass forms (acc - T) P^{-1} + addend
     NttFusion f4;
@@ -145,7 +157,7 @@ void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u
     ev_ntt(c, RowsArg{acc.p + (long)nl * N, accs, (long)ne * N}, 2 * n, LimbMap{np, 0, 0, c.nq}, true, f4);
     const long Ts = 2L * nl * N;
     DevBuf T((size_t)n * Ts, c.st);
-    k_moddown_conv(c.tab, c.logn, acc.p, accs, T.p, Ts, n, nl, np, c.nq, nullptr, nullptr, c.hat_p.p, c.st);
+    k_moddown_conv(c.tab, c.logn, acc.p, accs, ne, nl, np, T.p, Ts, nl, n, c.hat_p.p, c.nq, c.st);
     NttFusion f6;
     f6.out_mode = 2;
     f6.e1 = CRows{acc.p, accs, (long)ne * N};
@@ -155,10 +167,58 @@ void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u
     f6.k = c.pinv.p;
     f6.ksh = c.pinv_sh.p;
     ev_ntt(c, RowsArg{T.p, Ts, (long)nl * N}, 2 * n, qmap(nl), false, f6);
-    c.cnt.launches += 3;
+    c.cnt.launches += 1;
     c.cnt.keyswitch += n;
     // algorithmic bytes: input limbs + output limbs per ciphertext + the key once per batch
     c.prof_end(pa, 1, 8.0 * N * ((double)n * (nl + 2 * nl + add_polys * nl) + 2.0 * bt * ne), n);
+}
+
+// Relinearise and rescale in one pass, bit-identical to ev_mul_relin followed by ev_rescale (R10-R12):
+// with x_b = acc_b + [P] d_b (formed inside the key inner product), the relinearised ciphertext is
+// Y_b = (x_b - ModDownConv(x_b)) P^{-1} and its rescale is (Y_b + half - [r]) q_l^{-1}; both
+// corrections are computed in the coefficient domain (k_rr_conv) and removed by ONE forward NTT whose
+// epilogue forms (x_i - NTT(T_i)) (P q_l)^{-1}.  This saves the rescale's own INTT/NTT round trip.
+void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const CtView *lin_x, i64 C,
+                          const CtView &out) {
+    const int l = a.level, nl = l + 1;
+    if (l < 1) throw SecpeError{-2, "mul_relin_rescale: no level left"};
+    if (b.level != l || out.level != l - 1) throw SecpeError{-1, "mul_relin_rescale: levels"};
+    const long N = c.N, ds = 3L * nl * N;
+    const int n = a.n, np = c.np, ne = nl + np, bt = c.beta(l);
+    const LevelConsts &lc = c.level(l);
+    DevBuf d((size_t)n * ds, c.st);
+    if (lin_x) {
+        const LimbConst Cl = limb_const(c, C, nl);
+        k_tensor(c.tab, c.logn, crows_of(a), crows_of(b), d.p, ds, n, nl, c.st, crows_of(*lin_x), &Cl);
+    } else {
+        k_tensor(c.tab, c.logn, crows_of(a), crows_of(b), d.p, ds, n, nl, c.st);
+    }
+    c.cnt.launches++;
+    const size_t pa = c.prof_begin(1);
+    DevBuf acc;
+    ks_modup_inner(c, d.p + 2L * nl * N, ds, n, l, k.rlk.p, acc, d.p, ds);
+    const long accs = 2L * ne * N;
+    // INTT of the B rows (q_l row, then the special rows: contiguous rows l .. ne-1) with (B/s)^{-1} folded
+    NttFusion f4;
+    f4.k = lc.rr_fold.p;
+    f4.ksh = lc.rr_fold_sh.p;
+    ev_ntt(c, RowsArg{acc.p + (long)l * N, accs, (long)ne * N}, 2 * n, LimbMap{np + 1, 1, l, c.nq}, true, f4);
+    const long Ts = 2L * l * N;
+    DevBuf T((size_t)n * Ts, c.st);
+    k_rr_conv(c.tab, c.logn, acc.p, accs, ne, l, np, T.p, Ts, n, lc.rr_hat.p, lc.rr_hl.p, c.h_pinv[l], c.h_pinv_sh[l],
+              c.st);
+    NttFusion f6;
+    f6.out_mode = 2;
+    f6.e1 = CRows{acc.p, accs, (long)ne * N};
+    f6.out = rows_of(out);
+    f6.k = lc.rr_binv.p;
+    f6.ksh = lc.rr_binv_sh.p;
+    ev_ntt(c, RowsArg{T.p, Ts, (long)l * N}, 2 * n, qmap(l), false, f6);
+    c.cnt.launches += 1;
+    c.cnt.keyswitch += n;
+    c.cnt.rescale += n;
+    c.cnt.mulct += n;
+    c.prof_end(pa, 1, 8.0 * N * ((double)n * (3 * nl + 2 * l) + 2.0 * bt * ne), n);
 }
 
 void ev_mul_relin(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const CtView &out) {

@@ -60,29 +60,38 @@ void k_add_const(const Tab &tab, int logn, CRows a, RowsArg out, int n_polys, Li
 void k_mul_poly(const Tab &tab, int logn, CRows a, const u64 *b, RowsArg out, int n_polys, LimbMap lm,
                 cudaStream_t st);
 // tensor: d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1 for n_ct ciphertexts (a, b: CRows views);
-// d compact: ct c, poly p at d + c*d_ct_stride + p*nl*N
+// d compact: ct c, poly p at d + c*d_ct_stride + p*nl*N.  With lin (x != nullptr): d0 += C x0,
+// d1 += C x1 (C per-limb residues, the planned linear term of R13)
 void k_tensor(const Tab &tab, int logn, CRows a, CRows b, u64 *d, long d_ct_stride, int n_ct, int nl,
-              cudaStream_t st);
+              cudaStream_t st, CRows x = CRows{nullptr, 0, 0}, const LimbConst *C = nullptr);
 // automorphism in the NTT domain: out[i] = in[perm_g(i)]
 void k_automorph(int logn, CRows a, RowsArg out, int n_polys, int nl, u64 galois, cudaStream_t st);
 
 // ---- key switching (keyswitch.cu) ------------------------------------------------------------
 struct KsLevel;  // per-level constants (device pointers), see context.h
-// ModUp base conversion (coefficient domain): for every digit j and extended limb e not in I_j:
-//   ext[c][j][e] = sum_{i in I_j} [dc_i (Q'_j/q_i)^-1]_{q_i} [Q'_j/q_i]_{t_e}  mod t_e
-// dc: [n_ct][nl][N] coefficient form (inv_hat == nullptr: dc already holds [dc_i (Q'_j/q_i)^-1]); ext: [n_ct][beta][ne][N]
+// ModUp base conversion (coefficient domain, R10): for every digit j and extended limb e not in I_j:
+//   ext[c][j][e] = sum_{i in I_j} y_i [Q'_j/q_i]_{t_e}  mod t_e
+// dc: [n_ct][nl][N] holding y_i = [INTT(d)_i (Q'_j/q_i)^-1]_{q_i} (the factor folded into the INTT);
+// ext: [n_ct][beta][ne][N]; hat: split-30 packed constants [beta][16][ne]
 void k_modup(const Tab &tab, int logn, const u64 *dc, long dc_ct_stride, u64 *ext, long ext_ct_stride,
-             int n_ct, int nl, int np, int nq_total, int alpha, const u64 *inv_hat, const u64 *inv_hat_sh,
-             const u64 *hat, cudaStream_t st);
+             int n_ct, int nl, int np, int nq_total, int alpha, const u64 *hat, cudaStream_t st);
 // key inner product: acc[c][b][e] = sum_j X_j[e] * key_j[b][prime(e)], X_j[e] = d[c][e] if e in I_j else ext[c][j][e]
+// (+ pmod[e] * d01[c][b][e] on the Q limbs e < nl when d01 != nullptr: relinearise-and-rescale, R11b)
 void k_ks_inner(const Tab &tab, int logn, const u64 *d, long d_ct_stride, const u64 *ext, long ext_ct_stride,
                 const u64 *key, int nq_total, int np, u64 *acc, long acc_ct_stride, int n_ct, int nl,
-                int alpha, cudaStream_t st);
-// ModDown conversion: T[c][b][i] = sum_p [r_p (P/p)^-1]_p [P/p]_{q_i} mod q_i ; r = acc P-limbs (coeff form);
-// inv_hat_p == nullptr: the P-limbs already hold [r_p (P/p)^-1]_p (factor folded into the INTT)
-void k_moddown_conv(const Tab &tab, int logn, const u64 *acc, long acc_ct_stride, u64 *T, long T_ct_stride,
-                    int n_ct, int nl, int np, int nq_total, const u64 *inv_hat_p, const u64 *inv_hat_p_sh,
-                    const u64 *hat_p, cudaStream_t st);
+                int alpha, cudaStream_t st, const u64 *d01 = nullptr, long d01_ct_stride = 0,
+                const u64 *pmod = nullptr);
+// ModDown conversion (R11, R11b): T[c][b][i] = sum_{s < ns} y_s [B/s]_{q_i} mod q_i for i < nt, with
+// y_s = acc[c][b][row0 + s] (coefficient form, already times (B/s)^{-1}); hatpk[s * hstride + i]
+// split-30 packed
+void k_moddown_conv(const Tab &tab, int logn, const u64 *acc, long acc_ct_stride, int ne, int row0, int ns, u64 *T,
+                    long T_ct_stride, int nt, int n_ct, const u64 *hatpk, int hstride, cudaStream_t st);
+// fused ModDown + rescale conversion (see ks.cu rr_conv_kernel): acc rows l .. l+np hold INTT(x_l) and
+// the folded P-limbs; T[c][b][i] for i < l
+void k_rr_conv(const Tab &tab, int logn, const u64 *acc, long acc_ct_stride, int ne, int l, int np, u64 *T,
+               long T_ct_stride, int n_ct, const u64 *hatpk, const u64 *hl, u64 pinv_l, u64 pinv_l_sh,
+               cudaStream_t st);
+
 // ---- sampling / keys (sample.cu) ----------------------------------------------------------------
 // uniform residues in the NTT domain: out[l][k] for prime ids map (formula lm), counter layout per R6
 void k_sample_uniform(const Tab &tab, int logn, u64 seed, u64 tag, u64 *out, LimbMap lm, cudaStream_t st);

@@ -42,9 +42,7 @@ __device__ __forceinline__ void stv2(u64 *p, u64 a, u64 b) { *reinterpret_cast<u
 template <int A>
 __global__ void __launch_bounds__(TPB) modup_kernel(Tab tab, int logn, const u64 *__restrict__ dc, long dcs,
                                                     u64 *__restrict__ ext, long exts, int nl, int np, int nq_total,
-                                                    int alpha, int beta, const u64 *__restrict__ inv_hat,
-                                                    const u64 *__restrict__ inv_hat_sh,
-                                                    const u64 *__restrict__ hatpk) {
+                                                    int alpha, int beta, const u64 *__restrict__ hatpk) {
     static_assert(A % 2 == 0, "A even (16-byte constant pairs)");
     __shared__ __align__(16) u64 sc[MAXL * A];
     const int ct = blockIdx.y / beta, j = blockIdx.y % beta;
@@ -62,9 +60,8 @@ __global__ void __launch_bounds__(TPB) modup_kernel(Tab tab, int logn, const u64
         if (a < na) {
             const int i = i0 + a;
             const ulonglong2 x = ldv2(dc + ct * dcs + i * N + k);
-            // inv_hat == nullptr: the factor was folded into the INTT (input is already y)
-            const u64 y0 = inv_hat ? mul_shoup(x.x, inv_hat[i], inv_hat_sh[i], tab.q[i]) : x.x;
-            const u64 y1 = inv_hat ? mul_shoup(x.y, inv_hat[i], inv_hat_sh[i], tab.q[i]) : x.y;
+            // the factor (Q'_j/q_i)^{-1} is folded into the INTT: the input already is y
+            const u64 y0 = x.x, y1 = x.y;
             yl[a][0] = (uint32_t)y0 & M30, yh[a][0] = (uint32_t)(y0 >> 30);
             yl[a][1] = (uint32_t)y1 & M30, yh[a][1] = (uint32_t)(y1 >> 30);
         } else {
@@ -100,7 +97,8 @@ __global__ void __launch_bounds__(TPB) modup_kernel(Tab tab, int logn, const u64
 template <int MAXB>
 __global__ void ks_inner_kernel(Tab tab, int logn, const u64 *__restrict__ d, long ds, const u64 *__restrict__ ext,
                                 long exts, const u64 *__restrict__ key, int nq_total, int np,
-                                u64 *__restrict__ acc, long accs, int n_ct, int nl, int alpha, int beta) {
+                                u64 *__restrict__ acc, long accs, int n_ct, int nl, int alpha, int beta,
+                                const u64 *__restrict__ d01, long d01s, const u64 *__restrict__ pmod) {
     const int e = blockIdx.y;
     const long N = 1L << logn;
     const long k = (long)blockIdx.x * TPB + threadIdx.x;
@@ -124,55 +122,55 @@ __global__ void ks_inner_kernel(Tab tab, int logn, const u64 *__restrict__ d, lo
                 mac_wide(s0, x, kb[j]);
                 mac_wide(s1, x, ka[j]);
             }
+        if (d01 && e < nl) {  // relinearise-and-rescale (R11b): x_b = acc_b + [P]_{q_e} d_b on Q limbs
+            const u64 pm = pmod[e];
+            mac_wide(s0, d01[c * d01s + e * N + k], pm);
+            mac_wide(s1, d01[c * d01s + ((long)nl + e) * N + k], pm);
+        }
         acc[c * accs + (long)e * N + k] = barrett128(s0, q, r0, r1);
         acc[c * accs + (long)(ne + e) * N + k] = barrett128(s1, q, r0, r1);
     }
 }
 
-// ModDown conversion (R11).  grid: x = coefficient chunks (two per thread), y = ct * 2 + b.
-// Packed constants [P/p]_{q_i} in shared memory as sc[i][p] (NP words per i).
-template <int NP>
+// ModDown conversion (R11 / R11b).  grid: x = coefficient chunks (two per thread), y = ct * 2 + b.
+// Sources: ns rows starting at row0 of each acc polynomial (already holding [r_s (B/s)^{-1}]_s: the
+// factor is folded into the INTT); targets: q_0..q_{nt-1}.  Packed constants [B/s]_{q_i} at
+// hatpk[s * hstride + i], staged in shared memory as sc[i][s] (NS words per i).
+template <int NS>
 __global__ void __launch_bounds__(TPB) moddown_conv_kernel(Tab tab, int logn, const u64 *__restrict__ acc, long accs,
-                                                           u64 *__restrict__ T, long Ts, int nl, int np,
-                                                           int nq_total, const u64 *__restrict__ ihp,
-                                                           const u64 *__restrict__ ihp_sh,
-                                                           const u64 *__restrict__ hatpk) {
-    static_assert(NP % 2 == 0, "NP even");
-    __shared__ __align__(16) u64 sc[MAXL * NP];
+                                                           int ne, int row0, int ns, u64 *__restrict__ T, long Ts,
+                                                           int nt, const u64 *__restrict__ hatpk, int hstride) {
+    static_assert(NS % 2 == 0, "NS even");
+    __shared__ __align__(16) u64 sc[MAXL * NS];
     const int ct = blockIdx.y / 2, b = blockIdx.y % 2;
     const long N = 1L << logn;
-    const int ne = nl + np;
-    for (int t = threadIdx.x; t < nl * NP; t += TPB) {
-        const int i = t / NP, p = t % NP;
-        sc[t] = p < np ? hatpk[(long)p * nq_total + i] : 0;
+    for (int t = threadIdx.x; t < nt * NS; t += TPB) {
+        const int i = t / NS, p = t % NS;
+        sc[t] = p < ns ? hatpk[(long)p * hstride + i] : 0;
     }
     const long k = 2L * ((long)blockIdx.x * TPB + threadIdx.x);
-    const u64 *src = acc + ct * accs + ((long)b * ne + nl) * N + k;
-    uint32_t yl[NP][2], yh[NP][2];
+    const u64 *src = acc + ct * accs + ((long)b * ne + row0) * N + k;
+    uint32_t yl[NS][2], yh[NS][2];
 #pragma unroll
-    for (int p = 0; p < NP; p++) {
-        if (p < np) {
-            const int pr = nq_total + p;
+    for (int p = 0; p < NS; p++) {
+        if (p < ns) {
             const ulonglong2 x = ldv2(src + p * N);
-            // ihp == nullptr: the factor was folded into the INTT (input is already y)
-            const u64 y0 = ihp ? mul_shoup(x.x, ihp[p], ihp_sh[p], tab.q[pr]) : x.x;
-            const u64 y1 = ihp ? mul_shoup(x.y, ihp[p], ihp_sh[p], tab.q[pr]) : x.y;
-            yl[p][0] = (uint32_t)y0 & M30, yh[p][0] = (uint32_t)(y0 >> 30);
-            yl[p][1] = (uint32_t)y1 & M30, yh[p][1] = (uint32_t)(y1 >> 30);
+            yl[p][0] = (uint32_t)x.x & M30, yh[p][0] = (uint32_t)(x.x >> 30);
+            yl[p][1] = (uint32_t)x.y & M30, yh[p][1] = (uint32_t)(x.y >> 30);
         } else {
             yl[p][0] = yh[p][0] = yl[p][1] = yh[p][1] = 0;
         }
     }
     __syncthreads();
-    u64 *dst = T + ct * Ts + (long)b * nl * N + k;
-    for (int i = 0; i < nl; i++) {
+    u64 *dst = T + ct * Ts + (long)b * nt * N + k;
+    for (int i = 0; i < nt; i++) {
         Acc4 s0, s1;
         acc4_zero(s0);
         acc4_zero(s1);
-        const ulonglong2 *cp = reinterpret_cast<const ulonglong2 *>(sc + i * NP);
+        const ulonglong2 *cp = reinterpret_cast<const ulonglong2 *>(sc + i * NS);
 #pragma unroll
-        for (int p2 = 0; p2 < NP / 2; p2++) {
-            if (2 * p2 < np) {
+        for (int p2 = 0; p2 < NS / 2; p2++) {
+            if (2 * p2 < ns) {
                 const ulonglong2 c = cp[p2];
                 acc4_mac(s0, yl[2 * p2][0], yh[2 * p2][0], c.x);
                 acc4_mac(s1, yl[2 * p2][1], yh[2 * p2][1], c.x);
@@ -184,20 +182,101 @@ __global__ void __launch_bounds__(TPB) moddown_conv_kernel(Tab tab, int logn, co
              acc4_reduce(s1, tab.q[i], tab.br0[i], tab.br1[i]));
     }
 }
-
+// Fused ModDown + rescale conversion (ev_mul_relin_rescale).  grid: x = coefficient chunks (two
+// per thread), y = ct * 2 + b.  Rows l .. l + np of each acc polynomial hold, in coefficient form,
+// xc = INTT(x_l) and y_p = [INTT(x_p) (P/p)^{-1}]_p, where x = acc + [P] d.  Per coefficient:
+//   Y_l = (xc - sum_p y_p [P/p]_{q_l}) P^{-1} mod q_l        (the q_l limb of the ModDown output)
+//   r   = [Y_l + floor(q_l/2)]_{q_l}                           (R12)
+//   T_i = sum_p y_p [P/p]_{q_i} + r [P]_{q_i} - [P floor(q_l/2)]_{q_i}   for i < l
+// so that (x_i - NTT(T_i)) (P q_l)^{-1} equals ModDown followed by the rescale, exactly.
+template <int NS>
+__global__ void __launch_bounds__(TPB) rr_conv_kernel(Tab tab, int logn, const u64 *__restrict__ acc, long accs,
+                                                      int ne, int l, int np, u64 *__restrict__ T, long Ts,
+                                                      const u64 *__restrict__ hatpk, const u64 *__restrict__ hl,
+                                                      u64 pinv_l, u64 pinv_l_sh) {
+    static_assert(NS % 2 == 0, "NS even");
+    __shared__ __align__(16) u64 sc[MAXL * NS];
+    __shared__ u64 shl[MAXA];
+    const int ct = blockIdx.y / 2, b = blockIdx.y % 2;
+    const long N = 1L << logn;
+    const int ns = np + 2;
+    for (int t = threadIdx.x; t < l * NS; t += TPB) {
+        const int i = t / NS, p = t % NS;
+        sc[t] = p < ns ? hatpk[(long)p * l + i] : 0;
+    }
+    for (int t = threadIdx.x; t < np; t += TPB) shl[t] = hl[t];
+    const long k = 2L * ((long)blockIdx.x * TPB + threadIdx.x);
+    const u64 *src = acc + ct * accs + ((long)b * ne + l) * N + k;
+    uint32_t yl[NS][2], yh[NS][2];
+#pragma unroll
+    for (int p = 0; p < NS; p++) {
+        if (p < np) {
+            const ulonglong2 x = ldv2(src + (p + 1) * N);
+            yl[p][0] = (uint32_t)x.x & M30, yh[p][0] = (uint32_t)(x.x >> 30);
+            yl[p][1] = (uint32_t)x.y & M30, yh[p][1] = (uint32_t)(x.y >> 30);
+        } else {
+            yl[p][0] = yh[p][0] = yl[p][1] = yh[p][1] = 0;
+        }
+    }
+    __syncthreads();
+    {
+        const ulonglong2 xc = ldv2(src);
+        const u64 ql = tab.q[l], half = ql >> 1;
+        Acc4 s0, s1;
+        acc4_zero(s0);
+        acc4_zero(s1);
+#pragma unroll
+        for (int p = 0; p < NS; p++)
+            if (p < np) {
+                acc4_mac(s0, yl[p][0], yh[p][0], shl[p]);
+                acc4_mac(s1, yl[p][1], yh[p][1], shl[p]);
+            }
+        const u64 t0 = acc4_reduce(s0, ql, tab.br0[l], tab.br1[l]), t1 = acc4_reduce(s1, ql, tab.br0[l], tab.br1[l]);
+        const u64 r0 = csub(mul_shoup(submod(xc.x, t0, ql), pinv_l, pinv_l_sh, ql) + half, ql);
+        const u64 r1 = csub(mul_shoup(submod(xc.y, t1, ql), pinv_l, pinv_l_sh, ql) + half, ql);
+        // sources np (r) and np + 1 (the constant 1)
+#pragma unroll
+        for (int p = 0; p < NS; p++)
+            if (p == np) {
+                yl[p][0] = (uint32_t)r0 & M30, yh[p][0] = (uint32_t)(r0 >> 30);
+                yl[p][1] = (uint32_t)r1 & M30, yh[p][1] = (uint32_t)(r1 >> 30);
+            } else if (p == np + 1) {
+                yl[p][0] = yl[p][1] = 1;
+                yh[p][0] = yh[p][1] = 0;
+            }
+    }
+    u64 *dst = T + ct * Ts + (long)b * l * N + k;
+    for (int i = 0; i < l; i++) {
+        Acc4 s0, s1;
+        acc4_zero(s0);
+        acc4_zero(s1);
+        const ulonglong2 *cp = reinterpret_cast<const ulonglong2 *>(sc + i * NS);
+#pragma unroll
+        for (int p2 = 0; p2 < NS / 2; p2++) {
+            if (2 * p2 < ns) {
+                const ulonglong2 c = cp[p2];
+                acc4_mac(s0, yl[2 * p2][0], yh[2 * p2][0], c.x);
+                acc4_mac(s1, yl[2 * p2][1], yh[2 * p2][1], c.x);
+                acc4_mac(s0, yl[2 * p2 + 1][0], yh[2 * p2 + 1][0], c.y);
+                acc4_mac(s1, yl[2 * p2 + 1][1], yh[2 * p2 + 1][1], c.y);
+            }
+        }
+        stv2(dst + i * N, acc4_reduce(s0, tab.q[i], tab.br0[i], tab.br1[i]),
+             acc4_reduce(s1, tab.q[i], tab.br0[i], tab.br1[i]));
+    }
+}
 }  // namespace
 
 static inline unsigned chunks(int logn) { return (unsigned)((1L << logn) / TPB); }
 static inline unsigned chunks2(int logn) { return (unsigned)((1L << logn) / (2 * TPB)); }
 
 void k_modup(const Tab &tab, int logn, const u64 *dc, long dcs, u64 *ext, long exts, int n_ct, int nl, int np,
-             int nq_total, int alpha, const u64 *inv_hat, const u64 *inv_hat_sh, const u64 *hat, cudaStream_t st) {
+             int nq_total, int alpha, const u64 *hat, cudaStream_t st) {
     const int beta = (nl + alpha - 1) / alpha;
     if (alpha > MAXA) throw SecpeError{-1, "alpha > 16 not supported"};
     const dim3 grid(chunks2(logn), n_ct * beta);
 #define MODUP(A_)                                                                                          \
-    modup_kernel<A_><<<grid, TPB, 0, st>>>(tab, logn, dc, dcs, ext, exts, nl, np, nq_total, alpha, beta, inv_hat, \
-                                           inv_hat_sh, hat)
+    modup_kernel<A_><<<grid, TPB, 0, st>>>(tab, logn, dc, dcs, ext, exts, nl, np, nq_total, alpha, beta, hat)
     if (alpha <= 2)
         MODUP(2);
     else if (alpha <= 4)
@@ -212,41 +291,60 @@ void k_modup(const Tab &tab, int logn, const u64 *dc, long dcs, u64 *ext, long e
     LAUNCH_CHECK();
 }
 void k_ks_inner(const Tab &tab, int logn, const u64 *d, long ds, const u64 *ext, long exts, const u64 *key,
-                int nq_total, int np, u64 *acc, long accs, int n_ct, int nl, int alpha, cudaStream_t st) {
+                int nq_total, int np, u64 *acc, long accs, int n_ct, int nl, int alpha, cudaStream_t st,
+                const u64 *d01, long d01s, const u64 *pmod) {
     const int beta = (nl + alpha - 1) / alpha;
     const dim3 grid(chunks(logn), nl + np);
     // 128-bit accumulation of beta products < 2^124 each requires beta <= 16 per Barrett input bound
     // (2^125); larger dnum only occurs with small primes (toy: 40-bit, products < 2^80).
     if (beta <= 4)
         ks_inner_kernel<4><<<grid, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, n_ct, nl,
-                                                 alpha, beta);
+                                                 alpha, beta, d01, d01s, pmod);
     else if (beta <= 8)
         ks_inner_kernel<8><<<grid, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, n_ct, nl,
-                                                 alpha, beta);
+                                                 alpha, beta, d01, d01s, pmod);
     else if (beta <= 16)
         ks_inner_kernel<16><<<grid, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, n_ct, nl,
-                                                  alpha, beta);
+                                                  alpha, beta, d01, d01s, pmod);
     else if (beta <= 32)
         ks_inner_kernel<32><<<grid, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, n_ct, nl,
-                                                  alpha, beta);
+                                                  alpha, beta, d01, d01s, pmod);
     else
         throw SecpeError{-1, "dnum > 32 not supported"};
     LAUNCH_CHECK();
 }
-void k_moddown_conv(const Tab &tab, int logn, const u64 *acc, long accs, u64 *T, long Ts, int n_ct, int nl, int np,
-                    int nq_total, const u64 *ihp, const u64 *ihp_sh, const u64 *hat_p, cudaStream_t st) {
-    if (np > MAXA) throw SecpeError{-1, "more than 16 special primes not supported"};
+void k_moddown_conv(const Tab &tab, int logn, const u64 *acc, long accs, int ne, int row0, int ns, u64 *T,
+                    long Ts, int nt, int n_ct, const u64 *hatpk, int hstride, cudaStream_t st) {
+    if (ns > MAXA) throw SecpeError{-1, "more than 16 conversion sources not supported"};
     const dim3 grid(chunks2(logn), n_ct * 2);
-#define MDC(P_)                                                                                                  \
-    moddown_conv_kernel<P_><<<grid, TPB, 0, st>>>(tab, logn, acc, accs, T, Ts, nl, np, nq_total, ihp, ihp_sh, hat_p)
-    if (np <= 2)
+#define MDC(P_) \
+    moddown_conv_kernel<P_><<<grid, TPB, 0, st>>>(tab, logn, acc, accs, ne, row0, ns, T, Ts, nt, hatpk, hstride)
+    if (ns <= 2)
         MDC(2);
-    else if (np <= 4)
+    else if (ns <= 4)
         MDC(4);
-    else if (np <= 8)
+    else if (ns <= 8)
         MDC(8);
+    else if (ns <= 10)
+        MDC(10);
     else
         MDC(16);
 #undef MDC
+    LAUNCH_CHECK();
+}
+
+void k_rr_conv(const Tab &tab, int logn, const u64 *acc, long accs, int ne, int l, int np, u64 *T, long Ts, int n_ct,
+               const u64 *hatpk, const u64 *hl, u64 pinv_l, u64 pinv_l_sh, cudaStream_t st) {
+    if (np + 2 > MAXA) throw SecpeError{-1, "more than 14 special primes not supported"};
+    const dim3 grid(chunks2(logn), n_ct * 2);
+#define RRC(P_) \
+    rr_conv_kernel<P_><<<grid, TPB, 0, st>>>(tab, logn, acc, accs, ne, l, np, T, Ts, hatpk, hl, pinv_l, pinv_l_sh)
+    if (np + 2 <= 4)
+        RRC(4);
+    else if (np + 2 <= 10)
+        RRC(10);
+    else
+        RRC(16);
+#undef RRC
     LAUNCH_CHECK();
 }

@@ -25,10 +25,43 @@
 
 namespace {
 
+#ifndef NTT_MINB
+#define NTT_MINB 3  // resident CTAs per SM the register allocation targets (measured: 3 ~ 4 > 2)
+#endif
+#ifndef NTT_APPROX_HI
+#define NTT_APPROX_HI 1  // approximate Shoup quotient in the butterflies (measured: inverse -4%)
+#endif
 constexpr int RB = 4;        // bits held per thread
 constexpr int NV = 1 << RB;  // values per thread
 constexpr int SC = 16;       // columns per CTA in strided passes (16 x 8 B = one 128-B line)
 constexpr int CT = 256;      // threads per CTA in contiguous passes
+
+#if NTT_APPROX_HI
+// floor(y s / 2^64) - delta, delta in {0, 1}: the yl*sl partial product is dropped
+__device__ __forceinline__ u64 mulhi_approx(u64 y, u64 s) {
+    const uint32_t yl = (uint32_t)y, yh = (uint32_t)(y >> 32), sl = (uint32_t)s, sh = (uint32_t)(s >> 32);
+    u64 r;
+    asm("{\n\t.reg .u32 t0, t1, m0, m1, c;\n\t"
+        "mul.lo.u32 t0, %1, %4;\n\t"
+        "mul.hi.u32 t1, %1, %4;\n\t"
+        "mad.lo.cc.u32 m0, %2, %3, t0;\n\t"
+        "madc.hi.cc.u32 m1, %2, %3, t1;\n\t"
+        "addc.u32 c, 0, 0;\n\t"
+        "mov.b64 %0, {m1, c};\n\t"
+        "mad.wide.u32 %0, %1, %3, %0;\n\t"
+        "}"
+        : "=l"(r)
+        : "r"(yh), "r"(yl), "r"(sh), "r"(sl));
+    return r;
+}
+// T = y w - qhat' q in [0, 3q)
+__device__ __forceinline__ u64 shoup_bfly(u64 y, u64 w, u64 wsh, u64 q) { return y * w - mulhi_approx(y, wsh) * q; }
+// forward: corrected stages fold x >= 8q (inputs < 14q), outputs < 11q; uncorrected: inputs < 11q -> < 14q
+constexpr int FWD_FOLD = 8, FWD_T = 3;
+#else
+__device__ __forceinline__ u64 shoup_bfly(u64 y, u64 w, u64 wsh, u64 q) { return mul_shoup_lazy(y, w, wsh, q); }
+constexpr int FWD_FOLD = 4, FWD_T = 2;
+#endif
 
 // Forward CT butterfly, lazy every other stage: T = y w in [0, 2q); x' = X + T, y' = X - T + 2q.
 // Uncorrected stages (even global stage) take inputs < 6q (outputs < 8q); corrected stages (odd)
@@ -36,16 +69,18 @@ constexpr int CT = 256;      // threads per CTA in contiguous passes
 template <bool CORR>
 __device__ __forceinline__ void bfly_ct(u64 &x, u64 &y, u64 w, u64 wsh, u64 q, u64 q2) {
     u64 X = x;
-    if (CORR) X = X >= 2 * q2 ? X - 2 * q2 : X;
-    u64 T = mul_shoup_lazy(y, w, wsh, q);
+    if (CORR) X = X >= FWD_FOLD * q ? X - FWD_FOLD * q : X;
+    u64 T = shoup_bfly(y, w, wsh, q);
     x = X + T;
-    y = X - T + q2;
+    y = X - T + FWD_T * q;
 }
+// Inverse GS butterfly; values stay < 2q (exact Shoup) or < 4q (approximate quotient, T < 3q)
 __device__ __forceinline__ void bfly_gs(u64 &x, u64 &y, u64 w, u64 wsh, u64 q, u64 q2) {
+    constexpr int B = NTT_APPROX_HI ? 4 : 2;
     u64 X = x, Y = y;
     u64 T = X + Y;
-    x = T >= q2 ? T - q2 : T;
-    y = mul_shoup_lazy(X - Y + q2, w, wsh, q);
+    x = T >= B * q ? T - B * q : T;
+    y = shoup_bfly(X - Y + B * q, w, wsh, q);
 }
 
 // local index of held value v of thread tau when the held bits start at LO
@@ -235,7 +270,11 @@ __global__ void __launch_bounds__(CT, MINB) ntt_contig(PassArgs a) {
     do_round<S, INV, 1, true, LOGN>(v, tau, g, tw, q, q2);
     if (!INV) {
 #pragma unroll
-        for (int k = 0; k < NV; k++) v[k] = csub(csub(csub(v[k], 2 * q2), q2), q);  // < 6q -> [0, q)
+        for (int k = 0; k < NV; k++) {
+            u64 x = v[k];
+            if (NTT_APPROX_HI) x = csub(x, 8 * q);  // < 11q
+            v[k] = csub(csub(csub(x, 2 * q2), q2), q);  // < 8q -> [0, q)
+        }
         // no barrier: each thread rewrites exactly the words it read for round 1
 #pragma unroll
         for (int k = 0; k < NV; k++) smg[padr(held<LO1>(tau, k))] = v[k];
@@ -294,15 +333,6 @@ void max_smem_carveout(K kern) {
     }
 }
 
-int g_minb = -1;  // occupancy target (development switch SECPE_NTT_MINB = 3 | 4)
-int minb() {
-    if (g_minb < 0) {
-        const char *e = getenv("SECPE_NTT_MINB");
-        g_minb = (e && atoi(e) == 3) ? 3 : 4;
-    }
-    return g_minb;
-}
-
 template <int LOGN, bool INV, int IN, int MINB>
 void launch_strided_m(const PassArgs &a, int rows, cudaStream_t st) {
     constexpr int S = LOGN / 2;
@@ -319,17 +349,11 @@ void launch_contig_m(const PassArgs &a, int rows, cudaStream_t st) {
 }
 template <int LOGN, bool INV, int IN>
 void launch_strided(const PassArgs &a, int rows, cudaStream_t st) {
-    if (minb() == 3)
-        launch_strided_m<LOGN, INV, IN, 3>(a, rows, st);
-    else
-        launch_strided_m<LOGN, INV, IN, 4>(a, rows, st);
+    launch_strided_m<LOGN, INV, IN, NTT_MINB>(a, rows, st);
 }
 template <int LOGN, bool INV, int IO>
 void launch_contig(const PassArgs &a, int rows, cudaStream_t st) {
-    if (minb() == 3)
-        launch_contig_m<LOGN, INV, IO, 3>(a, rows, st);
-    else
-        launch_contig_m<LOGN, INV, IO, 4>(a, rows, st);
+    launch_contig_m<LOGN, INV, IO, NTT_MINB>(a, rows, st);
 }
 
 template <int LOGN>

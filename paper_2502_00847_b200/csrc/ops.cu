@@ -74,7 +74,8 @@ __global__ void mul_poly_kernel(Tab tab, int logn, CRows a, const u64 *__restric
 }
 
 // grid.y = ct * nl + limb
-__global__ void tensor_kernel(Tab tab, int logn, CRows a, CRows b, u64 *__restrict__ d, long ds, int nl) {
+__global__ void tensor_kernel(Tab tab, int logn, CRows a, CRows b, u64 *__restrict__ d, long ds, int nl, CRows x,
+                              LimbConst C) {
     const int ct = blockIdx.y / nl, limb = blockIdx.y % nl;
     const u64 q = tab.q[limb], r0 = tab.br0[limb], r1 = tab.br1[limb];
     const long N = 1L << logn, P = (long)nl * N;
@@ -93,6 +94,15 @@ __global__ void tensor_kernel(Tab tab, int logn, CRows a, CRows b, u64 *__restri
     d1.y = barrett128(t, q, r0, r1);
     d2.x = mulmod(a1.x, b1.x, q, r0, r1);
     d2.y = mulmod(a1.y, b1.y, q, r0, r1);
+    if (x.p) {
+        const u64 *X = x.p + ct * x.cs;
+        const ulonglong2 x0 = ld2(X + k), x1 = ld2(X + x.ps + k);
+        const u64 c = C.c[limb], csh = C.csh[limb];
+        d0.x = addmod(d0.x, mul_shoup(x0.x, c, csh, q), q);
+        d0.y = addmod(d0.y, mul_shoup(x0.y, c, csh, q), q);
+        d1.x = addmod(d1.x, mul_shoup(x1.x, c, csh, q), q);
+        d1.y = addmod(d1.y, mul_shoup(x1.y, c, csh, q), q);
+    }
     st2(D + k, d0);
     st2(D + P + k, d1);
     st2(D + 2 * P + k, d2);
@@ -143,8 +153,10 @@ void k_mul_poly(const Tab &tab, int logn, CRows a, const u64 *b, RowsArg out, in
     mul_poly_kernel<<<grid_rows(logn, n_polys * lm.nl), TPB, 0, st>>>(tab, logn, a, b, out, lm);
     LAUNCH_CHECK();
 }
-void k_tensor(const Tab &tab, int logn, CRows a, CRows b, u64 *d, long ds, int n_ct, int nl, cudaStream_t st) {
-    tensor_kernel<<<grid_rows(logn, n_ct * nl), TPB, 0, st>>>(tab, logn, a, b, d, ds, nl);
+void k_tensor(const Tab &tab, int logn, CRows a, CRows b, u64 *d, long ds, int n_ct, int nl, cudaStream_t st,
+              CRows x, const LimbConst *C) {
+    static const LimbConst zero{};
+    tensor_kernel<<<grid_rows(logn, n_ct * nl), TPB, 0, st>>>(tab, logn, a, b, d, ds, nl, x, C ? *C : zero);
     LAUNCH_CHECK();
 }
 void k_automorph(int logn, CRows a, RowsArg out, int n_polys, int nl, u64 galois, cudaStream_t st) {

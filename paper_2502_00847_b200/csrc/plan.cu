@@ -77,17 +77,26 @@ struct Ev {
         c.log("MULC", lv, Lt, St, std::to_string((long long)C));
         return out;
     }
-    // St = NAN: natural scale (S_a S_b) / q_l
-    Val mul_ct(const Val &a, const Val &b, double St, int Lt) {
+    // a (x) b [+ lc x] relinearised and rescaled in one step (R11b); St = NAN: natural scale (S_a S_b) / q_l.
+    // The linear term uses C = rha(lc Delta_c), Delta_c = (S_t q_l) / S_x (R9, R13).
+    Val mul_ct(const Val &a, const Val &b, double St, int Lt, const Val *linx = nullptr, double lc = 0.0) {
         const int lv = Lt + 1;
         if (lv < 1) throw SecpeError{-2, "mul_ct: no level left"};
         Val ad = drop(a, lv), bd = drop(b, lv);
-        Val prod = fresh(lv, a.scale() * b.scale());
-        ev_mul_relin(c, k, ad.v, bd.v, prod.v);
         const double s = std::isnan(St) ? (a.scale() * b.scale()) / q(lv) : St;
         Val out = fresh(Lt, s);
-        ev_rescale(c, prod.v, out.v);
-        c.log("MULCT", lv, Lt, s, "");
+        if (linx) {
+            Val xd = drop(*linx, lv);
+            const double dc = (s * q(lv)) / linx->scale();
+            const double Cd = round_half_away(lc * dc);
+            if (!(std::fabs(Cd) < 4611686018427387904.0)) throw SecpeError{-6, "constant exceeds 2^62"};
+            const i64 C = (i64)Cd;
+            ev_mul_relin_rescale(c, k, ad.v, bd.v, &xd.v, C, out.v);
+            c.log("MULCT", lv, Lt, s, std::to_string((long long)C));
+        } else {
+            ev_mul_relin_rescale(c, k, ad.v, bd.v, nullptr, 0, out.v);
+            c.log("MULCT", lv, Lt, s, "");
+        }
         return out;
     }
     Val mul_mask(const Val &x, const std::vector<double> &mask, double St) {
@@ -127,10 +136,9 @@ struct Ev {
         Val x4 = deg >= 7 ? mul_ct(x2, x2, NAN, l - 2) : Val{};
         Val x8 = deg >= 15 ? mul_ct(x4, x4, NAN, l - 3) : Val{};
         auto A = [&](int i, double S, int L) {
+            // (c_{4i+3} x) x^2 + c_{4i+1} x: the linear term joins the product before its rescale (R13)
             Val inner = mul_const(x, cf[4 * i + 3], (S * q(L + 1)) / x2.scale(), L + 1);
-            Val prod = mul_ct(inner, x2, S, L);
-            Val lin = mul_const(x, cf[4 * i + 1], S, L);
-            return add(prod, lin);
+            return mul_ct(inner, x2, S, L, &x, cf[4 * i + 1]);
         };
         auto B = [&](int i, double S, int L) {
             Val hi = A(2 * i + 1, (S * q(L + 1)) / x4.scale(), L + 1);
@@ -161,10 +169,9 @@ struct Ev {
         Val s = sign(d, cfg, c.scale);
         const int Ls = s.level();
         Val g = mul_const(d, 0.5, (Sy * q(Ls)) / s.scale(), Ls);
-        Val t2 = mul_ct(g, s, Sy, Ls - 1);
         Val ry = add(r, y);
-        Val h = mul_const(ry, 0.5, Sy, Ls - 1);
-        return add(h, t2);
+        // (r - y)/2 Sign(r - y) + (r + y)/2: the half-sum joins the product before its rescale
+        return mul_ct(g, s, Sy, Ls - 1, &ry, 0.5);
     }
     // Algorithm 1 with the H1..H6 steps of DESIGN.md section 2
     Val argmax(const Val &in, const Layout &lay, const SignCfg &cfg) {

@@ -70,6 +70,10 @@ SIGS = {
                                       ctypes.POINTER(CCt)]),
     "secpe_drop": (ctypes.c_int, [vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.POINTER(CCt)]),
     "secpe_mul_relin": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.POINTER(CCt), ctypes.POINTER(CCt)]),
+    "secpe_mul_relin_rescale": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.POINTER(CCt), ctypes.c_int32,
+                                               ctypes.POINTER(CCt)]),
+    "secpe_rotate_batch": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.c_int32,
+                                          ctypes.POINTER(CCt)]),
     "secpe_rescale": (ctypes.c_int, [vp, ctypes.POINTER(CCt), ctypes.POINTER(CCt)]),
     "secpe_rotate": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.POINTER(CCt)]),
     "secpe_sign_poly": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.POINTER(SignCfg), ctypes.c_double,
@@ -92,10 +96,11 @@ def lib():
     """Load libsecpe.so (built in-tree by paper_2502_00847_b200.build); raise if it is missing."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
+        path = os.environ.get("SECPE_LIB", LIB_PATH)  # development: alternative in-tree build variant
+        if not os.path.exists(path):
             raise RuntimeError("libsecpe.so not built: run `python -m paper_2502_00847_b200.build` "
                                "(there is no CPU fallback)")
-        L = ctypes.CDLL(LIB_PATH)
+        L = ctypes.CDLL(path)
         for name, (res, args) in SIGS.items():
             f = getattr(L, name)
             f.restype = res
@@ -333,6 +338,28 @@ class Context:
         ca, cb, co = a.c(), b.c(), out.c()
         _chk(lib().secpe_mul_relin(self.h, keys.h, ctypes.byref(ca), ctypes.byref(cb), ctypes.byref(co)))
         out.level, out.scale = co.level, co.scale
+        return out
+
+    def _batch(self, ct):
+        return (CCt * ct.n)(*[ct.c(i) for i in range(ct.n)])
+
+    def mul_relin_rescale(self, keys, a, b, out=None):
+        """Batched a (x) b relinearised and rescaled in one step (reading R11b); a, b batch Cts."""
+        if out is None:
+            out = self.new_ct(a.level - 1, a.n)
+        ca, cb = self._batch(a), self._batch(b)
+        co = (CCt * a.n)(*[CCt(ctypes.cast(out.t[i].data_ptr(), u64p), a.level - 1, 0.0) for i in range(a.n)])
+        _chk(lib().secpe_mul_relin_rescale(self.h, keys.h, ca, cb, a.n, co))
+        out.level, out.scale = co[0].level, co[0].scale
+        return out
+
+    def rotate_batch(self, keys, a, steps, out=None):
+        if out is None:
+            out = self.new_ct(a.level, a.n)
+        ca = self._batch(a)
+        co = (CCt * a.n)(*[CCt(ctypes.cast(out.t[i].data_ptr(), u64p), a.level, 0.0) for i in range(a.n)])
+        _chk(lib().secpe_rotate_batch(self.h, keys.h, ca, a.n, steps, co))
+        out.level, out.scale = co[0].level, co[0].scale
         return out
 
     def rescale(self, a):

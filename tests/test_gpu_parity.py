@@ -165,6 +165,14 @@ def test_ops_bit_exact_toy(toy_env):
     assert chk(mr, ev.mul_relin(ko, a, b))
     mc = g.mul_const(ga, 0.7, prm.scale, 4)
     assert chk(mc, ev.mul_const(a, 0.7, prm.scale, 4))
+    # fused relinearise-and-rescale (bit-identical to mul_relin then rescale), batched: (a, b), (b, a)
+    ab = P.secpe.Ct(torch.cat([ga.t, gb.t]), ga.level, ga.scale)
+    ba = P.secpe.Ct(torch.cat([gb.t, ga.t]), ga.level, ga.scale)
+    rr = g.mul_relin_rescale(kg, ab, ba)
+    want = ev.rescale(ev.mul_relin(ko, a, b))
+    assert rr.level == a.level - 1 and rr.scale == want.scale
+    assert np.array_equal(P.down(rr, 0), want.data) and np.array_equal(P.down(rr, 1), want.data)
+    assert np.abs(g.decrypt(kg, rr, 1) - z1 * z2).max() < 2 ** -10
     for s in (1, -1, 3, 64):
         assert chk(g.rotate(kg, ga, s), ev.rotate_raw(ko, a, s))
     lay = dict(synth.LAYOUTS["toy"], queries=16)
@@ -191,6 +199,12 @@ def test_ops_bit_exact_ks_config(S):
     assert np.abs(P.gpu.decrypt(kg, mg) - z1 * z2).max() < 2 ** -10
     ro = ev.rotate_raw(ko, a, 1)
     assert np.array_equal(P.down(g.rotate(kg, ga, 1)), ro.data)
+    # batched rotation and relinearise-and-rescale at full size (N = 2^16, 24 limbs)
+    rb = g.rotate_batch(kg, P.secpe.Ct(torch.cat([ga.t, ga.t]), ga.level, ga.scale), 1)
+    assert np.array_equal(P.down(rb, 1), ro.data)
+    rr = g.mul_relin_rescale(kg, ga, gb)
+    assert np.array_equal(P.down(rr), mo.data)
+    assert np.abs(g.decrypt(kg, rr) - z1 * z2).max() < 2 ** -10
 
 
 def test_sign_poly_bit_exact(toy_env):

@@ -302,6 +302,10 @@ def test_ops_against_slots(toy):
     assert np.abs(ev.decrypt(keys, ev.sub_raw(a, b)).real - (z1 - z2)).max() < tol
     m = ev.rescale(ev.mul_relin(keys, a, b))
     assert np.abs(ev.decrypt(keys, m).real - z1 * z2).max() < tol
+    # planned product with a linear term joined before the rescale (R13): a b + 0.25 a
+    f = ev.mul_ct(keys, a, b, toy.scale, a.level - 1, lin=(a, 0.25))
+    assert f.level == a.level - 1 and f.scale == toy.scale
+    assert np.abs(ev.decrypt(keys, f).real - (z1 * z2 + 0.25 * z1)).max() < tol
     for s in (1, -1, 3):
         r = ev.rotate_raw(keys, a, s)
         assert np.abs(ev.decrypt(keys, r).real - np.roll(z1, -s)).max() < tol
