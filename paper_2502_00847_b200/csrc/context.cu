@@ -234,10 +234,18 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
         for (long k = 0; k < N; k++) {
             const unsigned b = brv((unsigned)k, logn);
             const size_t o = (size_t)i * N + k;
-            tw[2 * o] = pw[b];
-            tw[2 * o + 1] = h_shoup(pw[b], qi);
-            itw[2 * o] = ipw[b];
-            itw[2 * o + 1] = h_shoup(ipw[b], qi);
+            if (qi < (1ULL << 46)) {
+                // exact-FP64 butterflies (ntt.cu FpA): dense doubles w in the first N words of the
+                // prime's 2N-word region
+                const double w = (double)pw[b], iw = (double)ipw[b];
+                std::memcpy(&tw[2 * (size_t)i * N + k], &w, 8);
+                std::memcpy(&itw[2 * (size_t)i * N + k], &iw, 8);
+            } else {
+                tw[2 * o] = pw[b];
+                tw[2 * o + 1] = h_shoup(pw[b], qi);
+                itw[2 * o] = ipw[b];
+                itw[2 * o + 1] = h_shoup(ipw[b], qi);
+            }
         }
     }
     h_br0 = hr0;

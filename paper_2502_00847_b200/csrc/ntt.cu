@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace {
@@ -63,25 +64,112 @@ __device__ __forceinline__ u64 shoup_bfly(u64 y, u64 w, u64 wsh, u64 q) { return
 constexpr int FWD_FOLD = 4, FWD_T = 2;
 #endif
 
-// Forward CT butterfly, lazy every other stage: T = y w in [0, 2q); x' = X + T, y' = X - T + 2q.
-// Uncorrected stages (even global stage) take inputs < 6q (outputs < 8q); corrected stages (odd)
-// take inputs < 8q, fold X = x >= 4q ? x - 4q : x < 4q, outputs < 6q.  8q < 2^64 (q < 2^60).
-template <bool CORR>
-__device__ __forceinline__ void bfly_ct(u64 &x, u64 &y, u64 w, u64 wsh, u64 q, u64 q2) {
-    u64 X = x;
-    if (CORR) X = X >= FWD_FOLD * q ? X - FWD_FOLD * q : X;
-    u64 T = shoup_bfly(y, w, wsh, q);
-    x = X + T;
-    y = X - T + FWD_T * q;
-}
-// Inverse GS butterfly; values stay < 2q (exact Shoup) or < 4q (approximate quotient, T < 3q)
-__device__ __forceinline__ void bfly_gs(u64 &x, u64 &y, u64 w, u64 wsh, u64 q, u64 q2) {
-    constexpr int B = NTT_APPROX_HI ? 4 : 2;
-    u64 X = x, Y = y;
-    u64 T = X + Y;
-    x = T >= B * q ? T - B * q : T;
-    y = shoup_bfly(X - Y + B * q, w, wsh, q);
-}
+// ---------------------------------------------------------------------------------------------
+// Arithmetic policies.  Values travel in 64-bit registers; a row (one prime) uses one policy for
+// both passes, so the intermediate buffer between the passes holds that policy's representation.
+// ---------------------------------------------------------------------------------------------
+struct PrimeC {
+    u64 q;
+    double qd, qinv;
+};
+
+// Integer Shoup path (any prime < 2^60).  Forward CT, lazy every other stage: T = y w in [0, 3q)
+// (approximate quotient) or [0, 2q); x' = X + T, y' = X - T + FWD_T q.  Corrected stages (odd global
+// stage) fold X = x >= FWD_FOLD q ? x - FWD_FOLD q : x.  Inverse GS keeps values < 4q (< 2q exact).
+struct IntA {
+    template <bool CORR>
+    static __device__ __forceinline__ void ct(u64 &x, u64 &y, ulonglong2 w, const PrimeC &P) {
+        const u64 q = P.q;
+        u64 X = x;
+        if (CORR) X = X >= FWD_FOLD * q ? X - FWD_FOLD * q : X;
+        const u64 T = shoup_bfly(y, w.x, w.y, q);
+        x = X + T;
+        y = X - T + FWD_T * q;
+    }
+    template <bool RED>
+    static __device__ __forceinline__ void gs(u64 &x, u64 &y, ulonglong2 w, const PrimeC &P) {
+        constexpr int B = NTT_APPROX_HI ? 4 : 2;
+        const u64 q = P.q, X = x, Y = y, T = X + Y;
+        x = T >= B * q ? T - B * q : T;
+        y = shoup_bfly(X - Y + B * q, w.x, w.y, q);
+    }
+    static __device__ __forceinline__ u64 in(u64 x, const PrimeC &) { return x; }
+    // {w, Shoup companion} (16-byte interleaved table)
+    static __device__ __forceinline__ ulonglong2 twiddle(const ulonglong2 *tw, int i, const PrimeC &) {
+        return __ldg(tw + i);
+    }
+    // forward output (< 11q or < 6q) -> [0, q)
+    static __device__ __forceinline__ u64 out_fwd(u64 x, const PrimeC &P) {
+        const u64 q = P.q;
+        if (NTT_APPROX_HI) x = csub(x, 8 * q);
+        return csub(csub(csub(x, 4 * q), 2 * q), q);
+    }
+    // inverse output times a per-limb factor k (Shoup companion ksh) -> [0, q)
+    static __device__ __forceinline__ u64 out_scaled(u64 x, u64 k, u64 ksh, const PrimeC &P) {
+        return mul_shoup(x, k, ksh, P.q);
+    }
+};
+
+// Exact FP64 path (primes < 2^46, i.e. the 45-bit chain of configs[4]).  Values are signed integers
+// held exactly in IEEE doubles (|v| < 2^51).  w y mod q with w_q = RN(w / q):
+//   k = rint(y w_q) (fma with the 1.5 2^52 magic constant), (ph, pl) = TwoProduct(k, q),
+//   r = fma(y, w, -ph) - pl  =  y w - k q  exactly,  |r| <= 0.75 q.
+// Forward CT needs no corrections at all (|v| <= q + 16 * 0.75 q); inverse GS reduces the sum on
+// every other stage (|v| <= 4q).  All operations are on the FP64 pipe, which the integer path leaves
+// idle; the explicit _rn intrinsics keep the compiler from contracting or reassociating.
+constexpr double FP_MAGIC = 6755399441055744.0;  // 1.5 * 2^52
+constexpr double TWO52 = 4503599627370496.0;
+constexpr u64 FP_LIMIT = 1ULL << 46;
+struct FpA {
+    static __device__ __forceinline__ double D(u64 b) { return __longlong_as_double((long long)b); }
+    static __device__ __forceinline__ u64 B(double d) { return (u64)__double_as_longlong(d); }
+    static __device__ __forceinline__ double rint_(double x) { return __dsub_rn(__dadd_rn(x, FP_MAGIC), FP_MAGIC); }
+    static __device__ __forceinline__ double mm(double y, double w, double wq, double qd) {
+        const double k = __dsub_rn(__fma_rn(y, wq, FP_MAGIC), FP_MAGIC);
+        const double ph = __dmul_rn(k, qd);
+        const double pl = __fma_rn(k, qd, -ph);
+        return __dsub_rn(__fma_rn(y, w, -ph), pl);
+    }
+    // centred representative, |result| <= q/2 (for |x| < 2^51)
+    static __device__ __forceinline__ double red(double x, const PrimeC &P) {
+        const double k = rint_(__dmul_rn(x, P.qinv));
+        return __fma_rn(-k, P.qd, x);
+    }
+    template <bool CORR>
+    static __device__ __forceinline__ void ct(u64 &x, u64 &y, ulonglong2 w, const PrimeC &P) {
+        const double X = D(x), T = mm(D(y), D(w.x), D(w.y), P.qd);
+        x = B(__dadd_rn(X, T));
+        y = B(__dsub_rn(X, T));
+    }
+    template <bool RED>
+    static __device__ __forceinline__ void gs(u64 &x, u64 &y, ulonglong2 w, const PrimeC &P) {
+        const double X = D(x), Y = D(y);
+        double s = __dadd_rn(X, Y);
+        if (RED) s = red(s, P);
+        y = B(mm(__dsub_rn(X, Y), D(w.x), D(w.y), P.qd));
+        x = B(s);
+    }
+    // dense table of doubles w (the prime's 2N-word table region holds N doubles); w_q = RN(w RN(1/q))
+    // has relative error <= 2^-52, so |y w_q - y w / q| <= 13 q 2^-52 < 0.2 and |r| <= 0.7 q still holds
+    static __device__ __forceinline__ ulonglong2 twiddle(const ulonglong2 *tw, int i, const PrimeC &P) {
+        const double w = __ldg(reinterpret_cast<const double *>(tw) + i);
+        return make_ulonglong2(B(w), B(__dmul_rn(w, P.qinv)));
+    }
+    // canonical integer (< 2^52) -> exact double
+    static __device__ __forceinline__ u64 in(u64 x, const PrimeC &) {
+        return B(__dsub_rn(D(x | 0x4330000000000000ULL), TWO52));
+    }
+    static __device__ __forceinline__ u64 canon(double t, const PrimeC &P) {
+        t = red(t, P);
+        if (t < 0) t = __dadd_rn(t, P.qd);
+        return B(__dadd_rn(t, TWO52)) & ((1ULL << 52) - 1);
+    }
+    static __device__ __forceinline__ u64 out_fwd(u64 x, const PrimeC &P) { return canon(D(x), P); }
+    static __device__ __forceinline__ u64 out_scaled(u64 x, u64 k, u64, const PrimeC &P) {
+        const double kd = D(in(k, P)), kq = __dmul_rn(kd, P.qinv);
+        return canon(mm(D(x), kd, kq, P.qd), P);
+    }
+};
 
 // local index of held value v of thread tau when the held bits start at LO
 template <int LO>
@@ -107,9 +195,9 @@ struct Rnd {
 // local index r, paired bit b: tw[2^sg + (g << (S-1-b)) + (r >> (b+1))] where sg is the global
 // stage (strided: S-1-b, g = 0; contiguous: LOGN-1-b, g = group).  It depends only on the held bits
 // above the paired one, so each distinct twiddle is loaded once.
-template <int S, bool INV, int K, bool CONTIG, int LOGN>
-__device__ __forceinline__ void do_round(u64 (&v)[NV], int tau, int g, const ulonglong2 *__restrict__ tw, u64 q,
-                                         u64 q2) {
+template <int S, bool INV, int K, bool CONTIG, int LOGN, class A>
+__device__ __forceinline__ void do_round(u64 (&v)[NV], int tau, int g, const ulonglong2 *__restrict__ tw,
+                                         const PrimeC &P) {
     using R = Rnd<S, INV>;
     constexpr int LO = R::lo(K);
 #pragma unroll
@@ -122,16 +210,20 @@ __device__ __forceinline__ void do_round(u64 (&v)[NV], int tau, int g, const ulo
         for (int u = 0; u < (1 << (RB - 1 - vb)); u++) {
             const int v0b = u << (vb + 1);
             const int r = held<LO>(tau, v0b);
-            const ulonglong2 w = __ldg(tw + ((1 << sg) + gterm + (r >> (b + 1))));
+            const ulonglong2 w = A::twiddle(tw, (1 << sg) + gterm + (r >> (b + 1)), P);
 #pragma unroll
             for (int l = 0; l < (1 << vb); l++) {
                 const int i0 = v0b | l, i1 = i0 | (1 << vb);
-                if (INV)
-                    bfly_gs(v[i0], v[i1], w.x, w.y, q, q2);
-                else if (sg & 1)
-                    bfly_ct<true>(v[i0], v[i1], w.x, w.y, q, q2);
-                else
-                    bfly_ct<false>(v[i0], v[i1], w.x, w.y, q, q2);
+                if (INV) {
+                    if (sg & 1)
+                        A::template gs<false>(v[i0], v[i1], w, P);
+                    else
+                        A::template gs<true>(v[i0], v[i1], w, P);
+                } else if (sg & 1) {
+                    A::template ct<true>(v[i0], v[i1], w, P);
+                } else {
+                    A::template ct<false>(v[i0], v[i1], w, P);
+                }
             }
         }
     }
@@ -152,21 +244,17 @@ struct PassArgs {
 // strided pass: group = column c, elements c + (N >> S) r, SC columns per CTA
 //   forward: stages 0..S-1 (first pass);  inverse: stages S-1..0 (last pass, * N^{-1})
 // ---------------------------------------------------------------------------------------------
-template <int LOGN, bool INV, int IN, int MINB>
-__global__ void __launch_bounds__(SC *(1 << (LOGN / 2 - RB)), MINB)
-    ntt_strided(PassArgs a) {
-    constexpr int S = LOGN / 2, G = 1 << S;
+template <int LOGN, bool INV, int IN, class A>
+__device__ __forceinline__ void strided_body(const PassArgs &a, u64 *sm, int poly, int limb, int prime,
+                                             const PrimeC &P) {
+    constexpr int S = LOGN / 2;
     constexpr long N = 1L << LOGN;
     constexpr int STRIDE = (int)(N >> S);
     using R = Rnd<S, INV>;
-    __shared__ u64 sm[G * SC];
-    const int nl = a.lm.nl;
-    const int poly = blockIdx.y / nl, limb = blockIdx.y % nl;
-    const int prime = prime_of(a.lm, limb);
     const int cl = threadIdx.x % SC, tau = threadIdx.x / SC;
     const int c = blockIdx.x * SC + cl;
     u64 *base = a.d.p + poly_off(a.d.cs, a.d.ps, poly) + limb * N + c;
-    const u64 q = a.tab.q[prime], q2 = 2 * q;
+    const u64 q = P.q;
     const ulonglong2 *tw = (INV ? a.tab.itw2 : a.tab.tw2) + prime * N;
     u64 v[NV];
     constexpr int LO0 = R::lo(0);
@@ -178,20 +266,23 @@ __global__ void __launch_bounds__(SC *(1 << (LOGN / 2 - RB)), MINB)
 #pragma unroll
         for (int k = 0; k < NV; k++) {
             const u64 r = csub(src[STRIDE * held<LO0>(tau, k)] + hl, ql);
-            v[k] = submod(hi, mul_shoup(r, 1, one_sh, q), q);
+            v[k] = A::in(submod(hi, mul_shoup(r, 1, one_sh, q), q), P);
         }
+    } else if (!INV) {
+#pragma unroll
+        for (int k = 0; k < NV; k++) v[k] = A::in(base[STRIDE * held<LO0>(tau, k)], P);
     } else {
 #pragma unroll
-        for (int k = 0; k < NV; k++) v[k] = base[STRIDE * held<LO0>(tau, k)];
+        for (int k = 0; k < NV; k++) v[k] = base[STRIDE * held<LO0>(tau, k)];  // intermediate representation
     }
-    do_round<S, INV, 0, false, LOGN>(v, tau, 0, tw, q, q2);
+    do_round<S, INV, 0, false, LOGN, A>(v, tau, 0, tw, P);
     if constexpr (R::NR > 1) {
 #pragma unroll
         for (int k = 0; k < NV; k++) sm[held<R::lo(0)>(tau, k) * SC + cl] = v[k];
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < NV; k++) v[k] = sm[held<R::lo(1)>(tau, k) * SC + cl];
-        do_round<S, INV, 1, false, LOGN>(v, tau, 0, tw, q, q2);
+        do_round<S, INV, 1, false, LOGN, A>(v, tau, 0, tw, P);
     }
     static_assert(R::NR <= 2, "strided pass: at most two rounds");
     constexpr int LOL = R::lo(R::NR - 1);
@@ -200,10 +291,32 @@ __global__ void __launch_bounds__(SC *(1 << (LOGN / 2 - RB)), MINB)
         const u64 ni = a.f.k ? a.f.k[limb] : a.tab.ninv[prime];
         const u64 nish = a.f.k ? a.f.ksh[limb] : a.tab.ninvsh[prime];
 #pragma unroll
-        for (int k = 0; k < NV; k++) v[k] = mul_shoup(v[k], ni, nish, q);
+        for (int k = 0; k < NV; k++) v[k] = A::out_scaled(v[k], ni, nish, P);
     }
 #pragma unroll
     for (int k = 0; k < NV; k++) base[STRIDE * held<LOL>(tau, k)] = v[k];
+}
+
+__device__ __forceinline__ PrimeC prime_consts(const Tab &tab, int prime) {
+    PrimeC P;
+    P.q = tab.q[prime];
+    P.qd = (double)P.q;
+    P.qinv = 1.0 / P.qd;
+    return P;
+}
+
+template <int LOGN, bool INV, int IN, int MINB>
+__global__ void __launch_bounds__(SC *(1 << (LOGN / 2 - RB)), MINB)
+    ntt_strided(PassArgs a) {
+    __shared__ u64 sm[(1 << (LOGN / 2)) * SC];
+    const int nl = a.lm.nl;
+    const int poly = blockIdx.y / nl, limb = blockIdx.y % nl;
+    const int prime = prime_of(a.lm, limb);
+    const PrimeC P = prime_consts(a.tab, prime);
+    if (P.q < FP_LIMIT)
+        strided_body<LOGN, INV, IN, FpA>(a, sm, poly, limb, prime, P);
+    else
+        strided_body<LOGN, INV, IN, IntA>(a, sm, poly, limb, prime, P);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -220,21 +333,18 @@ struct ContigCfg {
 };
 __device__ __forceinline__ int padr(int r) { return r + (r >> 4); }
 
-template <int LOGN, bool INV, int IO, int MINB>
-__global__ void __launch_bounds__(CT, MINB) ntt_contig(PassArgs a) {
+template <int LOGN, bool INV, int IO, class A>
+__device__ __forceinline__ void contig_body(const PassArgs &a, u64 *sm, int poly, int limb, int prime,
+                                            const PrimeC &P) {
     // IO: inverse -> IN_PLAIN | IN_SRC (first pass reads f.src rows);  forward -> OUT_* epilogue
     using CF = ContigCfg<LOGN>;
     constexpr int S = CF::S, G = CF::G, TPG = CF::TPG, CG = CF::CG, PITCH = CF::PITCH;
     constexpr long N = 1L << LOGN;
     using R = Rnd<S, INV>;
     static_assert(R::NR == 2, "contiguous pass: two rounds");
-    __shared__ __align__(16) u64 sm[CG * PITCH];
-    const int nl = a.lm.nl;
-    const int poly = blockIdx.y / nl, limb = blockIdx.y % nl;
-    const int prime = prime_of(a.lm, limb);
     const long boff = limb * N + (long)blockIdx.x * CG * G;  // tile offset inside the polynomial
     u64 *blk = a.d.p + poly_off(a.d.cs, a.d.ps, poly) + boff;
-    const u64 q = a.tab.q[prime], q2 = 2 * q;
+    const u64 q = P.q;
     const ulonglong2 *tw = (INV ? a.tab.itw2 : a.tab.tw2) + prime * N;
     const int gl = threadIdx.x / TPG, tau = threadIdx.x % TPG;
     const int g = blockIdx.x * CG + gl;
@@ -245,7 +355,7 @@ __global__ void __launch_bounds__(CT, MINB) ntt_contig(PassArgs a) {
         // forward round 0 holds r = 16 k + tau: lane-consecutive, load straight from global
         const u64 *src = blk + gl * G;
 #pragma unroll
-        for (int k = 0; k < NV; k++) v[k] = src[held<LO0>(tau, k)];
+        for (int k = 0; k < NV; k++) v[k] = src[held<LO0>(tau, k)];  // intermediate representation
     } else {
         const u64 *sp = (IO == IN_SRC) ? a.f.src.p + poly_off(a.f.src.cs, a.f.src.ps, poly) + boff : blk;
         const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(sp);
@@ -253,28 +363,24 @@ __global__ void __launch_bounds__(CT, MINB) ntt_contig(PassArgs a) {
         for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
             const ulonglong2 x = src[i];
             const int e = 2 * i, gg = e / G, r = e % G;
-            sm[gg * PITCH + padr(r)] = x.x;
-            sm[gg * PITCH + padr(r + 1)] = x.y;
+            sm[gg * PITCH + padr(r)] = A::in(x.x, P);
+            sm[gg * PITCH + padr(r + 1)] = A::in(x.y, P);
         }
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < NV; k++) v[k] = smg[padr(held<LO0>(tau, k))];
         // no barrier: each thread rewrites exactly the words it just read (same layout)
     }
-    do_round<S, INV, 0, true, LOGN>(v, tau, g, tw, q, q2);
+    do_round<S, INV, 0, true, LOGN, A>(v, tau, g, tw, P);
 #pragma unroll
     for (int k = 0; k < NV; k++) smg[padr(held<LO0>(tau, k))] = v[k];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < NV; k++) v[k] = smg[padr(held<LO1>(tau, k))];
-    do_round<S, INV, 1, true, LOGN>(v, tau, g, tw, q, q2);
+    do_round<S, INV, 1, true, LOGN, A>(v, tau, g, tw, P);
     if (!INV) {
 #pragma unroll
-        for (int k = 0; k < NV; k++) {
-            u64 x = v[k];
-            if (NTT_APPROX_HI) x = csub(x, 8 * q);  // < 11q
-            v[k] = csub(csub(csub(x, 2 * q2), q2), q);  // < 8q -> [0, q)
-        }
+        for (int k = 0; k < NV; k++) v[k] = A::out_fwd(v[k], P);
         // no barrier: each thread rewrites exactly the words it read for round 1
 #pragma unroll
         for (int k = 0; k < NV; k++) smg[padr(held<LO1>(tau, k))] = v[k];
@@ -322,6 +428,20 @@ __global__ void __launch_bounds__(CT, MINB) ntt_contig(PassArgs a) {
 #pragma unroll
         for (int k = 0; k < NV; k++) dst[held<LO1>(tau, k)] = v[k];
     }
+}
+
+template <int LOGN, bool INV, int IO, int MINB>
+__global__ void __launch_bounds__(CT, MINB) ntt_contig(PassArgs a) {
+    using CF = ContigCfg<LOGN>;
+    __shared__ __align__(16) u64 sm[CF::CG * CF::PITCH];
+    const int nl = a.lm.nl;
+    const int poly = blockIdx.y / nl, limb = blockIdx.y % nl;
+    const int prime = prime_of(a.lm, limb);
+    const PrimeC P = prime_consts(a.tab, prime);
+    if (P.q < FP_LIMIT)
+        contig_body<LOGN, INV, IO, FpA>(a, sm, poly, limb, prime, P);
+    else
+        contig_body<LOGN, INV, IO, IntA>(a, sm, poly, limb, prime, P);
 }
 
 template <typename K>

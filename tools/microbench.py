@@ -51,6 +51,19 @@ def bench_ntt(reps, stream, out):
                       alg_gbs_fwd=16 * N * limbs / (ms_f / 1000) / 1e9, alg_gbs_inv=16 * N * limbs / (ms_i / 1000) / 1e9)
 
 
+def bench_ntt45(reps, stream, out):
+    """configs[4] chain: 64 polys x 29 limbs of the ~2^45 primes q_1..q_29 (exact-FP64 butterflies)."""
+    ctx = secpe.Context(synth.PARAM_SETS["argmax"], stream=stream.cuda_stream)
+    P, L, N = 64, 29, ctx.N
+    x = torch.from_numpy(synth.uniform_residues(2002, ctx.q[1:30], P, ctx.logn)).cuda()
+    ms_f = timeit(lambda: ctx.ntt(x, 1, L), reps, stream)
+    ms_i = timeit(lambda: ctx.ntt(x, 1, L, inverse=True), reps, stream)
+    limbs = P * L
+    out["ntt45"] = dict(fwd_ms=ms_f, inv_ms=ms_i, us_per_limb_fwd=1000 * ms_f / limbs,
+                        us_per_limb_inv=1000 * ms_i / limbs,
+                        alg_gbs_fwd=16 * N * limbs / (ms_f / 1000) / 1e9, alg_gbs_inv=16 * N * limbs / (ms_i / 1000) / 1e9)
+
+
 def bench_ks(reps, stream, out):
     ctx = secpe.Context(synth.PARAM_SETS["ks"], stream=stream.cuda_stream)
     keys = ctx.keygen(synth.KEY_SEED_BASE + 3, [1])
@@ -101,6 +114,8 @@ def main():
     out = {}
     if "ntt" in a.what:
         bench_ntt(a.reps, stream, out)
+    if "ntt45" in a.what:
+        bench_ntt45(a.reps, stream, out)
     if "relin" in a.what or "rot" in a.what:
         bench_ks(a.reps, stream, out)
     if "argmax" in a.what:
