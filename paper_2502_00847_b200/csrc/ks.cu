@@ -92,8 +92,78 @@ __global__ void __launch_bounds__(TPB) modup_kernel(Tab tab, int logn, const u64
     }
 }
 
-// grid: x = coefficient chunks, y = extended limb e; loops over the n_ct ciphertexts so each key
-// word is read from HBM once per launch (held in registers across the batch).  MAXB >= beta.
+// Key inner product (R10).  grid: x = coefficient chunks (two coefficients per thread, 16-byte vectors),
+// y = extended limb e.  Loops over the n_ct ciphertexts so each key word is read from HBM once per
+// launch (held in registers across the batch); the next ciphertext's inputs are loaded before the
+// current one is reduced (two register sets), so twice the bytes are in flight.  MAXB = beta exactly
+// (beta <= 4); larger dnum uses the scalar ks_inner_kernel below.
+template <int MAXB>
+struct KsIn {
+    ulonglong2 x[MAXB], d0, d1;
+};
+template <int MAXB>
+__device__ __forceinline__ void ks_load(KsIn<MAXB> &in, int c, const u64 *__restrict__ d, long ds,
+                                        const u64 *__restrict__ ext, long exts, int e, int jd, int ne, int nl,
+                                        int beta, long N, long k, const u64 *__restrict__ d01, long d01s) {
+#pragma unroll
+    for (int j = 0; j < MAXB; j++)
+        if (j < beta)
+            in.x[j] = ldv2((j == jd) ? d + c * ds + e * N + k : ext + c * exts + ((long)j * ne + e) * N + k);
+    if (d01 && e < nl) {
+        in.d0 = ldv2(d01 + c * d01s + e * N + k);
+        in.d1 = ldv2(d01 + c * d01s + ((long)nl + e) * N + k);
+    }
+}
+
+template <int MAXB>
+__global__ void __launch_bounds__(TPB) ks_inner_vec_kernel(Tab tab, int logn, const u64 *__restrict__ d, long ds,
+                                                       const u64 *__restrict__ ext, long exts,
+                                                       const u64 *__restrict__ key, int nq_total, int np,
+                                                       u64 *__restrict__ acc, long accs, int n_ct, int nl, int alpha,
+                                                       int beta, const u64 *__restrict__ d01, long d01s,
+                                                       const u64 *__restrict__ pmod) {
+    const int e = blockIdx.y;
+    const long N = 1L << logn;
+    const long k = 2L * ((long)blockIdx.x * TPB + threadIdx.x);
+    const int ne = nl + np, nk = nq_total + np;
+    const int pr = e < nl ? e : nq_total + (e - nl);
+    const u64 q = tab.q[pr], r0 = tab.br0[pr], r1 = tab.br1[pr];
+    ulonglong2 kb[MAXB], ka[MAXB];
+#pragma unroll
+    for (int j = 0; j < MAXB; j++)
+        if (j < beta) {
+            kb[j] = ldv2(key + (((long)j * 2 + 0) * nk + pr) * N + k);
+            ka[j] = ldv2(key + (((long)j * 2 + 1) * nk + pr) * N + k);
+        }
+    const int jd = e < nl ? e / alpha : -1;  // digit containing e (Q limbs only)
+    const bool add = d01 && e < nl;          // relinearise-and-rescale: x_b = acc_b + [P]_{q_e} d_b on Q limbs
+    const u64 pm = add ? pmod[e] : 0;
+    KsIn<MAXB> cur, nxt;
+    ks_load<MAXB>(cur, 0, d, ds, ext, exts, e, jd, ne, nl, beta, N, k, d01, d01s);
+    for (int c = 0; c < n_ct; c++) {
+        if (c + 1 < n_ct) ks_load<MAXB>(nxt, c + 1, d, ds, ext, exts, e, jd, ne, nl, beta, N, k, d01, d01s);
+        U128 s0{0, 0}, s1{0, 0}, t0{0, 0}, t1{0, 0};  // (poly 0, poly 1) x (coefficient k, k + 1)
+#pragma unroll
+        for (int j = 0; j < MAXB; j++)
+            if (j < beta) {
+                mac_wide(s0, cur.x[j].x, kb[j].x);
+                mac_wide(t0, cur.x[j].y, kb[j].y);
+                mac_wide(s1, cur.x[j].x, ka[j].x);
+                mac_wide(t1, cur.x[j].y, ka[j].y);
+            }
+        if (add) {
+            mac_wide(s0, cur.d0.x, pm);
+            mac_wide(t0, cur.d0.y, pm);
+            mac_wide(s1, cur.d1.x, pm);
+            mac_wide(t1, cur.d1.y, pm);
+        }
+        stv2(acc + c * accs + (long)e * N + k, barrett128(s0, q, r0, r1), barrett128(t0, q, r0, r1));
+        stv2(acc + c * accs + (long)(ne + e) * N + k, barrett128(s1, q, r0, r1), barrett128(t1, q, r0, r1));
+        cur = nxt;
+    }
+}
+
+// scalar variant for dnum > 4 (small primes only: the toy ring): one coefficient per thread
 template <int MAXB>
 __global__ void ks_inner_kernel(Tab tab, int logn, const u64 *__restrict__ d, long ds, const u64 *__restrict__ ext,
                                 long exts, const u64 *__restrict__ key, int nq_total, int np,
@@ -105,24 +175,15 @@ __global__ void ks_inner_kernel(Tab tab, int logn, const u64 *__restrict__ d, lo
     const int ne = nl + np, nk = nq_total + np;
     const int pr = e < nl ? e : nq_total + (e - nl);
     const u64 q = tab.q[pr], r0 = tab.br0[pr], r1 = tab.br1[pr];
-    u64 kb[MAXB], ka[MAXB];
-#pragma unroll
-    for (int j = 0; j < MAXB; j++)
-        if (j < beta) {
-            kb[j] = __ldg(key + (((long)j * 2 + 0) * nk + pr) * N + k);
-            ka[j] = __ldg(key + (((long)j * 2 + 1) * nk + pr) * N + k);
-        }
-    const int jd = e < nl ? e / alpha : -1;  // digit containing e (Q limbs only)
+    const int jd = e < nl ? e / alpha : -1;
     for (int c = 0; c < n_ct; c++) {
         U128 s0{0, 0}, s1{0, 0};
-#pragma unroll
-        for (int j = 0; j < MAXB; j++)
-            if (j < beta) {
-                const u64 x = (j == jd) ? d[c * ds + e * N + k] : ext[c * exts + ((long)j * ne + e) * N + k];
-                mac_wide(s0, x, kb[j]);
-                mac_wide(s1, x, ka[j]);
-            }
-        if (d01 && e < nl) {  // relinearise-and-rescale (R11b): x_b = acc_b + [P]_{q_e} d_b on Q limbs
+        for (int j = 0; j < beta; j++) {
+            const u64 x = (j == jd) ? d[c * ds + e * N + k] : ext[c * exts + ((long)j * ne + e) * N + k];
+            mac_wide(s0, x, __ldg(key + (((long)j * 2 + 0) * nk + pr) * N + k));
+            mac_wide(s1, x, __ldg(key + (((long)j * 2 + 1) * nk + pr) * N + k));
+        }
+        if (d01 && e < nl) {
             const u64 pm = pmod[e];
             mac_wide(s0, d01[c * d01s + e * N + k], pm);
             mac_wide(s1, d01[c * d01s + ((long)nl + e) * N + k], pm);
@@ -294,23 +355,24 @@ void k_ks_inner(const Tab &tab, int logn, const u64 *d, long ds, const u64 *ext,
                 int nq_total, int np, u64 *acc, long accs, int n_ct, int nl, int alpha, cudaStream_t st,
                 const u64 *d01, long d01s, const u64 *pmod) {
     const int beta = (nl + alpha - 1) / alpha;
-    const dim3 grid(chunks(logn), nl + np);
-    // 128-bit accumulation of beta products < 2^124 each requires beta <= 16 per Barrett input bound
-    // (2^125); larger dnum only occurs with small primes (toy: 40-bit, products < 2^80).
-    if (beta <= 4)
-        ks_inner_kernel<4><<<grid, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, n_ct, nl,
-                                                 alpha, beta, d01, d01s, pmod);
-    else if (beta <= 8)
-        ks_inner_kernel<8><<<grid, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, n_ct, nl,
-                                                 alpha, beta, d01, d01s, pmod);
-    else if (beta <= 16)
-        ks_inner_kernel<16><<<grid, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, n_ct, nl,
-                                                  alpha, beta, d01, d01s, pmod);
-    else if (beta <= 32)
-        ks_inner_kernel<32><<<grid, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, n_ct, nl,
-                                                  alpha, beta, d01, d01s, pmod);
+    // 128-bit accumulation of beta + 1 products < 2^120 stays below the Barrett input bound 2^125
+    // (checked at context creation against the actual prime sizes).
+    const dim3 g2(chunks2(logn), nl + np), g1(chunks(logn), nl + np);
+#define KSV(B_)                                                                                                 \
+    ks_inner_vec_kernel<B_><<<g2, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, n_ct, nl, \
+                                                alpha, beta, d01, d01s, pmod)
+    if (beta == 1)
+        KSV(1);
+    else if (beta == 2)
+        KSV(2);
+    else if (beta == 3)
+        KSV(3);
+    else if (beta == 4)
+        KSV(4);
     else
-        throw SecpeError{-1, "dnum > 32 not supported"};
+        ks_inner_kernel<0><<<g1, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, n_ct, nl,
+                                               alpha, beta, d01, d01s, pmod);
+#undef KSV
     LAUNCH_CHECK();
 }
 void k_moddown_conv(const Tab &tab, int logn, const u64 *acc, long accs, int ne, int row0, int ns, u64 *T,
