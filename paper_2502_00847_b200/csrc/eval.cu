@@ -108,16 +108,24 @@ void ev_rescale(Ctx &c, const CtView &in, const CtView &out) {
 
 // ModUp + key inner product (R10): acc[ct][b][ne][N] over Q_level u P (NTT form).  d01/d01s: optional
 // tensor (d0, d1) rows whose [P] multiple is added on the Q limbs (R11b).
+// ten != nullptr: relinearisation of the tensor of ten->a, ten->b formed on the fly (d unused): the
+// INTT's first pass multiplies a1 b1, the inner product forms d0, d1 (+ C x) and adds [P] d_b.
 static void ks_modup_inner(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, DevBuf &acc,
-                           const u64 *d01 = nullptr, long d01s = 0) {
+                           const TensorSrc *ten = nullptr) {
     const long N = c.N;
     const int nl = level + 1, np = c.np, ne = nl + np, bt = c.beta(level);
     const LevelConsts &lc = c.level(level);
     // 1. y_i = [INTT(d)_i (Q'_j/q_i)^{-1}]_{q_i}: copy and the ModUp factor fused into the INTT
     DevBuf dc((size_t)n * nl * N, c.st);
     NttFusion f1;
-    f1.in_mode = 1;
-    f1.src = CRows{d, 2 * d_stride, d_stride};
+    if (ten) {
+        f1.in_mode = 3;  // d2 = a1 b1
+        f1.src = CRows{ten->a.p + ten->a.ps, 2 * ten->a.cs, ten->a.cs};
+        f1.src2 = CRows{ten->b.p + ten->b.ps, 2 * ten->b.cs, ten->b.cs};
+    } else {
+        f1.in_mode = 1;
+        f1.src = CRows{d, 2 * d_stride, d_stride};
+    }
     f1.k = lc.inv_hat_ninv.p;
     f1.ksh = lc.inv_hat_ninv_sh.p;
     ev_ntt(c, RowsArg{dc.p, 2L * nl * N, (long)nl * N}, n, qmap(nl), true, f1);
@@ -134,7 +142,7 @@ static void ks_modup_inner(Ctx &c, const u64 *d, long d_stride, int n, int level
     // 3. inner product with the switching key
     const long accs = 2L * ne * N;
     acc = DevBuf((size_t)n * accs, c.st);
-    k_ks_inner(c.tab, c.logn, d, d_stride, ext.p, exts, key, c.nq, np, acc.p, accs, n, nl, c.alpha, c.st, d01, d01s,
+    k_ks_inner(c.tab, c.logn, d, d_stride, ext.p, exts, key, c.nq, np, acc.p, accs, n, nl, c.alpha, c.st, ten,
                c.pmod.p);
     c.cnt.launches += 2;
 }
@@ -183,20 +191,21 @@ void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &
     const int l = a.level, nl = l + 1;
     if (l < 1) throw SecpeError{-2, "mul_relin_rescale: no level left"};
     if (b.level != l || out.level != l - 1) throw SecpeError{-1, "mul_relin_rescale: levels"};
-    const long N = c.N, ds = 3L * nl * N;
+    const long N = c.N;
     const int n = a.n, np = c.np, ne = nl + np, bt = c.beta(l);
     const LevelConsts &lc = c.level(l);
-    DevBuf d((size_t)n * ds, c.st);
+    // the tensor (d0, d1, d2) is never materialised: d2 = a1 b1 is formed by the INTT's first pass and
+    // d0, d1 (+ C x) inside the key inner product
+    TensorSrc ten{};
+    ten.a = crows_of(a);
+    ten.b = crows_of(b);
     if (lin_x) {
-        const LimbConst Cl = limb_const(c, C, nl);
-        k_tensor(c.tab, c.logn, crows_of(a), crows_of(b), d.p, ds, n, nl, c.st, crows_of(*lin_x), &Cl);
-    } else {
-        k_tensor(c.tab, c.logn, crows_of(a), crows_of(b), d.p, ds, n, nl, c.st);
+        ten.x = crows_of(*lin_x);
+        ten.C = limb_const(c, C, nl);
     }
-    c.cnt.launches++;
     const size_t pa = c.prof_begin(1);
     DevBuf acc;
-    ks_modup_inner(c, d.p + 2L * nl * N, ds, n, l, k.rlk.p, acc, d.p, ds);
+    ks_modup_inner(c, nullptr, 0, n, l, k.rlk.p, acc, &ten);
     const long accs = 2L * ne * N;
     // INTT of the B rows (q_l row, then the special rows: contiguous rows l .. ne-1) with (B/s)^{-1} folded
     NttFusion f4;

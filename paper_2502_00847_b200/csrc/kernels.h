@@ -25,6 +25,7 @@ struct LimbConst {
 // data: n_polys polynomials (RowsArg addressing) of lm.nl limbs each; in place unless fused.
 // Fusions (all optional; the default is a plain in-place transform):
 //   in_mode  1 (inverse): the first pass reads polynomial P, limb i from src (copy fused in)
+//   in_mode  3 (inverse): the first pass reads src[P] * src2[P] mod q_i (tensor term fused in)
 //   in_mode  2 (forward): rescale broadcast (R12): the input of limb i is
 //            [floor(q_l/2)]_{q_i} - [[x + floor(q_l/2)]_{q_l}]_{q_i}, x = src row of polynomial P
 //            (one coefficient-form limb, prime lp); half[i] = [floor(q_l/2)]_{q_i}
@@ -35,6 +36,7 @@ struct LimbConst {
 struct NttFusion {
     int in_mode = 0, out_mode = 0;
     CRows src{nullptr, 0, 0};
+    CRows src2{nullptr, 0, 0};  // in_mode 3 (inverse): the first pass reads src[P] * src2[P] mod q (tensor d2)
     int lp = 0;
     const u64 *half = nullptr;
     CRows e1{nullptr, 0, 0}, e2{nullptr, 0, 0};
@@ -76,11 +78,16 @@ struct KsLevel;  // per-level constants (device pointers), see context.h
 void k_modup(const Tab &tab, int logn, const u64 *dc, long dc_ct_stride, u64 *ext, long ext_ct_stride,
              int n_ct, int nl, int np, int nq_total, int alpha, const u64 *hat, cudaStream_t st);
 // key inner product: acc[c][b][e] = sum_j X_j[e] * key_j[b][prime(e)], X_j[e] = d[c][e] if e in I_j else ext[c][j][e]
-// (+ pmod[e] * d01[c][b][e] on the Q limbs e < nl when d01 != nullptr: relinearise-and-rescale, R11b)
+// Relinearise-and-rescale (ten != nullptr): the tensor of a and b is formed on the fly on the Q limbs:
+// d2 = a1 b1 replaces d, and pmod[e] * d_b is added with d0 = a0 b0 + C x0, d1 = a0 b1 + a1 b0 + C x1
+// (the optional linear term x, C of R13).
+struct TensorSrc {
+    CRows a, b, x;  // ciphertext views (c0 at p + ct * cs, c1 at + ps); x.p == nullptr: no linear term
+    LimbConst C;    // per-limb residues of the linear term's integer constant (Shoup companions)
+};
 void k_ks_inner(const Tab &tab, int logn, const u64 *d, long d_ct_stride, const u64 *ext, long ext_ct_stride,
                 const u64 *key, int nq_total, int np, u64 *acc, long acc_ct_stride, int n_ct, int nl,
-                int alpha, cudaStream_t st, const u64 *d01 = nullptr, long d01_ct_stride = 0,
-                const u64 *pmod = nullptr);
+                int alpha, cudaStream_t st, const TensorSrc *ten = nullptr, const u64 *pmod = nullptr);
 // ModDown conversion (R11, R11b): T[c][b][i] = sum_{s < ns} y_s [B/s]_{q_i} mod q_i for i < nt, with
 // y_s = acc[c][b][row0 + s] (coefficient form, already times (B/s)^{-1}); hatpk[s * hstride + i]
 // split-30 packed

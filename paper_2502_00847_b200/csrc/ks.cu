@@ -99,29 +99,50 @@ __global__ void __launch_bounds__(TPB) modup_kernel(Tab tab, int logn, const u64
 // (beta <= 4); larger dnum uses the scalar ks_inner_kernel below.
 template <int MAXB>
 struct KsIn {
-    ulonglong2 x[MAXB], d0, d1;
+    ulonglong2 x[MAXB], d0, d1, a0, a1, b0, b1, x0, x1;
 };
-template <int MAXB>
+template <int MAXB, bool TEN>
 __device__ __forceinline__ void ks_load(KsIn<MAXB> &in, int c, const u64 *__restrict__ d, long ds,
                                         const u64 *__restrict__ ext, long exts, int e, int jd, int ne, int nl,
-                                        int beta, long N, long k, const u64 *__restrict__ d01, long d01s) {
+                                        int beta, long N, long k, const TensorSrc &ten) {
 #pragma unroll
     for (int j = 0; j < MAXB; j++)
-        if (j < beta)
+        if (j < beta && (!TEN || j != jd))
             in.x[j] = ldv2((j == jd) ? d + c * ds + e * N + k : ext + c * exts + ((long)j * ne + e) * N + k);
-    if (d01 && e < nl) {
-        in.d0 = ldv2(d01 + c * d01s + e * N + k);
-        in.d1 = ldv2(d01 + c * d01s + ((long)nl + e) * N + k);
+    if (TEN && e < nl) {
+        const long o = e * N + k;
+        in.a0 = ldv2(ten.a.p + c * ten.a.cs + o);
+        in.a1 = ldv2(ten.a.p + c * ten.a.cs + ten.a.ps + o);
+        in.b0 = ldv2(ten.b.p + c * ten.b.cs + o);
+        in.b1 = ldv2(ten.b.p + c * ten.b.cs + ten.b.ps + o);
+        if (ten.x.p) {
+            in.x0 = ldv2(ten.x.p + c * ten.x.cs + o);
+            in.x1 = ldv2(ten.x.p + c * ten.x.cs + ten.x.ps + o);
+        }
     }
 }
 
-template <int MAXB>
-__global__ void __launch_bounds__(TPB) ks_inner_vec_kernel(Tab tab, int logn, const u64 *__restrict__ d, long ds,
-                                                       const u64 *__restrict__ ext, long exts,
-                                                       const u64 *__restrict__ key, int nq_total, int np,
-                                                       u64 *__restrict__ acc, long accs, int n_ct, int nl, int alpha,
-                                                       int beta, const u64 *__restrict__ d01, long d01s,
-                                                       const u64 *__restrict__ pmod) {
+// one coefficient of the tensor: (d0, d1, d2) mod q, with the optional linear term C x
+__device__ __forceinline__ void tensor1(u64 a0, u64 a1, u64 b0, u64 b1, bool lin, u64 x0, u64 x1, u64 c, u64 csh,
+                                        u64 q, u64 r0, u64 r1, u64 &d0, u64 &d1, u64 &d2) {
+    d0 = mulmod(a0, b0, q, r0, r1);
+    U128 t = mul_wide(a0, b1);
+    mac_wide(t, a1, b0);
+    d1 = barrett128(t, q, r0, r1);
+    d2 = mulmod(a1, b1, q, r0, r1);
+    if (lin) {
+        d0 = addmod(d0, mul_shoup(x0, c, csh, q), q);
+        d1 = addmod(d1, mul_shoup(x1, c, csh, q), q);
+    }
+}
+
+template <int MAXB, bool TEN>
+__global__ void __launch_bounds__(TPB, 2) ks_inner_vec_kernel(Tab tab, int logn, const u64 *__restrict__ d, long ds,
+                                                           const u64 *__restrict__ ext, long exts,
+                                                           const u64 *__restrict__ key, int nq_total, int np,
+                                                           u64 *__restrict__ acc, long accs, int n_ct, int nl,
+                                                           int alpha, int beta, TensorSrc ten,
+                                                           const u64 *__restrict__ pmod) {
     const int e = blockIdx.y;
     const long N = 1L << logn;
     const long k = 2L * ((long)blockIdx.x * TPB + threadIdx.x);
@@ -136,12 +157,26 @@ __global__ void __launch_bounds__(TPB) ks_inner_vec_kernel(Tab tab, int logn, co
             ka[j] = ldv2(key + (((long)j * 2 + 1) * nk + pr) * N + k);
         }
     const int jd = e < nl ? e / alpha : -1;  // digit containing e (Q limbs only)
-    const bool add = d01 && e < nl;          // relinearise-and-rescale: x_b = acc_b + [P]_{q_e} d_b on Q limbs
-    const u64 pm = add ? pmod[e] : 0;
+    const bool qrow = TEN && e < nl;         // relinearise-and-rescale: x_b = acc_b + [P]_{q_e} d_b on Q limbs
+    const u64 pm = qrow ? pmod[e] : 0;
+    const bool lin = TEN && ten.x.p;
+    const u64 cc = lin && e < nl ? ten.C.c[e] : 0, ccsh = lin && e < nl ? ten.C.csh[e] : 0;
+    // plain key switching double-buffers the next ciphertext's inputs; with the tensor formed on the fly
+    // the register budget goes to the tensor terms instead (single buffer)
     KsIn<MAXB> cur, nxt;
-    ks_load<MAXB>(cur, 0, d, ds, ext, exts, e, jd, ne, nl, beta, N, k, d01, d01s);
+    ks_load<MAXB, TEN>(cur, 0, d, ds, ext, exts, e, jd, ne, nl, beta, N, k, ten);
     for (int c = 0; c < n_ct; c++) {
-        if (c + 1 < n_ct) ks_load<MAXB>(nxt, c + 1, d, ds, ext, exts, e, jd, ne, nl, beta, N, k, d01, d01s);
+        if (!TEN && c + 1 < n_ct) ks_load<MAXB, TEN>(nxt, c + 1, d, ds, ext, exts, e, jd, ne, nl, beta, N, k, ten);
+        if (qrow) {
+            u64 e0, e1, e2, f0, f1, f2;
+            tensor1(cur.a0.x, cur.a1.x, cur.b0.x, cur.b1.x, lin, cur.x0.x, cur.x1.x, cc, ccsh, q, r0, r1, e0, e1, e2);
+            tensor1(cur.a0.y, cur.a1.y, cur.b0.y, cur.b1.y, lin, cur.x0.y, cur.x1.y, cc, ccsh, q, r0, r1, f0, f1, f2);
+#pragma unroll
+            for (int j = 0; j < MAXB; j++)
+                if (j == jd) cur.x[j] = make_ulonglong2(e2, f2);
+            cur.d0 = make_ulonglong2(e0, f0);
+            cur.d1 = make_ulonglong2(e1, f1);
+        }
         U128 s0{0, 0}, s1{0, 0}, t0{0, 0}, t1{0, 0};  // (poly 0, poly 1) x (coefficient k, k + 1)
 #pragma unroll
         for (int j = 0; j < MAXB; j++)
@@ -151,7 +186,7 @@ __global__ void __launch_bounds__(TPB) ks_inner_vec_kernel(Tab tab, int logn, co
                 mac_wide(s1, cur.x[j].x, ka[j].x);
                 mac_wide(t1, cur.x[j].y, ka[j].y);
             }
-        if (add) {
+        if (qrow) {
             mac_wide(s0, cur.d0.x, pm);
             mac_wide(t0, cur.d0.y, pm);
             mac_wide(s1, cur.d1.x, pm);
@@ -159,7 +194,11 @@ __global__ void __launch_bounds__(TPB) ks_inner_vec_kernel(Tab tab, int logn, co
         }
         stv2(acc + c * accs + (long)e * N + k, barrett128(s0, q, r0, r1), barrett128(t0, q, r0, r1));
         stv2(acc + c * accs + (long)(ne + e) * N + k, barrett128(s1, q, r0, r1), barrett128(t1, q, r0, r1));
-        cur = nxt;
+        if (TEN) {
+            if (c + 1 < n_ct) ks_load<MAXB, TEN>(cur, c + 1, d, ds, ext, exts, e, jd, ne, nl, beta, N, k, ten);
+        } else {
+            cur = nxt;
+        }
     }
 }
 
@@ -168,25 +207,35 @@ template <int MAXB>
 __global__ void ks_inner_kernel(Tab tab, int logn, const u64 *__restrict__ d, long ds, const u64 *__restrict__ ext,
                                 long exts, const u64 *__restrict__ key, int nq_total, int np,
                                 u64 *__restrict__ acc, long accs, int n_ct, int nl, int alpha, int beta,
-                                const u64 *__restrict__ d01, long d01s, const u64 *__restrict__ pmod) {
+                                TensorSrc ten, const u64 *__restrict__ pmod) {
     const int e = blockIdx.y;
     const long N = 1L << logn;
     const long k = (long)blockIdx.x * TPB + threadIdx.x;
+    const bool qrow = ten.a.p && e < nl;
     const int ne = nl + np, nk = nq_total + np;
     const int pr = e < nl ? e : nq_total + (e - nl);
     const u64 q = tab.q[pr], r0 = tab.br0[pr], r1 = tab.br1[pr];
     const int jd = e < nl ? e / alpha : -1;
     for (int c = 0; c < n_ct; c++) {
         U128 s0{0, 0}, s1{0, 0};
+        u64 d0 = 0, d1 = 0, d2 = 0;
+        if (qrow) {
+            const long o = e * N + k;
+            const bool lin = ten.x.p != nullptr;
+            tensor1(ten.a.p[c * ten.a.cs + o], ten.a.p[c * ten.a.cs + ten.a.ps + o], ten.b.p[c * ten.b.cs + o],
+                    ten.b.p[c * ten.b.cs + ten.b.ps + o], lin, lin ? ten.x.p[c * ten.x.cs + o] : 0,
+                    lin ? ten.x.p[c * ten.x.cs + ten.x.ps + o] : 0, lin ? ten.C.c[e] : 0, lin ? ten.C.csh[e] : 0, q,
+                    r0, r1, d0, d1, d2);
+        }
         for (int j = 0; j < beta; j++) {
-            const u64 x = (j == jd) ? d[c * ds + e * N + k] : ext[c * exts + ((long)j * ne + e) * N + k];
+            const u64 x = (j == jd) ? (qrow ? d2 : d[c * ds + e * N + k]) : ext[c * exts + ((long)j * ne + e) * N + k];
             mac_wide(s0, x, __ldg(key + (((long)j * 2 + 0) * nk + pr) * N + k));
             mac_wide(s1, x, __ldg(key + (((long)j * 2 + 1) * nk + pr) * N + k));
         }
-        if (d01 && e < nl) {
+        if (qrow) {
             const u64 pm = pmod[e];
-            mac_wide(s0, d01[c * d01s + e * N + k], pm);
-            mac_wide(s1, d01[c * d01s + ((long)nl + e) * N + k], pm);
+            mac_wide(s0, d0, pm);
+            mac_wide(s1, d1, pm);
         }
         acc[c * accs + (long)e * N + k] = barrett128(s0, q, r0, r1);
         acc[c * accs + (long)(ne + e) * N + k] = barrett128(s1, q, r0, r1);
@@ -353,14 +402,22 @@ void k_modup(const Tab &tab, int logn, const u64 *dc, long dcs, u64 *ext, long e
 }
 void k_ks_inner(const Tab &tab, int logn, const u64 *d, long ds, const u64 *ext, long exts, const u64 *key,
                 int nq_total, int np, u64 *acc, long accs, int n_ct, int nl, int alpha, cudaStream_t st,
-                const u64 *d01, long d01s, const u64 *pmod) {
+                const TensorSrc *ten, const u64 *pmod) {
     const int beta = (nl + alpha - 1) / alpha;
     // 128-bit accumulation of beta + 1 products < 2^120 stays below the Barrett input bound 2^125
     // (checked at context creation against the actual prime sizes).
     const dim3 g2(chunks2(logn), nl + np), g1(chunks(logn), nl + np);
-#define KSV(B_)                                                                                                 \
-    ks_inner_vec_kernel<B_><<<g2, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, n_ct, nl, \
-                                                alpha, beta, d01, d01s, pmod)
+    static const TensorSrc none{};
+    const TensorSrc &T = ten ? *ten : none;
+#define KSV(B_)                                                                                                   \
+    do {                                                                                                          \
+        if (ten)                                                                                                  \
+            ks_inner_vec_kernel<B_, true><<<g2, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, \
+                                                              accs, n_ct, nl, alpha, beta, T, pmod);              \
+        else                                                                                                      \
+            ks_inner_vec_kernel<B_, false><<<g2, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np,     \
+                                                               acc, accs, n_ct, nl, alpha, beta, T, pmod);       \
+    } while (0)
     if (beta == 1)
         KSV(1);
     else if (beta == 2)
@@ -371,7 +428,7 @@ void k_ks_inner(const Tab &tab, int logn, const u64 *d, long ds, const u64 *ext,
         KSV(4);
     else
         ks_inner_kernel<0><<<g1, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, n_ct, nl,
-                                               alpha, beta, d01, d01s, pmod);
+                                               alpha, beta, T, pmod);
 #undef KSV
     LAUNCH_CHECK();
 }

@@ -230,7 +230,7 @@ __device__ __forceinline__ void do_round(u64 (&v)[NV], int tau, int g, const ulo
 }
 
 // Fused prologue / epilogue modes (NttFusion in kernels.h)
-enum { IN_PLAIN = 0, IN_SRC = 1, IN_BCAST = 2 };
+enum { IN_PLAIN = 0, IN_SRC = 1, IN_BCAST = 2, IN_MUL = 3 };
 enum { OUT_PLAIN = 0, OUT_RESCALE = 1, OUT_MODDOWN = 2 };
 
 struct PassArgs {
@@ -336,7 +336,7 @@ __device__ __forceinline__ int padr(int r) { return r + (r >> 4); }
 template <int LOGN, bool INV, int IO, class A>
 __device__ __forceinline__ void contig_body(const PassArgs &a, u64 *sm, int poly, int limb, int prime,
                                             const PrimeC &P) {
-    // IO: inverse -> IN_PLAIN | IN_SRC (first pass reads f.src rows);  forward -> OUT_* epilogue
+    // IO: inverse -> IN_PLAIN | IN_SRC | IN_MUL (first pass reads f.src rows);  forward -> OUT_* epilogue
     using CF = ContigCfg<LOGN>;
     constexpr int S = CF::S, G = CF::G, TPG = CF::TPG, CG = CF::CG, PITCH = CF::PITCH;
     constexpr long N = 1L << LOGN;
@@ -357,11 +357,21 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, u64 *sm, int poly
 #pragma unroll
         for (int k = 0; k < NV; k++) v[k] = src[held<LO0>(tau, k)];  // intermediate representation
     } else {
-        const u64 *sp = (IO == IN_SRC) ? a.f.src.p + poly_off(a.f.src.cs, a.f.src.ps, poly) + boff : blk;
+        const u64 *sp = (IO == IN_SRC || IO == IN_MUL) ? a.f.src.p + poly_off(a.f.src.cs, a.f.src.ps, poly) + boff
+                                                       : blk;
         const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(sp);
+        const ulonglong2 *src2 = nullptr;
+        if (IO == IN_MUL)
+            src2 = reinterpret_cast<const ulonglong2 *>(a.f.src2.p + poly_off(a.f.src2.cs, a.f.src2.ps, poly) + boff);
+        const u64 br0 = a.tab.br0[prime], br1 = a.tab.br1[prime];
 #pragma unroll 4
         for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
-            const ulonglong2 x = src[i];
+            ulonglong2 x = src[i];
+            if (IO == IN_MUL) {
+                const ulonglong2 y = src2[i];
+                x.x = mulmod(x.x, y.x, q, br0, br1);
+                x.y = mulmod(x.y, y.y, q, br0, br1);
+            }
             const int e = 2 * i, gg = e / G, r = e % G;
             sm[gg * PITCH + padr(r)] = A::in(x.x, P);
             sm[gg * PITCH + padr(r + 1)] = A::in(x.y, P);
@@ -495,6 +505,8 @@ void run(const PassArgs &a, int rows, bool inverse, cudaStream_t st) {
     } else {
         if (f.in_mode == IN_SRC)
             launch_contig<LOGN, true, IN_SRC>(a, rows, st);
+        else if (f.in_mode == IN_MUL)
+            launch_contig<LOGN, true, IN_MUL>(a, rows, st);
         else
             launch_contig<LOGN, true, IN_PLAIN>(a, rows, st);
         LAUNCH_CHECK();
@@ -526,7 +538,7 @@ void ntt_forward(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm
 void ntt_inverse(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
                  const NttFusion &f) {
     if (n_polys <= 0 || lm.nl <= 0) return;
-    if ((f.in_mode != IN_PLAIN && f.in_mode != IN_SRC) || f.out_mode != OUT_PLAIN)
+    if ((f.in_mode != IN_PLAIN && f.in_mode != IN_SRC && f.in_mode != IN_MUL) || f.out_mode != OUT_PLAIN)
         throw SecpeError{-1, "ntt_inverse: bad fusion mode"};
     dispatch(logn, PassArgs{data, lm, tab, f}, n_polys * lm.nl, true, st);
 }
