@@ -199,9 +199,139 @@ void Ctx::log(const char *kind, int lin, int lout, double s, const std::string &
 }
 
 // ---------------------------------------------------------------------------------------------
+// tensor-core base-conversion groups of a level (bconv_tc.cu): ModUp per digit, fused ModDown +
+// rescale, plain ModDown.  Constants are exactly those of the integer kernels (R10, R11, R12).
+// ---------------------------------------------------------------------------------------------
+void Ctx::build_tc_groups(LevelConsts &lc, int l) {
+    const int nl = l + 1, ne = nl + np, bt = beta(l);
+    auto pid = [&](int e) { return e < nl ? e : nq + (e - nl); };
+    std::vector<TcGroup> groups;
+    std::vector<std::vector<uint8_t>> Bs;
+    bool ok = np >= 1 && np + 1 <= 12;
+    auto add = [&](TcGroup g, const std::vector<std::vector<u64>> &c, const std::vector<u64> &tp) {
+        if (g.ns + 1 > 12 || g.nt > TC_TMAX) ok = false;
+        if (!ok) return;
+        Bs.push_back(tc_bmatrix(c, tp));
+        groups.push_back(g);
+    };
+    // ModUp digits: sources y_i (i in I_j), targets every e outside the digit
+    for (int j = 0; j < bt; j++) {
+        const int i0 = j * alpha, i1 = std::min(i0 + alpha, nl), na = i1 - i0;
+        TcGroup g{};
+        g.ns = na;
+        g.src_row0 = i0;
+        std::vector<u64> tp;
+        std::vector<std::vector<u64>> c(na);
+        for (int e = 0; e < ne; e++) {
+            if (e >= i0 && e < i1) continue;
+            if (g.nt >= TC_TMAX) {
+                ok = false;
+                break;
+            }
+            const u64 t = primes[pid(e)];
+            g.prime[g.nt] = pid(e);
+            g.out_row[g.nt] = e;
+            tp.push_back(t);
+            for (int i = i0; i < i1; i++) {
+                u64 h = 1;
+                for (int i2 = i0; i2 < i1; i2++)
+                    if (i2 != i) h = h_mulmod(h, primes[i2] % t, t);
+                c[i - i0].push_back(h);
+            }
+            g.nt++;
+        }
+        add(g, c, tp);
+    }
+    // P, (P/p) and products with q_l
+    auto Pmod = [&](u64 t) {
+        u64 v = 1;
+        for (int p2 = 0; p2 < np; p2++) v = h_mulmod(v, primes[nq + p2] % t, t);
+        return v;
+    };
+    auto Phat = [&](int p, u64 t) {
+        u64 v = 1;
+        for (int p2 = 0; p2 < np; p2++)
+            if (p2 != p) v = h_mulmod(v, primes[nq + p2] % t, t);
+        return v;
+    };
+    // fused ModDown + rescale (l >= 1): sources y_p and the constant 1; target 0 = q_l (prelude), then q_i
+    {
+        TcGroup g{};
+        g.ns = np;
+        g.src_row0 = l + 1;
+        std::vector<u64> tp;
+        std::vector<std::vector<u64>> c(np + 1);
+        if (l >= 1 && l + 1 <= TC_TMAX) {
+            const u64 ql = primes[l];
+            g.prime[0] = l;
+            g.out_row[0] = -1;
+            tp.push_back(ql);
+            for (int p = 0; p < np; p++) c[p].push_back(Phat(p, ql));
+            c[np].push_back(0);
+            for (int i = 0; i < l; i++) {
+                const u64 qi = primes[i];
+                g.prime[1 + i] = i;
+                g.out_row[1 + i] = i;
+                g.pmod[1 + i] = Pmod(qi);
+                g.pmodsh[1 + i] = h_shoup(g.pmod[1 + i], qi);
+                tp.push_back(qi);
+                for (int p = 0; p < np; p++) c[p].push_back(Phat(p, qi));
+                const u64 ph = h_mulmod(Pmod(qi), (ql >> 1) % qi, qi);
+                c[np].push_back(ph ? qi - ph : 0);
+            }
+            g.nt = l + 1;
+            add(g, c, tp);
+        } else {
+            add(g, std::vector<std::vector<u64>>(np + 1), tp);  // empty placeholder (never launched)
+        }
+    }
+    // plain ModDown (rotations): sources y_p, targets q_0..q_l
+    {
+        TcGroup g{};
+        g.ns = np;
+        g.src_row0 = nl;
+        std::vector<u64> tp;
+        std::vector<std::vector<u64>> c(np);
+        if (nl <= TC_TMAX) {
+            for (int i = 0; i < nl; i++) {
+                g.prime[i] = i;
+                g.out_row[i] = i;
+                tp.push_back(primes[i]);
+                for (int p = 0; p < np; p++) c[p].push_back(Phat(p, primes[i]));
+            }
+            g.nt = nl;
+        } else {
+            ok = false;
+        }
+        add(g, c, tp);
+    }
+    lc.tc_ok = ok;
+    if (!ok) return;
+    // one device buffer for every B matrix; TcGroup.B point into it
+    std::vector<size_t> off;
+    size_t total = 0;
+    for (auto &b : Bs) {
+        off.push_back(total);
+        total += (b.size() + 255) / 256 * 256;
+    }
+    std::vector<u64> hb((total + 7) / 8, 0);
+    for (size_t i = 0; i < Bs.size(); i++) std::memcpy(reinterpret_cast<uint8_t *>(hb.data()) + off[i], Bs[i].data(), Bs[i].size());
+    lc.tc_B = upload(hb, st);
+    for (size_t i = 0; i < groups.size(); i++)
+        groups[i].B = reinterpret_cast<const uint8_t *>(lc.tc_B.p) + off[i];
+    std::vector<u64> hg((groups.size() * sizeof(TcGroup) + 7) / 8, 0);
+    std::memcpy(hg.data(), groups.data(), groups.size() * sizeof(TcGroup));
+    lc.tc_groups = upload(hg, st);
+}
+
+// ---------------------------------------------------------------------------------------------
 // context build
 // ---------------------------------------------------------------------------------------------
 void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int logn_, double scale_) {
+    {
+        const char *e = getenv("SECPE_NO_TC");  // development switch: integer base-conversion kernels
+        use_tc = !(e && atoi(e) == 1);
+    }
     logn = logn_;
     N = 1L << logn;
     nq = nq_;
@@ -394,6 +524,7 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
             lc->rr_binv = upload(binv, st);
             lc->rr_binv_sh = upload(binvsh, st);
         }
+        build_tc_groups(*lc, l);
         lvl.push_back(std::move(lc));
     }
     u64 cdt[20];

@@ -22,6 +22,33 @@ struct DevBuf {
     DevBuf &operator=(DevBuf &&o) noexcept;
 };
 
+// tensor-core base conversion (bconv_tc.cu): one conversion group = sources x targets + its B matrix
+constexpr int TC_TMAX = 32;
+struct TcGroup {
+    int ns;                  // sources (rows of the source polynomial starting at src_row0)
+    int nt;                  // targets (<= TC_TMAX)
+    int src_row0;
+    const uint8_t *B;        // device: canonical byte-sliced constant matrix, 8 * ntp rows x 96 bytes
+    int prime[TC_TMAX];      // target prime (global index)
+    int out_row[TC_TMAX];    // output row (limb) of the target in the destination polynomial
+    u64 pmod[TC_TMAX];       // rescale variant: [P]_{q_t} and its Shoup companion
+    u64 pmodsh[TC_TMAX];
+};
+struct TcArgs {
+    const u64 *src;
+    long s_cs, s_ps;         // source polynomial p at src + (p / pdiv) s_cs + (p % pdiv) s_ps
+    u64 *dst;
+    long d_cs, d_ps;
+    int pdiv, grouped;       // grouped: group = p % pdiv, else group 0 for every polynomial
+    int rr, const1;          // rr: fused ModDown + rescale prelude on target 0; const1: extra source == 1
+    u64 pinv_l, pinv_l_sh;
+    const TcGroup *groups;   // device
+    Tab tab;
+    int logn;
+};
+std::vector<uint8_t> tc_bmatrix(const std::vector<std::vector<u64>> &c, const std::vector<u64> &tprimes);
+void k_bconv_tc(const TcArgs &a, int n_polys, cudaStream_t st);
+
 // per-level key-switching / rescale constants (device)
 struct LevelConsts {
     int nl, beta;
@@ -31,6 +58,10 @@ struct LevelConsts {
     DevBuf half, qlinv, qlinv_sh;  // rescale by q_{nl-1}: [nl-1]
     // fused relinearise-and-rescale (ev_mul_relin_rescale), l = nl - 1 >= 1; see context.cu
     DevBuf rr_fold, rr_fold_sh, rr_hl, rr_hat, rr_binv, rr_binv_sh;
+    // tensor-core conversion groups: [0, beta) ModUp digits, beta: fused ModDown + rescale (l >= 1),
+    // beta + 1: plain ModDown; tc_ok = every group fits (<= 12 sources, <= 32 targets)
+    DevBuf tc_groups, tc_B;
+    bool tc_ok = false;
 };
 
 // CUDA-event profiling of the dominant kernels inside a timed region (bench.py roofline)
@@ -97,6 +128,8 @@ struct Ctx {
     long ct_words(int level) const { return 2L * (level + 1) * N; }
     void build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int logn_, double scale_);
     const LevelConsts &level(int l) const { return *lvl[l]; }
+    void build_tc_groups(LevelConsts &lc, int l);
+    bool use_tc = true;  // tensor-core base conversion (SECPE_NO_TC=1 selects the integer kernels)
     void log(const char *kind, int lin, int lout, double s, const std::string &extra);
 };
 

@@ -132,7 +132,22 @@ static void ks_modup_inner(Ctx &c, const u64 *d, long d_stride, int n, int level
     // 2. ModUp into every digit's complement, then NTT of the converted limbs
     const long exts = (long)bt * ne * N;
     DevBuf ext((size_t)n * exts, c.st);
-    k_modup(c.tab, c.logn, dc.p, (long)nl * N, ext.p, exts, n, nl, np, c.nq, c.alpha, lc.hat.p, c.st);
+    if (c.use_tc && lc.tc_ok) {
+        TcArgs t{};
+        t.src = dc.p;
+        t.s_cs = (long)nl * N;
+        t.dst = ext.p;
+        t.d_cs = exts;
+        t.d_ps = (long)ne * N;
+        t.pdiv = bt;
+        t.grouped = 1;
+        t.groups = reinterpret_cast<const TcGroup *>(lc.tc_groups.p);
+        t.tab = c.tab;
+        t.logn = c.logn;
+        k_bconv_tc(t, n * bt, c.st);
+    } else {
+        k_modup(c.tab, c.logn, dc.p, (long)nl * N, ext.p, exts, n, nl, np, c.nq, c.alpha, lc.hat.p, c.st);
+    }
     for (int j = 0; j < bt; j++) {
         const int i0 = j * c.alpha, i1 = std::min(i0 + c.alpha, nl);
         if (i0 > 0) ev_ntt(c, RowsArg{ext.p + (long)j * ne * N, 2 * exts, exts}, n, LimbMap{i0, i0, 0, 0}, false);
@@ -165,7 +180,23 @@ void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u
     ev_ntt(c, RowsArg{acc.p + (long)nl * N, accs, (long)ne * N}, 2 * n, LimbMap{np, 0, 0, c.nq}, true, f4);
     const long Ts = 2L * nl * N;
     DevBuf T((size_t)n * Ts, c.st);
-    k_moddown_conv(c.tab, c.logn, acc.p, accs, ne, nl, np, T.p, Ts, nl, n, c.hat_p.p, c.nq, c.st);
+    const LevelConsts &lc = c.level(level);
+    if (c.use_tc && lc.tc_ok) {
+        TcArgs t{};
+        t.src = acc.p;
+        t.s_cs = accs;
+        t.s_ps = (long)ne * N;
+        t.dst = T.p;
+        t.d_cs = Ts;
+        t.d_ps = (long)nl * N;
+        t.pdiv = 2;
+        t.groups = reinterpret_cast<const TcGroup *>(lc.tc_groups.p) + bt + 1;
+        t.tab = c.tab;
+        t.logn = c.logn;
+        k_bconv_tc(t, 2 * n, c.st);
+    } else {
+        k_moddown_conv(c.tab, c.logn, acc.p, accs, ne, nl, np, T.p, Ts, nl, n, c.hat_p.p, c.nq, c.st);
+    }
     NttFusion f6;
     f6.out_mode = 2;
     f6.e1 = CRows{acc.p, accs, (long)ne * N};
@@ -214,8 +245,27 @@ void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &
     ev_ntt(c, RowsArg{acc.p + (long)l * N, accs, (long)ne * N}, 2 * n, LimbMap{np + 1, 1, l, c.nq}, true, f4);
     const long Ts = 2L * l * N;
     DevBuf T((size_t)n * Ts, c.st);
-    k_rr_conv(c.tab, c.logn, acc.p, accs, ne, l, np, T.p, Ts, n, lc.rr_hat.p, lc.rr_hl.p, c.h_pinv[l], c.h_pinv_sh[l],
-              c.st);
+    if (c.use_tc && lc.tc_ok) {
+        TcArgs t{};
+        t.src = acc.p;
+        t.s_cs = accs;
+        t.s_ps = (long)ne * N;
+        t.dst = T.p;
+        t.d_cs = Ts;
+        t.d_ps = (long)l * N;
+        t.pdiv = 2;
+        t.rr = 1;
+        t.const1 = 1;
+        t.pinv_l = c.h_pinv[l];
+        t.pinv_l_sh = c.h_pinv_sh[l];
+        t.groups = reinterpret_cast<const TcGroup *>(lc.tc_groups.p) + bt;
+        t.tab = c.tab;
+        t.logn = c.logn;
+        k_bconv_tc(t, 2 * n, c.st);
+    } else {
+        k_rr_conv(c.tab, c.logn, acc.p, accs, ne, l, np, T.p, Ts, n, lc.rr_hat.p, lc.rr_hl.p, c.h_pinv[l],
+                  c.h_pinv_sh[l], c.st);
+    }
     NttFusion f6;
     f6.out_mode = 2;
     f6.e1 = CRows{acc.p, accs, (long)ne * N};
