@@ -12,16 +12,16 @@
 // IMAD.WIDE per source and target of the integer kernels; the epilogue (TMEM -> registers,
 // 128-bit recombination, one Barrett per output) is what remains on the integer pipes.
 //
-// CTA: 256 threads.  Threads 0..127 stage the byte slices of 128 coefficients into shared memory
+// CTA: 512 threads.  Four threads per coefficient row stage the byte slices of 128 coefficients into shared memory
 // in the canonical K-major no-swizzle UMMA layout (8 x 16-byte core matrices); one thread issues the
 // MMAs and commits to an mbarrier; then warp w reads TMEM lanes 32 (w % 4) .. +31 and handles the
-// targets t = w / 4, w / 4 + 2, ...  The B matrix of a conversion group is precomputed on the host
+// targets t = w / 4, w / 4 + 4, ...  The B matrix of a conversion group is precomputed on the host
 // (already in canonical layout) and copied to shared memory once per CTA.
 #include "context.h"
 
 namespace {
 
-constexpr int TC_THREADS = 256;
+constexpr int TC_THREADS = 512;  // 16 warps: 4 groups of 4 warps share the targets in the epilogue
 constexpr int TC_M = 128;
 constexpr int TC_K = 96;               // bytes of K (12 sources x 8 bytes)
 constexpr int LBO = 128;               // bytes between the two 16-byte K chunks of one MMA K-step
@@ -82,18 +82,18 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
     const uint32_t idesc = (2u << 4) | ((uint32_t)(8 * ntp >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
     const u64 *src = a.src + (long)(p / a.pdiv) * a.s_cs + (long)(p % a.pdiv) * a.s_ps + (long)G.src_row0 * N;
     u64 *dst = a.dst + (long)(p / a.pdiv) * a.d_cs + (long)(p % a.pdiv) * a.d_ps;
-    const int lq = warp & 3, tpar = warp >> 2;
+    const int lq = warp & 3, tpar = warp >> 2;  // TMEM lane quarter, target group (0..3)
     const int m = 32 * lq + lane;  // the coefficient (TMEM lane) this thread reads in the epilogue
     const int ntiles = (int)(N / TC_M);
     // staging: thread (row, half) holds sources s = half, half + 2, ... of coefficient row; the next
     // tile's values are loaded into registers before the current tile's epilogue
-    const int srow = tid & (TC_M - 1), shalf = tid >> 7;
-    u64 pre[6];
+    const int srow = tid & (TC_M - 1), shalf = tid >> 7;  // 4 threads per coefficient row
+    u64 pre[3];
     auto fetch = [&](int tile) {
         const long k0 = (long)tile * TC_M;
 #pragma unroll
-        for (int u = 0; u < 6; u++) {
-            const int s = shalf + 2 * u;
+        for (int u = 0; u < 3; u++) {
+            const int s = shalf + 4 * u;
             if (s < G.ns) pre[u] = src[(long)s * N + k0 + srow];
         }
     };
@@ -102,8 +102,8 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
         const long k0 = (long)tile * TC_M;
 #pragma unroll
-        for (int u = 0; u < 6; u++) {
-            const int s = shalf + 2 * u;
+        for (int u = 0; u < 3; u++) {
+            const int s = shalf + 4 * u;
             if (s < G.ns) *reinterpret_cast<u64 *>(sA + canon(srow, 8 * s)) = pre[u];
         }
         asm volatile("fence.proxy.async.shared::cta;\n");
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
             r = csub(mul_shoup(submod(xc, tl, ql), a.pinv_l, a.pinv_l_sh, ql) + (ql >> 1), ql);
             t0 = 1;
         }
-        for (int t = t0 + tpar; t < nt; t += 2) {
+        for (int t = t0 + tpar; t < nt; t += 4) {
             const int pr = G.prime[t];
             const u64 q = a.tab.q[pr];
             u64 z = reduce(t, q, 1.0 / (double)q);
