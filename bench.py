@@ -23,7 +23,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "encrypted argmax/s at N=2^16; NTT & key-switch HBM GB/s vs peak"
 UNIT = "query-argmax/s"
-WORKLOAD = "configs[4]: SecPE encrypted prompt-ensemble aggregation + Argmax, N=2^16, L=30 (q0 60-bit + 29x45-bit), " \
+WORKLOAD = "configs[4]: SecPE encrypted prompt-ensemble aggregation + Argmax, N=2^16, L=30 (30 x 45-bit primes), " \
            "scale 2^45, dnum=3 (8x60-bit special), 2048 queries x P=8 x K=2 per ciphertext, Sign (7,15,15) eps=2^-7"
 
 

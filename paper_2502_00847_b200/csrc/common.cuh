@@ -73,6 +73,7 @@ struct Tab {
     const ulonglong2 *itw2;  // [P][N] {psi^{-brv(i)}, Shoup companion}  (inverse GS twiddles)
     const u64 *ninv;   // [P] N^{-1} mod q
     const u64 *ninvsh; // [P]
+    u64 fp_mask;       // host-visible: bit i set when prime i < 2^46 (exact-FP64 NTT rows, ntt.cu FpA)
 };
 
 // limb l of a polynomial -> global prime index

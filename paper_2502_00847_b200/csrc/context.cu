@@ -388,7 +388,9 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
     d_tw = upload(tw, st);
     d_itw = upload(itw, st);
     tab = Tab{d_q.p, d_br0.p, d_br1.p, reinterpret_cast<const ulonglong2 *>(d_tw.p),
-              reinterpret_cast<const ulonglong2 *>(d_itw.p), d_ninv.p, d_ninvsh.p};
+              reinterpret_cast<const ulonglong2 *>(d_itw.p), d_ninv.p, d_ninvsh.p, 0};
+    for (int i = 0; i < P && i < 64; i++)
+        if (primes[i] < (1ULL << 46)) tab.fp_mask |= 1ULL << i;
 
     // ModDown constants: P = prod p
     std::vector<u64> vihp(std::max(np, 1)), vihpsh(std::max(np, 1)), vhatp((size_t)std::max(np, 1) * nq),

@@ -29,6 +29,9 @@ namespace {
 #ifndef NTT_MINB
 #define NTT_MINB 3  // resident CTAs per SM the register allocation targets (measured: 3 ~ 4 > 2)
 #endif
+#ifndef NTT_MINB_FP
+#define NTT_MINB_FP 4  // FP rows: 64 registers, no spills
+#endif
 #ifndef NTT_APPROX_HI
 #define NTT_APPROX_HI 1  // approximate Shoup quotient in the butterflies (measured: inverse -4%)
 #endif
@@ -238,6 +241,7 @@ struct PassArgs {
     LimbMap lm;
     Tab tab;
     NttFusion f;
+    int limb0, nsub;  // this launch covers limbs [limb0, limb0 + nsub) of every polynomial (one prime class)
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -305,18 +309,24 @@ __device__ __forceinline__ PrimeC prime_consts(const Tab &tab, int prime) {
     return P;
 }
 
-template <int LOGN, bool INV, int IN, int MINB>
-__global__ void __launch_bounds__(SC *(1 << (LOGN / 2 - RB)), MINB)
-    ntt_strided(PassArgs a) {
+// resident CTAs per SM the register allocation targets: FP rows fit 64 registers (4 CTAs), the
+// integer Shoup path needs 80 (3 CTAs)
+template <class A>
+struct MinB {
+    static constexpr int v = NTT_MINB;
+};
+template <>
+struct MinB<FpA> {
+    static constexpr int v = NTT_MINB_FP;
+};
+
+template <int LOGN, bool INV, int IN, class A>
+__global__ void __launch_bounds__(SC *(1 << (LOGN / 2 - RB)), MinB<A>::v) ntt_strided(PassArgs a) {
     __shared__ u64 sm[(1 << (LOGN / 2)) * SC];
-    const int nl = a.lm.nl;
-    const int poly = blockIdx.y / nl, limb = blockIdx.y % nl;
+    const int poly = blockIdx.y / a.nsub, limb = a.limb0 + blockIdx.y % a.nsub;
     const int prime = prime_of(a.lm, limb);
     const PrimeC P = prime_consts(a.tab, prime);
-    if (P.q < FP_LIMIT)
-        strided_body<LOGN, INV, IN, FpA>(a, sm, poly, limb, prime, P);
-    else
-        strided_body<LOGN, INV, IN, IntA>(a, sm, poly, limb, prime, P);
+    strided_body<LOGN, INV, IN, A>(a, sm, poly, limb, prime, P);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -440,18 +450,14 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, u64 *sm, int poly
     }
 }
 
-template <int LOGN, bool INV, int IO, int MINB>
-__global__ void __launch_bounds__(CT, MINB) ntt_contig(PassArgs a) {
+template <int LOGN, bool INV, int IO, class A>
+__global__ void __launch_bounds__(CT, MinB<A>::v) ntt_contig(PassArgs a) {
     using CF = ContigCfg<LOGN>;
     __shared__ __align__(16) u64 sm[CF::CG * CF::PITCH];
-    const int nl = a.lm.nl;
-    const int poly = blockIdx.y / nl, limb = blockIdx.y % nl;
+    const int poly = blockIdx.y / a.nsub, limb = a.limb0 + blockIdx.y % a.nsub;
     const int prime = prime_of(a.lm, limb);
     const PrimeC P = prime_consts(a.tab, prime);
-    if (P.q < FP_LIMIT)
-        contig_body<LOGN, INV, IO, FpA>(a, sm, poly, limb, prime, P);
-    else
-        contig_body<LOGN, INV, IO, IntA>(a, sm, poly, limb, prime, P);
+    contig_body<LOGN, INV, IO, A>(a, sm, poly, limb, prime, P);
 }
 
 template <typename K>
@@ -463,27 +469,56 @@ void max_smem_carveout(K kern) {
     }
 }
 
-template <int LOGN, bool INV, int IN, int MINB>
-void launch_strided_m(const PassArgs &a, int rows, cudaStream_t st) {
+template <int LOGN, bool INV, int IN, class A>
+void launch_strided_a(const PassArgs &a, int n_polys, cudaStream_t st) {
     constexpr int S = LOGN / 2;
-    max_smem_carveout(ntt_strided<LOGN, INV, IN, MINB>);
-    dim3 grid((unsigned)((1L << (LOGN - S)) / SC), rows);
-    ntt_strided<LOGN, INV, IN, MINB><<<grid, SC * (1 << (S - RB)), 0, st>>>(a);
+    max_smem_carveout(ntt_strided<LOGN, INV, IN, A>);
+    dim3 grid((unsigned)((1L << (LOGN - S)) / SC), n_polys * a.nsub);
+    ntt_strided<LOGN, INV, IN, A><<<grid, SC * (1 << (S - RB)), 0, st>>>(a);
 }
-template <int LOGN, bool INV, int IO, int MINB>
-void launch_contig_m(const PassArgs &a, int rows, cudaStream_t st) {
+template <int LOGN, bool INV, int IO, class A>
+void launch_contig_a(const PassArgs &a, int n_polys, cudaStream_t st) {
     using CF = ContigCfg<LOGN>;
-    max_smem_carveout(ntt_contig<LOGN, INV, IO, MINB>);
-    dim3 grid((unsigned)((1L << (LOGN - CF::S)) / CF::CG), rows);
-    ntt_contig<LOGN, INV, IO, MINB><<<grid, CT, 0, st>>>(a);
+    max_smem_carveout(ntt_contig<LOGN, INV, IO, A>);
+    dim3 grid((unsigned)((1L << (LOGN - CF::S)) / CF::CG), n_polys * a.nsub);
+    ntt_contig<LOGN, INV, IO, A><<<grid, CT, 0, st>>>(a);
+}
+// one launch per run of consecutive limbs of the same prime class (bit i of tab.fp_mask: prime i < 2^46)
+inline bool limb_fp(const PassArgs &a, int limb) {
+    const int p = prime_of(a.lm, limb);
+    return p < 64 && ((a.tab.fp_mask >> p) & 1);
+}
+template <class F>
+void for_runs(const PassArgs &a0, F launch) {
+    int l = 0;
+    while (l < a0.lm.nl) {
+        const bool fp = limb_fp(a0, l);
+        int e = l + 1;
+        while (e < a0.lm.nl && limb_fp(a0, e) == fp) e++;
+        PassArgs a = a0;
+        a.limb0 = l;
+        a.nsub = e - l;
+        launch(a, fp);
+        l = e;
+    }
 }
 template <int LOGN, bool INV, int IN>
-void launch_strided(const PassArgs &a, int rows, cudaStream_t st) {
-    launch_strided_m<LOGN, INV, IN, NTT_MINB>(a, rows, st);
+void launch_strided(const PassArgs &a0, int n_polys, cudaStream_t st) {
+    for_runs(a0, [&](const PassArgs &a, bool fp) {
+        if (fp)
+            launch_strided_a<LOGN, INV, IN, FpA>(a, n_polys, st);
+        else
+            launch_strided_a<LOGN, INV, IN, IntA>(a, n_polys, st);
+    });
 }
 template <int LOGN, bool INV, int IO>
-void launch_contig(const PassArgs &a, int rows, cudaStream_t st) {
-    launch_contig_m<LOGN, INV, IO, NTT_MINB>(a, rows, st);
+void launch_contig(const PassArgs &a0, int n_polys, cudaStream_t st) {
+    for_runs(a0, [&](const PassArgs &a, bool fp) {
+        if (fp)
+            launch_contig_a<LOGN, INV, IO, FpA>(a, n_polys, st);
+        else
+            launch_contig_a<LOGN, INV, IO, IntA>(a, n_polys, st);
+    });
 }
 
 template <int LOGN>
@@ -532,7 +567,7 @@ void ntt_forward(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm
                  const NttFusion &f) {
     if (n_polys <= 0 || lm.nl <= 0) return;
     if (f.in_mode != IN_PLAIN && f.in_mode != IN_BCAST) throw SecpeError{-1, "ntt_forward: bad input mode"};
-    dispatch(logn, PassArgs{data, lm, tab, f}, n_polys * lm.nl, false, st);
+    dispatch(logn, PassArgs{data, lm, tab, f, 0, lm.nl}, n_polys, false, st);
 }
 
 void ntt_inverse(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
@@ -540,5 +575,5 @@ void ntt_inverse(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm
     if (n_polys <= 0 || lm.nl <= 0) return;
     if ((f.in_mode != IN_PLAIN && f.in_mode != IN_SRC && f.in_mode != IN_MUL) || f.out_mode != OUT_PLAIN)
         throw SecpeError{-1, "ntt_inverse: bad fusion mode"};
-    dispatch(logn, PassArgs{data, lm, tab, f}, n_polys * lm.nl, true, st);
+    dispatch(logn, PassArgs{data, lm, tab, f, 0, lm.nl}, n_polys, true, st);
 }

@@ -518,7 +518,7 @@ def test_toy_argmax_end_to_end_oracle():
 
 @pytest.mark.slow
 def test_argmax_small_ring_7_15_15_oracle():
-    """configs[4] circuit (q0 60-bit, 29 x 45-bit, dnum 3, (7,15,15) Sign, K=2, P=8) on a 2^12 ring."""
+    """configs[4] circuit (30 x 45-bit, dnum 3, (7,15,15) Sign, K=2, P=8) on a 2^12 ring."""
     prm = ckks.Params(synth.PARAM_SETS["argmax_small"])
     st = load_sign("sign_7_15_15.json")
     lay = synth.LAYOUTS["argmax_small_k2"]
