@@ -130,7 +130,7 @@ def run_secpe(a):
     import torch.distributed as dist
 
     import synth
-    from paper_2502_00847_b200 import build, secpe
+    from paper_2502_00847_b200 import build, secpe, shard
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -150,7 +150,9 @@ def run_secpe(a):
     L = ctx.L
     inp = ctx.new_ct(L, B)
     for i in range(B):
-        scores = synth.softmax_scores(1000 * 5 + 100 * rank + i, lay["queries"], lay["prompts"], lay["classes"])
+        # rank r owns global ciphertexts [r B, (r + 1) B): the sharded job draws the single-rank job's inputs
+        scores = synth.softmax_scores(shard.input_seed(5, rank * B + i), lay["queries"], lay["prompts"],
+                                      lay["classes"])
         z = secpe.pack(scores, lay, ctx.N // 2)
         m = ctx.encode(z, ctx.scale)
         c = secpe.Ct(inp.t[i:i + 1], L, ctx.scale)
@@ -188,11 +190,8 @@ def run_secpe(a):
     torch.cuda.synchronize()
     counts = ctx.opcounts(reset=True)
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
+    ms = shard.max_over_ranks(e0.elapsed_time(e1), device="cuda")  # slowest rank's device time
     if ws > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
         dist.barrier()
     # roofline: the same K steps again with CUDA events recorded on the launching stream around every
     # NTT / key-switch / rescale span (kept out of the headline timing above)
@@ -206,7 +205,7 @@ def run_secpe(a):
     prof = ctx.profile_end()
     ms_prof = p0.elapsed_time(p1)
     queries = lay["queries"] * B * ws * a.steps
-    value = queries / (ms / 1000.0)
+    value = shard.job_throughput(lay["queries"] * B * a.steps, ws, ms)
 
     # end to end through the public API with host buffers (pinned), copies inside the timed region
     h_in = inp.t.cpu().pin_memory()
@@ -227,12 +226,8 @@ def run_secpe(a):
         h_out.copy_(out.t, non_blocking=True)
     f1.record(stream)
     torch.cuda.synchronize()
-    ms_e2e = f0.elapsed_time(f1)
-    if ws > 1:
-        t = torch.tensor([ms_e2e], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
-    e2e = queries / (ms_e2e / 1000.0)
+    ms_e2e = shard.max_over_ranks(f0.elapsed_time(f1), device="cuda")
+    e2e = shard.job_throughput(lay["queries"] * B * a.steps, ws, ms_e2e)
 
     if rank != 0:
         if ws > 1:

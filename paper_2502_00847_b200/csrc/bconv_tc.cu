@@ -19,6 +19,8 @@
 // (already in canonical layout) and copied to shared memory once per CTA.
 #include "context.h"
 
+#include <cstdlib>
+
 namespace {
 
 constexpr int TC_THREADS = 512;  // 16 warps: 4 groups of 4 warps share the targets in the epilogue
@@ -215,7 +217,12 @@ void k_bconv_tc(const TcArgs &a, int n_polys, cudaStream_t st) {
         attr = true;
     }
     const int ntiles = (int)((1L << a.logn) / TC_M);
-    const int tiles_per_cta = 4;
+    static int tiles_per_cta = 0;
+    if (!tiles_per_cta) {
+        const char *e = getenv("SECPE_TC_TPC");  // development switch
+        tiles_per_cta = e ? atoi(e) : 4;
+        if (tiles_per_cta < 1) tiles_per_cta = 1;
+    }
     const dim3 grid((ntiles + tiles_per_cta - 1) / tiles_per_cta, n_polys);
     bconv_tc_kernel<<<grid, TC_THREADS, tc_smem_bytes(), st>>>(a);
     LAUNCH_CHECK();
