@@ -125,6 +125,63 @@ def run_reference(a):
 # ------------------------------------------------------------------------------------------------
 # GPU arm
 # ------------------------------------------------------------------------------------------------
+def micro_configs(stream, reps=5):
+    """BASELINE configs[1]-[3] on one GPU (reported beside the headline; CUDA events, median of reps):
+    [1] 64 polys x 24 limbs NTT + INTT round trip; [2] 32 ciphertext pairs mul + relinearise + rescale
+    (one batched call); [3] 128 ciphertexts rotated by each of the 15 keys 2^k (one batched call per key)."""
+    import torch
+    import synth
+    from paper_2502_00847_b200 import secpe
+    peak, _ = peaks()
+
+    def t_ms(fn):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    out = {}
+    ctx = secpe.Context(synth.PARAM_SETS["ntt"], stream=stream.cuda_stream)
+    x = torch.from_numpy(synth.uniform_residues(2001, ctx.q, 64, ctx.logn)).cuda()
+    ms = t_ms(lambda: (ctx.ntt(x, 0, 24), ctx.ntt(x, 0, 24, inverse=True)))
+    gbs = 2 * 16 * ctx.N * 64 * 24 / (ms / 1000) / 1e9
+    out["configs[1]_ntt"] = {"ms_round_trip": ms, "limb_transforms_per_s": 2 * 64 * 24 / (ms / 1000),
+                             "alg_gbs": gbs, "frac_of_hbm": gbs / peak,
+                             "note": "60-bit primes: integer Shoup path (FMA-pipe bound, quarter-rate IMAD.WIDE)"}
+    del ctx, x
+    ctx = secpe.Context(synth.PARAM_SETS["ks"], stream=stream.cuda_stream)
+    keys = ctx.keygen(synth.KEY_SEED_BASE + 3, [1 << k for k in range(15)])
+    g = synth.rng(3001)
+    B = 32
+    a = ctx.new_ct(ctx.L, B)
+    b = ctx.new_ct(ctx.L, B)
+    for i in range(B):
+        for c, seed in ((a, 2 * i + 1), (b, 2 * i + 2)):
+            m = ctx.encode(g.uniform(-1, 1, ctx.N // 2), ctx.scale)
+            ctx.encrypt_coeffs(keys, m, ctx.L, ctx.scale, seed, out=secpe.Ct(c.t[i:i + 1], ctx.L, ctx.scale))
+    a.level = b.level = ctx.L
+    a.scale = b.scale = ctx.scale
+    o = ctx.new_ct(ctx.L - 1, B)
+    ms = t_ms(lambda: ctx.mul_relin_rescale(keys, a, b, out=o))
+    out["configs[2]_mul_relin_rescale"] = {"ms_per_batch": ms, "batch": B, "ops_per_s": B / (ms / 1000)}
+    R = 128
+    r = ctx.new_ct(ctx.L, R)
+    for i in range(R):
+        r.t[i].copy_(a.t[i % B])
+    r.level, r.scale = ctx.L, ctx.scale
+    ro = ctx.new_ct(ctx.L, R)
+    ms = t_ms(lambda: [ctx.rotate_batch(keys, r, 1 << k, out=ro) for k in range(15)])
+    out["configs[3]_rotation"] = {"ms_per_15_keys": ms, "cts": R, "rotations_per_s": 15 * R / (ms / 1000)}
+    return out
+
 def run_secpe(a):
     import torch
     import torch.distributed as dist
@@ -270,6 +327,8 @@ def run_secpe(a):
         "op_counts_per_step": {k: v / a.steps for k, v in counts.items()},
         "clocks": clk,
     }
+    if ws == 1 and not a.no_micro:
+        line["configs_1_to_3"] = micro_configs(stream)
     if ws == 1 and not a.no_cpu_baseline:
         dt, q, cores = oracle_argmax_once()
         line["cpu_baseline"] = {"value": q / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
@@ -289,6 +348,7 @@ def main():
     ap.add_argument("--batch", type=int, default=8, help="ciphertexts per rank per step")
     ap.add_argument("--impl", default="secpe", choices=["secpe", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-micro", action="store_true", help="skip the configs[1]-[3] lines")
     ap.add_argument("--ncu", action="store_true", help="run one profiled step (for ncu --profile-from-start off)")
     ap.add_argument("--ref-warmup", action="store_true", help="also run oracle warm-up steps (reference arm)")
     a = ap.parse_args()
