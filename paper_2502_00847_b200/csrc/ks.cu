@@ -122,6 +122,47 @@ __device__ __forceinline__ void ks_load(KsIn<MAXB> &in, int c, const u64 *__rest
     }
 }
 
+// Exact-FP64 tensor for primes < 2^46 (the configs[4] chain): operands < 2^46 are exact doubles;
+// w y mod q = fma(y, w, -k q) with k = rint(y w / q) (the ntt.cu FpA product), |r| <= 0.75 q, so the
+// FP64 pipe takes the products and the integer pipes keep only the key MACs.
+namespace fpt {
+constexpr double MAGIC = 6755399441055744.0, TWO52 = 4503599627370496.0;
+__device__ __forceinline__ double d(u64 x) {
+    return __dsub_rn(__longlong_as_double((long long)(x | 0x4330000000000000ULL)), TWO52);
+}
+__device__ __forceinline__ double mm(double y, double w, double wq, double qd) {
+    const double k = __dsub_rn(__fma_rn(y, wq, MAGIC), MAGIC);
+    const double ph = __dmul_rn(k, qd);
+    const double pl = __fma_rn(k, qd, -ph);
+    return __dsub_rn(__fma_rn(y, w, -ph), pl);
+}
+// canonical integer of an exact double |v| < 2^51
+__device__ __forceinline__ u64 canon(double v, double qd, double qinv) {
+    const double k = __dsub_rn(__dadd_rn(__dmul_rn(v, qinv), MAGIC), MAGIC);
+    double t = __fma_rn(-k, qd, v);
+    if (t < 0) t = __dadd_rn(t, qd);
+    return (u64)__double_as_longlong(__dadd_rn(t, TWO52)) & ((1ULL << 52) - 1);
+}
+}  // namespace fpt
+
+__device__ __forceinline__ void tensor1_fp(u64 a0, u64 a1, u64 b0, u64 b1, bool lin, u64 x0, u64 x1, u64 c, u64 q,
+                                           u64 &d0, u64 &d1, u64 &d2) {
+    const double qd = (double)q, qinv = 1.0 / qd;
+    const double A0 = fpt::d(a0), A1 = fpt::d(a1), B0 = fpt::d(b0), B1 = fpt::d(b1);
+    const double B0q = __dmul_rn(B0, qinv), B1q = __dmul_rn(B1, qinv);
+    double e0 = fpt::mm(A0, B0, B0q, qd);
+    double e1 = __dadd_rn(fpt::mm(A0, B1, B1q, qd), fpt::mm(A1, B0, B0q, qd));
+    const double e2 = fpt::mm(A1, B1, B1q, qd);
+    if (lin) {
+        const double C = fpt::d(c), Cq = __dmul_rn(C, qinv);
+        e0 = __dadd_rn(e0, fpt::mm(fpt::d(x0), C, Cq, qd));
+        e1 = __dadd_rn(e1, fpt::mm(fpt::d(x1), C, Cq, qd));
+    }
+    d0 = fpt::canon(e0, qd, qinv);
+    d1 = fpt::canon(e1, qd, qinv);
+    d2 = fpt::canon(e2, qd, qinv);
+}
+
 // one coefficient of the tensor: (d0, d1, d2) mod q, with the optional linear term C x
 __device__ __forceinline__ void tensor1(u64 a0, u64 a1, u64 b0, u64 b1, bool lin, u64 x0, u64 x1, u64 c, u64 csh,
                                         u64 q, u64 r0, u64 r1, u64 &d0, u64 &d1, u64 &d2) {
@@ -137,7 +178,7 @@ __device__ __forceinline__ void tensor1(u64 a0, u64 a1, u64 b0, u64 b1, bool lin
 }
 
 template <int MAXB, bool TEN>
-__global__ void __launch_bounds__(TPB, 2) ks_inner_vec_kernel(Tab tab, int logn, const u64 *__restrict__ d, long ds,
+__global__ void __launch_bounds__(TPB, TEN ? 2 : 3) ks_inner_vec_kernel(Tab tab, int logn, const u64 *__restrict__ d, long ds,
                                                            const u64 *__restrict__ ext, long exts,
                                                            const u64 *__restrict__ key, int nq_total, int np,
                                                            u64 *__restrict__ acc, long accs, int n_ct, int nl,
@@ -169,8 +210,15 @@ __global__ void __launch_bounds__(TPB, 2) ks_inner_vec_kernel(Tab tab, int logn,
         if (!TEN && c + 1 < n_ct) ks_load<MAXB, TEN>(nxt, c + 1, d, ds, ext, exts, e, jd, ne, nl, beta, N, k, ten);
         if (qrow) {
             u64 e0, e1, e2, f0, f1, f2;
-            tensor1(cur.a0.x, cur.a1.x, cur.b0.x, cur.b1.x, lin, cur.x0.x, cur.x1.x, cc, ccsh, q, r0, r1, e0, e1, e2);
-            tensor1(cur.a0.y, cur.a1.y, cur.b0.y, cur.b1.y, lin, cur.x0.y, cur.x1.y, cc, ccsh, q, r0, r1, f0, f1, f2);
+            if (q < (1ULL << 46)) {
+                tensor1_fp(cur.a0.x, cur.a1.x, cur.b0.x, cur.b1.x, lin, cur.x0.x, cur.x1.x, cc, q, e0, e1, e2);
+                tensor1_fp(cur.a0.y, cur.a1.y, cur.b0.y, cur.b1.y, lin, cur.x0.y, cur.x1.y, cc, q, f0, f1, f2);
+            } else {
+                tensor1(cur.a0.x, cur.a1.x, cur.b0.x, cur.b1.x, lin, cur.x0.x, cur.x1.x, cc, ccsh, q, r0, r1, e0, e1,
+                        e2);
+                tensor1(cur.a0.y, cur.a1.y, cur.b0.y, cur.b1.y, lin, cur.x0.y, cur.x1.y, cc, ccsh, q, r0, r1, f0, f1,
+                        f2);
+            }
 #pragma unroll
             for (int j = 0; j < MAXB; j++)
                 if (j == jd) cur.x[j] = make_ulonglong2(e2, f2);
