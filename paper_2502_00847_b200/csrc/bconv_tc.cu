@@ -51,6 +51,10 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
     uint8_t *sB = tsm + TC_M * TC_K;        // 8 * TC_TMAX * TC_K
     __shared__ __align__(8) uint64_t mbar;
     __shared__ uint32_t tslot;
+    // per-target constants staged once per CTA: prime, output row offset, 1/q, [P]_{q_t} (+ Shoup)
+    __shared__ u64 sq[TC_TMAX], spm[TC_TMAX], spmsh[TC_TMAX];
+    __shared__ double sqinv[TC_TMAX];
+    __shared__ long soff[TC_TMAX];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int p = blockIdx.y;
     const TcGroup &G = a.groups[a.grouped ? p % a.pdiv : 0];
@@ -63,6 +67,14 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tslot)),
                      "n"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid < nt) {
+        const u64 q = a.tab.q[G.prime[tid]];
+        sq[tid] = q;
+        sqinv[tid] = G.qinv[tid];
+        spm[tid] = G.pmod[tid];
+        spmsh[tid] = G.pmodsh[tid];
+        soff[tid] = (long)G.out_row[tid] << a.logn;
     }
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar)));
@@ -165,19 +177,17 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
         u64 r = 0;
         if (a.rr) {
             // fused ModDown + rescale prelude (target 0 = q_l): Y_l = (xc - T_l) P^{-1}, r = [Y_l + floor(q_l/2)]
-            const int pl = G.prime[0];
-            const u64 ql = a.tab.q[pl];
-            const u64 tl = reduce(0, ql, 1.0 / (double)ql);
+            const u64 ql = sq[0];
+            const u64 tl = reduce(0, ql, sqinv[0]);
             const u64 xc = src[(long)(-1) * N + k0 + m];
             r = csub(mul_shoup(submod(xc, tl, ql), a.pinv_l, a.pinv_l_sh, ql) + (ql >> 1), ql);
             t0 = 1;
         }
         for (int t = t0 + tpar; t < nt; t += 4) {
-            const int pr = G.prime[t];
-            const u64 q = a.tab.q[pr];
-            u64 z = reduce(t, q, 1.0 / (double)q);
-            if (a.rr) z = addmod(z, csub(mul_shoup(r, G.pmod[t], G.pmodsh[t], q), q), q);
-            dst[(long)G.out_row[t] * N + k0 + m] = z;
+            const u64 q = sq[t];
+            u64 z = reduce(t, q, sqinv[t]);
+            if (a.rr) z = addmod(z, csub(mul_shoup(r, spm[t], spmsh[t], q), q), q);
+            dst[soff[t] + k0 + m] = z;
         }
         asm volatile("tcgen05.fence::before_thread_sync;\n");
         __syncthreads();

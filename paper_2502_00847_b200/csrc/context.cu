@@ -307,6 +307,8 @@ void Ctx::build_tc_groups(LevelConsts &lc, int l) {
     }
     lc.tc_ok = ok;
     if (!ok) return;
+    for (auto &g : groups)
+        for (int t = 0; t < g.nt; t++) g.qinv[t] = 1.0 / (double)primes[g.prime[t]];
     // one device buffer for every B matrix; TcGroup.B point into it
     std::vector<size_t> off;
     size_t total = 0;

@@ -33,6 +33,7 @@ struct TcGroup {
     int out_row[TC_TMAX];    // output row (limb) of the target in the destination polynomial
     u64 pmod[TC_TMAX];       // rescale variant: [P]_{q_t} and its Shoup companion
     u64 pmodsh[TC_TMAX];
+    double qinv[TC_TMAX];    // RN(1 / q_t) for the FP64 quotient of the epilogue
 };
 struct TcArgs {
     const u64 *src;
