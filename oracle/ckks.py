@@ -544,10 +544,35 @@ class Oracle:
         self._log("MULC", lv, target_level, target_scale, str(C))
         return out
 
+    def lincomb(self, terms, target_scale, target_level):
+        """sum_i c_i x_i landing at (target_scale, target_level) with ONE rescale (reading R13): every
+        x_i dropped to l = target_level + 1, C_i = rha(c_i Delta_i), Delta_i = (S_t q_l) / S_{x_i},
+        integer products summed mod q, rescale, scale := S_t."""
+        lv = target_level + 1
+        acc, Cs = None, []
+        for x, c in terms:
+            x = self.drop(x, lv)
+            dc = (target_scale * float(self.prm.primes[lv])) / x.scale
+            C = round_half_away(c * dc)
+            if abs(C) >= 2 ** 62:
+                raise OverflowError("constant too large")
+            cx = self.mul_int_raw(x, C)
+            if acc is None:
+                acc = cx
+            else:
+                out = np.zeros_like(acc)
+                lib().o_add(self.prm.cptr, P(acc), P(cx), lv + 1, 2, P(out))
+                acc = out
+            Cs.append(str(C))
+        out = self.rescale(Ct(acc, target_scale * float(self.prm.primes[lv])), target_scale)
+        self._log("LINC", lv, target_level, target_scale, ",".join(Cs))
+        return out
+
     def mul_ct(self, keys, a, b, target_scale, target_level, lin=None):
-        """a (x) b [+ c x]: drop the inputs to target_level + 1 = l, tensor, optionally add the constant
-        product C x to (d0, d1) with C = rha(c Delta_c), Delta_c = (S_t q_l) / S_x (lin = (x, c); R9,
-        R13), relinearise, rescale.  Output scale := target_scale if given else (S_a * S_b) / q_l."""
+        """a (x) b [+ sum c x]: drop the inputs to target_level + 1 = l, tensor, optionally add the constant
+        products C x to (d0, d1) with C = rha(c Delta_c), Delta_c = (S_t q_l) / S_x (lin = (x, c) or a
+        list of such terms; R9, R13), relinearise, rescale.  Output scale := target_scale if given else
+        (S_a * S_b) / q_l."""
         lv = target_level + 1
         a = self.drop(a, lv)
         b = self.drop(b, lv)
@@ -555,17 +580,20 @@ class Oracle:
         d = self.tensor(a, b)
         extra = ""
         if lin is not None:
-            x, c = lin
-            x = self.drop(x, lv)
-            dc = (s * float(self.prm.primes[lv])) / x.scale
-            C = round_half_away(c * dc)
-            if abs(C) >= 2 ** 62:
-                raise OverflowError("constant too large")
-            cx = self.mul_int_raw(x, C)
-            d01 = np.zeros((2, lv + 1, self.prm.N), dtype=np.uint64)
-            lib().o_add(self.prm.cptr, P(np.ascontiguousarray(d[:2])), P(cx), lv + 1, 2, P(d01))
-            d[:2] = d01
-            extra = str(C)
+            terms = lin if isinstance(lin, list) else [lin]
+            Cs = []
+            for x, c in terms:
+                x = self.drop(x, lv)
+                dc = (s * float(self.prm.primes[lv])) / x.scale
+                C = round_half_away(c * dc)
+                if abs(C) >= 2 ** 62:
+                    raise OverflowError("constant too large")
+                cx = self.mul_int_raw(x, C)
+                d01 = np.zeros((2, lv + 1, self.prm.N), dtype=np.uint64)
+                lib().o_add(self.prm.cptr, P(np.ascontiguousarray(d[:2])), P(cx), lv + 1, 2, P(d01))
+                d[:2] = d01
+                Cs.append(str(C))
+            extra = ",".join(Cs)
         out = self.rescale(self.mul_relin(keys, a, b, d), s)
         self._log("MULCT", lv, target_level, s, extra)
         return out
@@ -639,6 +667,17 @@ class Mirror:
         self._log("MULC", lv, target_level, target_scale, str(C))
         return MirrorCt(c * x.v, target_level, target_scale)
 
+    def lincomb(self, terms, target_scale, target_level):
+        lv = target_level + 1
+        v, Cs = 0.0, []
+        for x, c in terms:
+            if x.level < lv:
+                raise ValueError("level")
+            Cs.append(str(round_half_away(c * ((target_scale * float(self.prm.primes[lv])) / x.scale))))
+            v = v + c * x.v
+        self._log("LINC", lv, target_level, target_scale, ",".join(Cs))
+        return MirrorCt(v, target_level, target_scale)
+
     def mul_ct(self, keys, a, b, target_scale, target_level, lin=None):
         lv = target_level + 1
         if a.level < lv or b.level < lv:
@@ -647,11 +686,14 @@ class Mirror:
         v = a.v * b.v
         extra = ""
         if lin is not None:
-            x, c = lin
-            if x.level < lv:
-                raise ValueError("level")
-            extra = str(round_half_away(c * ((s * float(self.prm.primes[lv])) / x.scale)))
-            v = v + c * x.v
+            terms = lin if isinstance(lin, list) else [lin]
+            Cs = []
+            for x, c in terms:
+                if x.level < lv:
+                    raise ValueError("level")
+                Cs.append(str(round_half_away(c * ((s * float(self.prm.primes[lv])) / x.scale))))
+                v = v + c * x.v
+            extra = ",".join(Cs)
         self._log("MULCT", lv, target_level, s, extra)
         return MirrorCt(v, target_level, s)
 

@@ -17,8 +17,10 @@ import numpy as np
 
 
 def poly_depth(deg):
-    """Multiplicative depth of the plan for an odd degree-`deg` polynomial: ceil(log2(deg+1))."""
-    return int(math.ceil(math.log2(deg + 1)))
+    """Multiplicative depth of the plan for an odd degree-`deg` polynomial: ceil(log2(deg+1)) for the
+    BSGS plans of degree 3 and 7, one more for degree 15 (Paterson-Stockmeyer with a shared x^3:
+    7 ct x ct products instead of 10, reading R13)."""
+    return 5 if deg == 15 else int(math.ceil(math.log2(deg + 1)))
 
 
 def eval_odd_poly(ev, keys, x, coeffs, target_scale):
@@ -58,11 +60,19 @@ def eval_odd_poly(ev, keys, x, coeffs, target_scale):
         return A(0, target_scale, l - 2)
     if deg == 7:
         return B(0, target_scale, l - 3)
-    L = l - 4
-    hi = B(1, (target_scale * q(L + 1)) / x8.scale, L + 1)
-    prod = ev.mul_ct(keys, hi, x8, target_scale, L)
-    lo = B(0, target_scale, L)
-    return ev.add(prod, lo)
+    # degree 15, Paterson-Stockmeyer (R13): baby steps x, x^3 (shared), giant steps x^4, x^8;
+    # q_k = c_{4k+1} x + c_{4k+3} x^3 are linear combinations (one rescale each, or folded into the
+    # product they are summed with); p = (q_1 x^4 + q_0) + (q_3 x^4 + q_2) x^8 at depth 5
+    T, Lo = target_scale, l - 5
+    x3 = ev.mul_ct(keys, x, x2, None, l - 2)
+    c = coeffs
+    S_b1 = (T * q(l - 4)) / x8.scale
+    q3 = ev.lincomb([(x, c[13]), (x3, c[15])], (S_b1 * q(l - 3)) / x4.scale, l - 3)
+    b1 = ev.mul_ct(keys, q3, x4, S_b1, l - 4, lin=[(x, c[9]), (x3, c[11])])
+    hi = ev.mul_ct(keys, b1, x8, T, Lo)
+    q1 = ev.lincomb([(x, c[5]), (x3, c[7])], (T * q(l - 4)) / x4.scale, l - 4)
+    b0 = ev.mul_ct(keys, q1, x4, T, Lo, lin=[(x, c[1]), (x3, c[3])])
+    return ev.add(b0, hi)
 
 
 def sign(ev, keys, x, stages, target_scale):

@@ -170,7 +170,8 @@ void ev_mul_relin(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const
 // a (x) b [+ C x] relinearised and rescaled by q_l in one pass (bit-identical to ev_mul_relin then
 // ev_rescale); out at level a.level - 1.  lin_x: optional linear term (nullptr: none), C its constant
 void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const CtView *lin_x, i64 C,
-                          const CtView &out);
+                          const CtView &out, const CtView *lin_x2 = nullptr, i64 C2 = 0);
+void ev_lincomb(Ctx &c, const CtView &a, i64 C1, const CtView *b, i64 C2, const CtView &out);
 void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView &out);
 void ev_mul_plain_ntt(Ctx &c, const CtView &a, const u64 *pt, const CtView &out);
 LimbConst limb_const(const Ctx &c, i64 C, int nl);

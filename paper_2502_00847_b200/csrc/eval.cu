@@ -68,6 +68,14 @@ void ev_add_int(Ctx &c, const CtView &a, i64 C, const CtView &out) {
     }
 }
 
+// C1 a + C2 b (b may be null) at out's level (no rescale; the planner rescales the sum once)
+void ev_lincomb(Ctx &c, const CtView &a, i64 C1, const CtView *b, i64 C2, const CtView &out) {
+    const int nl = out.level + 1;
+    k_lincomb2(c.tab, c.logn, crows_of(a), b ? crows_of(*b) : CRows{nullptr, 0, 0}, rows_of(out), 2 * a.n, qmap(nl),
+               limb_const(c, C1, nl), b ? limb_const(c, C2, nl) : LimbConst{}, c.st);
+    c.cnt.launches++;
+}
+
 void ev_mul_plain_ntt(Ctx &c, const CtView &a, const u64 *pt, const CtView &out) {
     const int nl = out.level + 1;
     k_mul_poly(c.tab, c.logn, crows_of(a), pt, rows_of(out), 2 * a.n, qmap(nl), c.st);
@@ -218,7 +226,7 @@ void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u
 // corrections are computed in the coefficient domain (k_rr_conv) and removed by ONE forward NTT whose
 // epilogue forms (x_i - NTT(T_i)) (P q_l)^{-1}.  This saves the rescale's own INTT/NTT round trip.
 void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const CtView *lin_x, i64 C,
-                          const CtView &out) {
+                          const CtView &out, const CtView *lin_x2, i64 C2) {
     const int l = a.level, nl = l + 1;
     if (l < 1) throw SecpeError{-2, "mul_relin_rescale: no level left"};
     if (b.level != l || out.level != l - 1) throw SecpeError{-1, "mul_relin_rescale: levels"};
@@ -233,6 +241,10 @@ void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &
     if (lin_x) {
         ten.x = crows_of(*lin_x);
         ten.C = limb_const(c, C, nl);
+    }
+    if (lin_x2) {
+        ten.x2 = crows_of(*lin_x2);
+        ten.C2 = limb_const(c, C2, nl);
     }
     const size_t pa = c.prof_begin(1);
     DevBuf acc;

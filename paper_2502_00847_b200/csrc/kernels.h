@@ -55,6 +55,9 @@ void k_copy_rows(int logn, CRows a, RowsArg out, int n_polys, int nl, cudaStream
 // out = a * c_l (Shoup, per-limb constant residues)
 void k_mul_const(const Tab &tab, int logn, CRows a, RowsArg out, int n_polys, LimbMap lm,
                  const LimbConst &c, cudaStream_t st);
+// out = C1 a + C2 b (b.p == nullptr: C1 a); per-limb constant residues with Shoup companions
+void k_lincomb2(const Tab &tab, int logn, CRows a, CRows b, RowsArg out, int n_polys, LimbMap lm,
+                const LimbConst &c1, const LimbConst &c2, cudaStream_t st);
 // out = a + c_l (only the rows given)
 void k_add_const(const Tab &tab, int logn, CRows a, RowsArg out, int n_polys, LimbMap lm,
                  const LimbConst &c, cudaStream_t st);
@@ -84,6 +87,8 @@ void k_modup(const Tab &tab, int logn, const u64 *dc, long dc_ct_stride, u64 *ex
 struct TensorSrc {
     CRows a, b, x;  // ciphertext views (c0 at p + ct * cs, c1 at + ps); x.p == nullptr: no linear term
     LimbConst C;    // per-limb residues of the linear term's integer constant (Shoup companions)
+    CRows x2;       // optional second linear term C2 x2 (x2.p == nullptr: none)
+    LimbConst C2;
 };
 void k_ks_inner(const Tab &tab, int logn, const u64 *d, long d_ct_stride, const u64 *ext, long ext_ct_stride,
                 const u64 *key, int nq_total, int np, u64 *acc, long acc_ct_stride, int n_ct, int nl,

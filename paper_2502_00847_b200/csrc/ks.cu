@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(TPB) modup_kernel(Tab tab, int logn, const u64
 // (beta <= 4); larger dnum uses the scalar ks_inner_kernel below.
 template <int MAXB>
 struct KsIn {
-    ulonglong2 x[MAXB], d0, d1, a0, a1, b0, b1, x0, x1;
+    ulonglong2 x[MAXB], d0, d1, a0, a1, b0, b1, x0, x1, y0, y1;
 };
 template <int MAXB, bool TEN>
 __device__ __forceinline__ void ks_load(KsIn<MAXB> &in, int c, const u64 *__restrict__ d, long ds,
@@ -118,6 +118,10 @@ __device__ __forceinline__ void ks_load(KsIn<MAXB> &in, int c, const u64 *__rest
         if (ten.x.p) {
             in.x0 = ldv2(ten.x.p + c * ten.x.cs + o);
             in.x1 = ldv2(ten.x.p + c * ten.x.cs + ten.x.ps + o);
+        }
+        if (ten.x2.p) {
+            in.y0 = ldv2(ten.x2.p + c * ten.x2.cs + o);
+            in.y1 = ldv2(ten.x2.p + c * ten.x2.cs + ten.x2.ps + o);
         }
     }
 }
@@ -145,8 +149,8 @@ __device__ __forceinline__ u64 canon(double v, double qd, double qinv) {
 }
 }  // namespace fpt
 
-__device__ __forceinline__ void tensor1_fp(u64 a0, u64 a1, u64 b0, u64 b1, bool lin, u64 x0, u64 x1, u64 c, u64 q,
-                                           u64 &d0, u64 &d1, u64 &d2) {
+__device__ __forceinline__ void tensor1_fp(u64 a0, u64 a1, u64 b0, u64 b1, bool lin, u64 x0, u64 x1, u64 c,
+                                           bool lin2, u64 y0, u64 y1, u64 c2, u64 q, u64 &d0, u64 &d1, u64 &d2) {
     const double qd = (double)q, qinv = 1.0 / qd;
     const double A0 = fpt::d(a0), A1 = fpt::d(a1), B0 = fpt::d(b0), B1 = fpt::d(b1);
     const double B0q = __dmul_rn(B0, qinv), B1q = __dmul_rn(B1, qinv);
@@ -158,6 +162,11 @@ __device__ __forceinline__ void tensor1_fp(u64 a0, u64 a1, u64 b0, u64 b1, bool 
         e0 = __dadd_rn(e0, fpt::mm(fpt::d(x0), C, Cq, qd));
         e1 = __dadd_rn(e1, fpt::mm(fpt::d(x1), C, Cq, qd));
     }
+    if (lin2) {
+        const double C = fpt::d(c2), Cq = __dmul_rn(C, qinv);
+        e0 = __dadd_rn(e0, fpt::mm(fpt::d(y0), C, Cq, qd));
+        e1 = __dadd_rn(e1, fpt::mm(fpt::d(y1), C, Cq, qd));
+    }
     d0 = fpt::canon(e0, qd, qinv);
     d1 = fpt::canon(e1, qd, qinv);
     d2 = fpt::canon(e2, qd, qinv);
@@ -165,7 +174,8 @@ __device__ __forceinline__ void tensor1_fp(u64 a0, u64 a1, u64 b0, u64 b1, bool 
 
 // one coefficient of the tensor: (d0, d1, d2) mod q, with the optional linear term C x
 __device__ __forceinline__ void tensor1(u64 a0, u64 a1, u64 b0, u64 b1, bool lin, u64 x0, u64 x1, u64 c, u64 csh,
-                                        u64 q, u64 r0, u64 r1, u64 &d0, u64 &d1, u64 &d2) {
+                                        bool lin2, u64 y0, u64 y1, u64 c2, u64 c2sh, u64 q, u64 r0, u64 r1, u64 &d0,
+                                        u64 &d1, u64 &d2) {
     d0 = mulmod(a0, b0, q, r0, r1);
     U128 t = mul_wide(a0, b1);
     mac_wide(t, a1, b0);
@@ -174,6 +184,10 @@ __device__ __forceinline__ void tensor1(u64 a0, u64 a1, u64 b0, u64 b1, bool lin
     if (lin) {
         d0 = addmod(d0, mul_shoup(x0, c, csh, q), q);
         d1 = addmod(d1, mul_shoup(x1, c, csh, q), q);
+    }
+    if (lin2) {
+        d0 = addmod(d0, mul_shoup(y0, c2, c2sh, q), q);
+        d1 = addmod(d1, mul_shoup(y1, c2, c2sh, q), q);
     }
 }
 
@@ -200,8 +214,9 @@ __global__ void __launch_bounds__(TPB, TEN ? 2 : 3) ks_inner_vec_kernel(Tab tab,
     const int jd = e < nl ? e / alpha : -1;  // digit containing e (Q limbs only)
     const bool qrow = TEN && e < nl;         // relinearise-and-rescale: x_b = acc_b + [P]_{q_e} d_b on Q limbs
     const u64 pm = qrow ? pmod[e] : 0;
-    const bool lin = TEN && ten.x.p;
+    const bool lin = TEN && ten.x.p, lin2 = TEN && ten.x2.p;
     const u64 cc = lin && e < nl ? ten.C.c[e] : 0, ccsh = lin && e < nl ? ten.C.csh[e] : 0;
+    const u64 c2 = lin2 && e < nl ? ten.C2.c[e] : 0, c2sh = lin2 && e < nl ? ten.C2.csh[e] : 0;
     // plain key switching double-buffers the next ciphertext's inputs; with the tensor formed on the fly
     // the register budget goes to the tensor terms instead (single buffer)
     KsIn<MAXB> cur, nxt;
@@ -211,13 +226,15 @@ __global__ void __launch_bounds__(TPB, TEN ? 2 : 3) ks_inner_vec_kernel(Tab tab,
         if (qrow) {
             u64 e0, e1, e2, f0, f1, f2;
             if (q < (1ULL << 46)) {
-                tensor1_fp(cur.a0.x, cur.a1.x, cur.b0.x, cur.b1.x, lin, cur.x0.x, cur.x1.x, cc, q, e0, e1, e2);
-                tensor1_fp(cur.a0.y, cur.a1.y, cur.b0.y, cur.b1.y, lin, cur.x0.y, cur.x1.y, cc, q, f0, f1, f2);
+                tensor1_fp(cur.a0.x, cur.a1.x, cur.b0.x, cur.b1.x, lin, cur.x0.x, cur.x1.x, cc, lin2, cur.y0.x,
+                           cur.y1.x, c2, q, e0, e1, e2);
+                tensor1_fp(cur.a0.y, cur.a1.y, cur.b0.y, cur.b1.y, lin, cur.x0.y, cur.x1.y, cc, lin2, cur.y0.y,
+                           cur.y1.y, c2, q, f0, f1, f2);
             } else {
-                tensor1(cur.a0.x, cur.a1.x, cur.b0.x, cur.b1.x, lin, cur.x0.x, cur.x1.x, cc, ccsh, q, r0, r1, e0, e1,
-                        e2);
-                tensor1(cur.a0.y, cur.a1.y, cur.b0.y, cur.b1.y, lin, cur.x0.y, cur.x1.y, cc, ccsh, q, r0, r1, f0, f1,
-                        f2);
+                tensor1(cur.a0.x, cur.a1.x, cur.b0.x, cur.b1.x, lin, cur.x0.x, cur.x1.x, cc, ccsh, lin2, cur.y0.x,
+                        cur.y1.x, c2, c2sh, q, r0, r1, e0, e1, e2);
+                tensor1(cur.a0.y, cur.a1.y, cur.b0.y, cur.b1.y, lin, cur.x0.y, cur.x1.y, cc, ccsh, lin2, cur.y0.y,
+                        cur.y1.y, c2, c2sh, q, r0, r1, f0, f1, f2);
             }
 #pragma unroll
             for (int j = 0; j < MAXB; j++)
@@ -269,11 +286,12 @@ __global__ void ks_inner_kernel(Tab tab, int logn, const u64 *__restrict__ d, lo
         u64 d0 = 0, d1 = 0, d2 = 0;
         if (qrow) {
             const long o = e * N + k;
-            const bool lin = ten.x.p != nullptr;
+            const bool lin = ten.x.p != nullptr, lin2 = ten.x2.p != nullptr;
             tensor1(ten.a.p[c * ten.a.cs + o], ten.a.p[c * ten.a.cs + ten.a.ps + o], ten.b.p[c * ten.b.cs + o],
                     ten.b.p[c * ten.b.cs + ten.b.ps + o], lin, lin ? ten.x.p[c * ten.x.cs + o] : 0,
-                    lin ? ten.x.p[c * ten.x.cs + ten.x.ps + o] : 0, lin ? ten.C.c[e] : 0, lin ? ten.C.csh[e] : 0, q,
-                    r0, r1, d0, d1, d2);
+                    lin ? ten.x.p[c * ten.x.cs + ten.x.ps + o] : 0, lin ? ten.C.c[e] : 0, lin ? ten.C.csh[e] : 0,
+                    lin2, lin2 ? ten.x2.p[c * ten.x2.cs + o] : 0, lin2 ? ten.x2.p[c * ten.x2.cs + ten.x2.ps + o] : 0,
+                    lin2 ? ten.C2.c[e] : 0, lin2 ? ten.C2.csh[e] : 0, q, r0, r1, d0, d1, d2);
         }
         for (int j = 0; j < beta; j++) {
             const u64 x = (j == jd) ? (qrow ? d2 : d[c * ds + e * N + k]) : ext[c * exts + ((long)j * ne + e) * N + k];

@@ -49,6 +49,24 @@ __global__ void mul_const_kernel(Tab tab, int logn, CRows a, RowsArg out, LimbMa
     st2(out.p + poly_off(out.cs, out.ps, poly) + off + k, x);
 }
 
+// out = C1 a + C2 b (per-limb constant residues, Shoup); b.p == nullptr: out = C1 a
+__global__ void lincomb2_kernel(Tab tab, int logn, CRows a, CRows b, RowsArg out, LimbMap lm, LimbConst c1,
+                                LimbConst c2) {
+    const int nl = lm.nl, poly = blockIdx.y / nl, limb = blockIdx.y % nl;
+    const u64 q = tab.q[prime_of(lm, limb)];
+    const long off = (long)limb << logn;
+    const long k = 2L * (blockIdx.x * TPB + threadIdx.x);
+    ulonglong2 x = ld2(a.p + poly_off(a.cs, a.ps, poly) + off + k);
+    x.x = mul_shoup(x.x, c1.c[limb], c1.csh[limb], q);
+    x.y = mul_shoup(x.y, c1.c[limb], c1.csh[limb], q);
+    if (b.p) {
+        const ulonglong2 y = ld2(b.p + poly_off(b.cs, b.ps, poly) + off + k);
+        x.x = addmod(x.x, mul_shoup(y.x, c2.c[limb], c2.csh[limb], q), q);
+        x.y = addmod(x.y, mul_shoup(y.y, c2.c[limb], c2.csh[limb], q), q);
+    }
+    st2(out.p + poly_off(out.cs, out.ps, poly) + off + k, x);
+}
+
 __global__ void add_const_kernel(Tab tab, int logn, CRows a, RowsArg out, LimbMap lm, LimbConst c) {
     const int nl = lm.nl, poly = blockIdx.y / nl, limb = blockIdx.y % nl;
     const u64 q = tab.q[prime_of(lm, limb)];
@@ -141,6 +159,11 @@ void k_copy_rows(int logn, CRows a, RowsArg out, int n_polys, int nl, cudaStream
 void k_mul_const(const Tab &tab, int logn, CRows a, RowsArg out, int n_polys, LimbMap lm, const LimbConst &c,
                  cudaStream_t st) {
     mul_const_kernel<<<grid_rows(logn, n_polys * lm.nl), TPB, 0, st>>>(tab, logn, a, out, lm, c);
+    LAUNCH_CHECK();
+}
+void k_lincomb2(const Tab &tab, int logn, CRows a, CRows b, RowsArg out, int n_polys, LimbMap lm,
+                const LimbConst &c1, const LimbConst &c2, cudaStream_t st) {
+    lincomb2_kernel<<<grid_rows(logn, n_polys * lm.nl), TPB, 0, st>>>(tab, logn, a, b, out, lm, c1, c2);
     LAUNCH_CHECK();
 }
 void k_add_const(const Tab &tab, int logn, CRows a, RowsArg out, int n_polys, LimbMap lm, const LimbConst &c,

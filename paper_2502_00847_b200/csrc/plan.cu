@@ -77,26 +77,56 @@ struct Ev {
         c.log("MULC", lv, Lt, St, std::to_string((long long)C));
         return out;
     }
-    // a (x) b [+ lc x] relinearised and rescaled in one step (R11b); St = NAN: natural scale (S_a S_b) / q_l.
-    // The linear term uses C = rha(lc Delta_c), Delta_c = (S_t q_l) / S_x (R9, R13).
-    Val mul_ct(const Val &a, const Val &b, double St, int Lt, const Val *linx = nullptr, double lc = 0.0) {
+    // integer constant C = rha(c Delta), Delta = (S_t q_l) / S_x (R9)
+    i64 lin_const(double cval, double St, int lv, double Sx) {
+        const double dc = (St * q(lv)) / Sx;
+        const double Cd = round_half_away(cval * dc);
+        if (!(std::fabs(Cd) < 4611686018427387904.0)) throw SecpeError{-6, "constant exceeds 2^62"};
+        return (i64)Cd;
+    }
+    using Lin = std::vector<std::pair<const Val *, double>>;
+    static std::string join(const std::vector<i64> &v) {
+        std::string r;
+        for (size_t i = 0; i < v.size(); i++) r += (i ? "," : "") + std::to_string((long long)v[i]);
+        return r;
+    }
+    // a (x) b [+ sum c x] relinearised and rescaled in one pass; St = NAN: natural scale (S_a S_b) / q_l.
+    // Up to two linear terms join the product before its rescale (R13).
+    Val mul_ct(const Val &a, const Val &b, double St, int Lt, const Lin &lin = {}) {
         const int lv = Lt + 1;
         if (lv < 1) throw SecpeError{-2, "mul_ct: no level left"};
+        if (lin.size() > 2) throw SecpeError{-1, "mul_ct: at most two linear terms"};
         Val ad = drop(a, lv), bd = drop(b, lv);
         const double s = std::isnan(St) ? (a.scale() * b.scale()) / q(lv) : St;
         Val out = fresh(Lt, s);
-        if (linx) {
-            Val xd = drop(*linx, lv);
-            const double dc = (s * q(lv)) / linx->scale();
-            const double Cd = round_half_away(lc * dc);
-            if (!(std::fabs(Cd) < 4611686018427387904.0)) throw SecpeError{-6, "constant exceeds 2^62"};
-            const i64 C = (i64)Cd;
-            ev_mul_relin_rescale(c, k, ad.v, bd.v, &xd.v, C, out.v);
-            c.log("MULCT", lv, Lt, s, std::to_string((long long)C));
-        } else {
-            ev_mul_relin_rescale(c, k, ad.v, bd.v, nullptr, 0, out.v);
-            c.log("MULCT", lv, Lt, s, "");
+        std::vector<Val> xs;
+        std::vector<i64> Cs;
+        for (auto &t : lin) {
+            xs.push_back(drop(*t.first, lv));
+            Cs.push_back(lin_const(t.second, s, lv, t.first->scale()));
         }
+        ev_mul_relin_rescale(c, k, ad.v, bd.v, xs.size() > 0 ? &xs[0].v : nullptr, xs.size() > 0 ? Cs[0] : 0, out.v,
+                             xs.size() > 1 ? &xs[1].v : nullptr, xs.size() > 1 ? Cs[1] : 0);
+        c.log("MULCT", lv, Lt, s, join(Cs));
+        return out;
+    }
+    // sum c_i x_i (one or two terms) at (St, Lt) with a single rescale (R13)
+    Val lincomb(const Lin &terms, double St, int Lt) {
+        const int lv = Lt + 1;
+        if (lv < 1) throw SecpeError{-2, "lincomb: no level left"};
+        if (terms.empty() || terms.size() > 2) throw SecpeError{-1, "lincomb: one or two terms"};
+        std::vector<Val> xs;
+        std::vector<i64> Cs;
+        for (auto &t : terms) {
+            xs.push_back(drop(*t.first, lv));
+            Cs.push_back(lin_const(t.second, St, lv, t.first->scale()));
+        }
+        Val tmp = fresh(lv, St * q(lv));
+        ev_lincomb(c, xs[0].v, Cs[0], xs.size() > 1 ? &xs[1].v : nullptr, xs.size() > 1 ? Cs[1] : 0, tmp.v);
+        Val out = fresh(Lt, St);
+        ev_rescale(c, tmp.v, out.v);
+        c.cnt.mulconst += n;
+        c.log("LINC", lv, Lt, St, join(Cs));
         return out;
     }
     Val mul_mask(const Val &x, const std::vector<double> &mask, double St) {
@@ -138,7 +168,7 @@ struct Ev {
         auto A = [&](int i, double S, int L) {
             // (c_{4i+3} x) x^2 + c_{4i+1} x: the linear term joins the product before its rescale (R13)
             Val inner = mul_const(x, cf[4 * i + 3], (S * q(L + 1)) / x2.scale(), L + 1);
-            return mul_ct(inner, x2, S, L, &x, cf[4 * i + 1]);
+            return mul_ct(inner, x2, S, L, {{&x, cf[4 * i + 1]}});
         };
         auto B = [&](int i, double S, int L) {
             Val hi = A(2 * i + 1, (S * q(L + 1)) / x4.scale(), L + 1);
@@ -148,11 +178,17 @@ struct Ev {
         };
         if (deg == 3) return A(0, T, l - 2);
         if (deg == 7) return B(0, T, l - 3);
-        const int L = l - 4;
-        Val hi = B(1, (T * q(L + 1)) / x8.scale(), L + 1);
-        Val prod = mul_ct(hi, x8, T, L);
-        Val lo = B(0, T, L);
-        return add(prod, lo);
+        // degree 15, Paterson-Stockmeyer (R13): x^3 shared, q_k = c_{4k+1} x + c_{4k+3} x^3 linear
+        // combinations, p = (q_1 x^4 + q_0) + (q_3 x^4 + q_2) x^8 at depth 5 with 7 ct x ct products
+        const int Lo = l - 5;
+        Val x3 = mul_ct(x, x2, NAN, l - 2);
+        const double Sb1 = (T * q(l - 4)) / x8.scale();
+        Val q3 = lincomb({{&x, cf[13]}, {&x3, cf[15]}}, (Sb1 * q(l - 3)) / x4.scale(), l - 3);
+        Val b1 = mul_ct(q3, x4, Sb1, l - 4, {{&x, cf[9]}, {&x3, cf[11]}});
+        Val hi = mul_ct(b1, x8, T, Lo);
+        Val q1 = lincomb({{&x, cf[5]}, {&x3, cf[7]}}, (T * q(l - 4)) / x4.scale(), l - 4);
+        Val b0 = mul_ct(q1, x4, T, Lo, {{&x, cf[1]}, {&x3, cf[3]}});
+        return add(b0, hi);
     }
     Val sign(Val x, const SignCfg &cfg, double T) {
         for (size_t i = 0; i < cfg.stages.size(); i++) {
@@ -171,7 +207,7 @@ struct Ev {
         Val g = mul_const(d, 0.5, (Sy * q(Ls)) / s.scale(), Ls);
         Val ry = add(r, y);
         // (r - y)/2 Sign(r - y) + (r + y)/2: the half-sum joins the product before its rescale
-        return mul_ct(g, s, Sy, Ls - 1, &ry, 0.5);
+        return mul_ct(g, s, Sy, Ls - 1, {{&ry, 0.5}});
     }
     // Algorithm 1 with the H1..H6 steps of DESIGN.md section 2
     Val argmax(const Val &in, const Layout &lay, const SignCfg &cfg) {
@@ -196,7 +232,8 @@ static int ilog2(int v) {
     while ((1 << r) < v) r++;
     return r;
 }
-static int poly_depth(int deg) { return ilog2(deg + 1); }
+// BSGS depth ceil(log2(d+1)) for degrees 3 and 7; the degree-15 Paterson-Stockmeyer plan uses one more
+static int poly_depth(int deg) { return deg == 15 ? 5 : ilog2(deg + 1); }
 
 int sign_depth(const SignCfg &cfg) {
     int d = 0;

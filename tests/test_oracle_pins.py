@@ -398,12 +398,18 @@ def test_sign_plan_equals_horner(sname):
     x = np.linspace(-1, 1, 2001)
     out = plan.sign(mir, None, ckks.MirrorCt(x, prm.L, prm.scale), st, prm.scale)
     assert np.abs(out.v - horner(st, x)).max() < 1e-9
-    assert out.level == prm.L - plan.sign_depth(st)  # depth law sum ceil(log2(d+1))
-    assert plan.sign_depth(st) == sum(math.ceil(math.log2(len(c))) for c in st)
+    assert out.level == prm.L - plan.sign_depth(st)
+    # depth law (ceil(log2(d+1)) for a BSGS plan), except degree 15 whose
+    # Paterson-Stockmeyer plan (R13) trades one level for three fewer ct x ct products
+    assert plan.sign_depth(st) == sum(math.ceil(math.log2(len(c))) + (len(c) == 16) for c in st)
+    nprod = {4: 2, 8: 5, 16: 7}  # ct x ct products per stage: deg 3, 7 (BSGS), 15 (PS)
+    assert sum(1 for l in mir.log if l.startswith("MULCT ")) == sum(nprod[len(c)] for c in st)
     # odd symmetry S(-x) = -S(x)
     assert np.abs(horner(st, -x) + horner(st, x)).max() < 1e-9
     # every planned addition saw identical scales, constants fit 62 bits
     assert all(abs(int(l.split()[4])) < 2 ** 62 for l in mir.log if l.startswith("MULC "))
+    assert all(abs(int(v)) < 2 ** 62 for l in mir.log if l.startswith(("LINC ", "MULCT ")) and len(l.split()) > 4
+               for v in l.split()[4].split(","))
 
 
 def test_sign_certificate_7_15_15():
@@ -492,7 +498,7 @@ def test_argmax_mirror_random_labels():
     gap = np.abs(mean[:, 0] - mean[:, 1])
     ok = gap >= 2.0 ** -7
     assert (plan.labels(out.v, lay)[ok] == plan.true_labels(scores)[ok]).all()
-    assert out.level == prm.L - plan.argmax_depth(lay, st) == 5
+    assert out.level == prm.L - plan.argmax_depth(lay, st) == 1  # 1 + (13 + 1) + 13 = 28 of 29 levels
 
 
 @pytest.mark.slow
@@ -530,7 +536,7 @@ def test_argmax_small_ring_7_15_15_oracle():
     out = plan.argmax(ev, keys, ct, lay, st)
     mir = ckks.Mirror(prm)
     ref = plan.argmax(mir, None, ckks.MirrorCt(z, prm.L, prm.scale), lay, st)
-    assert ev.log == mir.log and out.level == 5
+    assert ev.log == mir.log and out.level == 1
     dec = ev.decrypt(keys, out).real
     assert np.abs(dec - ref.v).max() < 2 ** -10
     mean = scores.mean(axis=1)
