@@ -156,12 +156,16 @@ static void ks_modup_inner(Ctx &c, const u64 *d, long d_stride, int n, int level
     } else {
         k_modup(c.tab, c.logn, dc.p, (long)nl * N, ext.p, exts, n, nl, np, c.nq, c.alpha, lc.hat.p, c.st);
     }
+    // NTT of the converted limbs: the Q limbs outside each digit per digit, then the special limbs of
+    // every digit of every ciphertext in one launch (n beta polynomials of np rows, stride ne N)
     for (int j = 0; j < bt; j++) {
         const int i0 = j * c.alpha, i1 = std::min(i0 + c.alpha, nl);
         if (i0 > 0) ev_ntt(c, RowsArg{ext.p + (long)j * ne * N, 2 * exts, exts}, n, LimbMap{i0, i0, 0, 0}, false);
-        ev_ntt(c, RowsArg{ext.p + ((long)j * ne + i1) * N, 2 * exts, exts}, n, LimbMap{ne - i1, nl - i1, i1, c.nq},
-               false);
+        if (i1 < nl)
+            ev_ntt(c, RowsArg{ext.p + ((long)j * ne + i1) * N, 2 * exts, exts}, n, LimbMap{nl - i1, nl - i1, i1, 0},
+                   false);
     }
+    ev_ntt(c, RowsArg{ext.p + (long)nl * N, 2L * ne * N, (long)ne * N}, n * bt, LimbMap{np, 0, 0, c.nq}, false);
     // 3. inner product with the switching key
     const long accs = 2L * ne * N;
     acc = DevBuf((size_t)n * accs, c.st);

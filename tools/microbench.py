@@ -80,7 +80,7 @@ def bench_ks(reps, stream, out):
 
 
 def bench_argmax(reps, stream, out, B=8):
-    ctx = secpe.Context(synth.PARAM_SETS["argmax"], stream=stream.cuda_stream)
+    ctx = secpe.Context(synth.PARAM_SETS[os.environ.get("SECPE_PSET", "argmax")], stream=stream.cuda_stream)
     lay = synth.LAYOUTS["argmax_k2"]
     st = [list(map(float, c)) for c in json.load(open(os.path.join(ROOT, "data", "sign_7_15_15.json")))["coeffs"]]
     keys = ctx.keygen(synth.KEY_SEED_BASE + 5, secpe.argmax_rotations(lay))
