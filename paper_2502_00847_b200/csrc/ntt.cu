@@ -98,9 +98,12 @@ struct IntA {
     }
     static __device__ __forceinline__ u64 in(u64 x, const PrimeC &) { return x; }
     // {w, Shoup companion} (16-byte interleaved table)
+    static constexpr bool PAIRS = false;
     static __device__ __forceinline__ ulonglong2 twiddle(const ulonglong2 *tw, int i, const PrimeC &) {
         return __ldg(tw + i);
     }
+    static __device__ __forceinline__ void twiddle2(const ulonglong2 *, int, const PrimeC &, ulonglong2 &,
+                                                    ulonglong2 &) {}
     // forward output (< 11q or < 6q) -> [0, q)
     static __device__ __forceinline__ u64 out_fwd(u64 x, const PrimeC &P) {
         const u64 q = P.q;
@@ -158,6 +161,14 @@ struct FpA {
         const double w = __ldg(reinterpret_cast<const double *>(tw) + i);
         return make_ulonglong2(B(w), B(__dmul_rn(w, P.qinv)));
     }
+    // entries i, i + 1 (i even) with one 16-byte load
+    static constexpr bool PAIRS = true;
+    static __device__ __forceinline__ void twiddle2(const ulonglong2 *tw, int i, const PrimeC &P, ulonglong2 &w0,
+                                                    ulonglong2 &w1) {
+        const double2 w = __ldg(reinterpret_cast<const double2 *>(reinterpret_cast<const double *>(tw) + i));
+        w0 = make_ulonglong2(B(w.x), B(__dmul_rn(w.x, P.qinv)));
+        w1 = make_ulonglong2(B(w.y), B(__dmul_rn(w.y, P.qinv)));
+    }
     // canonical integer (< 2^52) -> exact double
     static __device__ __forceinline__ u64 in(u64 x, const PrimeC &) {
         return B(__dsub_rn(D(x | 0x4330000000000000ULL), TWO52));
@@ -209,11 +220,23 @@ __device__ __forceinline__ void do_round(u64 (&v)[NV], int tau, int g, const ulo
         const int vb = b - LO;
         const int sg = CONTIG ? LOGN - 1 - b : S - 1 - b;
         const int gterm = CONTIG ? (g << (S - 1 - b)) : 0;
+        // the distinct twiddles of this stage are consecutive table entries idx0 + u
+        const int NTW = 1 << (RB - 1 - vb);  // compile-time after unrolling
+        ulonglong2 ws[1 << (RB - 1)];
+        {
+            const int idx0 = (1 << sg) + gterm + (held<LO>(tau, 0) >> (b + 1));
+            if (A::PAIRS && NTW >= 2) {
 #pragma unroll
-        for (int u = 0; u < (1 << (RB - 1 - vb)); u++) {
+                for (int u = 0; u < NTW; u += 2) A::twiddle2(tw, idx0 + u, P, ws[u], ws[u + 1]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < NTW; u++) ws[u] = A::twiddle(tw, idx0 + u, P);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < NTW; u++) {
             const int v0b = u << (vb + 1);
-            const int r = held<LO>(tau, v0b);
-            const ulonglong2 w = A::twiddle(tw, (1 << sg) + gterm + (r >> (b + 1)), P);
+            const ulonglong2 w = ws[u];
 #pragma unroll
             for (int l = 0; l < (1 << vb); l++) {
                 const int i0 = v0b | l, i1 = i0 | (1 << vb);
