@@ -329,7 +329,20 @@ void Ctx::build_tc_groups(LevelConsts &lc, int l) {
 // ---------------------------------------------------------------------------------------------
 // context build
 // ---------------------------------------------------------------------------------------------
+Ctx::~Ctx() {
+    if (st) cudaStreamSynchronize(st);
+    pt_cache.clear();  // may have been allocated on an auxiliary stream: free before destroying it
+    for (auto s : aux) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+    }
+}
+
 void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int logn_, double scale_) {
+    {
+        const char *e = getenv("SECPE_STREAMS");  // concurrent sub-batches in secpe_enc_argmax
+        n_streams = e ? std::max(1, atoi(e)) : 2;
+    }
     {
         const char *e = getenv("SECPE_NO_TC");  // development switch: integer base-conversion kernels
         use_tc = !(e && atoi(e) == 1);

@@ -123,6 +123,13 @@ struct Ctx {
     size_t prof_begin(int kind);
     void prof_end(size_t a, int kind, double bytes, long long units);
 
+    // encoded argmax masks (NTT form), keyed by layout / level / scale bits: encoded once per context
+    std::map<std::string, std::shared_ptr<DevBuf>> pt_cache;
+    // auxiliary streams for concurrent sub-batches (created on first use; SECPE_STREAMS, default 2)
+    std::vector<cudaStream_t> aux;
+    int n_streams = 2;
+    ~Ctx();
+
     int nprimes() const { return nq + np; }
     int L() const { return nq - 1; }
     int beta(int level) const { return (level + 1 + alpha - 1) / alpha; }

@@ -129,22 +129,35 @@ struct Ev {
         c.log("LINC", lv, Lt, St, join(Cs));
         return out;
     }
-    Val mul_mask(const Val &x, const std::vector<double> &mask, double St) {
+    // cache_key: non-empty for masks that are a function of the key alone (the argmax mask of a layout):
+    // the encoded plaintext is then kept in the context and reused (no host work or sync next time)
+    Val mul_mask(const Val &x, const std::vector<double> &mask, double St, const std::string &cache_key = "") {
         const int lv = x.level();
         if (lv < 1) throw SecpeError{-2, "mul_mask: no level left"};
         const double dm = (St * q(lv)) / x.scale();
         const long N = c.N;
-        std::vector<i64> M(N);
-        encode_mask(c, mask.data(), mask.size(), dm, M.data());
-        DevBuf mi(N, c.st), pt((size_t)(lv + 1) * N, c.st);
-        CUDA_CHECK(cudaMemcpyAsync(mi.p, M.data(), N * 8, cudaMemcpyHostToDevice, c.st));
-        k_int_to_rows(c.tab, c.logn, (const i64 *)mi.p, pt.p, LimbMap{lv + 1, lv + 1, 0, 0}, c.st);
-        ev_ntt(c, RowsArg{pt.p, 2L * (lv + 1) * N, (long)(lv + 1) * N}, 1, LimbMap{lv + 1, lv + 1, 0, 0}, false);
+        const std::string key = cache_key.empty() ? "" : cache_key + "/" + std::to_string(lv) + "/" + dbits(dm);
+        std::shared_ptr<DevBuf> pt;
+        if (!key.empty()) {
+            auto it = c.pt_cache.find(key);
+            if (it != c.pt_cache.end()) pt = it->second;
+        }
+        if (!pt) {
+            std::vector<i64> M(N);
+            encode_mask(c, mask.data(), mask.size(), dm, M.data());
+            DevBuf mi(N, c.st);
+            pt = std::make_shared<DevBuf>((size_t)(lv + 1) * N, c.st);
+            CUDA_CHECK(cudaMemcpyAsync(mi.p, M.data(), N * 8, cudaMemcpyHostToDevice, c.st));
+            k_int_to_rows(c.tab, c.logn, (const i64 *)mi.p, pt->p, LimbMap{lv + 1, lv + 1, 0, 0}, c.st);
+            ev_ntt(c, RowsArg{pt->p, 2L * (lv + 1) * N, (long)(lv + 1) * N}, 1, LimbMap{lv + 1, lv + 1, 0, 0},
+                   false);
+            CUDA_CHECK(cudaStreamSynchronize(c.st));  // M is host memory of this frame
+            if (!key.empty()) c.pt_cache[key] = pt;
+        }
         Val tmp = fresh(lv, x.scale() * dm);
-        ev_mul_plain_ntt(c, x.v, pt.p, tmp.v);
+        ev_mul_plain_ntt(c, x.v, pt->p, tmp.v);
         Val out = fresh(lv - 1, St);
         ev_rescale(c, tmp.v, out.v);
-        CUDA_CHECK(cudaStreamSynchronize(c.st));  // M is host memory of this frame
         c.log("MULP", lv, lv - 1, St, dbits(dm));
         return out;
     }
@@ -217,7 +230,9 @@ struct Ev {
         std::vector<double> mask(c.N / 2, 0.0);
         for (int qi = 0; qi < lay.queries; qi++)
             for (int kk = 0; kk < K; kk++) mask[(size_t)qi * lay.block + kk] = 1.0 / P;
-        y = mul_mask(y, mask, c.scale);
+        y = mul_mask(y, mask, c.scale,
+                     "argmax/" + std::to_string(lay.queries) + "/" + std::to_string(P) + "/" + std::to_string(K) + "/" +
+                         std::to_string(lay.block));
         y = add(y, rot(y, -K));
         Val ydup = y;
         for (int i = 0; (1 << i) < K; i++) y = hom_max(rot(y, 1 << i), y, cfg);
@@ -262,12 +277,62 @@ void run_sign(Ctx &c, const Keys &k, const CtView &in, const SignCfg &cfg, doubl
     ev_copy(c, r.v, out);
 }
 
+// The batch runs as up to c.n_streams concurrent sub-batches, each planned on its own stream (forked
+// from and joined back into the context stream): ciphertexts are independent, and kernels of one
+// sub-batch (e.g. integer-pipe NTTs or tensor-core conversions) overlap those of another (FP64 NTTs).
+// The planned op list of every sub-batch is the same; the op log is recorded with a single stream.
 void run_argmax(Ctx &c, const Keys &k, const CtView &in, const Layout &lay, const SignCfg &cfg, CtView &out) {
-    Ev ev{c, k, in.n};
-    Val x{nullptr, in};
-    Val r = ev.argmax(x, lay, cfg);
-    out.level = r.level();
-    out.scale = r.scale();
-    ev_copy(c, r.v, out);
+    const int S = (c.log_on || in.n < 2) ? 1 : std::min(c.n_streams, in.n);
+    if (S == 1) {
+        Ev ev{c, k, in.n};
+        Val x{nullptr, in};
+        Val r = ev.argmax(x, lay, cfg);
+        out.level = r.level();
+        out.scale = r.scale();
+        ev_copy(c, r.v, out);
+        return;
+    }
+    while ((int)c.aux.size() < S) {
+        cudaStream_t s;
+        CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        c.aux.push_back(s);
+    }
+    cudaStream_t main = c.st;
+    cudaEvent_t fork;
+    CUDA_CHECK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventRecord(fork, main));
+    std::vector<cudaEvent_t> done(S);
+    try {
+        for (int s = 0; s < S; s++) {
+            const int b = (int)((long)in.n * s / S), e = (int)((long)in.n * (s + 1) / S);
+            CUDA_CHECK(cudaStreamWaitEvent(c.aux[s], fork, 0));
+            c.st = c.aux[s];
+            {
+                CtView vin = in, vout = out;
+                vin.data += (long)b * in.stride;
+                vin.n = e - b;
+                vout.data += (long)b * out.stride;
+                vout.n = e - b;
+                Ev ev{c, k, vin.n};
+                Val x{nullptr, vin};
+                Val r = ev.argmax(x, lay, cfg);
+                out.level = r.level();
+                out.scale = r.scale();
+                vout.level = r.level();
+                ev_copy(c, r.v, vout);
+            }  // temporaries are freed on their own stream here
+            CUDA_CHECK(cudaEventCreateWithFlags(&done[s], cudaEventDisableTiming));
+            CUDA_CHECK(cudaEventRecord(done[s], c.st));
+            c.st = main;
+        }
+    } catch (...) {
+        c.st = main;
+        throw;
+    }
+    for (int s = 0; s < S; s++) {
+        CUDA_CHECK(cudaStreamWaitEvent(main, done[s], 0));
+        cudaEventDestroy(done[s]);
+    }
+    cudaEventDestroy(fork);
     (void)copy_in;
 }

@@ -235,6 +235,9 @@ def run_argmax_pair(S, pname, lname, sname, seed_in, n_ct=1, oracle_cts=1):
     out = g.enc_argmax(kg, batch, lay, st)
     glog = g.oplog(enable=False, clear=True)
     got = out.t.cpu().numpy()
+    # the unlogged call runs the batch as concurrent sub-batches on auxiliary streams: same integers
+    out2 = g.enc_argmax(kg, batch, lay, st)
+    assert np.array_equal(out2.t.cpu().numpy(), got) and out2.level == out.level and out2.scale == out.scale
     mir = ckks.Mirror(prm)
     for i in range(n_ct):
         z = plan.pack(scores[i], lay, prm.N // 2)
