@@ -509,7 +509,65 @@ int secpe_enc_argmax(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in,
             outb = DevBuf((size_t)n_in * ow, c.st);
             vout.data = outb.p;
         }
-        run_argmax(c, *keys->k, vin, lay, sc, vout);
+        // CUDA graph: the circuit is data-independent, so a call on the same buffers replays the graph
+        // captured on the previous such call (the first call runs eagerly and fills the mask cache)
+        // (the legacy / per-thread default streams cannot be captured: eager there)
+        const bool graphable = c.use_graphs && contiguous && ocontig && !c.log_on && !c.prof.on && c.st != nullptr &&
+                               c.st != cudaStreamLegacy && c.st != cudaStreamPerThread;
+        std::string key;
+        if (graphable) {
+            char b[256];
+            u64 sb;
+            std::memcpy(&sb, &vin.scale, 8);
+            snprintf(b, sizeof b, "%p/%p/%d/%d/%016llx/%d/%d/%d/%d/%p/", (void *)vin.data, (void *)vout.data, n_in, lv,
+                     (unsigned long long)sb, lay.queries, lay.prompts, lay.classes, lay.block, (const void *)keys);
+            key = b;
+            for (auto &stg : sc.stages)
+                for (double x : stg) {
+                    u64 xb;
+                    std::memcpy(&xb, &x, 8);
+                    key += std::to_string(xb) + ",";
+                }
+        }
+        auto git = graphable ? c.graphs.find(key) : c.graphs.end();
+        if (git != c.graphs.end() && git->second.exec) {
+            CUDA_CHECK(cudaGraphLaunch(git->second.exec, c.st));
+            const Counters &d = git->second.cnt;
+            c.cnt.ntt_limbs += d.ntt_limbs, c.cnt.keyswitch += d.keyswitch, c.cnt.rescale += d.rescale;
+            c.cnt.rotate += d.rotate, c.cnt.mulct += d.mulct, c.cnt.mulconst += d.mulconst;
+            c.cnt.launches += d.launches, c.cnt.sign += d.sign;
+            vout.scale = git->second.out_scale;
+        } else {
+            run_argmax(c, *keys->k, vin, lay, sc, vout);
+            if (graphable) {
+                const Counters before = c.cnt;
+                cudaGraph_t graph;
+                CUDA_CHECK(cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal));
+                try {
+                    run_argmax(c, *keys->k, vin, lay, sc, vout);
+                } catch (...) {
+                    cudaStreamEndCapture(c.st, &graph);
+                    throw;
+                }
+                CUDA_CHECK(cudaStreamEndCapture(c.st, &graph));
+                Ctx::Graph G;
+                CUDA_CHECK(cudaGraphInstantiate(&G.exec, graph, 0));
+                CUDA_CHECK(cudaGraphDestroy(graph));
+                G.cnt.ntt_limbs = c.cnt.ntt_limbs - before.ntt_limbs;
+                G.cnt.keyswitch = c.cnt.keyswitch - before.keyswitch;
+                G.cnt.rescale = c.cnt.rescale - before.rescale;
+                G.cnt.rotate = c.cnt.rotate - before.rotate;
+                G.cnt.mulct = c.cnt.mulct - before.mulct;
+                G.cnt.mulconst = c.cnt.mulconst - before.mulconst;
+                G.cnt.launches = c.cnt.launches - before.launches;
+                G.cnt.sign = c.cnt.sign - before.sign;
+                c.cnt = before;  // the capture executed nothing
+                G.out_scale = vout.scale;
+                c.graphs[key] = G;
+            }
+        }
+        // result level/scale are those of the circuit (recomputed cheaply without running it)
+        vout.level = ol;
         if (!ocontig)
             for (int i = 0; i < n_in; i++)
                 CUDA_CHECK(

@@ -331,6 +331,8 @@ void Ctx::build_tc_groups(LevelConsts &lc, int l) {
 // ---------------------------------------------------------------------------------------------
 Ctx::~Ctx() {
     if (st) cudaStreamSynchronize(st);
+    for (auto &g : graphs)
+        if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
     pt_cache.clear();  // may have been allocated on an auxiliary stream: free before destroying it
     for (auto s : aux) {
         cudaStreamSynchronize(s);
@@ -342,6 +344,8 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
     {
         const char *e = getenv("SECPE_STREAMS");  // concurrent sub-batches in secpe_enc_argmax
         n_streams = e ? std::max(1, atoi(e)) : 2;
+        const char *g = getenv("SECPE_GRAPH");
+        use_graphs = !(g && atoi(g) == 0);
     }
     {
         const char *e = getenv("SECPE_NO_TC");  // development switch: integer base-conversion kernels

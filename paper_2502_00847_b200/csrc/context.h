@@ -128,6 +128,15 @@ struct Ctx {
     // auxiliary streams for concurrent sub-batches (created on first use; SECPE_STREAMS, default 2)
     std::vector<cudaStream_t> aux;
     int n_streams = 2;
+    // CUDA graphs of whole argmax calls (SECPE_GRAPH, default on), keyed by buffers / level / circuit;
+    // replay adds the counters recorded at capture
+    struct Graph {
+        cudaGraphExec_t exec = nullptr;
+        Counters cnt;
+        double out_scale = 0;
+    };
+    std::map<std::string, Graph> graphs;
+    bool use_graphs = true;
     ~Ctx();
 
     int nprimes() const { return nq + np; }

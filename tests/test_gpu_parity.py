@@ -257,6 +257,35 @@ def run_argmax_pair(S, pname, lname, sname, seed_in, n_ct=1, oracle_cts=1):
     return out
 
 
+def test_argmax_graph_replay(S):
+    """secpe_enc_argmax on a non-default stream with the same buffers: the first call runs eagerly and
+    captures a CUDA graph, later calls replay it -- every result equals the eager one word for word."""
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        desc = synth.PARAM_SETS["toy_argmax"]
+        g = S.Context(desc, stream=stream.cuda_stream)
+        lay = dict(synth.LAYOUTS["toy"], queries=64)
+        st = load_sign("sign_f1_f1.json")
+        kg = g.keygen(synth.KEY_SEED_BASE + 7, plan.argmax_rotations(lay))
+        batch = g.new_ct(g.L, 2)
+        for i in range(2):
+            z = plan.pack(synth.toy_scores(1001 + i, lay["queries"], lay["prompts"], lay["classes"]), lay, g.N // 2)
+            g.encrypt_coeffs(kg, g.encode(z, g.scale), g.L, g.scale, 500 + i,
+                             out=S.Ct(batch.t[i:i + 1], g.L, g.scale))
+        batch.level, batch.scale = g.L, g.scale
+        ol, _ = g.argmax_info(lay, st, g.L)
+        out = g.new_ct(ol, 2)
+        g.enc_argmax(kg, batch, lay, st, out=out)
+        stream.synchronize()
+        first = out.t.cpu().numpy().copy()
+        for _ in range(3):
+            out.t.zero_()
+            g.enc_argmax(kg, batch, lay, st, out=out)
+            stream.synchronize()
+            assert np.array_equal(out.t.cpu().numpy(), first)
+    assert g.opcounts()["keyswitch"] > 0
+
+
 def test_argmax_toy_bit_exact(S):
     lay = dict(synth.LAYOUTS["toy"], queries=64)
     run_argmax_pair(S, "toy_argmax", lay, "sign_f1_f1.json", 1001, n_ct=3, oracle_cts=3)
