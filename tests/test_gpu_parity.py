@@ -286,6 +286,23 @@ def test_argmax_graph_replay(S):
     assert g.opcounts()["keyswitch"] > 0
 
 
+def test_integer_base_conversion_fallback(S, monkeypatch):
+    """SECPE_NO_TC=1 selects the integer split-30 base-conversion kernels (ModUp, ModDown, fused ModDown +
+    rescale) instead of the tensor-core ones: the same integers (configs[2]/[3] parameters)."""
+    monkeypatch.setenv("SECPE_NO_TC", "1")
+    P = Pair(S, "ks")
+    prm, g = P.prm, P.gpu
+    ev = ckks.Oracle(prm)
+    seed = synth.KEY_SEED_BASE + 3
+    ko, kg = ev.keygen(seed, [1]), g.keygen(seed, [1])
+    z1, z2 = synth.uniform_slots(41, prm.N // 2), synth.uniform_slots(42, prm.N // 2)
+    a = ev.encrypt(ko, z1, prm.scale, 1)
+    b = ev.encrypt(ko, z2, prm.scale, 2)
+    ga, gb = P.up(a), P.up(b)
+    assert np.array_equal(P.down(g.mul_relin_rescale(kg, ga, gb)), ev.rescale(ev.mul_relin(ko, a, b)).data)
+    assert np.array_equal(P.down(g.rotate(kg, ga, 1)), ev.rotate_raw(ko, a, 1).data)
+
+
 def test_argmax_toy_bit_exact(S):
     lay = dict(synth.LAYOUTS["toy"], queries=64)
     run_argmax_pair(S, "toy_argmax", lay, "sign_f1_f1.json", 1001, n_ct=3, oracle_cts=3)

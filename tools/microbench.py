@@ -119,7 +119,7 @@ def main():
     if "relin" in a.what or "rot" in a.what:
         bench_ks(a.reps, stream, out)
     if "argmax" in a.what:
-        bench_argmax(a.reps, stream, out)
+        bench_argmax(a.reps, stream, out, B=int(os.environ.get("SECPE_BATCH", "8")))
     print(json.dumps(out, indent=1))
 
 
