@@ -265,6 +265,7 @@ struct PassArgs {
     Tab tab;
     NttFusion f;
     int limb0, nsub;  // this launch covers limbs [limb0, limb0 + nsub) of every polynomial (one prime class)
+    int poly0;        // ... of polynomials poly0, poly0 + 1, ... (L2-sized chunks, see run())
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -346,7 +347,7 @@ struct MinB<FpA> {
 template <int LOGN, bool INV, int IN, class A>
 __global__ void __launch_bounds__(SC *(1 << (LOGN / 2 - RB)), MinB<A>::v) ntt_strided(PassArgs a) {
     __shared__ u64 sm[(1 << (LOGN / 2)) * SC];
-    const int poly = blockIdx.y / a.nsub, limb = a.limb0 + blockIdx.y % a.nsub;
+    const int poly = a.poly0 + blockIdx.y / a.nsub, limb = a.limb0 + blockIdx.y % a.nsub;
     const int prime = prime_of(a.lm, limb);
     const PrimeC P = prime_consts(a.tab, prime);
     strided_body<LOGN, INV, IN, A>(a, sm, poly, limb, prime, P);
@@ -477,7 +478,7 @@ template <int LOGN, bool INV, int IO, class A>
 __global__ void __launch_bounds__(CT, MinB<A>::v) ntt_contig(PassArgs a) {
     using CF = ContigCfg<LOGN>;
     __shared__ __align__(16) u64 sm[CF::CG * CF::PITCH];
-    const int poly = blockIdx.y / a.nsub, limb = a.limb0 + blockIdx.y % a.nsub;
+    const int poly = a.poly0 + blockIdx.y / a.nsub, limb = a.limb0 + blockIdx.y % a.nsub;
     const int prime = prime_of(a.lm, limb);
     const PrimeC P = prime_consts(a.tab, prime);
     contig_body<LOGN, INV, IO, A>(a, sm, poly, limb, prime, P);
@@ -544,8 +545,33 @@ void launch_contig(const PassArgs &a0, int n_polys, cudaStream_t st) {
     });
 }
 
+// Optionally (SECPE_NTT_CHUNK = rows) both passes run over L2-sized chunks of polynomials (about that many rows,
+// ~56 MB at N = 2^16), chunk after chunk, so the intermediate between the passes is read back from L2.
+int chunk_rows() {
+    static int r = -1;
+    if (r < 0) {
+        const char *e = getenv("SECPE_NTT_CHUNK");
+        r = e ? atoi(e) : 0;  // measured: no gain from L2 residency, tail effects dominate; off
+    }
+    return r;
+}
+
 template <int LOGN>
-void run(const PassArgs &a, int rows, bool inverse, cudaStream_t st) {
+void run_chunk(const PassArgs &a, int rows, bool inverse, cudaStream_t st);
+
+template <int LOGN>
+void run(const PassArgs &a0, int n_polys, bool inverse, cudaStream_t st) {
+    const int cr = chunk_rows();
+    const int per = cr <= 0 ? n_polys : std::max(1, cr / std::max(1, a0.lm.nl));
+    for (int p0 = 0; p0 < n_polys; p0 += per) {
+        PassArgs a = a0;
+        a.poly0 = p0;
+        run_chunk<LOGN>(a, std::min(per, n_polys - p0), inverse, st);
+    }
+}
+
+template <int LOGN>
+void run_chunk(const PassArgs &a, int rows, bool inverse, cudaStream_t st) {
     const NttFusion &f = a.f;
     if (!inverse) {
         if (f.in_mode == IN_BCAST)
@@ -590,7 +616,7 @@ void ntt_forward(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm
                  const NttFusion &f) {
     if (n_polys <= 0 || lm.nl <= 0) return;
     if (f.in_mode != IN_PLAIN && f.in_mode != IN_BCAST) throw SecpeError{-1, "ntt_forward: bad input mode"};
-    dispatch(logn, PassArgs{data, lm, tab, f, 0, lm.nl}, n_polys, false, st);
+    dispatch(logn, PassArgs{data, lm, tab, f, 0, lm.nl, 0}, n_polys, false, st);
 }
 
 void ntt_inverse(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
@@ -598,5 +624,5 @@ void ntt_inverse(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm
     if (n_polys <= 0 || lm.nl <= 0) return;
     if ((f.in_mode != IN_PLAIN && f.in_mode != IN_SRC && f.in_mode != IN_MUL) || f.out_mode != OUT_PLAIN)
         throw SecpeError{-1, "ntt_inverse: bad fusion mode"};
-    dispatch(logn, PassArgs{data, lm, tab, f, 0, lm.nl}, n_polys, true, st);
+    dispatch(logn, PassArgs{data, lm, tab, f, 0, lm.nl, 0}, n_polys, true, st);
 }
