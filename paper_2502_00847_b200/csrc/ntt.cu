@@ -121,7 +121,7 @@ struct IntA {
 //   k = rint(y w_q) (fma with the 1.5 2^52 magic constant), (ph, pl) = TwoProduct(k, q),
 //   r = fma(y, w, -ph) - pl  =  y w - k q  exactly,  |r| <= 0.75 q.
 // Forward CT needs no corrections at all (|v| <= q + 16 * 0.75 q); inverse GS reduces the sum on
-// every other stage (|v| <= 4q).  All operations are on the FP64 pipe, which the integer path leaves
+// every fourth stage (|v| <= 12 q; the product input X - Y <= 16 q keeps |y w / q| < 2^51).  All operations are on the FP64 pipe, which the integer path leaves
 // idle; the explicit _rn intrinsics keep the compiler from contracting or reassociating.
 constexpr double FP_MAGIC = 6755399441055744.0;  // 1.5 * 2^52
 constexpr double TWO52 = 4503599627370496.0;
@@ -241,7 +241,9 @@ __device__ __forceinline__ void do_round(u64 (&v)[NV], int tau, int g, const ulo
             for (int l = 0; l < (1 << vb); l++) {
                 const int i0 = v0b | l, i1 = i0 | (1 << vb);
                 if (INV) {
-                    if (sg & 1)
+                    // FpA reduces the GS sum on every fourth stage only (|v| <= 12 q in between); IntA
+                    // ignores the flag (its Harvey bounds reduce every stage)
+                    if (sg & 3)
                         A::template gs<false>(v[i0], v[i1], w, P);
                     else
                         A::template gs<true>(v[i0], v[i1], w, P);
