@@ -74,6 +74,8 @@ struct Tab {
     const u64 *ninv;   // [P] N^{-1} mod q
     const u64 *ninvsh; // [P]
     u64 fp_mask;       // host-visible: bit i set when prime i < 2^46 (exact-FP64 NTT rows, ntt.cu FpA)
+    const double *qd;  // [P] (double) q and RN(1 / q): no per-CTA int->double conversion or division
+    const double *qinv;
 };
 
 // limb l of a polynomial -> global prime index

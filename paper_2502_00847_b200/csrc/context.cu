@@ -407,7 +407,19 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
     d_tw = upload(tw, st);
     d_itw = upload(itw, st);
     tab = Tab{d_q.p, d_br0.p, d_br1.p, reinterpret_cast<const ulonglong2 *>(d_tw.p),
-              reinterpret_cast<const ulonglong2 *>(d_itw.p), d_ninv.p, d_ninvsh.p, 0};
+              reinterpret_cast<const ulonglong2 *>(d_itw.p), d_ninv.p, d_ninvsh.p, 0, nullptr, nullptr};
+    {
+        std::vector<u64> a(P), b(P);
+        for (int i = 0; i < P; i++) {
+            const double qd = (double)primes[i], qi = 1.0 / qd;
+            std::memcpy(&a[i], &qd, 8);
+            std::memcpy(&b[i], &qi, 8);
+        }
+        d_qd = upload(a, st);
+        d_qinv = upload(b, st);
+        tab.qd = reinterpret_cast<const double *>(d_qd.p);
+        tab.qinv = reinterpret_cast<const double *>(d_qinv.p);
+    }
     for (int i = 0; i < P && i < 64; i++)
         if (primes[i] < (1ULL << 46)) tab.fp_mask |= 1ULL << i;
 

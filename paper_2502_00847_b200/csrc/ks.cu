@@ -150,8 +150,8 @@ __device__ __forceinline__ u64 canon(double v, double qd, double qinv) {
 }  // namespace fpt
 
 __device__ __forceinline__ void tensor1_fp(u64 a0, u64 a1, u64 b0, u64 b1, bool lin, u64 x0, u64 x1, u64 c,
-                                           bool lin2, u64 y0, u64 y1, u64 c2, u64 q, u64 &d0, u64 &d1, u64 &d2) {
-    const double qd = (double)q, qinv = 1.0 / qd;
+                                           bool lin2, u64 y0, u64 y1, u64 c2, double qd, double qinv, u64 &d0,
+                                           u64 &d1, u64 &d2) {
     const double A0 = fpt::d(a0), A1 = fpt::d(a1), B0 = fpt::d(b0), B1 = fpt::d(b1);
     const double B0q = __dmul_rn(B0, qinv), B1q = __dmul_rn(B1, qinv);
     double e0 = fpt::mm(A0, B0, B0q, qd);
@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(TPB, TEN ? 2 : 3) ks_inner_vec_kernel(Tab tab,
     const bool lin = TEN && ten.x.p, lin2 = TEN && ten.x2.p;
     const u64 cc = lin && e < nl ? ten.C.c[e] : 0, ccsh = lin && e < nl ? ten.C.csh[e] : 0;
     const u64 c2 = lin2 && e < nl ? ten.C2.c[e] : 0, c2sh = lin2 && e < nl ? ten.C2.csh[e] : 0;
+    const double qd = TEN ? tab.qd[pr] : 0.0, qinv = TEN ? tab.qinv[pr] : 0.0;
     // plain key switching double-buffers the next ciphertext's inputs; with the tensor formed on the fly
     // the register budget goes to the tensor terms instead (single buffer)
     KsIn<MAXB> cur, nxt;
@@ -227,9 +228,9 @@ __global__ void __launch_bounds__(TPB, TEN ? 2 : 3) ks_inner_vec_kernel(Tab tab,
             u64 e0, e1, e2, f0, f1, f2;
             if (q < (1ULL << 46)) {
                 tensor1_fp(cur.a0.x, cur.a1.x, cur.b0.x, cur.b1.x, lin, cur.x0.x, cur.x1.x, cc, lin2, cur.y0.x,
-                           cur.y1.x, c2, q, e0, e1, e2);
+                           cur.y1.x, c2, qd, qinv, e0, e1, e2);
                 tensor1_fp(cur.a0.y, cur.a1.y, cur.b0.y, cur.b1.y, lin, cur.x0.y, cur.x1.y, cc, lin2, cur.y0.y,
-                           cur.y1.y, c2, q, f0, f1, f2);
+                           cur.y1.y, c2, qd, qinv, f0, f1, f2);
             } else {
                 tensor1(cur.a0.x, cur.a1.x, cur.b0.x, cur.b1.x, lin, cur.x0.x, cur.x1.x, cc, ccsh, lin2, cur.y0.x,
                         cur.y1.x, c2, c2sh, q, r0, r1, e0, e1, e2);

@@ -330,8 +330,8 @@ __device__ __forceinline__ void strided_body(const PassArgs &a, u64 *sm, int pol
 __device__ __forceinline__ PrimeC prime_consts(const Tab &tab, int prime) {
     PrimeC P;
     P.q = tab.q[prime];
-    P.qd = (double)P.q;
-    P.qinv = 1.0 / P.qd;
+    P.qd = tab.qd[prime];
+    P.qinv = tab.qinv[prime];
     return P;
 }
 
