@@ -202,6 +202,20 @@ int secpe_argmax_info(secpe_ctx *ctx, const secpe_layout *layout, const secpe_si
  * No secret key is taken or needed. */
 int secpe_enc_argmax(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n_in,
                      const secpe_layout *layout, const secpe_sign_cfg *cfg, secpe_ct *out);
+/* secpe_enc_argmax on ciphertexts held in HOST memory (the end-to-end server call).
+ * h_in: uint64[n_in][2][level+1][N] (ciphertext i at h_in + i * secpe_ct_bytes(level) / 8, all at
+ * `level` and `scale`); h_out: uint64[n_in][2][out_level+1][N], out_level / out_scale as
+ * secpe_argmax_info reports (written to *out_level / *out_scale when non-null).  The batch runs
+ * in chunks of `chunk` ciphertexts (<= 0: 8) through two device staging slots owned by the
+ * context: the host-to-device copy of a chunk runs on a context-owned copy stream while the
+ * previous chunk (possibly of the previous call) computes; each result is copied back on the
+ * context stream.  Pinned host memory gives overlapped transfers (pageable memory is correct
+ * but copies synchronously).  Enqueue-only: h_out is complete, and h_in may be reused, after
+ * secpe_sync(ctx).  Needs an explicit (non-default) context stream (else SECPE_EINVAL). */
+int secpe_enc_argmax_host(secpe_ctx *ctx, const secpe_keys *keys, const uint64_t *h_in, int32_t n_in,
+                          int32_t level, double scale, const secpe_layout *layout,
+                          const secpe_sign_cfg *cfg, uint64_t *h_out, int32_t chunk,
+                          int32_t *out_level, double *out_scale);
 
 /* ---- instrumentation ---------------------------------------------------------------------- */
 /* Enable (1) / disable (0) the planned-op log; secpe_oplog_get copies it (NUL-terminated)

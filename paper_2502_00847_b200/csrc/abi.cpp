@@ -475,6 +475,68 @@ int secpe_argmax_info(secpe_ctx *ctx, const secpe_layout *layout, const secpe_si
         *out_scale = ctx->c.scale;
     });
 }
+// One batched argmax on device views.  CUDA graph: the circuit is data-independent, so a call on the
+// same buffers replays the graph captured on the previous such call (the first call runs eagerly and
+// fills the mask cache); the legacy / per-thread default streams cannot be captured: eager there.
+static void argmax_views(Ctx &c, const secpe_keys *keys, const CtView &vin, const Layout &lay, const SignCfg &sc,
+                         CtView &vout, bool buffers_fixed) {
+    const bool graphable = c.use_graphs && buffers_fixed && !c.log_on && !c.prof.on && c.st != nullptr &&
+                           c.st != cudaStreamLegacy && c.st != cudaStreamPerThread;
+    std::string key;
+    if (graphable) {
+        char b[256];
+        u64 sb;
+        std::memcpy(&sb, &vin.scale, 8);
+        snprintf(b, sizeof b, "%p/%p/%d/%d/%016llx/%d/%d/%d/%d/%p/", (void *)vin.data, (void *)vout.data, vin.n,
+                 vin.level, (unsigned long long)sb, lay.queries, lay.prompts, lay.classes, lay.block,
+                 (const void *)keys);
+        key = b;
+        for (auto &stg : sc.stages)
+            for (double x : stg) {
+                u64 xb;
+                std::memcpy(&xb, &x, 8);
+                key += std::to_string(xb) + ",";
+            }
+    }
+    auto git = graphable ? c.graphs.find(key) : c.graphs.end();
+    if (git != c.graphs.end() && git->second.exec) {
+        CUDA_CHECK(cudaGraphLaunch(git->second.exec, c.st));
+        const Counters &d = git->second.cnt;
+        c.cnt.ntt_limbs += d.ntt_limbs, c.cnt.keyswitch += d.keyswitch, c.cnt.rescale += d.rescale;
+        c.cnt.rotate += d.rotate, c.cnt.mulct += d.mulct, c.cnt.mulconst += d.mulconst;
+        c.cnt.launches += d.launches, c.cnt.sign += d.sign;
+        vout.scale = git->second.out_scale;
+        return;
+    }
+    run_argmax(c, *keys->k, vin, lay, sc, vout);
+    if (!graphable) return;
+    const Counters before = c.cnt;
+    cudaGraph_t graph;
+    CUDA_CHECK(cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal));
+    try {
+        run_argmax(c, *keys->k, vin, lay, sc, vout);
+    } catch (...) {
+        cudaStreamEndCapture(c.st, &graph);
+        throw;
+    }
+    CUDA_CHECK(cudaStreamEndCapture(c.st, &graph));
+    Ctx::Graph G;
+    CUDA_CHECK(cudaGraphInstantiate(&G.exec, graph, 0));
+    CUDA_CHECK(cudaGraphDestroy(graph));
+    CUDA_CHECK(cudaGraphUpload(G.exec, c.st));  // pay the one-time upload now, not on the first replay
+    G.cnt.ntt_limbs = c.cnt.ntt_limbs - before.ntt_limbs;
+    G.cnt.keyswitch = c.cnt.keyswitch - before.keyswitch;
+    G.cnt.rescale = c.cnt.rescale - before.rescale;
+    G.cnt.rotate = c.cnt.rotate - before.rotate;
+    G.cnt.mulct = c.cnt.mulct - before.mulct;
+    G.cnt.mulconst = c.cnt.mulconst - before.mulconst;
+    G.cnt.launches = c.cnt.launches - before.launches;
+    G.cnt.sign = c.cnt.sign - before.sign;
+    c.cnt = before;  // the capture executed nothing
+    G.out_scale = vout.scale;
+    c.graphs[key] = G;
+}
+
 int secpe_enc_argmax(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n_in,
                      const secpe_layout *layout, const secpe_sign_cfg *cfg, secpe_ct *out) {
     return guard([&] {
@@ -509,63 +571,7 @@ int secpe_enc_argmax(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in,
             outb = DevBuf((size_t)n_in * ow, c.st);
             vout.data = outb.p;
         }
-        // CUDA graph: the circuit is data-independent, so a call on the same buffers replays the graph
-        // captured on the previous such call (the first call runs eagerly and fills the mask cache)
-        // (the legacy / per-thread default streams cannot be captured: eager there)
-        const bool graphable = c.use_graphs && contiguous && ocontig && !c.log_on && !c.prof.on && c.st != nullptr &&
-                               c.st != cudaStreamLegacy && c.st != cudaStreamPerThread;
-        std::string key;
-        if (graphable) {
-            char b[256];
-            u64 sb;
-            std::memcpy(&sb, &vin.scale, 8);
-            snprintf(b, sizeof b, "%p/%p/%d/%d/%016llx/%d/%d/%d/%d/%p/", (void *)vin.data, (void *)vout.data, n_in, lv,
-                     (unsigned long long)sb, lay.queries, lay.prompts, lay.classes, lay.block, (const void *)keys);
-            key = b;
-            for (auto &stg : sc.stages)
-                for (double x : stg) {
-                    u64 xb;
-                    std::memcpy(&xb, &x, 8);
-                    key += std::to_string(xb) + ",";
-                }
-        }
-        auto git = graphable ? c.graphs.find(key) : c.graphs.end();
-        if (git != c.graphs.end() && git->second.exec) {
-            CUDA_CHECK(cudaGraphLaunch(git->second.exec, c.st));
-            const Counters &d = git->second.cnt;
-            c.cnt.ntt_limbs += d.ntt_limbs, c.cnt.keyswitch += d.keyswitch, c.cnt.rescale += d.rescale;
-            c.cnt.rotate += d.rotate, c.cnt.mulct += d.mulct, c.cnt.mulconst += d.mulconst;
-            c.cnt.launches += d.launches, c.cnt.sign += d.sign;
-            vout.scale = git->second.out_scale;
-        } else {
-            run_argmax(c, *keys->k, vin, lay, sc, vout);
-            if (graphable) {
-                const Counters before = c.cnt;
-                cudaGraph_t graph;
-                CUDA_CHECK(cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal));
-                try {
-                    run_argmax(c, *keys->k, vin, lay, sc, vout);
-                } catch (...) {
-                    cudaStreamEndCapture(c.st, &graph);
-                    throw;
-                }
-                CUDA_CHECK(cudaStreamEndCapture(c.st, &graph));
-                Ctx::Graph G;
-                CUDA_CHECK(cudaGraphInstantiate(&G.exec, graph, 0));
-                CUDA_CHECK(cudaGraphDestroy(graph));
-                G.cnt.ntt_limbs = c.cnt.ntt_limbs - before.ntt_limbs;
-                G.cnt.keyswitch = c.cnt.keyswitch - before.keyswitch;
-                G.cnt.rescale = c.cnt.rescale - before.rescale;
-                G.cnt.rotate = c.cnt.rotate - before.rotate;
-                G.cnt.mulct = c.cnt.mulct - before.mulct;
-                G.cnt.mulconst = c.cnt.mulconst - before.mulconst;
-                G.cnt.launches = c.cnt.launches - before.launches;
-                G.cnt.sign = c.cnt.sign - before.sign;
-                c.cnt = before;  // the capture executed nothing
-                G.out_scale = vout.scale;
-                c.graphs[key] = G;
-            }
-        }
+        argmax_views(c, keys, vin, lay, sc, vout, contiguous && ocontig);
         // result level/scale are those of the circuit (recomputed cheaply without running it)
         vout.level = ol;
         if (!ocontig)
@@ -573,6 +579,67 @@ int secpe_enc_argmax(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in,
                 CUDA_CHECK(
                     cudaMemcpyAsync(out[i].data, outb.p + (long)i * ow, ow * 8, cudaMemcpyDeviceToDevice, c.st));
         for (int i = 0; i < n_in; i++) set_out(&out[i], vout);
+    });
+}
+
+int secpe_enc_argmax_host(secpe_ctx *ctx, const secpe_keys *keys, const uint64_t *h_in, int32_t n_in,
+                          int32_t level, double scale, const secpe_layout *layout, const secpe_sign_cfg *cfg,
+                          uint64_t *h_out, int32_t chunk, int32_t *out_level, double *out_scale) {
+    return guard([&] {
+        REQUIRE(ctx && keys && h_in && h_out && n_in >= 1, SECPE_EINVAL, "null argument");
+        Ctx &c = ctx->c;
+        REQUIRE(level >= 0 && level <= c.L(), SECPE_ELEVEL, "level out of range");
+        REQUIRE(c.st != cudaStreamLegacy && c.st != cudaStreamPerThread, SECPE_EINVAL,
+                "secpe_enc_argmax_host needs an explicit (non-default) context stream");
+        Layout lay = layout_of(c, layout);
+        SignCfg sc = sign_cfg(cfg);
+        const int ol = level - argmax_depth(lay, sc);
+        REQUIRE(ol >= 0, SECPE_ELEVEL, "not enough levels for the argmax circuit");
+        if (chunk <= 0) chunk = 8;
+        chunk = std::min(chunk, n_in);
+        const long cw = c.ct_words(level), ow = c.ct_words(ol);
+        Ctx::HostPipe &hp = c.pipe;
+        if (!hp.cp) {
+            CUDA_CHECK(cudaStreamCreateWithFlags(&hp.cp, cudaStreamNonBlocking));
+            for (int s = 0; s < 2; s++) {
+                CUDA_CHECK(cudaEventCreateWithFlags(&hp.loaded[s], cudaEventDisableTiming));
+                CUDA_CHECK(cudaEventCreateWithFlags(&hp.freed[s], cudaEventDisableTiming));
+                CUDA_CHECK(cudaEventRecord(hp.freed[s], c.st));
+            }
+        }
+        if (hp.in_words < (size_t)chunk * cw || hp.out_words < (size_t)chunk * ow) {
+            // grow both slots (after every earlier use of them has finished on the context stream)
+            CUDA_CHECK(cudaStreamWaitEvent(c.st, hp.freed[0], 0));
+            CUDA_CHECK(cudaStreamWaitEvent(c.st, hp.freed[1], 0));
+            hp.in_words = std::max(hp.in_words, (size_t)chunk * cw);
+            hp.out_words = std::max(hp.out_words, (size_t)chunk * ow);
+            for (int s = 0; s < 2; s++) {
+                hp.in[s] = DevBuf(hp.in_words, c.st);
+                hp.out[s] = DevBuf(hp.out_words, c.st);
+                CUDA_CHECK(cudaEventRecord(hp.freed[s], c.st));
+            }
+        }
+        double osc = c.scale;
+        for (int i0 = 0; i0 < n_in; i0 += chunk) {
+            const int n = std::min(chunk, n_in - i0);
+            const int s = hp.next++ & 1;
+            // copy stream: wait until slot s is free, then load this chunk (overlaps the other slot's compute)
+            CUDA_CHECK(cudaStreamWaitEvent(hp.cp, hp.freed[s], 0));
+            CUDA_CHECK(cudaMemcpyAsync(hp.in[s].p, h_in + (long)i0 * cw, (size_t)n * cw * 8, cudaMemcpyHostToDevice,
+                                       hp.cp));
+            CUDA_CHECK(cudaEventRecord(hp.loaded[s], hp.cp));
+            // context stream: compute on slot s, copy the result back, release the slot
+            CUDA_CHECK(cudaStreamWaitEvent(c.st, hp.loaded[s], 0));
+            CtView vin = compact_view(c, hp.in[s].p, n, level, scale);
+            CtView vout = compact_view(c, hp.out[s].p, n, ol, c.scale);
+            argmax_views(c, keys, vin, lay, sc, vout, true);
+            osc = vout.scale;
+            CUDA_CHECK(cudaMemcpyAsync(h_out + (long)i0 * ow, hp.out[s].p, (size_t)n * ow * 8, cudaMemcpyDeviceToHost,
+                                       c.st));
+            CUDA_CHECK(cudaEventRecord(hp.freed[s], c.st));
+        }
+        if (out_level) *out_level = ol;
+        if (out_scale) *out_scale = osc;
     });
 }
 

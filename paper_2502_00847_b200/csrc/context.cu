@@ -334,6 +334,14 @@ Ctx::~Ctx() {
     for (auto &g : graphs)
         if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
     pt_cache.clear();  // may have been allocated on an auxiliary stream: free before destroying it
+    if (pipe.cp) {
+        cudaStreamSynchronize(pipe.cp);
+        cudaStreamDestroy(pipe.cp);
+    }
+    for (int s = 0; s < 2; s++) {
+        if (pipe.loaded[s]) cudaEventDestroy(pipe.loaded[s]);
+        if (pipe.freed[s]) cudaEventDestroy(pipe.freed[s]);
+    }
     for (auto s : aux) {
         cudaStreamSynchronize(s);
         cudaStreamDestroy(s);

@@ -137,6 +137,15 @@ struct Ctx {
     };
     std::map<std::string, Graph> graphs;
     bool use_graphs = true;
+    // host-buffer argmax pipeline (secpe_enc_argmax_host): two device staging slots per direction and a
+    // copy stream; loaded[s]: slot s's inputs are on the device, freed[s]: slot s's last use has finished
+    struct HostPipe {
+        DevBuf in[2], out[2];
+        size_t in_words = 0, out_words = 0;
+        cudaStream_t cp = nullptr;
+        cudaEvent_t loaded[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
+        int next = 0;
+    } pipe;
     ~Ctx();
 
     int nprimes() const { return nq + np; }

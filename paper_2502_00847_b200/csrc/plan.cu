@@ -282,7 +282,8 @@ void run_sign(Ctx &c, const Keys &k, const CtView &in, const SignCfg &cfg, doubl
 // sub-batch (e.g. integer-pipe NTTs or tensor-core conversions) overlap those of another (FP64 NTTs).
 // The planned op list of every sub-batch is the same; the op log is recorded with a single stream.
 void run_argmax(Ctx &c, const Keys &k, const CtView &in, const Layout &lay, const SignCfg &cfg, CtView &out) {
-    const int S = (c.log_on || in.n < 2) ? 1 : std::min(c.n_streams, in.n);
+    // (one stream while the op log or the CUDA-event profiler is on: the profiled spans must not overlap)
+    const int S = (c.log_on || c.prof.on || in.n < 2) ? 1 : std::min(c.n_streams, in.n);
     if (S == 1) {
         Ev ev{c, k, in.n};
         Val x{nullptr, in};

@@ -82,6 +82,9 @@ SIGS = {
                                          i32p, f64p]),
     "secpe_enc_argmax": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.POINTER(Layout),
                                         ctypes.POINTER(SignCfg), ctypes.POINTER(CCt)]),
+    "secpe_enc_argmax_host": (ctypes.c_int, [vp, vp, u64p, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                                             ctypes.POINTER(Layout), ctypes.POINTER(SignCfg), u64p, ctypes.c_int32,
+                                             i32p, f64p]),
     "secpe_oplog_enable": (ctypes.c_int, [vp, ctypes.c_int32]),
     "secpe_oplog_get": (ctypes.c_int64, [vp, ctypes.c_char_p, ctypes.c_size_t]),
     "secpe_oplog_clear": (ctypes.c_int, [vp]),
@@ -405,6 +408,22 @@ class Context:
         _chk(lib().secpe_enc_argmax(self.h, keys.h, ins, cts.n, ctypes.byref(ly), ctypes.byref(cfg), outs))
         out.level, out.scale = outs[0].level, outs[0].scale
         return out
+
+    def enc_argmax_host(self, keys, h_in, level, scale, lay, stages, h_out=None, chunk=0):
+        """secpe_enc_argmax_host: h_in a host (CPU, ideally pinned) uint64 tensor [n][2][level+1][N];
+        returns (h_out, out_level, out_scale).  Enqueue-only: h_out is complete after sync()."""
+        cfg, ly = sign_cfg(stages), layout(lay)
+        assert h_in.device.type == "cpu" and h_in.dtype == torch.uint64 and h_in.is_contiguous()
+        n = h_in.shape[0]
+        ol, _ = self.argmax_info(lay, stages, level)
+        if h_out is None:
+            h_out = torch.empty((n, 2, ol + 1, self.N), dtype=torch.uint64, pin_memory=h_in.is_pinned())
+        assert h_out.device.type == "cpu" and h_out.is_contiguous() and h_out.numel() >= n * 2 * (ol + 1) * self.N
+        olv, osc = ctypes.c_int32(0), ctypes.c_double(0.0)
+        _chk(lib().secpe_enc_argmax_host(self.h, keys.h, ctypes.cast(h_in.data_ptr(), u64p), n, level, scale,
+                                         ctypes.byref(ly), ctypes.byref(cfg), ctypes.cast(h_out.data_ptr(), u64p),
+                                         chunk, ctypes.byref(olv), ctypes.byref(osc)))
+        return h_out, olv.value, osc.value
 
     # ---- instrumentation --------------------------------------------------------------------------
     def oplog(self, enable=None, clear=False):

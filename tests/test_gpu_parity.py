@@ -286,6 +286,42 @@ def test_argmax_graph_replay(S):
     assert g.opcounts()["keyswitch"] > 0
 
 
+def test_argmax_host_pipeline(S):
+    """secpe_enc_argmax_host (host buffers, two staging slots, copy stream) on a ragged chunking
+    (5 ciphertexts in chunks of 2) and twice in a row (slot reuse across calls), pinned and pageable:
+    every result equals the device-buffer secpe_enc_argmax word for word."""
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        desc = synth.PARAM_SETS["toy_argmax"]
+        g = S.Context(desc, stream=stream.cuda_stream)
+        lay = dict(synth.LAYOUTS["toy"], queries=64)
+        st = load_sign("sign_f1_f1.json")
+        kg = g.keygen(synth.KEY_SEED_BASE + 7, plan.argmax_rotations(lay))
+        n = 5
+        batch = g.new_ct(g.L, n)
+        for i in range(n):
+            z = plan.pack(synth.toy_scores(2001 + i, lay["queries"], lay["prompts"], lay["classes"]), lay, g.N // 2)
+            g.encrypt_coeffs(kg, g.encode(z, g.scale), g.L, g.scale, 600 + i,
+                             out=S.Ct(batch.t[i:i + 1], g.L, g.scale))
+        batch.level, batch.scale = g.L, g.scale
+        ol, osc = g.argmax_info(lay, st, g.L)
+        ref = g.enc_argmax(kg, batch, lay, st)
+        stream.synchronize()
+        want = ref.t.cpu().numpy()
+        for pinned in (True, False):
+            h_in = batch.t.cpu()
+            if pinned:
+                h_in = h_in.pin_memory()
+            outs = []
+            for _ in range(2):
+                h_out, lv, sc = g.enc_argmax_host(kg, h_in, g.L, g.scale, lay, st, chunk=2)
+                outs.append(h_out)
+                assert lv == ol and sc == ref.scale
+            g.sync()
+            for h_out in outs:
+                assert np.array_equal(h_out.numpy(), want)
+
+
 def test_integer_base_conversion_fallback(S, monkeypatch):
     """SECPE_NO_TC=1 selects the integer split-30 base-conversion kernels (ModUp, ModDown, fused ModDown +
     rescale) instead of the tensor-core ones: the same integers (configs[2]/[3] parameters)."""
