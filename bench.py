@@ -295,17 +295,23 @@ def run_secpe(a):
         return
 
     peak, peak_src = peaks()
-    ntt = prof["ntt"]
-    ks = prof["keyswitch"]
-    ach = ntt["bytes"] / (ntt["ms"] / 1000.0) / 1e9 if ntt["ms"] > 0 else 0.0
-    ks_ach = ks["bytes"] / (ks["ms"] / 1000.0) / 1e9 if ks["ms"] > 0 else 0.0
-    traffic = None
+    ntt, ntt_int, ks = prof["ntt_fp"], prof["ntt_int"], prof["keyswitch"]
+    gbs = lambda d: d["bytes"] / (d["ms"] / 1000.0) / 1e9 if d["ms"] > 0 else 0.0
+    ach, ks_ach = gbs(ntt), gbs(ks)
+    traffic, tsrc = None, None
     tp = os.path.join(ROOT, "profiles", "ntt_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_limb_transform")
+            tj = json.load(open(tp))
+            traffic, tsrc = tj["dram_bytes_per_limb_transform"], tj.get("source")
         except Exception:
             traffic = None
+    # FP64-pipe roof of the same kernels: (N/2) log2 N butterflies per limb transform, 8 FP64-pipe
+    # instructions each in the exact-FP64 formulation; peak = 148 SMs x 64 FP64
+    # lanes/clk x the SM clock sampled under load
+    clk_mhz = clk.get("sm_mhz") or 1965.0
+    fp64_peak = 148 * 64 * clk_mhz * 1e6 / 1e12
+    fp64_ach = (ctx.N // 2) * ctx.logn * 8 * ntt["units"] / (ntt["ms"] / 1000.0) / 1e12 if ntt["ms"] > 0 else 0.0
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -314,12 +320,20 @@ def run_secpe(a):
                    "parallelism": "ciphertexts sharded over ranks (replicated keys)" if ws > 1 else "single GPU",
                    "l2": "inputs larger than L2 (%.0f MB ciphertexts + %.0f MB keys per rank)" % (
                        B * inp.t[0].numel() * 8 / 1e6, 6 * 119.5)},
-        "roofline": {"bound": "hbm", "kernel": "ntt (forward+inverse, all launches in the timed region)",
+        "roofline": {"bound": "hbm", "kernel": "ntt on the 45-bit (FP64) rows: every forward/inverse launch in the "
+                                                "profiled region (%.0f limb transforms per step)" % (ntt["units"] / a.steps),
                      "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
-                     "peak_source": peak_src,
+                     "traffic_source": tsrc, "peak_source": peak_src,
                      "algorithmic_bytes_per_limb_transform": 16 * ctx.N,
-                     "ntt_share_of_step": ntt["ms"] / ms_prof,
-                     "profiled_region": "second timed region of the same %d steps (events around each span)" % a.steps,
+                     "share_of_step": ntt["ms"] / ms_prof,
+                     "fp64_pipe": {"achieved": fp64_ach, "peak": fp64_peak, "unit": "T FP64 instr/s",
+                                   "frac": fp64_ach / fp64_peak,
+                                   "peak_source": "148 SMs x 64 FP64 lanes/clk x %.0f MHz (sampled)" % clk_mhz},
+                     "profiled_region": "second timed region of the same %d steps, one stream, CUDA events around "
+                                        "every NTT launch and key-switch / rescale span" % a.steps,
+                     "ntt_integer_rows": {"achieved": gbs(ntt_int), "frac": gbs(ntt_int) / peak,
+                                          "share_of_step": ntt_int["ms"] / ms_prof, "unit": "GB/s",
+                                          "bound": "integer FMA pipe (quarter-rate IMAD.WIDE)"},
                      "keyswitch": {"achieved": ks_ach, "frac": ks_ach / peak, "share_of_step": ks["ms"] / ms_prof,
                                    "unit": "GB/s"},
                      "rescale_share_of_step": prof["rescale"]["ms"] / ms_prof},
@@ -345,9 +359,9 @@ def run_secpe(a):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=8, help="ciphertexts per rank per step")
+    ap.add_argument("--batch", type=int, default=16, help="ciphertexts per rank per step")
     ap.add_argument("--impl", default="secpe", choices=["secpe", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-micro", action="store_true", help="skip the configs[1]-[3] lines")

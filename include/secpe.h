@@ -223,11 +223,13 @@ int secpe_enc_argmax_host(secpe_ctx *ctx, const secpe_keys *keys, const uint64_t
 int secpe_oplog_enable(secpe_ctx *ctx, int32_t on);
 int64_t secpe_oplog_get(secpe_ctx *ctx, char *buf, size_t cap);
 int secpe_oplog_clear(secpe_ctx *ctx);
-/* CUDA-event profile of the NTT, key-switch and rescale spans enqueued between begin and end
- * (events recorded on the context stream around each span; end synchronises).  out[9]:
- * per kind k (0 NTT, 1 key switch, 2 rescale): out[3k] total ms, out[3k+1] algorithmic bytes
- * (NTT: 16 N per limb transform; key switch: (input + output limbs) per ciphertext + key once per
- * batch; rescale: 2(l+1) + 2l limbs per ciphertext), out[3k+2] units (limb transforms / ciphertexts). */
+/* CUDA-event profile of the NTT launches and the key-switch and rescale spans enqueued between begin
+ * and end (events recorded on the context stream around each span; end synchronises).  out[12]:
+ * per kind k (0 NTT launches on FP64 rows (primes < 2^46), 1 key switch, 2 rescale, 3 NTT launches
+ * on integer rows): out[3k] total ms, out[3k+1] algorithmic bytes (NTT: 16 N per limb transform,
+ * split evenly over its passes; key switch: (input + output limbs) per ciphertext + key once per
+ * batch; rescale: 2(l+1) + 2l limbs per ciphertext), out[3k+2] units (limb transforms per launch,
+ * summed / ciphertexts).  Returns SECPE_EINVAL when n_out < 12. */
 int secpe_profile_begin(secpe_ctx *ctx);
 int secpe_profile_end(secpe_ctx *ctx, double *out, int32_t n_out);
 /* host counts[8]: NTT limb-transforms, key switches, rescales, rotations, ct-ct products,

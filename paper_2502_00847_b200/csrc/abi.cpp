@@ -677,11 +677,11 @@ int secpe_profile_begin(secpe_ctx *ctx) {
 }
 int secpe_profile_end(secpe_ctx *ctx, double *out, int32_t n_out) {
     return guard([&] {
-        REQUIRE(ctx && out && n_out >= 9, SECPE_EINVAL, "need out[9]");
+        REQUIRE(ctx && out && n_out >= 12, SECPE_EINVAL, "need out[12]");
         Prof &p = ctx->c.prof;
         CUDA_CHECK(cudaStreamSynchronize(ctx->c.st));
         p.on = false;
-        for (int i = 0; i < 9; i++) out[i] = 0;
+        for (int i = 0; i < 12; i++) out[i] = 0;
         for (const auto &s : p.spans) {
             float ms = 0;
             CUDA_CHECK(cudaEventElapsedTime(&ms, p.pool[s.a], p.pool[s.b]));

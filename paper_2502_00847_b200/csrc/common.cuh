@@ -76,6 +76,7 @@ struct Tab {
     u64 fp_mask;       // host-visible: bit i set when prime i < 2^46 (exact-FP64 NTT rows, ntt.cu FpA)
     const double *qd;  // [P] (double) q and RN(1 / q): no per-CTA int->double conversion or division
     const double *qinv;
+    int ntt_cluster;   // host-visible: single-pass cluster NTT for 0 none, 1 FP rows, 2 all rows (SECPE_NTT_CLUSTER)
 };
 
 // limb l of a polynomial -> global prime index

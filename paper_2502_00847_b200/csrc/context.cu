@@ -182,7 +182,7 @@ size_t Ctx::prof_begin(int) {
     CUDA_CHECK(cudaEventRecord(prof.next(), st));
     return a;
 }
-void Ctx::prof_end(size_t a, int kind, double bytes, long long units) {
+void Ctx::prof_end(size_t a, int kind, double bytes, double units) {
     if (!prof.on) return;
     const size_t b = prof.used;
     CUDA_CHECK(cudaEventRecord(prof.next(), st));
@@ -358,6 +358,9 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
     {
         const char *e = getenv("SECPE_NO_TC");  // development switch: integer base-conversion kernels
         use_tc = !(e && atoi(e) == 1);
+        // development switch: single-pass cluster NTT (ntt.cu; measured slower on the FP64-bound rows, off)
+        const char *c = getenv("SECPE_NTT_CLUSTER");
+        ntt_cluster = c ? atoi(c) : 0;
     }
     logn = logn_;
     N = 1L << logn;
@@ -415,7 +418,7 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
     d_tw = upload(tw, st);
     d_itw = upload(itw, st);
     tab = Tab{d_q.p, d_br0.p, d_br1.p, reinterpret_cast<const ulonglong2 *>(d_tw.p),
-              reinterpret_cast<const ulonglong2 *>(d_itw.p), d_ninv.p, d_ninvsh.p, 0, nullptr, nullptr};
+              reinterpret_cast<const ulonglong2 *>(d_itw.p), d_ninv.p, d_ninvsh.p, 0, nullptr, nullptr, ntt_cluster};
     {
         std::vector<u64> a(P), b(P);
         for (int i = 0; i < P; i++) {

@@ -72,9 +72,9 @@ struct Prof {
     size_t used = 0;
     struct Span {
         size_t a, b;
-        int kind;      // 0 NTT, 1 key switch, 2 rescale
+        int kind;      // 0 NTT launch on FP64 rows, 1 key switch, 2 rescale, 3 NTT launch on integer rows
         double bytes;  // algorithmic bytes of the span
-        long long units;
+        double units;
     };
     std::vector<Span> spans;
     cudaEvent_t next();
@@ -121,7 +121,7 @@ struct Ctx {
     Counters cnt;
     Prof prof;
     size_t prof_begin(int kind);
-    void prof_end(size_t a, int kind, double bytes, long long units);
+    void prof_end(size_t a, int kind, double bytes, double units);
 
     // encoded argmax masks (NTT form), keyed by layout / level / scale bits: encoded once per context
     std::map<std::string, std::shared_ptr<DevBuf>> pt_cache;
@@ -156,6 +156,7 @@ struct Ctx {
     const LevelConsts &level(int l) const { return *lvl[l]; }
     void build_tc_groups(LevelConsts &lc, int l);
     bool use_tc = true;  // tensor-core base conversion (SECPE_NO_TC=1 selects the integer kernels)
+    int ntt_cluster = 0; // single-pass cluster NTT (SECPE_NTT_CLUSTER; copied into tab)
     void log(const char *kind, int lin, int lout, double s, const std::string &extra);
 };
 

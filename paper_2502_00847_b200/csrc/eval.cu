@@ -25,16 +25,33 @@ LimbConst limb_const(const Ctx &c, i64 C, int nl) {
     return lc;
 }
 
+namespace {
+// profiling hook: one span per NTT launch, kind 0 (FP64 rows) or 3 (integer rows), algorithmic bytes
+// (every limb read once and written once, split evenly over the passes)
+struct NttSpans {
+    Ctx *c;
+    size_t open = 0;
+};
+void ntt_mark(void *p, int phase, bool fp, double bytes, double limbs) {
+    NttSpans &s = *static_cast<NttSpans *>(p);
+    if (phase == 0)
+        s.open = s.c->prof_begin(fp ? 0 : 3);
+    else
+        s.c->prof_end(s.open, fp ? 0 : 3, bytes, limbs);
+}
+}  // namespace
+
 void ev_ntt(Ctx &c, RowsArg d, int n_polys, LimbMap lm, bool inverse, const NttFusion &f) {
-    const size_t pa = c.prof_begin(0);
+    NttSpans spans{&c};
+    const NttProfHook hook{&spans, ntt_mark};
+    if (c.prof.on) ntt_set_prof_hook(&hook);
     if (inverse)
         ntt_inverse(c.tab, c.logn, d, n_polys, lm, c.st, f);
     else
         ntt_forward(c.tab, c.logn, d, n_polys, lm, c.st, f);
+    if (c.prof.on) ntt_set_prof_hook(nullptr);
     c.cnt.ntt_limbs += (long long)n_polys * lm.nl;
     c.cnt.launches += 2;
-    // algorithmic bytes: every limb read once and written once
-    c.prof_end(pa, 0, 16.0 * (double)n_polys * lm.nl * c.N, (long long)n_polys * lm.nl);
 }
 
 void ev_copy(Ctx &c, const CtView &a, const CtView &out) {

@@ -46,6 +46,13 @@ struct NttFusion {
 };
 void ntt_forward(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
                  const NttFusion &f = NttFusion());
+// optional profiling hook (bench.py roofline): called before (phase 0) and after (phase 1) every launch
+// with the row class of the launch (FP64 or integer rows) and its algorithmic bytes; thread-local
+struct NttProfHook {
+    void *ctx;
+    void (*mark)(void *ctx, int phase, bool fp, double bytes, double limbs);
+};
+void ntt_set_prof_hook(const NttProfHook *h);
 void ntt_inverse(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
                  const NttFusion &f = NttFusion());
 

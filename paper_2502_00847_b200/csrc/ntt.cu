@@ -486,6 +486,235 @@ __global__ void __launch_bounds__(CT, MinB<A>::v) ntt_contig(PassArgs a) {
     contig_body<LOGN, INV, IO, A>(a, sm, poly, limb, prime, P);
 }
 
+// ---------------------------------------------------------------------------------------------
+// single-pass cluster NTT (LOGN = 16): one thread-block cluster of CL CTAs per limb.  The limb is
+// read from HBM once and written once; the transpose between the column stages and the row stages
+// goes through distributed shared memory instead of a second HBM round trip.
+//   forward: CTA j runs stages 0..S1-1 on columns [j CC, (j+1) CC) (loaded straight from HBM) and
+//            parks them in its shared memory as [r][col]; after a cluster barrier it gathers rows
+//            [j RR, (j+1) RR) from all CL CTAs (ld.shared::cluster), runs stages S1..LOGN-1 and
+//            writes the rows with the contiguous pass's epilogue (rescale / ModDown fusions).
+//   inverse: mirror image: rows first (prologue fusions: copy-in, tensor product), parked as
+//            [r_local][col], columns gathered from all CTAs, GS stages S1-1..0, * N^{-1} (or k).
+// Each CTA's buffer is read remotely only between the two cluster barriers; the second one is
+// split (arrive after the gather, wait before the buffer is reused) so round 0 of the second half
+// overlaps the other CTAs' gathers.
+// ---------------------------------------------------------------------------------------------
+#ifndef NTT_CLUSTER_CTAS
+#define NTT_CLUSTER_CTAS 16  // CTAs per cluster (16 = non-portable maximum: 256-thread CTAs, 4 per SM)
+#endif
+constexpr int CL = NTT_CLUSTER_CTAS;
+template <int LOGN>
+struct ClusterCfg {
+    static constexpr int S1 = LOGN / 2, S2 = LOGN - S1;
+    static constexpr int G1 = 1 << S1, G2 = 1 << S2;  // column length, row length
+    static constexpr int NCOL = G2, NROW = G1;
+    static constexpr int CC = NCOL / CL, RR = NROW / CL;  // columns / rows per CTA
+    static constexpr int THREADS = CC * (G1 / NV);
+    static_assert(THREADS == RR * (G2 / NV), "cluster NTT: column and row halves need the same thread count");
+    static constexpr int PITCH = G2 + G2 / 16;
+    static constexpr int XW = (1 << LOGN) / CL;  // exchange block words
+    static constexpr int SMEM_WORDS = XW > RR * PITCH ? XW : RR * PITCH;
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ u64 ld_dsmem(uint32_t a) {
+    u64 v;
+    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
+template <class A>
+struct MinBC {
+    static constexpr int v = 48 / CL;  // integer Shoup rows: ~80 registers
+};
+template <>
+struct MinBC<FpA> {
+    static constexpr int v = 64 / CL;  // FP rows: 64 registers
+};
+
+template <int LOGN, bool INV, int IN, int OUT, class A>
+__global__ void __launch_bounds__(ClusterCfg<LOGN>::THREADS, MinBC<A>::v) ntt_cluster(PassArgs a) {
+    using CF = ClusterCfg<LOGN>;
+    constexpr int S1 = CF::S1, S2 = CF::S2, G2 = CF::G2, NCOL = CF::NCOL, CC = CF::CC, RR = CF::RR;
+    constexpr int PITCH = CF::PITCH;
+    constexpr long N = 1L << LOGN;
+    constexpr int TPR = G2 / NV;
+    extern __shared__ __align__(16) u64 xs[];
+    const int rank = blockIdx.x;  // == %cluster_ctarank (cluster dims (CL,1,1), gridDim.x == CL)
+    const int poly = a.poly0 + blockIdx.y / a.nsub, limb = a.limb0 + blockIdx.y % a.nsub;
+    const int prime = prime_of(a.lm, limb);
+    const PrimeC P = prime_consts(a.tab, prime);
+    const u64 q = P.q;
+    const ulonglong2 *tw = (INV ? a.tab.itw2 : a.tab.tw2) + prime * N;
+    u64 *const limb_base = a.d.p + poly_off(a.d.cs, a.d.ps, poly) + limb * N;
+    const uint32_t xs_local = smem_addr(xs);
+    u64 v[NV];
+    // row half: row gl of this CTA's RR rows, tau = thread within the row
+    const int rgl = threadIdx.x / TPR, rtau = threadIdx.x % TPR;
+    const int grow = rank * RR + rgl;  // global row (= contiguous block index)
+    u64 *const smg = xs + rgl * PITCH;
+    // column half: column ccl of this CTA's CC columns
+    const int ccl = threadIdx.x % CC, ctau = threadIdx.x / CC;
+    const int gcol = rank * CC + ccl;
+
+    if (!INV) {
+        using R = Rnd<S1, false>;
+        static_assert(R::NR == 2, "cluster NTT: two rounds per half");
+        constexpr int LO0 = R::lo(0), LO1 = R::lo(1);
+        // ---- columns: stages 0..S1-1 ----
+        u64 *cb = limb_base + gcol;
+        if constexpr (IN == IN_BCAST) {
+            const u64 *src = a.f.src.p + poly_off(a.f.src.cs, a.f.src.ps, poly) + gcol;
+            const u64 ql = a.tab.q[a.f.lp], hl = ql >> 1, hi = a.f.half[limb], one_sh = a.tab.br1[prime];
+#pragma unroll
+            for (int k = 0; k < NV; k++) {
+                const u64 r = csub(src[NCOL * held<LO0>(ctau, k)] + hl, ql);
+                v[k] = A::in(submod(hi, mul_shoup(r, 1, one_sh, q), q), P);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < NV; k++) v[k] = A::in(cb[NCOL * held<LO0>(ctau, k)], P);
+        }
+        do_round<S1, false, 0, false, LOGN, A>(v, ctau, 0, tw, P);
+#pragma unroll
+        for (int k = 0; k < NV; k++) xs[held<LO0>(ctau, k) * CC + ccl] = v[k];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < NV; k++) v[k] = xs[held<LO1>(ctau, k) * CC + ccl];
+        do_round<S1, false, 1, false, LOGN, A>(v, ctau, 0, tw, P);
+        // park [r][col]: each thread rewrites exactly the words it read
+#pragma unroll
+        for (int k = 0; k < NV; k++) xs[held<LO1>(ctau, k) * CC + ccl] = v[k];
+        cluster_arrive();
+        cluster_wait();
+        // ---- rows: stages S1..LOGN-1 on row grow ----
+        using RB2 = Rnd<S2, false>;
+        constexpr int RLO0 = RB2::lo(0), RLO1 = RB2::lo(1);
+#pragma unroll
+        for (int k = 0; k < NV; k++) {
+            const int c = held<RLO0>(rtau, k);
+            v[k] = ld_dsmem(mapa_rank(xs_local + 8u * (uint32_t)(grow * CC + (c % CC)), (uint32_t)(c / CC)));
+        }
+        cluster_arrive();
+        do_round<S2, false, 0, true, LOGN, A>(v, rtau, grow, tw, P);
+        cluster_wait();
+#pragma unroll
+        for (int k = 0; k < NV; k++) smg[padr(held<RLO0>(rtau, k))] = v[k];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < NV; k++) v[k] = smg[padr(held<RLO1>(rtau, k))];
+        do_round<S2, false, 1, true, LOGN, A>(v, rtau, grow, tw, P);
+#pragma unroll
+        for (int k = 0; k < NV; k++) smg[padr(held<RLO1>(rtau, k))] = A::out_fwd(v[k], P);
+        __syncthreads();
+        // epilogue on 16-byte vectors over this CTA's RR contiguous rows
+        const long boff = limb * N + (long)rank * RR * G2;
+        const ulonglong2 *e1 = nullptr, *e2 = nullptr;
+        ulonglong2 *dst;
+        u64 kc = 0, kcsh = 0;
+        if (OUT == OUT_PLAIN) {
+            dst = reinterpret_cast<ulonglong2 *>(a.d.p + poly_off(a.d.cs, a.d.ps, poly) + boff);
+        } else {
+            e1 = reinterpret_cast<const ulonglong2 *>(a.f.e1.p + poly_off(a.f.e1.cs, a.f.e1.ps, poly) + boff);
+            if (OUT == OUT_MODDOWN && (poly & 1) < a.f.e2_polys)
+                e2 = reinterpret_cast<const ulonglong2 *>(a.f.e2.p + poly_off(a.f.e2.cs, a.f.e2.ps, poly) + boff);
+            dst = reinterpret_cast<ulonglong2 *>(a.f.out.p + poly_off(a.f.out.cs, a.f.out.ps, poly) + boff);
+            kc = a.f.k[limb];
+            kcsh = a.f.ksh[limb];
+        }
+#pragma unroll 4
+        for (int i = threadIdx.x; i < RR * G2 / 2; i += CF::THREADS) {
+            const int e = 2 * i, gg = e / G2, r = e % G2;
+            u64 x0 = xs[gg * PITCH + padr(r)], x1 = xs[gg * PITCH + padr(r + 1)];
+            if (OUT == OUT_RESCALE) {
+                const ulonglong2 c = e1[i];
+                x0 = mul_shoup(addmod(c.x, x0, q), kc, kcsh, q);
+                x1 = mul_shoup(addmod(c.y, x1, q), kc, kcsh, q);
+            } else if (OUT == OUT_MODDOWN) {
+                const ulonglong2 c = e1[i];
+                x0 = mul_shoup(submod(c.x, x0, q), kc, kcsh, q);
+                x1 = mul_shoup(submod(c.y, x1, q), kc, kcsh, q);
+                if (e2) {
+                    const ulonglong2 d = e2[i];
+                    x0 = addmod(x0, d.x, q);
+                    x1 = addmod(x1, d.y, q);
+                }
+            }
+            dst[i] = make_ulonglong2(x0, x1);
+        }
+    } else {
+        using RB2 = Rnd<S2, true>;
+        static_assert(RB2::NR == 2, "cluster NTT: two rounds per half");
+        constexpr int RLO0 = RB2::lo(0), RLO1 = RB2::lo(1);
+        // ---- rows: GS stages LOGN-1..S1 on this CTA's RR rows (prologue fusions) ----
+        const long boff = limb * N + (long)rank * RR * G2;
+        const u64 *sp = (IN == IN_SRC || IN == IN_MUL) ? a.f.src.p + poly_off(a.f.src.cs, a.f.src.ps, poly) + boff
+                                                       : limb_base + (long)rank * RR * G2;
+        const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(sp);
+        const ulonglong2 *src2 = nullptr;
+        if (IN == IN_MUL)
+            src2 = reinterpret_cast<const ulonglong2 *>(a.f.src2.p + poly_off(a.f.src2.cs, a.f.src2.ps, poly) + boff);
+        const u64 br0 = a.tab.br0[prime], br1 = a.tab.br1[prime];
+#pragma unroll 4
+        for (int i = threadIdx.x; i < RR * G2 / 2; i += CF::THREADS) {
+            ulonglong2 x = src[i];
+            if (IN == IN_MUL) {
+                const ulonglong2 y = src2[i];
+                x.x = mulmod(x.x, y.x, q, br0, br1);
+                x.y = mulmod(x.y, y.y, q, br0, br1);
+            }
+            const int e = 2 * i, gg = e / G2, r = e % G2;
+            xs[gg * PITCH + padr(r)] = A::in(x.x, P);
+            xs[gg * PITCH + padr(r + 1)] = A::in(x.y, P);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < NV; k++) v[k] = smg[padr(held<RLO0>(rtau, k))];
+        do_round<S2, true, 0, true, LOGN, A>(v, rtau, grow, tw, P);
+#pragma unroll
+        for (int k = 0; k < NV; k++) smg[padr(held<RLO0>(rtau, k))] = v[k];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < NV; k++) v[k] = smg[padr(held<RLO1>(rtau, k))];
+        do_round<S2, true, 1, true, LOGN, A>(v, rtau, grow, tw, P);
+        __syncthreads();  // the padded row layout is dead: park [r_local][col]
+#pragma unroll
+        for (int k = 0; k < NV; k++) xs[rgl * NCOL + held<RLO1>(rtau, k)] = v[k];
+        cluster_arrive();
+        cluster_wait();
+        // ---- columns: GS stages S1-1..0 on column gcol ----
+        using R = Rnd<S1, true>;
+        constexpr int LO0 = R::lo(0), LO1 = R::lo(1);
+#pragma unroll
+        for (int k = 0; k < NV; k++) {
+            const int r = held<LO0>(ctau, k);
+            v[k] = ld_dsmem(mapa_rank(xs_local + 8u * (uint32_t)((r % RR) * NCOL + gcol), (uint32_t)(r / RR)));
+        }
+        cluster_arrive();
+        do_round<S1, true, 0, false, LOGN, A>(v, ctau, 0, tw, P);
+        cluster_wait();
+#pragma unroll
+        for (int k = 0; k < NV; k++) xs[held<LO0>(ctau, k) * CC + ccl] = v[k];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < NV; k++) v[k] = xs[held<LO1>(ctau, k) * CC + ccl];
+        do_round<S1, true, 1, false, LOGN, A>(v, ctau, 0, tw, P);
+        const u64 ni = a.f.k ? a.f.k[limb] : a.tab.ninv[prime];
+        const u64 nish = a.f.k ? a.f.ksh[limb] : a.tab.ninvsh[prime];
+        u64 *cb = limb_base + gcol;
+#pragma unroll
+        for (int k = 0; k < NV; k++) cb[NCOL * held<LO1>(ctau, k)] = A::out_scaled(v[k], ni, nish, P);
+    }
+}
+
 template <typename K>
 void max_smem_carveout(K kern) {
     static bool done = false;  // per instantiation
@@ -514,8 +743,12 @@ inline bool limb_fp(const PassArgs &a, int limb) {
     const int p = prime_of(a.lm, limb);
     return p < 64 && ((a.tab.fp_mask >> p) & 1);
 }
+thread_local const NttProfHook *g_hook = nullptr;
+
+// calls launch(a, fp) once per run of same-class limbs; `passes` = launches per limb transform that
+// this call makes (2: one of the two passes, 1: single-pass cluster kernel) for the profiling hook
 template <class F>
-void for_runs(const PassArgs &a0, F launch) {
+void for_runs(const PassArgs &a0, int n_polys, int passes, long N, F launch) {
     int l = 0;
     while (l < a0.lm.nl) {
         const bool fp = limb_fp(a0, l);
@@ -524,13 +757,18 @@ void for_runs(const PassArgs &a0, F launch) {
         PassArgs a = a0;
         a.limb0 = l;
         a.nsub = e - l;
+        // per launch: its share of the limb transforms (a two-pass transform counts half in each pass)
+        const double limbs = (double)n_polys * a.nsub / passes;
+        const double bytes = 16.0 * limbs * (double)N;  // N words read + written once per transform
+        if (g_hook) g_hook->mark(g_hook->ctx, 0, fp, bytes, limbs);
         launch(a, fp);
+        if (g_hook) g_hook->mark(g_hook->ctx, 1, fp, bytes, limbs);
         l = e;
     }
 }
 template <int LOGN, bool INV, int IN>
 void launch_strided(const PassArgs &a0, int n_polys, cudaStream_t st) {
-    for_runs(a0, [&](const PassArgs &a, bool fp) {
+    for_runs(a0, n_polys, 2, 1L << LOGN, [&](const PassArgs &a, bool fp) {
         if (fp)
             launch_strided_a<LOGN, INV, IN, FpA>(a, n_polys, st);
         else
@@ -539,7 +777,7 @@ void launch_strided(const PassArgs &a0, int n_polys, cudaStream_t st) {
 }
 template <int LOGN, bool INV, int IO>
 void launch_contig(const PassArgs &a0, int n_polys, cudaStream_t st) {
-    for_runs(a0, [&](const PassArgs &a, bool fp) {
+    for_runs(a0, n_polys, 2, 1L << LOGN, [&](const PassArgs &a, bool fp) {
         if (fp)
             launch_contig_a<LOGN, INV, IO, FpA>(a, n_polys, st);
         else
@@ -572,9 +810,93 @@ void run(const PassArgs &a0, int n_polys, bool inverse, cudaStream_t st) {
     }
 }
 
+// Tab::ntt_cluster (SECPE_NTT_CLUSTER at context creation): 0 = two-pass everywhere (default; the FP rows
+// are FP64-pipe bound and the cluster barriers cost more than the saved HBM pass), 1 = single-pass
+// cluster kernel for FP rows, 2 = for every row
+inline int cluster_mode(const PassArgs &a) { return a.tab.ntt_cluster; }
+
+template <int LOGN, bool INV, int IN, int OUT, class A>
+void launch_cluster_a(const PassArgs &a, int n_polys, cudaStream_t st) {
+    using CF = ClusterCfg<LOGN>;
+    auto kern = ntt_cluster<LOGN, INV, IN, OUT, A>;
+    static bool done = false;  // per instantiation
+    if (!done) {
+        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_WORDS * 8));
+        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        if (CL > 8) CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        done = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(CL, n_polys * a.nsub);
+    cfg.blockDim = dim3(CF::THREADS);
+    cfg.dynamicSmemBytes = CF::SMEM_WORDS * 8;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a));
+}
+
+template <int LOGN, bool INV, int IN, int OUT>
+void launch_cluster_or_split(const PassArgs &a0, int n_polys, cudaStream_t st) {
+    const int mode = cluster_mode(a0);
+    for_runs(a0, n_polys, 1, 1L << LOGN, [&](const PassArgs &a, bool fp) {
+        if (fp && mode >= 1) {
+            launch_cluster_a<LOGN, INV, IN, OUT, FpA>(a, n_polys, st);
+        } else if (!fp && mode >= 2) {
+            launch_cluster_a<LOGN, INV, IN, OUT, IntA>(a, n_polys, st);
+        } else if (!INV) {
+            if (fp) {
+                launch_strided_a<LOGN, false, IN, FpA>(a, n_polys, st);
+                launch_contig_a<LOGN, false, OUT, FpA>(a, n_polys, st);
+            } else {
+                launch_strided_a<LOGN, false, IN, IntA>(a, n_polys, st);
+                launch_contig_a<LOGN, false, OUT, IntA>(a, n_polys, st);
+            }
+        } else {
+            if (fp) {
+                launch_contig_a<LOGN, true, IN, FpA>(a, n_polys, st);
+                launch_strided_a<LOGN, true, IN_PLAIN, FpA>(a, n_polys, st);
+            } else {
+                launch_contig_a<LOGN, true, IN, IntA>(a, n_polys, st);
+                launch_strided_a<LOGN, true, IN_PLAIN, IntA>(a, n_polys, st);
+            }
+        }
+        LAUNCH_CHECK();
+    });
+}
+
 template <int LOGN>
 void run_chunk(const PassArgs &a, int rows, bool inverse, cudaStream_t st) {
     const NttFusion &f = a.f;
+    if constexpr (LOGN == 16) {
+        if (cluster_mode(a) > 0) {
+            if (!inverse) {
+                const bool bc = f.in_mode == IN_BCAST;
+                if (f.out_mode == OUT_RESCALE)
+                    bc ? launch_cluster_or_split<LOGN, false, IN_BCAST, OUT_RESCALE>(a, rows, st)
+                       : launch_cluster_or_split<LOGN, false, IN_PLAIN, OUT_RESCALE>(a, rows, st);
+                else if (f.out_mode == OUT_MODDOWN)
+                    bc ? launch_cluster_or_split<LOGN, false, IN_BCAST, OUT_MODDOWN>(a, rows, st)
+                       : launch_cluster_or_split<LOGN, false, IN_PLAIN, OUT_MODDOWN>(a, rows, st);
+                else
+                    bc ? launch_cluster_or_split<LOGN, false, IN_BCAST, OUT_PLAIN>(a, rows, st)
+                       : launch_cluster_or_split<LOGN, false, IN_PLAIN, OUT_PLAIN>(a, rows, st);
+            } else {
+                if (f.in_mode == IN_SRC)
+                    launch_cluster_or_split<LOGN, true, IN_SRC, OUT_PLAIN>(a, rows, st);
+                else if (f.in_mode == IN_MUL)
+                    launch_cluster_or_split<LOGN, true, IN_MUL, OUT_PLAIN>(a, rows, st);
+                else
+                    launch_cluster_or_split<LOGN, true, IN_PLAIN, OUT_PLAIN>(a, rows, st);
+            }
+            return;
+        }
+    }
     if (!inverse) {
         if (f.in_mode == IN_BCAST)
             launch_strided<LOGN, false, IN_BCAST>(a, rows, st);
@@ -613,6 +935,8 @@ void dispatch(int logn, const PassArgs &a, int rows, bool inverse, cudaStream_t 
 }
 
 }  // namespace
+
+void ntt_set_prof_hook(const NttProfHook *h) { g_hook = h; }
 
 void ntt_forward(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
                  const NttFusion &f) {

@@ -353,3 +353,35 @@ def test_argmax_config5_full(S):
     """BASELINE configs[4] at full size (N = 2^16, 30 limbs, 2048 queries x P=8 x K=2), batch of 2 as bench:
     ciphertext 0 bit-exact against the oracle, every query's label exact above the margin."""
     run_argmax_pair(S, "argmax", "argmax_k2", "sign_7_15_15.json", 1000 * 5 + 1, n_ct=2, oracle_cts=1)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_cluster_ntt_path(S, monkeypatch, mode):
+    """SECPE_NTT_CLUSTER=1 (FP rows) / 2 (all rows): the single-pass thread-block-cluster NTT (ntt.cu
+    ntt_cluster, DSMEM transpose) gives the same integers as the oracle -- plain forward/inverse on the
+    configs[4] 45-bit chain + special primes and on the configs[1] 60-bit primes, and the fused
+    prologue/epilogue modes through mul_relin_rescale and rotate (configs[2]/[3] parameters)."""
+    monkeypatch.setenv("SECPE_NTT_CLUSTER", str(mode))
+    for name, first, n_limbs in (("argmax", 20, 18), ("ntt", 3, 5)):
+        prm = ckks.Params(synth.PARAM_SETS[name])
+        g = S.Context(synth.PARAM_SETS[name])
+        primes = prm.primes[first:first + n_limbs]
+        x = synth.uniform_residues(300 + first, primes, 2, prm.logn)
+        t = torch.from_numpy(x.copy()).cuda()
+        g.ntt(t, first, n_limbs)
+        got = t.cpu().numpy()
+        for pi, l in ((0, 0), (1, n_limbs - 1), (1, n_limbs // 2)):
+            assert np.array_equal(got[pi, l], ckks.ntt(x[pi, l], primes[l], prm.psi[first + l], prm.logn)), (name, pi, l)
+        g.ntt(t, first, n_limbs, inverse=True)
+        assert np.array_equal(t.cpu().numpy(), x)
+    P = Pair(S, "argmax" if mode == 1 else "ks")  # 45-bit FP rows / 60-bit integer rows
+    prm, g = P.prm, P.gpu
+    ev = ckks.Oracle(prm)
+    seed = synth.KEY_SEED_BASE + 3
+    ko, kg = ev.keygen(seed, [1]), g.keygen(seed, [1])
+    z1, z2 = synth.uniform_slots(51, prm.N // 2), synth.uniform_slots(52, prm.N // 2)
+    a = ev.encrypt(ko, z1, prm.scale, 1)
+    b = ev.encrypt(ko, z2, prm.scale, 2)
+    ga, gb = P.up(a), P.up(b)
+    assert np.array_equal(P.down(g.mul_relin_rescale(kg, ga, gb)), ev.rescale(ev.mul_relin(ko, a, b)).data)
+    assert np.array_equal(P.down(g.rotate(kg, ga, 1)), ev.rotate_raw(ko, a, 1).data)
