@@ -179,6 +179,17 @@ int secpe_mul_relin_rescale(secpe_ctx *ctx, const secpe_keys *keys, const secpe_
  * pass over the Galois key.  out[i] must not alias in[i]. */
 int secpe_rotate_batch(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n, int32_t steps,
                        secpe_ct *out);
+/* Hoisted rotations (reading R29; PAPER.md:237 rotates the same ciphertext by several
+ * steps): the n ciphertexts in[0..n) (same level and scale) rotated by each of steps[0..n_steps) with
+ * ONE ModUp of c1 shared by all steps: for Galois element g,
+ *   out = (sigma_g(c0) + ks0, ks1),  ks = ModDown(sum_j sigma_g(ModUp_j(c1)) * gk_g[j]).
+ * Not the same integers as secpe_rotate (ModUp does not commute with sigma_g); the same plaintext up
+ * to key-switching noise.  out is [n_steps][n], row-major: out[s * n + i] receives step s of ct i,
+ * level = out[0].level (<= input level; lower drops limbs), scale = input scale; must not alias in.
+ * Steps with g = 1 copy.  Errors: SECPE_ENOKEY for a missing Galois key (checked before any work),
+ * SECPE_EINVAL for null arguments, n < 1 or n_steps < 1. */
+int secpe_rotate_hoisted(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n,
+                         const int32_t *steps, int32_t n_steps, secpe_ct *out);
 /* Rescale by q_level: round(c / q_l) (round half up, reading R12).  out level = in level - 1,
  * out scale = scale / q_l.  out must not alias. */
 int secpe_rescale(secpe_ctx *ctx, const secpe_ct *in, secpe_ct *out);

@@ -82,6 +82,7 @@ def lib():
             "o_mul_plain": (None, [ctypes.c_void_p, u64p, I, u64p, u64p]),
             "o_tensor": (None, [ctypes.c_void_p, u64p, u64p, I, u64p]),
             "o_keyswitch": (None, [ctypes.c_void_p, u64p, I, u64p, u64p]),
+            "o_keyswitch_g": (None, [ctypes.c_void_p, u64p, I, u64p, ctypes.c_uint64, u64p]),
             "o_rescale": (None, [ctypes.c_void_p, u64p, I, u64p]),
             "o_mul_vec": (None, [u64p, u64p, U, U, u64p]),
             "o_automorph": (None, [ctypes.c_void_p, u64p, I, I, U, u64p]),
@@ -512,6 +513,36 @@ class Oracle:
         out[0] = o0
         out[1] = ks[1]
         return Ct(out, ct.scale)
+
+    def rotate_hoisted_raw(self, keys, ct, steps_list):
+        """N2: rotations of ONE ciphertext by several steps sharing one ModUp of c1
+        (PAPER.md:237 applies rotations to the same ciphertext; the hoisting itself is this build's
+        reading R29): for each step with Galois element g,
+            ks = ModDown( sum_j sigma_g(ModUp_j(c1)) * gk_g[j] ),   out = (sigma_g(c0) + ks0, ks1).
+        sigma_g is applied to the integer polynomials ModUp_j(c1), so the integers differ from
+        rotate_raw (ModUp of sigma_g(c1), O-12) by key-switching noise only."""
+        prm = self.prm
+        nl = ct.level + 1
+        c1 = np.ascontiguousarray(ct.data[1])
+        outs = []
+        for st in steps_list:
+            g = galois_elt(prm, st)
+            if g == 1:
+                outs.append(ct.copy())
+                continue
+            if g not in keys.gk:
+                raise KeyError("no Galois key for step %d" % st)
+            sig0 = np.zeros((1, nl, prm.N), dtype=np.uint64)
+            lib().o_automorph(prm.cptr, P(np.ascontiguousarray(ct.data[:1])), nl, 1, g, P(sig0))
+            ks = np.zeros((2, nl, prm.N), dtype=np.uint64)
+            lib().o_keyswitch_g(prm.cptr, P(c1), nl, P(keys.gk[g]), g, P(ks))
+            out = np.zeros_like(ct.data)
+            o0 = np.zeros((nl, prm.N), dtype=np.uint64)
+            lib().o_add(prm.cptr, P(np.ascontiguousarray(sig0[0])), P(np.ascontiguousarray(ks[0])), nl, 1, P(o0))
+            out[0] = o0
+            out[1] = ks[1]
+            outs.append(Ct(out, ct.scale))
+        return outs
 
     # ---- planned ops (logged; reading R9 scale planning) ------------------------------------
     def rot(self, keys, x, steps):

@@ -486,7 +486,21 @@ void o_tensor(const OCtx *c, const u64 *a, const u64 *b, int nl, u64 *d) {
  */
 /* ModUp + key inner product of O-10: returns acc[2][ne][N] (NTT form over Q_level u P, extended
  * index e < nl -> prime e, e >= nl -> special prime e - nl); *eid_out = extended index -> prime id */
-static u64 *ks_acc(const OCtx *c, const u64 *d, int nl, const u64 *swk, int **eid_out) {
+/* sigma_g on one coefficient-form residue vector mod q: X^k -> X^{kg mod 2N}, negated when
+ * kg mod 2N >= N (O-12) */
+static void sigma_coeff(const u64 *in, u64 *out, u64 n, u64 g, u64 q) {
+    u64 two_n = 2 * n;
+    for (u64 k = 0; k < n; k++) {
+        u64 e = (u64)(((u128)k * g) % two_n);
+        if (e >= n) out[e - n] = submod(0, in[k], q);
+        else out[e] = in[k];
+    }
+}
+
+/* g > 1 (N2, hoisted rotation): every extended digit polynomial ModUp_j(d) is replaced by
+ * sigma_g(ModUp_j(d)) -- the automorphism applied to the integer polynomial ModUp_j(d) limb by limb
+ * in the coefficient domain -- before the inner product with the Galois key of g. */
+static u64 *ks_acc(const OCtx *c, const u64 *d, int nl, const u64 *swk, u64 g, int **eid_out) {
     u64 n = NN(c);
     int nq = c->nq, np = c->np, ne = nl + np, nek = nq + np;
     (void)nq;
@@ -512,7 +526,15 @@ static u64 *ks_acc(const OCtx *c, const u64 *d, int nl, const u64 *swk, int **ei
         for (int e = 0; e < ne; e++) {
             u64 t = c->primes[eid[e]];
             u64 *x = ext + (u64)e * n;
-            if (e >= i0 && e < i1) { memcpy(x, d + (u64)e * n, n * sizeof(u64)); continue; }
+            if (e >= i0 && e < i1) {
+                if (g <= 1) { memcpy(x, d + (u64)e * n, n * sizeof(u64)); continue; }
+                u64 *y = (u64 *)malloc(n * sizeof(u64));
+                sigma_coeff(dc + (u64)e * n, y, n, g, t);
+                memcpy(x, y, n * sizeof(u64));
+                free(y);
+                o_ntt(x, c->logn, t, c->psi[eid[e]]);
+                continue;
+            }
             u64 hat_t[64]; /* (Q'_j/q_i) mod t */
             for (int i = i0; i < i1; i++) {
                 u64 h = 1;
@@ -526,6 +548,12 @@ static u64 *ks_acc(const OCtx *c, const u64 *d, int nl, const u64 *swk, int **ei
                     sum = addmod(sum, mulmod(y % t, hat_t[i - i0], t), t);
                 }
                 x[k] = sum;
+            }
+            if (g > 1) {
+                u64 *y = (u64 *)malloc(n * sizeof(u64));
+                sigma_coeff(x, y, n, g, t);
+                memcpy(x, y, n * sizeof(u64));
+                free(y);
             }
             o_ntt(x, c->logn, t, c->psi[eid[e]]);
         }
@@ -546,11 +574,17 @@ static u64 *ks_acc(const OCtx *c, const u64 *d, int nl, const u64 *swk, int **ei
     return acc;
 }
 
-void o_keyswitch(const OCtx *c, const u64 *d, int nl, const u64 *swk, u64 *ks) {
+void o_keyswitch_g(const OCtx *c, const u64 *d, int nl, const u64 *swk, u64 g, u64 *ks);
+void o_keyswitch(const OCtx *c, const u64 *d, int nl, const u64 *swk, u64 *ks) { o_keyswitch_g(c, d, nl, swk, 1, ks); }
+
+/* O-10 key switching with the automorphism sigma_g hoisted past ModUp (N2): ks0 + ks1 s ~=
+ * sigma_g(d) sigma_g(s) when swk is the Galois key of g -- ModUp of the un-rotated d, sigma_g on every
+ * extended digit, inner product, ModDown.  g = 1 is plain O-10. */
+void o_keyswitch_g(const OCtx *c, const u64 *d, int nl, const u64 *swk, u64 g, u64 *ks) {
     u64 n = NN(c);
     int nq = c->nq, np = c->np, ne = nl + np;
     int *eid;
-    u64 *acc = ks_acc(c, d, nl, swk, &eid);
+    u64 *acc = ks_acc(c, d, nl, swk, g, &eid);
     /* ModDown */
     for (int b = 0; b < 2; b++) {
         u64 *ab = acc + (u64)b * ne * n;

@@ -430,6 +430,28 @@ int secpe_rotate_batch(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *i
         batch_out_finish(c, out, n, vo, so);
     });
 }
+int secpe_rotate_hoisted(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n,
+                         const int32_t *steps, int32_t n_steps, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && keys && in && steps && out && n >= 1 && n_steps >= 1, SECPE_EINVAL, "null argument");
+        Ctx &c = ctx->c;
+        DevBuf si;
+        CtView vi = batch_in(c, in, n, si);
+        const int lv = out[0].level;
+        REQUIRE(lv >= 0 && lv <= vi.level, SECPE_ELEVEL, "output level above the input level");
+        std::vector<DevBuf> so(n_steps);
+        std::vector<CtView> vo(n_steps);
+        for (int s = 0; s < n_steps; s++) {
+            for (int i = 0; i < n; i++)
+                for (int j = 0; j < n; j++)
+                    REQUIRE(out[s * n + i].data != in[j].data, SECPE_EINVAL, "out must not alias in");
+            vo[s] = batch_out(c, out + (long)s * n, n, lv, vi.scale, so[s]);
+        }
+        std::vector<int> st(steps, steps + n_steps);
+        ev_rotate_hoisted(c, *keys->k, vi, st.data(), n_steps, vo.data());
+        for (int s = 0; s < n_steps; s++) batch_out_finish(c, out + (long)s * n, n, vo[s], so[s]);
+    });
+}
 int secpe_rescale(secpe_ctx *ctx, const secpe_ct *in, secpe_ct *out) {
     return guard([&] {
         REQUIRE(ctx && out && out->data, SECPE_EINVAL, "null argument");

@@ -199,6 +199,7 @@ void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &
                           const CtView &out, const CtView *lin_x2 = nullptr, i64 C2 = 0);
 void ev_lincomb(Ctx &c, const CtView &a, i64 C1, const CtView *b, i64 C2, const CtView &out);
 void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView &out);
+void ev_rotate_hoisted(Ctx &c, const Keys &k, const CtView &in, const int *steps, int n_steps, const CtView *outs);
 void ev_mul_plain_ntt(Ctx &c, const CtView &a, const u64 *pt, const CtView &out);
 LimbConst limb_const(const Ctx &c, i64 C, int nl);
 

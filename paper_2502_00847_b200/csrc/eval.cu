@@ -135,8 +135,9 @@ void ev_rescale(Ctx &c, const CtView &in, const CtView &out) {
 // tensor (d0, d1) rows whose [P] multiple is added on the Q limbs (R11b).
 // ten != nullptr: relinearisation of the tensor of ten->a, ten->b formed on the fly (d unused): the
 // INTT's first pass multiplies a1 b1, the inner product forms d0, d1 (+ C x) and adds [P] d_b.
-static void ks_modup_inner(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, DevBuf &acc,
-                           const TensorSrc *ten = nullptr) {
+// ModUp of d (or of the tensor's d2 = a1 b1): ext[c][j][e] in NTT form, exts = beta (nl + np) N per ct
+static void ks_modup(Ctx &c, const u64 *d, long d_stride, int n, int level, DevBuf &ext,
+                     const TensorSrc *ten = nullptr) {
     const long N = c.N;
     const int nl = level + 1, np = c.np, ne = nl + np, bt = c.beta(level);
     const LevelConsts &lc = c.level(level);
@@ -156,7 +157,7 @@ static void ks_modup_inner(Ctx &c, const u64 *d, long d_stride, int n, int level
     ev_ntt(c, RowsArg{dc.p, 2L * nl * N, (long)nl * N}, n, qmap(nl), true, f1);
     // 2. ModUp into every digit's complement, then NTT of the converted limbs
     const long exts = (long)bt * ne * N;
-    DevBuf ext((size_t)n * exts, c.st);
+    ext = DevBuf((size_t)n * exts, c.st);
     if (c.use_tc && lc.tc_ok) {
         TcArgs t{};
         t.src = dc.p;
@@ -183,16 +184,33 @@ static void ks_modup_inner(Ctx &c, const u64 *d, long d_stride, int n, int level
                    false);
     }
     ev_ntt(c, RowsArg{ext.p + (long)nl * N, 2L * ne * N, (long)ne * N}, n * bt, LimbMap{np, 0, 0, c.nq}, false);
-    // 3. inner product with the switching key
-    const long accs = 2L * ne * N;
+    c.cnt.launches += 1;
+}
+
+// 3. inner product of the ModUp digits with the switching key (galois > 1: of sigma_g of the digits)
+static void ks_inner(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, const DevBuf &ext,
+                     DevBuf &acc, const TensorSrc *ten = nullptr, u64 galois = 1) {
+    const long N = c.N;
+    const int nl = level + 1, np = c.np, ne = nl + np, bt = c.beta(level);
+    const long exts = (long)bt * ne * N, accs = 2L * ne * N;
     acc = DevBuf((size_t)n * accs, c.st);
     k_ks_inner(c.tab, c.logn, d, d_stride, ext.p, exts, key, c.nq, np, acc.p, accs, n, nl, c.alpha, c.st, ten,
-               c.pmod.p);
-    c.cnt.launches += 2;
+               c.pmod.p, galois);
+    c.cnt.launches += 1;
+}
+
+static void ks_modup_inner(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, DevBuf &acc,
+                           const TensorSrc *ten = nullptr) {
+    DevBuf ext;
+    ks_modup(c, d, d_stride, n, level, ext, ten);
+    ks_inner(c, d, d_stride, n, level, key, ext, acc, ten);
 }
 
 // Hybrid key switching of d (NTT form; ct c at d + c * d_stride, level limbs), result added to
 // `add` (add_polys of 2 polynomials; compact, ct stride add_stride) and written compact to out.
+static void ks_moddown(Ctx &c, DevBuf &acc, int n, int level, const u64 *add, long add_stride, int add_polys,
+                       u64 *out, long out_stride);
+
 void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, const u64 *add,
                   long add_stride, int add_polys, u64 *out, long out_stride) {
     const long N = c.N;
@@ -200,6 +218,17 @@ void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u
     const size_t pa = c.prof_begin(1);
     DevBuf acc;
     ks_modup_inner(c, d, d_stride, n, level, key, acc);
+    ks_moddown(c, acc, n, level, add, add_stride, add_polys, out, out_stride);
+    c.cnt.keyswitch += n;
+    // algorithmic bytes (SURVEY 8(d)): input limbs + output limbs per ciphertext + the key once per batch
+    c.prof_end(pa, 1, 8.0 * N * ((double)n * (nl + 2 * nl + add_polys * nl) + 2.0 * bt * ne), n);
+}
+
+// ModDown of acc (R11) with the addend fused into the final NTT's epilogue; result compact in out
+static void ks_moddown(Ctx &c, DevBuf &acc, int n, int level, const u64 *add, long add_stride, int add_polys,
+                       u64 *out, long out_stride) {
+    const long N = c.N;
+    const int nl = level + 1, np = c.np, ne = nl + np, bt = c.beta(level);
     const long accs = 2L * ne * N;
     // 4. ModDown: INTT of the special limbs (with (P/p)^{-1} folded in), conversion to Q, then an NTT
     //    whose last pass forms (acc - T) P^{-1} + addend
@@ -236,9 +265,6 @@ void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u
     f6.ksh = c.pinv_sh.p;
     ev_ntt(c, RowsArg{T.p, Ts, (long)nl * N}, 2 * n, qmap(nl), false, f6);
     c.cnt.launches += 1;
-    c.cnt.keyswitch += n;
-    // algorithmic bytes (SURVEY 8(d)): input limbs + output limbs per ciphertext + the key once per batch
-    c.prof_end(pa, 1, 8.0 * N * ((double)n * (nl + 2 * nl + add_polys * nl) + 2.0 * bt * ne), n);
 }
 
 // Relinearise and rescale in one pass, bit-identical to ev_mul_relin followed by ev_rescale (R10-R12):
@@ -339,4 +365,49 @@ void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView 
     c.cnt.launches++;
     ev_keyswitch(c, sig.p + (long)nl * N, ss, in.n, out.level, it->second.p, sig.p, ss, 1, out.data, out.stride);
     c.cnt.rotate += in.n;
+}
+
+// Hoisted rotations (N2, reading R29): one ModUp of c1 shared by every step; per step the key inner
+// product gathers sigma_g of the digits (k_ks_inner galois), ModDown adds sigma_g(c0) in its final NTT.
+// Same integers as the oracle's rotate_hoisted_raw (not as ev_rotate: ModUp does not commute with sigma_g).
+void ev_rotate_hoisted(Ctx &c, const Keys &k, const CtView &in, const int *steps, int n_steps, const CtView *outs) {
+    if (n_steps <= 0) return;
+    const int level = outs[0].level, nl = level + 1, n = in.n;
+    for (int i = 0; i < n_steps; i++) {
+        if (outs[i].level != level || outs[i].n != n) throw SecpeError{-1, "rotate_hoisted: output batches differ"};
+        const u64 g = galois_elt(c, steps[i]);
+        if (g != 1 && k.gk.find(g) == k.gk.end())
+            throw SecpeError{-4, "no Galois key for rotation step " + std::to_string(steps[i])};
+    }
+    if (level > in.level) throw SecpeError{-1, "rotate_hoisted: output level above input"};
+    const long N = c.N, np = c.np, ne = nl + np, bt = c.beta(level);
+    const size_t pa = c.prof_begin(1);
+    const u64 *c1 = in.data + in.ps;
+    DevBuf ext;
+    bool have_ext = false;
+    int n_ks = 0;
+    for (int i = 0; i < n_steps; i++) {
+        const u64 g = galois_elt(c, steps[i]);
+        if (g == 1) {
+            ev_copy(c, in, outs[i]);
+            continue;
+        }
+        if (!have_ext) {
+            ks_modup(c, c1, in.stride, n, level, ext);
+            have_ext = true;
+        }
+        const u64 *key = k.gk.find(g)->second.p;
+        DevBuf sig0((size_t)n * nl * N, c.st);  // sigma_g(c0) of every ciphertext, compact
+        k_automorph(c.logn, CRows{in.data, 2 * in.stride, in.stride}, RowsArg{sig0.p, 2L * nl * N, (long)nl * N}, n,
+                    nl, g, c.st);
+        c.cnt.launches++;
+        DevBuf acc;
+        ks_inner(c, c1, in.stride, n, level, key, ext, acc, nullptr, g);
+        ks_moddown(c, acc, n, level, sig0.p, (long)nl * N, 1, outs[i].data, outs[i].stride);
+        c.cnt.keyswitch += n;
+        c.cnt.rotate += n;
+        n_ks++;
+    }
+    // algorithmic bytes: c1 once + per rotation (c0 in, output, key once per batch)
+    c.prof_end(pa, 1, 8.0 * N * ((double)n * nl + n_ks * ((double)n * 3 * nl + 2.0 * bt * ne)), (double)n * n_ks);
 }

@@ -99,7 +99,8 @@ struct TensorSrc {
 };
 void k_ks_inner(const Tab &tab, int logn, const u64 *d, long d_ct_stride, const u64 *ext, long ext_ct_stride,
                 const u64 *key, int nq_total, int np, u64 *acc, long acc_ct_stride, int n_ct, int nl,
-                int alpha, cudaStream_t st, const TensorSrc *ten = nullptr, const u64 *pmod = nullptr);
+                int alpha, cudaStream_t st, const TensorSrc *ten = nullptr, const u64 *pmod = nullptr,
+                u64 galois = 1);  // galois > 1: read sigma_g(X_j) (NTT-domain gather; hoisted rotation, R29)
 // ModDown conversion (R11, R11b): T[c][b][i] = sum_{s < ns} y_s [B/s]_{q_i} mod q_i for i < nt, with
 // y_s = acc[c][b][row0 + s] (coefficient form, already times (B/s)^{-1}); hatpk[s * hstride + i]
 // split-30 packed

@@ -101,14 +101,30 @@ template <int MAXB>
 struct KsIn {
     ulonglong2 x[MAXB], d0, d1, a0, a1, b0, b1, x0, x1, y0, y1;
 };
+// Hoisted rotation (R29): the key inner product reads sigma_g(x) instead of x.  In the NTT domain
+// sigma_g is the permutation NTT(sigma_g a)[i] = NTT(a)[pi(i)], 2 brv(pi(i)) + 1 = g (2 brv(i) + 1) mod 2N;
+// for even k, pi(k + 1) = pi(k) ^ 1, so the output pair (k, k+1) reads one aligned source pair (swapped
+// when pi(k) is odd), and aligned blocks of 2^m map onto aligned blocks (coalesced gathers).
+__device__ __forceinline__ long gal_src(long k, int logn, u64 g, bool &swap) {
+    const unsigned e = 2u * (__brev((unsigned)k) >> (32 - logn)) + 1u;
+    const unsigned e2 = (unsigned)(((u64)e * g) & ((2ull << logn) - 1));
+    const unsigned j = __brev((e2 - 1u) >> 1) >> (32 - logn);
+    swap = j & 1u;
+    return (long)(j & ~1u);
+}
+
 template <int MAXB, bool TEN>
 __device__ __forceinline__ void ks_load(KsIn<MAXB> &in, int c, const u64 *__restrict__ d, long ds,
                                         const u64 *__restrict__ ext, long exts, int e, int jd, int ne, int nl,
-                                        int beta, long N, long k, const TensorSrc &ten) {
+                                        int beta, long N, long k, const TensorSrc &ten, long kx = -1,
+                                        bool swap = false) {
+    if (kx < 0) kx = k;
 #pragma unroll
     for (int j = 0; j < MAXB; j++)
-        if (j < beta && (!TEN || j != jd))
-            in.x[j] = ldv2((j == jd) ? d + c * ds + e * N + k : ext + c * exts + ((long)j * ne + e) * N + k);
+        if (j < beta && (!TEN || j != jd)) {
+            in.x[j] = ldv2((j == jd) ? d + c * ds + e * N + kx : ext + c * exts + ((long)j * ne + e) * N + kx);
+            if (swap) in.x[j] = make_ulonglong2(in.x[j].y, in.x[j].x);
+        }
     if (TEN && e < nl) {
         const long o = e * N + k;
         in.a0 = ldv2(ten.a.p + c * ten.a.cs + o);
@@ -197,10 +213,12 @@ __global__ void __launch_bounds__(TPB, TEN ? 2 : 3) ks_inner_vec_kernel(Tab tab,
                                                            const u64 *__restrict__ key, int nq_total, int np,
                                                            u64 *__restrict__ acc, long accs, int n_ct, int nl,
                                                            int alpha, int beta, TensorSrc ten,
-                                                           const u64 *__restrict__ pmod) {
+                                                           const u64 *__restrict__ pmod, u64 galois) {
     const int e = blockIdx.y;
     const long N = 1L << logn;
     const long k = 2L * ((long)blockIdx.x * TPB + threadIdx.x);
+    bool swap = false;
+    const long kx = (!TEN && galois > 1) ? gal_src(k, logn, galois, swap) : k;  // hoisted rotation gather
     const int ne = nl + np, nk = nq_total + np;
     const int pr = e < nl ? e : nq_total + (e - nl);
     const u64 q = tab.q[pr], r0 = tab.br0[pr], r1 = tab.br1[pr];
@@ -221,9 +239,10 @@ __global__ void __launch_bounds__(TPB, TEN ? 2 : 3) ks_inner_vec_kernel(Tab tab,
     // plain key switching double-buffers the next ciphertext's inputs; with the tensor formed on the fly
     // the register budget goes to the tensor terms instead (single buffer)
     KsIn<MAXB> cur, nxt;
-    ks_load<MAXB, TEN>(cur, 0, d, ds, ext, exts, e, jd, ne, nl, beta, N, k, ten);
+    ks_load<MAXB, TEN>(cur, 0, d, ds, ext, exts, e, jd, ne, nl, beta, N, k, ten, kx, swap);
     for (int c = 0; c < n_ct; c++) {
-        if (!TEN && c + 1 < n_ct) ks_load<MAXB, TEN>(nxt, c + 1, d, ds, ext, exts, e, jd, ne, nl, beta, N, k, ten);
+        if (!TEN && c + 1 < n_ct)
+            ks_load<MAXB, TEN>(nxt, c + 1, d, ds, ext, exts, e, jd, ne, nl, beta, N, k, ten, kx, swap);
         if (qrow) {
             u64 e0, e1, e2, f0, f1, f2;
             if (q < (1ULL << 46)) {
@@ -273,10 +292,15 @@ template <int MAXB>
 __global__ void ks_inner_kernel(Tab tab, int logn, const u64 *__restrict__ d, long ds, const u64 *__restrict__ ext,
                                 long exts, const u64 *__restrict__ key, int nq_total, int np,
                                 u64 *__restrict__ acc, long accs, int n_ct, int nl, int alpha, int beta,
-                                TensorSrc ten, const u64 *__restrict__ pmod) {
+                                TensorSrc ten, const u64 *__restrict__ pmod, u64 galois) {
     const int e = blockIdx.y;
     const long N = 1L << logn;
     const long k = (long)blockIdx.x * TPB + threadIdx.x;
+    long kx = k;
+    if (galois > 1) {
+        bool sw;
+        kx = gal_src(k & ~1L, logn, galois, sw) + ((k & 1) ^ (sw ? 1 : 0));
+    }
     const bool qrow = ten.a.p && e < nl;
     const int ne = nl + np, nk = nq_total + np;
     const int pr = e < nl ? e : nq_total + (e - nl);
@@ -295,7 +319,7 @@ __global__ void ks_inner_kernel(Tab tab, int logn, const u64 *__restrict__ d, lo
                     lin2 ? ten.C2.c[e] : 0, lin2 ? ten.C2.csh[e] : 0, q, r0, r1, d0, d1, d2);
         }
         for (int j = 0; j < beta; j++) {
-            const u64 x = (j == jd) ? (qrow ? d2 : d[c * ds + e * N + k]) : ext[c * exts + ((long)j * ne + e) * N + k];
+            const u64 x = (j == jd) ? (qrow ? d2 : d[c * ds + e * N + kx]) : ext[c * exts + ((long)j * ne + e) * N + kx];
             mac_wide(s0, x, __ldg(key + (((long)j * 2 + 0) * nk + pr) * N + k));
             mac_wide(s1, x, __ldg(key + (((long)j * 2 + 1) * nk + pr) * N + k));
         }
@@ -469,8 +493,9 @@ void k_modup(const Tab &tab, int logn, const u64 *dc, long dcs, u64 *ext, long e
 }
 void k_ks_inner(const Tab &tab, int logn, const u64 *d, long ds, const u64 *ext, long exts, const u64 *key,
                 int nq_total, int np, u64 *acc, long accs, int n_ct, int nl, int alpha, cudaStream_t st,
-                const TensorSrc *ten, const u64 *pmod) {
+                const TensorSrc *ten, const u64 *pmod, u64 galois) {
     const int beta = (nl + alpha - 1) / alpha;
+    if (ten && galois > 1) throw SecpeError{-1, "ks_inner: the galois gather is for plain key switching only"};
     // 128-bit accumulation of beta + 1 products < 2^120 stays below the Barrett input bound 2^125
     // (checked at context creation against the actual prime sizes).
     const dim3 g2(chunks2(logn), nl + np), g1(chunks(logn), nl + np);
@@ -480,10 +505,10 @@ void k_ks_inner(const Tab &tab, int logn, const u64 *d, long ds, const u64 *ext,
     do {                                                                                                          \
         if (ten)                                                                                                  \
             ks_inner_vec_kernel<B_, true><<<g2, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, \
-                                                              accs, n_ct, nl, alpha, beta, T, pmod);              \
+                                                              accs, n_ct, nl, alpha, beta, T, pmod, galois);      \
         else                                                                                                      \
             ks_inner_vec_kernel<B_, false><<<g2, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np,     \
-                                                               acc, accs, n_ct, nl, alpha, beta, T, pmod);       \
+                                                               acc, accs, n_ct, nl, alpha, beta, T, pmod, galois); \
     } while (0)
     if (beta == 1)
         KSV(1);
@@ -495,7 +520,7 @@ void k_ks_inner(const Tab &tab, int logn, const u64 *d, long ds, const u64 *ext,
         KSV(4);
     else
         ks_inner_kernel<0><<<g1, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, n_ct, nl,
-                                               alpha, beta, T, pmod);
+                                               alpha, beta, T, pmod, galois);
 #undef KSV
     LAUNCH_CHECK();
 }

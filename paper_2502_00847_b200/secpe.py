@@ -74,6 +74,8 @@ SIGS = {
                                                ctypes.POINTER(CCt)]),
     "secpe_rotate_batch": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.c_int32,
                                           ctypes.POINTER(CCt)]),
+    "secpe_rotate_hoisted": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, i32p, ctypes.c_int32,
+                                            ctypes.POINTER(CCt)]),
     "secpe_rescale": (ctypes.c_int, [vp, ctypes.POINTER(CCt), ctypes.POINTER(CCt)]),
     "secpe_rotate": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.POINTER(CCt)]),
     "secpe_sign_poly": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.POINTER(SignCfg), ctypes.c_double,
@@ -364,6 +366,20 @@ class Context:
         _chk(lib().secpe_rotate_batch(self.h, keys.h, ca, a.n, steps, co))
         out.level, out.scale = co[0].level, co[0].scale
         return out
+
+    def rotate_hoisted(self, keys, a, steps, level=None):
+        """secpe_rotate_hoisted: every ciphertext of batch `a` rotated by each step with one shared ModUp
+        (N2, reading R29).  Returns one output batch per step."""
+        lv = a.level if level is None else level
+        outs = [self.new_ct(lv, a.n) for _ in steps]
+        ca = self._batch(a)
+        co = (CCt * (a.n * len(steps)))(*[CCt(ctypes.cast(o.t[i].data_ptr(), u64p), lv, 0.0)
+                                         for o in outs for i in range(a.n)])
+        st = np.asarray(steps, dtype=np.int32)
+        _chk(lib().secpe_rotate_hoisted(self.h, keys.h, ca, a.n, st.ctypes.data_as(i32p), len(steps), co))
+        for s, o in enumerate(outs):
+            o.level, o.scale = co[s * a.n].level, co[s * a.n].scale
+        return outs
 
     def rescale(self, a):
         out = self._out(a.level - 1)

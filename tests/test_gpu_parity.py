@@ -385,3 +385,45 @@ def test_cluster_ntt_path(S, monkeypatch, mode):
     ga, gb = P.up(a), P.up(b)
     assert np.array_equal(P.down(g.mul_relin_rescale(kg, ga, gb)), ev.rescale(ev.mul_relin(ko, a, b)).data)
     assert np.array_equal(P.down(g.rotate(kg, ga, 1)), ev.rotate_raw(ko, a, 1).data)
+
+
+@pytest.mark.parametrize("name,steps,n_ct,level_drop", [
+    ("toy", [1, 2, -1, 0, 3], 2, 0),          # ragged step set incl. identity, batch of 2
+    ("toy", [1, -1], 1, 2),                   # outputs below the input level
+    ("ks", [1, 4, 16384], 1, 0),              # configs[3] primes (60-bit integer rows), N = 2^16
+    ("argmax", [2, -2], 1, 10),               # configs[4] 45-bit FP rows, mid-chain level
+])
+def test_rotate_hoisted_bit_exact(S, name, steps, n_ct, level_drop):
+    """N2 hoisted rotations (secpe_rotate_hoisted, reading R29): every (step, ciphertext) output equal
+    word for word to the oracle's rotate_hoisted_raw; decrypts to RotL(z, step) within 2^-10."""
+    P = pair(S, name)
+    prm, g = P.prm, P.gpu
+    ev = ckks.Oracle(prm)
+    seed = synth.KEY_SEED_BASE + 7
+    rot = sorted({s for s in steps if s % (prm.N // 2)})
+    ko, kg = ev.keygen(seed, rot), g.keygen(seed, rot)
+    level = prm.L - level_drop
+    cts = [ev.encrypt(ko, synth.uniform_slots(60 + i, prm.N // 2), prm.scale, 20 + i) for i in range(n_ct)]
+    cts = [ev.drop(c, level) if level < c.level else c for c in cts]
+    batch = S.Ct(torch.from_numpy(np.stack([c.data for c in cts])).cuda(), level, prm.scale)
+    outs = g.rotate_hoisted(kg, batch, steps)
+    torch.cuda.synchronize()
+    for i, c in enumerate(cts):
+        want = ev.rotate_hoisted_raw(ko, c, steps)
+        for s, (st, o) in enumerate(zip(steps, outs)):
+            assert o.level == level and o.scale == prm.scale
+            assert np.array_equal(o.t[i].cpu().numpy(), want[s].data), (name, st, i)
+    z0 = synth.uniform_slots(60, prm.N // 2)
+    for st, o in zip(steps, outs):
+        got = ev.decrypt(ko, ckks.Ct(o.t[0].cpu().numpy(), o.scale))
+        assert np.abs(got.real - np.roll(z0, -st)).max() < 2 ** -10
+
+
+def test_rotate_hoisted_errors(S):
+    P = pair(S, "toy")
+    prm, g = P.prm, P.gpu
+    kg = g.keygen(synth.KEY_SEED_BASE + 7, [1])
+    z = synth.uniform_slots(1, prm.N // 2)
+    a = g.encrypt(kg, z, prm.L, prm.scale, 1)
+    with pytest.raises(Exception, match="Galois"):
+        g.rotate_hoisted(kg, a, [1, 5])

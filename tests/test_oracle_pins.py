@@ -329,6 +329,65 @@ def test_ops_against_slots(toy):
     assert np.abs(ev.decrypt(keys, w).real - (z1 - 0.5)).max() < tol
 
 
+def _ntt_sigma(vals, g, logn):
+    """NTT-domain sigma_g by the evaluation-point identity NTT(sigma_g a)[i] = NTT(a)[j] with
+    2 brv(j) + 1 = g (2 brv(i) + 1) mod 2N (R4 ordering), independent of o_automorph."""
+    n = 1 << logn
+    out = [0] * n
+    for i in range(n):
+        e = (g * (2 * brv(i, logn) + 1)) % (2 * n)
+        out[i] = int(vals[brv((e - 1) // 2, logn)])
+    return out
+
+
+def test_hoisted_keyswitch_bigint_bound(tiny):
+    """N2 hoisted key switch (reading R29): <KS_g(d), (1, s)> - sigma_g(d) sigma_g(s) is small mod Q_l,
+    with sigma_g taken by its evaluation-point definition and the CRT lift in Python big ints; and the
+    integers differ from the non-hoisted KS(sigma_g(d)) (O-12: ModUp does not commute with sigma_g)."""
+    prm, ev = tiny, ckks.Oracle(tiny)
+    keys = ev.keygen(4, [1, 3])
+    L = ckks.lib()
+    rng = np.random.default_rng(18)
+    for steps in (1, 3):
+        g = ckks.galois_elt(prm, steps)
+        for level in (prm.L, prm.L - 1):
+            nl = level + 1
+            d = np.stack([rng.integers(0, q, prm.N).astype(np.uint64) for q in prm.q[:nl]])
+            ks = np.zeros((2, nl, prm.N), dtype=np.uint64)
+            L.o_keyswitch_g(prm.cptr, ckks.P(np.ascontiguousarray(d)), nl, ckks.P(keys.gk[g]), g, ckks.P(ks))
+            Q = 1
+            for q in prm.q[:nl]:
+                Q *= q
+            err = np.zeros((nl, prm.N), dtype=np.uint64)
+            for i, q in enumerate(prm.q[:nl]):
+                s = [int(v) for v in keys.s_ntt[i]]
+                sg, dg = _ntt_sigma(keys.s_ntt[i], g, prm.logn), _ntt_sigma(d[i], g, prm.logn)
+                err[i] = [(int(ks[0, i, k]) + int(ks[1, i, k]) * s[k] - dg[k] * sg[k]) % q for k in range(prm.N)]
+            ec = ckks.ntt_limbs(err, prm, list(range(nl)), inverse=True)
+            for k in range(prm.N):
+                x = 0
+                for i in range(nl):
+                    Qi = Q // prm.q[i]
+                    x += int(ec[i, k]) * Qi * pow(Qi, -1, prm.q[i])
+                assert abs(_centered(x, Q)) < 2 ** 20
+            dsig = np.stack([np.array(_ntt_sigma(d[i], g, prm.logn), dtype=np.uint64) for i in range(nl)])
+            assert not np.array_equal(ks, ev.keyswitch(dsig, keys.gk[g]))
+
+
+def test_hoisted_rotations_against_slots(toy):
+    """N2: one ModUp shared by several rotation steps; every output decrypts to RotL(z, step)."""
+    ev = ckks.Oracle(toy)
+    steps = [1, 2, 4, -1, 0]
+    keys = ev.keygen(5, [s for s in steps if s])
+    z = synth.uniform_slots(31, toy.N // 2)
+    a = ev.encrypt(keys, z, toy.scale, 1)
+    outs = ev.rotate_hoisted_raw(keys, a, steps)
+    for s, r in zip(steps, outs):
+        assert r.level == a.level and r.scale == a.scale
+        assert np.abs(ev.decrypt(keys, r).real - np.roll(z, -s)).max() < 2 ** -10
+    assert np.array_equal(outs[-1].data, a.data)  # step 0: identity
+
+
 def test_automorph_is_sigma_g(tiny):
     """o_automorph == coefficient map X^k -> X^{gk} applied by definition (Python)."""
     prm, ev = tiny, ckks.Oracle(tiny)
