@@ -24,14 +24,16 @@ PARAM_SETS = {
     "tiny_deep": dict(logn=8, q=[("below", 60, 1), ("nearest", 40, 16)], p=[("below", 61, 2)],
                       alpha=3, log_scale=40),
     # configs[4]'s prime structure on a 2^12 ring: CPU-sized check of the (7,15,15) circuit numerics.
-    "argmax_small": dict(logn=12, q=[("nearest", 45, 30)], p=[("below", 60, 8)],
+    "argmax_small": dict(logn=12, q=[("nearest", 45, 30)], p=[("below", 46, 10)],
                          alpha=10, log_scale=45),
     # BASELINE configs[1]: NTT microbench, 24 x 60-bit primes, N = 2^16.
     "ntt": dict(logn=16, q=[("below", 60, 24)], p=[], alpha=8, log_scale=50),
     # BASELINE configs[2]/[3]: 24 x 60-bit q, dnum = 3 -> alpha = 8, 8 special 60-bit primes, scale 2^50.
     "ks": dict(logn=16, q=[("below", 60, 24)], p=[("below", 60, 8)], alpha=8, log_scale=50),
-    # BASELINE configs[4]: q_0..q_29 ~ 2^45 (reading R23), 8 x 60-bit special, dnum = 3 (alpha = 10), scale 2^45.
-    "argmax": dict(logn=16, q=[("nearest", 45, 30)], p=[("below", 60, 8)],
+    # BASELINE configs[4]: q_0..q_29 ~ 2^45 (reading R23), dnum = 3 (alpha = 10), scale 2^45, 10 special
+    # primes below 2^46 (reading R24: P ~ 2^460 > every 10-prime digit ~ 2^450, and every row of Q u P
+    # takes the exact-FP64 NTT).
+    "argmax": dict(logn=16, q=[("nearest", 45, 30)], p=[("below", 46, 10)],
                    alpha=10, log_scale=45),
 }
 
