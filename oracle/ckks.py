@@ -599,16 +599,26 @@ class Oracle:
         self._log("LINC", lv, target_level, target_scale, ",".join(Cs))
         return out
 
-    def mul_ct(self, keys, a, b, target_scale, target_level, lin=None):
-        """a (x) b [+ sum c x]: drop the inputs to target_level + 1 = l, tensor, optionally add the constant
-        products C x to (d0, d1) with C = rha(c Delta_c), Delta_c = (S_t q_l) / S_x (lin = (x, c) or a
-        list of such terms; R9, R13), relinearise, rescale.  Output scale := target_scale if given else
-        (S_a * S_b) / q_l."""
+    def mul_ct(self, keys, a, b, target_scale, target_level, lin=None, prod2=None):
+        """a (x) b [+ a2 (x) b2] [+ sum c x]: drop the inputs to target_level + 1 = l, tensor, optionally add
+        a second tensor a2 (x) b2 (prod2 = (a2, b2); reading R13b: two products summed share ONE
+        relinearisation and rescale; needs a planned target scale), optionally add the constant products
+        C x to (d0, d1) with C = rha(c Delta_c), Delta_c = (S_t q_l) / S_x (lin = (x, c) or a list of such
+        terms; R9, R13), relinearise, rescale.  Output scale := target_scale if given else (S_a * S_b) / q_l."""
         lv = target_level + 1
         a = self.drop(a, lv)
         b = self.drop(b, lv)
         s = (a.scale * b.scale) / float(self.prm.primes[lv]) if target_scale is None else target_scale
         d = self.tensor(a, b)
+        kind = "MULCT"
+        if prod2 is not None:
+            if target_scale is None:
+                raise ValueError("a summed product needs a planned target scale")
+            d2 = self.tensor(self.drop(prod2[0], lv), self.drop(prod2[1], lv))
+            dsum = np.zeros_like(d)
+            lib().o_add(self.prm.cptr, P(np.ascontiguousarray(d)), P(np.ascontiguousarray(d2)), lv + 1, 3, P(dsum))
+            d = dsum
+            kind = "MULCT2"
         extra = ""
         if lin is not None:
             terms = lin if isinstance(lin, list) else [lin]
@@ -626,7 +636,7 @@ class Oracle:
                 Cs.append(str(C))
             extra = ",".join(Cs)
         out = self.rescale(self.mul_relin(keys, a, b, d), s)
-        self._log("MULCT", lv, target_level, s, extra)
+        self._log(kind, lv, target_level, s, extra)
         return out
 
     def mul_mask(self, x, mask_slots, target_scale):
@@ -709,12 +719,18 @@ class Mirror:
         self._log("LINC", lv, target_level, target_scale, ",".join(Cs))
         return MirrorCt(v, target_level, target_scale)
 
-    def mul_ct(self, keys, a, b, target_scale, target_level, lin=None):
+    def mul_ct(self, keys, a, b, target_scale, target_level, lin=None, prod2=None):
         lv = target_level + 1
         if a.level < lv or b.level < lv:
             raise ValueError("level")
         s = (a.scale * b.scale) / float(self.prm.primes[lv]) if target_scale is None else target_scale
         v = a.v * b.v
+        kind = "MULCT"
+        if prod2 is not None:
+            if target_scale is None or prod2[0].level < lv or prod2[1].level < lv:
+                raise ValueError("prod2")
+            v = v + prod2[0].v * prod2[1].v
+            kind = "MULCT2"
         extra = ""
         if lin is not None:
             terms = lin if isinstance(lin, list) else [lin]
@@ -725,7 +741,7 @@ class Mirror:
                 Cs.append(str(round_half_away(c * ((s * float(self.prm.primes[lv])) / x.scale))))
                 v = v + c * x.v
             extra = ",".join(Cs)
-        self._log("MULCT", lv, target_level, s, extra)
+        self._log(kind, lv, target_level, s, extra)
         return MirrorCt(v, target_level, s)
 
     def mul_mask(self, x, mask_slots, target_scale):

@@ -50,11 +50,11 @@ def eval_odd_poly(ev, keys, x, coeffs, target_scale):
         return ev.mul_ct(keys, inner, x2, S, L, lin=(x, coeffs[4 * i + 1]))
 
     def B(i, S, L):
-        # B_i = A_{2i} + x^4 A_{2i+1}  at (S, L)
+        # B_i = x^4 A_{2i+1} + A_{2i}  at (S, L); A_{2i} = (c x) x^2 + c' x is a second product summed
+        # with the first: both tensors share ONE relinearisation and rescale (reading R13b)
         hi = A(2 * i + 1, (S * q(L + 1)) / x4.scale, L + 1)
-        prod = ev.mul_ct(keys, hi, x4, S, L)
-        lo = A(2 * i, S, L)
-        return ev.add(prod, lo)
+        inner = ev.mul_const(x, coeffs[8 * i + 3], (S * q(L + 1)) / x2.scale, L + 1)
+        return ev.mul_ct(keys, hi, x4, S, L, lin=(x, coeffs[8 * i + 1]), prod2=(inner, x2))
 
     if deg == 3:
         return A(0, target_scale, l - 2)
@@ -69,10 +69,9 @@ def eval_odd_poly(ev, keys, x, coeffs, target_scale):
     S_b1 = (T * q(l - 4)) / x8.scale
     q3 = ev.lincomb([(x, c[13]), (x3, c[15])], (S_b1 * q(l - 3)) / x4.scale, l - 3)
     b1 = ev.mul_ct(keys, q3, x4, S_b1, l - 4, lin=[(x, c[9]), (x3, c[11])])
-    hi = ev.mul_ct(keys, b1, x8, T, Lo)
     q1 = ev.lincomb([(x, c[5]), (x3, c[7])], (T * q(l - 4)) / x4.scale, l - 4)
-    b0 = ev.mul_ct(keys, q1, x4, T, Lo, lin=[(x, c[1]), (x3, c[3])])
-    return ev.add(b0, hi)
+    # q_1 x^4 + q_0 + b_1 x^8: the two products share one relinearisation and rescale (reading R13b)
+    return ev.mul_ct(keys, q1, x4, T, Lo, lin=[(x, c[1]), (x3, c[3])], prod2=(b1, x8))
 
 
 def sign(ev, keys, x, stages, target_scale):

@@ -152,14 +152,15 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
         // epilogue: 8 int32 byte-plane sums per target -> value < 2^80 -> reduced with an FP64 quotient
         // V = lo + hi 2^32 with lo, hi < 2^48; k = floor(V / t) from doubles is off by at most one, so
         // r = V - k t (exact, mod 2^64) lies in [-t, 2t) and two corrections make it canonical.
-        auto reduce = [&](int t, u64 q, double qinv) -> u64 {
-            uint32_t g[8];
+        auto tld = [&](int t, uint32_t (&g)[8]) {
             const uint32_t addr = tmem + ((uint32_t)(32 * lq) << 16) + (uint32_t)(8 * t);
             asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
                          : "=r"(g[0]), "=r"(g[1]), "=r"(g[2]), "=r"(g[3]), "=r"(g[4]), "=r"(g[5]), "=r"(g[6]),
                            "=r"(g[7])
                          : "r"(addr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+        };
+        auto tld_wait = [] { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); };
+        auto reduce_g = [&](const uint32_t (&g)[8], u64 q, double qinv) -> u64 {
             const u64 lo = (u64)g[0] + ((u64)g[1] << 8) + ((u64)g[2] << 16) + ((u64)g[3] << 24);
             const u64 hi = (u64)g[4] + ((u64)g[5] << 8) + ((u64)g[6] << 16) + ((u64)g[7] << 24);
             const double two52 = 4503599627370496.0;
@@ -178,16 +179,33 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
         if (a.rr) {
             // fused ModDown + rescale prelude (target 0 = q_l): Y_l = (xc - T_l) P^{-1}, r = [Y_l + floor(q_l/2)]
             const u64 ql = sq[0];
-            const u64 tl = reduce(0, ql, sqinv[0]);
+            uint32_t g[8];
+            tld(0, g);
+            tld_wait();
+            const u64 tl = reduce_g(g, ql, sqinv[0]);
             const u64 xc = src[(long)(-1) * N + k0 + m];
             r = csub(mul_shoup(submod(xc, tl, ql), a.pinv_l, a.pinv_l_sh, ql) + (ql >> 1), ql);
             t0 = 1;
         }
-        for (int t = t0 + tpar; t < nt; t += 4) {
-            const u64 q = sq[t];
-            u64 z = reduce(t, q, sqinv[t]);
-            if (a.rr) z = addmod(z, csub(mul_shoup(r, spm[t], spmsh[t], q), q), q);
-            dst[soff[t] + k0 + m] = z;
+        // two targets per TMEM wait: both loads are in flight together
+        for (int t = t0 + tpar; t < nt; t += 8) {
+            const int t2 = t + 4;
+            uint32_t g[8], h[8];
+            tld(t, g);
+            if (t2 < nt) tld(t2, h);
+            tld_wait();
+            {
+                const u64 q = sq[t];
+                u64 z = reduce_g(g, q, sqinv[t]);
+                if (a.rr) z = addmod(z, csub(mul_shoup(r, spm[t], spmsh[t], q), q), q);
+                dst[soff[t] + k0 + m] = z;
+            }
+            if (t2 < nt) {
+                const u64 q = sq[t2];
+                u64 z = reduce_g(h, q, sqinv[t2]);
+                if (a.rr) z = addmod(z, csub(mul_shoup(r, spm[t2], spmsh[t2], q), q), q);
+                dst[soff[t2] + k0 + m] = z;
+            }
         }
         asm volatile("tcgen05.fence::before_thread_sync;\n");
         __syncthreads();

@@ -193,10 +193,12 @@ void ev_rescale(Ctx &c, const CtView &in, const CtView &out);
 void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, const u64 *add,
                   long add_stride, int add_polys, u64 *out, long out_stride);
 void ev_mul_relin(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const CtView &out);
-// a (x) b [+ C x] relinearised and rescaled by q_l in one pass (bit-identical to ev_mul_relin then
-// ev_rescale); out at level a.level - 1.  lin_x: optional linear term (nullptr: none), C its constant
+// a (x) b [+ a2 (x) b2] [+ C x] relinearised and rescaled by q_l in one pass (bit-identical to ev_mul_relin
+// then ev_rescale); out at level a.level - 1.  lin_x: optional linear term (nullptr: none), C its constant;
+// a2, b2: optional second product summed into the tensor before the relinearisation (R13b)
 void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const CtView *lin_x, i64 C,
-                          const CtView &out, const CtView *lin_x2 = nullptr, i64 C2 = 0);
+                          const CtView &out, const CtView *lin_x2 = nullptr, i64 C2 = 0, const CtView *a2 = nullptr,
+                          const CtView *b2 = nullptr);
 void ev_lincomb(Ctx &c, const CtView &a, i64 C1, const CtView *b, i64 C2, const CtView &out);
 void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView &out);
 void ev_rotate_hoisted(Ctx &c, const Keys &k, const CtView &in, const int *steps, int n_steps, const CtView *outs);

@@ -148,6 +148,11 @@ static void ks_modup(Ctx &c, const u64 *d, long d_stride, int n, int level, DevB
         f1.in_mode = 3;  // d2 = a1 b1
         f1.src = CRows{ten->a.p + ten->a.ps, 2 * ten->a.cs, ten->a.cs};
         f1.src2 = CRows{ten->b.p + ten->b.ps, 2 * ten->b.cs, ten->b.cs};
+        if (ten->a2.p) {  // d2 = a1 b1 + a2_1 b2_1 (R13b)
+            f1.in_mode = 4;
+            f1.src3 = CRows{ten->a2.p + ten->a2.ps, 2 * ten->a2.cs, ten->a2.cs};
+            f1.src4 = CRows{ten->b2.p + ten->b2.ps, 2 * ten->b2.cs, ten->b2.cs};
+        }
     } else {
         f1.in_mode = 1;
         f1.src = CRows{d, 2 * d_stride, d_stride};
@@ -273,7 +278,7 @@ static void ks_moddown(Ctx &c, DevBuf &acc, int n, int level, const u64 *add, lo
 // corrections are computed in the coefficient domain (k_rr_conv) and removed by ONE forward NTT whose
 // epilogue forms (x_i - NTT(T_i)) (P q_l)^{-1}.  This saves the rescale's own INTT/NTT round trip.
 void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const CtView *lin_x, i64 C,
-                          const CtView &out, const CtView *lin_x2, i64 C2) {
+                          const CtView &out, const CtView *lin_x2, i64 C2, const CtView *a2, const CtView *b2) {
     const int l = a.level, nl = l + 1;
     if (l < 1) throw SecpeError{-2, "mul_relin_rescale: no level left"};
     if (b.level != l || out.level != l - 1) throw SecpeError{-1, "mul_relin_rescale: levels"};
@@ -292,6 +297,12 @@ void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &
     if (lin_x2) {
         ten.x2 = crows_of(*lin_x2);
         ten.C2 = limb_const(c, C2, nl);
+    }
+    if (a2) {
+        if (!b2 || a2->level < l || b2->level < l || a2->n != n || b2->n != n)
+            throw SecpeError{-1, "mul_relin_rescale: second product"};
+        ten.a2 = crows_of(*a2);
+        ten.b2 = crows_of(*b2);
     }
     const size_t pa = c.prof_begin(1);
     DevBuf acc;
@@ -336,7 +347,7 @@ void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &
     c.cnt.keyswitch += n;
     c.cnt.rescale += n;
     c.cnt.mulct += n;
-    c.prof_end(pa, 1, 8.0 * N * ((double)n * (3 * nl + 2 * l) + 2.0 * bt * ne), n);
+    c.prof_end(pa, 1, 8.0 * N * ((double)n * ((a2 ? 5 : 3) * nl + 2 * l) + 2.0 * bt * ne), n);
 }
 
 void ev_mul_relin(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const CtView &out) {

@@ -26,6 +26,7 @@ struct LimbConst {
 // Fusions (all optional; the default is a plain in-place transform):
 //   in_mode  1 (inverse): the first pass reads polynomial P, limb i from src (copy fused in)
 //   in_mode  3 (inverse): the first pass reads src[P] * src2[P] mod q_i (tensor term fused in)
+//   in_mode  4 (inverse): ... src[P] * src2[P] + src3[P] * src4[P] mod q_i (two summed tensors, R13b)
 //   in_mode  2 (forward): rescale broadcast (R12): the input of limb i is
 //            [floor(q_l/2)]_{q_i} - [[x + floor(q_l/2)]_{q_l}]_{q_i}, x = src row of polynomial P
 //            (one coefficient-form limb, prime lp); half[i] = [floor(q_l/2)]_{q_i}
@@ -37,6 +38,7 @@ struct NttFusion {
     int in_mode = 0, out_mode = 0;
     CRows src{nullptr, 0, 0};
     CRows src2{nullptr, 0, 0};  // in_mode 3 (inverse): the first pass reads src[P] * src2[P] mod q (tensor d2)
+    CRows src3{nullptr, 0, 0}, src4{nullptr, 0, 0};  // in_mode 4: src*src2 + src3*src4 (two summed tensors' d2)
     int lp = 0;
     const u64 *half = nullptr;
     CRows e1{nullptr, 0, 0}, e2{nullptr, 0, 0};
@@ -93,6 +95,7 @@ void k_modup(const Tab &tab, int logn, const u64 *dc, long dc_ct_stride, u64 *ex
 // (the optional linear term x, C of R13).
 struct TensorSrc {
     CRows a, b, x;  // ciphertext views (c0 at p + ct * cs, c1 at + ps); x.p == nullptr: no linear term
+    CRows a2, b2;   // optional second product a2 (x) b2 summed before the relinearisation (R13b); a2.p == nullptr: none
     LimbConst C;    // per-limb residues of the linear term's integer constant (Shoup companions)
     CRows x2;       // optional second linear term C2 x2 (x2.p == nullptr: none)
     LimbConst C2;

@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(TPB) modup_kernel(Tab tab, int logn, const u64
 // (beta <= 4); larger dnum uses the scalar ks_inner_kernel below.
 template <int MAXB>
 struct KsIn {
-    ulonglong2 x[MAXB], d0, d1, a0, a1, b0, b1, x0, x1, y0, y1;
+    ulonglong2 x[MAXB], d0, d1, a0, a1, b0, b1, x0, x1, y0, y1, u0, u1, w0, w1;  // u, w: second product
 };
 // Hoisted rotation (R29): the key inner product reads sigma_g(x) instead of x.  In the NTT domain
 // sigma_g is the permutation NTT(sigma_g a)[i] = NTT(a)[pi(i)], 2 brv(pi(i)) + 1 = g (2 brv(i) + 1) mod 2N;
@@ -141,6 +141,15 @@ __device__ __forceinline__ void ks_load(KsIn<MAXB> &in, int c, const u64 *__rest
         }
     }
 }
+// second product of the tensor (R13b): loaded where it is consumed (not prefetched: register budget)
+template <int MAXB>
+__device__ __forceinline__ void ks_load_p2(KsIn<MAXB> &in, int c, int e, long N, long k, const TensorSrc &ten) {
+    const long o = e * N + k;
+    in.u0 = ldv2(ten.a2.p + c * ten.a2.cs + o);
+    in.u1 = ldv2(ten.a2.p + c * ten.a2.cs + ten.a2.ps + o);
+    in.w0 = ldv2(ten.b2.p + c * ten.b2.cs + o);
+    in.w1 = ldv2(ten.b2.p + c * ten.b2.cs + ten.b2.ps + o);
+}
 
 // Exact-FP64 tensor for primes < 2^46 (the configs[4] chain): operands < 2^46 are exact doubles;
 // w y mod q = fma(y, w, -k q) with k = rint(y w / q) (the ntt.cu FpA product), |r| <= 0.75 q, so the
@@ -167,12 +176,20 @@ __device__ __forceinline__ u64 canon(double v, double qd, double qinv) {
 
 __device__ __forceinline__ void tensor1_fp(u64 a0, u64 a1, u64 b0, u64 b1, bool lin, u64 x0, u64 x1, u64 c,
                                            bool lin2, u64 y0, u64 y1, u64 c2, double qd, double qinv, u64 &d0,
-                                           u64 &d1, u64 &d2) {
+                                           u64 &d1, u64 &d2, bool p2 = false, u64 u0 = 0, u64 u1 = 0, u64 w0 = 0,
+                                           u64 w1 = 0) {
     const double A0 = fpt::d(a0), A1 = fpt::d(a1), B0 = fpt::d(b0), B1 = fpt::d(b1);
     const double B0q = __dmul_rn(B0, qinv), B1q = __dmul_rn(B1, qinv);
     double e0 = fpt::mm(A0, B0, B0q, qd);
     double e1 = __dadd_rn(fpt::mm(A0, B1, B1q, qd), fpt::mm(A1, B0, B0q, qd));
-    const double e2 = fpt::mm(A1, B1, B1q, qd);
+    double e2 = fpt::mm(A1, B1, B1q, qd);
+    if (p2) {  // second product (R13b): |e| stays below 4 * 0.75 q + linear terms < 2^51
+        const double U0 = fpt::d(u0), U1 = fpt::d(u1), W0 = fpt::d(w0), W1 = fpt::d(w1);
+        const double W0q = __dmul_rn(W0, qinv), W1q = __dmul_rn(W1, qinv);
+        e0 = __dadd_rn(e0, fpt::mm(U0, W0, W0q, qd));
+        e1 = __dadd_rn(e1, __dadd_rn(fpt::mm(U0, W1, W1q, qd), fpt::mm(U1, W0, W0q, qd)));
+        e2 = __dadd_rn(e2, fpt::mm(U1, W1, W1q, qd));
+    }
     if (lin) {
         const double C = fpt::d(c), Cq = __dmul_rn(C, qinv);
         e0 = __dadd_rn(e0, fpt::mm(fpt::d(x0), C, Cq, qd));
@@ -191,12 +208,20 @@ __device__ __forceinline__ void tensor1_fp(u64 a0, u64 a1, u64 b0, u64 b1, bool 
 // one coefficient of the tensor: (d0, d1, d2) mod q, with the optional linear term C x
 __device__ __forceinline__ void tensor1(u64 a0, u64 a1, u64 b0, u64 b1, bool lin, u64 x0, u64 x1, u64 c, u64 csh,
                                         bool lin2, u64 y0, u64 y1, u64 c2, u64 c2sh, u64 q, u64 r0, u64 r1, u64 &d0,
-                                        u64 &d1, u64 &d2) {
-    d0 = mulmod(a0, b0, q, r0, r1);
+                                        u64 &d1, u64 &d2, bool p2 = false, u64 u0 = 0, u64 u1 = 0, u64 w0 = 0,
+                                        u64 w1 = 0) {
+    U128 t0 = mul_wide(a0, b0), t2 = mul_wide(a1, b1);
     U128 t = mul_wide(a0, b1);
     mac_wide(t, a1, b0);
+    if (p2) {  // second product (R13b); four 120-bit products stay below the Barrett bound 2^125
+        mac_wide(t0, u0, w0);
+        mac_wide(t2, u1, w1);
+        mac_wide(t, u0, w1);
+        mac_wide(t, u1, w0);
+    }
+    d0 = barrett128(t0, q, r0, r1);
     d1 = barrett128(t, q, r0, r1);
-    d2 = mulmod(a1, b1, q, r0, r1);
+    d2 = barrett128(t2, q, r0, r1);
     if (lin) {
         d0 = addmod(d0, mul_shoup(x0, c, csh, q), q);
         d1 = addmod(d1, mul_shoup(x1, c, csh, q), q);
@@ -232,7 +257,7 @@ __global__ void __launch_bounds__(TPB, TEN ? 2 : 3) ks_inner_vec_kernel(Tab tab,
     const int jd = e < nl ? e / alpha : -1;  // digit containing e (Q limbs only)
     const bool qrow = TEN && e < nl;         // relinearise-and-rescale: x_b = acc_b + [P]_{q_e} d_b on Q limbs
     const u64 pm = qrow ? pmod[e] : 0;
-    const bool lin = TEN && ten.x.p, lin2 = TEN && ten.x2.p;
+    const bool lin = TEN && ten.x.p, lin2 = TEN && ten.x2.p, p2 = TEN && ten.a2.p;
     const u64 cc = lin && e < nl ? ten.C.c[e] : 0, ccsh = lin && e < nl ? ten.C.csh[e] : 0;
     const u64 c2 = lin2 && e < nl ? ten.C2.c[e] : 0, c2sh = lin2 && e < nl ? ten.C2.csh[e] : 0;
     const double qd = TEN ? tab.qd[pr] : 0.0, qinv = TEN ? tab.qinv[pr] : 0.0;
@@ -245,16 +270,17 @@ __global__ void __launch_bounds__(TPB, TEN ? 2 : 3) ks_inner_vec_kernel(Tab tab,
             ks_load<MAXB, TEN>(nxt, c + 1, d, ds, ext, exts, e, jd, ne, nl, beta, N, k, ten, kx, swap);
         if (qrow) {
             u64 e0, e1, e2, f0, f1, f2;
+            if (p2) ks_load_p2<MAXB>(cur, c, e, N, k, ten);
             if (q < (1ULL << 46)) {
                 tensor1_fp(cur.a0.x, cur.a1.x, cur.b0.x, cur.b1.x, lin, cur.x0.x, cur.x1.x, cc, lin2, cur.y0.x,
-                           cur.y1.x, c2, qd, qinv, e0, e1, e2);
+                           cur.y1.x, c2, qd, qinv, e0, e1, e2, p2, cur.u0.x, cur.u1.x, cur.w0.x, cur.w1.x);
                 tensor1_fp(cur.a0.y, cur.a1.y, cur.b0.y, cur.b1.y, lin, cur.x0.y, cur.x1.y, cc, lin2, cur.y0.y,
-                           cur.y1.y, c2, qd, qinv, f0, f1, f2);
+                           cur.y1.y, c2, qd, qinv, f0, f1, f2, p2, cur.u0.y, cur.u1.y, cur.w0.y, cur.w1.y);
             } else {
                 tensor1(cur.a0.x, cur.a1.x, cur.b0.x, cur.b1.x, lin, cur.x0.x, cur.x1.x, cc, ccsh, lin2, cur.y0.x,
-                        cur.y1.x, c2, c2sh, q, r0, r1, e0, e1, e2);
+                        cur.y1.x, c2, c2sh, q, r0, r1, e0, e1, e2, p2, cur.u0.x, cur.u1.x, cur.w0.x, cur.w1.x);
                 tensor1(cur.a0.y, cur.a1.y, cur.b0.y, cur.b1.y, lin, cur.x0.y, cur.x1.y, cc, ccsh, lin2, cur.y0.y,
-                        cur.y1.y, c2, c2sh, q, r0, r1, f0, f1, f2);
+                        cur.y1.y, c2, c2sh, q, r0, r1, f0, f1, f2, p2, cur.u0.y, cur.u1.y, cur.w0.y, cur.w1.y);
             }
 #pragma unroll
             for (int j = 0; j < MAXB; j++)
@@ -316,7 +342,9 @@ __global__ void ks_inner_kernel(Tab tab, int logn, const u64 *__restrict__ d, lo
                     ten.b.p[c * ten.b.cs + ten.b.ps + o], lin, lin ? ten.x.p[c * ten.x.cs + o] : 0,
                     lin ? ten.x.p[c * ten.x.cs + ten.x.ps + o] : 0, lin ? ten.C.c[e] : 0, lin ? ten.C.csh[e] : 0,
                     lin2, lin2 ? ten.x2.p[c * ten.x2.cs + o] : 0, lin2 ? ten.x2.p[c * ten.x2.cs + ten.x2.ps + o] : 0,
-                    lin2 ? ten.C2.c[e] : 0, lin2 ? ten.C2.csh[e] : 0, q, r0, r1, d0, d1, d2);
+                    lin2 ? ten.C2.c[e] : 0, lin2 ? ten.C2.csh[e] : 0, q, r0, r1, d0, d1, d2, ten.a2.p != nullptr,
+                    ten.a2.p ? ten.a2.p[c * ten.a2.cs + o] : 0, ten.a2.p ? ten.a2.p[c * ten.a2.cs + ten.a2.ps + o] : 0,
+                    ten.a2.p ? ten.b2.p[c * ten.b2.cs + o] : 0, ten.a2.p ? ten.b2.p[c * ten.b2.cs + ten.b2.ps + o] : 0);
         }
         for (int j = 0; j < beta; j++) {
             const u64 x = (j == jd) ? (qrow ? d2 : d[c * ds + e * N + kx]) : ext[c * exts + ((long)j * ne + e) * N + kx];

@@ -258,7 +258,7 @@ __device__ __forceinline__ void do_round(u64 (&v)[NV], int tau, int g, const ulo
 }
 
 // Fused prologue / epilogue modes (NttFusion in kernels.h)
-enum { IN_PLAIN = 0, IN_SRC = 1, IN_BCAST = 2, IN_MUL = 3 };
+enum { IN_PLAIN = 0, IN_SRC = 1, IN_BCAST = 2, IN_MUL = 3, IN_MUL2 = 4 };
 enum { OUT_PLAIN = 0, OUT_RESCALE = 1, OUT_MODDOWN = 2 };
 
 struct PassArgs {
@@ -393,12 +393,17 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, u64 *sm, int poly
 #pragma unroll
         for (int k = 0; k < NV; k++) v[k] = src[held<LO0>(tau, k)];  // intermediate representation
     } else {
-        const u64 *sp = (IO == IN_SRC || IO == IN_MUL) ? a.f.src.p + poly_off(a.f.src.cs, a.f.src.ps, poly) + boff
-                                                       : blk;
+        const u64 *sp = (IO == IN_SRC || IO == IN_MUL || IO == IN_MUL2)
+                            ? a.f.src.p + poly_off(a.f.src.cs, a.f.src.ps, poly) + boff
+                            : blk;
         const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(sp);
-        const ulonglong2 *src2 = nullptr;
-        if (IO == IN_MUL)
+        const ulonglong2 *src2 = nullptr, *src3 = nullptr, *src4 = nullptr;
+        if (IO == IN_MUL || IO == IN_MUL2)
             src2 = reinterpret_cast<const ulonglong2 *>(a.f.src2.p + poly_off(a.f.src2.cs, a.f.src2.ps, poly) + boff);
+        if (IO == IN_MUL2) {
+            src3 = reinterpret_cast<const ulonglong2 *>(a.f.src3.p + poly_off(a.f.src3.cs, a.f.src3.ps, poly) + boff);
+            src4 = reinterpret_cast<const ulonglong2 *>(a.f.src4.p + poly_off(a.f.src4.cs, a.f.src4.ps, poly) + boff);
+        }
         const u64 br0 = a.tab.br0[prime], br1 = a.tab.br1[prime];
 #pragma unroll 4
         for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
@@ -407,6 +412,13 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, u64 *sm, int poly
                 const ulonglong2 y = src2[i];
                 x.x = mulmod(x.x, y.x, q, br0, br1);
                 x.y = mulmod(x.y, y.y, q, br0, br1);
+            } else if (IO == IN_MUL2) {
+                const ulonglong2 y = src2[i], z = src3[i], w = src4[i];
+                U128 t0 = mul_wide(x.x, y.x), t1 = mul_wide(x.y, y.y);
+                mac_wide(t0, z.x, w.x);
+                mac_wide(t1, z.y, w.y);
+                x.x = barrett128(t0, q, br0, br1);
+                x.y = barrett128(t1, q, br0, br1);
             }
             const int e = 2 * i, gg = e / G, r = e % G;
             sm[gg * PITCH + padr(r)] = A::in(x.x, P);
@@ -656,12 +668,17 @@ __global__ void __launch_bounds__(ClusterCfg<LOGN>::THREADS, MinBC<A>::v) ntt_cl
         constexpr int RLO0 = RB2::lo(0), RLO1 = RB2::lo(1);
         // ---- rows: GS stages LOGN-1..S1 on this CTA's RR rows (prologue fusions) ----
         const long boff = limb * N + (long)rank * RR * G2;
-        const u64 *sp = (IN == IN_SRC || IN == IN_MUL) ? a.f.src.p + poly_off(a.f.src.cs, a.f.src.ps, poly) + boff
-                                                       : limb_base + (long)rank * RR * G2;
+        const u64 *sp = (IN == IN_SRC || IN == IN_MUL || IN == IN_MUL2)
+                            ? a.f.src.p + poly_off(a.f.src.cs, a.f.src.ps, poly) + boff
+                            : limb_base + (long)rank * RR * G2;
         const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(sp);
-        const ulonglong2 *src2 = nullptr;
-        if (IN == IN_MUL)
+        const ulonglong2 *src2 = nullptr, *src3 = nullptr, *src4 = nullptr;
+        if (IN == IN_MUL || IN == IN_MUL2)
             src2 = reinterpret_cast<const ulonglong2 *>(a.f.src2.p + poly_off(a.f.src2.cs, a.f.src2.ps, poly) + boff);
+        if (IN == IN_MUL2) {
+            src3 = reinterpret_cast<const ulonglong2 *>(a.f.src3.p + poly_off(a.f.src3.cs, a.f.src3.ps, poly) + boff);
+            src4 = reinterpret_cast<const ulonglong2 *>(a.f.src4.p + poly_off(a.f.src4.cs, a.f.src4.ps, poly) + boff);
+        }
         const u64 br0 = a.tab.br0[prime], br1 = a.tab.br1[prime];
 #pragma unroll 4
         for (int i = threadIdx.x; i < RR * G2 / 2; i += CF::THREADS) {
@@ -670,6 +687,13 @@ __global__ void __launch_bounds__(ClusterCfg<LOGN>::THREADS, MinBC<A>::v) ntt_cl
                 const ulonglong2 y = src2[i];
                 x.x = mulmod(x.x, y.x, q, br0, br1);
                 x.y = mulmod(x.y, y.y, q, br0, br1);
+            } else if (IN == IN_MUL2) {
+                const ulonglong2 y = src2[i], z = src3[i], w = src4[i];
+                U128 t0 = mul_wide(x.x, y.x), t1 = mul_wide(x.y, y.y);
+                mac_wide(t0, z.x, w.x);
+                mac_wide(t1, z.y, w.y);
+                x.x = barrett128(t0, q, br0, br1);
+                x.y = barrett128(t1, q, br0, br1);
             }
             const int e = 2 * i, gg = e / G2, r = e % G2;
             xs[gg * PITCH + padr(r)] = A::in(x.x, P);
@@ -891,6 +915,8 @@ void run_chunk(const PassArgs &a, int rows, bool inverse, cudaStream_t st) {
                     launch_cluster_or_split<LOGN, true, IN_SRC, OUT_PLAIN>(a, rows, st);
                 else if (f.in_mode == IN_MUL)
                     launch_cluster_or_split<LOGN, true, IN_MUL, OUT_PLAIN>(a, rows, st);
+                else if (f.in_mode == IN_MUL2)
+                    launch_cluster_or_split<LOGN, true, IN_MUL2, OUT_PLAIN>(a, rows, st);
                 else
                     launch_cluster_or_split<LOGN, true, IN_PLAIN, OUT_PLAIN>(a, rows, st);
             }
@@ -915,6 +941,8 @@ void run_chunk(const PassArgs &a, int rows, bool inverse, cudaStream_t st) {
             launch_contig<LOGN, true, IN_SRC>(a, rows, st);
         else if (f.in_mode == IN_MUL)
             launch_contig<LOGN, true, IN_MUL>(a, rows, st);
+        else if (f.in_mode == IN_MUL2)
+            launch_contig<LOGN, true, IN_MUL2>(a, rows, st);
         else
             launch_contig<LOGN, true, IN_PLAIN>(a, rows, st);
         LAUNCH_CHECK();
@@ -948,7 +976,8 @@ void ntt_forward(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm
 void ntt_inverse(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
                  const NttFusion &f) {
     if (n_polys <= 0 || lm.nl <= 0) return;
-    if ((f.in_mode != IN_PLAIN && f.in_mode != IN_SRC && f.in_mode != IN_MUL) || f.out_mode != OUT_PLAIN)
+    if ((f.in_mode != IN_PLAIN && f.in_mode != IN_SRC && f.in_mode != IN_MUL && f.in_mode != IN_MUL2) ||
+        f.out_mode != OUT_PLAIN)
         throw SecpeError{-1, "ntt_inverse: bad fusion mode"};
     dispatch(logn, PassArgs{data, lm, tab, f, 0, lm.nl, 0}, n_polys, true, st);
 }

@@ -92,11 +92,15 @@ struct Ev {
     }
     // a (x) b [+ sum c x] relinearised and rescaled in one pass; St = NAN: natural scale (S_a S_b) / q_l.
     // Up to two linear terms join the product before its rescale (R13).
-    Val mul_ct(const Val &a, const Val &b, double St, int Lt, const Lin &lin = {}) {
+    // a2, b2 (optional): a second product summed into the tensor, one relinearisation for both (R13b)
+    Val mul_ct(const Val &a, const Val &b, double St, int Lt, const Lin &lin = {}, const Val *a2 = nullptr,
+               const Val *b2 = nullptr) {
         const int lv = Lt + 1;
         if (lv < 1) throw SecpeError{-2, "mul_ct: no level left"};
         if (lin.size() > 2) throw SecpeError{-1, "mul_ct: at most two linear terms"};
+        if (a2 && std::isnan(St)) throw SecpeError{-1, "mul_ct: a summed product needs a planned scale"};
         Val ad = drop(a, lv), bd = drop(b, lv);
+        Val a2d = a2 ? drop(*a2, lv) : Val{}, b2d = a2 ? drop(*b2, lv) : Val{};
         const double s = std::isnan(St) ? (a.scale() * b.scale()) / q(lv) : St;
         Val out = fresh(Lt, s);
         std::vector<Val> xs;
@@ -106,8 +110,9 @@ struct Ev {
             Cs.push_back(lin_const(t.second, s, lv, t.first->scale()));
         }
         ev_mul_relin_rescale(c, k, ad.v, bd.v, xs.size() > 0 ? &xs[0].v : nullptr, xs.size() > 0 ? Cs[0] : 0, out.v,
-                             xs.size() > 1 ? &xs[1].v : nullptr, xs.size() > 1 ? Cs[1] : 0);
-        c.log("MULCT", lv, Lt, s, join(Cs));
+                             xs.size() > 1 ? &xs[1].v : nullptr, xs.size() > 1 ? Cs[1] : 0, a2 ? &a2d.v : nullptr,
+                             a2 ? &b2d.v : nullptr);
+        c.log(a2 ? "MULCT2" : "MULCT", lv, Lt, s, join(Cs));
         return out;
     }
     // sum c_i x_i (one or two terms) at (St, Lt) with a single rescale (R13)
@@ -184,10 +189,11 @@ struct Ev {
             return mul_ct(inner, x2, S, L, {{&x, cf[4 * i + 1]}});
         };
         auto B = [&](int i, double S, int L) {
+            // x^4 A_{2i+1} + A_{2i}: A_{2i} = (c x) x^2 + c' x is a second product summed with the first,
+            // one relinearisation and rescale for both (R13b)
             Val hi = A(2 * i + 1, (S * q(L + 1)) / x4.scale(), L + 1);
-            Val prod = mul_ct(hi, x4, S, L);
-            Val lo = A(2 * i, S, L);
-            return add(prod, lo);
+            Val inner = mul_const(x, cf[8 * i + 3], (S * q(L + 1)) / x2.scale(), L + 1);
+            return mul_ct(hi, x4, S, L, {{&x, cf[8 * i + 1]}}, &inner, &x2);
         };
         if (deg == 3) return A(0, T, l - 2);
         if (deg == 7) return B(0, T, l - 3);
@@ -198,10 +204,9 @@ struct Ev {
         const double Sb1 = (T * q(l - 4)) / x8.scale();
         Val q3 = lincomb({{&x, cf[13]}, {&x3, cf[15]}}, (Sb1 * q(l - 3)) / x4.scale(), l - 3);
         Val b1 = mul_ct(q3, x4, Sb1, l - 4, {{&x, cf[9]}, {&x3, cf[11]}});
-        Val hi = mul_ct(b1, x8, T, Lo);
         Val q1 = lincomb({{&x, cf[5]}, {&x3, cf[7]}}, (T * q(l - 4)) / x4.scale(), l - 4);
-        Val b0 = mul_ct(q1, x4, T, Lo, {{&x, cf[1]}, {&x3, cf[3]}});
-        return add(b0, hi);
+        // q_1 x^4 + q_0 + b_1 x^8: the two products share one relinearisation and rescale (R13b)
+        return mul_ct(q1, x4, T, Lo, {{&x, cf[1]}, {&x3, cf[3]}}, &b1, &x8);
     }
     Val sign(Val x, const SignCfg &cfg, double T) {
         for (size_t i = 0; i < cfg.stages.size(); i++) {

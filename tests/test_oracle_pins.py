@@ -461,13 +461,17 @@ def test_sign_plan_equals_horner(sname):
     # depth law (ceil(log2(d+1)) for a BSGS plan), except degree 15 whose
     # Paterson-Stockmeyer plan (R13) trades one level for three fewer ct x ct products
     assert plan.sign_depth(st) == sum(math.ceil(math.log2(len(c))) + (len(c) == 16) for c in st)
-    nprod = {4: 2, 8: 5, 16: 7}  # ct x ct products per stage: deg 3, 7 (BSGS), 15 (PS)
-    assert sum(1 for l in mir.log if l.startswith("MULCT ")) == sum(nprod[len(c)] for c in st)
+    nprod = {4: 2, 8: 5, 16: 7}  # ct x ct products (tensors) per stage: deg 3, 7 (BSGS), 15 (PS)
+    nks = {4: 2, 8: 4, 16: 6}    # relinearisations: two summed products share one (reading R13b)
+    single = sum(1 for l in mir.log if l.startswith("MULCT "))
+    summed = sum(1 for l in mir.log if l.startswith("MULCT2 "))
+    assert single + 2 * summed == sum(nprod[len(c)] for c in st)
+    assert single + summed == sum(nks[len(c)] for c in st)
     # odd symmetry S(-x) = -S(x)
     assert np.abs(horner(st, -x) + horner(st, x)).max() < 1e-9
     # every planned addition saw identical scales, constants fit 62 bits
     assert all(abs(int(l.split()[4])) < 2 ** 62 for l in mir.log if l.startswith("MULC "))
-    assert all(abs(int(v)) < 2 ** 62 for l in mir.log if l.startswith(("LINC ", "MULCT ")) and len(l.split()) > 4
+    assert all(abs(int(v)) < 2 ** 62 for l in mir.log if l.startswith(("LINC ", "MULCT ", "MULCT2 ")) and len(l.split()) > 4
                for v in l.split()[4].split(","))
 
 
