@@ -53,13 +53,13 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
     __shared__ uint32_t tslot;
     // per-target constants staged once per CTA: prime, output row offset, 1/q, [P]_{q_t} (+ Shoup)
     __shared__ u64 sq[TC_TMAX], spm[TC_TMAX], spmsh[TC_TMAX];
-    __shared__ double sqinv[TC_TMAX];
+    __shared__ double sqinv[TC_TMAX], sqd[TC_TMAX], sw32[TC_TMAX], sw32q[TC_TMAX];
     __shared__ long soff[TC_TMAX];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int p = blockIdx.y;
     const TcGroup &G = a.groups[a.grouped ? p % a.pdiv : 0];
     const int nt = G.nt, ns = G.ns + (a.const1 ? 1 : 0);
-    const int ntp = (nt + 1) & ~1;  // N = 8 ntp, a multiple of 16
+    const int ncols = G.ncols, planes = G.planes;  // MMA N (multiple of 16), byte planes per target
     const int ksteps = (8 * ns + 31) / 32;
     const long N = 1L << a.logn;
 
@@ -72,6 +72,9 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
         const u64 q = a.tab.q[G.prime[tid]];
         sq[tid] = q;
         sqinv[tid] = G.qinv[tid];
+        sw32[tid] = G.w32[tid];
+        sqd[tid] = a.tab.qd[G.prime[tid]];  // exact (double) q
+        sw32q[tid] = G.w32q[tid];
         spm[tid] = G.pmod[tid];
         spmsh[tid] = G.pmodsh[tid];
         soff[tid] = (long)G.out_row[tid] << a.logn;
@@ -83,7 +86,7 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
     {  // B (canonical, 8 ntp rows x TC_K bytes) and a zeroed A (the constant-1 source written once)
         const uint4 *gb = reinterpret_cast<const uint4 *>(G.B);
         uint4 *b4 = reinterpret_cast<uint4 *>(sB);
-        for (int i = tid; i < 8 * ntp * TC_K / 16; i += TC_THREADS) b4[i] = gb[i];
+        for (int i = tid; i < ncols * TC_K / 16; i += TC_THREADS) b4[i] = gb[i];
         uint4 *a4 = reinterpret_cast<uint4 *>(sA);
         for (int i = tid; i < TC_M * TC_K / 16; i += TC_THREADS) a4[i] = make_uint4(0, 0, 0, 0);
     }
@@ -93,7 +96,7 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const uint32_t tmem = tslot;
-    const uint32_t idesc = (2u << 4) | ((uint32_t)(8 * ntp >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+    const uint32_t idesc = (2u << 4) | ((uint32_t)(ncols >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
     const u64 *src = a.src + (long)(p / a.pdiv) * a.s_cs + (long)(p % a.pdiv) * a.s_ps + (long)G.src_row0 * N;
     u64 *dst = a.dst + (long)(p / a.pdiv) * a.d_cs + (long)(p % a.pdiv) * a.d_ps;
     const int lq = warp & 3, tpar = warp >> 2;  // TMEM lane quarter, target group (0..3)
@@ -153,13 +156,46 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
         // V = lo + hi 2^32 with lo, hi < 2^48; k = floor(V / t) from doubles is off by at most one, so
         // r = V - k t (exact, mod 2^64) lies in [-t, 2t) and two corrections make it canonical.
         auto tld = [&](int t, uint32_t (&g)[8]) {
-            const uint32_t addr = tmem + ((uint32_t)(32 * lq) << 16) + (uint32_t)(8 * t);
-            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                         : "=r"(g[0]), "=r"(g[1]), "=r"(g[2]), "=r"(g[3]), "=r"(g[4]), "=r"(g[5]), "=r"(g[6]),
-                           "=r"(g[7])
-                         : "r"(addr));
+            const uint32_t lane_base = tmem + ((uint32_t)(32 * lq) << 16);
+            if (planes == 8) {
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                             : "=r"(g[0]), "=r"(g[1]), "=r"(g[2]), "=r"(g[3]), "=r"(g[4]), "=r"(g[5]), "=r"(g[6]),
+                               "=r"(g[7])
+                             : "r"(lane_base + (uint32_t)(8 * t)));
+            } else {
+                const uint32_t a6 = lane_base + (uint32_t)(6 * t);
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n"
+                             : "=r"(g[0]), "=r"(g[1]) : "r"(a6));
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n"
+                             : "=r"(g[2]), "=r"(g[3]) : "r"(a6 + 2));
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n"
+                             : "=r"(g[4]), "=r"(g[5]) : "r"(a6 + 4));
+                g[6] = g[7] = 0;
+            }
         };
         auto tld_wait = [] { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); };
+        // 6-plane epilogue (targets < 2^46), exact FP64 arithmetic (the ntt.cu FpA product):
+        //   A = G0 + G1 2^8 + G2 2^16 + G3 2^24 < 2^47 and B = G4 + G5 2^8 < 2^32 are exact doubles;
+        //   V mod q = (A + [B (2^32 mod q)]_q) mod q with the product reduced exactly (|r| <= 0.75 q)
+        auto reduce6 = [&](const uint32_t (&g)[8], int t) -> u64 {
+            const double two52 = 4503599627370496.0, magic = 6755399441055744.0;
+            double gd[6];
+#pragma unroll
+            for (int b = 0; b < 6; b++)
+                gd[b] = __dsub_rn(__hiloint2double(0x43300000, (int)g[b]), two52);
+            const double A = __fma_rn(gd[3], 16777216.0, __fma_rn(gd[2], 65536.0, __fma_rn(gd[1], 256.0, gd[0])));
+            const double Bv = __fma_rn(gd[5], 256.0, gd[4]);
+            const double qd = sqd[t], qinv = sqinv[t], w = sw32[t], wq = sw32q[t];
+            const double k = __dsub_rn(__fma_rn(Bv, wq, magic), magic);
+            const double ph = __dmul_rn(k, qd);
+            const double pl = __fma_rn(k, qd, -ph);
+            const double r1 = __dsub_rn(__fma_rn(Bv, w, -ph), pl);
+            const double sv = __dadd_rn(A, r1);
+            const double k2 = __dsub_rn(__dadd_rn(__dmul_rn(sv, qinv), magic), magic);
+            double r = __fma_rn(-k2, qd, sv);
+            if (r < 0) r = __dadd_rn(r, qd);
+            return (u64)__double_as_longlong(__dadd_rn(r, two52)) & ((1ULL << 52) - 1);
+        };
         auto reduce_g = [&](const uint32_t (&g)[8], u64 q, double qinv) -> u64 {
             const u64 lo = (u64)g[0] + ((u64)g[1] << 8) + ((u64)g[2] << 16) + ((u64)g[3] << 24);
             const u64 hi = (u64)g[4] + ((u64)g[5] << 8) + ((u64)g[6] << 16) + ((u64)g[7] << 24);
@@ -182,7 +218,7 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
             uint32_t g[8];
             tld(0, g);
             tld_wait();
-            const u64 tl = reduce_g(g, ql, sqinv[0]);
+            const u64 tl = planes == 6 ? reduce6(g, 0) : reduce_g(g, ql, sqinv[0]);
             const u64 xc = src[(long)(-1) * N + k0 + m];
             r = csub(mul_shoup(submod(xc, tl, ql), a.pinv_l, a.pinv_l_sh, ql) + (ql >> 1), ql);
             t0 = 1;
@@ -196,13 +232,13 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
             tld_wait();
             {
                 const u64 q = sq[t];
-                u64 z = reduce_g(g, q, sqinv[t]);
+                u64 z = planes == 6 ? reduce6(g, t) : reduce_g(g, q, sqinv[t]);
                 if (a.rr) z = addmod(z, csub(mul_shoup(r, spm[t], spmsh[t], q), q), q);
                 dst[soff[t] + k0 + m] = z;
             }
             if (t2 < nt) {
                 const u64 q = sq[t2];
-                u64 z = reduce_g(h, q, sqinv[t2]);
+                u64 z = planes == 6 ? reduce6(h, t2) : reduce_g(h, q, sqinv[t2]);
                 if (a.rr) z = addmod(z, csub(mul_shoup(r, spm[t2], spmsh[t2], q), q), q);
                 dst[soff[t2] + k0 + m] = z;
             }
@@ -218,15 +254,16 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
 
 // host: a conversion group's B matrix in canonical layout.  c[s][t] = the constant of source s for
 // target t (mod prime t); rows 8 t + b, columns 8 s + a hold byte b of (c 256^a mod t).
-std::vector<uint8_t> tc_bmatrix(const std::vector<std::vector<u64>> &c, const std::vector<u64> &tprimes) {
-    const int ns = (int)c.size(), nt = (int)tprimes.size(), ntp = (nt + 1) & ~1;
-    std::vector<uint8_t> B((size_t)8 * ntp * TC_K, 0);
+std::vector<uint8_t> tc_bmatrix(const std::vector<std::vector<u64>> &c, const std::vector<u64> &tprimes, int planes,
+                                int ncols) {
+    const int ns = (int)c.size(), nt = (int)tprimes.size();
+    std::vector<uint8_t> B((size_t)ncols * TC_K, 0);
     for (int t = 0; t < nt; t++) {
         const u64 q = tprimes[t];
         for (int s = 0; s < ns; s++) {
             u64 v = c[s][t] % q;
             for (int aa = 0; aa < 8; aa++) {
-                for (int b = 0; b < 8; b++) B[canon(8 * t + b, 8 * s + aa)] = (uint8_t)(v >> (8 * b));
+                for (int b = 0; b < planes; b++) B[canon(planes * t + b, 8 * s + aa)] = (uint8_t)(v >> (8 * b));
                 v = h_mulmod(v, 256, q);
             }
         }

@@ -202,6 +202,9 @@ void Ctx::log(const char *kind, int lin, int lout, double s, const std::string &
 // tensor-core base-conversion groups of a level (bconv_tc.cu): ModUp per digit, fused ModDown +
 // rescale, plain ModDown.  Constants are exactly those of the integer kernels (R10, R11, R12).
 // ---------------------------------------------------------------------------------------------
+#ifndef SECPE_TC_PLANES6
+#define SECPE_TC_PLANES6 1  // development switch: 0 = 8 byte planes and the integer epilogue everywhere
+#endif
 void Ctx::build_tc_groups(LevelConsts &lc, int l) {
     const int nl = l + 1, ne = nl + np, bt = beta(l);
     auto pid = [&](int e) { return e < nl ? e : nq + (e - nl); };
@@ -211,7 +214,16 @@ void Ctx::build_tc_groups(LevelConsts &lc, int l) {
     auto add = [&](TcGroup g, const std::vector<std::vector<u64>> &c, const std::vector<u64> &tp) {
         if (g.ns + 1 > 12 || g.nt > TC_TMAX) ok = false;
         if (!ok) return;
-        Bs.push_back(tc_bmatrix(c, tp));
+        // 6 byte planes suffice when every constant (< target prime) is < 2^48; the 6-plane epilogue is
+        // exact FP64 arithmetic, which needs the targets below 2^46
+        bool small = true;
+        for (u64 t : tp) small &= t < (1ULL << 46);
+        small = small && SECPE_TC_PLANES6;
+        g.planes = small ? 6 : 8;
+        const int ntp = (g.nt + 1) & ~1;
+        g.ncols = small ? ((6 * g.nt + 15) / 16) * 16 : 8 * ntp;
+        if (g.ncols < 16) g.ncols = 16;
+        Bs.push_back(tc_bmatrix(c, tp, g.planes, g.ncols));
         groups.push_back(g);
     };
     // ModUp digits: sources y_i (i in I_j), targets every e outside the digit
@@ -308,7 +320,13 @@ void Ctx::build_tc_groups(LevelConsts &lc, int l) {
     lc.tc_ok = ok;
     if (!ok) return;
     for (auto &g : groups)
-        for (int t = 0; t < g.nt; t++) g.qinv[t] = 1.0 / (double)primes[g.prime[t]];
+        for (int t = 0; t < g.nt; t++) {
+            const u64 q = primes[g.prime[t]];
+            g.qinv[t] = 1.0 / (double)q;
+            const u64 w = (u64)(((u128)1 << 32) % q);
+            g.w32[t] = (double)w;
+            g.w32q[t] = g.w32[t] * g.qinv[t];
+        }
     // one device buffer for every B matrix; TcGroup.B point into it
     std::vector<size_t> off;
     size_t total = 0;
