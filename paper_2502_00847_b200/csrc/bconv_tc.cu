@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
     __shared__ uint32_t tslot;
     // per-target constants staged once per CTA: prime, output row offset, 1/q, [P]_{q_t} (+ Shoup)
     __shared__ u64 sq[TC_TMAX], spm[TC_TMAX], spmsh[TC_TMAX];
-    __shared__ double sqinv[TC_TMAX], sqd[TC_TMAX], sw32[TC_TMAX], sw32q[TC_TMAX];
+    __shared__ double sqinv[TC_TMAX];
     __shared__ long soff[TC_TMAX];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int p = blockIdx.y;
@@ -72,9 +72,6 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
         const u64 q = a.tab.q[G.prime[tid]];
         sq[tid] = q;
         sqinv[tid] = G.qinv[tid];
-        sw32[tid] = G.w32[tid];
-        sqd[tid] = a.tab.qd[G.prime[tid]];  // exact (double) q
-        sw32q[tid] = G.w32q[tid];
         spm[tid] = G.pmod[tid];
         spmsh[tid] = G.pmodsh[tid];
         soff[tid] = (long)G.out_row[tid] << a.logn;
@@ -174,27 +171,22 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
             }
         };
         auto tld_wait = [] { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); };
-        // 6-plane epilogue (targets < 2^46), exact FP64 arithmetic (the ntt.cu FpA product):
-        //   A = G0 + G1 2^8 + G2 2^16 + G3 2^24 < 2^47 and B = G4 + G5 2^8 < 2^32 are exact doubles;
-        //   V mod q = (A + [B (2^32 mod q)]_q) mod q with the product reduced exactly (|r| <= 0.75 q)
+        // 6-plane epilogue (constants < 2^48): the same quotient reduction with the two zero planes
+        // dropped (hi = G4 + G5 2^8 < 2^32 is a plain 32-bit value)
         auto reduce6 = [&](const uint32_t (&g)[8], int t) -> u64 {
-            const double two52 = 4503599627370496.0, magic = 6755399441055744.0;
-            double gd[6];
-#pragma unroll
-            for (int b = 0; b < 6; b++)
-                gd[b] = __dsub_rn(__hiloint2double(0x43300000, (int)g[b]), two52);
-            const double A = __fma_rn(gd[3], 16777216.0, __fma_rn(gd[2], 65536.0, __fma_rn(gd[1], 256.0, gd[0])));
-            const double Bv = __fma_rn(gd[5], 256.0, gd[4]);
-            const double qd = sqd[t], qinv = sqinv[t], w = sw32[t], wq = sw32q[t];
-            const double k = __dsub_rn(__fma_rn(Bv, wq, magic), magic);
-            const double ph = __dmul_rn(k, qd);
-            const double pl = __fma_rn(k, qd, -ph);
-            const double r1 = __dsub_rn(__fma_rn(Bv, w, -ph), pl);
-            const double sv = __dadd_rn(A, r1);
-            const double k2 = __dsub_rn(__dadd_rn(__dmul_rn(sv, qinv), magic), magic);
-            double r = __fma_rn(-k2, qd, sv);
-            if (r < 0) r = __dadd_rn(r, qd);
-            return (u64)__double_as_longlong(__dadd_rn(r, two52)) & ((1ULL << 52) - 1);
+            const u64 q = sq[t];
+            const u64 lo = (u64)g[0] + ((u64)g[1] << 8) + ((u64)g[2] << 16) + ((u64)g[3] << 24);
+            const uint32_t hi = g[4] + (g[5] << 8);
+            const double two52 = 4503599627370496.0;
+            const double lod = __dsub_rn(__longlong_as_double((long long)(lo | 0x4330000000000000ULL)), two52);
+            const double hid = __dsub_rn(__hiloint2double(0x43300000, (int)hi), two52);
+            const double vd = __fma_rn(hid, 4294967296.0, lod);
+            const double kd = floor(__dmul_rn(vd, sqinv[t]));
+            const u64 k = (u64)__double_as_longlong(__dadd_rn(kd, two52)) & ((1ULL << 52) - 1);
+            long long r = (long long)(lo + ((u64)hi << 32) - k * q);
+            if (r < 0) r += (long long)q;
+            if ((u64)r >= q) r -= (long long)q;
+            return (u64)r;
         };
         auto reduce_g = [&](const uint32_t (&g)[8], u64 q, double qinv) -> u64 {
             const u64 lo = (u64)g[0] + ((u64)g[1] << 8) + ((u64)g[2] << 16) + ((u64)g[3] << 24);

@@ -214,8 +214,7 @@ void Ctx::build_tc_groups(LevelConsts &lc, int l) {
     auto add = [&](TcGroup g, const std::vector<std::vector<u64>> &c, const std::vector<u64> &tp) {
         if (g.ns + 1 > 12 || g.nt > TC_TMAX) ok = false;
         if (!ok) return;
-        // 6 byte planes suffice when every constant (< target prime) is < 2^48; the 6-plane epilogue is
-        // exact FP64 arithmetic, which needs the targets below 2^46
+        // 6 byte planes suffice when every constant (< target prime) is < 2^48
         bool small = true;
         for (u64 t : tp) small &= t < (1ULL << 46);
         small = small && SECPE_TC_PLANES6;
@@ -320,13 +319,7 @@ void Ctx::build_tc_groups(LevelConsts &lc, int l) {
     lc.tc_ok = ok;
     if (!ok) return;
     for (auto &g : groups)
-        for (int t = 0; t < g.nt; t++) {
-            const u64 q = primes[g.prime[t]];
-            g.qinv[t] = 1.0 / (double)q;
-            const u64 w = (u64)(((u128)1 << 32) % q);
-            g.w32[t] = (double)w;
-            g.w32q[t] = g.w32[t] * g.qinv[t];
-        }
+        for (int t = 0; t < g.nt; t++) g.qinv[t] = 1.0 / (double)primes[g.prime[t]];
     // one device buffer for every B matrix; TcGroup.B point into it
     std::vector<size_t> off;
     size_t total = 0;

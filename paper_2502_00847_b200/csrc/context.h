@@ -34,11 +34,8 @@ struct TcGroup {
     u64 pmod[TC_TMAX];       // rescale variant: [P]_{q_t} and its Shoup companion
     u64 pmodsh[TC_TMAX];
     double qinv[TC_TMAX];    // RN(1 / q_t) for the FP64 quotient of the epilogue
-    int planes;              // byte planes per target: 6 when every target prime is < 2^46 (exact-FP64
-                             // epilogue), else 8 (integer epilogue)
+    int planes;              // byte planes per target: 6 when every target prime is < 2^46, else 8
     int ncols;               // MMA N = TMEM columns used (multiple of 16, <= 256)
-    double w32[TC_TMAX];     // 6-plane epilogue: 2^32 mod q_t and RN(w / q_t)
-    double w32q[TC_TMAX];
 };
 struct TcArgs {
     const u64 *src;
