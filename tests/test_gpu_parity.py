@@ -427,3 +427,68 @@ def test_rotate_hoisted_errors(S):
     a = g.encrypt(kg, z, prm.L, prm.scale, 1)
     with pytest.raises(Exception, match="Galois"):
         g.rotate_hoisted(kg, a, [1, 5])
+
+
+@pytest.mark.slow
+def test_argmax_config5_bench_launch(S):
+    """BASELINE configs[4] in bench.py's launch configuration: 16 ciphertexts on a non-default stream
+    (two concurrent sub-batch streams, CUDA graph captured on the first call and replayed), full size.
+    The last ciphertext (second sub-batch) is compared word for word with the oracle; every query of
+    every ciphertext decodes to the plaintext argmax wherever the top-1 gap is above the Sign margin."""
+    stream = torch.cuda.Stream()
+    desc = synth.PARAM_SETS["argmax"]
+    prm = ckks.Params(desc)
+    lay = synth.LAYOUTS["argmax_k2"]
+    st = load_sign("sign_7_15_15.json")
+    steps = plan.argmax_rotations(lay)
+    seed = synth.KEY_SEED_BASE + 5
+    B = 16
+    with torch.cuda.stream(stream):
+        g = S.Context(desc, stream=stream.cuda_stream)
+        kg = g.keygen(seed, steps)
+        scores = [synth.softmax_scores(9000 + i, lay["queries"], lay["prompts"], lay["classes"]) for i in range(B)]
+        batch = g.new_ct(g.L, B)
+        for i in range(B - 1):  # library-encrypted (checked through decryption + labels)
+            z = S.pack(scores[i], lay, g.N // 2)
+            g.encrypt_coeffs(kg, g.encode(z, g.scale), g.L, g.scale, 900 + i, out=S.Ct(batch.t[i:i + 1], g.L, g.scale))
+        ev = ckks.Oracle(prm)
+        ko = ev.keygen(seed, steps)
+        last = ev.encrypt(ko, plan.pack(scores[-1], lay, prm.N // 2), prm.scale, 777)
+        batch.t[B - 1].copy_(torch.from_numpy(last.data))
+        batch.level, batch.scale = g.L, g.scale
+        ol, _ = g.argmax_info(lay, st, g.L)
+        out = g.new_ct(ol, B)
+        g.enc_argmax(kg, batch, lay, st, out=out)  # eager + capture
+        stream.synchronize()
+        first = out.t.cpu().numpy().copy()
+        out.t.zero_()
+        g.enc_argmax(kg, batch, lay, st, out=out)  # graph replay
+        stream.synchronize()
+        got = out.t.cpu().numpy()
+    assert np.array_equal(got, first)
+    want = plan.argmax(ev, ko, last, lay, st)
+    assert np.array_equal(got[B - 1], want.data) and out.level == want.level and out.scale == want.scale
+    for i in range(B):
+        dec = g.decrypt(kg, out, i)
+        srt = np.sort(scores[i].mean(axis=1), axis=1)
+        ok = srt[:, -1] - srt[:, -2] >= 2.0 ** -7
+        assert ok.mean() > 0.9
+        assert (S.labels(dec, lay)[ok] == plan.true_labels(scores[i])[ok]).all(), i
+
+
+def test_argmax_errors(S):
+    """Depth exhausted (K = 16 needs 60 levels > 29 without bootstrapping, reading R18), empty batch,
+    no level left to rescale: error codes, never a crash or a wrong result."""
+    P = pair(S, "argmax")
+    g = P.gpu
+    st = load_sign("sign_7_15_15.json")
+    with pytest.raises(S.SecpeError):
+        g.argmax_info(synth.LAYOUTS["argmax_k16"], st, P.prm.L)
+    P = pair(S, "toy")
+    g, prm = P.gpu, P.prm
+    kg = g.keygen(synth.KEY_SEED_BASE + 7, [1])
+    a = g.encrypt(kg, synth.uniform_slots(1, prm.N // 2), 0, prm.scale, 1)  # level 0
+    with pytest.raises(S.SecpeError):
+        g.rescale(a)
+    with pytest.raises(S.SecpeError):
+        g.mul_relin_rescale(kg, a, a)
