@@ -232,8 +232,11 @@ __device__ __forceinline__ void tensor1(u64 a0, u64 a1, u64 b0, u64 b1, bool lin
     }
 }
 
+#ifndef KS_TEN_MINB
+#define KS_TEN_MINB 2  // resident CTAs per SM the relinearise path's register allocation targets
+#endif
 template <int MAXB, bool TEN>
-__global__ void __launch_bounds__(TPB, TEN ? 2 : 3) ks_inner_vec_kernel(Tab tab, int logn, const u64 *__restrict__ d, long ds,
+__global__ void __launch_bounds__(TPB, TEN ? KS_TEN_MINB : 3) ks_inner_vec_kernel(Tab tab, int logn, const u64 *__restrict__ d, long ds,
                                                            const u64 *__restrict__ ext, long exts,
                                                            const u64 *__restrict__ key, int nq_total, int np,
                                                            u64 *__restrict__ acc, long accs, int n_ct, int nl,
@@ -310,6 +313,83 @@ __global__ void __launch_bounds__(TPB, TEN ? 2 : 3) ks_inner_vec_kernel(Tab tab,
         } else {
             cur = nxt;
         }
+    }
+}
+
+// Relinearise-and-rescale key inner product, one coefficient per thread: about half the registers of the
+// two-coefficient kernel (which holds 16-byte vectors of every tensor input), so three CTAs fit per SM
+// without spills.  Same integers (tensor1_fp / tensor1, 128-bit MACs, one Barrett per output).
+#ifndef KS_TEN1
+#define KS_TEN1 1
+#endif
+#ifndef KS_TEN1_MINB
+#define KS_TEN1_MINB 3
+#endif
+template <int MAXB>
+__global__ void __launch_bounds__(TPB, KS_TEN1_MINB) ks_inner_ten1_kernel(Tab tab, int logn, const u64 *__restrict__ ext,
+                                                                       long exts, const u64 *__restrict__ key,
+                                                                       int nq_total, int np, u64 *__restrict__ acc,
+                                                                       long accs, int n_ct, int nl, int alpha,
+                                                                       int beta, TensorSrc ten,
+                                                                       const u64 *__restrict__ pmod) {
+    const int e = blockIdx.y;
+    const long N = 1L << logn;
+    const long k = (long)blockIdx.x * TPB + threadIdx.x;
+    const int ne = nl + np, nk = nq_total + np;
+    const int pr = e < nl ? e : nq_total + (e - nl);
+    const u64 q = tab.q[pr], r0 = tab.br0[pr], r1 = tab.br1[pr];
+    u64 kb[MAXB], ka[MAXB];
+#pragma unroll
+    for (int j = 0; j < MAXB; j++)
+        if (j < beta) {
+            kb[j] = __ldg(key + (((long)j * 2 + 0) * nk + pr) * N + k);
+            ka[j] = __ldg(key + (((long)j * 2 + 1) * nk + pr) * N + k);
+        }
+    const int jd = e < nl ? e / alpha : -1;
+    const bool qrow = e < nl;
+    const u64 pm = qrow ? pmod[e] : 0;
+    const bool lin = ten.x.p != nullptr, lin2 = ten.x2.p != nullptr, p2 = ten.a2.p != nullptr;
+    const u64 cc = lin && qrow ? ten.C.c[e] : 0, ccsh = lin && qrow ? ten.C.csh[e] : 0;
+    const u64 c2 = lin2 && qrow ? ten.C2.c[e] : 0, c2sh = lin2 && qrow ? ten.C2.csh[e] : 0;
+    const double qd = tab.qd[pr], qinv = tab.qinv[pr];
+    const long o = e * N + k;
+    for (int c = 0; c < n_ct; c++) {
+        u64 x[MAXB];
+#pragma unroll
+        for (int j = 0; j < MAXB; j++)
+            if (j < beta && j != jd) x[j] = ext[c * exts + ((long)j * ne + e) * N + k];
+        u64 d0 = 0, d1 = 0;
+        if (qrow) {
+            const u64 a0 = ten.a.p[c * ten.a.cs + o], a1 = ten.a.p[c * ten.a.cs + ten.a.ps + o];
+            const u64 b0 = ten.b.p[c * ten.b.cs + o], b1 = ten.b.p[c * ten.b.cs + ten.b.ps + o];
+            const u64 x0 = lin ? ten.x.p[c * ten.x.cs + o] : 0, x1 = lin ? ten.x.p[c * ten.x.cs + ten.x.ps + o] : 0;
+            const u64 y0 = lin2 ? ten.x2.p[c * ten.x2.cs + o] : 0;
+            const u64 y1 = lin2 ? ten.x2.p[c * ten.x2.cs + ten.x2.ps + o] : 0;
+            const u64 u0 = p2 ? ten.a2.p[c * ten.a2.cs + o] : 0, u1 = p2 ? ten.a2.p[c * ten.a2.cs + ten.a2.ps + o] : 0;
+            const u64 w0 = p2 ? ten.b2.p[c * ten.b2.cs + o] : 0, w1 = p2 ? ten.b2.p[c * ten.b2.cs + ten.b2.ps + o] : 0;
+            u64 d2;
+            if (q < (1ULL << 46))
+                tensor1_fp(a0, a1, b0, b1, lin, x0, x1, cc, lin2, y0, y1, c2, qd, qinv, d0, d1, d2, p2, u0, u1, w0, w1);
+            else
+                tensor1(a0, a1, b0, b1, lin, x0, x1, cc, ccsh, lin2, y0, y1, c2, c2sh, q, r0, r1, d0, d1, d2, p2, u0, u1,
+                        w0, w1);
+#pragma unroll
+            for (int j = 0; j < MAXB; j++)
+                if (j == jd) x[j] = d2;
+        }
+        U128 s0{0, 0}, s1{0, 0};
+#pragma unroll
+        for (int j = 0; j < MAXB; j++)
+            if (j < beta) {
+                mac_wide(s0, x[j], kb[j]);
+                mac_wide(s1, x[j], ka[j]);
+            }
+        if (qrow) {
+            mac_wide(s0, d0, pm);
+            mac_wide(s1, d1, pm);
+        }
+        acc[c * accs + (long)e * N + k] = barrett128(s0, q, r0, r1);
+        acc[c * accs + (long)(ne + e) * N + k] = barrett128(s1, q, r0, r1);
     }
 }
 
@@ -531,7 +611,10 @@ void k_ks_inner(const Tab &tab, int logn, const u64 *d, long ds, const u64 *ext,
     const TensorSrc &T = ten ? *ten : none;
 #define KSV(B_)                                                                                                   \
     do {                                                                                                          \
-        if (ten)                                                                                                  \
+        if (ten && KS_TEN1)                                                                                       \
+            ks_inner_ten1_kernel<B_><<<g1, TPB, 0, st>>>(tab, logn, ext, exts, key, nq_total, np, acc, accs, n_ct, \
+                                                         nl, alpha, beta, T, pmod);                               \
+        else if (ten)                                                                                             \
             ks_inner_vec_kernel<B_, true><<<g2, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, \
                                                               accs, n_ct, nl, alpha, beta, T, pmod, galois);      \
         else                                                                                                      \
