@@ -112,6 +112,9 @@ size_t secpe_ct_bytes(const secpe_ctx *ctx, int32_t level);
  * rotation step in rot_steps (host[n_rot]; >0 RotL, <0 RotR).  Hybrid digits (reading R7). */
 int secpe_keygen(secpe_ctx *ctx, uint64_t seed, const int32_t *rot_steps, int32_t n_rot,
                  secpe_keys **out);
+/* Frees the key material.  Synchronises the owning context's stream and destroys every CUDA graph
+ * secpe_enc_argmax captured with these keys (a later keys object at the same address never replays
+ * them).  Keys may be destroyed before or after their context; null is a no-op. */
 void secpe_keys_destroy(secpe_keys *keys);
 /* Copy key material to host (synchronises), for parity tests.
  * which 0: secret s, NTT form over all n_q+n_p primes, uint64[n_q+n_p][N]

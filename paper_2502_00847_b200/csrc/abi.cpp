@@ -219,11 +219,21 @@ int secpe_keygen(secpe_ctx *ctx, uint64_t seed, const int32_t *rot_steps, int32_
         REQUIRE(ctx->c.np >= 1, SECPE_EINVAL, "key generation needs at least one special prime");
         auto h = std::make_unique<secpe_keys>();
         h->k = keygen(ctx->c, seed, rot_steps, n_rot);
+        h->k->owner = &ctx->c;
+        ctx->c.live_keys.insert(h->k);
         *out = h.release();
     });
 }
 void secpe_keys_destroy(secpe_keys *keys) {
     if (!keys) return;
+    if (keys->k && keys->k->owner) {
+        // captured argmax graphs read this key material: drop them before it is freed (a later keys
+        // object at the same address must never replay them)
+        Ctx &c = *keys->k->owner;
+        if (c.st) cudaStreamSynchronize(c.st);
+        c.drop_graphs(keys);
+        c.live_keys.erase(keys->k);
+    }
     delete keys->k;
     delete keys;
 }
@@ -546,6 +556,7 @@ static void argmax_views(Ctx &c, const secpe_keys *keys, const CtView &vin, cons
     CUDA_CHECK(cudaGraphInstantiate(&G.exec, graph, 0));
     CUDA_CHECK(cudaGraphDestroy(graph));
     CUDA_CHECK(cudaGraphUpload(G.exec, c.st));  // pay the one-time upload now, not on the first replay
+    G.keys = keys;
     G.cnt.ntt_limbs = c.cnt.ntt_limbs - before.ntt_limbs;
     G.cnt.keyswitch = c.cnt.keyswitch - before.keyswitch;
     G.cnt.rescale = c.cnt.rescale - before.rescale;

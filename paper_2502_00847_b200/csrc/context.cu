@@ -340,7 +340,19 @@ void Ctx::build_tc_groups(LevelConsts &lc, int l) {
 // ---------------------------------------------------------------------------------------------
 // context build
 // ---------------------------------------------------------------------------------------------
+void Ctx::drop_graphs(const void *keys) {
+    for (auto it = graphs.begin(); it != graphs.end();) {
+        if (it->second.keys == keys) {
+            if (it->second.exec) cudaGraphExecDestroy(it->second.exec);
+            it = graphs.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
+
 Ctx::~Ctx() {
+    for (Keys *k : live_keys) k->owner = nullptr;  // keys may outlive the context
     if (st) cudaStreamSynchronize(st);
     for (auto &g : graphs)
         if (g.second.exec) cudaGraphExecDestroy(g.second.exec);

@@ -1,6 +1,7 @@
 // context.h -- library context, keys, device buffers and the ciphertext evaluator.
 #pragma once
 #include <map>
+#include <set>
 #include <memory>
 #include <string>
 #include <vector>
@@ -137,8 +138,11 @@ struct Ctx {
         cudaGraphExec_t exec = nullptr;
         Counters cnt;
         double out_scale = 0;
+        const void *keys = nullptr;  // evaluation keys whose device memory the graph's kernels read
     };
     std::map<std::string, Graph> graphs;
+    std::set<Keys *> live_keys;          // keys generated on this context (owner back-pointers)
+    void drop_graphs(const void *keys);  // destroy every graph that reads these keys
     bool use_graphs = true;
     // host-buffer argmax pipeline (secpe_enc_argmax_host): two device staging slots per direction and a
     // copy stream; loaded[s]: slot s's inputs are on the device, freed[s]: slot s's last use has finished
@@ -164,6 +168,7 @@ struct Ctx {
 };
 
 struct Keys {
+    Ctx *owner = nullptr;  // context whose graph cache may reference this key material
     DevBuf s;      // [nq+np][N] NTT
     DevBuf pk;     // [2][nq][N]
     DevBuf rlk;    // [beta_top][2][nq+np][N]

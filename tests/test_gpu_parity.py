@@ -492,3 +492,38 @@ def test_argmax_errors(S):
         g.rescale(a)
     with pytest.raises(S.SecpeError):
         g.mul_relin_rescale(kg, a, a)
+
+
+def test_keys_destroy_drops_captured_graphs(S):
+    """A captured argmax graph reads its keys' device memory: destroying the keys must drop it, so a new
+    keys object (possibly at the same address) on the same buffers computes with the NEW keys."""
+    stream = torch.cuda.Stream()
+    desc = synth.PARAM_SETS["toy_argmax"]
+    lay = dict(synth.LAYOUTS["toy"], queries=64)
+    st = load_sign("sign_f1_f1.json")
+    rot = plan.argmax_rotations(lay)
+    with torch.cuda.stream(stream):
+        g = S.Context(desc, stream=stream.cuda_stream)
+        ref = S.Context(desc, stream=stream.cuda_stream)
+        batch = g.new_ct(g.L, 2)
+        batch.t.copy_(torch.from_numpy(np.random.default_rng(5).integers(0, 2 ** 20, batch.t.shape,
+                                                                            dtype=np.uint64)))
+        batch.level, batch.scale = g.L, g.scale
+        ol, _ = g.argmax_info(lay, st, g.L)
+        out = g.new_ct(ol, 2)
+        k1 = g.keygen(synth.KEY_SEED_BASE + 1, rot)
+        for _ in range(2):  # eager + capture, then replay
+            g.enc_argmax(k1, batch, lay, st, out=out)
+        del k1
+        k2 = g.keygen(synth.KEY_SEED_BASE + 2, rot)
+        g.enc_argmax(k2, batch, lay, st, out=out)
+        stream.synchronize()
+        got = out.t.cpu().numpy().copy()
+        r2 = ref.keygen(synth.KEY_SEED_BASE + 2, rot)
+        want = ref.enc_argmax(r2, batch, lay, st)
+        stream.synchronize()
+        assert np.array_equal(got, want.t.cpu().numpy())
+        del r2, ref  # keys and context destroyed in either order
+        k3 = g.keygen(synth.KEY_SEED_BASE + 3, rot)
+        del g
+        del k3
