@@ -54,6 +54,23 @@ void ev_ntt(Ctx &c, RowsArg d, int n_polys, LimbMap lm, bool inverse, const NttF
     c.cnt.launches += 2;
 }
 
+#ifndef SECPE_NTT_SEGS
+#define SECPE_NTT_SEGS 1  // development switch: 0 = one launch pair per segment
+#endif
+void ev_ntt_segs(Ctx &c, const std::vector<NttSeg> &segs, bool inverse) {
+    if (!SECPE_NTT_SEGS) {
+        for (auto &g : segs) ev_ntt(c, g.d, g.n_polys, g.lm, inverse);
+        return;
+    }
+    NttSpans spans{&c};
+    const NttProfHook hook{&spans, ntt_mark};
+    if (c.prof.on) ntt_set_prof_hook(&hook);
+    ntt_segments(c.tab, c.logn, segs.data(), (int)segs.size(), inverse, c.st);
+    if (c.prof.on) ntt_set_prof_hook(nullptr);
+    for (auto &g : segs) c.cnt.ntt_limbs += (long long)g.n_polys * g.lm.nl;
+    c.cnt.launches += 2;
+}
+
 void ev_copy(Ctx &c, const CtView &a, const CtView &out) {
     k_copy_rows(c.logn, crows_of(a), rows_of(out), 2 * a.n, out.level + 1, c.st);
     c.cnt.launches++;
@@ -181,14 +198,17 @@ static void ks_modup(Ctx &c, const u64 *d, long d_stride, int n, int level, DevB
     }
     // NTT of the converted limbs: the Q limbs outside each digit per digit, then the special limbs of
     // every digit of every ciphertext in one launch (n beta polynomials of np rows, stride ne N)
+    // (all of them batched into one launch pair per prime class: each alone is a small grid)
+    std::vector<NttSeg> segs;
     for (int j = 0; j < bt; j++) {
         const int i0 = j * c.alpha, i1 = std::min(i0 + c.alpha, nl);
-        if (i0 > 0) ev_ntt(c, RowsArg{ext.p + (long)j * ne * N, 2 * exts, exts}, n, LimbMap{i0, i0, 0, 0}, false);
+        if (i0 > 0) segs.push_back(NttSeg{RowsArg{ext.p + (long)j * ne * N, 2 * exts, exts}, n, LimbMap{i0, i0, 0, 0}});
         if (i1 < nl)
-            ev_ntt(c, RowsArg{ext.p + ((long)j * ne + i1) * N, 2 * exts, exts}, n, LimbMap{nl - i1, nl - i1, i1, 0},
-                   false);
+            segs.push_back(NttSeg{RowsArg{ext.p + ((long)j * ne + i1) * N, 2 * exts, exts}, n,
+                                  LimbMap{nl - i1, nl - i1, i1, 0}});
     }
-    ev_ntt(c, RowsArg{ext.p + (long)nl * N, 2L * ne * N, (long)ne * N}, n * bt, LimbMap{np, 0, 0, c.nq}, false);
+    segs.push_back(NttSeg{RowsArg{ext.p + (long)nl * N, 2L * ne * N, (long)ne * N}, n * bt, LimbMap{np, 0, 0, c.nq}});
+    ev_ntt_segs(c, segs, false);
     c.cnt.launches += 1;
 }
 

@@ -55,6 +55,14 @@ struct NttProfHook {
     void (*mark)(void *ctx, int phase, bool fp, double bytes, double limbs);
 };
 void ntt_set_prof_hook(const NttProfHook *h);
+// several independent plain in-place transforms (each: n_polys polynomials of lm.nl limbs in d) batched
+// into as few launches as possible (ntt.cu MAXSEG row ranges per launch and prime class)
+struct NttSeg {
+    RowsArg d;
+    int n_polys;
+    LimbMap lm;
+};
+void ntt_segments(const Tab &tab, int logn, const NttSeg *segs, int nseg, bool inverse, cudaStream_t st);
 void ntt_inverse(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
                  const NttFusion &f = NttFusion());
 

@@ -261,6 +261,16 @@ __device__ __forceinline__ void do_round(u64 (&v)[NV], int tau, int g, const ulo
 enum { IN_PLAIN = 0, IN_SRC = 1, IN_BCAST = 2, IN_MUL = 3, IN_MUL2 = 4 };
 enum { OUT_PLAIN = 0, OUT_RESCALE = 1, OUT_MODDOWN = 2 };
 
+// A launch covers one row range of one buffer, or (nseg > 0, plain transforms only) up to MAXSEG
+// independent row ranges of several buffers: small transforms batched into one grid (a transform of a
+// few rows costs about one CTA latency per pass, ~10 us, whatever its size).
+constexpr int MAXSEG = 8;
+struct Seg {
+    RowsArg d;
+    LimbMap lm;
+    int limb0, nsub;  // limbs [limb0, limb0 + nsub) of every polynomial of the segment
+    int row0;         // first grid row (blockIdx.y) of the segment
+};
 struct PassArgs {
     RowsArg d;  // transform buffer rows (row = poly * nl + limb)
     LimbMap lm;
@@ -268,22 +278,45 @@ struct PassArgs {
     NttFusion f;
     int limb0, nsub;  // this launch covers limbs [limb0, limb0 + nsub) of every polynomial (one prime class)
     int poly0;        // ... of polynomials poly0, poly0 + 1, ... (L2-sized chunks, see run())
+    int nseg = 0;     // > 0: the rows come from seg[0 .. nseg) instead (d, lm, limb0, nsub, poly0 unused)
+    Seg seg[MAXSEG];
 };
+
+// grid row y -> buffer, polynomial, limb, prime
+__device__ __forceinline__ void locate(const PassArgs &a, int y, RowsArg &d, int &poly, int &limb, int &prime) {
+    if (a.nseg == 0) {
+        d = a.d;
+        poly = a.poly0 + y / a.nsub;
+        limb = a.limb0 + y % a.nsub;
+        prime = prime_of(a.lm, limb);
+        return;
+    }
+    int si = 0;
+#pragma unroll
+    for (int i = 1; i < MAXSEG; i++)
+        if (i < a.nseg && y >= a.seg[i].row0) si = i;
+    const Seg &g = a.seg[si];
+    const int local = y - g.row0;
+    d = g.d;
+    poly = local / g.nsub;
+    limb = g.limb0 + local % g.nsub;
+    prime = prime_of(g.lm, limb);
+}
 
 // ---------------------------------------------------------------------------------------------
 // strided pass: group = column c, elements c + (N >> S) r, SC columns per CTA
 //   forward: stages 0..S-1 (first pass);  inverse: stages S-1..0 (last pass, * N^{-1})
 // ---------------------------------------------------------------------------------------------
 template <int LOGN, bool INV, int IN, class A>
-__device__ __forceinline__ void strided_body(const PassArgs &a, u64 *sm, int poly, int limb, int prime,
-                                             const PrimeC &P) {
+__device__ __forceinline__ void strided_body(const PassArgs &a, const RowsArg &d, u64 *sm, int poly, int limb,
+                                             int prime, const PrimeC &P) {
     constexpr int S = LOGN / 2;
     constexpr long N = 1L << LOGN;
     constexpr int STRIDE = (int)(N >> S);
     using R = Rnd<S, INV>;
     const int cl = threadIdx.x % SC, tau = threadIdx.x / SC;
     const int c = blockIdx.x * SC + cl;
-    u64 *base = a.d.p + poly_off(a.d.cs, a.d.ps, poly) + limb * N + c;
+    u64 *base = d.p + poly_off(d.cs, d.ps, poly) + limb * N + c;
     const u64 q = P.q;
     const ulonglong2 *tw = (INV ? a.tab.itw2 : a.tab.tw2) + prime * N;
     u64 v[NV];
@@ -349,10 +382,11 @@ struct MinB<FpA> {
 template <int LOGN, bool INV, int IN, class A>
 __global__ void __launch_bounds__(SC *(1 << (LOGN / 2 - RB)), MinB<A>::v) ntt_strided(PassArgs a) {
     __shared__ u64 sm[(1 << (LOGN / 2)) * SC];
-    const int poly = a.poly0 + blockIdx.y / a.nsub, limb = a.limb0 + blockIdx.y % a.nsub;
-    const int prime = prime_of(a.lm, limb);
+    RowsArg d;
+    int poly, limb, prime;
+    locate(a, blockIdx.y, d, poly, limb, prime);
     const PrimeC P = prime_consts(a.tab, prime);
-    strided_body<LOGN, INV, IN, A>(a, sm, poly, limb, prime, P);
+    strided_body<LOGN, INV, IN, A>(a, d, sm, poly, limb, prime, P);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -370,8 +404,8 @@ struct ContigCfg {
 __device__ __forceinline__ int padr(int r) { return r + (r >> 4); }
 
 template <int LOGN, bool INV, int IO, class A>
-__device__ __forceinline__ void contig_body(const PassArgs &a, u64 *sm, int poly, int limb, int prime,
-                                            const PrimeC &P) {
+__device__ __forceinline__ void contig_body(const PassArgs &a, const RowsArg &d, u64 *sm, int poly, int limb,
+                                            int prime, const PrimeC &P) {
     // IO: inverse -> IN_PLAIN | IN_SRC | IN_MUL (first pass reads f.src rows);  forward -> OUT_* epilogue
     using CF = ContigCfg<LOGN>;
     constexpr int S = CF::S, G = CF::G, TPG = CF::TPG, CG = CF::CG, PITCH = CF::PITCH;
@@ -379,7 +413,7 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, u64 *sm, int poly
     using R = Rnd<S, INV>;
     static_assert(R::NR == 2, "contiguous pass: two rounds");
     const long boff = limb * N + (long)blockIdx.x * CG * G;  // tile offset inside the polynomial
-    u64 *blk = a.d.p + poly_off(a.d.cs, a.d.ps, poly) + boff;
+    u64 *blk = d.p + poly_off(d.cs, d.ps, poly) + boff;
     const u64 q = P.q;
     const ulonglong2 *tw = (INV ? a.tab.itw2 : a.tab.tw2) + prime * N;
     const int gl = threadIdx.x / TPG, tau = threadIdx.x % TPG;
@@ -492,10 +526,11 @@ template <int LOGN, bool INV, int IO, class A>
 __global__ void __launch_bounds__(CT, MinB<A>::v) ntt_contig(PassArgs a) {
     using CF = ContigCfg<LOGN>;
     __shared__ __align__(16) u64 sm[CF::CG * CF::PITCH];
-    const int poly = a.poly0 + blockIdx.y / a.nsub, limb = a.limb0 + blockIdx.y % a.nsub;
-    const int prime = prime_of(a.lm, limb);
+    RowsArg d;
+    int poly, limb, prime;
+    locate(a, blockIdx.y, d, poly, limb, prime);
     const PrimeC P = prime_consts(a.tab, prime);
-    contig_body<LOGN, INV, IO, A>(a, sm, poly, limb, prime, P);
+    contig_body<LOGN, INV, IO, A>(a, d, sm, poly, limb, prime, P);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -965,6 +1000,91 @@ void dispatch(int logn, const PassArgs &a, int rows, bool inverse, cudaStream_t 
 }  // namespace
 
 void ntt_set_prof_hook(const NttProfHook *h) { g_hook = h; }
+
+namespace {
+// several independent plain forward transforms in as few launches as possible (MAXSEG row ranges per
+// launch, one launch pair per prime class)
+template <int LOGN>
+void run_segs(const Tab &tab, const NttSeg *segs, int nseg, bool inverse, cudaStream_t st) {
+    struct Run {
+        Seg g;
+        bool fp;
+        int rows;
+    };
+    std::vector<Run> runs;
+    for (int i = 0; i < nseg; i++) {
+        const NttSeg &x = segs[i];
+        if (x.n_polys <= 0 || x.lm.nl <= 0) continue;
+        auto isfp = [&](int l) {
+            const int p = prime_of(x.lm, l);
+            return p < 64 && ((tab.fp_mask >> p) & 1);
+        };
+        int l = 0;
+        while (l < x.lm.nl) {
+            const bool fp = isfp(l);
+            int e = l + 1;
+            while (e < x.lm.nl && isfp(e) == fp) e++;
+            runs.push_back(Run{Seg{x.d, x.lm, l, e - l, 0}, fp, x.n_polys * (e - l)});
+            l = e;
+        }
+    }
+    constexpr long N = 1L << LOGN;
+    for (int cls = 0; cls < 2; cls++) {
+        const bool fp = cls == 0;
+        PassArgs a{};
+        a.tab = tab;
+        a.nseg = 0;
+        int rows = 0;
+        auto flush = [&] {
+            if (!a.nseg) return;
+            a.nsub = rows;  // grid rows (n_polys = 1 below)
+            const double bytes = 16.0 * rows * (double)N / 2;
+            for (int pass = 0; pass < 2; pass++) {
+                if (g_hook) g_hook->mark(g_hook->ctx, 0, fp, bytes, rows / 2.0);
+                const bool first = pass == 0;
+                if (!inverse) {
+                    if (first)
+                        fp ? launch_strided_a<LOGN, false, IN_PLAIN, FpA>(a, 1, st)
+                           : launch_strided_a<LOGN, false, IN_PLAIN, IntA>(a, 1, st);
+                    else
+                        fp ? launch_contig_a<LOGN, false, OUT_PLAIN, FpA>(a, 1, st)
+                           : launch_contig_a<LOGN, false, OUT_PLAIN, IntA>(a, 1, st);
+                } else {
+                    if (first)
+                        fp ? launch_contig_a<LOGN, true, IN_PLAIN, FpA>(a, 1, st)
+                           : launch_contig_a<LOGN, true, IN_PLAIN, IntA>(a, 1, st);
+                    else
+                        fp ? launch_strided_a<LOGN, true, IN_PLAIN, FpA>(a, 1, st)
+                           : launch_strided_a<LOGN, true, IN_PLAIN, IntA>(a, 1, st);
+                }
+                LAUNCH_CHECK();
+                if (g_hook) g_hook->mark(g_hook->ctx, 1, fp, bytes, rows / 2.0);
+            }
+            a.nseg = 0;
+            rows = 0;
+        };
+        for (auto &r : runs) {
+            if (r.fp != fp) continue;
+            if (a.nseg == MAXSEG) flush();
+            r.g.row0 = rows;
+            a.seg[a.nseg++] = r.g;
+            rows += r.rows;
+        }
+        flush();
+    }
+}
+}  // namespace
+
+void ntt_segments(const Tab &tab, int logn, const NttSeg *segs, int nseg, bool inverse, cudaStream_t st) {
+    switch (logn) {
+        case 12: run_segs<12>(tab, segs, nseg, inverse, st); break;
+        case 13: run_segs<13>(tab, segs, nseg, inverse, st); break;
+        case 14: run_segs<14>(tab, segs, nseg, inverse, st); break;
+        case 15: run_segs<15>(tab, segs, nseg, inverse, st); break;
+        case 16: run_segs<16>(tab, segs, nseg, inverse, st); break;
+        default: throw SecpeError{-1, "NTT: log N must be in [12, 16]"};
+    }
+}
 
 void ntt_forward(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
                  const NttFusion &f) {
