@@ -32,6 +32,9 @@ namespace {
 #ifndef NTT_MINB_FP
 #define NTT_MINB_FP 4  // FP rows: 64 registers, no spills
 #endif
+#ifndef NTT_EPI_PREFETCH
+#define NTT_EPI_PREFETCH 1  // L2 prefetch of the rescale / ModDown epilogue operands at kernel start
+#endif
 #ifndef NTT_APPROX_HI
 #define NTT_APPROX_HI 1  // approximate Shoup quotient in the butterflies (measured: inverse -4%)
 #endif
@@ -415,6 +418,19 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, const RowsArg &d,
     const long boff = limb * N + (long)blockIdx.x * CG * G;  // tile offset inside the polynomial
     u64 *blk = d.p + poly_off(d.cs, d.ps, poly) + boff;
     const u64 q = P.q;
+#if NTT_EPI_PREFETCH
+    if (!INV && IO != OUT_PLAIN) {
+        // the epilogue operands do not depend on the transform: start pulling this tile's lines into L2
+        // now (one 128-byte line per thread) so the epilogue does not wait on DRAM latency
+        static_assert(CG * G * 8 == CT * 128, "one line per thread");
+        const char *p1 = reinterpret_cast<const char *>(a.f.e1.p + poly_off(a.f.e1.cs, a.f.e1.ps, poly) + boff);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p1 + threadIdx.x * 128));
+        if (IO == OUT_MODDOWN && (poly & 1) < a.f.e2_polys) {
+            const char *p2 = reinterpret_cast<const char *>(a.f.e2.p + poly_off(a.f.e2.cs, a.f.e2.ps, poly) + boff);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p2 + threadIdx.x * 128));
+        }
+    }
+#endif
     const ulonglong2 *tw = (INV ? a.tab.itw2 : a.tab.tw2) + prime * N;
     const int gl = threadIdx.x / TPG, tau = threadIdx.x % TPG;
     const int g = blockIdx.x * CG + gl;
