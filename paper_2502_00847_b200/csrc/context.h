@@ -200,7 +200,7 @@ void ev_mul_int(Ctx &c, const CtView &a, i64 C, const CtView &out);
 void ev_add_int(Ctx &c, const CtView &a, i64 C, const CtView &out);
 void ev_rescale(Ctx &c, const CtView &in, const CtView &out);
 void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, const u64 *add,
-                  long add_stride, int add_polys, u64 *out, long out_stride);
+                  long add_stride, int add_polys, u64 *out, long out_stride, const CRows *add3 = nullptr);
 void ev_mul_relin(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const CtView &out);
 // a (x) b [+ a2 (x) b2] [+ C x] relinearised and rescaled by q_l in one pass (bit-identical to ev_mul_relin
 // then ev_rescale); out at level a.level - 1.  lin_x: optional linear term (nullptr: none), C its constant;
@@ -209,7 +209,8 @@ void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &
                           const CtView &out, const CtView *lin_x2 = nullptr, i64 C2 = 0, const CtView *a2 = nullptr,
                           const CtView *b2 = nullptr);
 void ev_lincomb(Ctx &c, const CtView &a, i64 C1, const CtView *b, i64 C2, const CtView &out);
-void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView &out);
+void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView &out,
+               const CtView *add_after = nullptr);  // add_after: out = RotL(in) + add_after (fused)
 void ev_rotate_hoisted(Ctx &c, const Keys &k, const CtView &in, const int *steps, int n_steps, const CtView *outs);
 void ev_mul_plain_ntt(Ctx &c, const CtView &a, const u64 *pt, const CtView &out);
 LimbConst limb_const(const Ctx &c, i64 C, int nl);

@@ -234,16 +234,16 @@ static void ks_modup_inner(Ctx &c, const u64 *d, long d_stride, int n, int level
 // Hybrid key switching of d (NTT form; ct c at d + c * d_stride, level limbs), result added to
 // `add` (add_polys of 2 polynomials; compact, ct stride add_stride) and written compact to out.
 static void ks_moddown(Ctx &c, DevBuf &acc, int n, int level, const u64 *add, long add_stride, int add_polys,
-                       u64 *out, long out_stride);
+                       u64 *out, long out_stride, const CRows *add3 = nullptr);
 
 void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, const u64 *add,
-                  long add_stride, int add_polys, u64 *out, long out_stride) {
+                  long add_stride, int add_polys, u64 *out, long out_stride, const CRows *add3) {
     const long N = c.N;
     const int nl = level + 1, np = c.np, ne = nl + np, bt = c.beta(level);
     const size_t pa = c.prof_begin(1);
     DevBuf acc;
     ks_modup_inner(c, d, d_stride, n, level, key, acc);
-    ks_moddown(c, acc, n, level, add, add_stride, add_polys, out, out_stride);
+    ks_moddown(c, acc, n, level, add, add_stride, add_polys, out, out_stride, add3);
     c.cnt.keyswitch += n;
     // algorithmic bytes: input limbs + output limbs per ciphertext + the key once per batch
     c.prof_end(pa, 1, 8.0 * N * ((double)n * (nl + 2 * nl + add_polys * nl) + 2.0 * bt * ne), n);
@@ -251,7 +251,7 @@ void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u
 
 // ModDown of acc (R11) with the addend fused into the final NTT's epilogue; result compact in out
 static void ks_moddown(Ctx &c, DevBuf &acc, int n, int level, const u64 *add, long add_stride, int add_polys,
-                       u64 *out, long out_stride) {
+                       u64 *out, long out_stride, const CRows *add3) {
     const long N = c.N;
     const int nl = level + 1, np = c.np, ne = nl + np, bt = c.beta(level);
     const long accs = 2L * ne * N;
@@ -285,6 +285,7 @@ static void ks_moddown(Ctx &c, DevBuf &acc, int n, int level, const u64 *add, lo
     f6.e1 = CRows{acc.p, accs, (long)ne * N};
     f6.e2 = CRows{add, add_stride, (long)nl * N};
     f6.e2_polys = add ? add_polys : 0;
+    if (add3) f6.e3 = *add3;
     f6.out = RowsArg{out, out_stride, (long)nl * N};
     f6.k = c.pinv.p;
     f6.ksh = c.pinv_sh.p;
@@ -381,7 +382,7 @@ void ev_mul_relin(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const
     c.cnt.mulct += a.n;
 }
 
-void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView &out) {
+void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView &out, const CtView *add_after) {
     const u64 g = galois_elt(c, steps);
     const int nl = out.level + 1;
     if (g == 1) {
@@ -394,7 +395,13 @@ void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView 
     DevBuf sig((size_t)in.n * ss, c.st);
     k_automorph(c.logn, crows_of(in), RowsArg{sig.p, ss, (long)nl * N}, 2 * in.n, nl, g, c.st);
     c.cnt.launches++;
-    ev_keyswitch(c, sig.p + (long)nl * N, ss, in.n, out.level, it->second.p, sig.p, ss, 1, out.data, out.stride);
+    CRows a3{};
+    if (add_after) {
+        if (add_after->level < out.level || add_after->n != in.n) throw SecpeError{-1, "rotate: addend"};
+        a3 = crows_of(*add_after);
+    }
+    ev_keyswitch(c, sig.p + (long)nl * N, ss, in.n, out.level, it->second.p, sig.p, ss, 1, out.data, out.stride,
+                 add_after ? &a3 : nullptr);
     c.cnt.rotate += in.n;
 }
 

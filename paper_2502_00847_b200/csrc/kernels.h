@@ -43,6 +43,7 @@ struct NttFusion {
     const u64 *half = nullptr;
     CRows e1{nullptr, 0, 0}, e2{nullptr, 0, 0};
     int e2_polys = 0;
+    CRows e3{nullptr, 0, 0};  // out_mode 2: optional addend of every polynomial (a rotation's "y + RotL(y)")
     RowsArg out{nullptr, 0, 0};
     const u64 *k = nullptr, *ksh = nullptr;
 };

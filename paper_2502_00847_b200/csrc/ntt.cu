@@ -451,6 +451,10 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, const RowsArg &d,
             const char *p2 = reinterpret_cast<const char *>(a.f.e2.p + poly_off(a.f.e2.cs, a.f.e2.ps, poly) + boff);
             asm volatile("prefetch.global.L2 [%0];" ::"l"(p2 + threadIdx.x * 128));
         }
+        if (IO == OUT_MODDOWN && a.f.e3.p) {
+            const char *p3 = reinterpret_cast<const char *>(a.f.e3.p + poly_off(a.f.e3.cs, a.f.e3.ps, poly) + boff);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p3 + threadIdx.x * 128));
+        }
     }
 #endif
     const ulonglong2 *tw = (INV ? a.tab.itw2 : a.tab.tw2) + prime * N;
@@ -516,7 +520,7 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, const RowsArg &d,
         for (int k = 0; k < NV; k++) smg[padr(held<LO1>(tau, k))] = v[k];
         __syncthreads();
         // epilogue on 16-byte vectors; element e of the tile is at boff + e in its polynomial
-        const ulonglong2 *e1 = nullptr, *e2 = nullptr;
+        const ulonglong2 *e1 = nullptr, *e2 = nullptr, *e3 = nullptr;
         ulonglong2 *dst;
         u64 kc = 0, kcsh = 0;
         if (IO == OUT_PLAIN) {
@@ -526,6 +530,8 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, const RowsArg &d,
             e1 = reinterpret_cast<const ulonglong2 *>(a.f.e1.p + poly_off(a.f.e1.cs, a.f.e1.ps, P) + boff);
             if (IO == OUT_MODDOWN && (P & 1) < a.f.e2_polys)
                 e2 = reinterpret_cast<const ulonglong2 *>(a.f.e2.p + poly_off(a.f.e2.cs, a.f.e2.ps, P) + boff);
+            if (IO == OUT_MODDOWN && a.f.e3.p)
+                e3 = reinterpret_cast<const ulonglong2 *>(a.f.e3.p + poly_off(a.f.e3.cs, a.f.e3.ps, P) + boff);
             dst = reinterpret_cast<ulonglong2 *>(a.f.out.p + poly_off(a.f.out.cs, a.f.out.ps, P) + boff);
             kc = a.f.k[limb];
             kcsh = a.f.ksh[limb];
@@ -546,6 +552,11 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, const RowsArg &d,
                 x1 = mul_shoup(submod(c.y, x1, q), kc, kcsh, q);
                 if (e2) {
                     const ulonglong2 d = e2[i];
+                    x0 = addmod(x0, d.x, q);
+                    x1 = addmod(x1, d.y, q);
+                }
+                if (e3) {
+                    const ulonglong2 d = e3[i];
                     x0 = addmod(x0, d.x, q);
                     x1 = addmod(x1, d.y, q);
                 }
@@ -703,7 +714,7 @@ __global__ void __launch_bounds__(ClusterCfg<LOGN>::THREADS, MinBC<A>::v) ntt_cl
         __syncthreads();
         // epilogue on 16-byte vectors over this CTA's RR contiguous rows
         const long boff = limb * N + (long)rank * RR * G2;
-        const ulonglong2 *e1 = nullptr, *e2 = nullptr;
+        const ulonglong2 *e1 = nullptr, *e2 = nullptr, *e3 = nullptr;
         ulonglong2 *dst;
         u64 kc = 0, kcsh = 0;
         if (OUT == OUT_PLAIN) {
@@ -712,6 +723,8 @@ __global__ void __launch_bounds__(ClusterCfg<LOGN>::THREADS, MinBC<A>::v) ntt_cl
             e1 = reinterpret_cast<const ulonglong2 *>(a.f.e1.p + poly_off(a.f.e1.cs, a.f.e1.ps, poly) + boff);
             if (OUT == OUT_MODDOWN && (poly & 1) < a.f.e2_polys)
                 e2 = reinterpret_cast<const ulonglong2 *>(a.f.e2.p + poly_off(a.f.e2.cs, a.f.e2.ps, poly) + boff);
+            if (OUT == OUT_MODDOWN && a.f.e3.p)
+                e3 = reinterpret_cast<const ulonglong2 *>(a.f.e3.p + poly_off(a.f.e3.cs, a.f.e3.ps, poly) + boff);
             dst = reinterpret_cast<ulonglong2 *>(a.f.out.p + poly_off(a.f.out.cs, a.f.out.ps, poly) + boff);
             kc = a.f.k[limb];
             kcsh = a.f.ksh[limb];
@@ -730,6 +743,11 @@ __global__ void __launch_bounds__(ClusterCfg<LOGN>::THREADS, MinBC<A>::v) ntt_cl
                 x1 = mul_shoup(submod(c.y, x1, q), kc, kcsh, q);
                 if (e2) {
                     const ulonglong2 d = e2[i];
+                    x0 = addmod(x0, d.x, q);
+                    x1 = addmod(x1, d.y, q);
+                }
+                if (e3) {
+                    const ulonglong2 d = e3[i];
                     x0 = addmod(x0, d.x, q);
                     x1 = addmod(x1, d.y, q);
                 }

@@ -30,6 +30,9 @@ struct Val {
 
 }  // namespace
 
+#ifndef SECPE_FUSE_ROTADD
+#define SECPE_FUSE_ROTADD 1  // development switch
+#endif
 struct Ev {
     Ctx &c;
     const Keys &k;
@@ -59,6 +62,16 @@ struct Ev {
         Val out = fresh(x.level(), x.scale());
         ev_rotate(c, k, x.v, steps, out.v);
         c.log("ROT", x.level(), x.level(), x.scale(), std::to_string(galois_elt(c, steps)));
+        return out;
+    }
+    // y + Rot(y, steps): the addition fused into the rotation's final NTT epilogue (same integers as
+    // rot then add; the op log keeps both lines)
+    Val rot_add(const Val &y, int steps) {
+        if (!SECPE_FUSE_ROTADD || galois_elt(c, steps) == 1) return add(y, rot(y, steps));
+        Val out = fresh(y.level(), y.scale());
+        ev_rotate(c, k, y.v, steps, out.v, &y.v);
+        c.log("ROT", y.level(), y.level(), y.scale(), std::to_string(galois_elt(c, steps)));
+        c.log("ADD", y.level(), y.level(), y.scale(), "");
         return out;
     }
     Val mul_const(const Val &x, double cval, double St, int Lt) {
@@ -231,14 +244,14 @@ struct Ev {
     Val argmax(const Val &in, const Layout &lay, const SignCfg &cfg) {
         const int P = lay.prompts, K = lay.classes;
         Val y = in;
-        for (int t = 0; (1 << t) < P; t++) y = add(y, rot(y, K << t));
+        for (int t = 0; (1 << t) < P; t++) y = rot_add(y, K << t);
         std::vector<double> mask(c.N / 2, 0.0);
         for (int qi = 0; qi < lay.queries; qi++)
             for (int kk = 0; kk < K; kk++) mask[(size_t)qi * lay.block + kk] = 1.0 / P;
         y = mul_mask(y, mask, c.scale,
                      "argmax/" + std::to_string(lay.queries) + "/" + std::to_string(P) + "/" + std::to_string(K) + "/" +
                          std::to_string(lay.block));
-        y = add(y, rot(y, -K));
+        y = rot_add(y, -K);
         Val ydup = y;
         for (int i = 0; (1 << i) < K; i++) y = hom_max(rot(y, 1 << i), y, cfg);
         Val d = sub(ydup, y);
