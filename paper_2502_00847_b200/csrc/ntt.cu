@@ -187,9 +187,13 @@ struct FpA {
         return B(__dadd_rn(t, TWO52)) & ((1ULL << 52) - 1);
     }
     static __device__ __forceinline__ u64 out_fwd(u64 x, const PrimeC &P) { return canon(D(x), P); }
+    // mm's result already lies in [-0.75 q, 0.75 q]: one conditional add of q makes it canonical (no
+    // second quotient)
     static __device__ __forceinline__ u64 out_scaled(u64 x, u64 k, u64, const PrimeC &P) {
         const double kd = D(in(k, P)), kq = __dmul_rn(kd, P.qinv);
-        return canon(mm(D(x), kd, kq, P.qd), P);
+        double t = mm(D(x), kd, kq, P.qd);
+        if (t < 0) t = __dadd_rn(t, P.qd);
+        return B(__dadd_rn(t, TWO52)) & ((1ULL << 52) - 1);
     }
 };
 
