@@ -527,3 +527,40 @@ def test_keys_destroy_drops_captured_graphs(S):
         k3 = g.keygen(synth.KEY_SEED_BASE + 3, rot)
         del g
         del k3
+
+
+def test_argmax_degenerate_scores_bit_exact(S):
+    """Degenerate inputs of the method on the configs[4] circuit (2^12 ring): exact ties (Sign(0) = 0,
+    every tied slot ~1, PAPER.md:184 / reading R28), all-zero and all-one prompts, extreme one-hot
+    scores.  Ciphertext bit-exact vs the oracle; decrypted window within 2^-10 of the plaintext mirror."""
+    P = pair(S, "argmax_small")
+    prm, g = P.prm, P.gpu
+    lay = synth.LAYOUTS["argmax_small_k2"]
+    st = load_sign("sign_7_15_15.json")
+    nq, Pp, K = lay["queries"], lay["prompts"], lay["classes"]
+    rng = np.random.default_rng(77)
+    scores = rng.uniform(0, 1, (nq, Pp, K))
+    scores[0] = 0.5                      # exact tie
+    scores[1] = 0.0                      # all zero
+    scores[2] = 1.0                      # all one
+    scores[3, :, 0], scores[3, :, 1] = 1.0, 0.0
+    scores[4, :, 0], scores[4, :, 1] = 0.0, 1.0
+    scores[5, :4, :] = [0.9, 0.1]        # half the prompts vote each way: aggregated tie
+    scores[5, 4:, :] = [0.1, 0.9]
+    seed = synth.KEY_SEED_BASE + 7
+    steps = plan.argmax_rotations(lay)
+    ev = ckks.Oracle(prm)
+    ko, kg = ev.keygen(seed, steps), g.keygen(seed, steps)
+    ct = ev.encrypt(ko, plan.pack(scores, lay, prm.N // 2), prm.scale, 41)
+    out = g.enc_argmax(kg, P.up(ct), lay, st)
+    want = plan.argmax(ev, ko, ct, lay, st)
+    assert np.array_equal(P.down(out), want.data)
+    ref = plan.argmax(ckks.Mirror(prm), None, ckks.MirrorCt(plan.pack(scores, lay, prm.N // 2), prm.L, prm.scale),
+                      lay, st)
+    dec = g.decrypt(kg, out)
+    b = lay["block"]
+    for qi in range(nq):
+        assert np.abs(dec[qi * b: qi * b + K] - ref.v[qi * b: qi * b + K]).max() < 2 ** -10
+    for qi in (0, 1, 2, 5):              # ties: both window slots ~1
+        assert np.all(np.abs(dec[qi * b: qi * b + K] - 1.0) < 0.05)
+    assert S.labels(dec, lay)[3] == 0 and S.labels(dec, lay)[4] == 1
