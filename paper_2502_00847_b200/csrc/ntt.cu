@@ -32,6 +32,9 @@ namespace {
 #ifndef NTT_MINB_FP
 #define NTT_MINB_FP 4  // FP rows: 64 registers, no spills
 #endif
+#ifndef NTT_PDL
+#define NTT_PDL 1  // programmatic dependent launch of the NTT passes
+#endif
 #ifndef NTT_WAVE_PREFETCH
 #define NTT_WAVE_PREFETCH 1  // first forward pass: the next wave's input tiles prefetched into L2
                              // (isolated forward NTT 0.451 -> 0.420 us/limb; the same for the first
@@ -397,6 +400,9 @@ __global__ void __launch_bounds__(SC *(1 << (LOGN / 2 - RB)), MinB<A>::v) ntt_st
     __shared__ u64 sm[(1 << (LOGN / 2)) * SC];
     RowsArg d;
     int poly, limb, prime;
+#if NTT_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
 #if NTT_WAVE_PREFETCH
     if (!INV && IN == IN_PLAIN && a.wave > 0) {
         // the tile a CTA of the next wave will read: one 128-byte row segment per thread into L2
@@ -581,6 +587,9 @@ __global__ void __launch_bounds__(CT, MinB<A>::v) ntt_contig(PassArgs a) {
     __shared__ __align__(16) u64 sm[CF::CG * CF::PITCH];
     RowsArg d;
     int poly, limb, prime;
+#if NTT_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
 
     locate(a, blockIdx.y, d, poly, limb, prime);
     const PrimeC P = prime_consts(a.tab, prime);
@@ -844,6 +853,28 @@ void max_smem_carveout(K kern) {
     }
 }
 
+// Programmatic dependent launch (NTT_PDL): the kernel may be scheduled while its predecessor on the
+// stream drains; griddepcontrol.wait at its top blocks until the predecessor has completed and its
+// writes are visible, so only the launch latency and CTA rasterisation overlap the predecessor's tail.
+template <typename K>
+void launch_pdl(K kern, dim3 grid, dim3 block, cudaStream_t st, const PassArgs &a) {
+    if (!NTT_PDL) {
+        kern<<<grid, block, 0, st>>>(a);
+        return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a));
+}
+
 // CTAs of a kernel resident at once on the device (occupancy x SMs), cached per kernel
 template <typename K>
 int resident_ctas(K kern, int threads) {
@@ -865,7 +896,7 @@ void launch_strided_a(const PassArgs &a0, int n_polys, cudaStream_t st) {
     PassArgs a = a0;
     a.wave = resident_ctas(ntt_strided<LOGN, INV, IN, A>, SC * (1 << (S - RB)));
     dim3 grid((unsigned)((1L << (LOGN - S)) / SC), n_polys * a.nsub);
-    ntt_strided<LOGN, INV, IN, A><<<grid, SC * (1 << (S - RB)), 0, st>>>(a);
+    launch_pdl(ntt_strided<LOGN, INV, IN, A>, grid, dim3(SC * (1 << (S - RB))), st, a);
 }
 template <int LOGN, bool INV, int IO, class A>
 void launch_contig_a(const PassArgs &a0, int n_polys, cudaStream_t st) {
@@ -873,7 +904,7 @@ void launch_contig_a(const PassArgs &a0, int n_polys, cudaStream_t st) {
     max_smem_carveout(ntt_contig<LOGN, INV, IO, A>);
     const PassArgs &a = a0;
     dim3 grid((unsigned)((1L << (LOGN - CF::S)) / CF::CG), n_polys * a.nsub);
-    ntt_contig<LOGN, INV, IO, A><<<grid, CT, 0, st>>>(a);
+    launch_pdl(ntt_contig<LOGN, INV, IO, A>, grid, dim3(CT), st, a);
 }
 // one launch per run of consecutive limbs of the same prime class (bit i of tab.fp_mask: prime i < 2^46)
 inline bool limb_fp(const PassArgs &a, int limb) {
