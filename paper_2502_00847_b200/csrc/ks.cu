@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(TPB) modup_kernel(Tab tab, int logn, const u64
 // (beta <= 4); larger dnum uses the scalar ks_inner_kernel below.
 template <int MAXB>
 struct KsIn {
-    ulonglong2 x[MAXB], d0, d1, a0, a1, b0, b1, x0, x1, y0, y1, u0, u1, w0, w1;  // u, w: second product
+    ulonglong2 x[MAXB];
 };
 // Hoisted rotation (R29): the key inner product reads sigma_g(x) instead of x.  In the NTT domain
 // sigma_g is the permutation NTT(sigma_g a)[i] = NTT(a)[pi(i)], 2 brv(pi(i)) + 1 = g (2 brv(i) + 1) mod 2N;
@@ -113,42 +113,17 @@ __device__ __forceinline__ long gal_src(long k, int logn, u64 g, bool &swap) {
     return (long)(j & ~1u);
 }
 
-template <int MAXB, bool TEN>
+// digit j's value at (e, pair kx): the input itself for the digit containing e, else its ModUp
+template <int MAXB>
 __device__ __forceinline__ void ks_load(KsIn<MAXB> &in, int c, const u64 *__restrict__ d, long ds,
-                                        const u64 *__restrict__ ext, long exts, int e, int jd, int ne, int nl,
-                                        int beta, long N, long k, const TensorSrc &ten, long kx = -1,
-                                        bool swap = false) {
-    if (kx < 0) kx = k;
+                                        const u64 *__restrict__ ext, long exts, int e, int jd, int ne, int beta,
+                                        long N, long kx, bool swap) {
 #pragma unroll
     for (int j = 0; j < MAXB; j++)
-        if (j < beta && (!TEN || j != jd)) {
+        if (j < beta) {
             in.x[j] = ldv2((j == jd) ? d + c * ds + e * N + kx : ext + c * exts + ((long)j * ne + e) * N + kx);
             if (swap) in.x[j] = make_ulonglong2(in.x[j].y, in.x[j].x);
         }
-    if (TEN && e < nl) {
-        const long o = e * N + k;
-        in.a0 = ldv2(ten.a.p + c * ten.a.cs + o);
-        in.a1 = ldv2(ten.a.p + c * ten.a.cs + ten.a.ps + o);
-        in.b0 = ldv2(ten.b.p + c * ten.b.cs + o);
-        in.b1 = ldv2(ten.b.p + c * ten.b.cs + ten.b.ps + o);
-        if (ten.x.p) {
-            in.x0 = ldv2(ten.x.p + c * ten.x.cs + o);
-            in.x1 = ldv2(ten.x.p + c * ten.x.cs + ten.x.ps + o);
-        }
-        if (ten.x2.p) {
-            in.y0 = ldv2(ten.x2.p + c * ten.x2.cs + o);
-            in.y1 = ldv2(ten.x2.p + c * ten.x2.cs + ten.x2.ps + o);
-        }
-    }
-}
-// second product of the tensor (R13b): loaded where it is consumed (not prefetched: register budget)
-template <int MAXB>
-__device__ __forceinline__ void ks_load_p2(KsIn<MAXB> &in, int c, int e, long N, long k, const TensorSrc &ten) {
-    const long o = e * N + k;
-    in.u0 = ldv2(ten.a2.p + c * ten.a2.cs + o);
-    in.u1 = ldv2(ten.a2.p + c * ten.a2.cs + ten.a2.ps + o);
-    in.w0 = ldv2(ten.b2.p + c * ten.b2.cs + o);
-    in.w1 = ldv2(ten.b2.p + c * ten.b2.cs + ten.b2.ps + o);
 }
 
 // Exact-FP64 tensor for primes < 2^46 (the configs[4] chain): operands < 2^46 are exact doubles;
@@ -232,21 +207,19 @@ __device__ __forceinline__ void tensor1(u64 a0, u64 a1, u64 b0, u64 b1, bool lin
     }
 }
 
-#ifndef KS_TEN_MINB
-#define KS_TEN_MINB 2  // resident CTAs per SM the relinearise path's register allocation targets
-#endif
-template <int MAXB, bool TEN>
-__global__ void __launch_bounds__(TPB, TEN ? KS_TEN_MINB : 3) ks_inner_vec_kernel(Tab tab, int logn, const u64 *__restrict__ d, long ds,
-                                                           const u64 *__restrict__ ext, long exts,
-                                                           const u64 *__restrict__ key, int nq_total, int np,
-                                                           u64 *__restrict__ acc, long accs, int n_ct, int nl,
-                                                           int alpha, int beta, TensorSrc ten,
-                                                           const u64 *__restrict__ pmod, u64 galois) {
+// Plain key inner product (rotations): two coefficients per thread (16-byte vectors), the key words in
+// registers across the ciphertext batch, the next ciphertext's inputs double-buffered.
+template <int MAXB>
+__global__ void __launch_bounds__(TPB, 3) ks_inner_vec_kernel(Tab tab, int logn, const u64 *__restrict__ d, long ds,
+                                                            const u64 *__restrict__ ext, long exts,
+                                                            const u64 *__restrict__ key, int nq_total, int np,
+                                                            u64 *__restrict__ acc, long accs, int n_ct, int nl,
+                                                            int alpha, int beta, u64 galois) {
     const int e = blockIdx.y;
     const long N = 1L << logn;
     const long k = 2L * ((long)blockIdx.x * TPB + threadIdx.x);
     bool swap = false;
-    const long kx = (!TEN && galois > 1) ? gal_src(k, logn, galois, swap) : k;  // hoisted rotation gather
+    const long kx = galois > 1 ? gal_src(k, logn, galois, swap) : k;  // hoisted rotation gather
     const int ne = nl + np, nk = nq_total + np;
     const int pr = e < nl ? e : nq_total + (e - nl);
     const u64 q = tab.q[pr], r0 = tab.br0[pr], r1 = tab.br1[pr];
@@ -258,39 +231,10 @@ __global__ void __launch_bounds__(TPB, TEN ? KS_TEN_MINB : 3) ks_inner_vec_kerne
             ka[j] = ldv2(key + (((long)j * 2 + 1) * nk + pr) * N + k);
         }
     const int jd = e < nl ? e / alpha : -1;  // digit containing e (Q limbs only)
-    const bool qrow = TEN && e < nl;         // relinearise-and-rescale: x_b = acc_b + [P]_{q_e} d_b on Q limbs
-    const u64 pm = qrow ? pmod[e] : 0;
-    const bool lin = TEN && ten.x.p, lin2 = TEN && ten.x2.p, p2 = TEN && ten.a2.p;
-    const u64 cc = lin && e < nl ? ten.C.c[e] : 0, ccsh = lin && e < nl ? ten.C.csh[e] : 0;
-    const u64 c2 = lin2 && e < nl ? ten.C2.c[e] : 0, c2sh = lin2 && e < nl ? ten.C2.csh[e] : 0;
-    const double qd = TEN ? tab.qd[pr] : 0.0, qinv = TEN ? tab.qinv[pr] : 0.0;
-    // plain key switching double-buffers the next ciphertext's inputs; with the tensor formed on the fly
-    // the register budget goes to the tensor terms instead (single buffer)
     KsIn<MAXB> cur, nxt;
-    ks_load<MAXB, TEN>(cur, 0, d, ds, ext, exts, e, jd, ne, nl, beta, N, k, ten, kx, swap);
+    ks_load<MAXB>(cur, 0, d, ds, ext, exts, e, jd, ne, beta, N, kx, swap);
     for (int c = 0; c < n_ct; c++) {
-        if (!TEN && c + 1 < n_ct)
-            ks_load<MAXB, TEN>(nxt, c + 1, d, ds, ext, exts, e, jd, ne, nl, beta, N, k, ten, kx, swap);
-        if (qrow) {
-            u64 e0, e1, e2, f0, f1, f2;
-            if (p2) ks_load_p2<MAXB>(cur, c, e, N, k, ten);
-            if (q < (1ULL << 46)) {
-                tensor1_fp(cur.a0.x, cur.a1.x, cur.b0.x, cur.b1.x, lin, cur.x0.x, cur.x1.x, cc, lin2, cur.y0.x,
-                           cur.y1.x, c2, qd, qinv, e0, e1, e2, p2, cur.u0.x, cur.u1.x, cur.w0.x, cur.w1.x);
-                tensor1_fp(cur.a0.y, cur.a1.y, cur.b0.y, cur.b1.y, lin, cur.x0.y, cur.x1.y, cc, lin2, cur.y0.y,
-                           cur.y1.y, c2, qd, qinv, f0, f1, f2, p2, cur.u0.y, cur.u1.y, cur.w0.y, cur.w1.y);
-            } else {
-                tensor1(cur.a0.x, cur.a1.x, cur.b0.x, cur.b1.x, lin, cur.x0.x, cur.x1.x, cc, ccsh, lin2, cur.y0.x,
-                        cur.y1.x, c2, c2sh, q, r0, r1, e0, e1, e2, p2, cur.u0.x, cur.u1.x, cur.w0.x, cur.w1.x);
-                tensor1(cur.a0.y, cur.a1.y, cur.b0.y, cur.b1.y, lin, cur.x0.y, cur.x1.y, cc, ccsh, lin2, cur.y0.y,
-                        cur.y1.y, c2, c2sh, q, r0, r1, f0, f1, f2, p2, cur.u0.y, cur.u1.y, cur.w0.y, cur.w1.y);
-            }
-#pragma unroll
-            for (int j = 0; j < MAXB; j++)
-                if (j == jd) cur.x[j] = make_ulonglong2(e2, f2);
-            cur.d0 = make_ulonglong2(e0, f0);
-            cur.d1 = make_ulonglong2(e1, f1);
-        }
+        if (c + 1 < n_ct) ks_load<MAXB>(nxt, c + 1, d, ds, ext, exts, e, jd, ne, beta, N, kx, swap);
         U128 s0{0, 0}, s1{0, 0}, t0{0, 0}, t1{0, 0};  // (poly 0, poly 1) x (coefficient k, k + 1)
 #pragma unroll
         for (int j = 0; j < MAXB; j++)
@@ -300,28 +244,15 @@ __global__ void __launch_bounds__(TPB, TEN ? KS_TEN_MINB : 3) ks_inner_vec_kerne
                 mac_wide(s1, cur.x[j].x, ka[j].x);
                 mac_wide(t1, cur.x[j].y, ka[j].y);
             }
-        if (qrow) {
-            mac_wide(s0, cur.d0.x, pm);
-            mac_wide(t0, cur.d0.y, pm);
-            mac_wide(s1, cur.d1.x, pm);
-            mac_wide(t1, cur.d1.y, pm);
-        }
         stv2(acc + c * accs + (long)e * N + k, barrett128(s0, q, r0, r1), barrett128(t0, q, r0, r1));
         stv2(acc + c * accs + (long)(ne + e) * N + k, barrett128(s1, q, r0, r1), barrett128(t1, q, r0, r1));
-        if (TEN) {
-            if (c + 1 < n_ct) ks_load<MAXB, TEN>(cur, c + 1, d, ds, ext, exts, e, jd, ne, nl, beta, N, k, ten);
-        } else {
-            cur = nxt;
-        }
+        cur = nxt;
     }
 }
 
 // Relinearise-and-rescale key inner product, one coefficient per thread: about half the registers of the
 // two-coefficient kernel (which holds 16-byte vectors of every tensor input), so three CTAs fit per SM
 // without spills.  Same integers (tensor1_fp / tensor1, 128-bit MACs, one Barrett per output).
-#ifndef KS_TEN1
-#define KS_TEN1 1
-#endif
 #ifndef KS_TEN1_MINB
 #define KS_TEN1_MINB 3
 #endif
@@ -611,15 +542,12 @@ void k_ks_inner(const Tab &tab, int logn, const u64 *d, long ds, const u64 *ext,
     const TensorSrc &T = ten ? *ten : none;
 #define KSV(B_)                                                                                                   \
     do {                                                                                                          \
-        if (ten && KS_TEN1)                                                                                       \
+        if (ten)                                                                                                  \
             ks_inner_ten1_kernel<B_><<<g1, TPB, 0, st>>>(tab, logn, ext, exts, key, nq_total, np, acc, accs, n_ct, \
                                                          nl, alpha, beta, T, pmod);                               \
-        else if (ten)                                                                                             \
-            ks_inner_vec_kernel<B_, true><<<g2, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, \
-                                                              accs, n_ct, nl, alpha, beta, T, pmod, galois);      \
         else                                                                                                      \
-            ks_inner_vec_kernel<B_, false><<<g2, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np,     \
-                                                               acc, accs, n_ct, nl, alpha, beta, T, pmod, galois); \
+            ks_inner_vec_kernel<B_><<<g2, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, \
+                                                        n_ct, nl, alpha, beta, galois);                           \
     } while (0)
     if (beta == 1)
         KSV(1);

@@ -953,29 +953,16 @@ void launch_contig(const PassArgs &a0, int n_polys, cudaStream_t st) {
     });
 }
 
-// Optionally (SECPE_NTT_CHUNK = rows) both passes run over L2-sized chunks of polynomials (about that many rows,
-// ~56 MB at N = 2^16), chunk after chunk, so the intermediate between the passes is read back from L2.
-int chunk_rows() {
-    static int r = -1;
-    if (r < 0) {
-        const char *e = getenv("SECPE_NTT_CHUNK");
-        r = e ? atoi(e) : 0;  // measured: no gain from L2 residency, tail effects dominate; off
-    }
-    return r;
-}
-
 template <int LOGN>
 void run_chunk(const PassArgs &a, int rows, bool inverse, cudaStream_t st);
 
+// (an L2-chunked variant -- both passes over ~56 MB of rows at a time so the intermediate is re-read
+// from L2 -- was measured no faster and removed: profiles/r01_notes.md)
 template <int LOGN>
 void run(const PassArgs &a0, int n_polys, bool inverse, cudaStream_t st) {
-    const int cr = chunk_rows();
-    const int per = cr <= 0 ? n_polys : std::max(1, cr / std::max(1, a0.lm.nl));
-    for (int p0 = 0; p0 < n_polys; p0 += per) {
-        PassArgs a = a0;
-        a.poly0 = p0;
-        run_chunk<LOGN>(a, std::min(per, n_polys - p0), inverse, st);
-    }
+    PassArgs a = a0;
+    a.poly0 = 0;
+    run_chunk<LOGN>(a, n_polys, inverse, st);
 }
 
 // Tab::ntt_cluster (SECPE_NTT_CLUSTER at context creation): 0 = two-pass everywhere (default; the FP rows
