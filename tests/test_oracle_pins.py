@@ -306,6 +306,20 @@ def test_ops_against_slots(toy):
     f = ev.mul_ct(keys, a, b, toy.scale, a.level - 1, lin=(a, 0.25))
     assert f.level == a.level - 1 and f.scale == toy.scale
     assert np.abs(ev.decrypt(keys, f).real - (z1 * z2 + 0.25 * z1)).max() < tol
+    # two summed products with one relinearisation and rescale (R13b): a b + b b - 0.5 a
+    f2 = ev.mul_ct(keys, a, b, toy.scale, a.level - 1, lin=(a, -0.5), prod2=(b, b))
+    assert f2.level == a.level - 1 and f2.scale == toy.scale
+    assert np.abs(ev.decrypt(keys, f2).real - (z1 * z2 + z2 * z2 - 0.5 * z1)).max() < tol
+    # ... and its integers equal the relinearisation of the summed tensors written out (O-10 on d + d')
+    lv = a.level
+    d = ev.tensor(a, b)
+    dd = ev.tensor(b, b)
+    dsum = ((d.astype(object) + dd.astype(object)) % np.array(toy.primes[:lv + 1], dtype=object)[None, :, None]).astype(np.uint64)
+    C = ckks.round_half_away(-0.5 * ((toy.scale * float(toy.primes[lv])) / a.scale))
+    ca = ev.mul_int_raw(a, C)
+    dsum[:2] = ((dsum[:2].astype(object) + ca.astype(object)) % np.array(toy.primes[:lv + 1], dtype=object)[None, :, None]).astype(np.uint64)
+    manual = ev.rescale(ev.mul_relin(keys, a, b, dsum), toy.scale)
+    assert np.array_equal(manual.data, f2.data)
     for s in (1, -1, 3):
         r = ev.rotate_raw(keys, a, s)
         assert np.abs(ev.decrypt(keys, r).real - np.roll(z1, -s)).max() < tol
