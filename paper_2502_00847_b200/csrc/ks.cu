@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(TPB, 3) ks_inner_vec_kernel(Tab tab, int logn,
 // two-coefficient kernel (which holds 16-byte vectors of every tensor input), so three CTAs fit per SM
 // without spills.  Same integers (tensor1_fp / tensor1, 128-bit MACs, one Barrett per output).
 #ifndef KS_TEN1_MINB
-#define KS_TEN1_MINB 3
+#define KS_TEN1_MINB 3  // (two ciphertexts per iteration at 2 CTAs/SM measured 1.3 % slower)
 #endif
 template <int MAXB>
 __global__ void __launch_bounds__(TPB, KS_TEN1_MINB) ks_inner_ten1_kernel(Tab tab, int logn, const u64 *__restrict__ ext,
@@ -284,36 +284,48 @@ __global__ void __launch_bounds__(TPB, KS_TEN1_MINB) ks_inner_ten1_kernel(Tab ta
     const u64 c2 = lin2 && qrow ? ten.C2.c[e] : 0, c2sh = lin2 && qrow ? ten.C2.csh[e] : 0;
     const double qd = tab.qd[pr], qinv = tab.qinv[pr];
     const long o = e * N + k;
-    for (int c = 0; c < n_ct; c++) {
-        u64 x[MAXB];
+    struct In {
+        u64 x[MAXB], a0, a1, b0, b1, x0, x1, y0, y1, u0, u1, w0, w1;
+    };
+    auto load = [&](int c, In &in) {
 #pragma unroll
         for (int j = 0; j < MAXB; j++)
-            if (j < beta && j != jd) x[j] = ext[c * exts + ((long)j * ne + e) * N + k];
+            if (j < beta && j != jd) in.x[j] = ext[c * exts + ((long)j * ne + e) * N + k];
+        if (qrow) {
+            in.a0 = ten.a.p[c * ten.a.cs + o];
+            in.a1 = ten.a.p[c * ten.a.cs + ten.a.ps + o];
+            in.b0 = ten.b.p[c * ten.b.cs + o];
+            in.b1 = ten.b.p[c * ten.b.cs + ten.b.ps + o];
+            in.x0 = lin ? ten.x.p[c * ten.x.cs + o] : 0;
+            in.x1 = lin ? ten.x.p[c * ten.x.cs + ten.x.ps + o] : 0;
+            in.y0 = lin2 ? ten.x2.p[c * ten.x2.cs + o] : 0;
+            in.y1 = lin2 ? ten.x2.p[c * ten.x2.cs + ten.x2.ps + o] : 0;
+            in.u0 = p2 ? ten.a2.p[c * ten.a2.cs + o] : 0;
+            in.u1 = p2 ? ten.a2.p[c * ten.a2.cs + ten.a2.ps + o] : 0;
+            in.w0 = p2 ? ten.b2.p[c * ten.b2.cs + o] : 0;
+            in.w1 = p2 ? ten.b2.p[c * ten.b2.cs + ten.b2.ps + o] : 0;
+        }
+    };
+    auto compute = [&](int c, In &in) {
         u64 d0 = 0, d1 = 0;
         if (qrow) {
-            const u64 a0 = ten.a.p[c * ten.a.cs + o], a1 = ten.a.p[c * ten.a.cs + ten.a.ps + o];
-            const u64 b0 = ten.b.p[c * ten.b.cs + o], b1 = ten.b.p[c * ten.b.cs + ten.b.ps + o];
-            const u64 x0 = lin ? ten.x.p[c * ten.x.cs + o] : 0, x1 = lin ? ten.x.p[c * ten.x.cs + ten.x.ps + o] : 0;
-            const u64 y0 = lin2 ? ten.x2.p[c * ten.x2.cs + o] : 0;
-            const u64 y1 = lin2 ? ten.x2.p[c * ten.x2.cs + ten.x2.ps + o] : 0;
-            const u64 u0 = p2 ? ten.a2.p[c * ten.a2.cs + o] : 0, u1 = p2 ? ten.a2.p[c * ten.a2.cs + ten.a2.ps + o] : 0;
-            const u64 w0 = p2 ? ten.b2.p[c * ten.b2.cs + o] : 0, w1 = p2 ? ten.b2.p[c * ten.b2.cs + ten.b2.ps + o] : 0;
             u64 d2;
             if (q < (1ULL << 46))
-                tensor1_fp(a0, a1, b0, b1, lin, x0, x1, cc, lin2, y0, y1, c2, qd, qinv, d0, d1, d2, p2, u0, u1, w0, w1);
+                tensor1_fp(in.a0, in.a1, in.b0, in.b1, lin, in.x0, in.x1, cc, lin2, in.y0, in.y1, c2, qd, qinv, d0, d1,
+                           d2, p2, in.u0, in.u1, in.w0, in.w1);
             else
-                tensor1(a0, a1, b0, b1, lin, x0, x1, cc, ccsh, lin2, y0, y1, c2, c2sh, q, r0, r1, d0, d1, d2, p2, u0, u1,
-                        w0, w1);
+                tensor1(in.a0, in.a1, in.b0, in.b1, lin, in.x0, in.x1, cc, ccsh, lin2, in.y0, in.y1, c2, c2sh, q, r0, r1,
+                        d0, d1, d2, p2, in.u0, in.u1, in.w0, in.w1);
 #pragma unroll
             for (int j = 0; j < MAXB; j++)
-                if (j == jd) x[j] = d2;
+                if (j == jd) in.x[j] = d2;
         }
         U128 s0{0, 0}, s1{0, 0};
 #pragma unroll
         for (int j = 0; j < MAXB; j++)
             if (j < beta) {
-                mac_wide(s0, x[j], kb[j]);
-                mac_wide(s1, x[j], ka[j]);
+                mac_wide(s0, in.x[j], kb[j]);
+                mac_wide(s1, in.x[j], ka[j]);
             }
         if (qrow) {
             mac_wide(s0, d0, pm);
@@ -321,6 +333,11 @@ __global__ void __launch_bounds__(TPB, KS_TEN1_MINB) ks_inner_ten1_kernel(Tab ta
         }
         acc[c * accs + (long)e * N + k] = barrett128(s0, q, r0, r1);
         acc[c * accs + (long)(ne + e) * N + k] = barrett128(s1, q, r0, r1);
+    };
+    for (int c = 0; c < n_ct; c++) {
+        In A;
+        load(c, A);
+        compute(c, A);
     }
 }
 
