@@ -18,7 +18,10 @@
  *  - Device pointers (marked "dev") are caller-owned, 16-byte aligned, and must stay valid
  *    until the enqueued work completes.  Host pointers ("host") are read or written before
  *    the call returns.  The library never frees caller memory.  Context and keys are
- *    library-owned and immutable after creation (safe to share read-only across threads).
+ *    library-owned.  Keys are immutable after generation.  A context is NOT safe to use from
+ *    several threads at once: it keeps per-context caches (captured CUDA graphs, encoded masks,
+ *    auxiliary streams, host staging buffers), op counters, the op log and the profiler; use one
+ *    context per thread (each with its own keys), or serialise the calls.
  *  - Calls enqueue work on the context stream and return; secpe_decrypt*, secpe_key_export,
  *    secpe_sync and the host-returning calls synchronise.
  *  - Errors: a negative status; secpe_last_error() returns a thread-local message.
