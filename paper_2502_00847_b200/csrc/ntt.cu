@@ -15,9 +15,14 @@
 // instruction of a half-warp covers one full 128-byte line; contiguous passes read (forward) or
 // write (inverse) straight from registers in a lane-consecutive layout and stage the other side
 // through padded shared memory with 16-byte vectors.
-// Arithmetic: Harvey lazy butterflies with Shoup twiddles (all primes < 2^60); forward values stay
-// below 8q with a correction on every other stage only (bfly_ct), inverse in [0, 2q); the last pass
-// reduces to [0, q) (the inverse folds in N^{-1}).  Forward input may be any value < 4q.
+// Arithmetic (per row, by prime class): primes < 2^46 use exact-FP64 butterflies (FpA: signed integers
+// held exactly in doubles, TwoProduct remainders, no forward corrections); larger primes (< 2^60) use
+// Harvey lazy butterflies with Shoup twiddles (IntA: forward values below 8q with a correction on every
+// other stage, inverse in [0, 4q)).  The last pass reduces to [0, q) (the inverse folds in N^{-1} or a
+// caller-supplied per-limb factor).  Launch level: programmatic dependent launch, an L2 prefetch of the
+// next wave's tiles in the first forward pass and of the epilogue operands in the fused epilogues,
+// batched-segment launches of independent transforms (ntt_segments), and an optional single-pass
+// thread-block-cluster kernel (ntt_cluster, SECPE_NTT_CLUSTER).
 #include "common.cuh"
 #include "kernels.h"
 
