@@ -372,7 +372,7 @@ def run_secpe(a):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=16, help="ciphertexts per rank per step")
     ap.add_argument("--impl", default="secpe", choices=["secpe", "reference"])
