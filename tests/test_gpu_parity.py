@@ -564,3 +564,30 @@ def test_argmax_degenerate_scores_bit_exact(S):
     for qi in (0, 1, 2, 5):              # ties: both window slots ~1
         assert np.all(np.abs(dec[qi * b: qi * b + K] - 1.0) < 0.05)
     assert S.labels(dec, lay)[3] == 0 and S.labels(dec, lay)[4] == 1
+
+
+def test_argmax_k16_shape_bit_exact(S):
+    """BASELINE configs[4]'s K = 16 variant shape (P = 8 prompts x K = 16 classes in 128-slot blocks; QuickMax
+    with four iterations, rotations 1..8, aggregation steps 16..64) on a 30-prime 2^12 ring.  The (7,15,15)
+    Sign needs 60 levels here (reading R18), so the depth-4 toy Sign f1 o f1 stands in: ciphertext bit-exact
+    vs the oracle, decrypted within 2^-10 of the plaintext mirror, labels exact (top-1 gap >= 0.1)."""
+    P = pair(S, "argmax_small")
+    prm, g = P.prm, P.gpu
+    lay = dict(queries=16, prompts=8, classes=16, block=128)
+    st = load_sign("sign_f1_f1.json")
+    steps = plan.argmax_rotations(lay)
+    seed = synth.KEY_SEED_BASE + 9
+    ev = ckks.Oracle(prm)
+    ko, kg = ev.keygen(seed, steps), g.keygen(seed, steps)
+    scores = synth.toy_scores(4242, lay["queries"], lay["prompts"], lay["classes"])
+    z = plan.pack(scores, lay, prm.N // 2)
+    ct = ev.encrypt(ko, z, prm.scale, 17)
+    out = g.enc_argmax(kg, P.up(ct), lay, st)
+    want = plan.argmax(ev, ko, ct, lay, st)
+    assert np.array_equal(P.down(out), want.data) and out.level == want.level
+    ref = plan.argmax(ckks.Mirror(prm), None, ckks.MirrorCt(z, prm.L, prm.scale), lay, st)
+    dec = g.decrypt(kg, out)
+    b, K = lay["block"], lay["classes"]
+    for qi in range(lay["queries"]):
+        assert np.abs(dec[qi * b: qi * b + K] - ref.v[qi * b: qi * b + K]).max() < 2 ** -10
+    assert (S.labels(dec, lay) == plan.true_labels(scores)).all()
