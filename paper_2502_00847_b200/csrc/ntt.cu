@@ -141,7 +141,6 @@ struct IntA {
 // idle; the explicit _rn intrinsics keep the compiler from contracting or reassociating.
 constexpr double FP_MAGIC = 6755399441055744.0;  // 1.5 * 2^52
 constexpr double TWO52 = 4503599627370496.0;
-constexpr u64 FP_LIMIT = 1ULL << 46;
 struct FpA {
     static __device__ __forceinline__ double D(u64 b) { return __longlong_as_double((long long)b); }
     static __device__ __forceinline__ u64 B(double d) { return (u64)__double_as_longlong(d); }
