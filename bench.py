@@ -217,10 +217,12 @@ def run_secpe(a):
     B = a.batch
     L = ctx.L
     inp = ctx.new_ct(L, B)
+    all_scores = []
     for i in range(B):
         # rank r owns global ciphertexts [r B, (r + 1) B): the sharded job draws the single-rank job's inputs
         scores = synth.softmax_scores(shard.input_seed(5, rank * B + i), lay["queries"], lay["prompts"],
                                       lay["classes"])
+        all_scores.append(scores)
         z = secpe.pack(scores, lay, ctx.N // 2)
         m = ctx.encode(z, ctx.scale)
         c = secpe.Ct(inp.t[i:i + 1], L, ctx.scale)
@@ -299,6 +301,25 @@ def run_secpe(a):
     ms_e2e = shard.max_over_ranks(f0.elapsed_time(f1), device="cuda")
     e2e = shard.job_throughput(lay["queries"] * B * a.steps, ws, ms_e2e)
 
+    # client side, outside every timed region: decrypt the step's outputs and decode the labels (argmax
+    # over each query's K window slots, reading R19) against the plaintext argmax of the mean scores
+    n_ok = n_ok_margin = n_margin = n_q = 0
+    for i in range(B):
+        dec = ctx.decrypt(keys, out, i)
+        got = secpe.labels(dec, lay)
+        mean = all_scores[i].mean(axis=1)
+        srt = np.sort(mean, axis=1)
+        above = srt[:, -1] - srt[:, -2] >= 2.0 ** -7  # the Sign margin of the (7,15,15) design
+        truth = np.argmax(mean, axis=1)
+        n_q += len(truth)
+        n_ok += int((got == truth).sum())
+        n_ok_margin += int((got == truth)[above].sum())
+        n_margin += int(above.sum())
+    accuracy = {"queries": n_q, "labels_exact": n_ok / n_q, "labels_exact_above_margin": n_ok_margin / max(1, n_margin),
+                "in_margin_fraction": 1.0 - n_margin / n_q,
+                "note": "decrypted one-hot decoded by argmax over each query's window vs argmax of the plaintext "
+                        "mean scores; 'above margin' = top-1 gap >= 2^-7"}
+
     if rank != 0:
         if ws > 1:
             dist.barrier()
@@ -353,6 +374,7 @@ def run_secpe(a):
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h_in.numel() * 8),
                 "d2h_bytes_per_step": int(h_out.numel() * 8)},
         "gpu_launches": int(counts["launches"]),
+        "accuracy": accuracy,
         "op_counts_per_step": {k: v / a.steps for k, v in counts.items()},
         "clocks": clk,
     }
