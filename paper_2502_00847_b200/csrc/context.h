@@ -209,6 +209,8 @@ void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &
                           const CtView &out, const CtView *lin_x2 = nullptr, i64 C2 = 0, const CtView *a2 = nullptr,
                           const CtView *b2 = nullptr);
 void ev_lincomb(Ctx &c, const CtView &a, i64 C1, const CtView *b, i64 C2, const CtView &out);
+// rescale(C1 x1 + C2 x2) with the constant products fused into the rescale's transforms (x2 optional)
+void ev_rescale_lin(Ctx &c, const CtView &x1, i64 C1, const CtView *x2, i64 C2, const CtView &out);
 void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView &out,
                const CtView *add_after = nullptr);  // add_after: out = RotL(in) + add_after (fused)
 void ev_rotate_hoisted(Ctx &c, const Keys &k, const CtView &in, const int *steps, int n_steps, const CtView *outs);

@@ -148,6 +148,45 @@ void ev_rescale(Ctx &c, const CtView &in, const CtView &out) {
     c.prof_end(pa, 2, 8.0 * (double)n * (2 * (l + 1) + 2 * l) * N, n);
 }
 
+// Rescale of C1 x1 (+ C2 x2) with the constant products fused in (no intermediate ciphertext): the INTT
+// of the top limb forms C1 x1 + C2 x2 in its first pass, the rescale epilogue forms it per limb.  The
+// same integers as ev_mul_int / ev_lincomb followed by ev_rescale.
+void ev_rescale_lin(Ctx &c, const CtView &x1, i64 C1, const CtView *x2, i64 C2, const CtView &out) {
+    const size_t pa = c.prof_begin(2);
+    const int l = out.level + 1;
+    if (l < 1) throw SecpeError{-2, "rescale: no level left"};
+    if (x1.level < l || (x2 && x2->level < l)) throw SecpeError{-1, "rescale_lin: input level"};
+    const long N = c.N;
+    const int n = x1.n;
+    DevBuf last(2L * n * N, c.st), T(2L * n * l * N, c.st);
+    NttFusion fi;
+    fi.in_mode = 5;
+    fi.lin = x2 ? 2 : 1;
+    fi.C1 = C1;
+    fi.C2 = C2;
+    fi.src = CRows{x1.data + l * N, x1.stride, x1.ps};
+    if (x2) fi.src2 = CRows{x2->data + l * N, x2->stride, x2->ps};
+    ev_ntt(c, RowsArg{last.p, 2 * N, N}, 2 * n, LimbMap{1, 1, l, 0}, true, fi);
+    const LevelConsts &lc = c.level(l);
+    NttFusion ff;
+    ff.in_mode = 2;
+    ff.src = CRows{last.p, 2 * N, N};
+    ff.lp = l;
+    ff.half = lc.half.p;
+    ff.out_mode = 1;
+    ff.e1 = crows_of(x1);
+    ff.lin = fi.lin;
+    ff.C1 = C1;
+    ff.C2 = C2;
+    if (x2) ff.e1b = crows_of(*x2);
+    ff.out = rows_of(out);
+    ff.k = lc.qlinv.p;
+    ff.ksh = lc.qlinv_sh.p;
+    ev_ntt(c, RowsArg{T.p, 2L * l * N, (long)l * N}, 2 * n, qmap(l), false, ff);
+    c.cnt.rescale += n;
+    c.prof_end(pa, 2, 8.0 * (double)n * ((x2 ? 4 : 2) * (l + 1) + 2 * l) * N, n);
+}
+
 // ModUp + key inner product (R10): acc[ct][b][ne][N] over Q_level u P (NTT form).  d01/d01s: optional
 // tensor (d0, d1) rows whose [P] multiple is added on the Q limbs (R11b).
 // ten != nullptr: relinearisation of the tensor of ten->a, ten->b formed on the fly (d unused): the

@@ -27,6 +27,7 @@ struct LimbConst {
 //   in_mode  1 (inverse): the first pass reads polynomial P, limb i from src (copy fused in)
 //   in_mode  3 (inverse): the first pass reads src[P] * src2[P] mod q_i (tensor term fused in)
 //   in_mode  4 (inverse): ... src[P] * src2[P] + src3[P] * src4[P] mod q_i (two summed tensors, R13b)
+//   in_mode  5 (inverse): ... C1 src[P] + C2 src2[P] mod q_i (src2 when lin == 2; constant products, R9)
 //   in_mode  2 (forward): rescale broadcast (R12): the input of limb i is
 //            [floor(q_l/2)]_{q_i} - [[x + floor(q_l/2)]_{q_l}]_{q_i}, x = src row of polynomial P
 //            (one coefficient-form limb, prime lp); half[i] = [floor(q_l/2)]_{q_i}
@@ -44,6 +45,12 @@ struct NttFusion {
     CRows e1{nullptr, 0, 0}, e2{nullptr, 0, 0};
     int e2_polys = 0;
     CRows e3{nullptr, 0, 0};  // out_mode 2: optional addend of every polynomial (a rotation's "y + RotL(y)")
+    // constant products fused into a rescale (reading R9's MULC / LINC): the rescaled value is
+    // C1 src + C2 src2 instead of src (in_mode 5 on the INTT of the top limb), and the rescale epilogue
+    // (out_mode 1) uses C1 e1 + C2 e1b instead of e1; lin = number of terms (0: plain)
+    int lin = 0;
+    i64 C1 = 0, C2 = 0;
+    CRows e1b{nullptr, 0, 0};
     RowsArg out{nullptr, 0, 0};
     const u64 *k = nullptr, *ksh = nullptr;
 };

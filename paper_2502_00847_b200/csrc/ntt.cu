@@ -204,6 +204,12 @@ struct FpA {
     }
 };
 
+// [C]_q for a signed constant |C| < 2^62 (R9 constants), with the prime's Barrett constants
+__device__ __forceinline__ u64 smod_dev(i64 C, u64 q, u64 br0, u64 br1) {
+    const u64 m = barrett128(U128{(u64)(C < 0 ? -C : C), 0}, q, br0, br1);
+    return (C < 0 && m) ? q - m : m;
+}
+
 // local index of held value v of thread tau when the held bits start at LO
 template <int LO>
 __device__ __forceinline__ int held(int tau, int v) {
@@ -277,7 +283,7 @@ __device__ __forceinline__ void do_round(u64 (&v)[NV], int tau, int g, const ulo
 }
 
 // Fused prologue / epilogue modes (NttFusion in kernels.h)
-enum { IN_PLAIN = 0, IN_SRC = 1, IN_BCAST = 2, IN_MUL = 3, IN_MUL2 = 4 };
+enum { IN_PLAIN = 0, IN_SRC = 1, IN_BCAST = 2, IN_MUL = 3, IN_MUL2 = 4, IN_LIN = 5 };
 enum { OUT_PLAIN = 0, OUT_RESCALE = 1, OUT_MODDOWN = 2 };
 
 // A launch covers one row range of one buffer, or (nseg > 0, plain transforms only) up to MAXSEG
@@ -461,6 +467,10 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, const RowsArg &d,
         static_assert(CG * G * 8 == CT * 128, "one line per thread");
         const char *p1 = reinterpret_cast<const char *>(a.f.e1.p + poly_off(a.f.e1.cs, a.f.e1.ps, poly) + boff);
         asm volatile("prefetch.global.L2 [%0];" ::"l"(p1 + threadIdx.x * 128));
+        if (IO == OUT_RESCALE && a.f.lin == 2) {
+            const char *pb = reinterpret_cast<const char *>(a.f.e1b.p + poly_off(a.f.e1b.cs, a.f.e1b.ps, poly) + boff);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + threadIdx.x * 128));
+        }
         if (IO == OUT_MODDOWN && (poly & 1) < a.f.e2_polys) {
             const char *p2 = reinterpret_cast<const char *>(a.f.e2.p + poly_off(a.f.e2.cs, a.f.e2.ps, poly) + boff);
             asm volatile("prefetch.global.L2 [%0];" ::"l"(p2 + threadIdx.x * 128));
@@ -483,22 +493,33 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, const RowsArg &d,
 #pragma unroll
         for (int k = 0; k < NV; k++) v[k] = src[held<LO0>(tau, k)];  // intermediate representation
     } else {
-        const u64 *sp = (IO == IN_SRC || IO == IN_MUL || IO == IN_MUL2)
+        const u64 *sp = (IO == IN_SRC || IO == IN_MUL || IO == IN_MUL2 || IO == IN_LIN)
                             ? a.f.src.p + poly_off(a.f.src.cs, a.f.src.ps, poly) + boff
                             : blk;
         const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(sp);
         const ulonglong2 *src2 = nullptr, *src3 = nullptr, *src4 = nullptr;
-        if (IO == IN_MUL || IO == IN_MUL2)
+        if (IO == IN_MUL || IO == IN_MUL2 || (IO == IN_LIN && a.f.lin == 2))
             src2 = reinterpret_cast<const ulonglong2 *>(a.f.src2.p + poly_off(a.f.src2.cs, a.f.src2.ps, poly) + boff);
         if (IO == IN_MUL2) {
             src3 = reinterpret_cast<const ulonglong2 *>(a.f.src3.p + poly_off(a.f.src3.cs, a.f.src3.ps, poly) + boff);
             src4 = reinterpret_cast<const ulonglong2 *>(a.f.src4.p + poly_off(a.f.src4.cs, a.f.src4.ps, poly) + boff);
         }
         const u64 br0 = a.tab.br0[prime], br1 = a.tab.br1[prime];
+        const u64 lc1 = IO == IN_LIN ? smod_dev(a.f.C1, q, br0, br1) : 0;
+        const u64 lc2 = IO == IN_LIN && a.f.lin == 2 ? smod_dev(a.f.C2, q, br0, br1) : 0;
 #pragma unroll 4
         for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
             ulonglong2 x = src[i];
-            if (IO == IN_MUL) {
+            if (IO == IN_LIN) {
+                U128 t0 = mul_wide(x.x, lc1), t1 = mul_wide(x.y, lc1);
+                if (src2) {
+                    const ulonglong2 y = src2[i];
+                    mac_wide(t0, y.x, lc2);
+                    mac_wide(t1, y.y, lc2);
+                }
+                x.x = barrett128(t0, q, br0, br1);
+                x.y = barrett128(t1, q, br0, br1);
+            } else if (IO == IN_MUL) {
                 const ulonglong2 y = src2[i];
                 x.x = mulmod(x.x, y.x, q, br0, br1);
                 x.y = mulmod(x.y, y.y, q, br0, br1);
@@ -534,14 +555,23 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, const RowsArg &d,
         for (int k = 0; k < NV; k++) smg[padr(held<LO1>(tau, k))] = v[k];
         __syncthreads();
         // epilogue on 16-byte vectors; element e of the tile is at boff + e in its polynomial
-        const ulonglong2 *e1 = nullptr, *e2 = nullptr, *e3 = nullptr;
+        const ulonglong2 *e1 = nullptr, *e2 = nullptr, *e3 = nullptr, *e1b = nullptr;
         ulonglong2 *dst;
-        u64 kc = 0, kcsh = 0;
+        u64 kc = 0, kcsh = 0, lc1 = 0, lc2 = 0, br0e = 0, br1e = 0;
         if (IO == OUT_PLAIN) {
             dst = reinterpret_cast<ulonglong2 *>(blk);
         } else {
             const int P = poly;
             e1 = reinterpret_cast<const ulonglong2 *>(a.f.e1.p + poly_off(a.f.e1.cs, a.f.e1.ps, P) + boff);
+            if (IO == OUT_RESCALE && a.f.lin) {
+                br0e = a.tab.br0[prime];
+                br1e = a.tab.br1[prime];
+                lc1 = smod_dev(a.f.C1, q, br0e, br1e);
+                if (a.f.lin == 2) {
+                    lc2 = smod_dev(a.f.C2, q, br0e, br1e);
+                    e1b = reinterpret_cast<const ulonglong2 *>(a.f.e1b.p + poly_off(a.f.e1b.cs, a.f.e1b.ps, P) + boff);
+                }
+            }
             if (IO == OUT_MODDOWN && (P & 1) < a.f.e2_polys)
                 e2 = reinterpret_cast<const ulonglong2 *>(a.f.e2.p + poly_off(a.f.e2.cs, a.f.e2.ps, P) + boff);
             if (IO == OUT_MODDOWN && a.f.e3.p)
@@ -555,8 +585,18 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, const RowsArg &d,
             const int e = 2 * i, gg = e / G, r = e % G;
             u64 x0 = sm[gg * PITCH + padr(r)], x1 = sm[gg * PITCH + padr(r + 1)];
             if (IO == OUT_RESCALE) {
-                // (c_i + NTT(T)_i) * q_l^{-1}
-                const ulonglong2 c = e1[i];
+                // (c_i + NTT(T)_i) * q_l^{-1};  c_i = C1 e1_i (+ C2 e1b_i) for a fused constant product
+                ulonglong2 c = e1[i];
+                if (a.f.lin) {
+                    U128 t0 = mul_wide(c.x, lc1), t1 = mul_wide(c.y, lc1);
+                    if (e1b) {
+                        const ulonglong2 y = e1b[i];
+                        mac_wide(t0, y.x, lc2);
+                        mac_wide(t1, y.y, lc2);
+                    }
+                    c.x = barrett128(t0, q, br0e, br1e);
+                    c.y = barrett128(t1, q, br0e, br1e);
+                }
                 x0 = mul_shoup(addmod(c.x, x0, q), kc, kcsh, q);
                 x1 = mul_shoup(addmod(c.y, x1, q), kc, kcsh, q);
             } else if (IO == OUT_MODDOWN) {
@@ -1033,7 +1073,7 @@ template <int LOGN>
 void run_chunk(const PassArgs &a, int rows, bool inverse, cudaStream_t st) {
     const NttFusion &f = a.f;
     if constexpr (LOGN == 16) {
-        if (cluster_mode(a) > 0) {
+        if (cluster_mode(a) > 0 && !f.lin) {  // (fused constant products: two-pass kernels only)
             if (!inverse) {
                 const bool bc = f.in_mode == IN_BCAST;
                 if (f.out_mode == OUT_RESCALE)
@@ -1052,6 +1092,8 @@ void run_chunk(const PassArgs &a, int rows, bool inverse, cudaStream_t st) {
                     launch_cluster_or_split<LOGN, true, IN_MUL, OUT_PLAIN>(a, rows, st);
                 else if (f.in_mode == IN_MUL2)
                     launch_cluster_or_split<LOGN, true, IN_MUL2, OUT_PLAIN>(a, rows, st);
+                else if (f.in_mode == IN_LIN)
+                    launch_cluster_or_split<LOGN, true, IN_LIN, OUT_PLAIN>(a, rows, st);
                 else
                     launch_cluster_or_split<LOGN, true, IN_PLAIN, OUT_PLAIN>(a, rows, st);
             }
@@ -1078,6 +1120,8 @@ void run_chunk(const PassArgs &a, int rows, bool inverse, cudaStream_t st) {
             launch_contig<LOGN, true, IN_MUL>(a, rows, st);
         else if (f.in_mode == IN_MUL2)
             launch_contig<LOGN, true, IN_MUL2>(a, rows, st);
+        else if (f.in_mode == IN_LIN)
+            launch_contig<LOGN, true, IN_LIN>(a, rows, st);
         else
             launch_contig<LOGN, true, IN_PLAIN>(a, rows, st);
         LAUNCH_CHECK();
@@ -1196,7 +1240,8 @@ void ntt_forward(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm
 void ntt_inverse(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
                  const NttFusion &f) {
     if (n_polys <= 0 || lm.nl <= 0) return;
-    if ((f.in_mode != IN_PLAIN && f.in_mode != IN_SRC && f.in_mode != IN_MUL && f.in_mode != IN_MUL2) ||
+    if ((f.in_mode != IN_PLAIN && f.in_mode != IN_SRC && f.in_mode != IN_MUL && f.in_mode != IN_MUL2 &&
+         f.in_mode != IN_LIN) ||
         f.out_mode != OUT_PLAIN)
         throw SecpeError{-1, "ntt_inverse: bad fusion mode"};
     dispatch(logn, PassArgs{data, lm, tab, f, 0, lm.nl, 0}, n_polys, true, st);

@@ -30,6 +30,9 @@ struct Val {
 
 }  // namespace
 
+#ifndef SECPE_FUSE_LIN
+#define SECPE_FUSE_LIN 1  // development switch: constant products fused into their rescale
+#endif
 #ifndef SECPE_FUSE_ROTADD
 #define SECPE_FUSE_ROTADD 1  // development switch
 #endif
@@ -82,10 +85,14 @@ struct Ev {
         const double Cd = round_half_away(cval * dc);
         if (!(std::fabs(Cd) < 4611686018427387904.0)) throw SecpeError{-6, "constant exceeds 2^62"};
         const i64 C = (i64)Cd;
-        Val tmp = fresh(lv, x.scale() * dc);
-        ev_mul_int(c, xd.v, C, tmp.v);
         Val out = fresh(Lt, St);
-        ev_rescale(c, tmp.v, out.v);
+        if (SECPE_FUSE_LIN) {
+            ev_rescale_lin(c, xd.v, C, nullptr, 0, out.v);  // C x rescaled, the product fused in
+        } else {
+            Val tmp = fresh(lv, x.scale() * dc);
+            ev_mul_int(c, xd.v, C, tmp.v);
+            ev_rescale(c, tmp.v, out.v);
+        }
         c.cnt.mulconst += n;
         c.log("MULC", lv, Lt, St, std::to_string((long long)C));
         return out;
@@ -139,10 +146,14 @@ struct Ev {
             xs.push_back(drop(*t.first, lv));
             Cs.push_back(lin_const(t.second, St, lv, t.first->scale()));
         }
-        Val tmp = fresh(lv, St * q(lv));
-        ev_lincomb(c, xs[0].v, Cs[0], xs.size() > 1 ? &xs[1].v : nullptr, xs.size() > 1 ? Cs[1] : 0, tmp.v);
         Val out = fresh(Lt, St);
-        ev_rescale(c, tmp.v, out.v);
+        if (SECPE_FUSE_LIN) {
+            ev_rescale_lin(c, xs[0].v, Cs[0], xs.size() > 1 ? &xs[1].v : nullptr, xs.size() > 1 ? Cs[1] : 0, out.v);
+        } else {
+            Val tmp = fresh(lv, St * q(lv));
+            ev_lincomb(c, xs[0].v, Cs[0], xs.size() > 1 ? &xs[1].v : nullptr, xs.size() > 1 ? Cs[1] : 0, tmp.v);
+            ev_rescale(c, tmp.v, out.v);
+        }
         c.cnt.mulconst += n;
         c.log("LINC", lv, Lt, St, join(Cs));
         return out;
