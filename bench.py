@@ -283,7 +283,7 @@ def run_secpe(a):
     h_in = inp.t.cpu().pin_memory()
     h_out = torch.empty(out.t.shape, dtype=torch.uint64).pin_memory()
     for _ in range(max(4, a.warmup)):  # both staging slots captured and replayed once
-        ctx.enc_argmax_host(keys, h_in, L, ctx.scale, lay, st, h_out=h_out)
+        ctx.enc_argmax_host(keys, h_in, L, ctx.scale, lay, st, h_out=h_out, chunk=B)
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
@@ -292,7 +292,7 @@ def run_secpe(a):
     t_host = time.perf_counter()
     f0.record(stream)
     for i in range(a.steps):
-        ctx.enc_argmax_host(keys, h_in, L, ctx.scale, lay, st, h_out=h_out)
+        ctx.enc_argmax_host(keys, h_in, L, ctx.scale, lay, st, h_out=h_out, chunk=B)
         fe[i + 1].record(stream)
     t_host = time.perf_counter() - t_host
     torch.cuda.synchronize()

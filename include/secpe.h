@@ -223,7 +223,7 @@ int secpe_enc_argmax(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in,
  * h_in: uint64[n_in][2][level+1][N] (ciphertext i at h_in + i * secpe_ct_bytes(level) / 8, all at
  * `level` and `scale`); h_out: uint64[n_in][2][out_level+1][N], out_level / out_scale as
  * secpe_argmax_info reports (written to *out_level / *out_scale when non-null).  The batch runs
- * in chunks of `chunk` ciphertexts (<= 0: 8) through two device staging slots owned by the
+ * in chunks of `chunk` ciphertexts (<= 0: 16) through two device staging slots owned by the
  * context: the host-to-device copy of a chunk runs on a context-owned copy stream while the
  * previous chunk (possibly of the previous call) computes; each result is copied back on the
  * context stream.  Pinned host memory gives overlapped transfers (pageable memory is correct

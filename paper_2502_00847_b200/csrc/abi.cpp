@@ -628,7 +628,7 @@ int secpe_enc_argmax_host(secpe_ctx *ctx, const secpe_keys *keys, const uint64_t
         SignCfg sc = sign_cfg(cfg);
         const int ol = level - argmax_depth(lay, sc);
         REQUIRE(ol >= 0, SECPE_ELEVEL, "not enough levels for the argmax circuit");
-        if (chunk <= 0) chunk = 8;
+        if (chunk <= 0) chunk = 16;  // (16 ciphertexts per launch sequence: the measured sweet spot)
         chunk = std::min(chunk, n_in);
         const long cw = c.ct_words(level), ow = c.ct_words(ol);
         Ctx::HostPipe &hp = c.pipe;
