@@ -146,8 +146,10 @@ int secpe_decrypt(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *ct, do
                   size_t n);
 
 /* ---- primitives (server; all device buffers) ---------------------------------------------- */
-/* In-place forward / inverse negacyclic NTT of polys dev uint64[n_polys][n_limbs][N];
- * limb l uses prime index first_prime + l of the chain q_0..q_L, p_0..p_{k-1}. */
+/* In-place forward / inverse negacyclic NTT of polys dev uint64[n_polys][n_limbs][N] (R4; implied by
+ * PAPER.md:92, arithmetic in R_Q); limb l uses prime index first_prime + l of the chain q_0..q_L,
+ * p_0..p_{k-1}; inputs canonical residues, outputs canonical.  n_polys = 0 is a no-op (polys may be
+ * null).  SECPE_EINVAL: null ctx, negative n_polys, or a limb range outside the chain. */
 int secpe_ntt(secpe_ctx *ctx, uint64_t *polys, int32_t n_polys, int32_t first_prime, int32_t n_limbs);
 int secpe_intt(secpe_ctx *ctx, uint64_t *polys, int32_t n_polys, int32_t first_prime, int32_t n_limbs);
 

@@ -301,7 +301,7 @@ int secpe_decrypt(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *ct, do
 
 static int ntt_common(secpe_ctx *ctx, uint64_t *polys, int32_t n_polys, int32_t first, int32_t n_limbs, bool inv) {
     return guard([&] {
-        REQUIRE(ctx && polys, SECPE_EINVAL, "null argument");
+        REQUIRE(ctx && (polys || n_polys == 0), SECPE_EINVAL, "null argument");
         Ctx &c = ctx->c;
         REQUIRE(n_polys >= 0 && n_limbs >= 1 && first >= 0 && first + n_limbs <= c.nprimes(), SECPE_EINVAL,
                 "limb range out of the prime chain");

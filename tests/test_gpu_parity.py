@@ -591,3 +591,21 @@ def test_argmax_k16_shape_bit_exact(S):
     for qi in range(lay["queries"]):
         assert np.abs(dec[qi * b: qi * b + K] - ref.v[qi * b: qi * b + K]).max() < 2 ** -10
     assert (S.labels(dec, lay) == plan.true_labels(scores)).all()
+
+
+def test_empty_inputs(S):
+    """Empty batches: a zero-polynomial NTT is a no-op; an empty argmax batch or step list is SECPE_EINVAL."""
+    import ctypes
+    P = pair(S, "toy")
+    g, prm = P.gpu, P.prm
+    t = torch.zeros((0, 8, prm.N), dtype=torch.uint64, device="cuda")
+    g.ntt(t, 0, 8)
+    lay = dict(synth.LAYOUTS["toy"], queries=1)
+    st = load_sign("sign_f1_f1.json")
+    kg = g.keygen(synth.KEY_SEED_BASE + 7, plan.argmax_rotations(lay))
+    cfg, ly = S.sign_cfg(st), S.layout(lay)
+    rc = S.lib().secpe_enc_argmax(g.h, kg.h, None, 0, ctypes.byref(ly), ctypes.byref(cfg), None)
+    assert rc == -1
+    a = g.encrypt(kg, synth.uniform_slots(1, prm.N // 2), prm.L, prm.scale, 1)
+    with pytest.raises(S.SecpeError):
+        g.rotate_hoisted(kg, a, [])
