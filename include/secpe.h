@@ -217,8 +217,13 @@ int secpe_argmax_info(secpe_ctx *ctx, const secpe_layout *layout, const secpe_si
  * aggregate prompts by rotate-and-sum, mask/normalise (Eq. 5), duplicate, QuickMax with
  * Eq. 6, Sign(y - y_max) + 1 (Eq. 2).  in: host[n_in] ciphertexts (same level and scale);
  * out: host[n_in], out[i].data sized for the level secpe_argmax_info reports.  The batch is
- * evaluated together so every key is read once per op for all n_in ciphertexts.
- * No secret key is taken or needed. */
+ * evaluated together so every key is read once per op for all n_in ciphertexts, as up to two
+ * concurrent sub-batches on context-owned streams.  On a non-default context stream the call is
+ * captured as a CUDA graph the second time the same (buffers, level, layout, Sign, keys) are seen and
+ * replayed from the third time on (at most 16 graphs per context, oldest evicted; secpe_keys_destroy
+ * drops the graphs of its keys).  No secret key is taken or needed.
+ * Errors: SECPE_EINVAL (null arguments, n_in < 1, mixed levels/scales), SECPE_ELAYOUT, SECPE_ELEVEL
+ * (not enough levels, e.g. K = 16 with the (7,15,15) Sign at L = 29), SECPE_ENOKEY, SECPE_ECUDA. */
 int secpe_enc_argmax(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n_in,
                      const secpe_layout *layout, const secpe_sign_cfg *cfg, secpe_ct *out);
 /* secpe_enc_argmax on ciphertexts held in HOST memory (the end-to-end server call).

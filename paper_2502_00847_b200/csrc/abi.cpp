@@ -542,6 +542,21 @@ static void argmax_views(Ctx &c, const secpe_keys *keys, const CtView &vin, cons
     }
     run_argmax(c, *keys->k, vin, lay, sc, vout);
     if (!graphable) return;
+    // capture only buffers seen twice (a caller allocating fresh buffers every call would otherwise pay a
+    // capture per call and grow the cache); keep at most kMaxGraphs graphs
+    if (++c.graph_seen[key] < 2) {
+        if (c.graph_seen.size() > 4 * Ctx::kMaxGraphs) c.graph_seen.clear();
+        return;
+    }
+    if ((int)c.graphs.size() >= Ctx::kMaxGraphs && !c.graph_order.empty()) {
+        CUDA_CHECK(cudaStreamSynchronize(c.st));  // the evicted graph may still be running
+        auto old = c.graphs.find(c.graph_order.front());
+        if (old != c.graphs.end()) {
+            if (old->second.exec) cudaGraphExecDestroy(old->second.exec);
+            c.graphs.erase(old);
+        }
+        c.graph_order.erase(c.graph_order.begin());
+    }
     const Counters before = c.cnt;
     cudaGraph_t graph;
     CUDA_CHECK(cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal));
@@ -568,6 +583,8 @@ static void argmax_views(Ctx &c, const secpe_keys *keys, const CtView &vin, cons
     c.cnt = before;  // the capture executed nothing
     G.out_scale = vout.scale;
     c.graphs[key] = G;
+    c.graph_order.push_back(key);
+    c.graph_seen.erase(key);
 }
 
 int secpe_enc_argmax(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n_in,

@@ -344,6 +344,7 @@ void Ctx::drop_graphs(const void *keys) {
     for (auto it = graphs.begin(); it != graphs.end();) {
         if (it->second.keys == keys) {
             if (it->second.exec) cudaGraphExecDestroy(it->second.exec);
+            graph_order.erase(std::remove(graph_order.begin(), graph_order.end(), it->first), graph_order.end());
             it = graphs.erase(it);
         } else {
             ++it;

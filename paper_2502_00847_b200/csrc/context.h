@@ -141,6 +141,9 @@ struct Ctx {
         const void *keys = nullptr;  // evaluation keys whose device memory the graph's kernels read
     };
     std::map<std::string, Graph> graphs;
+    std::map<std::string, int> graph_seen;  // eager calls per key: capture on the second sighting only
+    std::vector<std::string> graph_order;   // capture order (the oldest graph is evicted beyond kMaxGraphs)
+    static constexpr int kMaxGraphs = 16;
     std::set<Keys *> live_keys;          // keys generated on this context (owner back-pointers)
     void drop_graphs(const void *keys);  // destroy every graph that reads these keys
     bool use_graphs = true;
