@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
             if (s < G.ns) pre[u] = src[(long)s * N + k0 + srow];
         }
     };
+    pdl_wait();  // TMEM, constants and the B matrix above do not depend on the previous kernel
     if ((int)blockIdx.x < ntiles) fetch(blockIdx.x);
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
@@ -281,6 +282,6 @@ void k_bconv_tc(const TcArgs &a, int n_polys, cudaStream_t st) {
         if (tiles_per_cta < 1) tiles_per_cta = 1;
     }
     const dim3 grid((ntiles + tiles_per_cta - 1) / tiles_per_cta, n_polys);
-    bconv_tc_kernel<<<grid, TC_THREADS, tc_smem_bytes(), st>>>(a);
+    launch_pdl_k(bconv_tc_kernel, grid, dim3(TC_THREADS), tc_smem_bytes(), st, a);
     LAUNCH_CHECK();
 }

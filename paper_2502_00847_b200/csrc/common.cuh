@@ -11,6 +11,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 typedef uint64_t u64;
@@ -104,3 +105,25 @@ void set_error(const std::string &m);
                                      __FILE__ + ":" + std::to_string(__LINE__)};            \
     } while (0)
 #define LAUNCH_CHECK() CUDA_CHECK(cudaGetLastError())
+
+#ifndef SECPE_PDL
+#define SECPE_PDL 1  // development switch
+#endif
+// Programmatic dependent launch: the kernel may be scheduled while its stream predecessor drains; it
+// calls pdl_wait() before touching the predecessor's outputs (setup that reads only constants, keys or
+// tables can come first).  Without the launch attribute pdl_wait() is a no-op.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+void launch_pdl_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = SECPE_PDL ? 1 : 0;
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}

@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(TPB, 3) ks_inner_vec_kernel(Tab tab, int logn,
             ka[j] = ldv2(key + (((long)j * 2 + 1) * nk + pr) * N + k);
         }
     const int jd = e < nl ? e / alpha : -1;  // digit containing e (Q limbs only)
+    pdl_wait();
     KsIn<MAXB> cur, nxt;
     ks_load<MAXB>(cur, 0, d, ds, ext, exts, e, jd, ne, beta, N, kx, swap);
     for (int c = 0; c < n_ct; c++) {
@@ -279,6 +280,7 @@ __global__ void __launch_bounds__(TPB, KS_TEN1_MINB) ks_inner_ten1_kernel(Tab ta
     const int jd = e < nl ? e / alpha : -1;
     const bool qrow = e < nl;
     const u64 pm = qrow ? pmod[e] : 0;
+    pdl_wait();  // the key words above are not produced by the previous kernel
     const bool lin = ten.x.p != nullptr, lin2 = ten.x2.p != nullptr, p2 = ten.a2.p != nullptr;
     const u64 cc = lin && qrow ? ten.C.c[e] : 0, ccsh = lin && qrow ? ten.C.csh[e] : 0;
     const u64 c2 = lin2 && qrow ? ten.C2.c[e] : 0, c2sh = lin2 && qrow ? ten.C2.csh[e] : 0;
@@ -560,11 +562,11 @@ void k_ks_inner(const Tab &tab, int logn, const u64 *d, long ds, const u64 *ext,
 #define KSV(B_)                                                                                                   \
     do {                                                                                                          \
         if (ten)                                                                                                  \
-            ks_inner_ten1_kernel<B_><<<g1, TPB, 0, st>>>(tab, logn, ext, exts, key, nq_total, np, acc, accs, n_ct, \
-                                                         nl, alpha, beta, T, pmod);                               \
+            launch_pdl_k(ks_inner_ten1_kernel<B_>, g1, dim3(TPB), 0, st, tab, logn, ext, exts, key, nq_total, np, \
+                         acc, accs, n_ct, nl, alpha, beta, T, pmod);                                              \
         else                                                                                                      \
-            ks_inner_vec_kernel<B_><<<g2, TPB, 0, st>>>(tab, logn, d, ds, ext, exts, key, nq_total, np, acc, accs, \
-                                                        n_ct, nl, alpha, beta, galois);                           \
+            launch_pdl_k(ks_inner_vec_kernel<B_>, g2, dim3(TPB), 0, st, tab, logn, d, ds, ext, exts, key, nq_total, \
+                         np, acc, accs, n_ct, nl, alpha, beta, galois);                                           \
     } while (0)
     if (beta == 1)
         KSV(1);

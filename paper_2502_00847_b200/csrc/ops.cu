@@ -130,6 +130,7 @@ __device__ __forceinline__ unsigned brv_bits(unsigned x, int bits) { return __br
 
 // out[i] = in[i'] with 2 brv(i') + 1 = g (2 brv(i) + 1) mod 2N
 __global__ void automorph_kernel(int logn, CRows a, RowsArg out, int nl, u64 g) {
+    pdl_wait();
     const int poly = blockIdx.y / nl, limb = blockIdx.y % nl;
     const long off = (long)limb << logn;
     const unsigned mask2n = (2u << logn) - 1;
@@ -183,6 +184,6 @@ void k_tensor(const Tab &tab, int logn, CRows a, CRows b, u64 *d, long ds, int n
     LAUNCH_CHECK();
 }
 void k_automorph(int logn, CRows a, RowsArg out, int n_polys, int nl, u64 galois, cudaStream_t st) {
-    automorph_kernel<<<grid_rows(logn, n_polys * nl), TPB, 0, st>>>(logn, a, out, nl, galois);
+    launch_pdl_k(automorph_kernel, grid_rows(logn, n_polys * nl), dim3(TPB), 0, st, logn, a, out, nl, galois);
     LAUNCH_CHECK();
 }
