@@ -371,6 +371,7 @@ def run_secpe(a):
                      "keyswitch": {"achieved": ks_ach, "frac": ks_ach / peak, "share_of_step": ks["ms"] / ms_prof,
                                    "unit": "GB/s"},
                      "rescale_share_of_step": prof["rescale"]["ms"] / ms_prof},
+        "stage_share_of_step": {k[6:]: v["ms"] / ms_prof for k, v in prof.items() if k.startswith("stage_")},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h_in.numel() * 8),
                 "d2h_bytes_per_step": int(h_out.numel() * 8)},
         "gpu_launches": int(counts["launches"]),

@@ -253,7 +253,9 @@ int secpe_oplog_clear(secpe_ctx *ctx);
  * on integer rows): out[3k] total ms, out[3k+1] algorithmic bytes (NTT: 16 N per limb transform,
  * split evenly over its passes; key switch: (input + output limbs) per ciphertext + key once per
  * batch; rescale: 2(l+1) + 2l limbs per ciphertext), out[3k+2] units (limb transforms per launch,
- * summed / ciphertexts).  Returns SECPE_EINVAL when n_out < 12. */
+ * summed / ciphertexts).  With n_out >= 27 also the argmax circuit stages as kinds 4..8 (H1
+ * aggregation, H2 mask, H3 duplication, H4 QuickMax incl. its Sign, H6 final Sign + 1; ms in
+ * out[3k], ciphertexts in out[3k+2]).  Returns SECPE_EINVAL when n_out < 12. */
 int secpe_profile_begin(secpe_ctx *ctx);
 int secpe_profile_end(secpe_ctx *ctx, double *out, int32_t n_out);
 /* host counts[8]: NTT limb-transforms, key switches, rescales, rotations, ct-ct products,

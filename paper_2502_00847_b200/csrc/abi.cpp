@@ -731,8 +731,9 @@ int secpe_profile_end(secpe_ctx *ctx, double *out, int32_t n_out) {
         Prof &p = ctx->c.prof;
         CUDA_CHECK(cudaStreamSynchronize(ctx->c.st));
         p.on = false;
-        for (int i = 0; i < 12; i++) out[i] = 0;
+        for (int i = 0; i < n_out; i++) out[i] = 0;
         for (const auto &s : p.spans) {
+            if (3 * s.kind + 2 >= n_out) continue;  // stage spans (kinds 4..8) only when asked for
             float ms = 0;
             CUDA_CHECK(cudaEventElapsedTime(&ms, p.pool[s.a], p.pool[s.b]));
             out[3 * s.kind + 0] += ms;

@@ -76,7 +76,8 @@ struct Prof {
     size_t used = 0;
     struct Span {
         size_t a, b;
-        int kind;      // 0 NTT launch on FP64 rows, 1 key switch, 2 rescale, 3 NTT launch on integer rows
+        int kind;      // 0 NTT launch on FP64 rows, 1 key switch, 2 rescale, 3 NTT launch on integer rows,
+                       // 4..8 argmax stages H1, H2, H3, H4, H6
         double bytes;  // algorithmic bytes of the span
         double units;
     };

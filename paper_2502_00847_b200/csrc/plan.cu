@@ -252,22 +252,34 @@ struct Ev {
         return mul_ct(g, s, Sy, Ls - 1, {{&ry, 0.5}});
     }
     // Algorithm 1 with the H1..H6 steps of DESIGN.md section 2
+    // profiler spans of the circuit stages (kinds 4..8: H1, H2, H3, H4, H6; only when profiling)
     Val argmax(const Val &in, const Layout &lay, const SignCfg &cfg) {
         const int P = lay.prompts, K = lay.classes;
         Val y = in;
+        size_t sp = c.prof_begin(4);
         for (int t = 0; (1 << t) < P; t++) y = rot_add(y, K << t);
+        c.prof_end(sp, 4, 0, n);
         std::vector<double> mask(c.N / 2, 0.0);
         for (int qi = 0; qi < lay.queries; qi++)
             for (int kk = 0; kk < K; kk++) mask[(size_t)qi * lay.block + kk] = 1.0 / P;
+        sp = c.prof_begin(5);
         y = mul_mask(y, mask, c.scale,
                      "argmax/" + std::to_string(lay.queries) + "/" + std::to_string(P) + "/" + std::to_string(K) + "/" +
                          std::to_string(lay.block));
+        c.prof_end(sp, 5, 0, n);
+        sp = c.prof_begin(6);
         y = rot_add(y, -K);
+        c.prof_end(sp, 6, 0, n);
         Val ydup = y;
+        sp = c.prof_begin(7);
         for (int i = 0; (1 << i) < K; i++) y = hom_max(rot(y, 1 << i), y, cfg);
+        c.prof_end(sp, 7, 0, n);
+        sp = c.prof_begin(8);
         Val d = sub(ydup, y);
         Val z = sign(d, cfg, c.scale);
-        return add_const(z, 1.0);
+        Val r = add_const(z, 1.0);
+        c.prof_end(sp, 8, 0, n);
+        return r;
     }
 };
 
