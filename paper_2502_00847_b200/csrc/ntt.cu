@@ -37,6 +37,20 @@ namespace {
 #ifndef NTT_MINB_FP
 #define NTT_MINB_FP 4  // FP rows: 64 registers, no spills
 #endif
+#ifndef NTT_STREAMING
+#define NTT_STREAMING 1  // data loads/stores with the streaming (evict-first) cache hint: L1 kept for twiddles
+#endif
+#if NTT_STREAMING
+#define NTT_LD(p) __ldcs(p)
+#define NTT_LD2(p) __ldcs(p)
+#define NTT_ST(p, v) __stcs(p, v)
+#define NTT_ST2(p, v) __stcs(p, v)
+#else
+#define NTT_LD(p) (*(p))
+#define NTT_LD2(p) (*(p))
+#define NTT_ST(p, v) (*(p) = (v))
+#define NTT_ST2(p, v) (*(p) = (v))
+#endif
 #ifndef NTT_PDL
 #define NTT_PDL 1  // programmatic dependent launch of the NTT passes
 #endif
@@ -359,7 +373,7 @@ __device__ __forceinline__ void strided_body(const PassArgs &a, const RowsArg &d
         }
     } else if (!INV) {
 #pragma unroll
-        for (int k = 0; k < NV; k++) v[k] = A::in(base[STRIDE * held<LO0>(tau, k)], P);
+        for (int k = 0; k < NV; k++) v[k] = A::in(NTT_LD(base + STRIDE * held<LO0>(tau, k)), P);
     } else {
 #pragma unroll
         for (int k = 0; k < NV; k++) v[k] = base[STRIDE * held<LO0>(tau, k)];  // intermediate representation
@@ -383,7 +397,7 @@ __device__ __forceinline__ void strided_body(const PassArgs &a, const RowsArg &d
         for (int k = 0; k < NV; k++) v[k] = A::out_scaled(v[k], ni, nish, P);
     }
 #pragma unroll
-    for (int k = 0; k < NV; k++) base[STRIDE * held<LOL>(tau, k)] = v[k];
+    for (int k = 0; k < NV; k++) NTT_ST(base + STRIDE * held<LOL>(tau, k), v[k]);
 }
 
 __device__ __forceinline__ PrimeC prime_consts(const Tab &tab, int prime) {
@@ -491,7 +505,7 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, const RowsArg &d,
         // forward round 0 holds r = 16 k + tau: lane-consecutive, load straight from global
         const u64 *src = blk + gl * G;
 #pragma unroll
-        for (int k = 0; k < NV; k++) v[k] = src[held<LO0>(tau, k)];  // intermediate representation
+        for (int k = 0; k < NV; k++) v[k] = NTT_LD(src + held<LO0>(tau, k));  // intermediate representation
     } else {
         const u64 *sp = (IO == IN_SRC || IO == IN_MUL || IO == IN_MUL2 || IO == IN_LIN)
                             ? a.f.src.p + poly_off(a.f.src.cs, a.f.src.ps, poly) + boff
@@ -509,7 +523,7 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, const RowsArg &d,
         const u64 lc2 = IO == IN_LIN && a.f.lin == 2 ? smod_dev(a.f.C2, q, br0, br1) : 0;
 #pragma unroll 4
         for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
-            ulonglong2 x = src[i];
+            ulonglong2 x = NTT_LD2(src + i);
             if (IO == IN_LIN) {
                 U128 t0 = mul_wide(x.x, lc1), t1 = mul_wide(x.y, lc1);
                 if (src2) {
@@ -615,13 +629,13 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, const RowsArg &d,
                     x1 = addmod(x1, d.y, q);
                 }
             }
-            dst[i] = make_ulonglong2(x0, x1);
+            NTT_ST2(dst + i, make_ulonglong2(x0, x1));
         }
     } else {
         // inverse round 1 holds r = 16 k + tau (LO = S - 4): store straight to global
         u64 *dst = blk + gl * G;
 #pragma unroll
-        for (int k = 0; k < NV; k++) dst[held<LO1>(tau, k)] = v[k];
+        for (int k = 0; k < NV; k++) NTT_ST(dst + held<LO1>(tau, k), v[k]);
     }
 }
 
