@@ -609,3 +609,33 @@ def test_empty_inputs(S):
     a = g.encrypt(kg, synth.uniform_slots(1, prm.N // 2), prm.L, prm.scale, 1)
     with pytest.raises(S.SecpeError):
         g.rotate_hoisted(kg, a, [])
+
+
+@pytest.mark.parametrize("logn", [13, 14, 15])
+def test_other_ring_dimensions(S, logn):
+    """The NTT and key-switching templates for N = 2^13..2^15 (the configs use 2^12 and 2^16): forward /
+    inverse NTT, relinearise-and-rescale and a rotation, bit-exact vs the oracle on a small chain."""
+    desc = dict(logn=logn, q=[("nearest", 40, 6)], p=[("below", 50, 2)], alpha=3, log_scale=40)
+    prm = ckks.Params(desc)
+    g = S.Context(desc)
+    x = synth.uniform_residues(70 + logn, prm.primes[:8], 2, logn)
+    t = torch.from_numpy(x.copy()).cuda()
+    g.ntt(t, 0, 8)
+    got = t.cpu().numpy()
+    for pi, l in ((0, 0), (1, 7), (1, 3)):
+        assert np.array_equal(got[pi, l], ckks.ntt(x[pi, l], prm.primes[l], prm.psi[l], logn)), (pi, l)
+    g.ntt(t, 0, 8, inverse=True)
+    assert np.array_equal(t.cpu().numpy(), x)
+    ev = ckks.Oracle(prm)
+    seed = synth.KEY_SEED_BASE + 11
+    ko, kg = ev.keygen(seed, [1]), g.keygen(seed, [1])
+    a = ev.encrypt(ko, synth.uniform_slots(5, prm.N // 2), prm.scale, 1)
+    b = ev.encrypt(ko, synth.uniform_slots(6, prm.N // 2), prm.scale, 2)
+    ga = S.Ct(torch.from_numpy(a.data[None].copy()).cuda(), a.level, a.scale)
+    gb = S.Ct(torch.from_numpy(b.data[None].copy()).cuda(), b.level, b.scale)
+    out = g.mul_relin_rescale(kg, ga, gb)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.t[0].cpu().numpy(), ev.rescale(ev.mul_relin(ko, a, b)).data)
+    r = g.rotate(kg, ga, 1)
+    torch.cuda.synchronize()
+    assert np.array_equal(r.t[0].cpu().numpy(), ev.rotate_raw(ko, a, 1).data)
