@@ -639,3 +639,25 @@ def test_other_ring_dimensions(S, logn):
     r = g.rotate(kg, ga, 1)
     torch.cuda.synchronize()
     assert np.array_equal(r.t[0].cpu().numpy(), ev.rotate_raw(ko, a, 1).data)
+
+
+@pytest.mark.parametrize("alpha", [2, 4, 8])
+def test_key_switching_digit_counts(S, alpha):
+    """dnum = 4, 2, 1 at the top level (alpha = 2, 4, 8 over 8 primes): the key inner-product template
+    instances for beta = 4 / 2 / 1 (both kernels) and the conversion groups, bit-exact vs the oracle."""
+    desc = dict(logn=12, q=[("nearest", 40, 8)], p=[("below", 50, max(2, alpha // 2))], alpha=alpha, log_scale=40)
+    prm = ckks.Params(desc)
+    g = S.Context(desc)
+    ev = ckks.Oracle(prm)
+    seed = synth.KEY_SEED_BASE + 13
+    ko, kg = ev.keygen(seed, [3]), g.keygen(seed, [3])
+    a = ev.encrypt(ko, synth.uniform_slots(7, prm.N // 2), prm.scale, 1)
+    b = ev.encrypt(ko, synth.uniform_slots(8, prm.N // 2), prm.scale, 2)
+    ga = S.Ct(torch.from_numpy(a.data[None].copy()).cuda(), a.level, a.scale)
+    gb = S.Ct(torch.from_numpy(b.data[None].copy()).cuda(), b.level, b.scale)
+    out = g.mul_relin_rescale(kg, ga, gb)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.t[0].cpu().numpy(), ev.rescale(ev.mul_relin(ko, a, b)).data)
+    r = g.rotate(kg, ga, 3)
+    torch.cuda.synchronize()
+    assert np.array_equal(r.t[0].cpu().numpy(), ev.rotate_raw(ko, a, 3).data)
