@@ -198,6 +198,16 @@ int secpe_rotate_batch(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *i
  * SECPE_EINVAL for null arguments, n < 1 or n_steps < 1. */
 int secpe_rotate_hoisted(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n,
                          const int32_t *steps, int32_t n_steps, secpe_ct *out);
+/* Diagonal-form homomorphic linear transform (reading R30; the matrix-vector products that CKKS
+ * bootstrapping's CoeffToSlot / SlotToCoeff are built from):
+ *   out = Rescale( sum_i pt_i (.) RotL(in, steps[i]) )
+ * with the rotations hoisted (one ModUp, R29).  in: one ciphertext at level l >= 1.  pts: dev
+ * uint64[n][l+1][N], pt_i's NTT-form residues (an integer plaintext encoded at scale pt_scale; rows
+ * 0..l used), steps: host[n] (0 = identity).  out: level l - 1, scale (in.scale * pt_scale) / q_l,
+ * must not alias in.  Errors: SECPE_EINVAL (null arguments, n < 1), SECPE_ELEVEL (l < 1),
+ * SECPE_ENOKEY (a step without its Galois key). */
+int secpe_linear_transform(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const uint64_t *pts,
+                           const int32_t *steps, int32_t n, double pt_scale, secpe_ct *out);
 /* Rescale by q_level: round(c / q_l) (round half up, reading R12).  out level = in level - 1,
  * out scale = scale / q_l.  out must not alias. */
 int secpe_rescale(secpe_ctx *ctx, const secpe_ct *in, secpe_ct *out);

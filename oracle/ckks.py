@@ -544,6 +544,33 @@ class Oracle:
             outs.append(Ct(out, ct.scale))
         return outs
 
+    def plain_ntt(self, m, level):
+        """NTT-form residues [level+1][N] of a signed integer plaintext m (int64[N])."""
+        prm = self.prm
+        pt = np.zeros((level + 1, prm.N), dtype=np.uint64)
+        lib().o_int_to_ntt(prm.cptr, P(np.ascontiguousarray(m, dtype=np.int64)), level + 1,
+                           P(np.arange(level + 1, dtype=np.int32)), P(pt))
+        return pt
+
+    def linear_transform(self, keys, ct, pts, steps, pt_scale):
+        """Homomorphic diagonal-form matrix-vector product (reading R30; the linear transforms of CKKS
+        bootstrapping's CoeffToSlot / SlotToCoeff, are products of these):
+            out = Rescale( sum_i pt_i (.) RotL(ct, steps[i]) ),
+        the rotations hoisted (R29, one ModUp), pt_i integer plaintexts in NTT form (encoded at pt_scale),
+        the products summed exactly mod q, one rescale (R12).  Output scale (S_ct pt_scale) / q_level."""
+        prm = self.prm
+        if len(pts) != len(steps) or not steps:
+            raise ValueError("one plaintext per step")
+        rots = self.rotate_hoisted_raw(keys, ct, steps)
+        nl = ct.level + 1
+        acc = np.zeros((2, nl, prm.N), dtype=np.uint64)
+        for r, pt in zip(rots, pts):
+            prod = self.mul_plain_raw(r, pt)
+            nxt = np.zeros_like(acc)
+            lib().o_add(prm.cptr, P(acc), P(prod), nl, 2, P(nxt))
+            acc = nxt
+        return self.rescale(Ct(acc, ct.scale * pt_scale))
+
     # ---- planned ops (logged; reading R9 scale planning) ------------------------------------
     def rot(self, keys, x, steps):
         g = galois_elt(self.prm, steps)

@@ -462,6 +462,22 @@ int secpe_rotate_hoisted(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct 
         for (int s = 0; s < n_steps; s++) batch_out_finish(c, out + (long)s * n, n, vo[s], so[s]);
     });
 }
+int secpe_linear_transform(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const uint64_t *pts,
+                           const int32_t *steps, int32_t n, double pt_scale, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && keys && in && pts && steps && out && out->data && n >= 1, SECPE_EINVAL, "null argument");
+        Ctx &c = ctx->c;
+        CtView vi = view_of(c, in);
+        REQUIRE(vi.level >= 1, SECPE_ELEVEL, "no level left to rescale");
+        REQUIRE(out->data != in->data, SECPE_EINVAL, "out must not alias in");
+        const double osc = (vi.scale * pt_scale) / (double)c.primes[vi.level];
+        CtView vo = compact_view(c, out->data, 1, vi.level - 1, osc);
+        std::vector<int> st(steps, steps + n);
+        ev_linear_transform(c, *keys->k, vi, pts, (long)(vi.level + 1) * c.N, st.data(), n, vo);
+        vo.scale = osc;
+        set_out(out, vo);
+    });
+}
 int secpe_rescale(secpe_ctx *ctx, const secpe_ct *in, secpe_ct *out) {
     return guard([&] {
         REQUIRE(ctx && out && out->data, SECPE_EINVAL, "null argument");

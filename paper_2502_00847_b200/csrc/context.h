@@ -218,6 +218,8 @@ void ev_rescale_lin(Ctx &c, const CtView &x1, i64 C1, const CtView *x2, i64 C2, 
 void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView &out,
                const CtView *add_after = nullptr);  // add_after: out = RotL(in) + add_after (fused)
 void ev_rotate_hoisted(Ctx &c, const Keys &k, const CtView &in, const int *steps, int n_steps, const CtView *outs);
+void ev_linear_transform(Ctx &c, const Keys &k, const CtView &in, const u64 *pts, long pt_stride, const int *steps,
+                         int n, const CtView &out);
 void ev_mul_plain_ntt(Ctx &c, const CtView &a, const u64 *pt, const CtView &out);
 LimbConst limb_const(const Ctx &c, i64 C, int nl);
 

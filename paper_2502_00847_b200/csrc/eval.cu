@@ -444,6 +444,27 @@ void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView 
     c.cnt.rotate += in.n;
 }
 
+// Hoisted diagonal-form linear transform (R30): out = Rescale(sum_i pt_i (.) RotL(in, steps[i])), one
+// ModUp shared by all rotations (R29); pt_i dev [level+1][N] NTT-form rows at pts + i * pt_stride.
+void ev_linear_transform(Ctx &c, const Keys &k, const CtView &in, const u64 *pts, long pt_stride, const int *steps,
+                         int n, const CtView &out) {
+    if (n < 1) throw SecpeError{-1, "linear_transform: no diagonals"};
+    if (in.n != 1) throw SecpeError{-1, "linear_transform: one ciphertext"};
+    const int l = in.level, nl = l + 1;
+    if (l < 1) throw SecpeError{-2, "linear_transform: no level left to rescale"};
+    if (out.level != l - 1) throw SecpeError{-1, "linear_transform: output level"};
+    const long N = c.N, cw = 2L * nl * N;
+    DevBuf rot((size_t)n * cw, c.st);
+    std::vector<CtView> outs(n);
+    for (int i = 0; i < n; i++) outs[i] = compact_view(c, rot.p + (long)i * cw, 1, l, in.scale);
+    ev_rotate_hoisted(c, k, in, steps, n, outs.data());
+    DevBuf acc(cw, c.st);
+    const CtView va = compact_view(c, acc.p, 1, l, in.scale);
+    k_mac_plain(c.tab, c.logn, CRows{rot.p, cw, (long)nl * N}, cw, pts, pt_stride, n, rows_of(va), 2, qmap(nl), c.st);
+    c.cnt.launches++;
+    ev_rescale(c, va, out);
+}
+
 // Hoisted rotations (N2, reading R29): one ModUp of c1 shared by every step; per step the key inner
 // product gathers sigma_g of the digits (k_ks_inner galois), ModDown adds sigma_g(c0) in its final NTT.
 // Same integers as the oracle's rotate_hoisted_raw (not as ev_rotate: ModUp does not commute with sigma_g).

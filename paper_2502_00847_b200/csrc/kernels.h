@@ -94,6 +94,10 @@ void k_mul_poly(const Tab &tab, int logn, CRows a, const u64 *b, RowsArg out, in
 // d1 += C x1 (C per-limb residues, the planned linear term of R13)
 void k_tensor(const Tab &tab, int logn, CRows a, CRows b, u64 *d, long d_ct_stride, int n_ct, int nl,
               cudaStream_t st, CRows x = CRows{nullptr, 0, 0}, const LimbConst *C = nullptr);
+// linear transform accumulation (R30): out[P][l] = sum_{s<n} pt[s][l] * a_s[P][l] mod q_l, ciphertext s of
+// the batch at a.p + s * as (same CRows layout), plaintext s at pt + s * pts ([l][N] rows, NTT form)
+void k_mac_plain(const Tab &tab, int logn, CRows a, long as, const u64 *pt, long pts, int n, RowsArg out, int n_polys,
+                 LimbMap lm, cudaStream_t st);
 // automorphism in the NTT domain: out[i] = in[perm_g(i)]
 void k_automorph(int logn, CRows a, RowsArg out, int n_polys, int nl, u64 galois, cudaStream_t st);
 

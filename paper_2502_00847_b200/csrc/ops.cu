@@ -146,7 +146,36 @@ __global__ void automorph_kernel(int logn, CRows a, RowsArg out, int nl, u64 g) 
     }
     st2(out.p + poly_off(out.cs, out.ps, poly) + off + i0, make_ulonglong2(r[0], r[1]));
 }
+// out[P][l] = sum_s pt_s[l] * a_s[P][l] mod q_l (linear transform, R30): a_s = ciphertext s of a batch
+// (stride as), pt_s at pt + s * ps_stride; 128-bit accumulation reduced every 16 products
+__global__ void mac_plain_kernel(Tab tab, int logn, CRows a, long as, const u64 *__restrict__ pt, long pts, int n,
+                                 RowsArg out, LimbMap lm) {
+    const int nl = lm.nl, poly = blockIdx.y / nl, limb = blockIdx.y % nl;
+    const int pr = prime_of(lm, limb);
+    const u64 q = tab.q[pr], r0 = tab.br0[pr], r1 = tab.br1[pr];
+    const long off = (long)limb << logn;
+    const long k = 2L * ((long)blockIdx.x * TPB + threadIdx.x);
+    U128 s0{0, 0}, s1{0, 0};
+    for (int s = 0; s < n; s++) {
+        const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(a.p + s * as + poly_off(a.cs, a.ps, poly) + off + k);
+        const ulonglong2 w = *reinterpret_cast<const ulonglong2 *>(pt + s * pts + off + k);
+        mac_wide(s0, x.x, w.x);
+        mac_wide(s1, x.y, w.y);
+        if ((s & 15) == 15) {
+            s0 = U128{barrett128(s0, q, r0, r1), 0};
+            s1 = U128{barrett128(s1, q, r0, r1), 0};
+        }
+    }
+    *reinterpret_cast<ulonglong2 *>(out.p + poly_off(out.cs, out.ps, poly) + off + k) =
+        make_ulonglong2(barrett128(s0, q, r0, r1), barrett128(s1, q, r0, r1));
+}
 }  // namespace
+
+void k_mac_plain(const Tab &tab, int logn, CRows a, long as, const u64 *pt, long pts, int n, RowsArg out, int n_polys,
+                 LimbMap lm, cudaStream_t st) {
+    mac_plain_kernel<<<grid_rows(logn, n_polys * lm.nl), TPB, 0, st>>>(tab, logn, a, as, pt, pts, n, out, lm);
+    LAUNCH_CHECK();
+}
 
 void k_addsub(const Tab &tab, int logn, CRows a, CRows b, RowsArg out, int n_polys, LimbMap lm, bool sub,
               cudaStream_t st) {

@@ -76,6 +76,8 @@ SIGS = {
                                           ctypes.POINTER(CCt)]),
     "secpe_rotate_hoisted": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, i32p, ctypes.c_int32,
                                             ctypes.POINTER(CCt)]),
+    "secpe_linear_transform": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), u64p, i32p, ctypes.c_int32,
+                                              ctypes.c_double, ctypes.POINTER(CCt)]),
     "secpe_rescale": (ctypes.c_int, [vp, ctypes.POINTER(CCt), ctypes.POINTER(CCt)]),
     "secpe_rotate": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.POINTER(CCt)]),
     "secpe_sign_poly": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.POINTER(SignCfg), ctypes.c_double,
@@ -380,6 +382,19 @@ class Context:
         for s, o in enumerate(outs):
             o.level, o.scale = co[s * a.n].level, co[s * a.n].scale
         return outs
+
+    def linear_transform(self, keys, a, pts, steps, pt_scale):
+        """secpe_linear_transform (reading R30): Rescale(sum_i pts[i] (.) RotL(a, steps[i])); pts a cuda
+        uint64 tensor [n][a.level+1][N] of NTT-form plaintext residues."""
+        assert pts.is_cuda and pts.dtype == torch.uint64 and pts.is_contiguous()
+        assert pts.shape[0] == len(steps) and pts.shape[1] == a.level + 1
+        out = self._out(a.level - 1)
+        ca, co = a.c(), out.c()
+        st = np.asarray(steps, dtype=np.int32)
+        _chk(lib().secpe_linear_transform(self.h, keys.h, ctypes.byref(ca), ctypes.cast(pts.data_ptr(), u64p),
+                                          st.ctypes.data_as(i32p), len(steps), pt_scale, ctypes.byref(co)))
+        out.level, out.scale = co.level, co.scale
+        return out
 
     def rescale(self, a):
         out = self._out(a.level - 1)

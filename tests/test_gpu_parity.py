@@ -661,3 +661,34 @@ def test_key_switching_digit_counts(S, alpha):
     r = g.rotate(kg, ga, 3)
     torch.cuda.synchronize()
     assert np.array_equal(r.t[0].cpu().numpy(), ev.rotate_raw(ko, a, 3).data)
+
+
+@pytest.mark.parametrize("name,steps,level_drop", [
+    ("toy", [0, 1, 2, 5, -3], 0),
+    ("argmax", [0, 1, 3, 2048, -7, 16], 12),
+])
+def test_linear_transform_bit_exact(S, name, steps, level_drop):
+    """secpe_linear_transform (reading R30, a building block of bootstrapping's CoeffToSlot / SlotToCoeff):
+    word for word equal to the oracle's linear_transform; decrypts to the plaintext matrix-vector product."""
+    P = pair(S, name)
+    prm, g = P.prm, P.gpu
+    ev = ckks.Oracle(prm)
+    seed = synth.KEY_SEED_BASE + 17
+    rot = sorted({s for s in steps if s})
+    ko, kg = ev.keygen(seed, rot), g.keygen(seed, rot)
+    n = prm.N // 2
+    rng = np.random.default_rng(31)
+    z = rng.uniform(-1, 1, n)
+    diags = [rng.uniform(-1, 1, n) for _ in steps]
+    ct = ev.encrypt(ko, z, prm.scale, 9)
+    level = prm.L - level_drop
+    if level < ct.level:
+        ct = ev.drop(ct, level)
+    pt_scale = float(prm.primes[level])
+    pts = [ev.plain_ntt(ckks.encode(prm, d, pt_scale), level) for d in diags]
+    want = ev.linear_transform(ko, ct, pts, steps, pt_scale)
+    got = g.linear_transform(kg, P.up(ct), torch.from_numpy(np.stack(pts)).cuda(), steps, pt_scale)
+    assert got.level == want.level and got.scale == want.scale
+    assert np.array_equal(P.down(got), want.data)
+    ref = sum(d * np.roll(z, -s) for d, s in zip(diags, steps))
+    assert np.abs(ev.decrypt(ko, want).real - ref).max() < 2 ** -10

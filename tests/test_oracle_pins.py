@@ -402,6 +402,25 @@ def test_hoisted_rotations_against_slots(toy):
     assert np.array_equal(outs[-1].data, a.data)  # step 0: identity
 
 
+def test_linear_transform_against_matrix(toy):
+    """R30: the hoisted diagonal-form linear transform decrypts to the plaintext matrix-vector product
+    y[t] = sum_i d_i[t] z[t + s_i] (numpy, independent of the oracle's arithmetic) within 2^-10."""
+    ev = ckks.Oracle(toy)
+    steps = [0, 1, 2, 5, -3]
+    keys = ev.keygen(21, [s for s in steps if s])
+    n = toy.N // 2
+    rng = np.random.default_rng(4)
+    z = rng.uniform(-1, 1, n)
+    diags = [rng.uniform(-1, 1, n) for _ in steps]
+    ct = ev.encrypt(keys, z, toy.scale, 3)
+    pt_scale = float(toy.primes[ct.level])  # one rescale returns the ciphertext's own scale
+    pts = [ev.plain_ntt(ckks.encode(toy, d, pt_scale), ct.level) for d in diags]
+    out = ev.linear_transform(keys, ct, pts, steps, pt_scale)
+    assert out.level == ct.level - 1 and out.scale == ct.scale * pt_scale / float(toy.primes[ct.level])
+    want = sum(d * np.roll(z, -s) for d, s in zip(diags, steps))
+    assert np.abs(ev.decrypt(keys, out).real - want).max() < 2 ** -10
+
+
 def test_automorph_is_sigma_g(tiny):
     """o_automorph == coefficient map X^k -> X^{gk} applied by definition (Python)."""
     prm, ev = tiny, ckks.Oracle(tiny)
