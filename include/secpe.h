@@ -208,6 +208,15 @@ int secpe_rotate_hoisted(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct 
  * SECPE_ENOKEY (a step without its Galois key). */
 int secpe_linear_transform(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const uint64_t *pts,
                            const int32_t *steps, int32_t n, double pt_scale, secpe_ct *out);
+/* Baby-step giant-step form (reading R31): with n1 baby and n2 giant steps,
+ *   out = Rescale( sum_{g<n2} RotL( sum_{j<n1} pt_{g,j} (.) RotL(in, j), g n1 ) ),
+ * the baby rotations hoisted (R29), the giant rotations plain (secpe_rotate's integers), one rescale;
+ * with pt_{g,j} = encode(RotR(d_{g n1 + j}, g n1)) this is sum_i d_i (.) RotL(in, i) over n1 n2 diagonals
+ * with n1 + n2 - 2 rotations instead of n1 n2 - 1.  pts: dev uint64[n2][n1][l+1][N] (NTT form); Galois
+ * keys needed for 1..n1-1 and n1, 2 n1, ..., (n2-1) n1.  out: level l - 1, scale (in.scale pt_scale)/q_l,
+ * must not alias in.  Errors: SECPE_EINVAL, SECPE_ELEVEL (l < 1), SECPE_ENOKEY. */
+int secpe_linear_transform_bsgs(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const uint64_t *pts,
+                                int32_t n1, int32_t n2, double pt_scale, secpe_ct *out);
 /* Rescale by q_level: round(c / q_l) (round half up, reading R12).  out level = in level - 1,
  * out scale = scale / q_l.  out must not alias. */
 int secpe_rescale(secpe_ctx *ctx, const secpe_ct *in, secpe_ct *out);

@@ -571,6 +571,36 @@ class Oracle:
             acc = nxt
         return self.rescale(Ct(acc, ct.scale * pt_scale))
 
+    def linear_transform_bsgs(self, keys, ct, pts, n1, n2, pt_scale):
+        """Baby-step giant-step form of linear_transform (reading R31; how bootstrapping evaluates its
+        dense CoeffToSlot / SlotToCoeff factors with about 2 sqrt(n) rotations instead of n):
+            out = Rescale( sum_{g < n2} RotL( sum_{j < n1} pts[g][j] (.) RotL(ct, j), g n1 ) )
+        the baby rotations hoisted (R29), the giant ones plain (O-12), every product and sum exact mod q,
+        one rescale.  With pts[g][j] = encode(RotR(d_{g n1 + j}, g n1)) this is sum_i d_i (.) RotL(ct, i)."""
+        prm = self.prm
+        if len(pts) != n2 or any(len(r) != n1 for r in pts):
+            raise ValueError("pts must be n2 lists of n1 plaintexts")
+        nl = ct.level + 1
+        baby = self.rotate_hoisted_raw(keys, ct, list(range(n1)))
+        acc = None
+        for g in range(n2):
+            inner = np.zeros((2, nl, prm.N), dtype=np.uint64)
+            for j in range(n1):
+                prod = self.mul_plain_raw(baby[j], pts[g][j])
+                nxt = np.zeros_like(inner)
+                lib().o_add(prm.cptr, P(inner), P(prod), nl, 2, P(nxt))
+                inner = nxt
+            term = Ct(inner, ct.scale * pt_scale)
+            if g:
+                term = self.rotate_raw(keys, term, g * n1)
+            if acc is None:
+                acc = term.data
+            else:
+                nxt = np.zeros_like(acc)
+                lib().o_add(prm.cptr, P(acc), P(term.data), nl, 2, P(nxt))
+                acc = nxt
+        return self.rescale(Ct(acc, ct.scale * pt_scale))
+
     # ---- planned ops (logged; reading R9 scale planning) ------------------------------------
     def rot(self, keys, x, steps):
         g = galois_elt(self.prm, steps)

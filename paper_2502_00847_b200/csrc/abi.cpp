@@ -478,6 +478,25 @@ int secpe_linear_transform(secpe_ctx *ctx, const secpe_keys *keys, const secpe_c
         set_out(out, vo);
     });
 }
+int secpe_linear_transform_bsgs(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const uint64_t *pts,
+                                int32_t n1, int32_t n2, double pt_scale, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && keys && in && pts && out && out->data && n1 >= 1 && n2 >= 1, SECPE_EINVAL, "null argument");
+        Ctx &c = ctx->c;
+        CtView vi = view_of(c, in);
+        REQUIRE(vi.level >= 1, SECPE_ELEVEL, "no level left to rescale");
+        REQUIRE(out->data != in->data, SECPE_EINVAL, "out must not alias in");
+        for (int j = 1; j < n1; j++)
+            REQUIRE(keys->k->gk.count(galois_elt(c, j)), SECPE_ENOKEY, "no Galois key for a baby step");
+        for (int g = 1; g < n2; g++)
+            REQUIRE(keys->k->gk.count(galois_elt(c, g * n1)), SECPE_ENOKEY, "no Galois key for a giant step");
+        const double osc = (vi.scale * pt_scale) / (double)c.primes[vi.level];
+        CtView vo = compact_view(c, out->data, 1, vi.level - 1, osc);
+        ev_linear_transform_bsgs(c, *keys->k, vi, pts, (long)(vi.level + 1) * c.N, n1, n2, vo);
+        vo.scale = osc;
+        set_out(out, vo);
+    });
+}
 int secpe_rescale(secpe_ctx *ctx, const secpe_ct *in, secpe_ct *out) {
     return guard([&] {
         REQUIRE(ctx && out && out->data, SECPE_EINVAL, "null argument");

@@ -78,6 +78,8 @@ SIGS = {
                                             ctypes.POINTER(CCt)]),
     "secpe_linear_transform": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), u64p, i32p, ctypes.c_int32,
                                               ctypes.c_double, ctypes.POINTER(CCt)]),
+    "secpe_linear_transform_bsgs": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), u64p, ctypes.c_int32, ctypes.c_int32,
+                                                   ctypes.c_double, ctypes.POINTER(CCt)]),
     "secpe_rescale": (ctypes.c_int, [vp, ctypes.POINTER(CCt), ctypes.POINTER(CCt)]),
     "secpe_rotate": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.POINTER(CCt)]),
     "secpe_sign_poly": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.POINTER(SignCfg), ctypes.c_double,
@@ -393,6 +395,17 @@ class Context:
         st = np.asarray(steps, dtype=np.int32)
         _chk(lib().secpe_linear_transform(self.h, keys.h, ctypes.byref(ca), ctypes.cast(pts.data_ptr(), u64p),
                                           st.ctypes.data_as(i32p), len(steps), pt_scale, ctypes.byref(co)))
+        out.level, out.scale = co.level, co.scale
+        return out
+
+    def linear_transform_bsgs(self, keys, a, pts, n1, n2, pt_scale):
+        """secpe_linear_transform_bsgs (reading R31); pts a cuda uint64 tensor [n2][n1][a.level+1][N]."""
+        assert pts.is_cuda and pts.dtype == torch.uint64 and pts.is_contiguous()
+        assert tuple(pts.shape[:3]) == (n2, n1, a.level + 1)
+        out = self._out(a.level - 1)
+        ca, co = a.c(), out.c()
+        _chk(lib().secpe_linear_transform_bsgs(self.h, keys.h, ctypes.byref(ca), ctypes.cast(pts.data_ptr(), u64p),
+                                               n1, n2, pt_scale, ctypes.byref(co)))
         out.level, out.scale = co.level, co.scale
         return out
 

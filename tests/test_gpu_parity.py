@@ -692,3 +692,54 @@ def test_linear_transform_bit_exact(S, name, steps, level_drop):
     assert np.array_equal(P.down(got), want.data)
     ref = sum(d * np.roll(z, -s) for d, s in zip(diags, steps))
     assert np.abs(ev.decrypt(ko, want).real - ref).max() < 2 ** -10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,n1,n2,level_drop", [
+    ("toy", 4, 3, 0),
+    ("toy", 1, 3, 0),   # giant steps only
+    ("toy", 3, 1, 0),   # baby steps only (= R30 with steps 0..n1-1)
+    ("argmax", 4, 3, 12),
+])
+def test_linear_transform_bsgs_bit_exact(S, name, n1, n2, level_drop):
+    """secpe_linear_transform_bsgs (reading R31): word for word equal to the oracle's
+    linear_transform_bsgs; decrypts to sum_i d_i (.) RotL(z, i) over n1 n2 diagonals."""
+    P = pair(S, name)
+    prm, g = P.prm, P.gpu
+    ev = ckks.Oracle(prm)
+    seed = synth.KEY_SEED_BASE + 19
+    rot = list(range(1, n1)) + [j * n1 for j in range(1, n2)]
+    ko, kg = ev.keygen(seed, rot), g.keygen(seed, rot)
+    n = prm.N // 2
+    rng = np.random.default_rng(37)
+    z = rng.uniform(-1, 1, n)
+    d = [rng.uniform(-1, 1, n) for _ in range(n1 * n2)]
+    ct = ev.encrypt(ko, z, prm.scale, 11)
+    level = prm.L - level_drop
+    if level < ct.level:
+        ct = ev.drop(ct, level)
+    pt_scale = float(prm.primes[level])
+    pts = [[ev.plain_ntt(ckks.encode(prm, np.roll(d[j * n1 + i], j * n1), pt_scale), level) for i in range(n1)]
+           for j in range(n2)]
+    want = ev.linear_transform_bsgs(ko, ct, pts, n1, n2, pt_scale)
+    got = g.linear_transform_bsgs(kg, P.up(ct), torch.from_numpy(np.stack([np.stack(r) for r in pts])).cuda(),
+                                  n1, n2, pt_scale)
+    assert got.level == want.level and got.scale == want.scale
+    assert np.array_equal(P.down(got), want.data)
+    ref = sum(d[i] * np.roll(z, -i) for i in range(n1 * n2))
+    assert np.abs(ev.decrypt(ko, want).real - ref).max() < 2 ** -10
+
+
+@pytest.mark.gpu
+def test_linear_transform_bsgs_errors(S):
+    """R31 argument checks: a missing giant-step key, n1 or n2 < 1 are rejected, nothing written."""
+    P = pair(S, "toy")
+    prm, g = P.prm, P.gpu
+    ev = ckks.Oracle(prm)
+    ko, kg = ev.keygen(5, [1]), g.keygen(5, [1])
+    ct = P.up(ev.encrypt(ko, np.zeros(prm.N // 2), prm.scale, 1))
+    pts = torch.zeros((2, 2, ct.level + 1, prm.N), dtype=torch.uint64, device="cuda")
+    with pytest.raises(S.SecpeError):
+        g.linear_transform_bsgs(kg, ct, pts, 2, 2, 1.0)   # needs the key for step 2
+    with pytest.raises(S.SecpeError):
+        g.linear_transform_bsgs(kg, ct, pts[:, :0].contiguous(), 0, 2, 1.0)

@@ -421,6 +421,25 @@ def test_linear_transform_against_matrix(toy):
     assert np.abs(ev.decrypt(keys, out).real - want).max() < 2 ** -10
 
 
+def test_linear_transform_bsgs_against_matrix(toy):
+    """R31: the baby-step giant-step transform with pre-rotated diagonals decrypts to
+    y = sum_{i < n1 n2} d_i (.) RotL(z, i) (numpy) within 2^-10."""
+    ev = ckks.Oracle(toy)
+    n1, n2 = 4, 3
+    keys = ev.keygen(23, list(range(1, n1)) + [g * n1 for g in range(1, n2)])
+    n = toy.N // 2
+    rng = np.random.default_rng(6)
+    z = rng.uniform(-1, 1, n)
+    d = [rng.uniform(-1, 1, n) for _ in range(n1 * n2)]
+    ct = ev.encrypt(keys, z, toy.scale, 5)
+    pt_scale = float(toy.primes[ct.level])
+    pts = [[ev.plain_ntt(ckks.encode(toy, np.roll(d[g * n1 + j], g * n1), pt_scale), ct.level) for j in range(n1)]
+           for g in range(n2)]
+    out = ev.linear_transform_bsgs(keys, ct, pts, n1, n2, pt_scale)
+    want = sum(d[i] * np.roll(z, -i) for i in range(n1 * n2))
+    assert np.abs(ev.decrypt(keys, out).real - want).max() < 2 ** -10
+
+
 def test_automorph_is_sigma_g(tiny):
     """o_automorph == coefficient map X^k -> X^{gk} applied by definition (Python)."""
     prm, ev = tiny, ckks.Oracle(tiny)
