@@ -15,6 +15,9 @@ What each part follows (PAPER.md line numbers; readings R* are listed in DESIGN.
   Max .................... PAPER.md:208-210 (Eq. 6)
   Argmax ................. PAPER.md:214-235 (Algorithm 1), :141 (aggregation), :197-204 (Eq. 5),
                            :239 (2n slots per argmax)
+  Bootstrapping .......... SURVEY 8(f) N3 (PAPER.md:94-96, :327 bootstraps at L = 35): conjugation
+                           (R32), ModRaise (R33), CoeffToSlot / SlotToCoeff (R34), EvalMod (R35);
+                           the plan is in plan.py
 """
 import ctypes
 import math
@@ -333,9 +336,15 @@ class Ct:
         return Ct(self.data.copy(), self.scale)
 
 
+# Step value meaning complex conjugation of the slots (reading R32): sigma_g with g = 2N - 1 (X -> X^-1)
+CONJ = -(2 ** 31)
+
+
 def galois_elt(prm, steps):
-    """RotL(s): g = 5^s mod 2N; RotR(s) = RotL(N/2 - s) (reading R2)."""
+    """RotL(s): g = 5^s mod 2N; RotR(s) = RotL(N/2 - s) (reading R2); CONJ: g = 2N - 1 (R32)."""
     N = prm.N
+    if steps == CONJ:
+        return 2 * N - 1
     s = steps % (N // 2)
     return pow(5, s, 2 * N)
 
@@ -601,7 +610,30 @@ class Oracle:
                 acc = nxt
         return self.rescale(Ct(acc, ct.scale * pt_scale))
 
+    def mod_raise(self, ct, level):
+        """ModRaise (reading R33, the first step of CKKS bootstrapping): a level-0
+        ciphertext (c0, c1) mod q_0 is read as the integer polynomials with centred coefficients in
+        (-q_0/2, q_0/2] and reduced mod every prime of Q_level.  It then decrypts to
+        t = c0 + c1 s = m + q_0 I over the integers, I a small integer polynomial (|I| <= (h+1)/2)."""
+        if ct.level != 0:
+            raise ValueError("mod_raise takes a level-0 ciphertext")
+        prm = self.prm
+        q0 = prm.primes[0]
+        out = np.zeros((2, level + 1, prm.N), dtype=np.uint64)
+        for i in range(2):
+            coef = ntt_limbs(ct.data[i, :1], prm, [0], inverse=True)[0]
+            v = np.array([int(c) - q0 if int(c) > (q0 - 1) // 2 else int(c) for c in coef], dtype=np.int64)
+            out[i] = self.plain_ntt(v, level)
+        r = Ct(out, ct.scale)
+        self._log("MODRAISE", 0, level, ct.scale)
+        return r
+
     # ---- planned ops (logged; reading R9 scale planning) ------------------------------------
+    def lt_bsgs(self, keys, x, pts, n1, n2, pt_scale):
+        out = self.linear_transform_bsgs(keys, x, pts, n1, n2, pt_scale)
+        self._log("LTB", x.level, out.level, out.scale, "%dx%d" % (n1, n2))
+        return out
+
     def rot(self, keys, x, steps):
         g = galois_elt(self.prm, steps)
         out = self.rotate_raw(keys, x, steps)

@@ -15,6 +15,8 @@ import math
 
 import numpy as np
 
+CONJ_STEP = -(2 ** 31)  # = ckks.CONJ: slot conjugation (reading R32)
+
 
 def poly_depth(deg):
     """Multiplicative depth of the plan for an odd degree-`deg` polynomial: ceil(log2(deg+1)) for the
@@ -175,3 +177,138 @@ def labels(z, layout):
 def true_labels(scores):
     """Plaintext truth: argmax of the mean-over-prompts scores, first index on ties."""
     return np.argmax(scores.mean(axis=1), axis=1)
+
+
+# ---------------------------------------------------------------------------------------------
+# CKKS bootstrapping (SURVEY 8(f) N3; the paper bootstraps with L = 35, K = 14, PAPER.md:94-96,
+# :327).  Readings R32-R35 (DESIGN.md): conjugation, ModRaise, dense CoeffToSlot / SlotToCoeff as
+# baby-step giant-step linear transforms (R31), EvalMod as 2 cos((2 pi K x - pi/2) / 2^r) followed
+# by r double-angle steps d <- d^2 - 2.
+# ---------------------------------------------------------------------------------------------
+def eval_poly15(ev, keys, x, c, target_scale):
+    """General degree-15 p(x) = sum_i c_i x^i landing at level x.level - 5, scale target_scale (R35).
+
+    The odd plan's Paterson-Stockmeyer shape (R13) with the even terms added: baby steps x, x^2, x^3,
+    giant steps x^4, x^8; q_k = c_{4k} + c_{4k+1} x + c_{4k+2} x^2 + c_{4k+3} x^3 (a two-term linear
+    combination, a one-term one and a constant); p = (q_0 + q_1 x^4) + (q_2 + q_3 x^4) x^8."""
+    if len(c) != 16:
+        raise ValueError("degree-15 coefficients c_0..c_15")
+    prm = ev.prm
+    q = lambda lv: float(prm.primes[lv])
+    l = x.level
+    T, Lo = target_scale, l - 5
+    x2 = ev.mul_ct(keys, x, x, None, l - 1)
+    x3 = ev.mul_ct(keys, x, x2, None, l - 2)
+    x4 = ev.mul_ct(keys, x2, x2, None, l - 2)
+    x8 = ev.mul_ct(keys, x4, x4, None, l - 3)
+    S_b1 = (T * q(l - 4)) / x8.scale
+    S_q3 = (S_b1 * q(l - 3)) / x4.scale
+    q3 = ev.lincomb([(x, c[13]), (x3, c[15])], S_q3, l - 3)
+    q3 = ev.add_const(ev.add(q3, ev.lincomb([(x2, c[14])], S_q3, l - 3)), c[12])
+    b1 = ev.mul_ct(keys, q3, x4, S_b1, l - 4, lin=[(x, c[9]), (x3, c[11])])
+    b1 = ev.add_const(ev.add(b1, ev.lincomb([(x2, c[10])], S_b1, l - 4)), c[8])
+    S_q1 = (T * q(l - 4)) / x4.scale
+    q1 = ev.lincomb([(x, c[5]), (x3, c[7])], S_q1, l - 4)
+    q1 = ev.add_const(ev.add(q1, ev.lincomb([(x2, c[6])], S_q1, l - 4)), c[4])
+    p = ev.mul_ct(keys, q1, x4, T, Lo, lin=[(x, c[1]), (x3, c[3])], prod2=(b1, x8))
+    return ev.add_const(ev.add(p, ev.lincomb([(x2, c[2])], T, Lo)), c[0])
+
+
+def boot_poly(K, r):
+    """Power-basis coefficients c_0..c_15 of 2 cos(a x + b), a = 2 pi K / 2^r, b = -pi / 2^(r+1), on
+    [-1, 1] (R35): its Taylor series at 0, c_i = 2 a^i cos(b + i pi / 2) / i!, truncated after x^15
+    (remainder <= 2 a^16 / 16!; every coefficient exact to a double's rounding)."""
+    a = 2.0 * math.pi * K / 2.0 ** r
+    b = -math.pi / 2.0 ** (r + 1)
+    return [2.0 * a ** i * math.cos(b + i * math.pi / 2) / math.factorial(i) for i in range(16)]
+
+
+def boot_depth(r):
+    """Levels one bootstrap consumes: CoeffToSlot 1, normalisation 1, polynomial 5, r doublings,
+    SlotToCoeff 1."""
+    return 8 + r
+
+
+def boot_rotations(n1, n2):
+    """Galois keys bootstrapping needs: baby steps 1..n1-1, giant steps n1, 2 n1, ..., conjugation."""
+    return list(range(1, n1)) + [g * n1 for g in range(1, n2)] + [CONJ_STEP]
+
+
+def boot_matrices(prm, R):
+    """Slot-domain matrices (R34), n = N/2, e_j = 5^j mod 2N, zeta = e^{i pi / N}:
+    A[k, j] = zeta^{-e_j k} / n (encode's inverse: (A z)_k = t_k + i t_{k+n} for the real integer
+    polynomial t behind the slots z, both divided by the scale), U[j, k] = zeta^{e_j k} (decode).
+    CoeffToSlot: A/2 and -i A/2 (u + conj(u) then gives Re and Im of A z);
+    SlotToCoeff: c U and i c U with c = R / (4 pi) (the doubled cosine's 2 and EvalMod's R / 2 pi)."""
+    from oracle.ckks import _rot_group
+    N, n = prm.N, prm.N // 2
+    e = _rot_group(N).astype(np.float64)
+    k = np.arange(n, dtype=np.float64)
+    A = np.exp(-1j * np.pi * np.outer(k, e) / N) / n
+    U = np.exp(1j * np.pi * np.outer(e, k) / N)
+    c = R / (4.0 * np.pi)
+    return dict(cts_re=A / 2, cts_im=-0.5j * A, stc_re=c * U, stc_im=1j * c * U)
+
+
+def bsgs_pts(ev, M, n1, n2, level, pt_scale):
+    """pts[g][j] = NTT(encode(RotR(d_{g n1 + j}, g n1), pt_scale)) at `level`, d_i[t] = M[t, (t + i) mod n]
+    (R30/R31)."""
+    from oracle.ckks import encode
+    n = M.shape[0]
+    if n1 * n2 != n:
+        raise ValueError("n1 n2 must equal the slot count")
+    t = np.arange(n)
+    out = []
+    for g in range(n2):
+        row = []
+        for j in range(n1):
+            i = g * n1 + j
+            d = M[t, (t + i) % n]
+            row.append(ev.plain_ntt(encode(ev.prm, np.roll(d, g * n1), pt_scale), level))
+        out.append(row)
+    return out
+
+
+def boot_config(ev, in_scale, level, K, r, n1, n2):
+    """Everything the bootstrap plan takes besides the ciphertext: the EvalMod range K and doublings r,
+    the BSGS split, the polynomial and the four encoded matrices at their levels and scales."""
+    prm = ev.prm
+    R = float(prm.primes[0]) / in_scale
+    Ms = boot_matrices(prm, R)
+    l_stc = level - 7 - r
+    cts_scale, stc_scale = float(prm.primes[level]), float(prm.primes[l_stc])
+    cfg = dict(level=level, K=float(K), r=r, n1=n1, n2=n2, poly=boot_poly(K, r), cts_scale=cts_scale,
+               stc_scale=stc_scale, stc_level=l_stc)
+    for name in ("cts_re", "cts_im"):
+        cfg[name] = bsgs_pts(ev, Ms[name], n1, n2, level, cts_scale)
+    for name in ("stc_re", "stc_im"):
+        cfg[name] = bsgs_pts(ev, Ms[name], n1, n2, l_stc, stc_scale)
+    return cfg
+
+
+def bootstrap(ev, keys, ct, cfg):
+    """CKKS bootstrapping of a level-0 ciphertext (readings R32-R35):
+      ModRaise to cfg level L                          t = m + q_0 I
+      CoeffToSlot (two BSGS transforms)                u = A z / 2, u' = -i A z / 2
+      x = u + conj(u), x' = u' + conj(u')              slots t_k / S and t_{k+n} / S
+      normalise x / (K R), R = q_0 / S                 in [-1, 1]
+      d = 2 cos((2 pi K x - pi/2) / 2^r), r times d <- d^2 - 2    d = 2 sin(2 pi t / q_0)
+      SlotToCoeff (two BSGS transforms, summed)        z = U (d_re + i d_im) R / (4 pi)
+    The output decrypts to the input's slots at a higher level."""
+    prm = ev.prm
+    L, K, r, n1, n2 = cfg["level"], cfg["K"], cfg["r"], cfg["n1"], cfg["n2"]
+    S0 = ct.scale
+    z = ev.mod_raise(ct, L)
+    us = [ev.lt_bsgs(keys, z, cfg[nm], n1, n2, cfg["cts_scale"]) for nm in ("cts_re", "cts_im")]
+    inv = 1.0 / (K * (float(prm.primes[0]) / S0))
+    ds = []
+    for u in us:
+        x = ev.add(u, ev.rot(keys, u, CONJ_STEP))
+        xn = ev.mul_const(x, inv, prm.scale, x.level - 1)
+        d = eval_poly15(ev, keys, xn, cfg["poly"], prm.scale)
+        for _ in range(r):
+            d = ev.add_const(ev.mul_ct(keys, d, d, None, d.level - 1), -2.0)  # natural scale (R9)
+        ds.append(d)
+    o_re = ev.lt_bsgs(keys, ds[0], cfg["stc_re"], n1, n2, cfg["stc_scale"])
+    o_im = ev.lt_bsgs(keys, ds[1], cfg["stc_im"], n1, n2, cfg["stc_scale"])
+    return ev.add(o_re, o_im)

@@ -26,6 +26,14 @@ PARAM_SETS = {
     # configs[4]'s prime structure on a 2^12 ring: CPU-sized check of the (7,15,15) circuit numerics.
     "argmax_small": dict(logn=12, q=[("nearest", 45, 30)], p=[("below", 46, 10)],
                          alpha=10, log_scale=45),
+    # Bootstrapping (readings R32-R35): q_0 ~ 2^60 over scale 2^50 (R = q_0 / S ~ 2^10),
+    # a 50-bit chain long enough for one bootstrap (8 + r levels) plus a few, 7 special 60-bit primes
+    # (alpha = 7: every digit < P).  boot_tiny: CPU-sized (oracle pins); boot: the smallest ring the
+    # library takes (N = 2^12, 2048 slots, BSGS 64 x 32).
+    "boot_tiny": dict(logn=8, q=[("below", 60, 1), ("nearest", 50, 18)], p=[("below", 60, 7)],
+                      alpha=7, log_scale=50),
+    "boot": dict(logn=12, q=[("below", 60, 1), ("nearest", 50, 20)], p=[("below", 60, 7)],
+                 alpha=7, log_scale=50),
     # BASELINE configs[1]: NTT microbench, 24 x 60-bit primes, N = 2^16.
     "ntt": dict(logn=16, q=[("below", 60, 24)], p=[], alpha=8, log_scale=50),
     # BASELINE configs[2]/[3]: 24 x 60-bit q, dnum = 3 -> alpha = 8, 8 special 60-bit primes, scale 2^50.

@@ -657,3 +657,107 @@ def test_argmax_small_ring_7_15_15_oracle():
     mean = scores.mean(axis=1)
     ok = np.abs(mean[:, 0] - mean[:, 1]) >= 2.0 ** -7
     assert (plan.labels(dec, lay)[ok] == plan.true_labels(scores)[ok]).all()
+
+
+# ---------------------------------------------------------------------------------------------
+# O-20 bootstrapping building blocks (readings R32-R35)
+# ---------------------------------------------------------------------------------------------
+BOOT_TINY = dict(n1=16, n2=8, K=24, r=8)
+
+
+@pytest.fixture(scope="module")
+def boot_tiny():
+    prm = ckks.Params(synth.PARAM_SETS["boot_tiny"])
+    ev = ckks.Oracle(prm)
+    keys = ev.keygen(7, plan.boot_rotations(BOOT_TINY["n1"], BOOT_TINY["n2"]))
+    return prm, ev, keys
+
+
+def test_conjugation_is_complex_conjugate(boot_tiny):
+    """R32: sigma_{2N-1} (step CONJ) maps the slots of a complex message to their complex conjugates."""
+    prm, ev, keys = boot_tiny
+    n = prm.N // 2
+    rng = np.random.default_rng(8)
+    z = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    ct = ev.encrypt(keys, z, prm.scale, 3, level=4)
+    assert ckks.galois_elt(prm, ckks.CONJ) == 2 * prm.N - 1
+    out = ev.rotate_raw(keys, ct, ckks.CONJ)
+    m = np.array([float(v) for v in ev.decrypt_int(keys, out)])
+    got = ckks.decode(prm, m, out.scale)
+    assert np.abs(got - np.conj(z)).max() < 2 ** -30
+
+
+def test_mod_raise_adds_multiple_of_q0(boot_tiny):
+    """R33: the raised ciphertext decrypts to t = m + q_0 I over the integers, |I_k| <= (h + 1)/2 with h the
+    secret's Hamming weight (|c0 + c1 s| <= q_0 (1 + h) / 2 for centred c0, c1)."""
+    prm, ev, keys = boot_tiny
+    ct = ev.encrypt(keys, np.linspace(-1, 1, prm.N // 2), prm.scale, 4, level=0)
+    up = ev.mod_raise(ct, prm.L)
+    assert up.level == prm.L and up.scale == ct.scale
+    t, m = ev.decrypt_int(keys, up), ev.decrypt_int(keys, ct)
+    q0, h = prm.primes[0], int(np.count_nonzero(keys.s))
+    assert all((a - b) % q0 == 0 for a, b in zip(t, m))
+    I = [(a - b) // q0 for a, b in zip(t, m)]
+    assert max(abs(i) for i in I) <= (h + 1) // 2
+    assert any(i != 0 for i in I)  # a non-trivial raise
+
+
+def test_boot_matrices_invert_decoding(boot_tiny):
+    """R34: for a real polynomial t, the slots z_j = sum_k t_k zeta^{5^j k} (the definition, written out here)
+    satisfy A z = t_lo + i t_hi and U (t_lo + i t_hi) = z."""
+    prm = boot_tiny[0]
+    N, n = prm.N, prm.N // 2
+    rng = np.random.default_rng(2)
+    t = rng.integers(-1000, 1000, N).astype(np.float64)
+    z = np.array([sum(t[k] * np.exp(1j * np.pi * (pow(5, j, 2 * N) * k % (2 * N)) / N) for k in range(N))
+                  for j in range(n)])
+    M = plan.boot_matrices(prm, 1.0)
+    A = 2 * M["cts_re"]
+    w = A @ z
+    assert np.abs(w - (t[:n] + 1j * t[n:])).max() < 1e-8
+    U = M["stc_re"] * 4 * np.pi
+    assert np.abs(U @ (t[:n] + 1j * t[n:]) - z).max() < 1e-7
+    assert np.allclose(M["cts_im"], -1j * M["cts_re"]) and np.allclose(M["stc_im"], 1j * M["stc_re"])
+
+
+def test_boot_poly_is_doubled_cosine():
+    """R35: the degree-15 Taylor coefficients match 2 cos((2 pi K x - pi/2) / 2^r) on [-1, 1] (closed form),
+    and r double-angle steps d <- d^2 - 2 turn it into 2 sin(2 pi K x)."""
+    K, r = 24, 8
+    c = plan.boot_poly(K, r)
+    x = np.linspace(-1, 1, 2001)
+    d = np.polynomial.polynomial.polyval(x, c)
+    assert np.abs(d - 2 * np.cos((2 * np.pi * K * x - np.pi / 2) / 2 ** r)).max() < 1e-14
+    for _ in range(r):
+        d = d * d - 2
+    assert np.abs(d - 2 * np.sin(2 * np.pi * K * x)).max() < 1e-9
+
+
+def test_eval_poly15_general(boot_tiny):
+    """R35: the general degree-15 plan decrypts to sum_i c_i x^i (numpy polyval) and uses 5 levels."""
+    prm, ev, keys = boot_tiny
+    n = prm.N // 2
+    rng = np.random.default_rng(12)
+    z = rng.uniform(-1, 1, n)
+    c = list(rng.uniform(-1, 1, 16) / np.arange(1, 17))
+    ct = ev.encrypt(keys, z, prm.scale, 9, level=8)
+    out = plan.eval_poly15(ev, keys, ct, c, prm.scale)
+    assert out.level == 3 and out.scale == prm.scale
+    assert np.abs(ev.decrypt(keys, out).real - np.polynomial.polynomial.polyval(z, c)).max() < 2 ** -30
+
+
+def test_bootstrap_refreshes_levels(boot_tiny):
+    """N3 end to end: a level-0 ciphertext bootstraps to level L - (8 + r) and still decrypts to its slots
+    (within 2^-14; the precision budget of DESIGN.md R35)."""
+    prm, ev, keys = boot_tiny
+    n = prm.N // 2
+    rng = np.random.default_rng(3)
+    z = rng.uniform(-1, 1, n)
+    ct = ev.encrypt(keys, z, prm.scale, 5, level=0)
+    cfg = plan.boot_config(ev, ct.scale, prm.L, BOOT_TINY["K"], BOOT_TINY["r"], BOOT_TINY["n1"], BOOT_TINY["n2"])
+    out = plan.bootstrap(ev, keys, ct, cfg)
+    assert out.level == prm.L - plan.boot_depth(BOOT_TINY["r"])
+    assert np.abs(ev.decrypt(keys, out).real - z).max() < 2 ** -14
+    # and it computes on: one more product after the refresh
+    sq = ev.mul_ct(keys, out, out, None, out.level - 1)
+    assert np.abs(ev.decrypt(keys, sq).real - z * z).max() < 2 ** -13
