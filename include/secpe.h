@@ -47,6 +47,10 @@ enum {
     SECPE_ENOMEM = -8
 };
 
+/* Rotation "step" meaning complex conjugation of the slots (reading R32): the Galois element 2N - 1
+ * (X -> X^-1).  Accepted wherever a rotation step is (secpe_keygen's rot_steps, secpe_rotate). */
+#define SECPE_CONJ ((int32_t)(-2147483647 - 1))
+
 typedef struct secpe_ctx secpe_ctx;   /* opaque: parameters + device tables + stream */
 typedef struct secpe_keys secpe_keys; /* opaque: secret/public/relinearisation/Galois keys (device) */
 
@@ -115,6 +119,13 @@ size_t secpe_ct_bytes(const secpe_ctx *ctx, int32_t level);
  * rotation step in rot_steps (host[n_rot]; >0 RotL, <0 RotR).  Hybrid digits (reading R7). */
 int secpe_keygen(secpe_ctx *ctx, uint64_t seed, const int32_t *rot_steps, int32_t n_rot,
                  secpe_keys **out);
+/* As secpe_keygen with a sparse ternary secret of Hamming weight `hamming` (reading R36, the secret
+ * bootstrapping uses to keep |I| and the EvalMod range K small): draw x_ctr = SplitMix64(seed, tag 1)
+ * for ctr = 0, 1, ...; the top log_n bits pick a coefficient; a still-zero one becomes -1 (x odd) or
+ * +1; stop at `hamming` nonzeros.  hamming = 0: the uniform ternary secret of secpe_keygen.
+ * SECPE_EINVAL: hamming outside [0, N]. */
+int secpe_keygen_sparse(secpe_ctx *ctx, uint64_t seed, int32_t hamming, const int32_t *rot_steps, int32_t n_rot,
+                        secpe_keys **out);
 /* Frees the key material.  Synchronises the owning context's stream and destroys every CUDA graph
  * secpe_enc_argmax captured with these keys (a later keys object at the same address never replays
  * them).  Keys may be destroyed before or after their context; null is a no-op. */
@@ -219,6 +230,55 @@ int secpe_linear_transform_bsgs(secpe_ctx *ctx, const secpe_keys *keys, const se
                                 int32_t n1, int32_t n2, double pt_scale, secpe_ct *out);
 /* Rescale by q_level: round(c / q_l) (round half up, reading R12).  out level = in level - 1,
  * out scale = scale / q_l.  out must not alias. */
+/* ---- bootstrapping (the paper bootstraps at L = 35) ----
+ * ModRaise (reading R33): a level-0 ciphertext (c0, c1) mod q_0, read as integer polynomials with
+ * centred coefficients in (-q_0/2, q_0/2], reduced mod every prime of Q_level.  It then decrypts to
+ * t = m + q_0 I, I a small integer polynomial.  out: level `level` (1 <= level <= L), in's scale,
+ * out->data sized secpe_ct_bytes(level), must not alias in.  SECPE_EINVAL: in not at level 0. */
+int secpe_mod_raise(secpe_ctx *ctx, const secpe_ct *in, int32_t level, secpe_ct *out);
+/* CKKS bootstrapping (readings R32-R35), for full slot packing (N/2 slots):
+ *   ModRaise to `level`; CoeffToSlot u = M_re z, u' = M_im z (BSGS transforms, R31);
+ *   x = u + conj(u), x' = u' + conj(u') (the polynomial's coefficients t_k / S and t_{k+N/2} / S);
+ *   x / (K R), R = q_0 / S; d = p(x) with p ~ 2 cos((2 pi K x - pi/2) / 2^r) (power basis, degree 15);
+ *   r times d <- d^2 - 2 (so d = 2 sin(2 pi t / q_0)); SlotToCoeff out = W_re d + W_im d' (BSGS).
+ * The caller encodes the four matrices' diagonals (NTT form, pts[g][j] = encode(RotR(diag_{g n1 + j},
+ * g n1)) as for secpe_linear_transform_bsgs): M_re = A/2, M_im = -i A/2, A[k][j] = zeta^{-5^j k} / (N/2);
+ * W_re = c U, W_im = i c U, U[j][k] = zeta^{5^j k}, c = R / (4 pi).  Keys: Galois keys for 1..n1-1,
+ * n1, ..., (n2-1) n1 and SECPE_CONJ.  The input must decrypt to m with |I| + |m| / q_0 <= K. */
+typedef struct {
+    int32_t level;           /* ModRaise target L */
+    int32_t n1, n2;          /* BSGS split of the N/2 diagonals: n1 * n2 == N/2 */
+    double K;                /* EvalMod range (above) */
+    int32_t r;               /* double-angle steps */
+    const double *poly;      /* host[16]: c_0..c_15 */
+    const uint64_t *cts_re;  /* dev uint64[n2][n1][level+1][N], encoded at cts_scale */
+    const uint64_t *cts_im;
+    double cts_scale;
+    const uint64_t *stc_re;  /* dev uint64[n2][n1][level-7-r+1][N], encoded at stc_scale */
+    const uint64_t *stc_im;
+    double stc_scale;
+} secpe_boot_cfg;
+/* Library-built bootstrapping material (the caller-side encoding above done by the library, host
+ * double precision + device NTT): the polynomial = Taylor coefficients of 2 cos(a x + b), a = 2 pi K / 2^r,
+ * b = -pi / 2^(r+1), and the four matrices for inputs of scale in_scale, CoeffToSlot encoded at
+ * q_level, SlotToCoeff at q_{level-7-r}.  Device memory: 2 n1 n2 ((level + 1) + (level - 6 - r)) N words.
+ * secpe_boot_get_cfg fills *cfg with pointers into it (valid until secpe_boot_destroy).
+ * Errors: SECPE_EINVAL (n1 n2 != N/2, K <= 0, r outside [0, 30]), SECPE_ELEVEL, SECPE_EOVERFLOW. */
+typedef struct secpe_boot secpe_boot;
+int secpe_boot_create(secpe_ctx *ctx, int32_t level, double K, int32_t r, int32_t n1, int32_t n2, double in_scale,
+                      secpe_boot **out);
+int secpe_boot_get_cfg(const secpe_boot *boot, secpe_boot_cfg *cfg);
+void secpe_boot_destroy(secpe_boot *boot);
+/* Copy matrix `which` (0 cts_re, 1 cts_im, 2 stc_re, 3 stc_im) to host uint64[n2][n1][limbs][N], for
+ * parity tests (synchronises); n_words must equal that size. */
+int secpe_boot_export(secpe_ctx *ctx, const secpe_boot *boot, int32_t which, uint64_t *host_out, size_t n_words);
+/* Levels one bootstrap consumes (8 + r): out level = cfg->level - secpe_boot_depth(cfg). */
+int32_t secpe_boot_depth(const secpe_boot_cfg *cfg);
+/* in: level 0; out->data sized secpe_ct_bytes(cfg->level - secpe_boot_depth(cfg)); out->level / scale
+ * set.  Errors: SECPE_EINVAL (shape, n1 n2 != N/2, level), SECPE_ENOKEY (a missing Galois key). */
+int secpe_bootstrap(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const secpe_boot_cfg *cfg,
+                    secpe_ct *out);
+
 int secpe_rescale(secpe_ctx *ctx, const secpe_ct *in, secpe_ct *out);
 /* PAPER.md:104-105 RotL(a, steps) (steps < 0: RotR(a, -steps)).  out must not alias. */
 int secpe_rotate(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t steps,

@@ -72,6 +72,7 @@ def lib():
             "o_uniform": (U, [U, U, U, U, I, U]),
             "o_sample_uniform": (None, [U, U, I, I, u64p, intp, u64p]),
             "o_sample_ternary": (None, [U, U, I, i64p]),
+            "o_sample_sparse": (None, [U, U, I, I, i64p]),
             "o_sample_gauss": (None, [U, U, I, u64p, I, i64p]),
             "o_int_to_ntt": (None, [ctypes.c_void_p, i64p, I, intp, u64p]),
             "o_keygen_pk": (None, [ctypes.c_void_p, U, u64p, u64p, I, u64p]),
@@ -362,14 +363,20 @@ class Oracle:
         self.counts = {}
 
     # ---- keys ----------------------------------------------------------------
-    def keygen(self, seed, rot_steps=()):
+    def keygen(self, seed, rot_steps=(), h=0):
+        """h = 0: uniform ternary secret (R6); h > 0: sparse ternary secret of Hamming weight h (R36)."""
         prm = self.prm
         L = lib()
         N, ne = prm.N, prm.nq + prm.np_
         k = Keys()
         k.seed = seed
         s = np.zeros(N, dtype=np.int64)
-        L.o_sample_ternary(seed, L.o_tag(1, 0, 0), prm.logn, P(s))
+        if h:
+            if not 0 < h <= N:
+                raise ValueError("Hamming weight out of range")
+            L.o_sample_sparse(seed, L.o_tag(1, 0, 0), prm.logn, h, P(s))
+        else:
+            L.o_sample_ternary(seed, L.o_tag(1, 0, 0), prm.logn, P(s))
         k.s = s
         k.s_ntt = np.zeros((ne, N), dtype=np.uint64)
         L.o_int_to_ntt(prm.cptr, P(s), ne, P(np.arange(ne, dtype=np.int32)), P(k.s_ntt))

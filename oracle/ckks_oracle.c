@@ -260,6 +260,20 @@ void o_sample_ternary(u64 seed, u64 tag, int logn, i64 *out) {
         out[k] = v == 0 ? 0 : (v == 1 ? 1 : -1);
     }
 }
+/* sparse ternary secret of Hamming weight h (reading R36, bootstrapping's sparse secret): draw
+ * x_ctr for ctr = 0, 1, ...; position = top logn bits of x; if that coefficient is still 0 it becomes
+ * -1 when x is odd, else +1; stop after h nonzeros.  out must be zeroed; h <= N. */
+void o_sample_sparse(u64 seed, u64 tag, int logn, int h, i64 *out) {
+    int cnt = 0;
+    for (u64 ctr = 0; cnt < h; ctr++) {
+        u64 x = o_draw(seed, tag, ctr);
+        u64 pos = x >> (64 - logn);
+        if (out[pos] == 0) {
+            out[pos] = (x & 1) ? -1 : 1;
+            cnt++;
+        }
+    }
+}
 /* discrete Gaussian via CDT: sign = top bit, u = low 63 bits, |e| = min{m : u < T[m]} */
 void o_sample_gauss(u64 seed, u64 tag, int logn, const u64 *cdt, int ncdt, i64 *out) {
     u64 n = (u64)1 << logn;

@@ -242,10 +242,11 @@ def boot_matrices(prm, R):
     SlotToCoeff: c U and i c U with c = R / (4 pi) (the doubled cosine's 2 and EvalMod's R / 2 pi)."""
     from oracle.ckks import _rot_group
     N, n = prm.N, prm.N // 2
-    e = _rot_group(N).astype(np.float64)
-    k = np.arange(n, dtype=np.float64)
-    A = np.exp(-1j * np.pi * np.outer(k, e) / N) / n
-    U = np.exp(1j * np.pi * np.outer(e, k) / N)
+    e = _rot_group(N).astype(np.int64)
+    k = np.arange(n, dtype=np.int64)
+    # zeta^m with the exponent m = e_j k reduced mod 2N exactly (zeta^{2N} = 1) before the angle is formed
+    A = np.exp(-1j * np.pi * (np.outer(k, e) % (2 * N)).astype(np.float64) / N) / n
+    U = np.exp(1j * np.pi * (np.outer(e, k) % (2 * N)).astype(np.float64) / N)
     c = R / (4.0 * np.pi)
     return dict(cts_re=A / 2, cts_im=-0.5j * A, stc_re=c * U, stc_im=1j * c * U)
 

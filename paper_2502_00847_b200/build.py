@@ -18,7 +18,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-ffp-contract=off",
          "-Xptxas", "-warn-spills"]
 SOURCES = ["ntt.cu", "ops.cu", "ks.cu", "bconv_tc.cu", "sample.cu", "context.cu", "eval.cu", "plan.cu", "client.cu",
-           "encode.cpp", "abi.cpp"]
+           "encode.cpp", "boot.cpp", "abi.cpp"]
 
 
 def _headers_mtime():

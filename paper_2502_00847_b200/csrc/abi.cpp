@@ -9,7 +9,7 @@
 #include "../../include/secpe.h"
 #include "context.h"
 
-Keys *keygen(Ctx &c, u64 seed, const int *rot, int n_rot);
+Keys *keygen(Ctx &c, u64 seed, const int *rot, int n_rot, int h);
 void encrypt_coeffs(Ctx &c, const Keys &k, const i64 *coeffs, int level, u64 seed, u64 *ct);
 void decrypt_residues(Ctx &c, const Keys &k, const CtView &ct, u64 *host_out);
 void decrypt_slots(Ctx &c, const Keys &k, const CtView &ct, double *slots, size_t n);
@@ -214,11 +214,16 @@ size_t secpe_ct_bytes(const secpe_ctx *ctx, int32_t level) {
 }
 
 int secpe_keygen(secpe_ctx *ctx, uint64_t seed, const int32_t *rot_steps, int32_t n_rot, secpe_keys **out) {
+    return secpe_keygen_sparse(ctx, seed, 0, rot_steps, n_rot, out);
+}
+int secpe_keygen_sparse(secpe_ctx *ctx, uint64_t seed, int32_t hamming, const int32_t *rot_steps, int32_t n_rot,
+                        secpe_keys **out) {
     return guard([&] {
         REQUIRE(ctx && out && (n_rot == 0 || rot_steps), SECPE_EINVAL, "null argument");
         REQUIRE(ctx->c.np >= 1, SECPE_EINVAL, "key generation needs at least one special prime");
+        REQUIRE(hamming >= 0 && hamming <= ctx->c.N, SECPE_EINVAL, "Hamming weight out of range");
         auto h = std::make_unique<secpe_keys>();
-        h->k = keygen(ctx->c, seed, rot_steps, n_rot);
+        h->k = keygen(ctx->c, seed, rot_steps, n_rot, hamming);
         h->k->owner = &ctx->c;
         ctx->c.live_keys.insert(h->k);
         *out = h.release();
@@ -475,6 +480,80 @@ int secpe_linear_transform(secpe_ctx *ctx, const secpe_keys *keys, const secpe_c
         std::vector<int> st(steps, steps + n);
         ev_linear_transform(c, *keys->k, vi, pts, (long)(vi.level + 1) * c.N, st.data(), n, vo);
         vo.scale = osc;
+        set_out(out, vo);
+    });
+}
+int secpe_mod_raise(secpe_ctx *ctx, const secpe_ct *in, int32_t level, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && in && out && out->data, SECPE_EINVAL, "null argument");
+        Ctx &c = ctx->c;
+        CtView vi = view_of(c, in);
+        REQUIRE(vi.level == 0, SECPE_EINVAL, "mod_raise takes a level-0 ciphertext");
+        REQUIRE(level >= 1 && level < c.nq, SECPE_EINVAL, "target level out of range");
+        REQUIRE(out->data != in->data, SECPE_EINVAL, "out must not alias in");
+        CtView vo = compact_view(c, out->data, 1, level, vi.scale);
+        ev_mod_raise(c, vi, vo);
+        set_out(out, vo);
+    });
+}
+static BootCfg boot_cfg(const Ctx &c, const secpe_boot_cfg *cfg) {
+    REQUIRE(cfg && cfg->poly && cfg->cts_re && cfg->cts_im && cfg->stc_re && cfg->stc_im, SECPE_EINVAL,
+            "bad bootstrap config");
+    REQUIRE(cfg->n1 >= 1 && cfg->n2 >= 1 && (long)cfg->n1 * cfg->n2 == c.N / 2, SECPE_EINVAL, "n1 n2 must be N/2");
+    REQUIRE(cfg->r >= 0 && cfg->r <= 30 && cfg->K > 0, SECPE_EINVAL, "bad EvalMod range");
+    BootCfg b{cfg->level, cfg->n1, cfg->n2, cfg->r, cfg->K, std::vector<double>(cfg->poly, cfg->poly + 16),
+              cfg->cts_re, cfg->cts_im, cfg->stc_re, cfg->stc_im, cfg->cts_scale, cfg->stc_scale};
+    REQUIRE(b.level < c.nq && b.level - boot_depth(b) >= 0, SECPE_ELEVEL, "not enough levels for a bootstrap");
+    return b;
+}
+struct secpe_boot {
+    std::unique_ptr<BootSetup> b;
+};
+int secpe_boot_create(secpe_ctx *ctx, int32_t level, double K, int32_t r, int32_t n1, int32_t n2, double in_scale,
+                      secpe_boot **out) {
+    return guard([&] {
+        REQUIRE(ctx && out && in_scale > 0, SECPE_EINVAL, "null argument");
+        auto h = std::make_unique<secpe_boot>();
+        h->b.reset(boot_setup(ctx->c, level, K, r, n1, n2, in_scale));
+        *out = h.release();
+    });
+}
+int secpe_boot_get_cfg(const secpe_boot *boot, secpe_boot_cfg *cfg) {
+    return guard([&] {
+        REQUIRE(boot && boot->b && cfg, SECPE_EINVAL, "null argument");
+        const BootCfg &b = boot->b->cfg;
+        *cfg = secpe_boot_cfg{b.level, b.n1, b.n2, b.K, b.r, b.poly.data(), b.cts_re, b.cts_im, b.cts_scale,
+                              b.stc_re, b.stc_im, b.stc_scale};
+    });
+}
+void secpe_boot_destroy(secpe_boot *boot) { delete boot; }
+int secpe_boot_export(secpe_ctx *ctx, const secpe_boot *boot, int32_t which, uint64_t *host_out, size_t n_words) {
+    return guard([&] {
+        REQUIRE(ctx && boot && boot->b && host_out && which >= 0 && which < 4, SECPE_EINVAL, "bad argument");
+        const BootSetup &b = *boot->b;
+        const DevBuf *m[4] = {&b.cts_re, &b.cts_im, &b.stc_re, &b.stc_im};
+        REQUIRE(n_words == m[which]->words, SECPE_EINVAL, "n_words does not match the matrix size");
+        CUDA_CHECK(cudaMemcpyAsync(host_out, m[which]->p, n_words * 8, cudaMemcpyDeviceToHost, ctx->c.st));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->c.st));
+    });
+}
+int32_t secpe_boot_depth(const secpe_boot_cfg *cfg) { return cfg ? 8 + cfg->r : -1; }
+int secpe_bootstrap(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const secpe_boot_cfg *cfg,
+                    secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && keys && in && out && out->data, SECPE_EINVAL, "null argument");
+        Ctx &c = ctx->c;
+        BootCfg b = boot_cfg(c, cfg);
+        CtView vi = view_of(c, in);
+        REQUIRE(vi.level == 0, SECPE_EINVAL, "bootstrap takes a level-0 ciphertext");
+        REQUIRE(out->data != in->data, SECPE_EINVAL, "out must not alias in");
+        for (int j = 1; j < b.n1; j++)
+            REQUIRE(keys->k->gk.count(galois_elt(c, j)), SECPE_ENOKEY, "no Galois key for a baby step");
+        for (int g = 1; g < b.n2; g++)
+            REQUIRE(keys->k->gk.count(galois_elt(c, g * b.n1)), SECPE_ENOKEY, "no Galois key for a giant step");
+        REQUIRE(keys->k->gk.count(galois_elt(c, kConjStep)), SECPE_ENOKEY, "no conjugation key");
+        CtView vo = compact_view(c, out->data, 1, b.level - boot_depth(b), 0.0);
+        run_bootstrap(c, *keys->k, vi, b, vo);
         set_out(out, vo);
     });
 }

@@ -46,12 +46,22 @@ static void gen_swk(Ctx &c, const Keys &k, u64 seed, u64 g, const u64 *sp, DevBu
     }
 }
 
-Keys *keygen(Ctx &c, u64 seed, const int *rot, int n_rot) {
+Keys *keygen(Ctx &c, u64 seed, const int *rot, int n_rot, int h) {
     auto k = std::make_unique<Keys>();
     const int P = c.nprimes();
     const long N = c.N;
     k->s = DevBuf((size_t)P * N, c.st);
-    small_to_ntt(c, seed, tag(1, 0, 0), 0, k->s.p, allmap(c));
+    if (h > 0) {  // sparse secret (R36), sampled on the host
+        std::vector<i64> sh(N);
+        h_sample_sparse(seed, tag(1, 0, 0), c.logn, h, sh.data());
+        DevBuf m(N, c.st);
+        CUDA_CHECK(cudaMemcpyAsync(m.p, sh.data(), N * 8, cudaMemcpyHostToDevice, c.st));
+        k_int_to_rows(c.tab, c.logn, (const i64 *)m.p, k->s.p, allmap(c), c.st);
+        ev_ntt(c, RowsArg{k->s.p, 2L * P * N, (long)P * N}, 1, allmap(c), false);
+        CUDA_CHECK(cudaStreamSynchronize(c.st));  // sh is host memory of this frame
+    } else {
+        small_to_ntt(c, seed, tag(1, 0, 0), 0, k->s.p, allmap(c));
+    }
     // public key (-a s + e, a) over Q_L
     k->pk = DevBuf(2L * c.nq * N, c.st);
     {

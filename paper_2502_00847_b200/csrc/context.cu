@@ -155,6 +155,7 @@ void h_cdt(u64 *out, int n) {
 }
 
 u64 galois_elt(const Ctx &c, int steps) {
+    if (steps == kConjStep) return (u64)(2 * c.N - 1);  // conjugation (R32)
     const long half = c.N / 2;
     long s = ((steps % half) + half) % half;
     return h_powmod(5, (u64)s, (u64)(2 * c.N));

@@ -1,5 +1,6 @@
 // context.h -- library context, keys, device buffers and the ciphertext evaluator.
 #pragma once
+#include <climits>
 #include <map>
 #include <set>
 #include <memory>
@@ -220,6 +221,7 @@ void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView 
 void ev_rotate_hoisted(Ctx &c, const Keys &k, const CtView &in, const int *steps, int n_steps, const CtView *outs);
 void ev_linear_transform(Ctx &c, const Keys &k, const CtView &in, const u64 *pts, long pt_stride, const int *steps,
                          int n, const CtView &out);
+void ev_mod_raise(Ctx &c, const CtView &in, const CtView &out);
 void ev_linear_transform_bsgs(Ctx &c, const Keys &k, const CtView &in, const u64 *pts, long pt_stride, int n1, int n2,
                               const CtView &out);
 void ev_mul_plain_ntt(Ctx &c, const CtView &a, const u64 *pt, const CtView &out);
@@ -230,11 +232,30 @@ void encode_real(const Ctx &c, const double *slots, size_t n, double scale, std:
 void encode_int(const Ctx &c, const double *slots, size_t n, double scale, i64 *out);
 void decode_real(const Ctx &c, const std::vector<double> &coef, double scale, double *slots, size_t n);
 void encode_mask(const Ctx &c, const double *slots, size_t n, double delta, i64 *out);
+void encode_complex_int(const Ctx &c, const double *re, const double *im, size_t n, double scale, i64 *out);
 
 // circuits (plan.cu)
 struct SignCfg {
     std::vector<std::vector<double>> stages;
 };
+// CKKS bootstrapping configuration (readings R32-R35; secpe_boot_cfg)
+struct BootCfg {
+    int level, n1, n2, r;
+    double K;
+    std::vector<double> poly;  // 16 power-basis coefficients
+    const u64 *cts_re, *cts_im, *stc_re, *stc_im;
+    double cts_scale, stc_scale;
+};
+constexpr int kConjStep = INT32_MIN;  // SECPE_CONJ: slot conjugation, Galois element 2N - 1 (R32)
+int boot_depth(const BootCfg &b);
+// library-built bootstrapping material (secpe_boot_create): the EvalMod polynomial and the four encoded
+// matrices, NTT form, [n2][n1][limbs][N] each
+struct BootSetup {
+    BootCfg cfg;
+    DevBuf cts_re, cts_im, stc_re, stc_im;
+};
+BootSetup *boot_setup(Ctx &c, int level, double K, int r, int n1, int n2, double in_scale);
+void run_bootstrap(Ctx &c, const Keys &k, const CtView &in, const BootCfg &b, CtView &out);
 struct Layout {
     int queries, prompts, classes, block;
 };

@@ -80,6 +80,29 @@ void encode_int(const Ctx &c, const double *slots, size_t n, double scale, i64 *
     }
 }
 
+// complex slots (bootstrapping's matrix diagonals, R34): w[5^j] = z_j, w[-5^j] = conj(z_j); for real z the
+// same integers as encode_int
+void encode_complex_int(const Ctx &c, const double *re, const double *im, size_t n, double scale, i64 *out) {
+    const long N = c.N;
+    if ((long)n > N / 2) throw SecpeError{-1, "encode: more values than slots"};
+    std::vector<cd> w(2 * N, cd(0, 0));
+    const auto e = rot_group(N);
+    for (size_t j = 0; j < n; j++) {
+        w[e[j]] = cd(re[j], im[j]);
+        w[(2 * N - e[j]) % (2 * N)] = cd(re[j], -im[j]);
+    }
+    std::vector<cd> W(N);
+    for (long t = 0; t < N; t++) W[t] = w[2 * t + 1];
+    fft(W, -1);
+    for (long k = 0; k < N; k++) {
+        const double ang = -M_PI * (double)k / (double)N;
+        const cd z = cd(std::cos(ang), std::sin(ang)) * W[k];
+        const double r = std::round(z.real() / (double)N * scale);
+        if (!(std::fabs(r) < 4611686018427387904.0)) throw SecpeError{-6, "encoded coefficient exceeds 2^62"};
+        out[k] = (i64)r;
+    }
+}
+
 // R16: M_k = rha(delta * rha(m_k 2^24) / 2^24), m_k the unit-scale real coefficients
 void encode_mask(const Ctx &c, const double *slots, size_t n, double delta, i64 *out) {
     std::vector<double> coef;

@@ -466,6 +466,21 @@ void ev_linear_transform(Ctx &c, const Keys &k, const CtView &in, const u64 *pts
     ev_rescale(c, va, out);
 }
 
+// ModRaise (R33, bootstrapping's first step): level-0 (c0, c1) -> INTT of limb 0 -> centred lift ->
+// residues mod q_0..q_L -> NTT.  The result decrypts to t = m + q_0 I over the integers.
+void ev_mod_raise(Ctx &c, const CtView &in, const CtView &out) {
+    if (in.level != 0) throw SecpeError{-1, "mod_raise: input must be at level 0"};
+    if (out.level < 1 || out.n != in.n) throw SecpeError{-1, "mod_raise: output level"};
+    const long N = c.N;
+    const int np = 2 * in.n;
+    DevBuf coef((size_t)np * N, c.st);
+    k_copy_rows(c.logn, crows_of(in), RowsArg{coef.p, 2 * N, N}, np, 1, c.st);
+    ev_ntt(c, RowsArg{coef.p, 2 * N, N}, np, qmap(1), true);
+    k_mod_raise(c.tab, c.logn, coef.p, rows_of(out), np, out.level + 1, c.st);
+    ev_ntt(c, rows_of(out), np, qmap(out.level + 1), false);
+    c.cnt.launches += 2;
+}
+
 // Baby-step giant-step linear transform (R31): out = Rescale( sum_{g<n2} RotL( sum_{j<n1} pt_{g,j} (.) RotL(in, j),
 // g n1 ) ); the baby rotations hoisted (R29), each giant rotation's addition fused into its epilogue.
 // pt_{g,j}: dev [level+1][N] rows at pts + (g n1 + j) pt_stride.

@@ -140,9 +140,13 @@ void k_rr_conv(const Tab &tab, int logn, const u64 *acc, long acc_ct_stride, int
 void k_sample_uniform(const Tab &tab, int logn, u64 seed, u64 tag, u64 *out, LimbMap lm, cudaStream_t st);
 // signed small polynomial: kind 0 ternary, 1 Gaussian (cdt in constant memory)
 void k_sample_small(int logn, u64 seed, u64 tag, int kind, i64 *out, cudaStream_t st);
+// host: sparse ternary secret of Hamming weight h (reading R36), out[N]
+void h_sample_sparse(u64 seed, u64 tag, int logn, int h, i64 *out);
 void set_cdt(const u64 *cdt, int n);
 // residues of a signed int64 polynomial: out[l][k] = m[k] mod q_l (coefficient form)
 void k_int_to_rows(const Tab &tab, int logn, const i64 *m, u64 *out, LimbMap lm, cudaStream_t st);
+// ModRaise (R33): centred lift of coefficient-form rows mod q_0 (coef[n_polys][N]) to nl limbs
+void k_mod_raise(const Tab &tab, int logn, const u64 *coef, RowsArg out, int n_polys, int nl, cudaStream_t st);
 // out = -a*s + e  (+ gadget * sp on limbs with gadget flag) ; all NTT form, rows lm
 void k_key_combine(const Tab &tab, int logn, const u64 *a, const u64 *s, const u64 *e, const u64 *sp,
                    const LimbConst *gadget, u64 *out, LimbMap lm, cudaStream_t st);

@@ -355,7 +355,8 @@ __global__ void ks_inner_kernel(Tab tab, int logn, const u64 *__restrict__ d, lo
     long kx = k;
     if (galois > 1) {
         bool sw;
-        kx = gal_src(k & ~1L, logn, galois, sw) + ((k & 1) ^ (sw ? 1 : 0));
+        const long base = gal_src(k & ~1L, logn, galois, sw);  // sets sw: sequenced before its use
+        kx = base + ((k & 1) ^ (sw ? 1 : 0));
     }
     const bool qrow = ten.a.p && e < nl;
     const int ne = nl + np, nk = nq_total + np;

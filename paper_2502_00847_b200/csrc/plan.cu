@@ -200,6 +200,68 @@ struct Ev {
         return out;
     }
 
+    // ---- bootstrapping (readings R32-R35) ---------------------------------------
+    Val mod_raise(const Val &x, int level) {
+        Val out = fresh(level, x.scale());
+        ev_mod_raise(c, x.v, out.v);
+        c.log("MODRAISE", 0, level, x.scale(), "");
+        return out;
+    }
+    // Rescale(sum_g RotL(sum_j pt_{g,j} (.) RotL(x, j), g n1)) (R31); output scale (S_x pt_scale) / q_l
+    Val lt_bsgs(const Val &x, const u64 *pts, int n1, int n2, double pt_scale) {
+        if (n != 1) throw SecpeError{-1, "lt_bsgs: one ciphertext"};
+        const int l = x.level();
+        const double s = (x.scale() * pt_scale) / q(l);
+        Val out = fresh(l - 1, s);
+        ev_linear_transform_bsgs(c, k, x.v, pts, (long)(l + 1) * c.N, n1, n2, out.v);
+        c.log("LTB", l, l - 1, s, std::to_string(n1) + "x" + std::to_string(n2));
+        return out;
+    }
+    // general degree-15 p(x) = sum_i c_i x^i at (T, level(x) - 5) (R35): the odd plan's Paterson-Stockmeyer
+    // shape with the even terms added, q_k = c_{4k} + c_{4k+1} x + c_{4k+2} x^2 + c_{4k+3} x^3,
+    // p = (q_0 + q_1 x^4) + (q_2 + q_3 x^4) x^8
+    Val poly15(const Val &x, const std::vector<double> &cf, double T) {
+        const int l = x.level(), Lo = l - 5;
+        Val x2 = mul_ct(x, x, NAN, l - 1);
+        Val x3 = mul_ct(x, x2, NAN, l - 2);
+        Val x4 = mul_ct(x2, x2, NAN, l - 2);
+        Val x8 = mul_ct(x4, x4, NAN, l - 3);
+        const double Sb1 = (T * q(l - 4)) / x8.scale();
+        const double Sq3 = (Sb1 * q(l - 3)) / x4.scale();
+        Val q3 = lincomb({{&x, cf[13]}, {&x3, cf[15]}}, Sq3, l - 3);
+        Val q3e = lincomb({{&x2, cf[14]}}, Sq3, l - 3);
+        q3 = add_const(add(q3, q3e), cf[12]);
+        Val b1 = mul_ct(q3, x4, Sb1, l - 4, {{&x, cf[9]}, {&x3, cf[11]}});
+        Val b1e = lincomb({{&x2, cf[10]}}, Sb1, l - 4);
+        b1 = add_const(add(b1, b1e), cf[8]);
+        const double Sq1 = (T * q(l - 4)) / x4.scale();
+        Val q1 = lincomb({{&x, cf[5]}, {&x3, cf[7]}}, Sq1, l - 4);
+        Val q1e = lincomb({{&x2, cf[6]}}, Sq1, l - 4);
+        q1 = add_const(add(q1, q1e), cf[4]);
+        Val p = mul_ct(q1, x4, T, Lo, {{&x, cf[1]}, {&x3, cf[3]}}, &b1, &x8);
+        Val pe = lincomb({{&x2, cf[2]}}, T, Lo);
+        return add_const(add(p, pe), cf[0]);
+    }
+    // ModRaise -> CoeffToSlot (two BSGS transforms) -> x = u + conj(u) -> x / (K R) -> doubled cosine ->
+    // r steps d <- d^2 - 2 (natural scales) -> SlotToCoeff (two BSGS transforms, summed)
+    Val bootstrap(const Val &in, const BootCfg &b) {
+        const double S0 = in.scale();
+        Val z = mod_raise(in, b.level);
+        Val us[2] = {lt_bsgs(z, b.cts_re, b.n1, b.n2, b.cts_scale), lt_bsgs(z, b.cts_im, b.n1, b.n2, b.cts_scale)};
+        const double inv = 1.0 / (b.K * ((double)c.primes[0] / S0));
+        Val ds[2];
+        for (int i = 0; i < 2; i++) {
+            Val x = rot_add(us[i], kConjStep);
+            Val xn = mul_const(x, inv, c.scale, x.level() - 1);
+            Val d = poly15(xn, b.poly, c.scale);
+            for (int j = 0; j < b.r; j++) d = add_const(mul_ct(d, d, NAN, d.level() - 1), -2.0);
+            ds[i] = d;
+        }
+        Val o_re = lt_bsgs(ds[0], b.stc_re, b.n1, b.n2, b.stc_scale);
+        Val o_im = lt_bsgs(ds[1], b.stc_im, b.n1, b.n2, b.stc_scale);
+        return add(o_re, o_im);
+    }
+
     // ---- composite sign --------------------------------------------------------------------
     Val odd_poly(const Val &x, const std::vector<double> &cf, double T) {
         const int deg = (int)cf.size() - 1;
@@ -305,6 +367,17 @@ std::vector<int> argmax_rotations(const Layout &lay) {
     r.push_back(-lay.classes);
     for (int i = 0; (1 << i) < lay.classes; i++) r.push_back(1 << i);
     return r;
+}
+
+int boot_depth(const BootCfg &b) { return 8 + b.r; }
+
+void run_bootstrap(Ctx &c, const Keys &k, const CtView &in, const BootCfg &b, CtView &out) {
+    Ev ev{c, k, in.n};
+    Val x{nullptr, in};
+    Val r = ev.bootstrap(x, b);
+    out.level = r.level();
+    out.scale = r.scale();
+    ev_copy(c, r.v, out);
 }
 
 static void copy_in(Ctx &c, const CtView &src, const Val &dst) { ev_copy(c, src, dst.v); }

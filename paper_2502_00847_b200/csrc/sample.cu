@@ -5,6 +5,8 @@
 // the GPU.  Uniform residues (NTT domain): floor(X q / 2^128) with X = draws 2c, 2c+1 where
 // c = prime_index * N + k.  Ternary: floor(x 3 / 2^64) -> {0, 1, -1}.  Gaussian sigma = 3.2:
 // cumulative table over |e| <= 19 on the low 63 bits, sign = top bit.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -115,6 +117,22 @@ u64 host_state(u64 seed, u64 tag) { return host_mix(seed ^ host_mix(tag + GAMMA)
 inline dim3 g1(int logn, int rows) { return dim3((unsigned)((1L << logn) / TPB), rows); }
 }  // namespace
 
+// sparse ternary secret of Hamming weight h (R36), host side (key generation is client work): the ctr-th
+// draw's top logn bits pick a coefficient; a still-zero one becomes -1 (odd draw) or +1; h nonzeros
+void h_sample_sparse(u64 seed, u64 tag, int logn, int h, i64 *out) {
+    const u64 s0 = host_state(seed, tag);
+    std::fill(out, out + (1L << logn), (i64)0);
+    int cnt = 0;
+    for (u64 ctr = 0; cnt < h; ctr++) {
+        const u64 x = host_mix(s0 + (ctr + 1) * GAMMA);
+        const u64 pos = x >> (64 - logn);
+        if (out[pos] == 0) {
+            out[pos] = (x & 1) ? -1 : 1;
+            cnt++;
+        }
+    }
+}
+
 void set_cdt(const u64 *cdt, int n) {
     CUDA_CHECK(cudaMemcpyToSymbol(c_cdt, cdt, sizeof(u64) * n));
     CUDA_CHECK(cudaMemcpyToSymbol(c_ncdt, &n, sizeof(int)));
@@ -129,6 +147,25 @@ void k_sample_small(int logn, u64 seed, u64 tag, int kind, i64 *out, cudaStream_
 }
 void k_int_to_rows(const Tab &tab, int logn, const i64 *m, u64 *out, LimbMap lm, cudaStream_t st) {
     int_to_rows_kernel<<<g1(logn, lm.nl), TPB, 0, st>>>(tab, logn, m, out, lm);
+    LAUNCH_CHECK();
+}
+// ModRaise (R33): coefficient-form residues mod q_0 (coef[P][N], P = polynomial) centred into
+// (-q_0/2, q_0/2] and reduced mod every ciphertext prime q_0..q_{nl-1} (coefficient form out)
+__global__ void mod_raise_kernel(Tab tab, int logn, const u64 *__restrict__ coef, RowsArg out, int nl) {
+    const int limb = blockIdx.y, P = blockIdx.z;
+    const u64 k = (u64)blockIdx.x * TPB + threadIdx.x;
+    const u64 q0 = tab.q[0], q = tab.q[limb];
+    const u64 a = coef[((long)P << logn) + k];
+    const bool neg = a > (q0 - 1) / 2;
+    const u64 mag = neg ? q0 - a : a;  // |centred value| < q_0 / 2
+    u64 r = barrett128(U128{mag, 0}, q, tab.br0[limb], tab.br1[limb]);
+    if (neg && r) r = q - r;
+    out.p[poly_off(out.cs, out.ps, P) + ((long)limb << logn) + k] = r;
+}
+void k_mod_raise(const Tab &tab, int logn, const u64 *coef, RowsArg out, int n_polys, int nl, cudaStream_t st) {
+    dim3 g = g1(logn, nl);
+    g.z = n_polys;
+    mod_raise_kernel<<<g, TPB, 0, st>>>(tab, logn, coef, out, nl);
     LAUNCH_CHECK();
 }
 void k_key_combine(const Tab &tab, int logn, const u64 *a, const u64 *s, const u64 *e, const u64 *sp,

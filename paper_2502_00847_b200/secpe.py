@@ -31,6 +31,15 @@ class SignCfg(ctypes.Structure):
     _fields_ = [("n_stages", ctypes.c_int32), ("degrees", i32p), ("coeffs", f64p)]
 
 
+class CBootCfg(ctypes.Structure):
+    _fields_ = [("level", ctypes.c_int32), ("n1", ctypes.c_int32), ("n2", ctypes.c_int32), ("K", ctypes.c_double),
+                ("r", ctypes.c_int32), ("poly", f64p), ("cts_re", u64p), ("cts_im", u64p), ("cts_scale", ctypes.c_double),
+                ("stc_re", u64p), ("stc_im", u64p), ("stc_scale", ctypes.c_double)]
+
+
+CONJ = -(2 ** 31)  # SECPE_CONJ: the rotation step meaning slot conjugation
+
+
 class Layout(ctypes.Structure):
     _fields_ = [("queries", ctypes.c_int32), ("prompts", ctypes.c_int32), ("classes", ctypes.c_int32),
                 ("block", ctypes.c_int32)]
@@ -50,6 +59,7 @@ SIGS = {
     "secpe_ctx_info": (ctypes.c_int, [vp, u64p, u64p]),
     "secpe_ct_bytes": (ctypes.c_size_t, [vp, ctypes.c_int32]),
     "secpe_keygen": (ctypes.c_int, [vp, ctypes.c_uint64, i32p, ctypes.c_int32, ctypes.POINTER(vp)]),
+    "secpe_keygen_sparse": (ctypes.c_int, [vp, ctypes.c_uint64, ctypes.c_int32, i32p, ctypes.c_int32, ctypes.POINTER(vp)]),
     "secpe_keys_destroy": (None, [vp]),
     "secpe_key_export": (ctypes.c_int, [vp, vp, ctypes.c_int32, ctypes.c_uint64, u64p, ctypes.c_size_t]),
     "secpe_encode": (ctypes.c_int, [vp, f64p, ctypes.c_size_t, ctypes.c_double, i64p]),
@@ -78,6 +88,14 @@ SIGS = {
                                             ctypes.POINTER(CCt)]),
     "secpe_linear_transform": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), u64p, i32p, ctypes.c_int32,
                                               ctypes.c_double, ctypes.POINTER(CCt)]),
+    "secpe_mod_raise": (ctypes.c_int, [vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.POINTER(CCt)]),
+    "secpe_boot_depth": (ctypes.c_int32, [ctypes.POINTER(CBootCfg)]),
+    "secpe_boot_create": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.c_int32, ctypes.c_double, ctypes.POINTER(vp)]),
+    "secpe_boot_get_cfg": (ctypes.c_int, [vp, ctypes.POINTER(CBootCfg)]),
+    "secpe_boot_destroy": (None, [vp]),
+    "secpe_boot_export": (ctypes.c_int, [vp, vp, ctypes.c_int32, u64p, ctypes.c_size_t]),
+    "secpe_bootstrap": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.POINTER(CBootCfg), ctypes.POINTER(CCt)]),
     "secpe_linear_transform_bsgs": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), u64p, ctypes.c_int32, ctypes.c_int32,
                                                    ctypes.c_double, ctypes.POINTER(CCt)]),
     "secpe_rescale": (ctypes.c_int, [vp, ctypes.POINTER(CCt), ctypes.POINTER(CCt)]),
@@ -196,6 +214,33 @@ class Keys:
         return out
 
 
+class Boot:
+    """secpe_boot handle: library-built bootstrapping material (device memory owned by the library)."""
+
+    def __init__(self, ctx, handle):
+        self.ctx, self.h = ctx, handle
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.secpe_boot_destroy(self.h)
+            self.h = None
+
+    def export(self, which):
+        """Matrix `which` (0 cts_re, 1 cts_im, 2 stc_re, 3 stc_im) as host uint64[n2][n1][limbs][N]."""
+        c = self.cfg()
+        lv = c["level"] if which < 2 else c["level"] - 7 - c["r"]
+        out = np.zeros((c["n2"], c["n1"], lv + 1, self.ctx.N), dtype=np.uint64)
+        _chk(lib().secpe_boot_export(self.ctx.h, self.h, which, out.ctypes.data_as(u64p), out.size))
+        return out
+
+    def cfg(self):
+        """(level, n1, n2, K, r, poly[16], cts_scale, stc_scale) of the configuration."""
+        c = CBootCfg()
+        _chk(lib().secpe_boot_get_cfg(self.h, ctypes.byref(c)))
+        return dict(level=c.level, n1=c.n1, n2=c.n2, K=c.K, r=c.r, poly=[c.poly[i] for i in range(16)],
+                    cts_scale=c.cts_scale, stc_scale=c.stc_scale, raw=c)
+
+
 class Context:
     """Parameters + device tables on the current torch CUDA stream."""
 
@@ -244,11 +289,12 @@ class Context:
         return Ct(self.alloc(level, n), level, 0.0)
 
     # ---- keys / client ----------------------------------------------------------------------------
-    def keygen(self, seed, rot_steps=()):
+    def keygen(self, seed, rot_steps=(), h=0):
+        """secpe_keygen (h = 0) / secpe_keygen_sparse (Hamming weight h, reading R36)."""
         r = np.array(list(rot_steps) or [0], dtype=np.int32)
-        h = vp()
-        _chk(lib().secpe_keygen(self.h, seed, r.ctypes.data_as(i32p), len(rot_steps), ctypes.byref(h)))
-        return Keys(self, h)
+        kh = vp()
+        _chk(lib().secpe_keygen_sparse(self.h, seed, h, r.ctypes.data_as(i32p), len(rot_steps), ctypes.byref(kh)))
+        return Keys(self, kh)
 
     def encode(self, slots, scale):
         z = np.ascontiguousarray(slots, dtype=np.float64)
@@ -395,6 +441,46 @@ class Context:
         st = np.asarray(steps, dtype=np.int32)
         _chk(lib().secpe_linear_transform(self.h, keys.h, ctypes.byref(ca), ctypes.cast(pts.data_ptr(), u64p),
                                           st.ctypes.data_as(i32p), len(steps), pt_scale, ctypes.byref(co)))
+        out.level, out.scale = co.level, co.scale
+        return out
+
+    def mod_raise(self, a, level):
+        """secpe_mod_raise (reading R33)."""
+        out = self._out(level)
+        ca, co = a.c(), out.c()
+        _chk(lib().secpe_mod_raise(self.h, ctypes.byref(ca), level, ctypes.byref(co)))
+        out.level, out.scale = co.level, co.scale
+        return out
+
+    def boot_create(self, level, K, r, n1, n2, in_scale):
+        """secpe_boot_create: library-built bootstrapping material (readings R34, R35)."""
+        h = vp()
+        _chk(lib().secpe_boot_create(self.h, level, K, r, n1, n2, in_scale, ctypes.byref(h)))
+        return Boot(self, h)
+
+    def bootstrap_with(self, keys, a, boot):
+        """secpe_bootstrap with the configuration of a Boot object (secpe_boot_get_cfg)."""
+        cfg = CBootCfg()
+        _chk(lib().secpe_boot_get_cfg(boot.h, ctypes.byref(cfg)))
+        out = self._out(max(cfg.level - lib().secpe_boot_depth(ctypes.byref(cfg)), 0))
+        ca, co = a.c(), out.c()
+        _chk(lib().secpe_bootstrap(self.h, keys.h, ctypes.byref(ca), ctypes.byref(cfg), ctypes.byref(co)))
+        out.level, out.scale = co.level, co.scale
+        return out
+
+    def bootstrap(self, keys, a, level, n1, n2, K, r, poly, cts_re, cts_im, cts_scale, stc_re, stc_im, stc_scale):
+        """secpe_bootstrap (readings R32-R35); the four matrices as cuda uint64 tensors
+        [n2][n1][limbs][N] (NTT-form encoded diagonals)."""
+        for t in (cts_re, cts_im, stc_re, stc_im):
+            assert t.is_cuda and t.dtype == torch.uint64 and t.is_contiguous()
+        pc = np.ascontiguousarray(poly, dtype=np.float64)
+        assert pc.shape == (16,)
+        ptr = lambda t: ctypes.cast(t.data_ptr(), u64p)
+        cfg = CBootCfg(level, n1, n2, K, r, pc.ctypes.data_as(f64p), ptr(cts_re), ptr(cts_im), cts_scale,
+                       ptr(stc_re), ptr(stc_im), stc_scale)
+        out = self._out(max(level - lib().secpe_boot_depth(ctypes.byref(cfg)), 0))
+        ca, co = a.c(), out.c()
+        _chk(lib().secpe_bootstrap(self.h, keys.h, ctypes.byref(ca), ctypes.byref(cfg), ctypes.byref(co)))
         out.level, out.scale = co.level, co.scale
         return out
 

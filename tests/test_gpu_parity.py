@@ -743,3 +743,129 @@ def test_linear_transform_bsgs_errors(S):
         g.linear_transform_bsgs(kg, ct, pts, 2, 2, 1.0)   # needs the key for step 2
     with pytest.raises(S.SecpeError):
         g.linear_transform_bsgs(kg, ct, pts[:, :0].contiguous(), 0, 2, 1.0)
+
+
+# ---------------------------------------------------------------------------------------------
+# Bootstrapping (readings R32-R36) on the "boot" parameters (N = 2^12, 2048 slots)
+# ---------------------------------------------------------------------------------------------
+BOOT = dict(n1=64, n2=32, K=16, r=8, h=64)
+
+
+@pytest.fixture(scope="module")
+def boot(S):
+    P = pair(S, "boot")
+    ev = ckks.Oracle(P.prm)
+    rot = plan.boot_rotations(BOOT["n1"], BOOT["n2"])
+    seed = synth.KEY_SEED_BASE + 23
+    return P, ev, ev.keygen(seed, rot, h=BOOT["h"]), P.gpu.keygen(seed, rot, h=BOOT["h"])
+
+
+@pytest.mark.gpu
+def test_sparse_keys_and_conjugation_bit_exact(boot):
+    """R36 sparse secret and every key built on it word for word; R32 conjugation (SECPE_CONJ) word for
+    word equal to the oracle's sigma_{2N-1} + key switch."""
+    P, ev, ko, kg = boot
+    prm = P.prm
+    assert np.array_equal(kg.export(0), ko.s_ntt)
+    assert np.array_equal(kg.export(2), ko.rlk)
+    gc = ckks.galois_elt(prm, ckks.CONJ)
+    assert np.array_equal(kg.export(3, gc), ko.gk[gc])
+    rng = np.random.default_rng(4)
+    z = rng.uniform(-1, 1, prm.N // 2)
+    ct = ev.encrypt(ko, z, prm.scale, 21, level=6)
+    want = ev.rotate_raw(ko, ct, ckks.CONJ)
+    got = P.gpu.rotate(kg, P.up(ct), P.secpe.CONJ)
+    assert np.array_equal(P.down(got), want.data)
+
+
+@pytest.mark.gpu
+def test_mod_raise_bit_exact(boot):
+    """R33 ModRaise word for word, to the top and to a middle level; level-0 input required."""
+    P, ev, ko, kg = boot
+    prm = P.prm
+    ct = ev.encrypt(ko, np.linspace(-1, 1, prm.N // 2), prm.scale, 22, level=0)
+    for lv in (prm.L, 7):
+        want = ev.mod_raise(ct, lv)
+        got = P.gpu.mod_raise(P.up(ct), lv)
+        assert got.level == lv and got.scale == ct.scale
+        assert np.array_equal(P.down(got), want.data)
+    with pytest.raises(P.secpe.SecpeError):
+        P.gpu.mod_raise(P.up(ev.encrypt(ko, np.zeros(4), prm.scale, 1, level=2)), prm.L)
+
+
+@pytest.fixture(scope="module")
+def boot_cfg(boot):
+    P, ev = boot[0], boot[1]
+    return plan.boot_config(ev, P.prm.scale, P.prm.L, BOOT["K"], BOOT["r"], BOOT["n1"], BOOT["n2"])
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_bootstrap_bit_exact(boot, boot_cfg):
+    """N3 end to end: secpe_bootstrap of a level-0 ciphertext is word for word the oracle's bootstrap plan
+    (same op list), lands at level L - (8 + r) and decrypts to the input slots within 2^-12."""
+    P, ev, ko, kg = boot
+    prm, g = P.prm, P.gpu
+    rng = np.random.default_rng(5)
+    z = rng.uniform(-1, 1, prm.N // 2)
+    ct = ev.encrypt(ko, z, prm.scale, 23, level=0)
+    cfg = boot_cfg
+    ev.log.clear()
+    want = plan.bootstrap(ev, ko, ct, cfg)
+    olog = list(ev.log)
+    dev = {nm: torch.from_numpy(np.stack([np.stack(row) for row in cfg[nm]])).cuda()
+           for nm in ("cts_re", "cts_im", "stc_re", "stc_im")}
+    g.oplog(enable=True, clear=True)
+    got = g.bootstrap(kg, P.up(ct), cfg["level"], BOOT["n1"], BOOT["n2"], cfg["K"], cfg["r"], cfg["poly"],
+                      dev["cts_re"], dev["cts_im"], cfg["cts_scale"], dev["stc_re"], dev["stc_im"], cfg["stc_scale"])
+    glog = g.oplog(enable=False, clear=True)
+    assert glog == olog
+    assert got.level == want.level == prm.L - plan.boot_depth(BOOT["r"]) and got.scale == want.scale
+    assert np.array_equal(P.down(got), want.data)
+    assert np.abs(g.decrypt(kg, got) - z).max() < 2 ** -12
+    # errors: a level-0 input is required; a missing key is reported
+    with pytest.raises(P.secpe.SecpeError):
+        g.bootstrap(kg, P.up(ev.encrypt(ko, z, prm.scale, 2, level=1)), cfg["level"], BOOT["n1"], BOOT["n2"],
+                    cfg["K"], cfg["r"], cfg["poly"], dev["cts_re"], dev["cts_im"], cfg["cts_scale"], dev["stc_re"],
+                    dev["stc_im"], cfg["stc_scale"])
+    k2 = g.keygen(5, [1])
+    with pytest.raises(P.secpe.SecpeError):
+        g.bootstrap(k2, P.up(ct), cfg["level"], BOOT["n1"], BOOT["n2"], cfg["K"], cfg["r"], cfg["poly"],
+                    dev["cts_re"], dev["cts_im"], cfg["cts_scale"], dev["stc_re"], dev["stc_im"], cfg["stc_scale"])
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_boot_setup_matches_oracle_encoding(boot, boot_cfg):
+    """secpe_boot_create (library-built material): the same polynomial (to a double's rounding), scales, and
+    encoded matrices whose integer coefficients equal the oracle's except for +-1 at rare rounding ties of
+    two double-precision FFTs; bootstrapping with it decrypts like the oracle-encoded one."""
+    P, ev, ko, kg = boot
+    prm, g, cfg = P.prm, P.gpu, boot_cfg
+    b = g.boot_create(prm.L, BOOT["K"], BOOT["r"], BOOT["n1"], BOOT["n2"], prm.scale)
+    c = b.cfg()
+    assert c["level"] == cfg["level"] and c["cts_scale"] == cfg["cts_scale"] and c["stc_scale"] == cfg["stc_scale"]
+    assert np.allclose(c["poly"], cfg["poly"], rtol=1e-13, atol=1e-300)
+    q0 = prm.primes[0]
+    for w, nm in enumerate(("cts_re", "cts_im", "stc_re", "stc_im")):
+        got = b.export(w)
+        want = np.stack([np.stack(row) for row in cfg[nm]])
+        assert got.shape == want.shape
+        same = (got == want).all(axis=(2, 3))
+        if same.all():
+            continue
+        gi = ckks.ntt_limbs(got[~same][:, :1], prm, [0], inverse=True)[:, 0].astype(object)
+        wi = ckks.ntt_limbs(want[~same][:, :1], prm, [0], inverse=True)[:, 0].astype(object)
+        d = (gi - wi) % q0
+        d = np.where(d > q0 // 2, d - q0, d)
+        wc = np.where(wi > q0 // 2, wi - q0, wi)
+        # two double-precision FFTs of values up to max|w| agree to about 2^-46 max|w| (N = 2^12)
+        tol = 1 + int(float(np.abs(wc).max()) * 2.0 ** -46)
+        assert np.abs(d).max() <= tol, (nm, int(np.abs(d).max()), tol)
+        assert np.count_nonzero(d) <= 5e-3 * got.shape[0] * got.shape[1] * prm.N, nm  # ~2^-11 FFT error at 2^38
+    rng = np.random.default_rng(6)
+    z = rng.uniform(-1, 1, prm.N // 2)
+    ct = ev.encrypt(ko, z, prm.scale, 24, level=0)
+    out = g.bootstrap_with(kg, P.up(ct), b)
+    assert out.level == prm.L - plan.boot_depth(BOOT["r"])
+    assert np.abs(g.decrypt(kg, out) - z).max() < 2 ** -12

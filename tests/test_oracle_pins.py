@@ -662,15 +662,37 @@ def test_argmax_small_ring_7_15_15_oracle():
 # ---------------------------------------------------------------------------------------------
 # O-20 bootstrapping building blocks (readings R32-R35)
 # ---------------------------------------------------------------------------------------------
-BOOT_TINY = dict(n1=16, n2=8, K=24, r=8)
+BOOT_TINY = dict(n1=16, n2=8, K=16, r=8, h=64)
 
 
 @pytest.fixture(scope="module")
 def boot_tiny():
     prm = ckks.Params(synth.PARAM_SETS["boot_tiny"])
     ev = ckks.Oracle(prm)
-    keys = ev.keygen(7, plan.boot_rotations(BOOT_TINY["n1"], BOOT_TINY["n2"]))
+    keys = ev.keygen(7, plan.boot_rotations(BOOT_TINY["n1"], BOOT_TINY["n2"]), h=BOOT_TINY["h"])
     return prm, ev, keys
+
+
+def test_sparse_secret(boot_tiny):
+    """R36: the sparse secret has exactly h nonzeros, all +-1, is a function of the seed alone, and its first
+    nonzero sits where the first draw's top log N bits point (the sampler's definition, recomputed here
+    from SplitMix64)."""
+    prm, ev, keys = boot_tiny
+    s = keys.s
+    assert np.count_nonzero(s) == BOOT_TINY["h"] and set(np.unique(s)) <= {-1, 0, 1}
+    assert np.array_equal(ev.keygen(7, (), h=BOOT_TINY["h"]).s, s)
+    assert not np.array_equal(ev.keygen(8, (), h=BOOT_TINY["h"]).s, s)
+    M = (1 << 64) - 1
+    G = 0x9E3779B97F4A7C15
+
+    def mix(z):
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        return z ^ (z >> 31)
+    tag = 1 << 48
+    s0 = mix(7 ^ mix((tag + G) & M))
+    x = mix((s0 + G) & M)
+    assert s[x >> (64 - prm.logn)] == (-1 if x & 1 else 1)
 
 
 def test_conjugation_is_complex_conjugate(boot_tiny):
@@ -723,7 +745,7 @@ def test_boot_matrices_invert_decoding(boot_tiny):
 def test_boot_poly_is_doubled_cosine():
     """R35: the degree-15 Taylor coefficients match 2 cos((2 pi K x - pi/2) / 2^r) on [-1, 1] (closed form),
     and r double-angle steps d <- d^2 - 2 turn it into 2 sin(2 pi K x)."""
-    K, r = 24, 8
+    K, r = 16, 8
     c = plan.boot_poly(K, r)
     x = np.linspace(-1, 1, 2001)
     d = np.polynomial.polynomial.polyval(x, c)
