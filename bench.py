@@ -209,7 +209,40 @@ def micro_configs(stream, reps=5):
     out["configs[3]_rotation"] = {"ms_per_15_keys": ms_h, "cts": R, "rotations_per_s": 15 * R / (ms_h / 1000),
                                   "hoisted": True,
                                   "not_hoisted": {"ms_per_15_keys": ms, "rotations_per_s": 15 * R / (ms / 1000)}}
+    del ctx, keys, a, b, r, o
+    out["N3_bootstrap"] = bootstrap_bench(stream, t_ms)
     return out
+
+
+def bootstrap_bench(stream, t_ms):
+    """one CKKS bootstrap (readings R32-R36) of a level-0 ciphertext at N = 2^12 (2048 slots,
+    dense BSGS 64 x 32 CoeffToSlot / SlotToCoeff, sparse secret h = 64, K = 16, r = 8), library-built matrices
+    (secpe_boot_create).  Latency of one call on one GPU, CUDA events, median."""
+    import torch
+    import synth
+    from paper_2502_00847_b200 import secpe
+    ctx = secpe.Context(synth.PARAM_SETS["boot"], stream=stream.cuda_stream)
+    n1, n2, K, r, h = 64, 32, 16, 8, 64
+    rot = list(range(1, n1)) + [j * n1 for j in range(1, n2)] + [secpe.CONJ]
+    keys = ctx.keygen(synth.KEY_SEED_BASE + 23, rot, h=h)
+    t0 = time.time()
+    boot = ctx.boot_create(ctx.L, K, r, n1, n2, ctx.scale)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    z = synth.rng(4001).uniform(-1, 1, ctx.N // 2)
+    c0 = ctx.new_ct(0)
+    ctx.encrypt_coeffs(keys, ctx.encode(z, ctx.scale), 0, ctx.scale, 77, out=c0)
+    c0.level, c0.scale = 0, ctx.scale
+    res = [None]
+
+    def one():
+        res[0] = ctx.bootstrap_with(keys, c0, boot)
+    ms = t_ms(one)
+    err = float(abs(ctx.decrypt(keys, res[0]) - z).max())
+    ks = 2 * (n1 - 1 + n2 - 1) * 2 + 2 + 2 * (7 + r)
+    return {"ms_per_bootstrap": ms, "logn": ctx.logn, "slots": ctx.N // 2, "level_in": 0, "raised_to": ctx.L,
+            "level_out": res[0].level, "key_switches": ks, "max_abs_err": err, "setup_s": setup_s,
+            "note": "dense BSGS DFT matrices (2 n1 n2 pts each); N = 2^16 needs the factorised DFT (next)"}
 
 def run_secpe(a):
     import torch
