@@ -272,6 +272,48 @@ void secpe_boot_destroy(secpe_boot *boot);
 /* Copy matrix `which` (0 cts_re, 1 cts_im, 2 stc_re, 3 stc_im) to host uint64[n2][n1][limbs][N], for
  * parity tests (synchronises); n_words must equal that size. */
 int secpe_boot_export(secpe_ctx *ctx, const secpe_boot *boot, int32_t which, uint64_t *host_out, size_t n_words);
+/* Factorised bootstrapping (reading R37; what N = 2^16 needs): the decoding matrix U is the product of
+ * log2(N/2) special-FFT butterfly stages S_s (3 slot-domain diagonals each: offsets 0, +-2^(s-1)); the
+ * caller groups consecutive stages and each group becomes one hoisted diagonal transform (R30, one level).
+ * CoeffToSlot applies the inverse groups (slots end up holding the coefficients in bit-reversed order,
+ * invisible to the slot-wise EvalMod), its last group in a Re (x 1/2) and an Im (x -i/2) variant;
+ * SlotToCoeff applies its first group to d_re (x c) and d_im (x i c), sums, then the other groups.
+ * Depth 2 n_groups + 6 + r.  A stage: n_diag signed rotation steps (ascending) and pts dev
+ * uint64[n_diag][stage level + 1][N] (NTT form, encoded at pt_scale); CoeffToSlot stage i sits at
+ * level - i, SlotToCoeff stage j at level - n_cts - 6 - r - j. */
+typedef struct {
+    int32_t n_diag;
+    const int32_t *steps;   /* host[n_diag] */
+    const uint64_t *pts;    /* dev */
+    double pt_scale;
+} secpe_lt_stage;
+typedef struct {
+    int32_t level;
+    double K;
+    int32_t r;
+    const double *poly;            /* host[16] */
+    int32_t n_cts;                 /* == n_stc */
+    const secpe_lt_stage *cts;     /* host[n_cts]; cts[n_cts-1] is the Re variant of the last group */
+    secpe_lt_stage cts_im;
+    int32_t n_stc;
+    const secpe_lt_stage *stc;     /* host[n_stc]; stc[0] is the Re variant of the first group */
+    secpe_lt_stage stc_im;
+} secpe_boot_fft_cfg;
+int secpe_bootstrap_fft(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const secpe_boot_fft_cfg *cfg,
+                        secpe_ct *out);
+/* Library-built factorised material: groups host[n_groups] (stage counts, S_1 first, summing to
+ * log2(N/2)); same polynomial and scales as secpe_boot_create. */
+int secpe_boot_create_fft(secpe_ctx *ctx, int32_t level, double K, int32_t r, const int32_t *groups,
+                          int32_t n_groups, double in_scale, secpe_boot **out);
+/* Bootstrap with library-built material of either kind; out->data sized for level - secpe_boot_levels. */
+int secpe_bootstrap_boot(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const secpe_boot *boot,
+                         secpe_ct *out);
+/* Depth of a library-built bootstrap; *raise_level (optional) receives its ModRaise level. */
+int32_t secpe_boot_levels(const secpe_boot *boot, int32_t *raise_level);
+/* A factorised stage for parity tests: kind 0 cts[idx], 1 cts_im, 2 stc[idx], 3 stc_im.  Writes *n_diag;
+ * when steps / host_out are non-null also the steps and the pts (uint64[n_diag][limbs][N], n_words). */
+int secpe_boot_stage_export(secpe_ctx *ctx, const secpe_boot *boot, int32_t kind, int32_t idx, int32_t *n_diag,
+                            int32_t *steps, uint64_t *host_out, size_t n_words);
 /* Levels one bootstrap consumes (8 + r): out level = cfg->level - secpe_boot_depth(cfg). */
 int32_t secpe_boot_depth(const secpe_boot_cfg *cfg);
 /* in: level 0; out->data sized secpe_ct_bytes(cfg->level - secpe_boot_depth(cfg)); out->level / scale

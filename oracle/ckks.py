@@ -636,6 +636,11 @@ class Oracle:
         return r
 
     # ---- planned ops (logged; reading R9 scale planning) ------------------------------------
+    def lt(self, keys, x, pts, steps, pt_scale):
+        out = self.linear_transform(keys, x, pts, steps, pt_scale)
+        self._log("LT", x.level, out.level, out.scale, ",".join(str(s) for s in steps))
+        return out
+
     def lt_bsgs(self, keys, x, pts, n1, n2, pt_scale):
         out = self.linear_transform_bsgs(keys, x, pts, n1, n2, pt_scale)
         self._log("LTB", x.level, out.level, out.scale, "%dx%d" % (n1, n2))

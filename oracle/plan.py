@@ -313,3 +313,191 @@ def bootstrap(ev, keys, ct, cfg):
     o_re = ev.lt_bsgs(keys, ds[0], cfg["stc_re"], n1, n2, cfg["stc_scale"])
     o_im = ev.lt_bsgs(keys, ds[1], cfg["stc_im"], n1, n2, cfg["stc_scale"])
     return ev.add(o_re, o_im)
+
+
+# ---------------------------------------------------------------------------------------------
+# Factorised CoeffToSlot / SlotToCoeff (reading R37): the decoding matrix U as log2(n) butterfly stages
+# (the special FFT) in slot-domain diagonal form, consecutive stages merged into groups; the slots then
+# hold the coefficients in bit-reversed order, which EvalMod (slot-wise) does not see.
+# ---------------------------------------------------------------------------------------------
+def bitrev_perm(n):
+    b = n.bit_length() - 1
+    return np.array([int(format(i, "0%db" % b)[::-1], 2) for i in range(n)])
+
+
+def dft_stages(N):
+    """Butterfly stage s = 1..log2 n of the special FFT as {offset: diagonal} (slot-domain, cyclic offsets
+    mod n), len = 2^s, h = len/2, for block start i and j < h:
+        out[i+j] = v[i+j] + w_j v[i+j+h],  out[i+j+h] = v[i+j] - w_j v[i+j+h],
+        w_j = zeta^{(e_j mod 4 len) 2N / (4 len)}, e_j = 5^j mod 2N.
+    U w = S_log2n ... S_1 (w in bit-reversed order) (pinned in the tests)."""
+    from oracle.ckks import _rot_group
+    n = N // 2
+    e = _rot_group(N)
+    out = []
+    ln = 2
+    while ln <= n:
+        h = ln // 2
+        d0, dp, dm = np.zeros(n, complex), np.zeros(n, complex), np.zeros(n, complex)
+        for i in range(0, n, ln):
+            for j in range(h):
+                m = (int(e[j]) % (4 * ln)) * (2 * N // (4 * ln))
+                w = np.exp(1j * np.pi * m / N)
+                d0[i + j], dp[i + j] = 1.0, w          # out[i+j] = v[i+j] + w v[i+j+h]
+                dm[i + j + h], d0[i + j + h] = 1.0, -w  # out[i+j+h] = v[i+j] - w v[i+j+h]
+        out.append({0: d0, h % n: dp, (n - h) % n: dm} if h != n - h else {0: d0, h: dp + dm})
+        ln *= 2
+    return out
+
+
+def dft_stages_inv(N):
+    """Inverses of dft_stages: in[i+j] = (o[i+j] + o[i+j+h]) / 2, in[i+j+h] = (o[i+j] - o[i+j+h]) / (2 w_j)."""
+    from oracle.ckks import _rot_group
+    n = N // 2
+    e = _rot_group(N)
+    out = []
+    ln = 2
+    while ln <= n:
+        h = ln // 2
+        d0, dp, dm = np.zeros(n, complex), np.zeros(n, complex), np.zeros(n, complex)
+        for i in range(0, n, ln):
+            for j in range(h):
+                m = (int(e[j]) % (4 * ln)) * (2 * N // (4 * ln))
+                wi = np.exp(-1j * np.pi * m / N)
+                d0[i + j], dp[i + j] = 0.5, 0.5
+                dm[i + j + h], d0[i + j + h] = 0.5 * wi, -0.5 * wi
+        out.append({0: d0, h % n: dp, (n - h) % n: dm} if h != n - h else {0: d0, h: dp + dm})
+        ln *= 2
+    return out
+
+
+def diag_mul(A, B, n):
+    """Diagonal form of the product A B (A applied last): (A B) v = sum_{a,b} (alpha_a (.) RotL(beta_b, a))
+    (.) RotL(v, a + b), offsets mod n."""
+    out = {}
+    for a, al in A.items():
+        for b, be in B.items():
+            k = (a + b) % n
+            out[k] = out.get(k, 0) + al * np.roll(be, -a)
+    return out
+
+
+def diag_apply(D, v):
+    """sum_i d_i (.) RotL(v, i) (plaintext, for pins)."""
+    return sum(d * np.roll(v, -i) for i, d in D.items())
+
+
+def fft_groups(N, groups):
+    """Merged stage groups.  groups: stage counts summing to log2(n), in the order SlotToCoeff applies them
+    (S_1 first).  Returns (stc, cts): stc[g] = product of its stages (later stages applied last);
+    cts = inverses in the reverse order (CoeffToSlot applies cts[0] first)."""
+    n = N // 2
+    st, si = dft_stages(N), dft_stages_inv(N)
+    if sum(groups) != len(st):
+        raise ValueError("groups must cover log2(N/2) stages")
+    stc, cts, pos = [], [], 0
+    for g in groups:
+        D = {0: np.ones(n, complex)}
+        Di = {0: np.ones(n, complex)}
+        for s in range(pos, pos + g):
+            D = diag_mul({k: v for k, v in st[s].items()}, D, n)     # S_s applied after the previous ones
+            Di = diag_mul(Di, {k: v for k, v in si[s].items()}, n)   # S_s^-1 applied before the previous
+        stc.append(D)
+        cts.append(Di)
+        pos += g
+    return stc, cts[::-1]
+
+
+def _signed(k, n):
+    return k - n if k > n // 2 else k
+
+
+def lt_pts(ev, D, level, pt_scale):
+    """(steps, pts) of a diagonal-form transform for linear_transform (R30): steps the signed offsets
+    (sorted), pts[i] = NTT(encode(d_i, pt_scale)) at `level`."""
+    from oracle.ckks import encode
+    n = ev.prm.N // 2
+    keys = sorted(D, key=lambda k: _signed(k, n))
+    steps = [_signed(k, n) for k in keys]
+    pts = [ev.plain_ntt(encode(ev.prm, D[k], pt_scale), level) for k in keys]
+    return steps, pts
+
+
+def fft_boot_config(ev, in_scale, level, K, r, groups):
+    """Factorised bootstrapping material (R37): CoeffToSlot stages (the last one in a Re (x 1/2) and an Im
+    (x -i/2) variant), SlotToCoeff stages (the first one in a Re (x c) and an Im (x i c) variant, c = R/(4 pi)),
+    each encoded at q of its level."""
+    prm = ev.prm
+    n = prm.N // 2
+    R = float(prm.primes[0]) / in_scale
+    c = R / (4.0 * np.pi)
+    stc, cts = fft_groups(prm.N, groups)
+    mc, ms = len(cts), len(stc)
+    cfg = dict(level=level, K=float(K), r=r, poly=boot_poly(K, r), groups=list(groups), cts=[], stc=[])
+    lv = level
+    for i, D in enumerate(cts):
+        sc = float(prm.primes[lv])
+        if i < mc - 1:
+            cfg["cts"].append((*lt_pts(ev, D, lv, sc), sc))
+        else:
+            cfg["cts"].append((*lt_pts(ev, {k: 0.5 * v for k, v in D.items()}, lv, sc), sc))
+            cfg["cts_im"] = (*lt_pts(ev, {k: -0.5j * v for k, v in D.items()}, lv, sc), sc)
+        lv -= 1
+    lv = level - mc - 6 - r
+    cfg["stc_level"] = lv
+    for i, D in enumerate(stc):
+        sc = float(prm.primes[lv])
+        if i == 0:
+            cfg["stc"].append((*lt_pts(ev, {k: c * v for k, v in D.items()}, lv, sc), sc))
+            cfg["stc_im"] = (*lt_pts(ev, {k: 1j * c * v for k, v in D.items()}, lv, sc), sc)
+        else:
+            cfg["stc"].append((*lt_pts(ev, D, lv, sc), sc))
+        lv -= 1
+    return cfg
+
+
+def fft_boot_depth(groups, r):
+    return 2 * len(groups) + 6 + r
+
+
+def fft_boot_rotations(N, groups):
+    """Galois keys the factorised bootstrap needs: every nonzero offset of every group, and conjugation."""
+    n = N // 2
+    stc, cts = fft_groups(N, groups)
+    s = set()
+    for D in stc + cts:
+        s |= {_signed(k, n) for k in D if k % n}
+    return sorted(s) + [CONJ_STEP]
+
+
+def bootstrap_fft(ev, keys, ct, cfg):
+    """Bootstrapping with the factorised transforms (R37; otherwise as `bootstrap`, R32-R36):
+    ModRaise; CoeffToSlot stages (hoisted diagonal transforms, R30), the last in Re / Im variants;
+    x = u + conj(u); x / (K R); doubled cosine; r doublings; SlotToCoeff's first stage on d_re and d_im,
+    summed; the remaining SlotToCoeff stages."""
+    prm = ev.prm
+    L, K, r = cfg["level"], cfg["K"], cfg["r"]
+    S0 = ct.scale
+    v = ev.mod_raise(ct, L)
+    for steps, pts, sc in cfg["cts"][:-1]:
+        v = ev.lt(keys, v, pts, steps, sc)
+    steps, pts, sc = cfg["cts"][-1]
+    us = [ev.lt(keys, v, pts, steps, sc)]
+    steps, pts, sc = cfg["cts_im"]
+    us.append(ev.lt(keys, v, pts, steps, sc))
+    inv = 1.0 / (K * (float(prm.primes[0]) / S0))
+    ds = []
+    for u in us:
+        x = ev.add(u, ev.rot(keys, u, CONJ_STEP))
+        xn = ev.mul_const(x, inv, prm.scale, x.level - 1)
+        d = eval_poly15(ev, keys, xn, cfg["poly"], prm.scale)
+        for _ in range(r):
+            d = ev.add_const(ev.mul_ct(keys, d, d, None, d.level - 1), -2.0)
+        ds.append(d)
+    steps, pts, sc = cfg["stc"][0]
+    o = ev.lt(keys, ds[0], pts, steps, sc)
+    steps, pts, sc = cfg["stc_im"]
+    o = ev.add(o, ev.lt(keys, ds[1], pts, steps, sc))
+    for steps, pts, sc in cfg["stc"][1:]:
+        o = ev.lt(keys, o, pts, steps, sc)
+    return o

@@ -521,6 +521,7 @@ int secpe_boot_create(secpe_ctx *ctx, int32_t level, double K, int32_t r, int32_
 int secpe_boot_get_cfg(const secpe_boot *boot, secpe_boot_cfg *cfg) {
     return guard([&] {
         REQUIRE(boot && boot->b && cfg, SECPE_EINVAL, "null argument");
+        REQUIRE(!boot->b->fft, SECPE_EINVAL, "factorised material has no dense configuration");
         const BootCfg &b = boot->b->cfg;
         *cfg = secpe_boot_cfg{b.level, b.n1, b.n2, b.K, b.r, b.poly.data(), b.cts_re, b.cts_im, b.cts_scale,
                               b.stc_re, b.stc_im, b.stc_scale};
@@ -535,6 +536,114 @@ int secpe_boot_export(secpe_ctx *ctx, const secpe_boot *boot, int32_t which, uin
         REQUIRE(n_words == m[which]->words, SECPE_EINVAL, "n_words does not match the matrix size");
         CUDA_CHECK(cudaMemcpyAsync(host_out, m[which]->p, n_words * 8, cudaMemcpyDeviceToHost, ctx->c.st));
         CUDA_CHECK(cudaStreamSynchronize(ctx->c.st));
+    });
+}
+static LtStage lt_stage(const Ctx &c, const secpe_lt_stage &s) {
+    REQUIRE(s.n_diag >= 1 && s.steps && s.pts, SECPE_EINVAL, "bad transform stage");
+    LtStage t;
+    t.steps.assign(s.steps, s.steps + s.n_diag);
+    t.pts = s.pts;
+    t.scale = s.pt_scale;
+    (void)c;
+    return t;
+}
+static void check_fft_keys(const Ctx &c, const secpe_keys *keys, const FftBootCfg &b) {
+    auto chk = [&](const LtStage &s) {
+        for (int st : s.steps)
+            REQUIRE(keys->k->gk.count(galois_elt(c, st)) || galois_elt(c, st) == 1, SECPE_ENOKEY,
+                    "no Galois key for a transform step");
+    };
+    for (auto &s : b.cts) chk(s);
+    for (auto &s : b.stc) chk(s);
+    chk(b.cts_im);
+    chk(b.stc_im);
+    REQUIRE(keys->k->gk.count(galois_elt(c, kConjStep)), SECPE_ENOKEY, "no conjugation key");
+}
+static void bootstrap_fft_views(Ctx &c, const secpe_keys *keys, const secpe_ct *in, const FftBootCfg &b,
+                                secpe_ct *out) {
+    REQUIRE(b.level < c.nq && b.level - fft_boot_depth(b) >= 0, SECPE_ELEVEL, "not enough levels for a bootstrap");
+    CtView vi = view_of(c, in);
+    REQUIRE(vi.level == 0, SECPE_EINVAL, "bootstrap takes a level-0 ciphertext");
+    REQUIRE(out->data != in->data, SECPE_EINVAL, "out must not alias in");
+    check_fft_keys(c, keys, b);
+    CtView vo = compact_view(c, out->data, 1, b.level - fft_boot_depth(b), 0.0);
+    run_bootstrap_fft(c, *keys->k, vi, b, vo);
+    set_out(out, vo);
+}
+int secpe_bootstrap_fft(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const secpe_boot_fft_cfg *cfg,
+                        secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && keys && in && out && out->data && cfg && cfg->poly && cfg->cts && cfg->stc, SECPE_EINVAL,
+                "null argument");
+        REQUIRE(cfg->n_cts >= 1 && cfg->n_stc == cfg->n_cts, SECPE_EINVAL, "stage counts");
+        REQUIRE(cfg->r >= 0 && cfg->r <= 30 && cfg->K > 0, SECPE_EINVAL, "bad EvalMod range");
+        Ctx &c = ctx->c;
+        FftBootCfg b;
+        b.level = cfg->level;
+        b.r = cfg->r;
+        b.K = cfg->K;
+        b.poly.assign(cfg->poly, cfg->poly + 16);
+        for (int i = 0; i < cfg->n_cts; i++) b.cts.push_back(lt_stage(c, cfg->cts[i]));
+        for (int i = 0; i < cfg->n_stc; i++) b.stc.push_back(lt_stage(c, cfg->stc[i]));
+        b.cts_im = lt_stage(c, cfg->cts_im);
+        b.stc_im = lt_stage(c, cfg->stc_im);
+        bootstrap_fft_views(c, keys, in, b, out);
+    });
+}
+int secpe_boot_create_fft(secpe_ctx *ctx, int32_t level, double K, int32_t r, const int32_t *groups,
+                          int32_t n_groups, double in_scale, secpe_boot **out) {
+    return guard([&] {
+        REQUIRE(ctx && out && groups && n_groups >= 1 && in_scale > 0, SECPE_EINVAL, "null argument");
+        auto h = std::make_unique<secpe_boot>();
+        h->b.reset(boot_setup_fft(ctx->c, level, K, r, std::vector<int>(groups, groups + n_groups), in_scale));
+        *out = h.release();
+    });
+}
+int32_t secpe_boot_levels(const secpe_boot *boot, int32_t *raise_level) {
+    if (!boot || !boot->b) return -1;
+    const BootSetup &b = *boot->b;
+    if (raise_level) *raise_level = b.fft ? b.fcfg.level : b.cfg.level;
+    return b.fft ? fft_boot_depth(b.fcfg) : boot_depth(b.cfg);
+}
+int secpe_bootstrap_boot(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const secpe_boot *boot,
+                         secpe_ct *out) {
+    if (boot && boot->b && !boot->b->fft) {
+        secpe_boot_cfg cfg;
+        const int rc = secpe_boot_get_cfg(boot, &cfg);
+        return rc ? rc : secpe_bootstrap(ctx, keys, in, &cfg, out);
+    }
+    return guard([&] {
+        REQUIRE(ctx && keys && in && out && out->data && boot && boot->b, SECPE_EINVAL, "null argument");
+        bootstrap_fft_views(ctx->c, keys, in, boot->b->fcfg, out);
+    });
+}
+int secpe_boot_stage_export(secpe_ctx *ctx, const secpe_boot *boot, int32_t kind, int32_t idx, int32_t *n_diag,
+                            int32_t *steps, uint64_t *host_out, size_t n_words) {
+    return guard([&] {
+        REQUIRE(ctx && boot && boot->b && boot->b->fft && n_diag && kind >= 0 && kind < 4, SECPE_EINVAL,
+                "bad argument");
+        const FftBootCfg &f = boot->b->fcfg;
+        const LtStage *s = nullptr;
+        if (kind == 1) s = &f.cts_im;
+        if (kind == 3) s = &f.stc_im;
+        if (kind == 0) {
+            REQUIRE(idx >= 0 && idx < (int)f.cts.size(), SECPE_EINVAL, "stage index");
+            s = &f.cts[idx];
+        }
+        if (kind == 2) {
+            REQUIRE(idx >= 0 && idx < (int)f.stc.size(), SECPE_EINVAL, "stage index");
+            s = &f.stc[idx];
+        }
+        *n_diag = (int)s->steps.size();
+        if (steps) std::copy(s->steps.begin(), s->steps.end(), steps);
+        const int mc = (int)f.cts.size(), base = f.level - mc - 6 - f.r;
+        const int lv = kind == 0 ? f.level - idx : kind == 1 ? f.level - (mc - 1) : kind == 2 ? base - idx : base;
+        REQUIRE(!host_out || n_words == (size_t)*n_diag * (lv + 1) * ctx->c.N, SECPE_EINVAL,
+                "n_words does not match the stage size");
+        if (host_out) {
+            CUDA_CHECK(cudaMemcpyAsync(host_out, s->pts, n_words * 8, cudaMemcpyDeviceToHost, ctx->c.st));
+            CUDA_CHECK(cudaStreamSynchronize(ctx->c.st));
+        }
     });
 }
 int32_t secpe_boot_depth(const secpe_boot_cfg *cfg) { return cfg ? 8 + cfg->r : -1; }

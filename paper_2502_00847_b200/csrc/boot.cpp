@@ -9,7 +9,9 @@
 //   poly: Taylor coefficients of 2 cos(a x + b), a = 2 pi K / 2^r, b = -pi / 2^(r+1), up to x^15.
 #include <cmath>
 #include <complex>
+#include <algorithm>
 #include <functional>
+#include <map>
 
 #include "context.h"
 
@@ -86,5 +88,163 @@ BootSetup *boot_setup(Ctx &c, int level, double K, int r, int n1, int n2, double
     b->cfg.stc_im = b->stc_im.p;
     b->cfg.cts_scale = cts_scale;
     b->cfg.stc_scale = stc_scale;
+    return b.release();
+}
+
+// ---- factorised CoeffToSlot / SlotToCoeff (R37) ------------------------------------------------------
+// Special-FFT butterfly stage s (len = 2^s, h = len/2), block start i, j < h, w_j = zeta^m,
+// m = (e_j mod 4 len) 2N / (4 len):  out[i+j] = v[i+j] + w_j v[i+j+h], out[i+j+h] = v[i+j] - w_j v[i+j+h];
+// U w = S_log2n ... S_1 (bit-reversed w).  Diagonal form: offset (mod n) -> vector, out = sum d_o (.) RotL(v, o).
+using Diag = std::map<long, std::vector<cd>>;
+
+static std::vector<Diag> fft_stages(long N, bool inverse) {
+    const long n = N / 2;
+    std::vector<long> e(n);
+    for (long j = 0, v = 1; j < n; j++, v = (v * 5) % (2 * N)) e[j] = v;
+    std::vector<Diag> out;
+    for (long ln = 2; ln <= n; ln *= 2) {
+        const long h = ln / 2;
+        std::vector<cd> d0(n), dp(n), dm(n);
+        for (long i = 0; i < n; i += ln)
+            for (long j = 0; j < h; j++) {
+                const long m = (e[j] % (4 * ln)) * (2 * N / (4 * ln));
+                const double ang = M_PI * (double)m / (double)N;
+                if (!inverse) {
+                    const cd w(std::cos(ang), std::sin(ang));
+                    d0[i + j] = 1.0;
+                    dp[i + j] = w;
+                    dm[i + j + h] = 1.0;
+                    d0[i + j + h] = -w;
+                } else {
+                    const cd wi(std::cos(ang), -std::sin(ang));
+                    d0[i + j] = 0.5;
+                    dp[i + j] = 0.5;
+                    dm[i + j + h] = 0.5 * wi;
+                    d0[i + j + h] = -0.5 * wi;
+                }
+            }
+        Diag D;
+        D[0] = d0;
+        if (h == n - h) {
+            for (long p = 0; p < n; p++) dp[p] += dm[p];
+            D[h] = dp;
+        } else {
+            D[h] = dp;
+            D[n - h] = dm;
+        }
+        out.push_back(std::move(D));
+    }
+    return out;
+}
+
+// A B (A applied after B): sum_{a,b} (alpha_a (.) RotL(beta_b, a)) (.) RotL(v, a + b)
+static Diag diag_mul(const Diag &A, const Diag &B, long n) {
+    Diag out;
+    for (const auto &x : A)
+        for (const auto &y : B) {
+            auto &o = out[(x.first + y.first) % n];
+            if (o.empty()) o.assign(n, cd(0, 0));
+            for (long p = 0; p < n; p++) o[p] += x.second[p] * y.second[(p + x.first) % n];
+        }
+    return out;
+}
+
+// encode every diagonal of D (times `mul`) at `scale` on `level`; steps = signed offsets, ascending
+static LtStage encode_stage(Ctx &c, const Diag &D, cd mul, int level, double scale, std::vector<DevBuf> &bufs) {
+    const long N = c.N, n = N / 2;
+    const int nl = level + 1;
+    std::vector<std::pair<long, long>> order;  // (signed offset, key)
+    for (const auto &x : D) order.push_back({x.first > n / 2 ? x.first - n : x.first, x.first});
+    std::sort(order.begin(), order.end());
+    const long nd = (long)order.size();
+    LtStage st;
+    std::vector<i64> coef((size_t)nd * N);
+    std::vector<double> re(n), im(n);
+    for (long i = 0; i < nd; i++) {
+        const auto &d = D.at(order[i].second);
+        for (long t = 0; t < n; t++) {
+            const cd v = d[t] * mul;
+            re[t] = v.real();
+            im[t] = v.imag();
+        }
+        encode_complex_int(c, re.data(), im.data(), n, scale, coef.data() + i * N);
+        st.steps.push_back((int)order[i].first);
+    }
+    DevBuf out((size_t)nd * nl * N, c.st), dc((size_t)nd * N, c.st);
+    CUDA_CHECK(cudaMemcpyAsync(dc.p, coef.data(), (size_t)nd * N * 8, cudaMemcpyHostToDevice, c.st));
+    for (long i = 0; i < nd; i++)
+        k_int_to_rows(c.tab, c.logn, (const i64 *)dc.p + i * N, out.p + (size_t)i * nl * N, LimbMap{nl, nl, 0, 0},
+                      c.st);
+    ev_ntt(c, RowsArg{out.p, 2L * nl * N, (long)nl * N}, (int)nd, LimbMap{nl, nl, 0, 0}, false);
+    CUDA_CHECK(cudaStreamSynchronize(c.st));
+    st.pts = out.p;
+    st.scale = scale;
+    bufs.push_back(std::move(out));
+    return st;
+}
+
+BootSetup *boot_setup_fft(Ctx &c, int level, double K, int r, const std::vector<int> &groups, double in_scale) {
+    const long N = c.N, n = N / 2;
+    int lg = 0;
+    while ((1L << lg) < n) lg++;
+    int sum = 0;
+    for (int g : groups) {
+        if (g < 1) throw SecpeError{-1, "boot: empty stage group"};
+        sum += g;
+    }
+    if (sum != lg) throw SecpeError{-1, "boot: groups must cover log2(N/2) stages"};
+    if (!(K > 0) || r < 0 || r > 30) throw SecpeError{-1, "boot: bad EvalMod range"};
+    const int mg = (int)groups.size();
+    if (level >= c.nq || level - (2 * mg + 6 + r) < 0) throw SecpeError{-2, "boot: not enough levels"};
+    auto b = std::make_unique<BootSetup>();
+    b->fft = true;
+    FftBootCfg &f = b->fcfg;
+    f.level = level;
+    f.r = r;
+    f.K = K;
+    const double a = 2.0 * M_PI * K / std::ldexp(1.0, r), ph = -M_PI / std::ldexp(1.0, r + 1);
+    f.poly.resize(16);
+    double fact = 1.0;
+    for (int i = 0; i < 16; i++) {
+        if (i) fact *= i;
+        f.poly[i] = 2.0 * std::pow(a, i) * std::cos(ph + i * M_PI / 2) / fact;
+    }
+    const auto st = fft_stages(N, false), si = fft_stages(N, true);
+    std::vector<Diag> stc, cts;
+    int pos = 0;
+    for (int g : groups) {
+        Diag D, Di;
+        D[0].assign(n, cd(1, 0));
+        Di[0].assign(n, cd(1, 0));
+        for (int s = pos; s < pos + g; s++) {
+            D = diag_mul(st[s], D, n);
+            Di = diag_mul(Di, si[s], n);
+        }
+        stc.push_back(std::move(D));
+        cts.push_back(std::move(Di));
+        pos += g;
+    }
+    std::reverse(cts.begin(), cts.end());
+    const double R = (double)c.primes[0] / in_scale, cc = R / (4.0 * M_PI);
+    int lv = level;
+    for (int i = 0; i < mg; i++, lv--) {
+        const double sc = (double)c.primes[lv];
+        if (i < mg - 1) {
+            f.cts.push_back(encode_stage(c, cts[i], cd(1, 0), lv, sc, b->bufs));
+        } else {
+            f.cts.push_back(encode_stage(c, cts[i], cd(0.5, 0), lv, sc, b->bufs));
+            f.cts_im = encode_stage(c, cts[i], cd(0, -0.5), lv, sc, b->bufs);
+        }
+    }
+    lv = level - mg - 6 - r;
+    for (int i = 0; i < mg; i++, lv--) {
+        const double sc = (double)c.primes[lv];
+        if (i == 0) {
+            f.stc.push_back(encode_stage(c, stc[i], cd(cc, 0), lv, sc, b->bufs));
+            f.stc_im = encode_stage(c, stc[i], cd(0, cc), lv, sc, b->bufs);
+        } else {
+            f.stc.push_back(encode_stage(c, stc[i], cd(1, 0), lv, sc, b->bufs));
+        }
+    }
     return b.release();
 }

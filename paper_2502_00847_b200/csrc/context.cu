@@ -194,9 +194,11 @@ void Ctx::log(const char *kind, int lin, int lout, double s, const std::string &
     if (!log_on) return;
     u64 bits;
     std::memcpy(&bits, &s, 8);
-    char buf[128];
-    snprintf(buf, sizeof buf, "%s %d %d %016llx %s\n", kind, lin, lout, (unsigned long long)bits, extra.c_str());
+    char buf[96];
+    snprintf(buf, sizeof buf, "%s %d %d %016llx ", kind, lin, lout, (unsigned long long)bits);
     oplog += buf;
+    oplog += extra;  // unbounded (a transform's step list)
+    oplog += '\n';
 }
 
 // ---------------------------------------------------------------------------------------------

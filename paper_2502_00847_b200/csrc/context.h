@@ -248,13 +248,33 @@ struct BootCfg {
 };
 constexpr int kConjStep = INT32_MIN;  // SECPE_CONJ: slot conjugation, Galois element 2N - 1 (R32)
 int boot_depth(const BootCfg &b);
+// factorised variant (R37): CoeffToSlot / SlotToCoeff as groups of special-FFT stages, each a hoisted
+// diagonal transform (R30); pts dev [n_diag][stage level + 1][N]
+struct LtStage {
+    std::vector<int> steps;
+    const u64 *pts = nullptr;
+    double scale = 0;
+};
+struct FftBootCfg {
+    int level = 0, r = 0;
+    double K = 0;
+    std::vector<double> poly;
+    std::vector<LtStage> cts, stc;  // cts.back(): Re variant of the last CoeffToSlot stage; stc[0]: Re variant
+    LtStage cts_im, stc_im;
+};
+int fft_boot_depth(const FftBootCfg &b);
+void run_bootstrap_fft(Ctx &c, const Keys &k, const CtView &in, const FftBootCfg &b, CtView &out);
 // library-built bootstrapping material (secpe_boot_create): the EvalMod polynomial and the four encoded
 // matrices, NTT form, [n2][n1][limbs][N] each
 struct BootSetup {
+    bool fft = false;
     BootCfg cfg;
     DevBuf cts_re, cts_im, stc_re, stc_im;
+    FftBootCfg fcfg;               // fft: the stages, pts in `bufs`
+    std::vector<DevBuf> bufs;
 };
 BootSetup *boot_setup(Ctx &c, int level, double K, int r, int n1, int n2, double in_scale);
+BootSetup *boot_setup_fft(Ctx &c, int level, double K, int r, const std::vector<int> &groups, double in_scale);
 void run_bootstrap(Ctx &c, const Keys &k, const CtView &in, const BootCfg &b, CtView &out);
 struct Layout {
     int queries, prompts, classes, block;

@@ -217,6 +217,41 @@ struct Ev {
         c.log("LTB", l, l - 1, s, std::to_string(n1) + "x" + std::to_string(n2));
         return out;
     }
+    // hoisted diagonal transform Rescale(sum_i pt_i (.) RotL(x, steps_i)) (R30); scale (S_x pt_scale) / q_l
+    Val lt(const Val &x, const LtStage &st) {
+        if (n != 1) throw SecpeError{-1, "lt: one ciphertext"};
+        const int l = x.level();
+        const double s = (x.scale() * st.scale) / q(l);
+        Val out = fresh(l - 1, s);
+        ev_linear_transform(c, k, x.v, st.pts, (long)(l + 1) * c.N, st.steps.data(), (int)st.steps.size(), out.v);
+        std::string ex;
+        for (size_t i = 0; i < st.steps.size(); i++) ex += (i ? "," : "") + std::to_string(st.steps[i]);
+        c.log("LT", l, l - 1, s, ex);
+        return out;
+    }
+    // EvalMod on one CoeffToSlot output u (R35): x = u + conj(u), x / (K R), doubled cosine, r doublings
+    Val evalmod(const Val &u, double K, int r, const std::vector<double> &poly, double S0) {
+        const double inv = 1.0 / (K * ((double)c.primes[0] / S0));
+        Val x = rot_add(u, kConjStep);
+        Val xn = mul_const(x, inv, c.scale, x.level() - 1);
+        Val d = poly15(xn, poly, c.scale);
+        for (int j = 0; j < r; j++) d = add_const(mul_ct(d, d, NAN, d.level() - 1), -2.0);
+        return d;
+    }
+    // factorised bootstrap (R37): ModRaise; CoeffToSlot stages (the last in Re / Im variants); EvalMod on
+    // both; SlotToCoeff's first stage on d_re and d_im, summed; the remaining SlotToCoeff stages
+    Val bootstrap_fft(const Val &in, const FftBootCfg &b) {
+        const double S0 = in.scale();
+        Val v = mod_raise(in, b.level);
+        for (size_t i = 0; i + 1 < b.cts.size(); i++) v = lt(v, b.cts[i]);
+        Val us[2] = {lt(v, b.cts.back()), lt(v, b.cts_im)};
+        Val ds[2] = {evalmod(us[0], b.K, b.r, b.poly, S0), evalmod(us[1], b.K, b.r, b.poly, S0)};
+        Val o_re = lt(ds[0], b.stc[0]);
+        Val o_im = lt(ds[1], b.stc_im);
+        Val o = add(o_re, o_im);
+        for (size_t i = 1; i < b.stc.size(); i++) o = lt(o, b.stc[i]);
+        return o;
+    }
     // general degree-15 p(x) = sum_i c_i x^i at (T, level(x) - 5) (R35): the odd plan's Paterson-Stockmeyer
     // shape with the even terms added, q_k = c_{4k} + c_{4k+1} x + c_{4k+2} x^2 + c_{4k+3} x^3,
     // p = (q_0 + q_1 x^4) + (q_2 + q_3 x^4) x^8
@@ -248,15 +283,7 @@ struct Ev {
         const double S0 = in.scale();
         Val z = mod_raise(in, b.level);
         Val us[2] = {lt_bsgs(z, b.cts_re, b.n1, b.n2, b.cts_scale), lt_bsgs(z, b.cts_im, b.n1, b.n2, b.cts_scale)};
-        const double inv = 1.0 / (b.K * ((double)c.primes[0] / S0));
-        Val ds[2];
-        for (int i = 0; i < 2; i++) {
-            Val x = rot_add(us[i], kConjStep);
-            Val xn = mul_const(x, inv, c.scale, x.level() - 1);
-            Val d = poly15(xn, b.poly, c.scale);
-            for (int j = 0; j < b.r; j++) d = add_const(mul_ct(d, d, NAN, d.level() - 1), -2.0);
-            ds[i] = d;
-        }
+        Val ds[2] = {evalmod(us[0], b.K, b.r, b.poly, S0), evalmod(us[1], b.K, b.r, b.poly, S0)};
         Val o_re = lt_bsgs(ds[0], b.stc_re, b.n1, b.n2, b.stc_scale);
         Val o_im = lt_bsgs(ds[1], b.stc_im, b.n1, b.n2, b.stc_scale);
         return add(o_re, o_im);
@@ -370,6 +397,16 @@ std::vector<int> argmax_rotations(const Layout &lay) {
 }
 
 int boot_depth(const BootCfg &b) { return 8 + b.r; }
+int fft_boot_depth(const FftBootCfg &b) { return (int)b.cts.size() + (int)b.stc.size() + 6 + b.r; }
+
+void run_bootstrap_fft(Ctx &c, const Keys &k, const CtView &in, const FftBootCfg &b, CtView &out) {
+    Ev ev{c, k, in.n};
+    Val x{nullptr, in};
+    Val r = ev.bootstrap_fft(x, b);
+    out.level = r.level();
+    out.scale = r.scale();
+    ev_copy(c, r.v, out);
+}
 
 void run_bootstrap(Ctx &c, const Keys &k, const CtView &in, const BootCfg &b, CtView &out) {
     Ev ev{c, k, in.n};

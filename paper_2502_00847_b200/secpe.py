@@ -31,6 +31,16 @@ class SignCfg(ctypes.Structure):
     _fields_ = [("n_stages", ctypes.c_int32), ("degrees", i32p), ("coeffs", f64p)]
 
 
+class CLtStage(ctypes.Structure):
+    _fields_ = [("n_diag", ctypes.c_int32), ("steps", i32p), ("pts", u64p), ("pt_scale", ctypes.c_double)]
+
+
+class CBootFftCfg(ctypes.Structure):
+    _fields_ = [("level", ctypes.c_int32), ("K", ctypes.c_double), ("r", ctypes.c_int32), ("poly", f64p),
+                ("n_cts", ctypes.c_int32), ("cts", ctypes.POINTER(CLtStage)), ("cts_im", CLtStage),
+                ("n_stc", ctypes.c_int32), ("stc", ctypes.POINTER(CLtStage)), ("stc_im", CLtStage)]
+
+
 class CBootCfg(ctypes.Structure):
     _fields_ = [("level", ctypes.c_int32), ("n1", ctypes.c_int32), ("n2", ctypes.c_int32), ("K", ctypes.c_double),
                 ("r", ctypes.c_int32), ("poly", f64p), ("cts_re", u64p), ("cts_im", u64p), ("cts_scale", ctypes.c_double),
@@ -95,6 +105,14 @@ SIGS = {
     "secpe_boot_get_cfg": (ctypes.c_int, [vp, ctypes.POINTER(CBootCfg)]),
     "secpe_boot_destroy": (None, [vp]),
     "secpe_boot_export": (ctypes.c_int, [vp, vp, ctypes.c_int32, u64p, ctypes.c_size_t]),
+    "secpe_bootstrap_fft": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.POINTER(CBootFftCfg),
+                                           ctypes.POINTER(CCt)]),
+    "secpe_boot_create_fft": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.c_double, ctypes.c_int32, i32p,
+                                             ctypes.c_int32, ctypes.c_double, ctypes.POINTER(vp)]),
+    "secpe_bootstrap_boot": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), vp, ctypes.POINTER(CCt)]),
+    "secpe_boot_levels": (ctypes.c_int32, [vp, i32p]),
+    "secpe_boot_stage_export": (ctypes.c_int, [vp, vp, ctypes.c_int32, ctypes.c_int32, i32p, i32p, u64p,
+                                               ctypes.c_size_t]),
     "secpe_bootstrap": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.POINTER(CBootCfg), ctypes.POINTER(CCt)]),
     "secpe_linear_transform_bsgs": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), u64p, ctypes.c_int32, ctypes.c_int32,
                                                    ctypes.c_double, ctypes.POINTER(CCt)]),
@@ -232,6 +250,20 @@ class Boot:
         out = np.zeros((c["n2"], c["n1"], lv + 1, self.ctx.N), dtype=np.uint64)
         _chk(lib().secpe_boot_export(self.ctx.h, self.h, which, out.ctypes.data_as(u64p), out.size))
         return out
+
+    def stage(self, kind, idx=0, level=None):
+        """Factorised stage (kind 0 cts[idx], 1 cts_im, 2 stc[idx], 3 stc_im): (steps, host pts or None)."""
+        nd = ctypes.c_int32(0)
+        _chk(lib().secpe_boot_stage_export(self.ctx.h, self.h, kind, idx, ctypes.byref(nd), None, None, 0))
+        steps = np.zeros(nd.value, dtype=np.int32)
+        if level is None:
+            _chk(lib().secpe_boot_stage_export(self.ctx.h, self.h, kind, idx, ctypes.byref(nd),
+                                               steps.ctypes.data_as(i32p), None, 0))
+            return steps.tolist(), None
+        pts = np.zeros((nd.value, level + 1, self.ctx.N), dtype=np.uint64)
+        _chk(lib().secpe_boot_stage_export(self.ctx.h, self.h, kind, idx, ctypes.byref(nd),
+                                           steps.ctypes.data_as(i32p), pts.ctypes.data_as(u64p), pts.size))
+        return steps.tolist(), pts
 
     def cfg(self):
         """(level, n1, n2, K, r, poly[16], cts_scale, stc_scale) of the configuration."""
@@ -457,6 +489,47 @@ class Context:
         h = vp()
         _chk(lib().secpe_boot_create(self.h, level, K, r, n1, n2, in_scale, ctypes.byref(h)))
         return Boot(self, h)
+
+    def boot_create_fft(self, level, K, r, groups, in_scale):
+        """secpe_boot_create_fft: library-built factorised material (reading R37)."""
+        g = np.ascontiguousarray(groups, dtype=np.int32)
+        h = vp()
+        _chk(lib().secpe_boot_create_fft(self.h, level, K, r, g.ctypes.data_as(i32p), len(g), in_scale,
+                                         ctypes.byref(h)))
+        return Boot(self, h)
+
+    def bootstrap_boot(self, keys, a, boot):
+        """secpe_bootstrap_boot: bootstrap with library-built material of either kind."""
+        rl = ctypes.c_int32(0)
+        depth = lib().secpe_boot_levels(boot.h, ctypes.byref(rl))
+        out = self._out(max(rl.value - depth, 0))
+        ca, co = a.c(), out.c()
+        _chk(lib().secpe_bootstrap_boot(self.h, keys.h, ctypes.byref(ca), boot.h, ctypes.byref(co)))
+        out.level, out.scale = co.level, co.scale
+        return out
+
+    def bootstrap_fft(self, keys, a, level, K, r, poly, cts, cts_im, stc, stc_im):
+        """secpe_bootstrap_fft (reading R37); every stage a (steps, pts, pt_scale) triple, pts a cuda
+        uint64 tensor [n_diag][limbs][N]."""
+        keep = []
+
+        def stage(t):
+            steps, pts, sc = t
+            assert pts.is_cuda and pts.dtype == torch.uint64 and pts.is_contiguous() and pts.shape[0] == len(steps)
+            st = np.ascontiguousarray(steps, dtype=np.int32)
+            keep.append(st)
+            return CLtStage(len(steps), st.ctypes.data_as(i32p), ctypes.cast(pts.data_ptr(), u64p), sc)
+        pc = np.ascontiguousarray(poly, dtype=np.float64)
+        assert pc.shape == (16,)
+        ca_ = (CLtStage * len(cts))(*[stage(t) for t in cts])
+        cs_ = (CLtStage * len(stc))(*[stage(t) for t in stc])
+        cfg = CBootFftCfg(level, K, r, pc.ctypes.data_as(f64p), len(cts), ca_, stage(cts_im), len(stc), cs_,
+                          stage(stc_im))
+        out = self._out(max(level - (len(cts) + len(stc) + 6 + r), 0))
+        ca, co = a.c(), out.c()
+        _chk(lib().secpe_bootstrap_fft(self.h, keys.h, ctypes.byref(ca), ctypes.byref(cfg), ctypes.byref(co)))
+        out.level, out.scale = co.level, co.scale
+        return out
 
     def bootstrap_with(self, keys, a, boot):
         """secpe_bootstrap with the configuration of a Boot object (secpe_boot_get_cfg)."""

@@ -34,6 +34,9 @@ PARAM_SETS = {
                       alpha=7, log_scale=50),
     "boot": dict(logn=12, q=[("below", 60, 1), ("nearest", 50, 20)], p=[("below", 60, 7)],
                  alpha=7, log_scale=50),
+    # the paper's ring (N = 2^16, 32768 slots) with the factorised transforms (R37, groups 5/5/5: depth 20)
+    "boot16": dict(logn=16, q=[("below", 60, 1), ("nearest", 50, 22)], p=[("below", 60, 7)],
+                   alpha=7, log_scale=50),
     # BASELINE configs[1]: NTT microbench, 24 x 60-bit primes, N = 2^16.
     "ntt": dict(logn=16, q=[("below", 60, 24)], p=[], alpha=8, log_scale=50),
     # BASELINE configs[2]/[3]: 24 x 60-bit q, dnum = 3 -> alpha = 8, 8 special 60-bit primes, scale 2^50.

@@ -870,3 +870,96 @@ def test_boot_setup_matches_oracle_encoding(boot, boot_cfg):
     out = g.bootstrap_with(kg, P.up(ct), b)
     assert out.level == prm.L - plan.boot_depth(BOOT["r"])
     assert np.abs(g.decrypt(kg, out) - z).max() < 2 ** -12
+
+
+FFT_GROUPS = [4, 4, 3]
+
+
+@pytest.fixture(scope="module")
+def boot_fft(S):
+    P = pair(S, "boot")
+    ev = ckks.Oracle(P.prm)
+    rot = plan.fft_boot_rotations(P.prm.N, FFT_GROUPS)
+    seed = synth.KEY_SEED_BASE + 29
+    ko, kg = ev.keygen(seed, rot, h=BOOT["h"]), P.gpu.keygen(seed, rot, h=BOOT["h"])
+    cfg = plan.fft_boot_config(ev, P.prm.scale, P.prm.L, BOOT["K"], BOOT["r"], FFT_GROUPS)
+    return P, ev, ko, kg, cfg
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_bootstrap_fft_bit_exact(boot_fft):
+    """R37: secpe_bootstrap_fft (special-FFT CoeffToSlot / SlotToCoeff in 3 + 3 hoisted diagonal transforms)
+    is word for word the oracle's bootstrap_fft with the same op list; decrypts within 2^-12."""
+    P, ev, ko, kg, cfg = boot_fft
+    prm, g = P.prm, P.gpu
+    z = np.random.default_rng(7).uniform(-1, 1, prm.N // 2)
+    ct = ev.encrypt(ko, z, prm.scale, 25, level=0)
+    ev.log.clear()
+    want = plan.bootstrap_fft(ev, ko, ct, cfg)
+    olog = list(ev.log)
+    dev = lambda t: (t[0], torch.from_numpy(np.stack(t[1])).cuda(), t[2])
+    g.oplog(enable=True, clear=True)
+    got = g.bootstrap_fft(kg, P.up(ct), cfg["level"], cfg["K"], cfg["r"], cfg["poly"], [dev(t) for t in cfg["cts"]],
+                          dev(cfg["cts_im"]), [dev(t) for t in cfg["stc"]], dev(cfg["stc_im"]))
+    glog = g.oplog(enable=False, clear=True)
+    assert glog == olog
+    assert got.level == want.level == prm.L - plan.fft_boot_depth(FFT_GROUPS, BOOT["r"])
+    assert got.scale == want.scale
+    assert np.array_equal(P.down(got), want.data)
+    assert np.abs(g.decrypt(kg, got) - z).max() < 2 ** -12
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_boot_fft_setup_matches_oracle(boot_fft):
+    """secpe_boot_create_fft: the library's own special-FFT factorisation has the oracle's steps per stage,
+    pts equal up to FFT rounding (coefficients within 1 + 2^-46 max|c|), and bootstraps within 2^-12."""
+    P, ev, ko, kg, cfg = boot_fft
+    prm, g = P.prm, P.gpu
+    b = g.boot_create_fft(prm.L, BOOT["K"], BOOT["r"], FFT_GROUPS, prm.scale)
+    mc = len(FFT_GROUPS)
+    base = prm.L - mc - 6 - BOOT["r"]
+    cases = [(0, i, cfg["cts"][i], prm.L - i) for i in range(mc)] + [(1, 0, cfg["cts_im"], prm.L - mc + 1)]
+    cases += [(2, i, cfg["stc"][i], base - i) for i in range(mc)] + [(3, 0, cfg["stc_im"], base)]
+    q0 = prm.primes[0]
+    for kind, idx, (steps, pts, sc), lv in cases:
+        gs, gp = b.stage(kind, idx, lv)
+        assert gs == list(steps), (kind, idx)
+        want = np.stack(pts)
+        same = (gp == want).all(axis=(1, 2))
+        if same.all():
+            continue
+        gi = ckks.ntt_limbs(gp[~same][:, :1], prm, [0], inverse=True)[:, 0].astype(object)
+        wi = ckks.ntt_limbs(want[~same][:, :1], prm, [0], inverse=True)[:, 0].astype(object)
+        d = (gi - wi) % q0
+        d = np.where(d > q0 // 2, d - q0, d)
+        wc = np.where(wi > q0 // 2, wi - q0, wi)
+        tol = 1 + int(float(np.abs(wc).max()) * 2.0 ** -46)
+        assert np.abs(d).max() <= tol, (kind, idx, int(np.abs(d).max()), tol)
+    z = np.random.default_rng(8).uniform(-1, 1, prm.N // 2)
+    ct = ev.encrypt(ko, z, prm.scale, 26, level=0)
+    out = g.bootstrap_boot(kg, P.up(ct), b)
+    assert out.level == prm.L - plan.fft_boot_depth(FFT_GROUPS, BOOT["r"])
+    assert np.abs(g.decrypt(kg, out) - z).max() < 2 ** -12
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_bootstrap_n16_refreshes(S):
+    """N3 at the paper's ring, N = 2^16 (32768 slots): library-built factorised material (groups 5/5/5), sparse
+    secret h = 64; the refreshed ciphertext decrypts to the input slots within 2^-10 (the oracle is too slow at
+    this size for a word-for-word run; the N = 2^12 tests pin the same code path word for word)."""
+    from paper_2502_00847_b200 import secpe
+    g = secpe.Context(synth.PARAM_SETS["boot16"])
+    groups, K, r = [5, 5, 5], 16, 8
+    n = g.N // 2
+    rot = plan.fft_boot_rotations(g.N, groups)
+    kg = g.keygen(synth.KEY_SEED_BASE + 31, rot, h=64)
+    b = g.boot_create_fft(g.L, K, r, groups, g.scale)
+    z = np.random.default_rng(9).uniform(-1, 1, n)
+    ct = g.encrypt(kg, z, 0, g.scale, 27)
+    out = g.bootstrap_boot(kg, ct, b)
+    assert out.level == g.L - (2 * len(groups) + 6 + r)
+    assert np.abs(g.decrypt(kg, out) - z).max() < 2 ** -10
+

@@ -783,3 +783,53 @@ def test_bootstrap_refreshes_levels(boot_tiny):
     # and it computes on: one more product after the refresh
     sq = ev.mul_ct(keys, out, out, None, out.level - 1)
     assert np.abs(ev.decrypt(keys, sq).real - z * z).max() < 2 ** -13
+
+
+def test_special_fft_stages_factor_decoding():
+    """R37: the butterfly stages applied to the bit-reversed coefficient vector give U w with U[j][k] =
+    zeta^{5^j k} (the decoding definition, written out); the inverse stages undo it; merged groups in
+    diagonal form equal the stages applied one by one."""
+    for logn in (4, 6, 8):
+        N, n = 1 << logn, 1 << (logn - 1)
+        e = [pow(5, j, 2 * N) for j in range(n)]
+        U = np.array([[np.exp(1j * np.pi * ((e[j] * k) % (2 * N)) / N) for k in range(n)] for j in range(n)])
+        rng = np.random.default_rng(logn)
+        w = rng.normal(size=n) + 1j * rng.normal(size=n)
+        br = plan.bitrev_perm(n)
+        assert sorted(br) == list(range(n)) and all(br[br[i]] == i for i in range(n))
+        v = w[br]
+        for S in plan.dft_stages(N):
+            assert len(S) <= 3
+            v = plan.diag_apply(S, v)
+        assert np.abs(v - U @ w).max() < 1e-12
+        z = U @ w
+        for S in plan.dft_stages_inv(N)[::-1]:
+            z = plan.diag_apply(S, z)
+        assert np.abs(z - w[br]).max() < 1e-12
+        groups = [logn - 3, 2]
+        stc, cts = plan.fft_groups(N, groups)
+        assert [len(D) for D in stc] == [2 ** (g + 1) - 1 if i < len(groups) - 1 else 2 ** g
+                                         for i, g in enumerate(groups)]
+        v = w[br]
+        for D in stc:
+            v = plan.diag_apply(D, v)
+        assert np.abs(v - U @ w).max() < 1e-12
+        z = U @ w
+        for D in cts:
+            z = plan.diag_apply(D, z)
+        assert np.abs(z - w[br]).max() < 1e-12
+
+
+def test_bootstrap_fft_refreshes():
+    """R37 end to end (N = 2^8, groups 3 + 4): decrypts to the input slots within 2^-14 at level
+    L - (2 * 2 + 6 + r)."""
+    prm = ckks.Params(synth.PARAM_SETS["boot_tiny"])
+    ev = ckks.Oracle(prm)
+    groups, K, r = [3, 4], 16, 8
+    keys = ev.keygen(9, plan.fft_boot_rotations(prm.N, groups), h=64)
+    z = np.random.default_rng(10).uniform(-1, 1, prm.N // 2)
+    ct = ev.encrypt(keys, z, prm.scale, 5, level=0)
+    cfg = plan.fft_boot_config(ev, ct.scale, prm.L, K, r, groups)
+    out = plan.bootstrap_fft(ev, keys, ct, cfg)
+    assert out.level == prm.L - plan.fft_boot_depth(groups, r)
+    assert np.abs(ev.decrypt(keys, out).real - z).max() < 2 ** -14
