@@ -215,14 +215,15 @@ def micro_configs(stream, reps=5):
 
 
 def bootstrap_bench(stream, t_ms):
-    """one CKKS bootstrap (readings R32-R36) of a level-0 ciphertext at N = 2^12 (2048 slots,
-    dense BSGS 64 x 32 CoeffToSlot / SlotToCoeff, sparse secret h = 64, K = 16, r = 8), library-built matrices
-    (secpe_boot_create).  Latency of one call on one GPU, CUDA events, median."""
+    """one CKKS bootstrap (readings R32-R37) of a level-0 ciphertext, sparse secret h = 64,
+    K = 16, r = 7, library-built material: N = 2^12 with dense BSGS 64 x 32 transforms (secpe_boot_create) and
+    N = 2^16 with the factorised special-FFT transforms (secpe_boot_create_fft).  Latency of one call on one
+    GPU, CUDA events, median."""
     import torch
     import synth
     from paper_2502_00847_b200 import secpe
     ctx = secpe.Context(synth.PARAM_SETS["boot"], stream=stream.cuda_stream)
-    n1, n2, K, r, h = 64, 32, 16, 8, 64
+    n1, n2, K, r, h = 64, 32, 16, 7, 64
     rot = list(range(1, n1)) + [j * n1 for j in range(1, n2)] + [secpe.CONJ]
     keys = ctx.keygen(synth.KEY_SEED_BASE + 23, rot, h=h)
     t0 = time.time()
@@ -240,9 +241,34 @@ def bootstrap_bench(stream, t_ms):
     ms = t_ms(one)
     err = float(abs(ctx.decrypt(keys, res[0]) - z).max())
     ks = 2 * (n1 - 1 + n2 - 1) * 2 + 2 + 2 * (7 + r)
-    return {"ms_per_bootstrap": ms, "logn": ctx.logn, "slots": ctx.N // 2, "level_in": 0, "raised_to": ctx.L,
-            "level_out": res[0].level, "key_switches": ks, "max_abs_err": err, "setup_s": setup_s,
-            "note": "dense BSGS DFT matrices (2 n1 n2 pts each); N = 2^16 needs the factorised DFT (next)"}
+    out = {"N=2^12_dense": {"ms_per_bootstrap": ms, "logn": ctx.logn, "slots": ctx.N // 2, "level_in": 0,
+                            "raised_to": ctx.L, "level_out": res[0].level, "key_switches": ks, "max_abs_err": err,
+                            "setup_s": setup_s, "transforms": "dense BSGS 64 x 32 (R34)"}}
+    del boot, keys, res, c0, ctx
+    # the paper's ring: factorised special-FFT transforms (R37), groups 5/5/5
+    ctx = secpe.Context(synth.PARAM_SETS["boot16"], stream=stream.cuda_stream)
+    groups = [5, 5, 5]
+    t0 = time.time()
+    boot = ctx.boot_create_fft(ctx.L, K, r, groups, ctx.scale)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    steps = boot.steps()
+    keys = ctx.keygen(synth.KEY_SEED_BASE + 31, steps, h=h)
+    z = synth.rng(4002).uniform(-1, 1, ctx.N // 2)
+    c0 = ctx.new_ct(0)
+    ctx.encrypt_coeffs(keys, ctx.encode(z, ctx.scale), 0, ctx.scale, 78, out=c0)
+    c0.level, c0.scale = 0, ctx.scale
+    res = [None]
+
+    def one16():
+        res[0] = ctx.bootstrap_boot(keys, c0, boot)
+    ms = t_ms(one16)
+    err = float(abs(ctx.decrypt(keys, res[0]) - z).max())
+    out["N=2^16_fft"] = {"ms_per_bootstrap": ms, "logn": ctx.logn, "slots": ctx.N // 2, "level_in": 0,
+                         "raised_to": ctx.L, "level_out": res[0].level, "galois_keys": len(steps),
+                         "max_abs_err": err, "setup_s": setup_s,
+                         "transforms": "special-FFT groups 5/5/5, hoisted diagonal transforms (R37)"}
+    return out
 
 def run_secpe(a):
     import torch

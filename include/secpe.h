@@ -308,6 +308,9 @@ int secpe_boot_create_fft(secpe_ctx *ctx, int32_t level, double K, int32_t r, co
 /* Bootstrap with library-built material of either kind; out->data sized for level - secpe_boot_levels. */
 int secpe_bootstrap_boot(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const secpe_boot *boot,
                          secpe_ct *out);
+/* Rotation steps (SECPE_CONJ included) whose Galois keys a library-built bootstrap needs, ascending with
+ * SECPE_CONJ last; returns their count, writes min(count, cap) of them to steps (may be null). */
+int32_t secpe_boot_steps(const secpe_boot *boot, int32_t *steps, int32_t cap);
 /* Depth of a library-built bootstrap; *raise_level (optional) receives its ModRaise level. */
 int32_t secpe_boot_levels(const secpe_boot *boot, int32_t *raise_level);
 /* A factorised stage for parity tests: kind 0 cts[idx], 1 cts_im, 2 stc[idx], 3 stc_im.  Writes *n_diag;

@@ -599,6 +599,28 @@ int secpe_boot_create_fft(secpe_ctx *ctx, int32_t level, double K, int32_t r, co
         *out = h.release();
     });
 }
+int32_t secpe_boot_steps(const secpe_boot *boot, int32_t *steps, int32_t cap) {
+    if (!boot || !boot->b) return -1;
+    const BootSetup &b = *boot->b;
+    std::set<int> st;
+    if (b.fft) {
+        auto add = [&](const LtStage &s) {
+            for (int x : s.steps)
+                if (x) st.insert(x);
+        };
+        for (auto &s : b.fcfg.cts) add(s);
+        for (auto &s : b.fcfg.stc) add(s);
+        add(b.fcfg.cts_im);
+        add(b.fcfg.stc_im);
+    } else {
+        for (int j = 1; j < b.cfg.n1; j++) st.insert(j);
+        for (int g = 1; g < b.cfg.n2; g++) st.insert(g * b.cfg.n1);
+    }
+    std::vector<int> v(st.begin(), st.end());
+    v.push_back(kConjStep);
+    for (int i = 0; i < (int)v.size() && i < cap && steps; i++) steps[i] = v[i];
+    return (int32_t)v.size();
+}
 int32_t secpe_boot_levels(const secpe_boot *boot, int32_t *raise_level) {
     if (!boot || !boot->b) return -1;
     const BootSetup &b = *boot->b;

@@ -111,6 +111,7 @@ SIGS = {
                                              ctypes.c_int32, ctypes.c_double, ctypes.POINTER(vp)]),
     "secpe_bootstrap_boot": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), vp, ctypes.POINTER(CCt)]),
     "secpe_boot_levels": (ctypes.c_int32, [vp, i32p]),
+    "secpe_boot_steps": (ctypes.c_int32, [vp, i32p, ctypes.c_int32]),
     "secpe_boot_stage_export": (ctypes.c_int, [vp, vp, ctypes.c_int32, ctypes.c_int32, i32p, i32p, u64p,
                                                ctypes.c_size_t]),
     "secpe_bootstrap": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.POINTER(CBootCfg), ctypes.POINTER(CCt)]),
@@ -250,6 +251,13 @@ class Boot:
         out = np.zeros((c["n2"], c["n1"], lv + 1, self.ctx.N), dtype=np.uint64)
         _chk(lib().secpe_boot_export(self.ctx.h, self.h, which, out.ctypes.data_as(u64p), out.size))
         return out
+
+    def steps(self):
+        """Rotation steps whose keys this bootstrap needs (secpe_boot_steps; SECPE_CONJ last)."""
+        n = lib().secpe_boot_steps(self.h, None, 0)
+        out = np.zeros(max(n, 1), dtype=np.int32)
+        lib().secpe_boot_steps(self.h, out.ctypes.data_as(i32p), n)
+        return out[:n].tolist()
 
     def stage(self, kind, idx=0, level=None):
         """Factorised stage (kind 0 cts[idx], 1 cts_im, 2 stc[idx], 3 stc_im): (steps, host pts or None)."""

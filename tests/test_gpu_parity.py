@@ -748,7 +748,7 @@ def test_linear_transform_bsgs_errors(S):
 # ---------------------------------------------------------------------------------------------
 # Bootstrapping (readings R32-R36) on the "boot" parameters (N = 2^12, 2048 slots)
 # ---------------------------------------------------------------------------------------------
-BOOT = dict(n1=64, n2=32, K=16, r=8, h=64)
+BOOT = dict(n1=64, n2=32, K=16, r=7, h=64)
 
 
 @pytest.fixture(scope="module")
@@ -948,11 +948,11 @@ def test_boot_fft_setup_matches_oracle(boot_fft):
 @pytest.mark.slow
 def test_bootstrap_n16_refreshes(S):
     """N3 at the paper's ring, N = 2^16 (32768 slots): library-built factorised material (groups 5/5/5), sparse
-    secret h = 64; the refreshed ciphertext decrypts to the input slots within 2^-10 (the oracle is too slow at
+    secret h = 64; the refreshed ciphertext decrypts to the input slots within 2^-11 (the oracle is too slow at
     this size for a word-for-word run; the N = 2^12 tests pin the same code path word for word)."""
     from paper_2502_00847_b200 import secpe
     g = secpe.Context(synth.PARAM_SETS["boot16"])
-    groups, K, r = [5, 5, 5], 16, 8
+    groups, K, r = [5, 5, 5], 16, 7
     n = g.N // 2
     rot = plan.fft_boot_rotations(g.N, groups)
     kg = g.keygen(synth.KEY_SEED_BASE + 31, rot, h=64)
@@ -961,5 +961,5 @@ def test_bootstrap_n16_refreshes(S):
     ct = g.encrypt(kg, z, 0, g.scale, 27)
     out = g.bootstrap_boot(kg, ct, b)
     assert out.level == g.L - (2 * len(groups) + 6 + r)
-    assert np.abs(g.decrypt(kg, out) - z).max() < 2 ** -10
+    assert np.abs(g.decrypt(kg, out) - z).max() < 2 ** -11
 
