@@ -317,6 +317,23 @@ int32_t secpe_boot_levels(const secpe_boot *boot, int32_t *raise_level);
  * when steps / host_out are non-null also the steps and the pts (uint64[n_diag][limbs][N], n_words). */
 int secpe_boot_stage_export(secpe_ctx *ctx, const secpe_boot *boot, int32_t kind, int32_t idx, int32_t *n_diag,
                             int32_t *steps, uint64_t *host_out, size_t n_words);
+/* SURVEY 8(f) N4 (reading R38): secpe_enc_argmax (Algorithm 1) for layouts whose
+ * comparisons do not fit the level budget (K = 16: four Max steps + the final Sign), refreshing with a
+ * factorised bootstrap: before a Max when fewer than sign_depth + 2 levels remain (one is kept for the
+ * next refresh) and before the final Sign when fewer than sign_depth remain.  A refresh is a constant
+ * product by 1 onto level 0 at boot_scale (the input scale the bootstrap material was built for), the
+ * bootstrap, and a constant product by 1 back to the context's nominal scale.  One ciphertext after
+ * another (in[i] / out[i] as secpe_enc_argmax, all at one level and scale).  Errors: SECPE_ELEVEL when a
+ * refresh cannot fit, SECPE_ENOKEY, SECPE_EINVAL, SECPE_ELAYOUT. */
+int secpe_argmax_boot_info(secpe_ctx *ctx, const secpe_layout *layout, const secpe_sign_cfg *cfg,
+                           const secpe_boot *boot, int32_t in_level, int32_t *out_level);
+int secpe_enc_argmax_boot(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n_in,
+                          const secpe_layout *layout, const secpe_sign_cfg *cfg, const secpe_boot *boot,
+                          double boot_scale, secpe_ct *out);
+/* The same with caller-encoded factorised material (parity tests). */
+int secpe_enc_argmax_boot_cfg(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n_in,
+                              const secpe_layout *layout, const secpe_sign_cfg *cfg, const secpe_boot_fft_cfg *bcfg,
+                              double boot_scale, secpe_ct *out);
 /* Levels one bootstrap consumes (8 + r): out level = cfg->level - secpe_boot_depth(cfg). */
 int32_t secpe_boot_depth(const secpe_boot_cfg *cfg);
 /* in: level 0; out->data sized secpe_ct_bytes(cfg->level - secpe_boot_depth(cfg)); out->level / scale

@@ -305,8 +305,8 @@ def bootstrap(ev, keys, ct, cfg):
     ds = []
     for u in us:
         x = ev.add(u, ev.rot(keys, u, CONJ_STEP))
-        xn = ev.mul_const(x, inv, prm.scale, x.level - 1)
-        d = eval_poly15(ev, keys, xn, cfg["poly"], prm.scale)
+        xn = ev.mul_const(x, inv, S0, x.level - 1)  # EvalMod runs at the input's scale (R38)
+        d = eval_poly15(ev, keys, xn, cfg["poly"], S0)
         for _ in range(r):
             d = ev.add_const(ev.mul_ct(keys, d, d, None, d.level - 1), -2.0)  # natural scale (R9)
         ds.append(d)
@@ -489,8 +489,8 @@ def bootstrap_fft(ev, keys, ct, cfg):
     ds = []
     for u in us:
         x = ev.add(u, ev.rot(keys, u, CONJ_STEP))
-        xn = ev.mul_const(x, inv, prm.scale, x.level - 1)
-        d = eval_poly15(ev, keys, xn, cfg["poly"], prm.scale)
+        xn = ev.mul_const(x, inv, S0, x.level - 1)  # EvalMod runs at the input's scale (R38)
+        d = eval_poly15(ev, keys, xn, cfg["poly"], S0)
         for _ in range(r):
             d = ev.add_const(ev.mul_ct(keys, d, d, None, d.level - 1), -2.0)
         ds.append(d)
@@ -501,3 +501,38 @@ def bootstrap_fft(ev, keys, ct, cfg):
     for steps, pts, sc in cfg["stc"][1:]:
         o = ev.lt(keys, o, pts, steps, sc)
     return o
+
+
+# ---------------------------------------------------------------------------------------------
+# N4: Argmax over K classes when the level budget runs out (K = 16 needs 4 comparisons of
+# 12 levels each plus the final Sign), with a bootstrap (R37) before every comparison
+# that would not fit (reading R38).
+# ---------------------------------------------------------------------------------------------
+def argmax_boot(ev, keys, y, layout, stages, boot, boot_scale):
+    """Algorithm 1 as `argmax`, refreshing y (before a Max) or y_dup - y_max (before the final Sign) when
+    fewer levels remain than the step needs (a Max keeps one level for the next refresh): one constant
+    product by 1 landing at level 0 and scale boot_scale (the scale the bootstrap material expects),
+    boot(ct), then one constant product by 1 back to the nominal scale (so that y_dup - y_max sees
+    bit-identical scales)."""
+    P, K = layout["prompts"], layout["classes"]
+    n_slots = ev.prm.N // 2
+    check_layout(layout, n_slots)
+    for t in range(int(math.log2(P))):
+        y = ev.add(y, ev.rot(keys, y, K << t))
+    y = ev.mul_mask(y, mask_slots(layout, n_slots), ev.prm.scale)
+    y = ev.add(y, ev.rot(keys, y, -K))
+    ydup = y
+    sd = sign_depth(stages)
+
+    def refresh(x):
+        b = boot(ev.mul_const(x, 1.0, boot_scale, 0))
+        return ev.mul_const(b, 1.0, ev.prm.scale, b.level - 1)
+    for i in range(int(math.log2(K))):
+        if y.level < sd + 2:
+            y = refresh(y)
+        y = hom_max(ev, keys, ev.rot(keys, y, 1 << i), y, stages)
+    d = ev.sub(ydup, y)
+    if d.level < sd:
+        d = refresh(d)
+    z = sign(ev, keys, d, stages, ev.prm.scale)
+    return ev.add_const(z, 1.0)

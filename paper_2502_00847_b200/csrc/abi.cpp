@@ -570,24 +570,66 @@ static void bootstrap_fft_views(Ctx &c, const secpe_keys *keys, const secpe_ct *
     run_bootstrap_fft(c, *keys->k, vi, b, vo);
     set_out(out, vo);
 }
+static FftBootCfg fft_cfg_of(const Ctx &c, const secpe_boot_fft_cfg *cfg) {
+    REQUIRE(cfg && cfg->poly && cfg->cts && cfg->stc, SECPE_EINVAL, "null bootstrap configuration");
+    REQUIRE(cfg->n_cts >= 1 && cfg->n_stc == cfg->n_cts, SECPE_EINVAL, "stage counts");
+    REQUIRE(cfg->r >= 0 && cfg->r <= 30 && cfg->K > 0, SECPE_EINVAL, "bad EvalMod range");
+    FftBootCfg b;
+    b.level = cfg->level;
+    b.r = cfg->r;
+    b.K = cfg->K;
+    b.poly.assign(cfg->poly, cfg->poly + 16);
+    for (int i = 0; i < cfg->n_cts; i++) b.cts.push_back(lt_stage(c, cfg->cts[i]));
+    for (int i = 0; i < cfg->n_stc; i++) b.stc.push_back(lt_stage(c, cfg->stc[i]));
+    b.cts_im = lt_stage(c, cfg->cts_im);
+    b.stc_im = lt_stage(c, cfg->stc_im);
+    return b;
+}
 int secpe_bootstrap_fft(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const secpe_boot_fft_cfg *cfg,
                         secpe_ct *out) {
     return guard([&] {
-        REQUIRE(ctx && keys && in && out && out->data && cfg && cfg->poly && cfg->cts && cfg->stc, SECPE_EINVAL,
-                "null argument");
-        REQUIRE(cfg->n_cts >= 1 && cfg->n_stc == cfg->n_cts, SECPE_EINVAL, "stage counts");
-        REQUIRE(cfg->r >= 0 && cfg->r <= 30 && cfg->K > 0, SECPE_EINVAL, "bad EvalMod range");
-        Ctx &c = ctx->c;
-        FftBootCfg b;
-        b.level = cfg->level;
-        b.r = cfg->r;
-        b.K = cfg->K;
-        b.poly.assign(cfg->poly, cfg->poly + 16);
-        for (int i = 0; i < cfg->n_cts; i++) b.cts.push_back(lt_stage(c, cfg->cts[i]));
-        for (int i = 0; i < cfg->n_stc; i++) b.stc.push_back(lt_stage(c, cfg->stc[i]));
-        b.cts_im = lt_stage(c, cfg->cts_im);
-        b.stc_im = lt_stage(c, cfg->stc_im);
-        bootstrap_fft_views(c, keys, in, b, out);
+        REQUIRE(ctx && keys && in && out && out->data, SECPE_EINVAL, "null argument");
+        bootstrap_fft_views(ctx->c, keys, in, fft_cfg_of(ctx->c, cfg), out);
+    });
+}
+// N4 (R38): argmax with bootstrapping, one ciphertext after another
+static void argmax_boot_views(Ctx &c, const secpe_keys *keys, const secpe_ct *in, int n_in, const secpe_layout *layout,
+                              const secpe_sign_cfg *scfg, const FftBootCfg &b, double boot_scale, secpe_ct *out) {
+    REQUIRE(keys && in && out && n_in >= 1 && boot_scale > 0, SECPE_EINVAL, "null argument");
+    Layout lay = layout_of(c, layout);
+    SignCfg sc = sign_cfg(scfg);
+    check_fft_keys(c, keys, b);
+    for (int i = 0; i < n_in; i++) {
+        CtView vi = view_of(c, &in[i]);
+        REQUIRE(in[i].level == in[0].level && in[i].scale == in[0].scale, SECPE_EINVAL, "batch levels differ");
+        REQUIRE(out[i].data && out[i].data != in[i].data, SECPE_EINVAL, "bad output buffer");
+        const int ol = argmax_boot_level(lay, sc, b, vi.level);
+        CtView vo = compact_view(c, out[i].data, 1, ol, c.scale);
+        run_argmax_boot(c, *keys->k, vi, lay, sc, b, boot_scale, vo);
+        set_out(&out[i], vo);
+    }
+}
+int secpe_argmax_boot_info(secpe_ctx *ctx, const secpe_layout *layout, const secpe_sign_cfg *cfg,
+                           const secpe_boot *boot, int32_t in_level, int32_t *out_level) {
+    return guard([&] {
+        REQUIRE(ctx && boot && boot->b && boot->b->fft && out_level, SECPE_EINVAL, "null argument");
+        *out_level = argmax_boot_level(layout_of(ctx->c, layout), sign_cfg(cfg), boot->b->fcfg, in_level);
+    });
+}
+int secpe_enc_argmax_boot(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n_in,
+                          const secpe_layout *layout, const secpe_sign_cfg *cfg, const secpe_boot *boot,
+                          double boot_scale, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && boot && boot->b && boot->b->fft, SECPE_EINVAL, "needs factorised bootstrap material");
+        argmax_boot_views(ctx->c, keys, in, n_in, layout, cfg, boot->b->fcfg, boot_scale, out);
+    });
+}
+int secpe_enc_argmax_boot_cfg(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n_in,
+                              const secpe_layout *layout, const secpe_sign_cfg *cfg, const secpe_boot_fft_cfg *bcfg,
+                              double boot_scale, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx, SECPE_EINVAL, "null argument");
+        argmax_boot_views(ctx->c, keys, in, n_in, layout, cfg, fft_cfg_of(ctx->c, bcfg), boot_scale, out);
     });
 }
 int secpe_boot_create_fft(secpe_ctx *ctx, int32_t level, double K, int32_t r, const int32_t *groups,

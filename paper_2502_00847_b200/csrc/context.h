@@ -264,6 +264,11 @@ struct FftBootCfg {
 };
 int fft_boot_depth(const FftBootCfg &b);
 void run_bootstrap_fft(Ctx &c, const Keys &k, const CtView &in, const FftBootCfg &b, CtView &out);
+struct SignCfg;
+struct Layout;
+int argmax_boot_level(const Layout &lay, const SignCfg &cfg, const FftBootCfg &b, int in_level);
+void run_argmax_boot(Ctx &c, const Keys &k, const CtView &in, const Layout &lay, const SignCfg &cfg,
+                     const FftBootCfg &b, double boot_scale, CtView &out);
 // library-built bootstrapping material (secpe_boot_create): the EvalMod polynomial and the four encoded
 // matrices, NTT form, [n2][n1][limbs][N] each
 struct BootSetup {

@@ -233,8 +233,8 @@ struct Ev {
     Val evalmod(const Val &u, double K, int r, const std::vector<double> &poly, double S0) {
         const double inv = 1.0 / (K * ((double)c.primes[0] / S0));
         Val x = rot_add(u, kConjStep);
-        Val xn = mul_const(x, inv, c.scale, x.level() - 1);
-        Val d = poly15(xn, poly, c.scale);
+        Val xn = mul_const(x, inv, S0, x.level() - 1);  // EvalMod at the input's scale (R38)
+        Val d = poly15(xn, poly, S0);
         for (int j = 0; j < r; j++) d = add_const(mul_ct(d, d, NAN, d.level() - 1), -2.0);
         return d;
     }
@@ -340,6 +340,35 @@ struct Ev {
         // (r - y)/2 Sign(r - y) + (r + y)/2: the half-sum joins the product before its rescale
         return mul_ct(g, s, Sy, Ls - 1, {{&ry, 0.5}});
     }
+    // N4 (R38): Algorithm 1 with a bootstrap (factorised, R37) before every Max / the final Sign that would
+    // not fit: scale-up to level 0 at boot_scale, bootstrap, normalise back to the nominal scale
+    Val refresh(const Val &x, const FftBootCfg &b, double boot_scale) {
+        Val xs = mul_const(x, 1.0, boot_scale, 0);
+        Val r = bootstrap_fft(xs, b);
+        return mul_const(r, 1.0, c.scale, r.level() - 1);
+    }
+    Val argmax_boot(const Val &in, const Layout &lay, const SignCfg &cfg, const FftBootCfg &b, double boot_scale) {
+        const int P = lay.prompts, K = lay.classes;
+        Val y = in;
+        for (int t = 0; (1 << t) < P; t++) y = rot_add(y, K << t);
+        std::vector<double> mask(c.N / 2, 0.0);
+        for (int qi = 0; qi < lay.queries; qi++)
+            for (int kk = 0; kk < K; kk++) mask[(size_t)qi * lay.block + kk] = 1.0 / P;
+        y = mul_mask(y, mask, c.scale,
+                     "argmax/" + std::to_string(lay.queries) + "/" + std::to_string(P) + "/" + std::to_string(K) + "/" +
+                         std::to_string(lay.block));
+        y = rot_add(y, -K);
+        Val ydup = y;
+        const int sd = sign_depth(cfg);
+        for (int i = 0; (1 << i) < K; i++) {
+            if (y.level() < sd + 2) y = refresh(y, b, boot_scale);
+            y = hom_max(rot(y, 1 << i), y, cfg);
+        }
+        Val d = sub(ydup, y);
+        if (d.level() < sd) d = refresh(d, b, boot_scale);
+        Val z = sign(d, cfg, c.scale);
+        return add_const(z, 1.0);
+    }
     // Algorithm 1 with the H1..H6 steps of DESIGN.md section 2
     // profiler spans of the circuit stages (kinds 4..8: H1, H2, H3, H4, H6; only when profiling)
     Val argmax(const Val &in, const Layout &lay, const SignCfg &cfg) {
@@ -398,6 +427,46 @@ std::vector<int> argmax_rotations(const Layout &lay) {
 
 int boot_depth(const BootCfg &b) { return 8 + b.r; }
 int fft_boot_depth(const FftBootCfg &b) { return (int)b.cts.size() + (int)b.stc.size() + 6 + b.r; }
+
+// output level of argmax_boot for an input at in_level (the plan's level walk, no arithmetic)
+int argmax_boot_level(const Layout &lay, const SignCfg &cfg, const FftBootCfg &b, int in_level) {
+    const int sd = sign_depth(cfg), bl = b.level - fft_boot_depth(b) - 1;  // level after refresh
+    int y = in_level - 1;                                                   // mask
+    if (y < 0) throw SecpeError{-2, "not enough levels for the mask"};
+    for (int i = 0; (1 << i) < lay.classes; i++) {
+        if (y < sd + 2) {
+            if (y < 1) throw SecpeError{-2, "no level left for a refresh"};
+            y = bl;
+        }
+        if (y < sd + 1) throw SecpeError{-2, "a refresh leaves too few levels for a Max"};
+        y -= sd + 1;
+    }
+    int d = std::min(in_level - 1, y);
+    if (d < sd) {
+        if (d < 1) throw SecpeError{-2, "no level left for a refresh"};
+        d = bl;
+    }
+    if (d < sd) throw SecpeError{-2, "a refresh leaves too few levels for the final Sign"};
+    return d - sd;
+}
+
+void run_argmax_boot(Ctx &c, const Keys &k, const CtView &in, const Layout &lay, const SignCfg &cfg,
+                     const FftBootCfg &b, double boot_scale, CtView &out) {
+    Ev ev{c, k, 1};
+    for (int i = 0; i < in.n; i++) {
+        CtView vi = in, vo = out;
+        vi.data = in.data + (long)i * in.stride;
+        vi.n = 1;
+        vo.data = out.data + (long)i * out.stride;
+        vo.n = 1;
+        Val r = ev.argmax_boot(Val{nullptr, vi}, lay, cfg, b, boot_scale);
+        vo.level = r.level();
+        vo.scale = r.scale();
+        ev_copy(c, r.v, vo);
+        out.level = r.level();
+        out.scale = r.scale();
+    }
+}
 
 void run_bootstrap_fft(Ctx &c, const Keys &k, const CtView &in, const FftBootCfg &b, CtView &out) {
     Ev ev{c, k, in.n};

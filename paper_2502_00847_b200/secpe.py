@@ -112,6 +112,13 @@ SIGS = {
     "secpe_bootstrap_boot": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), vp, ctypes.POINTER(CCt)]),
     "secpe_boot_levels": (ctypes.c_int32, [vp, i32p]),
     "secpe_boot_steps": (ctypes.c_int32, [vp, i32p, ctypes.c_int32]),
+    "secpe_argmax_boot_info": (ctypes.c_int, [vp, ctypes.POINTER(Layout), ctypes.POINTER(SignCfg), vp,
+                                              ctypes.c_int32, i32p]),
+    "secpe_enc_argmax_boot": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.POINTER(Layout),
+                                             ctypes.POINTER(SignCfg), vp, ctypes.c_double, ctypes.POINTER(CCt)]),
+    "secpe_enc_argmax_boot_cfg": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.POINTER(Layout),
+                                                 ctypes.POINTER(SignCfg), ctypes.POINTER(CBootFftCfg),
+                                                 ctypes.c_double, ctypes.POINTER(CCt)]),
     "secpe_boot_stage_export": (ctypes.c_int, [vp, vp, ctypes.c_int32, ctypes.c_int32, i32p, i32p, u64p,
                                                ctypes.c_size_t]),
     "secpe_bootstrap": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.POINTER(CBootCfg), ctypes.POINTER(CCt)]),
@@ -516,9 +523,9 @@ class Context:
         out.level, out.scale = co.level, co.scale
         return out
 
-    def bootstrap_fft(self, keys, a, level, K, r, poly, cts, cts_im, stc, stc_im):
-        """secpe_bootstrap_fft (reading R37); every stage a (steps, pts, pt_scale) triple, pts a cuda
-        uint64 tensor [n_diag][limbs][N]."""
+    @staticmethod
+    def _fft_cfg(level, K, r, poly, cts, cts_im, stc, stc_im):
+        """secpe_boot_fft_cfg from (steps, pts, pt_scale) stages; returns (cfg, keep-alive list)."""
         keep = []
 
         def stage(t):
@@ -531,8 +538,41 @@ class Context:
         assert pc.shape == (16,)
         ca_ = (CLtStage * len(cts))(*[stage(t) for t in cts])
         cs_ = (CLtStage * len(stc))(*[stage(t) for t in stc])
+        keep += [pc, ca_, cs_]
         cfg = CBootFftCfg(level, K, r, pc.ctypes.data_as(f64p), len(cts), ca_, stage(cts_im), len(stc), cs_,
                           stage(stc_im))
+        return cfg, keep
+
+    def enc_argmax_boot(self, keys, cts, lay, stages, boot, boot_scale, fft_cfg=None):
+        """secpe_enc_argmax_boot (N4, reading R38) with library-built material `boot`, or
+        secpe_enc_argmax_boot_cfg when fft_cfg = (level, K, r, poly, cts, cts_im, stc, stc_im) is given."""
+        scfg, ly = sign_cfg(stages), layout(lay)
+        ol = ctypes.c_int32(0)
+        if fft_cfg is None:
+            _chk(lib().secpe_argmax_boot_info(self.h, ctypes.byref(ly), ctypes.byref(scfg), boot.h, cts.level,
+                                              ctypes.byref(ol)))
+        else:
+            ol.value = 0
+        out = self.new_ct(max(ol.value, 0) if fft_cfg is None else cts.level, cts.n)
+        ins = (CCt * cts.n)(*[cts.c(i) for i in range(cts.n)])
+        outs = (CCt * cts.n)(*[CCt(ctypes.cast(out.t[i].data_ptr(), u64p), 0, 0.0) for i in range(cts.n)])
+        if fft_cfg is None:
+            _chk(lib().secpe_enc_argmax_boot(self.h, keys.h, ins, cts.n, ctypes.byref(ly), ctypes.byref(scfg),
+                                             boot.h, boot_scale, outs))
+        else:
+            bc, keep = self._fft_cfg(*fft_cfg)
+            _chk(lib().secpe_enc_argmax_boot_cfg(self.h, keys.h, ins, cts.n, ctypes.byref(ly), ctypes.byref(scfg),
+                                                 ctypes.byref(bc), boot_scale, outs))
+        out.level, out.scale = outs[0].level, outs[0].scale
+        n, N = cts.n, self.N
+        # each output is written compactly ([2][level+1][N]) at the start of its slot
+        out.t = out.t.reshape(n, -1)[:, : 2 * (out.level + 1) * N].reshape(n, 2, out.level + 1, N).contiguous()
+        return out
+
+    def bootstrap_fft(self, keys, a, level, K, r, poly, cts, cts_im, stc, stc_im):
+        """secpe_bootstrap_fft (reading R37); every stage a (steps, pts, pt_scale) triple, pts a cuda
+        uint64 tensor [n_diag][limbs][N]."""
+        cfg, keep = self._fft_cfg(level, K, r, poly, cts, cts_im, stc, stc_im)
         out = self._out(max(level - (len(cts) + len(stc) + 6 + r), 0))
         ca, co = a.c(), out.c()
         _chk(lib().secpe_bootstrap_fft(self.h, keys.h, ctypes.byref(ca), ctypes.byref(cfg), ctypes.byref(co)))

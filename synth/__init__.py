@@ -34,6 +34,16 @@ PARAM_SETS = {
                       alpha=7, log_scale=50),
     "boot": dict(logn=12, q=[("below", 60, 1), ("nearest", 50, 20)], p=[("below", 60, 7)],
                  alpha=7, log_scale=50),
+    # N4 (reading R38): argmax with bootstrapping.  Levels 1..16 are 45-bit primes at the nominal scale 2^45
+    # (the Sign polynomials' constants, up to 2^14.8, need Delta_c ~ q <= 2^47); the 19 levels above are
+    # 50-bit primes for the bootstrap (ModRaise to the top, EvalMod at scale 2^50).  A refresh lands at
+    # level 16: one normalisation, one Max (14 levels), one level left for the next refresh's scale-up.
+    "boot_argmax_tiny": dict(logn=8, q=[("below", 60, 1), ("nearest", 45, 16), ("nearest", 50, 17)],
+                             p=[("below", 60, 7)], alpha=7, log_scale=45),
+    "boot_argmax": dict(logn=12, q=[("below", 60, 1), ("nearest", 45, 16), ("nearest", 50, 19)],
+                        p=[("below", 60, 7)], alpha=7, log_scale=45),
+    "boot_argmax16": dict(logn=16, q=[("below", 60, 1), ("nearest", 45, 16), ("nearest", 50, 19)],
+                          p=[("below", 60, 7)], alpha=7, log_scale=45),
     # the paper's ring (N = 2^16, 32768 slots) with the factorised transforms (R37, groups 5/5/5: depth 20)
     "boot16": dict(logn=16, q=[("below", 60, 1), ("nearest", 50, 22)], p=[("below", 60, 7)],
                    alpha=7, log_scale=50),
@@ -55,6 +65,8 @@ LAYOUTS = {
     "argmax_k2": dict(queries=2048, prompts=8, classes=2, block=16),
     "argmax_k16": dict(queries=256, prompts=8, classes=16, block=128),
     "argmax_small_k2": dict(queries=128, prompts=8, classes=2, block=16),
+    "tiny_k16": dict(queries=1, prompts=8, classes=16, block=128),
+    "boot_k16": dict(queries=16, prompts=8, classes=16, block=128),
 }
 
 KEY_SEED_BASE = 0x5EC9E000

@@ -963,3 +963,66 @@ def test_bootstrap_n16_refreshes(S):
     assert out.level == g.L - (2 * len(groups) + 6 + r)
     assert np.abs(g.decrypt(kg, out) - z).max() < 2 ** -11
 
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_argmax_boot_k16_bit_exact(S):
+    """N4 (reading R38): secpe_enc_argmax_boot_cfg with K = 16 (16 queries per ciphertext at N = 2^12, four
+    bootstraps) is word for word the oracle's argmax_boot with the same op list, and every label is exact
+    above the Sign margin."""
+    P = pair(S, "boot_argmax")
+    prm, g = P.prm, P.gpu
+    ev = ckks.Oracle(prm)
+    lay = synth.LAYOUTS["boot_k16"]
+    st = load_sign("sign_7_15_15.json")
+    groups = [4, 4, 3]
+    rot = plan.argmax_rotations(lay) + plan.fft_boot_rotations(prm.N, groups)
+    seed = synth.KEY_SEED_BASE + 37
+    ko, kg = ev.keygen(seed, rot, h=64), g.keygen(seed, rot, h=64)
+    bs = 2.0 ** 50
+    cfg = plan.fft_boot_config(ev, bs, prm.L, 16, 7, groups)
+    scores = synth.softmax_scores(41, lay["queries"], lay["prompts"], lay["classes"])
+    ct = ev.encrypt(ko, plan.pack(scores, lay, prm.N // 2), prm.scale, 43, level=16)
+    ev.log.clear()
+    want = plan.argmax_boot(ev, ko, ct, lay, st, lambda c: plan.bootstrap_fft(ev, ko, c, cfg), bs)
+    olog = list(ev.log)
+    dev = lambda t: (t[0], torch.from_numpy(np.stack(t[1])).cuda(), t[2])
+    fc = (cfg["level"], cfg["K"], cfg["r"], cfg["poly"], [dev(t) for t in cfg["cts"]], dev(cfg["cts_im"]),
+          [dev(t) for t in cfg["stc"]], dev(cfg["stc_im"]))
+    g.oplog(enable=True, clear=True)
+    got = g.enc_argmax_boot(kg, P.up(ct), lay, st, None, bs, fft_cfg=fc)
+    glog = g.oplog(enable=False, clear=True)
+    assert glog == olog
+    assert got.level == want.level and got.scale == want.scale
+    assert np.array_equal(P.down(got), want.data)
+    dec = g.decrypt(kg, got)
+    mean = scores.mean(axis=1)
+    srt = np.sort(mean, axis=1)
+    ok = srt[:, -1] - srt[:, -2] >= 2.0 ** -7
+    assert ok.sum() >= 8
+    assert (S.labels(dec, lay)[ok] == plan.true_labels(scores)[ok]).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_argmax_boot_k16_n16(S):
+    """N4 at the paper's ring: K = 16, 256 queries per ciphertext at N = 2^16 with library-built factorised
+    bootstrap material (secpe_enc_argmax_boot); every label above the Sign margin is exact (property check:
+    the oracle cannot run this size word for word; the N = 2^12 test pins the same plan)."""
+    from paper_2502_00847_b200 import secpe
+    g = secpe.Context(synth.PARAM_SETS["boot_argmax16"])
+    lay = synth.LAYOUTS["argmax_k16"]
+    st = load_sign("sign_7_15_15.json")
+    bs = 2.0 ** 50
+    b = g.boot_create_fft(g.L, 16, 7, [5, 5, 5], bs)
+    kg = g.keygen(synth.KEY_SEED_BASE + 39, sorted(set(plan.argmax_rotations(lay))) + b.steps(), h=64)
+    scores = synth.softmax_scores(47, lay["queries"], lay["prompts"], lay["classes"])
+    ct = g.encrypt(kg, plan.pack(scores, lay, g.N // 2), 16, g.scale, 49)
+    out = g.enc_argmax_boot(kg, ct, lay, st, b, bs)
+    dec = g.decrypt(kg, out)
+    mean = scores.mean(axis=1)
+    srt = np.sort(mean, axis=1)
+    ok = srt[:, -1] - srt[:, -2] >= 2.0 ** -7
+    assert ok.sum() >= 200
+    assert (S.labels(dec, lay)[ok] == plan.true_labels(scores)[ok]).all()

@@ -833,3 +833,31 @@ def test_bootstrap_fft_refreshes():
     out = plan.bootstrap_fft(ev, keys, ct, cfg)
     assert out.level == prm.L - plan.fft_boot_depth(groups, r)
     assert np.abs(ev.decrypt(keys, out).real - z).max() < 2 ** -14
+
+
+def test_argmax_boot_k16_one_hot():
+    """N4 (reading R38): Algorithm 1 with K = 16 classes (four Max steps + the final Sign, more levels than the
+    chain holds) refreshes with four bootstraps and still returns the one-hot of the true label."""
+    prm = ckks.Params(synth.PARAM_SETS["boot_argmax_tiny"])
+    ev = ckks.Oracle(prm)
+    lay = synth.LAYOUTS["tiny_k16"]
+    d = json.load(open(os.path.join(os.path.dirname(__file__), "..", "data", "sign_7_15_15.json")))
+    st = [list(map(float, c)) for c in d["coeffs"]]
+    groups = [4, 3]
+    rot = plan.argmax_rotations(lay) + plan.fft_boot_rotations(prm.N, groups)
+    keys = ev.keygen(11, rot, h=64)
+    cfg = plan.fft_boot_config(ev, 2.0 ** 50, prm.L, 16, 7, groups)
+    nb = [0]
+
+    def boot(c):
+        nb[0] += 1
+        assert c.level == 0 and c.scale == 2.0 ** 50
+        return plan.bootstrap_fft(ev, keys, c, cfg)
+    scores = synth.softmax_scores(5, lay["queries"], lay["prompts"], lay["classes"])
+    ct = ev.encrypt(keys, plan.pack(scores, lay, prm.N // 2), prm.scale, 3, level=16)
+    out = plan.argmax_boot(ev, keys, ct, lay, st, boot, 2.0 ** 50)
+    assert nb[0] == 4 and out.scale == prm.scale
+    dec = ev.decrypt(keys, out).real
+    want = np.zeros(lay["classes"])
+    want[plan.true_labels(scores)[0]] = 1.0
+    assert np.abs(dec[: lay["classes"]] - want).max() < 2 ** -5
