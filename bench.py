@@ -211,6 +211,7 @@ def micro_configs(stream, reps=5):
                                   "not_hoisted": {"ms_per_15_keys": ms, "rotations_per_s": 15 * R / (ms / 1000)}}
     del ctx, keys, a, b, r, o
     out["N3_bootstrap"] = bootstrap_bench(stream, t_ms)
+    out["N4_argmax_k16"] = argmax_k16_bench(stream, t_ms)
     return out
 
 
@@ -269,6 +270,43 @@ def bootstrap_bench(stream, t_ms):
                          "max_abs_err": err, "setup_s": setup_s,
                          "transforms": "special-FFT groups 5/5/5, hoisted diagonal transforms (R37)"}
     return out
+
+
+def argmax_k16_bench(stream, t_ms):
+    """SURVEY 8(f) N4 (reading R38): Algorithm 1 with K = 16 classes at N = 2^16 (256 queries x 8 prompts per
+    ciphertext), refreshed by four factorised bootstraps per ciphertext (secpe_enc_argmax_boot); one
+    ciphertext per call, CUDA events, median.  Labels checked against the plaintext argmax above the margin."""
+    import torch
+    import synth
+    from paper_2502_00847_b200 import secpe
+    ctx = secpe.Context(synth.PARAM_SETS["boot_argmax16"], stream=stream.cuda_stream)
+    lay = synth.LAYOUTS["argmax_k16"]
+    st = load_sign("sign_7_15_15.json")
+    bs = 2.0 ** 50
+    boot = ctx.boot_create_fft(ctx.L, 16, 7, [5, 5, 5], bs)
+    P, K = lay["prompts"], lay["classes"]
+    rot = [K << t for t in range(P.bit_length() - 1)] + [-K] + [1 << i for i in range(K.bit_length() - 1)]
+    keys = ctx.keygen(synth.KEY_SEED_BASE + 39, sorted(set(rot)) + boot.steps(), h=64)
+    scores = synth.softmax_scores(47, lay["queries"], P, K)
+    z = np.zeros(ctx.N // 2)
+    for qi in range(lay["queries"]):
+        for p in range(P):
+            z[qi * lay["block"] + p * K: qi * lay["block"] + (p + 1) * K] = scores[qi, p]
+    ct = ctx.encrypt(keys, z, 16, ctx.scale, 49)
+    res = [None]
+
+    def one():
+        res[0] = ctx.enc_argmax_boot(keys, ct, lay, st, boot, bs)
+    ms = t_ms(one)
+    dec = ctx.decrypt(keys, res[0])
+    lab = secpe.labels(dec, lay)
+    mean = scores.mean(axis=1)
+    srt = np.sort(mean, axis=1)
+    ok = srt[:, -1] - srt[:, -2] >= 2.0 ** -7
+    return {"ms_per_ciphertext": ms, "queries_per_ciphertext": lay["queries"], "classes": K, "prompts": P,
+            "query_argmax_per_s": lay["queries"] / (ms / 1000), "bootstraps_per_ciphertext": 4,
+            "labels_exact_above_margin": float((lab[ok] == np.argmax(mean, axis=1)[ok]).mean()),
+            "in_margin_fraction": float(1 - ok.mean()), "logn": ctx.logn, "chain": "q0 60 + 16 x 45 + 19 x 50 bit"}
 
 def run_secpe(a):
     import torch

@@ -28,6 +28,7 @@ def main():
             ts.append(a.elapsed_time(b))
         return statistics.median(ts)
     print(json.dumps(bench.bootstrap_bench(stream, t_ms)))
+    print(json.dumps(bench.argmax_k16_bench(stream, t_ms)))
 
 
 if __name__ == "__main__":
