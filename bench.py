@@ -250,7 +250,7 @@ def bootstrap_bench(stream, t_ms):
     ctx = secpe.Context(synth.PARAM_SETS["boot16"], stream=stream.cuda_stream)
     groups = [5, 5, 5]
     t0 = time.time()
-    boot = ctx.boot_create_fft(ctx.L, K, r, groups, ctx.scale)
+    boot = ctx.boot_create_fft(ctx.L, K, r, groups, ctx.scale, bsgs=True)
     torch.cuda.synchronize()
     setup_s = time.time() - t0
     steps = boot.steps()
@@ -268,7 +268,7 @@ def bootstrap_bench(stream, t_ms):
     out["N=2^16_fft"] = {"ms_per_bootstrap": ms, "logn": ctx.logn, "slots": ctx.N // 2, "level_in": 0,
                          "raised_to": ctx.L, "level_out": res[0].level, "galois_keys": len(steps),
                          "max_abs_err": err, "setup_s": setup_s,
-                         "transforms": "special-FFT groups 5/5/5, hoisted diagonal transforms (R37)"}
+                         "transforms": "special-FFT groups 5/5/5, baby-step giant-step form (R37, R39)"}
     return out
 
 
@@ -283,7 +283,7 @@ def argmax_k16_bench(stream, t_ms):
     lay = synth.LAYOUTS["argmax_k16"]
     st = load_sign("sign_7_15_15.json")
     bs = 2.0 ** 50
-    boot = ctx.boot_create_fft(ctx.L, 16, 7, [5, 5, 5], bs)
+    boot = ctx.boot_create_fft(ctx.L, 16, 7, [5, 5, 5], bs, bsgs=True)
     P, K = lay["prompts"], lay["classes"]
     rot = [K << t for t in range(P.bit_length() - 1)] + [-K] + [1 << i for i in range(K.bit_length() - 1)]
     keys = ctx.keygen(synth.KEY_SEED_BASE + 39, sorted(set(rot)) + boot.steps(), h=64)

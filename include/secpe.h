@@ -286,6 +286,13 @@ typedef struct {
     const int32_t *steps;   /* host[n_diag] */
     const uint64_t *pts;    /* dev */
     double pt_scale;
+    /* baby-step giant-step form (reading R39) when n_giant > 0: steps / n_diag unused, pts dev
+     * uint64[n_giant][n_baby][stage level + 1][N] with pts[g][j] = encode(RotR(d_{baby_j + giant_g}, giant_g))
+     * (zero where no diagonal); out = Rescale(sum_g RotL(sum_j pts[g][j] (.) RotL(x, baby_j), giant_g)) */
+    int32_t n_baby;
+    const int32_t *baby;    /* host[n_baby] */
+    int32_t n_giant;
+    const int32_t *giant;   /* host[n_giant] */
 } secpe_lt_stage;
 typedef struct {
     int32_t level;
@@ -302,9 +309,10 @@ typedef struct {
 int secpe_bootstrap_fft(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const secpe_boot_fft_cfg *cfg,
                         secpe_ct *out);
 /* Library-built factorised material: groups host[n_groups] (stage counts, S_1 first, summing to
- * log2(N/2)); same polynomial and scales as secpe_boot_create. */
+ * log2(N/2)); same polynomial and scales as secpe_boot_create; bsgs != 0: every group in baby-step
+ * giant-step form (R39: n1 = the power of two >= sqrt(#diagonals) baby steps, about as many giant steps). */
 int secpe_boot_create_fft(secpe_ctx *ctx, int32_t level, double K, int32_t r, const int32_t *groups,
-                          int32_t n_groups, double in_scale, secpe_boot **out);
+                          int32_t n_groups, double in_scale, int32_t bsgs, secpe_boot **out);
 /* Bootstrap with library-built material of either kind; out->data sized for level - secpe_boot_levels. */
 int secpe_bootstrap_boot(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const secpe_boot *boot,
                          secpe_ct *out);
@@ -317,6 +325,10 @@ int32_t secpe_boot_levels(const secpe_boot *boot, int32_t *raise_level);
  * when steps / host_out are non-null also the steps and the pts (uint64[n_diag][limbs][N], n_words). */
 int secpe_boot_stage_export(secpe_ctx *ctx, const secpe_boot *boot, int32_t kind, int32_t idx, int32_t *n_diag,
                             int32_t *steps, uint64_t *host_out, size_t n_words);
+/* The same for a baby-step giant-step stage: *n_baby, *n_giant, and (when non-null) the steps and the pts
+ * (uint64[n_giant][n_baby][limbs][N], n_words). */
+int secpe_boot_stage_export_bsgs(secpe_ctx *ctx, const secpe_boot *boot, int32_t kind, int32_t idx, int32_t *n_baby,
+                                 int32_t *n_giant, int32_t *baby, int32_t *giant, uint64_t *host_out, size_t n_words);
 /* SURVEY 8(f) N4 (reading R38): secpe_enc_argmax (Algorithm 1) for layouts whose
  * comparisons do not fit the level budget (K = 16: four Max steps + the final Sign), refreshing with a
  * factorised bootstrap: before a Max when fewer than sign_depth + 2 levels remain (one is kept for the

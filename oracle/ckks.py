@@ -635,7 +635,43 @@ class Oracle:
         self._log("MODRAISE", 0, level, ct.scale)
         return r
 
+    def linear_transform_bsgs_gen(self, keys, ct, pts, baby, giant, pt_scale):
+        """General baby-step giant-step transform (reading R39):
+            out = Rescale( sum_g RotL( sum_j pts[g][j] (.) RotL(ct, baby[j]), giant[g] ) ),
+        the baby rotations hoisted (R29), the giant ones plain (a zero giant step is no rotation), every
+        product and sum exact mod q, the terms accumulated in g order.  With
+        pts[g][j] = encode(RotR(d_{baby[j] + giant[g]}, giant[g])) this is sum_o d_o (.) RotL(ct, o)."""
+        prm = self.prm
+        if len(pts) != len(giant) or any(len(r) != len(baby) for r in pts):
+            raise ValueError("pts must be len(giant) lists of len(baby) plaintexts")
+        nl = ct.level + 1
+        bab = self.rotate_hoisted_raw(keys, ct, list(baby))
+        acc = None
+        for g, G in enumerate(giant):
+            inner = np.zeros((2, nl, prm.N), dtype=np.uint64)
+            for j in range(len(baby)):
+                prod = self.mul_plain_raw(bab[j], pts[g][j])
+                nxt = np.zeros_like(inner)
+                lib().o_add(prm.cptr, P(inner), P(prod), nl, 2, P(nxt))
+                inner = nxt
+            term = Ct(inner, ct.scale * pt_scale)
+            if G:
+                term = self.rotate_raw(keys, term, G)
+            if acc is None:
+                acc = term.data
+            else:
+                nxt = np.zeros_like(acc)
+                lib().o_add(prm.cptr, P(acc), P(term.data), nl, 2, P(nxt))
+                acc = nxt
+        return self.rescale(Ct(acc, ct.scale * pt_scale))
+
     # ---- planned ops (logged; reading R9 scale planning) ------------------------------------
+    def lt_gen(self, keys, x, pts, baby, giant, pt_scale):
+        out = self.linear_transform_bsgs_gen(keys, x, pts, baby, giant, pt_scale)
+        self._log("LTG", x.level, out.level, out.scale,
+                  ",".join(str(s) for s in baby) + ";" + ",".join(str(s) for s in giant))
+        return out
+
     def lt(self, keys, x, pts, steps, pt_scale):
         out = self.linear_transform(keys, x, pts, steps, pt_scale)
         self._log("LT", x.level, out.level, out.scale, ",".join(str(s) for s in steps))

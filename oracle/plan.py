@@ -423,7 +423,54 @@ def lt_pts(ev, D, level, pt_scale):
     return steps, pts
 
 
-def fft_boot_config(ev, in_scale, level, K, r, groups):
+def bsgs_split(D, n):
+    """Baby-step giant-step split of a diagonal set whose signed offsets are the multiples u k,
+    k_min <= k <= k_max, of one step u (every merged special-FFT group is, R39): n1 = the power of two
+    >= sqrt(count), baby u j (j < n1), giant u (k_min + n1 g) (g < ceil(count / n1)).  Returns
+    (baby, giant, {(g, j): offset key or None}) -- None where k > k_max (a zero diagonal)."""
+    offs = sorted(_signed(k, n) for k in D)
+    nz = [abs(o) for o in offs if o]
+    u = 0
+    for o in nz:
+        u = math.gcd(u, o)
+    u = u or 1
+    ks = [o // u for o in offs]
+    kmin, kmax = ks[0], ks[-1]
+    if ks != list(range(kmin, kmax + 1)):
+        raise ValueError("offsets are not a contiguous progression")
+    cnt = kmax - kmin + 1
+    n1 = 1
+    while n1 * n1 < cnt:
+        n1 *= 2
+    n2 = -(-cnt // n1)
+    baby = [u * j for j in range(n1)]
+    giant = [u * (kmin + n1 * g) for g in range(n2)]
+    where = {}
+    for g in range(n2):
+        for j in range(n1):
+            k = kmin + n1 * g + j
+            where[(g, j)] = (u * k) % n if k <= kmax else None
+    return baby, giant, where
+
+
+def lt_bsgs_pts(ev, D, level, pt_scale):
+    """(baby, giant, pts) of a diagonal-form transform for linear_transform_bsgs_gen (R39):
+    pts[g][j] = NTT(encode(RotR(d_{baby_j + giant_g}, giant_g), pt_scale)), zero where no diagonal."""
+    from oracle.ckks import encode
+    n = ev.prm.N // 2
+    baby, giant, where = bsgs_split(D, n)
+    pts = []
+    for g, G in enumerate(giant):
+        row = []
+        for j in range(len(baby)):
+            k = where[(g, j)]
+            d = D[k] if k is not None else np.zeros(n, complex)
+            row.append(ev.plain_ntt(encode(ev.prm, np.roll(d, G), pt_scale), level))
+        pts.append(row)
+    return baby, giant, pts
+
+
+def fft_boot_config(ev, in_scale, level, K, r, groups, bsgs=False):
     """Factorised bootstrapping material (R37): CoeffToSlot stages (the last one in a Re (x 1/2) and an Im
     (x -i/2) variant), SlotToCoeff stages (the first one in a Re (x c) and an Im (x i c) variant, c = R/(4 pi)),
     each encoded at q of its level."""
@@ -434,24 +481,25 @@ def fft_boot_config(ev, in_scale, level, K, r, groups):
     stc, cts = fft_groups(prm.N, groups)
     mc, ms = len(cts), len(stc)
     cfg = dict(level=level, K=float(K), r=r, poly=boot_poly(K, r), groups=list(groups), cts=[], stc=[])
+    enc = lt_bsgs_pts if bsgs else lt_pts
     lv = level
     for i, D in enumerate(cts):
         sc = float(prm.primes[lv])
         if i < mc - 1:
-            cfg["cts"].append((*lt_pts(ev, D, lv, sc), sc))
+            cfg["cts"].append((*enc(ev, D, lv, sc), sc))
         else:
-            cfg["cts"].append((*lt_pts(ev, {k: 0.5 * v for k, v in D.items()}, lv, sc), sc))
-            cfg["cts_im"] = (*lt_pts(ev, {k: -0.5j * v for k, v in D.items()}, lv, sc), sc)
+            cfg["cts"].append((*enc(ev, {k: 0.5 * v for k, v in D.items()}, lv, sc), sc))
+            cfg["cts_im"] = (*enc(ev, {k: -0.5j * v for k, v in D.items()}, lv, sc), sc)
         lv -= 1
     lv = level - mc - 6 - r
     cfg["stc_level"] = lv
     for i, D in enumerate(stc):
         sc = float(prm.primes[lv])
         if i == 0:
-            cfg["stc"].append((*lt_pts(ev, {k: c * v for k, v in D.items()}, lv, sc), sc))
-            cfg["stc_im"] = (*lt_pts(ev, {k: 1j * c * v for k, v in D.items()}, lv, sc), sc)
+            cfg["stc"].append((*enc(ev, {k: c * v for k, v in D.items()}, lv, sc), sc))
+            cfg["stc_im"] = (*enc(ev, {k: 1j * c * v for k, v in D.items()}, lv, sc), sc)
         else:
-            cfg["stc"].append((*lt_pts(ev, D, lv, sc), sc))
+            cfg["stc"].append((*enc(ev, D, lv, sc), sc))
         lv -= 1
     return cfg
 
@@ -460,14 +508,26 @@ def fft_boot_depth(groups, r):
     return 2 * len(groups) + 6 + r
 
 
-def fft_boot_rotations(N, groups):
-    """Galois keys the factorised bootstrap needs: every nonzero offset of every group, and conjugation."""
+def fft_boot_rotations(N, groups, bsgs=False):
+    """Galois keys the factorised bootstrap needs: every nonzero offset of every group (diagonal form) or
+    every nonzero baby and giant step (R39), and conjugation."""
     n = N // 2
     stc, cts = fft_groups(N, groups)
     s = set()
     for D in stc + cts:
-        s |= {_signed(k, n) for k in D if k % n}
+        if bsgs:
+            baby, giant, _ = bsgs_split(D, n)
+            s |= {x for x in baby + giant if x % n}
+        else:
+            s |= {_signed(k, n) for k in D if k % n}
     return sorted(s) + [CONJ_STEP]
+
+
+def _lt_stage(ev, keys, x, t):
+    """A stage of bootstrap_fft: (steps, pts, scale) diagonal form (R30) or (baby, giant, pts, scale) (R39)."""
+    if len(t) == 3:
+        return ev.lt(keys, x, t[1], t[0], t[2])
+    return ev.lt_gen(keys, x, t[2], t[0], t[1], t[3])
 
 
 def bootstrap_fft(ev, keys, ct, cfg):
@@ -479,12 +539,9 @@ def bootstrap_fft(ev, keys, ct, cfg):
     L, K, r = cfg["level"], cfg["K"], cfg["r"]
     S0 = ct.scale
     v = ev.mod_raise(ct, L)
-    for steps, pts, sc in cfg["cts"][:-1]:
-        v = ev.lt(keys, v, pts, steps, sc)
-    steps, pts, sc = cfg["cts"][-1]
-    us = [ev.lt(keys, v, pts, steps, sc)]
-    steps, pts, sc = cfg["cts_im"]
-    us.append(ev.lt(keys, v, pts, steps, sc))
+    for t in cfg["cts"][:-1]:
+        v = _lt_stage(ev, keys, v, t)
+    us = [_lt_stage(ev, keys, v, cfg["cts"][-1]), _lt_stage(ev, keys, v, cfg["cts_im"])]
     inv = 1.0 / (K * (float(prm.primes[0]) / S0))
     ds = []
     for u in us:
@@ -494,12 +551,10 @@ def bootstrap_fft(ev, keys, ct, cfg):
         for _ in range(r):
             d = ev.add_const(ev.mul_ct(keys, d, d, None, d.level - 1), -2.0)
         ds.append(d)
-    steps, pts, sc = cfg["stc"][0]
-    o = ev.lt(keys, ds[0], pts, steps, sc)
-    steps, pts, sc = cfg["stc_im"]
-    o = ev.add(o, ev.lt(keys, ds[1], pts, steps, sc))
-    for steps, pts, sc in cfg["stc"][1:]:
-        o = ev.lt(keys, o, pts, steps, sc)
+    o = _lt_stage(ev, keys, ds[0], cfg["stc"][0])
+    o = ev.add(o, _lt_stage(ev, keys, ds[1], cfg["stc_im"]))
+    for t in cfg["stc"][1:]:
+        o = _lt_stage(ev, keys, o, t)
     return o
 
 

@@ -539,9 +539,15 @@ int secpe_boot_export(secpe_ctx *ctx, const secpe_boot *boot, int32_t which, uin
     });
 }
 static LtStage lt_stage(const Ctx &c, const secpe_lt_stage &s) {
-    REQUIRE(s.n_diag >= 1 && s.steps && s.pts, SECPE_EINVAL, "bad transform stage");
     LtStage t;
-    t.steps.assign(s.steps, s.steps + s.n_diag);
+    if (s.n_giant > 0) {
+        REQUIRE(s.n_baby >= 1 && s.baby && s.giant && s.pts, SECPE_EINVAL, "bad baby-step giant-step stage");
+        t.baby.assign(s.baby, s.baby + s.n_baby);
+        t.giant.assign(s.giant, s.giant + s.n_giant);
+    } else {
+        REQUIRE(s.n_diag >= 1 && s.steps && s.pts, SECPE_EINVAL, "bad transform stage");
+        t.steps.assign(s.steps, s.steps + s.n_diag);
+    }
     t.pts = s.pts;
     t.scale = s.pt_scale;
     (void)c;
@@ -549,9 +555,10 @@ static LtStage lt_stage(const Ctx &c, const secpe_lt_stage &s) {
 }
 static void check_fft_keys(const Ctx &c, const secpe_keys *keys, const FftBootCfg &b) {
     auto chk = [&](const LtStage &s) {
-        for (int st : s.steps)
-            REQUIRE(keys->k->gk.count(galois_elt(c, st)) || galois_elt(c, st) == 1, SECPE_ENOKEY,
-                    "no Galois key for a transform step");
+        for (const auto *v : {&s.steps, &s.baby, &s.giant})
+            for (int st : *v)
+                REQUIRE(keys->k->gk.count(galois_elt(c, st)) || galois_elt(c, st) == 1, SECPE_ENOKEY,
+                        "no Galois key for a transform step");
     };
     for (auto &s : b.cts) chk(s);
     for (auto &s : b.stc) chk(s);
@@ -633,11 +640,12 @@ int secpe_enc_argmax_boot_cfg(secpe_ctx *ctx, const secpe_keys *keys, const secp
     });
 }
 int secpe_boot_create_fft(secpe_ctx *ctx, int32_t level, double K, int32_t r, const int32_t *groups,
-                          int32_t n_groups, double in_scale, secpe_boot **out) {
+                          int32_t n_groups, double in_scale, int32_t bsgs, secpe_boot **out) {
     return guard([&] {
         REQUIRE(ctx && out && groups && n_groups >= 1 && in_scale > 0, SECPE_EINVAL, "null argument");
         auto h = std::make_unique<secpe_boot>();
-        h->b.reset(boot_setup_fft(ctx->c, level, K, r, std::vector<int>(groups, groups + n_groups), in_scale));
+        h->b.reset(boot_setup_fft(ctx->c, level, K, r, std::vector<int>(groups, groups + n_groups), in_scale,
+                                  bsgs != 0));
         *out = h.release();
     });
 }
@@ -647,8 +655,9 @@ int32_t secpe_boot_steps(const secpe_boot *boot, int32_t *steps, int32_t cap) {
     std::set<int> st;
     if (b.fft) {
         auto add = [&](const LtStage &s) {
-            for (int x : s.steps)
-                if (x) st.insert(x);
+            for (const auto *v : {&s.steps, &s.baby, &s.giant})
+                for (int x : *v)
+                    if (galois_elt(*b.ctx, x) != 1) st.insert(x);
         };
         for (auto &s : b.fcfg.cts) add(s);
         for (auto &s : b.fcfg.stc) add(s);
@@ -679,6 +688,33 @@ int secpe_bootstrap_boot(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct 
     return guard([&] {
         REQUIRE(ctx && keys && in && out && out->data && boot && boot->b, SECPE_EINVAL, "null argument");
         bootstrap_fft_views(ctx->c, keys, in, boot->b->fcfg, out);
+    });
+}
+static const LtStage &boot_stage(const FftBootCfg &f, int kind, int idx, int &lv) {
+    const int mc = (int)f.cts.size(), base = f.level - mc - 6 - f.r;
+    REQUIRE(kind >= 0 && kind < 4, SECPE_EINVAL, "stage kind");
+    if (kind == 0 || kind == 2)
+        REQUIRE(idx >= 0 && idx < (kind == 0 ? (int)f.cts.size() : (int)f.stc.size()), SECPE_EINVAL, "stage index");
+    lv = kind == 0 ? f.level - idx : kind == 1 ? f.level - (mc - 1) : kind == 2 ? base - idx : base;
+    return kind == 0 ? f.cts[idx] : kind == 1 ? f.cts_im : kind == 2 ? f.stc[idx] : f.stc_im;
+}
+int secpe_boot_stage_export_bsgs(secpe_ctx *ctx, const secpe_boot *boot, int32_t kind, int32_t idx, int32_t *n_baby,
+                                 int32_t *n_giant, int32_t *baby, int32_t *giant, uint64_t *host_out, size_t n_words) {
+    return guard([&] {
+        REQUIRE(ctx && boot && boot->b && boot->b->fft && n_baby && n_giant, SECPE_EINVAL, "bad argument");
+        int lv = 0;
+        const LtStage &s = boot_stage(boot->b->fcfg, kind, idx, lv);
+        REQUIRE(!s.giant.empty(), SECPE_EINVAL, "not a baby-step giant-step stage");
+        *n_baby = (int)s.baby.size();
+        *n_giant = (int)s.giant.size();
+        if (baby) std::copy(s.baby.begin(), s.baby.end(), baby);
+        if (giant) std::copy(s.giant.begin(), s.giant.end(), giant);
+        REQUIRE(!host_out || n_words == (size_t)*n_baby * *n_giant * (lv + 1) * ctx->c.N, SECPE_EINVAL,
+                "n_words does not match the stage size");
+        if (host_out) {
+            CUDA_CHECK(cudaMemcpyAsync(host_out, s.pts, n_words * 8, cudaMemcpyDeviceToHost, ctx->c.st));
+            CUDA_CHECK(cudaStreamSynchronize(ctx->c.st));
+        }
     });
 }
 int secpe_boot_stage_export(secpe_ctx *ctx, const secpe_boot *boot, int32_t kind, int32_t idx, int32_t *n_diag,

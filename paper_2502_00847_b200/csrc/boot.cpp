@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <functional>
 #include <map>
+#include <numeric>
 
 #include "context.h"
 
@@ -52,6 +53,7 @@ BootSetup *boot_setup(Ctx &c, int level, double K, int r, int n1, int n2, double
     const int l_stc = level - 7 - r;
     if (level >= c.nq || l_stc < 1) throw SecpeError{-2, "boot: not enough levels"};
     auto b = std::make_unique<BootSetup>();
+    b->ctx = &c;
     const double a = 2.0 * M_PI * K / std::ldexp(1.0, r), ph = -M_PI / std::ldexp(1.0, r + 1);
     b->cfg.poly.resize(16);
     double fact = 1.0;
@@ -183,7 +185,55 @@ static LtStage encode_stage(Ctx &c, const Diag &D, cd mul, int level, double sca
     return st;
 }
 
-BootSetup *boot_setup_fft(Ctx &c, int level, double K, int r, const std::vector<int> &groups, double in_scale) {
+// baby-step giant-step form (R39): the signed offsets of a merged group are u k, k_min <= k <= k_max;
+// n1 = the power of two >= sqrt(count), baby u j, giant u (k_min + n1 g), pts[g][j] = encode(RotR(d_k, giant_g))
+// with k = k_min + n1 g + j (a zero polynomial past k_max)
+static LtStage encode_stage_bsgs(Ctx &c, const Diag &D, cd mul, int level, double scale, std::vector<DevBuf> &bufs) {
+    const long N = c.N, n = N / 2;
+    const int nl = level + 1;
+    std::vector<long> offs;
+    for (const auto &x : D) offs.push_back(x.first > n / 2 ? x.first - n : x.first);
+    std::sort(offs.begin(), offs.end());
+    long u = 0;
+    for (long o : offs) u = std::gcd(u, std::labs(o));
+    if (u == 0) u = 1;
+    const long kmin = offs.front() / u, kmax = offs.back() / u, cnt = kmax - kmin + 1;
+    if (cnt != (long)offs.size()) throw SecpeError{-1, "boot: offsets are not a contiguous progression"};
+    long n1 = 1;
+    while (n1 * n1 < cnt) n1 *= 2;
+    const long n2 = (cnt + n1 - 1) / n1;
+    LtStage st;
+    for (long j = 0; j < n1; j++) st.baby.push_back((int)(u * j));
+    for (long g = 0; g < n2; g++) st.giant.push_back((int)(u * (kmin + n1 * g)));
+    std::vector<i64> coef((size_t)n1 * n2 * N);
+    std::vector<double> re(n), im(n);
+    for (long g = 0; g < n2; g++)
+        for (long j = 0; j < n1; j++) {
+            const long kk = kmin + n1 * g + j, G = st.giant[g];
+            const auto it = kk <= kmax ? D.find(((u * kk) % n + n) % n) : D.end();
+            for (long t = 0; t < n; t++) {
+                const cd v = it == D.end() ? cd(0, 0) : it->second[((t - G) % n + n) % n] * mul;
+                re[t] = v.real();
+                im[t] = v.imag();
+            }
+            encode_complex_int(c, re.data(), im.data(), n, scale, coef.data() + (g * n1 + j) * N);
+        }
+    const long npt = n1 * n2;
+    DevBuf out((size_t)npt * nl * N, c.st), dc((size_t)npt * N, c.st);
+    CUDA_CHECK(cudaMemcpyAsync(dc.p, coef.data(), (size_t)npt * N * 8, cudaMemcpyHostToDevice, c.st));
+    for (long i = 0; i < npt; i++)
+        k_int_to_rows(c.tab, c.logn, (const i64 *)dc.p + i * N, out.p + (size_t)i * nl * N, LimbMap{nl, nl, 0, 0},
+                      c.st);
+    ev_ntt(c, RowsArg{out.p, 2L * nl * N, (long)nl * N}, (int)npt, LimbMap{nl, nl, 0, 0}, false);
+    CUDA_CHECK(cudaStreamSynchronize(c.st));
+    st.pts = out.p;
+    st.scale = scale;
+    bufs.push_back(std::move(out));
+    return st;
+}
+
+BootSetup *boot_setup_fft(Ctx &c, int level, double K, int r, const std::vector<int> &groups, double in_scale,
+                          bool bsgs) {
     const long N = c.N, n = N / 2;
     int lg = 0;
     while ((1L << lg) < n) lg++;
@@ -197,7 +247,11 @@ BootSetup *boot_setup_fft(Ctx &c, int level, double K, int r, const std::vector<
     const int mg = (int)groups.size();
     if (level >= c.nq || level - (2 * mg + 6 + r) < 0) throw SecpeError{-2, "boot: not enough levels"};
     auto b = std::make_unique<BootSetup>();
+    b->ctx = &c;
     b->fft = true;
+    auto enc = [&](const Diag &D, cd mul, int lv, double sc) {
+        return bsgs ? encode_stage_bsgs(c, D, mul, lv, sc, b->bufs) : encode_stage(c, D, mul, lv, sc, b->bufs);
+    };
     FftBootCfg &f = b->fcfg;
     f.level = level;
     f.r = r;
@@ -230,20 +284,20 @@ BootSetup *boot_setup_fft(Ctx &c, int level, double K, int r, const std::vector<
     for (int i = 0; i < mg; i++, lv--) {
         const double sc = (double)c.primes[lv];
         if (i < mg - 1) {
-            f.cts.push_back(encode_stage(c, cts[i], cd(1, 0), lv, sc, b->bufs));
+            f.cts.push_back(enc(cts[i], cd(1, 0), lv, sc));
         } else {
-            f.cts.push_back(encode_stage(c, cts[i], cd(0.5, 0), lv, sc, b->bufs));
-            f.cts_im = encode_stage(c, cts[i], cd(0, -0.5), lv, sc, b->bufs);
+            f.cts.push_back(enc(cts[i], cd(0.5, 0), lv, sc));
+            f.cts_im = enc(cts[i], cd(0, -0.5), lv, sc);
         }
     }
     lv = level - mg - 6 - r;
     for (int i = 0; i < mg; i++, lv--) {
         const double sc = (double)c.primes[lv];
         if (i == 0) {
-            f.stc.push_back(encode_stage(c, stc[i], cd(cc, 0), lv, sc, b->bufs));
-            f.stc_im = encode_stage(c, stc[i], cd(0, cc), lv, sc, b->bufs);
+            f.stc.push_back(enc(stc[i], cd(cc, 0), lv, sc));
+            f.stc_im = enc(stc[i], cd(0, cc), lv, sc);
         } else {
-            f.stc.push_back(encode_stage(c, stc[i], cd(1, 0), lv, sc, b->bufs));
+            f.stc.push_back(enc(stc[i], cd(1, 0), lv, sc));
         }
     }
     return b.release();

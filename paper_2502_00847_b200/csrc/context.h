@@ -222,6 +222,8 @@ void ev_rotate_hoisted(Ctx &c, const Keys &k, const CtView &in, const int *steps
 void ev_linear_transform(Ctx &c, const Keys &k, const CtView &in, const u64 *pts, long pt_stride, const int *steps,
                          int n, const CtView &out);
 void ev_mod_raise(Ctx &c, const CtView &in, const CtView &out);
+void ev_linear_transform_bsgs_gen(Ctx &c, const Keys &k, const CtView &in, const u64 *pts, long pt_stride,
+                                  const int *baby, int n1, const int *giant, int n2, const CtView &out);
 void ev_linear_transform_bsgs(Ctx &c, const Keys &k, const CtView &in, const u64 *pts, long pt_stride, int n1, int n2,
                               const CtView &out);
 void ev_mul_plain_ntt(Ctx &c, const CtView &a, const u64 *pt, const CtView &out);
@@ -251,7 +253,8 @@ int boot_depth(const BootCfg &b);
 // factorised variant (R37): CoeffToSlot / SlotToCoeff as groups of special-FFT stages, each a hoisted
 // diagonal transform (R30); pts dev [n_diag][stage level + 1][N]
 struct LtStage {
-    std::vector<int> steps;
+    std::vector<int> steps;         // diagonal form (R30), or empty with:
+    std::vector<int> baby, giant;   // baby-step giant-step form (R39), pts [giant][baby]
     const u64 *pts = nullptr;
     double scale = 0;
 };
@@ -272,6 +275,7 @@ void run_argmax_boot(Ctx &c, const Keys &k, const CtView &in, const Layout &lay,
 // library-built bootstrapping material (secpe_boot_create): the EvalMod polynomial and the four encoded
 // matrices, NTT form, [n2][n1][limbs][N] each
 struct BootSetup {
+    const Ctx *ctx = nullptr;
     bool fft = false;
     BootCfg cfg;
     DevBuf cts_re, cts_im, stc_re, stc_im;
@@ -279,7 +283,8 @@ struct BootSetup {
     std::vector<DevBuf> bufs;
 };
 BootSetup *boot_setup(Ctx &c, int level, double K, int r, int n1, int n2, double in_scale);
-BootSetup *boot_setup_fft(Ctx &c, int level, double K, int r, const std::vector<int> &groups, double in_scale);
+BootSetup *boot_setup_fft(Ctx &c, int level, double K, int r, const std::vector<int> &groups, double in_scale,
+                          bool bsgs);
 void run_bootstrap(Ctx &c, const Keys &k, const CtView &in, const BootCfg &b, CtView &out);
 struct Layout {
     int queries, prompts, classes, block;

@@ -481,39 +481,53 @@ void ev_mod_raise(Ctx &c, const CtView &in, const CtView &out) {
     c.cnt.launches += 2;
 }
 
-// Baby-step giant-step linear transform (R31): out = Rescale( sum_{g<n2} RotL( sum_{j<n1} pt_{g,j} (.) RotL(in, j),
-// g n1 ) ); the baby rotations hoisted (R29), each giant rotation's addition fused into its epilogue.
-// pt_{g,j}: dev [level+1][N] rows at pts + (g n1 + j) pt_stride.
-void ev_linear_transform_bsgs(Ctx &c, const Keys &k, const CtView &in, const u64 *pts, long pt_stride, int n1, int n2,
-                              const CtView &out) {
+// General baby-step giant-step transform (R39): out = Rescale( sum_g RotL( sum_j pt_{g,j} (.) RotL(in, baby_j),
+// giant_g ) ); the baby rotations hoisted (R29), each giant rotation's addition fused into its key switch
+// epilogue (a zero giant step is a plain copy / addition).  pt_{g,j}: dev [level+1][N] rows at
+// pts + (g n1 + j) pt_stride.
+void ev_linear_transform_bsgs_gen(Ctx &c, const Keys &k, const CtView &in, const u64 *pts, long pt_stride,
+                                  const int *baby, int n1, const int *giant, int n2, const CtView &out) {
     if (n1 < 1 || n2 < 1) throw SecpeError{-1, "linear_transform_bsgs: empty"};
     if (in.n != 1) throw SecpeError{-1, "linear_transform_bsgs: one ciphertext"};
     const int l = in.level, nl = l + 1;
     if (l < 1) throw SecpeError{-2, "linear_transform_bsgs: no level left to rescale"};
     if (out.level != l - 1) throw SecpeError{-1, "linear_transform_bsgs: output level"};
     const long N = c.N, cw = 2L * nl * N;
-    std::vector<int> bsteps(n1);
-    for (int j = 0; j < n1; j++) bsteps[j] = j;
     DevBuf rot((size_t)n1 * cw, c.st);
     std::vector<CtView> outs(n1);
     for (int j = 0; j < n1; j++) outs[j] = compact_view(c, rot.p + (long)j * cw, 1, l, in.scale);
-    ev_rotate_hoisted(c, k, in, bsteps.data(), n1, outs.data());
+    ev_rotate_hoisted(c, k, in, baby, n1, outs.data());
     DevBuf inner(cw, c.st), accb[2] = {DevBuf(cw, c.st), DevBuf(cw, c.st)};
     const CtView vin = compact_view(c, inner.p, 1, l, in.scale);
     int cur = 0;
     for (int g = 0; g < n2; g++) {
-        const CtView dst = compact_view(c, g == 0 ? accb[0].p : inner.p, 1, l, in.scale);
+        // the first term lands in the accumulator directly when it needs no rotation
+        const bool direct = g == 0 && galois_elt(c, giant[0]) == 1;
+        const CtView dst = compact_view(c, direct ? accb[0].p : inner.p, 1, l, in.scale);
         k_mac_plain(c.tab, c.logn, CRows{rot.p, cw, (long)nl * N}, cw, pts + (long)g * n1 * pt_stride, pt_stride, n1,
                     rows_of(dst), 2, qmap(nl), c.st);
         c.cnt.launches++;
-        if (g > 0) {
+        if (direct) continue;
+        if (g == 0) {
+            ev_rotate(c, k, vin, giant[0], compact_view(c, accb[0].p, 1, l, in.scale));
+        } else {
             const CtView acc = compact_view(c, accb[cur].p, 1, l, in.scale);
             const CtView nxt = compact_view(c, accb[cur ^ 1].p, 1, l, in.scale);
-            ev_rotate(c, k, vin, g * n1, nxt, &acc);  // nxt = RotL(inner, g n1) + acc
+            ev_rotate(c, k, vin, giant[g], nxt, &acc);  // nxt = RotL(inner, giant_g) + acc
             cur ^= 1;
         }
     }
     ev_rescale(c, compact_view(c, accb[cur].p, 1, l, in.scale), out);
+}
+
+// Baby-step giant-step linear transform (R31): baby steps 0..n1-1, giant steps g n1
+void ev_linear_transform_bsgs(Ctx &c, const Keys &k, const CtView &in, const u64 *pts, long pt_stride, int n1, int n2,
+                              const CtView &out) {
+    if (n1 < 1 || n2 < 1) throw SecpeError{-1, "linear_transform_bsgs: empty"};
+    std::vector<int> baby(n1), giant(n2);
+    for (int j = 0; j < n1; j++) baby[j] = j;
+    for (int g = 0; g < n2; g++) giant[g] = g * n1;
+    ev_linear_transform_bsgs_gen(c, k, in, pts, pt_stride, baby.data(), n1, giant.data(), n2, out);
 }
 
 // Hoisted rotations (N2, reading R29): one ModUp of c1 shared by every step; per step the key inner

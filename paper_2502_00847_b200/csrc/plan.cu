@@ -218,15 +218,26 @@ struct Ev {
         return out;
     }
     // hoisted diagonal transform Rescale(sum_i pt_i (.) RotL(x, steps_i)) (R30); scale (S_x pt_scale) / q_l
+    // or its baby-step giant-step form (R39) when the stage carries baby / giant steps
     Val lt(const Val &x, const LtStage &st) {
         if (n != 1) throw SecpeError{-1, "lt: one ciphertext"};
         const int l = x.level();
         const double s = (x.scale() * st.scale) / q(l);
         Val out = fresh(l - 1, s);
-        ev_linear_transform(c, k, x.v, st.pts, (long)(l + 1) * c.N, st.steps.data(), (int)st.steps.size(), out.v);
-        std::string ex;
-        for (size_t i = 0; i < st.steps.size(); i++) ex += (i ? "," : "") + std::to_string(st.steps[i]);
-        c.log("LT", l, l - 1, s, ex);
+        auto join = [](const std::vector<int> &v) {
+            std::string r;
+            for (size_t i = 0; i < v.size(); i++) r += (i ? "," : "") + std::to_string(v[i]);
+            return r;
+        };
+        if (!st.giant.empty()) {
+            ev_linear_transform_bsgs_gen(c, k, x.v, st.pts, (long)(l + 1) * c.N, st.baby.data(), (int)st.baby.size(),
+                                         st.giant.data(), (int)st.giant.size(), out.v);
+            c.log("LTG", l, l - 1, s, join(st.baby) + ";" + join(st.giant));
+        } else {
+            ev_linear_transform(c, k, x.v, st.pts, (long)(l + 1) * c.N, st.steps.data(), (int)st.steps.size(),
+                                out.v);
+            c.log("LT", l, l - 1, s, join(st.steps));
+        }
         return out;
     }
     // EvalMod on one CoeffToSlot output u (R35): x = u + conj(u), x / (K R), doubled cosine, r doublings

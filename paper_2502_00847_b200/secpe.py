@@ -32,7 +32,8 @@ class SignCfg(ctypes.Structure):
 
 
 class CLtStage(ctypes.Structure):
-    _fields_ = [("n_diag", ctypes.c_int32), ("steps", i32p), ("pts", u64p), ("pt_scale", ctypes.c_double)]
+    _fields_ = [("n_diag", ctypes.c_int32), ("steps", i32p), ("pts", u64p), ("pt_scale", ctypes.c_double),
+                ("n_baby", ctypes.c_int32), ("baby", i32p), ("n_giant", ctypes.c_int32), ("giant", i32p)]
 
 
 class CBootFftCfg(ctypes.Structure):
@@ -108,7 +109,9 @@ SIGS = {
     "secpe_bootstrap_fft": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.POINTER(CBootFftCfg),
                                            ctypes.POINTER(CCt)]),
     "secpe_boot_create_fft": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.c_double, ctypes.c_int32, i32p,
-                                             ctypes.c_int32, ctypes.c_double, ctypes.POINTER(vp)]),
+                                             ctypes.c_int32, ctypes.c_double, ctypes.c_int32, ctypes.POINTER(vp)]),
+    "secpe_boot_stage_export_bsgs": (ctypes.c_int, [vp, vp, ctypes.c_int32, ctypes.c_int32, i32p, i32p, i32p, i32p,
+                                                    u64p, ctypes.c_size_t]),
     "secpe_bootstrap_boot": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), vp, ctypes.POINTER(CCt)]),
     "secpe_boot_levels": (ctypes.c_int32, [vp, i32p]),
     "secpe_boot_steps": (ctypes.c_int32, [vp, i32p, ctypes.c_int32]),
@@ -265,6 +268,19 @@ class Boot:
         out = np.zeros(max(n, 1), dtype=np.int32)
         lib().secpe_boot_steps(self.h, out.ctypes.data_as(i32p), n)
         return out[:n].tolist()
+
+    def stage_bsgs(self, kind, idx, level):
+        """Baby-step giant-step stage: (baby, giant, host pts [n_giant][n_baby][level+1][N])."""
+        nb, ng = ctypes.c_int32(0), ctypes.c_int32(0)
+        _chk(lib().secpe_boot_stage_export_bsgs(self.ctx.h, self.h, kind, idx, ctypes.byref(nb), ctypes.byref(ng),
+                                                None, None, None, 0))
+        b_ = np.zeros(nb.value, dtype=np.int32)
+        g_ = np.zeros(ng.value, dtype=np.int32)
+        pts = np.zeros((ng.value, nb.value, level + 1, self.ctx.N), dtype=np.uint64)
+        _chk(lib().secpe_boot_stage_export_bsgs(self.ctx.h, self.h, kind, idx, ctypes.byref(nb), ctypes.byref(ng),
+                                                b_.ctypes.data_as(i32p), g_.ctypes.data_as(i32p),
+                                                pts.ctypes.data_as(u64p), pts.size))
+        return b_.tolist(), g_.tolist(), pts
 
     def stage(self, kind, idx=0, level=None):
         """Factorised stage (kind 0 cts[idx], 1 cts_im, 2 stc[idx], 3 stc_im): (steps, host pts or None)."""
@@ -505,12 +521,12 @@ class Context:
         _chk(lib().secpe_boot_create(self.h, level, K, r, n1, n2, in_scale, ctypes.byref(h)))
         return Boot(self, h)
 
-    def boot_create_fft(self, level, K, r, groups, in_scale):
-        """secpe_boot_create_fft: library-built factorised material (reading R37)."""
+    def boot_create_fft(self, level, K, r, groups, in_scale, bsgs=False):
+        """secpe_boot_create_fft: library-built factorised material (reading R37; bsgs: R39 form)."""
         g = np.ascontiguousarray(groups, dtype=np.int32)
         h = vp()
         _chk(lib().secpe_boot_create_fft(self.h, level, K, r, g.ctypes.data_as(i32p), len(g), in_scale,
-                                         ctypes.byref(h)))
+                                         1 if bsgs else 0, ctypes.byref(h)))
         return Boot(self, h)
 
     def bootstrap_boot(self, keys, a, boot):
@@ -529,11 +545,21 @@ class Context:
         keep = []
 
         def stage(t):
+            if len(t) == 4:  # (baby, giant, pts [n_giant][n_baby][limbs][N], scale): R39 form
+                baby, giant, pts, sc = t
+                assert pts.is_cuda and pts.dtype == torch.uint64 and pts.is_contiguous()
+                assert tuple(pts.shape[:2]) == (len(giant), len(baby))
+                b_ = np.ascontiguousarray(baby, dtype=np.int32)
+                g_ = np.ascontiguousarray(giant, dtype=np.int32)
+                keep.extend([b_, g_])
+                return CLtStage(0, None, ctypes.cast(pts.data_ptr(), u64p), sc, len(baby), b_.ctypes.data_as(i32p),
+                                len(giant), g_.ctypes.data_as(i32p))
             steps, pts, sc = t
             assert pts.is_cuda and pts.dtype == torch.uint64 and pts.is_contiguous() and pts.shape[0] == len(steps)
             st = np.ascontiguousarray(steps, dtype=np.int32)
             keep.append(st)
-            return CLtStage(len(steps), st.ctypes.data_as(i32p), ctypes.cast(pts.data_ptr(), u64p), sc)
+            return CLtStage(len(steps), st.ctypes.data_as(i32p), ctypes.cast(pts.data_ptr(), u64p), sc, 0, None, 0,
+                            None)
         pc = np.ascontiguousarray(poly, dtype=np.float64)
         assert pc.shape == (16,)
         ca_ = (CLtStage * len(cts))(*[stage(t) for t in cts])

@@ -947,16 +947,16 @@ def test_boot_fft_setup_matches_oracle(boot_fft):
 @pytest.mark.gpu
 @pytest.mark.slow
 def test_bootstrap_n16_refreshes(S):
-    """N3 at the paper's ring, N = 2^16 (32768 slots): library-built factorised material (groups 5/5/5), sparse
+    """N3 at the paper's ring, N = 2^16 (32768 slots): library-built factorised material (groups 5/5/5, baby-step
+    giant-step form), sparse
     secret h = 64; the refreshed ciphertext decrypts to the input slots within 2^-11 (the oracle is too slow at
     this size for a word-for-word run; the N = 2^12 tests pin the same code path word for word)."""
     from paper_2502_00847_b200 import secpe
     g = secpe.Context(synth.PARAM_SETS["boot16"])
     groups, K, r = [5, 5, 5], 16, 7
     n = g.N // 2
-    rot = plan.fft_boot_rotations(g.N, groups)
-    kg = g.keygen(synth.KEY_SEED_BASE + 31, rot, h=64)
-    b = g.boot_create_fft(g.L, K, r, groups, g.scale)
+    b = g.boot_create_fft(g.L, K, r, groups, g.scale, bsgs=True)
+    kg = g.keygen(synth.KEY_SEED_BASE + 31, b.steps(), h=64)
     z = np.random.default_rng(9).uniform(-1, 1, n)
     ct = g.encrypt(kg, z, 0, g.scale, 27)
     out = g.bootstrap_boot(kg, ct, b)
@@ -1015,7 +1015,7 @@ def test_argmax_boot_k16_n16(S):
     lay = synth.LAYOUTS["argmax_k16"]
     st = load_sign("sign_7_15_15.json")
     bs = 2.0 ** 50
-    b = g.boot_create_fft(g.L, 16, 7, [5, 5, 5], bs)
+    b = g.boot_create_fft(g.L, 16, 7, [5, 5, 5], bs, bsgs=True)
     kg = g.keygen(synth.KEY_SEED_BASE + 39, sorted(set(plan.argmax_rotations(lay))) + b.steps(), h=64)
     scores = synth.softmax_scores(47, lay["queries"], lay["prompts"], lay["classes"])
     ct = g.encrypt(kg, plan.pack(scores, lay, g.N // 2), 16, g.scale, 49)
@@ -1026,3 +1026,78 @@ def test_argmax_boot_k16_n16(S):
     ok = srt[:, -1] - srt[:, -2] >= 2.0 ** -7
     assert ok.sum() >= 200
     assert (S.labels(dec, lay)[ok] == plan.true_labels(scores)[ok]).all()
+
+
+@pytest.fixture(scope="module")
+def boot_fft_bsgs(S):
+    P = pair(S, "boot")
+    ev = ckks.Oracle(P.prm)
+    rot = plan.fft_boot_rotations(P.prm.N, FFT_GROUPS, bsgs=True)
+    seed = synth.KEY_SEED_BASE + 33
+    ko, kg = ev.keygen(seed, rot, h=BOOT["h"]), P.gpu.keygen(seed, rot, h=BOOT["h"])
+    cfg = plan.fft_boot_config(ev, P.prm.scale, P.prm.L, BOOT["K"], BOOT["r"], FFT_GROUPS, bsgs=True)
+    return P, ev, ko, kg, cfg
+
+
+def _dev_stage(t):
+    if len(t) == 3:
+        return (t[0], torch.from_numpy(np.stack(t[1])).cuda(), t[2])
+    return (t[0], t[1], torch.from_numpy(np.stack([np.stack(r) for r in t[2]])).cuda(), t[3])
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_bootstrap_fft_bsgs_bit_exact(boot_fft_bsgs):
+    """R39: the factorised bootstrap with every group in baby-step giant-step form (secpe_lt_stage with baby /
+    giant steps; general giant steps incl. negative and zero) is word for word the oracle's, same op list."""
+    P, ev, ko, kg, cfg = boot_fft_bsgs
+    prm, g = P.prm, P.gpu
+    z = np.random.default_rng(17).uniform(-1, 1, prm.N // 2)
+    ct = ev.encrypt(ko, z, prm.scale, 35, level=0)
+    ev.log.clear()
+    want = plan.bootstrap_fft(ev, ko, ct, cfg)
+    olog = list(ev.log)
+    g.oplog(enable=True, clear=True)
+    got = g.bootstrap_fft(kg, P.up(ct), cfg["level"], cfg["K"], cfg["r"], cfg["poly"],
+                          [_dev_stage(t) for t in cfg["cts"]], _dev_stage(cfg["cts_im"]),
+                          [_dev_stage(t) for t in cfg["stc"]], _dev_stage(cfg["stc_im"]))
+    glog = g.oplog(enable=False, clear=True)
+    assert glog == olog and any(l.startswith("LTG") for l in glog)
+    assert got.level == want.level and got.scale == want.scale
+    assert np.array_equal(P.down(got), want.data)
+    assert np.abs(g.decrypt(kg, got) - z).max() < 2 ** -12
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_boot_fft_bsgs_setup_matches_oracle(boot_fft_bsgs):
+    """secpe_boot_create_fft(bsgs): the library's baby / giant steps equal the oracle's split, pts equal up to FFT
+    rounding, secpe_boot_steps lists exactly the oracle's keys, and it bootstraps within 2^-12."""
+    P, ev, ko, kg, cfg = boot_fft_bsgs
+    prm, g = P.prm, P.gpu
+    b = g.boot_create_fft(prm.L, BOOT["K"], BOOT["r"], FFT_GROUPS, prm.scale, bsgs=True)
+    assert b.steps() == plan.fft_boot_rotations(prm.N, FFT_GROUPS, bsgs=True)
+    mc = len(FFT_GROUPS)
+    base = prm.L - mc - 6 - BOOT["r"]
+    cases = [(0, i, cfg["cts"][i], prm.L - i) for i in range(mc)] + [(1, 0, cfg["cts_im"], prm.L - mc + 1)]
+    cases += [(2, i, cfg["stc"][i], base - i) for i in range(mc)] + [(3, 0, cfg["stc_im"], base)]
+    q0 = prm.primes[0]
+    for kind, idx, (baby, giant, pts, sc), lv in cases:
+        gb, gg, gp = b.stage_bsgs(kind, idx, lv)
+        assert gb == list(baby) and gg == list(giant), (kind, idx)
+        want = np.stack([np.stack(r) for r in pts]).reshape(-1, lv + 1, prm.N)
+        gp = gp.reshape(-1, lv + 1, prm.N)
+        same = (gp == want).all(axis=(1, 2))
+        if same.all():
+            continue
+        gi = ckks.ntt_limbs(gp[~same][:, :1], prm, [0], inverse=True)[:, 0].astype(object)
+        wi = ckks.ntt_limbs(want[~same][:, :1], prm, [0], inverse=True)[:, 0].astype(object)
+        d = (gi - wi) % q0
+        d = np.where(d > q0 // 2, d - q0, d)
+        wc = np.where(wi > q0 // 2, wi - q0, wi)
+        tol = 1 + int(float(np.abs(wc).max()) * 2.0 ** -46)
+        assert np.abs(d).max() <= tol, (kind, idx, int(np.abs(d).max()), tol)
+    z = np.random.default_rng(18).uniform(-1, 1, prm.N // 2)
+    ct = ev.encrypt(ko, z, prm.scale, 36, level=0)
+    out = g.bootstrap_boot(kg, P.up(ct), b)
+    assert np.abs(g.decrypt(kg, out) - z).max() < 2 ** -12

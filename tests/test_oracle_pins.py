@@ -861,3 +861,43 @@ def test_argmax_boot_k16_one_hot():
     want = np.zeros(lay["classes"])
     want[plan.true_labels(scores)[0]] = 1.0
     assert np.abs(dec[: lay["classes"]] - want).max() < 2 ** -5
+
+
+def test_bsgs_split_equals_diagonal_form():
+    """R39: every merged special-FFT group in baby-step giant-step form,
+    sum_g RotL(sum_j RotR(d_{b_j + G_g}, G_g) (.) RotL(v, b_j), G_g), equals its diagonal form on a plaintext
+    vector; baby / giant counts about sqrt(#diagonals)."""
+    N = 1 << 8
+    n = N // 2
+    v = np.random.default_rng(3).normal(size=n) + 0j
+    for groups in ([3, 4], [2, 2, 3], [7]):
+        stc, cts = plan.fft_groups(N, groups)
+        for D in stc + cts:
+            baby, giant, where = plan.bsgs_split(D, n)
+            assert len(baby) * len(giant) >= len(D) and len(baby) < 2 * math.sqrt(len(D)) + 1
+            acc = 0
+            for g, G in enumerate(giant):
+                inner = 0
+                for j, b in enumerate(baby):
+                    k = where[(g, j)]
+                    d = D[k] if k is not None else np.zeros(n)
+                    inner = inner + np.roll(d, G) * np.roll(v, -b)
+                acc = acc + np.roll(inner, -G)
+            assert np.abs(acc - plan.diag_apply(D, v)).max() < 1e-9
+
+
+def test_bootstrap_fft_bsgs_refreshes():
+    """R39 end to end (N = 2^8): the baby-step giant-step bootstrap needs fewer keys and still refreshes within
+    2^-14."""
+    prm = ckks.Params(synth.PARAM_SETS["boot_tiny"])
+    ev = ckks.Oracle(prm)
+    groups, K, r = [3, 4], 16, 7
+    rot = plan.fft_boot_rotations(prm.N, groups, bsgs=True)
+    assert len(rot) < len(plan.fft_boot_rotations(prm.N, groups))
+    keys = ev.keygen(9, rot, h=64)
+    z = np.random.default_rng(10).uniform(-1, 1, prm.N // 2)
+    ct = ev.encrypt(keys, z, prm.scale, 5, level=0)
+    cfg = plan.fft_boot_config(ev, ct.scale, prm.L, K, r, groups, bsgs=True)
+    out = plan.bootstrap_fft(ev, keys, ct, cfg)
+    assert out.level == prm.L - plan.fft_boot_depth(groups, r)
+    assert np.abs(ev.decrypt(keys, out).real - z).max() < 2 ** -14
