@@ -265,7 +265,22 @@ def bootstrap_bench(stream, t_ms):
         res[0] = ctx.bootstrap_boot(keys, c0, boot)
     ms = t_ms(one16)
     err = float(abs(ctx.decrypt(keys, res[0]) - z).max())
-    out["N=2^16_fft"] = {"ms_per_bootstrap": ms, "logn": ctx.logn, "slots": ctx.N // 2, "level_in": 0,
+    # where one bootstrap's time goes (the library's CUDA-event profiler, one extra untimed call)
+    torch.cuda.synchronize()
+    ctx.opcounts(reset=True)
+    ctx.profile_begin()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    one16()
+    e1.record(stream)
+    prof = ctx.profile_end()
+    torch.cuda.synchronize()
+    tot = e0.elapsed_time(e1)
+    cnt = ctx.opcounts(reset=True)
+    breakdown = {"keyswitch_share": prof["keyswitch"]["ms"] / tot, "rescale_share": prof["rescale"]["ms"] / tot,
+                 "ntt_share": prof["ntt"]["ms"] / tot, "profiled_ms": tot, "key_switches": cnt["keyswitch"],
+                 "ntt_limbs": cnt["ntt_limbs"], "launches": cnt["launches"]}
+    out["N=2^16_fft"] = {"breakdown": breakdown, "ms_per_bootstrap": ms, "logn": ctx.logn, "slots": ctx.N // 2, "level_in": 0,
                          "raised_to": ctx.L, "level_out": res[0].level, "galois_keys": len(steps),
                          "max_abs_err": err, "setup_s": setup_s,
                          "transforms": "special-FFT groups 5/5/5, baby-step giant-step form (R37, R39)"}
