@@ -606,15 +606,13 @@ static void argmax_boot_views(Ctx &c, const secpe_keys *keys, const secpe_ct *in
     Layout lay = layout_of(c, layout);
     SignCfg sc = sign_cfg(scfg);
     check_fft_keys(c, keys, b);
-    for (int i = 0; i < n_in; i++) {
-        CtView vi = view_of(c, &in[i]);
-        REQUIRE(in[i].level == in[0].level && in[i].scale == in[0].scale, SECPE_EINVAL, "batch levels differ");
-        REQUIRE(out[i].data && out[i].data != in[i].data, SECPE_EINVAL, "bad output buffer");
-        const int ol = argmax_boot_level(lay, sc, b, vi.level);
-        CtView vo = compact_view(c, out[i].data, 1, ol, c.scale);
-        run_argmax_boot(c, *keys->k, vi, lay, sc, b, boot_scale, vo);
-        set_out(&out[i], vo);
-    }
+    DevBuf inb, outb;
+    CtView vin = batch_in(c, in, n_in, inb);
+    for (int i = 0; i < n_in; i++) REQUIRE(out[i].data != in[i].data, SECPE_EINVAL, "out must not alias in");
+    const int ol = argmax_boot_level(lay, sc, b, vin.level);
+    CtView vout = batch_out(c, out, n_in, ol, c.scale, outb);
+    run_argmax_boot(c, *keys->k, vin, lay, sc, b, boot_scale, vout);
+    batch_out_finish(c, out, n_in, vout, outb);
 }
 int secpe_argmax_boot_info(secpe_ctx *ctx, const secpe_layout *layout, const secpe_sign_cfg *cfg,
                            const secpe_boot *boot, int32_t in_level, int32_t *out_level) {

@@ -450,18 +450,18 @@ void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView 
 void ev_linear_transform(Ctx &c, const Keys &k, const CtView &in, const u64 *pts, long pt_stride, const int *steps,
                          int n, const CtView &out) {
     if (n < 1) throw SecpeError{-1, "linear_transform: no diagonals"};
-    if (in.n != 1) throw SecpeError{-1, "linear_transform: one ciphertext"};
-    const int l = in.level, nl = l + 1;
+    const int l = in.level, nl = l + 1, B = in.n;  // a batch of B ciphertexts, one transform
     if (l < 1) throw SecpeError{-2, "linear_transform: no level left to rescale"};
-    if (out.level != l - 1) throw SecpeError{-1, "linear_transform: output level"};
-    const long N = c.N, cw = 2L * nl * N;
-    DevBuf rot((size_t)n * cw, c.st);
+    if (out.level != l - 1 || out.n != B) throw SecpeError{-1, "linear_transform: output level"};
+    const long N = c.N, cw = 2L * nl * N, bw = (long)B * cw;
+    DevBuf rot((size_t)n * bw, c.st);
     std::vector<CtView> outs(n);
-    for (int i = 0; i < n; i++) outs[i] = compact_view(c, rot.p + (long)i * cw, 1, l, in.scale);
+    for (int i = 0; i < n; i++) outs[i] = compact_view(c, rot.p + (long)i * bw, B, l, in.scale);
     ev_rotate_hoisted(c, k, in, steps, n, outs.data());
-    DevBuf acc(cw, c.st);
-    const CtView va = compact_view(c, acc.p, 1, l, in.scale);
-    k_mac_plain(c.tab, c.logn, CRows{rot.p, cw, (long)nl * N}, cw, pts, pt_stride, n, rows_of(va), 2, qmap(nl), c.st);
+    DevBuf acc(bw, c.st);
+    const CtView va = compact_view(c, acc.p, B, l, in.scale);
+    k_mac_plain(c.tab, c.logn, CRows{rot.p, cw, (long)nl * N}, bw, pts, pt_stride, n, rows_of(va), 2 * B, qmap(nl),
+                c.st);
     c.cnt.launches++;
     ev_rescale(c, va, out);
 }
@@ -488,36 +488,35 @@ void ev_mod_raise(Ctx &c, const CtView &in, const CtView &out) {
 void ev_linear_transform_bsgs_gen(Ctx &c, const Keys &k, const CtView &in, const u64 *pts, long pt_stride,
                                   const int *baby, int n1, const int *giant, int n2, const CtView &out) {
     if (n1 < 1 || n2 < 1) throw SecpeError{-1, "linear_transform_bsgs: empty"};
-    if (in.n != 1) throw SecpeError{-1, "linear_transform_bsgs: one ciphertext"};
-    const int l = in.level, nl = l + 1;
+    const int l = in.level, nl = l + 1, B = in.n;  // a batch of B ciphertexts, one transform
     if (l < 1) throw SecpeError{-2, "linear_transform_bsgs: no level left to rescale"};
-    if (out.level != l - 1) throw SecpeError{-1, "linear_transform_bsgs: output level"};
-    const long N = c.N, cw = 2L * nl * N;
-    DevBuf rot((size_t)n1 * cw, c.st);
+    if (out.level != l - 1 || out.n != B) throw SecpeError{-1, "linear_transform_bsgs: output level"};
+    const long N = c.N, cw = 2L * nl * N, bw = (long)B * cw;
+    DevBuf rot((size_t)n1 * bw, c.st);
     std::vector<CtView> outs(n1);
-    for (int j = 0; j < n1; j++) outs[j] = compact_view(c, rot.p + (long)j * cw, 1, l, in.scale);
+    for (int j = 0; j < n1; j++) outs[j] = compact_view(c, rot.p + (long)j * bw, B, l, in.scale);
     ev_rotate_hoisted(c, k, in, baby, n1, outs.data());
-    DevBuf inner(cw, c.st), accb[2] = {DevBuf(cw, c.st), DevBuf(cw, c.st)};
-    const CtView vin = compact_view(c, inner.p, 1, l, in.scale);
+    DevBuf inner(bw, c.st), accb[2] = {DevBuf(bw, c.st), DevBuf(bw, c.st)};
+    const CtView vin = compact_view(c, inner.p, B, l, in.scale);
     int cur = 0;
     for (int g = 0; g < n2; g++) {
         // the first term lands in the accumulator directly when it needs no rotation
         const bool direct = g == 0 && galois_elt(c, giant[0]) == 1;
-        const CtView dst = compact_view(c, direct ? accb[0].p : inner.p, 1, l, in.scale);
-        k_mac_plain(c.tab, c.logn, CRows{rot.p, cw, (long)nl * N}, cw, pts + (long)g * n1 * pt_stride, pt_stride, n1,
-                    rows_of(dst), 2, qmap(nl), c.st);
+        const CtView dst = compact_view(c, direct ? accb[0].p : inner.p, B, l, in.scale);
+        k_mac_plain(c.tab, c.logn, CRows{rot.p, cw, (long)nl * N}, bw, pts + (long)g * n1 * pt_stride, pt_stride, n1,
+                    rows_of(dst), 2 * B, qmap(nl), c.st);
         c.cnt.launches++;
         if (direct) continue;
         if (g == 0) {
-            ev_rotate(c, k, vin, giant[0], compact_view(c, accb[0].p, 1, l, in.scale));
+            ev_rotate(c, k, vin, giant[0], compact_view(c, accb[0].p, B, l, in.scale));
         } else {
-            const CtView acc = compact_view(c, accb[cur].p, 1, l, in.scale);
-            const CtView nxt = compact_view(c, accb[cur ^ 1].p, 1, l, in.scale);
+            const CtView acc = compact_view(c, accb[cur].p, B, l, in.scale);
+            const CtView nxt = compact_view(c, accb[cur ^ 1].p, B, l, in.scale);
             ev_rotate(c, k, vin, giant[g], nxt, &acc);  // nxt = RotL(inner, giant_g) + acc
             cur ^= 1;
         }
     }
-    ev_rescale(c, compact_view(c, accb[cur].p, 1, l, in.scale), out);
+    ev_rescale(c, compact_view(c, accb[cur].p, B, l, in.scale), out);
 }
 
 // Baby-step giant-step linear transform (R31): baby steps 0..n1-1, giant steps g n1

@@ -209,7 +209,6 @@ struct Ev {
     }
     // Rescale(sum_g RotL(sum_j pt_{g,j} (.) RotL(x, j), g n1)) (R31); output scale (S_x pt_scale) / q_l
     Val lt_bsgs(const Val &x, const u64 *pts, int n1, int n2, double pt_scale) {
-        if (n != 1) throw SecpeError{-1, "lt_bsgs: one ciphertext"};
         const int l = x.level();
         const double s = (x.scale() * pt_scale) / q(l);
         Val out = fresh(l - 1, s);
@@ -220,7 +219,6 @@ struct Ev {
     // hoisted diagonal transform Rescale(sum_i pt_i (.) RotL(x, steps_i)) (R30); scale (S_x pt_scale) / q_l
     // or its baby-step giant-step form (R39) when the stage carries baby / giant steps
     Val lt(const Val &x, const LtStage &st) {
-        if (n != 1) throw SecpeError{-1, "lt: one ciphertext"};
         const int l = x.level();
         const double s = (x.scale() * st.scale) / q(l);
         Val out = fresh(l - 1, s);
@@ -461,22 +459,15 @@ int argmax_boot_level(const Layout &lay, const SignCfg &cfg, const FftBootCfg &b
     return d - sd;
 }
 
+// the whole batch through one plan: every key (and every transform plaintext) is read once per op for all
+// in.n ciphertexts
 void run_argmax_boot(Ctx &c, const Keys &k, const CtView &in, const Layout &lay, const SignCfg &cfg,
                      const FftBootCfg &b, double boot_scale, CtView &out) {
-    Ev ev{c, k, 1};
-    for (int i = 0; i < in.n; i++) {
-        CtView vi = in, vo = out;
-        vi.data = in.data + (long)i * in.stride;
-        vi.n = 1;
-        vo.data = out.data + (long)i * out.stride;
-        vo.n = 1;
-        Val r = ev.argmax_boot(Val{nullptr, vi}, lay, cfg, b, boot_scale);
-        vo.level = r.level();
-        vo.scale = r.scale();
-        ev_copy(c, r.v, vo);
-        out.level = r.level();
-        out.scale = r.scale();
-    }
+    Ev ev{c, k, in.n};
+    Val r = ev.argmax_boot(Val{nullptr, in}, lay, cfg, b, boot_scale);
+    out.level = r.level();
+    out.scale = r.scale();
+    ev_copy(c, r.v, out);
 }
 
 void run_bootstrap_fft(Ctx &c, const Keys &k, const CtView &in, const FftBootCfg &b, CtView &out) {

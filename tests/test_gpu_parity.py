@@ -1017,15 +1017,21 @@ def test_argmax_boot_k16_n16(S):
     bs = 2.0 ** 50
     b = g.boot_create_fft(g.L, 16, 7, [5, 5, 5], bs, bsgs=True)
     kg = g.keygen(synth.KEY_SEED_BASE + 39, sorted(set(plan.argmax_rotations(lay))) + b.steps(), h=64)
-    scores = synth.softmax_scores(47, lay["queries"], lay["prompts"], lay["classes"])
-    ct = g.encrypt(kg, plan.pack(scores, lay, g.N // 2), 16, g.scale, 49)
-    out = g.enc_argmax_boot(kg, ct, lay, st, b, bs)
-    dec = g.decrypt(kg, out)
-    mean = scores.mean(axis=1)
-    srt = np.sort(mean, axis=1)
-    ok = srt[:, -1] - srt[:, -2] >= 2.0 ** -7
-    assert ok.sum() >= 200
-    assert (S.labels(dec, lay)[ok] == plan.true_labels(scores)[ok]).all()
+    sc2 = [synth.softmax_scores(47 + i, lay["queries"], lay["prompts"], lay["classes"]) for i in range(2)]
+    cts = [g.encrypt(kg, plan.pack(sc, lay, g.N // 2), 16, g.scale, 49 + i) for i, sc in enumerate(sc2)]
+    batch = S.Ct(torch.cat([c.t for c in cts]), 16, g.scale)
+    out = g.enc_argmax_boot(kg, batch, lay, st, b, bs)
+    # the batched plan (keys and transform plaintexts read once per op for both) gives the single-ciphertext words
+    one = g.enc_argmax_boot(kg, cts[1], lay, st, b, bs)
+    assert one.level == out.level and one.scale == out.scale
+    assert torch.equal(one.t[0], out.t[1])
+    for i, scores in enumerate(sc2):
+        dec = g.decrypt(kg, out, i)
+        mean = scores.mean(axis=1)
+        srt = np.sort(mean, axis=1)
+        ok = srt[:, -1] - srt[:, -2] >= 2.0 ** -7
+        assert ok.sum() >= 200
+        assert (S.labels(dec, lay)[ok] == plan.true_labels(scores)[ok]).all()
 
 
 @pytest.fixture(scope="module")
