@@ -212,6 +212,7 @@ def micro_configs(stream, reps=5):
     del ctx, keys, a, b, r, o
     out["N3_bootstrap"] = bootstrap_bench(stream, t_ms)
     out["N4_argmax_k16"] = argmax_k16_bench(stream, t_ms)
+    out["N4_argmax_n256"] = argmax_boot_bench(stream, t_ms, "argmax_n256", 8, 6.0)
     return out
 
 
@@ -287,7 +288,11 @@ def bootstrap_bench(stream, t_ms):
     return out
 
 
-def argmax_k16_bench(stream, t_ms):
+def argmax_k16_bench(stream, t_ms, B=8):
+    return argmax_boot_bench(stream, t_ms, "argmax_k16", B, 2.0)
+
+
+def argmax_boot_bench(stream, t_ms, lname, B, sigma):
     """SURVEY 8(f) N4 (reading R38): Algorithm 1 with K = 16 classes at N = 2^16 (256 queries x 8 prompts per
     ciphertext), refreshed by four factorised bootstraps per ciphertext (secpe_enc_argmax_boot); one
     ciphertext per call, CUDA events, median.  Labels checked against the plaintext argmax above the margin."""
@@ -295,15 +300,15 @@ def argmax_k16_bench(stream, t_ms):
     import synth
     from paper_2502_00847_b200 import secpe
     ctx = secpe.Context(synth.PARAM_SETS["boot_argmax16"], stream=stream.cuda_stream)
-    lay = synth.LAYOUTS["argmax_k16"]
+    lay = synth.LAYOUTS[lname]
     st = load_sign("sign_7_15_15.json")
     bs = 2.0 ** 50
     boot = ctx.boot_create_fft(ctx.L, 16, 7, [5, 5, 5], bs, bsgs=True)
     P, K = lay["prompts"], lay["classes"]
     rot = [K << t for t in range(P.bit_length() - 1)] + [-K] + [1 << i for i in range(K.bit_length() - 1)]
     keys = ctx.keygen(synth.KEY_SEED_BASE + 39, sorted(set(rot)) + boot.steps(), h=64)
-    B = 4  # ciphertexts per call: one plan, keys and transform plaintexts read once per op for the batch
-    scores = [synth.softmax_scores(47 + i, lay["queries"], P, K) for i in range(B)]
+    # B ciphertexts per call: one plan, keys and transform plaintexts read once per op for the batch
+    scores = [synth.softmax_scores(47 + i, lay["queries"], P, K, sigma=sigma) for i in range(B)]
     cts = []
     for i in range(B):
         z = np.zeros(ctx.N // 2)
@@ -327,7 +332,8 @@ def argmax_k16_bench(stream, t_ms):
         tot += int(ok.sum())
         inm += int((~ok).sum())
     return {"ms_per_call": ms, "ciphertexts_per_call": B, "queries_per_ciphertext": lay["queries"], "classes": K,
-            "prompts": P, "query_argmax_per_s": B * lay["queries"] / (ms / 1000), "bootstraps_per_ciphertext": 4,
+            "prompts": P, "query_argmax_per_s": B * lay["queries"] / (ms / 1000),
+            "bootstraps_per_ciphertext": K.bit_length() - 1, "logit_sigma": sigma,
             "labels_exact_above_margin": good / tot, "in_margin_fraction": inm / (B * lay["queries"]),
             "logn": ctx.logn, "chain": "q0 60 + 16 x 45 + 19 x 50 bit"}
 

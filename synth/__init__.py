@@ -67,6 +67,9 @@ LAYOUTS = {
     "argmax_small_k2": dict(queries=128, prompts=8, classes=2, block=16),
     "tiny_k16": dict(queries=1, prompts=8, classes=16, block=128),
     "boot_k16": dict(queries=16, prompts=8, classes=16, block=128),
+    # SURVEY 8(f) N4 "n = 256 with 64 per ciphertext" (2n slots per argmax): 256 classes, 2 prompts
+    "argmax_n256": dict(queries=64, prompts=2, classes=256, block=512),
+    "boot_n256": dict(queries=4, prompts=2, classes=256, block=512),
 }
 
 KEY_SEED_BASE = 0x5EC9E000

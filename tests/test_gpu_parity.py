@@ -1107,3 +1107,41 @@ def test_boot_fft_bsgs_setup_matches_oracle(boot_fft_bsgs):
     ct = ev.encrypt(ko, z, prm.scale, 36, level=0)
     out = g.bootstrap_boot(kg, P.up(ct), b)
     assert np.abs(g.decrypt(kg, out) - z).max() < 2 ** -12
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_argmax_boot_n256_bit_exact(S):
+    """N4 large n (SURVEY 8(f) N4 "n = 256 with 64 per ciphertext"): 256 classes, eight Max steps
+    and eight bootstraps per ciphertext; at N = 2^12 (4 queries per ciphertext) word for word the oracle's plan,
+    labels exact above the margin."""
+    P = pair(S, "boot_argmax")
+    prm, g = P.prm, P.gpu
+    ev = ckks.Oracle(prm)
+    lay = synth.LAYOUTS["boot_n256"]
+    st = load_sign("sign_7_15_15.json")
+    groups = [4, 4, 3]
+    rot = plan.argmax_rotations(lay) + plan.fft_boot_rotations(prm.N, groups, bsgs=True)
+    seed = synth.KEY_SEED_BASE + 41
+    ko, kg = ev.keygen(seed, rot, h=64), g.keygen(seed, rot, h=64)
+    bs = 2.0 ** 50
+    cfg = plan.fft_boot_config(ev, bs, prm.L, 16, 7, groups, bsgs=True)
+    scores = synth.softmax_scores(51, lay["queries"], lay["prompts"], lay["classes"], sigma=6.0)
+    ct = ev.encrypt(ko, plan.pack(scores, lay, prm.N // 2), prm.scale, 53, level=16)
+    nb = [0]
+
+    def boot(c):
+        nb[0] += 1
+        return plan.bootstrap_fft(ev, ko, c, cfg)
+    want = plan.argmax_boot(ev, ko, ct, lay, st, boot, bs)
+    assert nb[0] == 8
+    fc = (cfg["level"], cfg["K"], cfg["r"], cfg["poly"], [_dev_stage(t) for t in cfg["cts"]],
+          _dev_stage(cfg["cts_im"]), [_dev_stage(t) for t in cfg["stc"]], _dev_stage(cfg["stc_im"]))
+    got = g.enc_argmax_boot(kg, P.up(ct), lay, st, None, bs, fft_cfg=fc)
+    assert got.level == want.level and got.scale == want.scale
+    assert np.array_equal(P.down(got), want.data)
+    mean = scores.mean(axis=1)
+    srt = np.sort(mean, axis=1)
+    ok = srt[:, -1] - srt[:, -2] >= 2.0 ** -7
+    assert ok.sum() >= 2
+    assert (S.labels(g.decrypt(kg, got), lay)[ok] == plan.true_labels(scores)[ok]).all()

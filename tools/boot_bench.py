@@ -28,7 +28,9 @@ def main():
             ts.append(a.elapsed_time(b))
         return statistics.median(ts)
     print(json.dumps(bench.bootstrap_bench(stream, t_ms)))
-    print(json.dumps(bench.argmax_k16_bench(stream, t_ms)))
+    for B in [int(b) for b in os.environ.get("SECPE_N4_BATCHES", "8").split(",")]:
+        print(json.dumps(bench.argmax_k16_bench(stream, t_ms, B)))
+    print(json.dumps(bench.argmax_boot_bench(stream, t_ms, "argmax_n256", 8, 6.0)))
 
 
 if __name__ == "__main__":
