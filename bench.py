@@ -213,6 +213,7 @@ def micro_configs(stream, reps=5):
     out["N3_bootstrap"] = bootstrap_bench(stream, t_ms)
     out["N4_argmax_k16"] = argmax_k16_bench(stream, t_ms)
     out["N4_argmax_n256"] = argmax_boot_bench(stream, t_ms, "argmax_n256", 8, 6.0)
+    out["N4_clip_80x1000"] = clip_bench(stream, t_ms)
     return out
 
 
@@ -286,6 +287,54 @@ def bootstrap_bench(stream, t_ms):
                          "max_abs_err": err, "setup_s": setup_s,
                          "transforms": "special-FFT groups 5/5/5, baby-step giant-step form (R37, R39)"}
     return out
+
+
+def clip_bench(stream, t_ms, G=2, prompts=80, classes=1000):
+    """SURVEY 8(f) N4 CLIP scale: `prompts` prompts x `classes` classes (padded to 1024 with
+    zero scores), 16 queries per query set at N = 2^16, 2 prompts per ciphertext and prompts / 2 ciphertexts
+    per query set summed first (prompt_cts), ten bootstraps per query set; G query sets per call."""
+    import torch
+    import synth
+    from paper_2502_00847_b200 import secpe
+    ctx = secpe.Context(synth.PARAM_SETS["boot_argmax16"], stream=stream.cuda_stream)
+    lay = synth.LAYOUTS["clip"]
+    st = load_sign("sign_7_15_15.json")
+    bs = 2.0 ** 50
+    boot = ctx.boot_create_fft(ctx.L, 16, 7, [5, 5, 5], bs, bsgs=True)
+    P, K, Q, blk = lay["prompts"], lay["classes"], lay["queries"], lay["block"]
+    pc = prompts // P
+    rot = [K << t for t in range(P.bit_length() - 1)] + [-K] + [1 << i for i in range(K.bit_length() - 1)]
+    keys = ctx.keygen(synth.KEY_SEED_BASE + 45, sorted(set(rot)) + boot.steps(), h=64)
+    scores, cts = [], []
+    for gi in range(G):
+        sc = np.zeros((Q, prompts, K))
+        sc[:, :, :classes] = synth.ensemble_scores(61 + gi, Q, prompts, classes)
+        scores.append(sc)
+        for i in range(pc):
+            z = np.zeros(ctx.N // 2)
+            for qi in range(Q):
+                for p in range(P):
+                    z[qi * blk + p * K: qi * blk + (p + 1) * K] = sc[qi, i * P + p]
+            cts.append(ctx.encrypt(keys, z, 16, ctx.scale, 1000 * gi + i))
+    batch = secpe.Ct(torch.cat([c.t for c in cts]), 16, ctx.scale)
+    del cts
+    res = [None]
+
+    def run():
+        res[0] = ctx.enc_argmax_boot(keys, batch, lay, st, boot, bs, prompt_cts=pc)
+    ms = t_ms(run)
+    good = tot = 0
+    for gi in range(G):
+        lab = secpe.labels(ctx.decrypt(keys, res[0], gi), lay)
+        mean = scores[gi].mean(axis=1)
+        srt = np.sort(mean, axis=1)
+        ok = srt[:, -1] - srt[:, -2] >= 2.0 ** -7
+        good += int((lab[ok] == np.argmax(mean, axis=1)[ok]).sum())
+        tot += int(ok.sum())
+    return {"ms_per_call": ms, "query_sets_per_call": G, "queries_per_set": Q, "prompts": prompts,
+            "classes": classes, "prompt_ciphertexts_per_set": pc, "query_argmax_per_s": G * Q / (ms / 1000),
+            "bootstraps_per_set": K.bit_length() - 1, "labels_exact_above_margin": good / max(tot, 1),
+            "above_margin": tot, "logn": ctx.logn}
 
 
 def argmax_k16_bench(stream, t_ms, B=8):

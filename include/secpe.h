@@ -334,18 +334,22 @@ int secpe_boot_stage_export_bsgs(secpe_ctx *ctx, const secpe_boot *boot, int32_t
  * factorised bootstrap: before a Max when fewer than sign_depth + 2 levels remain (one is kept for the
  * next refresh) and before the final Sign when fewer than sign_depth remain.  A refresh is a constant
  * product by 1 onto level 0 at boot_scale (the input scale the bootstrap material was built for), the
- * bootstrap, and a constant product by 1 back to the context's nominal scale.  One ciphertext after
- * another (in[i] / out[i] as secpe_enc_argmax, all at one level and scale).  Errors: SECPE_ELEVEL when a
- * refresh cannot fit, SECPE_ENOKEY, SECPE_EINVAL, SECPE_ELAYOUT. */
+ * bootstrap, and a constant product by 1 back to the context's nominal scale.  The batch runs as one
+ * plan (every key and transform plaintext read once per op for all of it).  prompt_cts >= 1: the prompts
+ * of one query set are spread over prompt_cts ciphertexts (CLIP-scale prompt counts),
+ * in[g * prompt_cts + i] = member i of group g, all in the same layout; H1 first sums each group in member
+ * order and the mask normalises by layout->prompts x prompt_cts.  n_in = groups x
+ * prompt_cts inputs (one level and scale); out: host[groups].  Errors: SECPE_ELEVEL when a refresh cannot
+ * fit, SECPE_ENOKEY, SECPE_EINVAL, SECPE_ELAYOUT. */
 int secpe_argmax_boot_info(secpe_ctx *ctx, const secpe_layout *layout, const secpe_sign_cfg *cfg,
                            const secpe_boot *boot, int32_t in_level, int32_t *out_level);
 int secpe_enc_argmax_boot(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n_in,
-                          const secpe_layout *layout, const secpe_sign_cfg *cfg, const secpe_boot *boot,
-                          double boot_scale, secpe_ct *out);
+                          int32_t prompt_cts, const secpe_layout *layout, const secpe_sign_cfg *cfg,
+                          const secpe_boot *boot, double boot_scale, secpe_ct *out);
 /* The same with caller-encoded factorised material (parity tests). */
 int secpe_enc_argmax_boot_cfg(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n_in,
-                              const secpe_layout *layout, const secpe_sign_cfg *cfg, const secpe_boot_fft_cfg *bcfg,
-                              double boot_scale, secpe_ct *out);
+                              int32_t prompt_cts, const secpe_layout *layout, const secpe_sign_cfg *cfg,
+                              const secpe_boot_fft_cfg *bcfg, double boot_scale, secpe_ct *out);
 /* Levels one bootstrap consumes (8 + r): out level = cfg->level - secpe_boot_depth(cfg). */
 int32_t secpe_boot_depth(const secpe_boot_cfg *cfg);
 /* in: level 0; out->data sized secpe_ct_bytes(cfg->level - secpe_boot_depth(cfg)); out->level / scale

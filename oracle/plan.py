@@ -563,18 +563,29 @@ def bootstrap_fft(ev, keys, ct, cfg):
 # 12 levels each plus the final Sign), with a bootstrap (R37) before every comparison
 # that would not fit (reading R38).
 # ---------------------------------------------------------------------------------------------
-def argmax_boot(ev, keys, y, layout, stages, boot, boot_scale):
+def argmax_boot(ev, keys, y, layout, stages, boot, boot_scale, prompt_cts=1):
     """Algorithm 1 as `argmax`, refreshing y (before a Max) or y_dup - y_max (before the final Sign) when
     fewer levels remain than the step needs (a Max keeps one level for the next refresh): one constant
     product by 1 landing at level 0 and scale boot_scale (the scale the bootstrap material expects),
     boot(ct), then one constant product by 1 back to the nominal scale (so that y_dup - y_max sees
-    bit-identical scales)."""
+    bit-identical scales).
+
+    prompt_cts > 1 (CLIP-scale prompt counts): y is a list of prompt_cts ciphertexts holding
+    disjoint prompt sets in the same layout; H1 first sums them in list order (y* = sum y_i),
+    and the mask normalises by prompts x prompt_cts (Eq. 5 with D_max = the total prompt count)."""
     P, K = layout["prompts"], layout["classes"]
     n_slots = ev.prm.N // 2
     check_layout(layout, n_slots)
+    if prompt_cts > 1:
+        if len(y) != prompt_cts:
+            raise ValueError("one ciphertext per prompt group")
+        acc = y[0]
+        for c in y[1:]:
+            acc = ev.add(acc, c)
+        y = acc
     for t in range(int(math.log2(P))):
         y = ev.add(y, ev.rot(keys, y, K << t))
-    y = ev.mul_mask(y, mask_slots(layout, n_slots), ev.prm.scale)
+    y = ev.mul_mask(y, mask_slots(layout, n_slots) / prompt_cts, ev.prm.scale)
     y = ev.add(y, ev.rot(keys, y, -K))
     ydup = y
     sd = sign_depth(stages)

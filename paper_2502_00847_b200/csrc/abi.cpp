@@ -601,18 +601,22 @@ int secpe_bootstrap_fft(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *
 }
 // N4 (R38): argmax with bootstrapping, one ciphertext after another
 static void argmax_boot_views(Ctx &c, const secpe_keys *keys, const secpe_ct *in, int n_in, const secpe_layout *layout,
-                              const secpe_sign_cfg *scfg, const FftBootCfg &b, double boot_scale, secpe_ct *out) {
+                              const secpe_sign_cfg *scfg, const FftBootCfg &b, double boot_scale, int prompt_cts,
+                              secpe_ct *out) {
     REQUIRE(keys && in && out && n_in >= 1 && boot_scale > 0, SECPE_EINVAL, "null argument");
+    REQUIRE(prompt_cts >= 1 && n_in % prompt_cts == 0, SECPE_EINVAL, "n_in must be a multiple of prompt_cts");
     Layout lay = layout_of(c, layout);
     SignCfg sc = sign_cfg(scfg);
     check_fft_keys(c, keys, b);
+    const int n_out = n_in / prompt_cts;
     DevBuf inb, outb;
     CtView vin = batch_in(c, in, n_in, inb);
-    for (int i = 0; i < n_in; i++) REQUIRE(out[i].data != in[i].data, SECPE_EINVAL, "out must not alias in");
+    for (int i = 0; i < n_out; i++)
+        for (int j = 0; j < n_in; j++) REQUIRE(out[i].data != in[j].data, SECPE_EINVAL, "out must not alias in");
     const int ol = argmax_boot_level(lay, sc, b, vin.level);
-    CtView vout = batch_out(c, out, n_in, ol, c.scale, outb);
-    run_argmax_boot(c, *keys->k, vin, lay, sc, b, boot_scale, vout);
-    batch_out_finish(c, out, n_in, vout, outb);
+    CtView vout = batch_out(c, out, n_out, ol, c.scale, outb);
+    run_argmax_boot(c, *keys->k, vin, lay, sc, b, boot_scale, prompt_cts, vout);
+    batch_out_finish(c, out, n_out, vout, outb);
 }
 int secpe_argmax_boot_info(secpe_ctx *ctx, const secpe_layout *layout, const secpe_sign_cfg *cfg,
                            const secpe_boot *boot, int32_t in_level, int32_t *out_level) {
@@ -622,19 +626,19 @@ int secpe_argmax_boot_info(secpe_ctx *ctx, const secpe_layout *layout, const sec
     });
 }
 int secpe_enc_argmax_boot(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n_in,
-                          const secpe_layout *layout, const secpe_sign_cfg *cfg, const secpe_boot *boot,
-                          double boot_scale, secpe_ct *out) {
+                          int32_t prompt_cts, const secpe_layout *layout, const secpe_sign_cfg *cfg,
+                          const secpe_boot *boot, double boot_scale, secpe_ct *out) {
     return guard([&] {
         REQUIRE(ctx && boot && boot->b && boot->b->fft, SECPE_EINVAL, "needs factorised bootstrap material");
-        argmax_boot_views(ctx->c, keys, in, n_in, layout, cfg, boot->b->fcfg, boot_scale, out);
+        argmax_boot_views(ctx->c, keys, in, n_in, layout, cfg, boot->b->fcfg, boot_scale, prompt_cts, out);
     });
 }
 int secpe_enc_argmax_boot_cfg(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n_in,
-                              const secpe_layout *layout, const secpe_sign_cfg *cfg, const secpe_boot_fft_cfg *bcfg,
-                              double boot_scale, secpe_ct *out) {
+                              int32_t prompt_cts, const secpe_layout *layout, const secpe_sign_cfg *cfg,
+                              const secpe_boot_fft_cfg *bcfg, double boot_scale, secpe_ct *out) {
     return guard([&] {
         REQUIRE(ctx, SECPE_EINVAL, "null argument");
-        argmax_boot_views(ctx->c, keys, in, n_in, layout, cfg, fft_cfg_of(ctx->c, bcfg), boot_scale, out);
+        argmax_boot_views(ctx->c, keys, in, n_in, layout, cfg, fft_cfg_of(ctx->c, bcfg), boot_scale, prompt_cts, out);
     });
 }
 int secpe_boot_create_fft(secpe_ctx *ctx, int32_t level, double K, int32_t r, const int32_t *groups,

@@ -271,7 +271,7 @@ struct SignCfg;
 struct Layout;
 int argmax_boot_level(const Layout &lay, const SignCfg &cfg, const FftBootCfg &b, int in_level);
 void run_argmax_boot(Ctx &c, const Keys &k, const CtView &in, const Layout &lay, const SignCfg &cfg,
-                     const FftBootCfg &b, double boot_scale, CtView &out);
+                     const FftBootCfg &b, double boot_scale, int prompt_cts, CtView &out);
 // library-built bootstrapping material (secpe_boot_create): the EvalMod polynomial and the four encoded
 // matrices, NTT form, [n2][n1][limbs][N] each
 struct BootSetup {

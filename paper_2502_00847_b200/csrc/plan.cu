@@ -356,16 +356,20 @@ struct Ev {
         Val r = bootstrap_fft(xs, b);
         return mul_const(r, 1.0, c.scale, r.level() - 1);
     }
-    Val argmax_boot(const Val &in, const Layout &lay, const SignCfg &cfg, const FftBootCfg &b, double boot_scale) {
-        const int P = lay.prompts, K = lay.classes;
-        Val y = in;
+    // ins: the prompt groups (prompt_cts ciphertexts per query set, summed first: PAPER.md:141 y* = sum y_i);
+    // the mask normalises by prompts x prompt_cts
+    Val argmax_boot(const std::vector<Val> &ins, const Layout &lay, const SignCfg &cfg, const FftBootCfg &b,
+                    double boot_scale) {
+        const int P = lay.prompts, K = lay.classes, pc = (int)ins.size();
+        Val y = ins[0];
+        for (int i = 1; i < pc; i++) y = add(y, ins[i]);
         for (int t = 0; (1 << t) < P; t++) y = rot_add(y, K << t);
         std::vector<double> mask(c.N / 2, 0.0);
         for (int qi = 0; qi < lay.queries; qi++)
-            for (int kk = 0; kk < K; kk++) mask[(size_t)qi * lay.block + kk] = 1.0 / P;
+            for (int kk = 0; kk < K; kk++) mask[(size_t)qi * lay.block + kk] = (1.0 / P) / pc;
         y = mul_mask(y, mask, c.scale,
                      "argmax/" + std::to_string(lay.queries) + "/" + std::to_string(P) + "/" + std::to_string(K) + "/" +
-                         std::to_string(lay.block));
+                         std::to_string(lay.block) + "/" + std::to_string(pc));
         y = rot_add(y, -K);
         Val ydup = y;
         const int sd = sign_depth(cfg);
@@ -462,9 +466,19 @@ int argmax_boot_level(const Layout &lay, const SignCfg &cfg, const FftBootCfg &b
 // the whole batch through one plan: every key (and every transform plaintext) is read once per op for all
 // in.n ciphertexts
 void run_argmax_boot(Ctx &c, const Keys &k, const CtView &in, const Layout &lay, const SignCfg &cfg,
-                     const FftBootCfg &b, double boot_scale, CtView &out) {
-    Ev ev{c, k, in.n};
-    Val r = ev.argmax_boot(Val{nullptr, in}, lay, cfg, b, boot_scale);
+                     const FftBootCfg &b, double boot_scale, int prompt_cts, CtView &out) {
+    if (prompt_cts < 1 || in.n % prompt_cts) throw SecpeError{-1, "argmax_boot: n_in must be a multiple of prompt_cts"};
+    const int B = in.n / prompt_cts;
+    Ev ev{c, k, B};
+    std::vector<Val> ins;
+    for (int i = 0; i < prompt_cts; i++) {  // member i of every group: ciphertexts i, i + pc, ...
+        CtView v = in;
+        v.data = in.data + (long)i * in.stride;
+        v.stride = in.stride * prompt_cts;
+        v.n = B;
+        ins.push_back(Val{nullptr, v});
+    }
+    Val r = ev.argmax_boot(ins, lay, cfg, b, boot_scale);
     out.level = r.level();
     out.scale = r.scale();
     ev_copy(c, r.v, out);

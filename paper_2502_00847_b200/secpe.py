@@ -117,11 +117,12 @@ SIGS = {
     "secpe_boot_steps": (ctypes.c_int32, [vp, i32p, ctypes.c_int32]),
     "secpe_argmax_boot_info": (ctypes.c_int, [vp, ctypes.POINTER(Layout), ctypes.POINTER(SignCfg), vp,
                                               ctypes.c_int32, i32p]),
-    "secpe_enc_argmax_boot": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.POINTER(Layout),
-                                             ctypes.POINTER(SignCfg), vp, ctypes.c_double, ctypes.POINTER(CCt)]),
-    "secpe_enc_argmax_boot_cfg": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.POINTER(Layout),
-                                                 ctypes.POINTER(SignCfg), ctypes.POINTER(CBootFftCfg),
-                                                 ctypes.c_double, ctypes.POINTER(CCt)]),
+    "secpe_enc_argmax_boot": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.c_int32,
+                                             ctypes.POINTER(Layout), ctypes.POINTER(SignCfg), vp, ctypes.c_double,
+                                             ctypes.POINTER(CCt)]),
+    "secpe_enc_argmax_boot_cfg": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.c_int32,
+                                                 ctypes.POINTER(Layout), ctypes.POINTER(SignCfg),
+                                                 ctypes.POINTER(CBootFftCfg), ctypes.c_double, ctypes.POINTER(CCt)]),
     "secpe_boot_stage_export": (ctypes.c_int, [vp, vp, ctypes.c_int32, ctypes.c_int32, i32p, i32p, u64p,
                                                ctypes.c_size_t]),
     "secpe_bootstrap": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.POINTER(CBootCfg), ctypes.POINTER(CCt)]),
@@ -569,28 +570,31 @@ class Context:
                           stage(stc_im))
         return cfg, keep
 
-    def enc_argmax_boot(self, keys, cts, lay, stages, boot, boot_scale, fft_cfg=None):
+    def enc_argmax_boot(self, keys, cts, lay, stages, boot, boot_scale, fft_cfg=None, prompt_cts=1):
         """secpe_enc_argmax_boot (N4, reading R38) with library-built material `boot`, or
-        secpe_enc_argmax_boot_cfg when fft_cfg = (level, K, r, poly, cts, cts_im, stc, stc_im) is given."""
+        secpe_enc_argmax_boot_cfg when fft_cfg = (level, K, r, poly, cts, cts_im, stc, stc_im) is given.
+        prompt_cts: consecutive groups of that many ciphertexts are one query set's prompt groups."""
         scfg, ly = sign_cfg(stages), layout(lay)
+        assert cts.n % prompt_cts == 0
+        n_out = cts.n // prompt_cts
         ol = ctypes.c_int32(0)
         if fft_cfg is None:
             _chk(lib().secpe_argmax_boot_info(self.h, ctypes.byref(ly), ctypes.byref(scfg), boot.h, cts.level,
                                               ctypes.byref(ol)))
         else:
             ol.value = 0
-        out = self.new_ct(max(ol.value, 0) if fft_cfg is None else cts.level, cts.n)
+        out = self.new_ct(max(ol.value, 0) if fft_cfg is None else cts.level, n_out)
         ins = (CCt * cts.n)(*[cts.c(i) for i in range(cts.n)])
-        outs = (CCt * cts.n)(*[CCt(ctypes.cast(out.t[i].data_ptr(), u64p), 0, 0.0) for i in range(cts.n)])
+        outs = (CCt * n_out)(*[CCt(ctypes.cast(out.t[i].data_ptr(), u64p), 0, 0.0) for i in range(n_out)])
         if fft_cfg is None:
-            _chk(lib().secpe_enc_argmax_boot(self.h, keys.h, ins, cts.n, ctypes.byref(ly), ctypes.byref(scfg),
-                                             boot.h, boot_scale, outs))
+            _chk(lib().secpe_enc_argmax_boot(self.h, keys.h, ins, cts.n, prompt_cts, ctypes.byref(ly),
+                                             ctypes.byref(scfg), boot.h, boot_scale, outs))
         else:
             bc, keep = self._fft_cfg(*fft_cfg)
-            _chk(lib().secpe_enc_argmax_boot_cfg(self.h, keys.h, ins, cts.n, ctypes.byref(ly), ctypes.byref(scfg),
-                                                 ctypes.byref(bc), boot_scale, outs))
+            _chk(lib().secpe_enc_argmax_boot_cfg(self.h, keys.h, ins, cts.n, prompt_cts, ctypes.byref(ly),
+                                                 ctypes.byref(scfg), ctypes.byref(bc), boot_scale, outs))
         out.level, out.scale = outs[0].level, outs[0].scale
-        n, N = cts.n, self.N
+        n, N = n_out, self.N
         # each output is written compactly ([2][level+1][N]) at the start of its slot
         out.t = out.t.reshape(n, -1)[:, : 2 * (out.level + 1) * N].reshape(n, 2, out.level + 1, N).contiguous()
         return out

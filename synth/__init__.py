@@ -70,6 +70,10 @@ LAYOUTS = {
     # SURVEY 8(f) N4 "n = 256 with 64 per ciphertext" (2n slots per argmax): 256 classes, 2 prompts
     "argmax_n256": dict(queries=64, prompts=2, classes=256, block=512),
     "boot_n256": dict(queries=4, prompts=2, classes=256, block=512),
+    # CLIP scale (80 / 247 prompts, 1000 classes padded to 1024): 2 prompts per
+    # ciphertext, the rest spread over several ciphertexts summed first (prompt_cts)
+    "clip": dict(queries=16, prompts=2, classes=1024, block=2048),
+    "boot_clip": dict(queries=1, prompts=2, classes=1024, block=2048),
 }
 
 KEY_SEED_BASE = 0x5EC9E000
@@ -83,6 +87,16 @@ def softmax_scores(seed, queries, prompts, classes, sigma=2.0):
     """Per-prompt class scores: logits ~ N(0, sigma) iid, softmax over classes. Shape (q, P, K)."""
     g = rng(seed)
     logits = g.normal(0.0, sigma, size=(queries, prompts, classes))
+    e = np.exp(logits - logits.max(axis=2, keepdims=True))
+    return e / e.sum(axis=2, keepdims=True)
+
+
+def ensemble_scores(seed, queries, prompts, classes, sigma_class=4.0, sigma_prompt=1.0):
+    """Prompt-ensemble scores with agreeing prompts (the CLIP setting): logits = a per-(query,
+    class) consensus ~ N(0, sigma_class) + per-prompt noise ~ N(0, sigma_prompt), softmax over classes."""
+    g = rng(seed)
+    base = g.normal(0.0, sigma_class, size=(queries, 1, classes))
+    logits = base + g.normal(0.0, sigma_prompt, size=(queries, prompts, classes))
     e = np.exp(logits - logits.max(axis=2, keepdims=True))
     return e / e.sum(axis=2, keepdims=True)
 

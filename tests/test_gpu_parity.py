@@ -1145,3 +1145,52 @@ def test_argmax_boot_n256_bit_exact(S):
     ok = srt[:, -1] - srt[:, -2] >= 2.0 ** -7
     assert ok.sum() >= 2
     assert (S.labels(g.decrypt(kg, got), lay)[ok] == plan.true_labels(scores)[ok]).all()
+
+
+def _pack_groups(scores, lay, n_slots, pc):
+    """Prompt groups: member i holds prompts i * P .. i * P + P - 1 of every query (same layout)."""
+    P = lay["prompts"]
+    return [plan.pack(scores[:, i * P:(i + 1) * P], lay, n_slots) for i in range(pc)]
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_argmax_boot_clip_prompt_groups_bit_exact(S):
+    """N4 CLIP scale: 1024 classes, 6 prompts spread over 3 ciphertexts (prompt_cts = 3)
+    summed first, ten bootstraps per query set; at N = 2^12 word for word the oracle's plan, label exact."""
+    P = pair(S, "boot_argmax")
+    prm, g = P.prm, P.gpu
+    ev = ckks.Oracle(prm)
+    lay = synth.LAYOUTS["boot_clip"]
+    pc = 3
+    st = load_sign("sign_7_15_15.json")
+    groups = [4, 4, 3]
+    rot = plan.argmax_rotations(lay) + plan.fft_boot_rotations(prm.N, groups, bsgs=True)
+    seed = synth.KEY_SEED_BASE + 43
+    ko, kg = ev.keygen(seed, rot, h=64), g.keygen(seed, rot, h=64)
+    bs = 2.0 ** 50
+    cfg = plan.fft_boot_config(ev, bs, prm.L, 16, 7, groups, bsgs=True)
+    scores = synth.softmax_scores(55, lay["queries"], lay["prompts"] * pc, lay["classes"], sigma=6.0)
+    cts = [ev.encrypt(ko, z, prm.scale, 60 + i, level=16) for i, z in enumerate(_pack_groups(scores, lay, prm.N // 2, pc))]
+    nb = [0]
+
+    def boot(c):
+        nb[0] += 1
+        return plan.bootstrap_fft(ev, ko, c, cfg)
+    ev.log.clear()
+    want = plan.argmax_boot(ev, ko, cts, lay, st, boot, bs, prompt_cts=pc)
+    olog = list(ev.log)
+    assert nb[0] == 10
+    fc = (cfg["level"], cfg["K"], cfg["r"], cfg["poly"], [_dev_stage(t) for t in cfg["cts"]],
+          _dev_stage(cfg["cts_im"]), [_dev_stage(t) for t in cfg["stc"]], _dev_stage(cfg["stc_im"]))
+    batch = S.Ct(torch.from_numpy(np.stack([c.data for c in cts])).cuda(), 16, prm.scale)
+    g.oplog(enable=True, clear=True)
+    got = g.enc_argmax_boot(kg, batch, lay, st, None, bs, fft_cfg=fc, prompt_cts=pc)
+    glog = g.oplog(enable=False, clear=True)
+    assert glog == olog
+    assert got.n == 1 and got.level == want.level and got.scale == want.scale
+    assert np.array_equal(P.down(got), want.data)
+    mean = scores.mean(axis=1)
+    srt = np.sort(mean, axis=1)
+    assert srt[0, -1] - srt[0, -2] >= 2.0 ** -7
+    assert S.labels(g.decrypt(kg, got), lay)[0] == plan.true_labels(scores)[0]

@@ -31,6 +31,7 @@ def main():
     for B in [int(b) for b in os.environ.get("SECPE_N4_BATCHES", "8").split(",")]:
         print(json.dumps(bench.argmax_k16_bench(stream, t_ms, B)))
     print(json.dumps(bench.argmax_boot_bench(stream, t_ms, "argmax_n256", 8, 6.0)))
+    print(json.dumps(bench.clip_bench(stream, t_ms)))
 
 
 if __name__ == "__main__":
