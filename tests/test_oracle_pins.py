@@ -901,3 +901,25 @@ def test_bootstrap_fft_bsgs_refreshes():
     out = plan.bootstrap_fft(ev, keys, ct, cfg)
     assert out.level == prm.L - plan.fft_boot_depth(groups, r)
     assert np.abs(ev.decrypt(keys, out).real - z).max() < 2 ** -14
+
+
+def test_argmax_boot_prompt_groups_equal_one_ciphertext():
+    """N4 prompt groups (PAPER.md:141 y* = sum y_i across ciphertexts): splitting 8 prompts into two ciphertexts
+    of 4 (prompt_cts = 2) decrypts to the same one-hot as the true label of the mean over all 8 prompts."""
+    prm = ckks.Params(synth.PARAM_SETS["boot_argmax_tiny"])
+    ev = ckks.Oracle(prm)
+    lay = dict(queries=1, prompts=4, classes=16, block=128)
+    d = json.load(open(os.path.join(os.path.dirname(__file__), "..", "data", "sign_7_15_15.json")))
+    st = [list(map(float, c)) for c in d["coeffs"]]
+    groups = [4, 3]
+    keys = ev.keygen(13, plan.argmax_rotations(lay) + plan.fft_boot_rotations(prm.N, groups, bsgs=True), h=64)
+    cfg = plan.fft_boot_config(ev, 2.0 ** 50, prm.L, 16, 7, groups, bsgs=True)
+    scores = synth.ensemble_scores(7, 1, 8, 16)
+    cts = [ev.encrypt(keys, plan.pack(scores[:, 4 * i:4 * i + 4], lay, prm.N // 2), prm.scale, 20 + i, level=16)
+           for i in range(2)]
+    out = plan.argmax_boot(ev, keys, cts, lay, st, lambda c: plan.bootstrap_fft(ev, keys, c, cfg), 2.0 ** 50,
+                           prompt_cts=2)
+    dec = ev.decrypt(keys, out).real[:16]
+    want = np.zeros(16)
+    want[plan.true_labels(scores)[0]] = 1.0
+    assert np.abs(dec - want).max() < 2 ** -5
