@@ -1194,3 +1194,33 @@ def test_argmax_boot_clip_prompt_groups_bit_exact(S):
     srt = np.sort(mean, axis=1)
     assert srt[0, -1] - srt[0, -2] >= 2.0 ** -7
     assert S.labels(g.decrypt(kg, got), lay)[0] == plan.true_labels(scores)[0]
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_bootstrap_n16_bit_exact(S):
+    """N3 at full size (N = 2^16, 32768 slots, groups 5/5/5 in baby-step giant-step form, 39 Galois keys): the
+    GPU bootstrap with the oracle's encoded material is word for word the oracle's (about two minutes of oracle
+    time), same op list, refresh within 2^-11."""
+    P = pair(S, "boot16")
+    prm, g = P.prm, P.gpu
+    ev = ckks.Oracle(prm)
+    groups = [5, 5, 5]
+    rot = plan.fft_boot_rotations(prm.N, groups, bsgs=True)
+    seed = synth.KEY_SEED_BASE + 47
+    ko, kg = ev.keygen(seed, rot, h=64), g.keygen(seed, rot, h=64)
+    z = np.random.default_rng(21).uniform(-1, 1, prm.N // 2)
+    ct = ev.encrypt(ko, z, prm.scale, 71, level=0)
+    cfg = plan.fft_boot_config(ev, prm.scale, prm.L, 16, 7, groups, bsgs=True)
+    ev.log.clear()
+    want = plan.bootstrap_fft(ev, ko, ct, cfg)
+    olog = list(ev.log)
+    g.oplog(enable=True, clear=True)
+    got = g.bootstrap_fft(kg, P.up(ct), cfg["level"], cfg["K"], cfg["r"], cfg["poly"],
+                          [_dev_stage(t) for t in cfg["cts"]], _dev_stage(cfg["cts_im"]),
+                          [_dev_stage(t) for t in cfg["stc"]], _dev_stage(cfg["stc_im"]))
+    glog = g.oplog(enable=False, clear=True)
+    assert glog == olog
+    assert got.level == want.level and got.scale == want.scale
+    assert np.array_equal(P.down(got), want.data)
+    assert np.abs(g.decrypt(kg, got) - z).max() < 2 ** -11
