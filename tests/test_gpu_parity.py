@@ -1224,3 +1224,43 @@ def test_bootstrap_n16_bit_exact(S):
     assert got.level == want.level and got.scale == want.scale
     assert np.array_equal(P.down(got), want.data)
     assert np.abs(g.decrypt(kg, got) - z).max() < 2 ** -11
+
+
+@pytest.mark.gpu
+def test_bootstrap_api_errors(S):
+    """Argument checks of the bootstrapping entry points: stage groups that do not cover log2(N/2), a
+    non-level-0 input, a missing Galois key, prompt groups that do not divide the batch, too few levels."""
+    P = pair(S, "boot")
+    g = P.gpu
+    with pytest.raises(S.SecpeError):
+        g.boot_create_fft(g.L, 16, 7, [4, 4], g.scale, bsgs=True)      # 8 of 11 stages
+    with pytest.raises(S.SecpeError):
+        g.boot_create_fft(g.L, 16, 7, [4, 4, 3, 0], g.scale)           # empty group
+    with pytest.raises(S.SecpeError):
+        g.boot_create_fft(10, 16, 7, [4, 4, 3], g.scale)               # depth 19 > level 10
+    with pytest.raises(S.SecpeError):
+        g.boot_create(g.L, 16, 7, 64, 16, g.scale)                      # n1 n2 != N/2
+    b = g.boot_create_fft(g.L, 16, 7, [4, 4, 3], g.scale, bsgs=True)
+    steps = b.steps()
+    assert steps[-1] == S.CONJ and len(set(steps)) == len(steps)
+    kg = g.keygen(3, steps, h=64)
+    z = np.zeros(g.N // 2)
+    with pytest.raises(S.SecpeError):
+        g.bootstrap_boot(kg, g.encrypt(kg, z, 1, g.scale, 1), b)        # level 1, not 0
+    with pytest.raises(S.SecpeError):
+        g.bootstrap_boot(g.keygen(3, steps[:-1], h=64), g.encrypt(kg, z, 0, g.scale, 2), b)  # no conj key
+    out = g.bootstrap_boot(kg, g.encrypt(kg, z, 0, g.scale, 3), b)
+    assert out.level == g.L - (2 * 3 + 6 + 7)
+    lay = synth.LAYOUTS["boot_k16"]
+    st = load_sign("sign_7_15_15.json")
+    two = S.Ct(torch.cat([g.encrypt(kg, z, 16, g.scale, 4).t] * 3), 16, g.scale)
+    with pytest.raises((S.SecpeError, AssertionError)):
+        g.enc_argmax_boot(kg, two, lay, st, b, 2.0 ** 50, prompt_cts=2)   # 3 ciphertexts, groups of 2
+
+
+def test_bsgs_split_rejects_gaps():
+    """R39's split needs a contiguous progression of offsets (every merged special-FFT group has one)."""
+    n = 64
+    D = {0: np.ones(n), 2: np.ones(n), 6: np.ones(n)}
+    with pytest.raises(ValueError):
+        plan.bsgs_split(D, n)
