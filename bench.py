@@ -250,7 +250,7 @@ def bootstrap_bench(stream, t_ms):
     del boot, keys, res, c0, ctx
     # the paper's ring: factorised special-FFT transforms (R37), groups 5/5/5
     ctx = secpe.Context(synth.PARAM_SETS["boot16"], stream=stream.cuda_stream)
-    groups = [5, 5, 5]
+    groups = [4, 5, 6]
     t0 = time.time()
     boot = ctx.boot_create_fft(ctx.L, K, r, groups, ctx.scale, bsgs=True)
     torch.cuda.synchronize()
@@ -285,7 +285,7 @@ def bootstrap_bench(stream, t_ms):
     out["N=2^16_fft"] = {"breakdown": breakdown, "ms_per_bootstrap": ms, "logn": ctx.logn, "slots": ctx.N // 2, "level_in": 0,
                          "raised_to": ctx.L, "level_out": res[0].level, "galois_keys": len(steps),
                          "max_abs_err": err, "setup_s": setup_s,
-                         "transforms": "special-FFT groups 5/5/5, baby-step giant-step form (R37, R39)"}
+                         "transforms": "special-FFT groups 4/5/6, baby-step giant-step form (R37, R39)"}
     return out
 
 
@@ -300,7 +300,7 @@ def clip_bench(stream, t_ms, G=2, prompts=80, classes=1000):
     lay = synth.LAYOUTS["clip"]
     st = load_sign("sign_7_15_15.json")
     bs = 2.0 ** 50
-    boot = ctx.boot_create_fft(ctx.L, 16, 7, [5, 5, 5], bs, bsgs=True)
+    boot = ctx.boot_create_fft(ctx.L, 16, 7, [4, 5, 6], bs, bsgs=True)
     P, K, Q, blk = lay["prompts"], lay["classes"], lay["queries"], lay["block"]
     pc = prompts // P
     rot = [K << t for t in range(P.bit_length() - 1)] + [-K] + [1 << i for i in range(K.bit_length() - 1)]
@@ -352,7 +352,7 @@ def argmax_boot_bench(stream, t_ms, lname, B, sigma):
     lay = synth.LAYOUTS[lname]
     st = load_sign("sign_7_15_15.json")
     bs = 2.0 ** 50
-    boot = ctx.boot_create_fft(ctx.L, 16, 7, [5, 5, 5], bs, bsgs=True)
+    boot = ctx.boot_create_fft(ctx.L, 16, 7, [4, 5, 6], bs, bsgs=True)
     P, K = lay["prompts"], lay["classes"]
     rot = [K << t for t in range(P.bit_length() - 1)] + [-K] + [1 << i for i in range(K.bit_length() - 1)]
     keys = ctx.keygen(synth.KEY_SEED_BASE + 39, sorted(set(rot)) + boot.steps(), h=64)
