@@ -296,11 +296,11 @@ def clip_bench(stream, t_ms, G=2, prompts=80, classes=1000):
     import torch
     import synth
     from paper_2502_00847_b200 import secpe
-    ctx = secpe.Context(synth.PARAM_SETS["boot_argmax16"], stream=stream.cuda_stream)
+    ctx = secpe.Context(synth.PARAM_SETS["boot_argmax16_g4"], stream=stream.cuda_stream)
     lay = synth.LAYOUTS["clip"]
     st = load_sign("sign_7_15_15.json")
     bs = 2.0 ** 50
-    boot = ctx.boot_create_fft(ctx.L, 16, 7, [4, 5, 6], bs, bsgs=True)
+    boot = ctx.boot_create_fft(ctx.L, 16, 7, [3, 4, 4, 4], bs, bsgs=True)
     P, K, Q, blk = lay["prompts"], lay["classes"], lay["queries"], lay["block"]
     pc = prompts // P
     rot = [K << t for t in range(P.bit_length() - 1)] + [-K] + [1 << i for i in range(K.bit_length() - 1)]
@@ -341,18 +341,18 @@ def argmax_k16_bench(stream, t_ms, B=8):
     return argmax_boot_bench(stream, t_ms, "argmax_k16", B, 2.0)
 
 
-def argmax_boot_bench(stream, t_ms, lname, B, sigma):
+def argmax_boot_bench(stream, t_ms, lname, B, sigma, pname="boot_argmax16_g4", groups=(3, 4, 4, 4)):
     """SURVEY 8(f) N4 (reading R38): Algorithm 1 with K = 16 classes at N = 2^16 (256 queries x 8 prompts per
     ciphertext), refreshed by four factorised bootstraps per ciphertext (secpe_enc_argmax_boot); one
     ciphertext per call, CUDA events, median.  Labels checked against the plaintext argmax above the margin."""
     import torch
     import synth
     from paper_2502_00847_b200 import secpe
-    ctx = secpe.Context(synth.PARAM_SETS["boot_argmax16"], stream=stream.cuda_stream)
+    ctx = secpe.Context(synth.PARAM_SETS[pname], stream=stream.cuda_stream)
     lay = synth.LAYOUTS[lname]
     st = load_sign("sign_7_15_15.json")
     bs = 2.0 ** 50
-    boot = ctx.boot_create_fft(ctx.L, 16, 7, [4, 5, 6], bs, bsgs=True)
+    boot = ctx.boot_create_fft(ctx.L, 16, 7, list(groups), bs, bsgs=True)
     P, K = lay["prompts"], lay["classes"]
     rot = [K << t for t in range(P.bit_length() - 1)] + [-K] + [1 << i for i in range(K.bit_length() - 1)]
     keys = ctx.keygen(synth.KEY_SEED_BASE + 39, sorted(set(rot)) + boot.steps(), h=64)
@@ -384,7 +384,7 @@ def argmax_boot_bench(stream, t_ms, lname, B, sigma):
             "prompts": P, "query_argmax_per_s": B * lay["queries"] / (ms / 1000),
             "bootstraps_per_ciphertext": K.bit_length() - 1, "logit_sigma": sigma,
             "labels_exact_above_margin": good / tot, "in_margin_fraction": inm / (B * lay["queries"]),
-            "logn": ctx.logn, "chain": "q0 60 + 16 x 45 + 19 x 50 bit"}
+            "logn": ctx.logn, "chain": pname + ": q0 60 + 16 x 45 + 21 x 50 bit", "groups": list(groups)}
 
 def run_secpe(a):
     import torch

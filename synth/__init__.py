@@ -44,6 +44,9 @@ PARAM_SETS = {
                         p=[("below", 60, 7)], alpha=7, log_scale=45),
     "boot_argmax16": dict(logn=16, q=[("below", 60, 1), ("nearest", 45, 16), ("nearest", 50, 19)],
                           p=[("below", 60, 7)], alpha=7, log_scale=45),
+    # the same with two more bootstrap levels, for four stage groups (3/4/4/4: fewer key switches per group)
+    "boot_argmax16_g4": dict(logn=16, q=[("below", 60, 1), ("nearest", 45, 16), ("nearest", 50, 21)],
+                             p=[("below", 60, 7)], alpha=7, log_scale=45),
     # the paper's ring (N = 2^16, 32768 slots) with the factorised transforms (R37, groups 5/5/5: depth 20)
     "boot16": dict(logn=16, q=[("below", 60, 1), ("nearest", 50, 22)], p=[("below", 60, 7)],
                    alpha=7, log_scale=50),
