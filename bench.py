@@ -261,10 +261,10 @@ def bootstrap_bench(stream, t_ms):
     c0 = ctx.new_ct(0)
     ctx.encrypt_coeffs(keys, ctx.encode(z, ctx.scale), 0, ctx.scale, 78, out=c0)
     c0.level, c0.scale = 0, ctx.scale
-    res = [None]
+    res = [ctx.new_ct(ctx.L - (2 * len(groups) + 6 + r))]  # one output buffer: the call replays a CUDA graph
 
     def one16():
-        res[0] = ctx.bootstrap_boot(keys, c0, boot)
+        res[0] = ctx.bootstrap_boot(keys, c0, boot, out=res[0])
     ms = t_ms(one16)
     err = float(abs(ctx.decrypt(keys, res[0]) - z).max())
     # where one bootstrap's time goes (the library's CUDA-event profiler, one extra untimed call)

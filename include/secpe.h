@@ -268,6 +268,8 @@ typedef struct secpe_boot secpe_boot;
 int secpe_boot_create(secpe_ctx *ctx, int32_t level, double K, int32_t r, int32_t n1, int32_t n2, double in_scale,
                       secpe_boot **out);
 int secpe_boot_get_cfg(const secpe_boot *boot, secpe_boot_cfg *cfg);
+/* Synchronises the owning context's stream and drops the CUDA graphs that read the material; may run
+ * before or after the context's destruction; null is a no-op. */
 void secpe_boot_destroy(secpe_boot *boot);
 /* Copy matrix `which` (0 cts_re, 1 cts_im, 2 stc_re, 3 stc_im) to host uint64[n2][n1][limbs][N], for
  * parity tests (synchronises); n_words must equal that size. */
@@ -313,7 +315,11 @@ int secpe_bootstrap_fft(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *
  * giant-step form (R39: n1 = the power of two >= sqrt(#diagonals) baby steps, about as many giant steps). */
 int secpe_boot_create_fft(secpe_ctx *ctx, int32_t level, double K, int32_t r, const int32_t *groups,
                           int32_t n_groups, double in_scale, int32_t bsgs, secpe_boot **out);
-/* Bootstrap with library-built material of either kind; out->data sized for level - secpe_boot_levels. */
+/* Bootstrap with library-built material of either kind; out->data sized for level - secpe_boot_levels.
+ * Factorised material on a non-default context stream: the call is captured as a CUDA graph the second
+ * time the same (in, out, scale, material, keys) are seen and replayed afterwards (as secpe_enc_argmax);
+ * secpe_boot_destroy and secpe_keys_destroy drop such graphs.  secpe_enc_argmax_boot does the same on
+ * unstaged (contiguous) input and output batches. */
 int secpe_bootstrap_boot(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const secpe_boot *boot,
                          secpe_ct *out);
 /* Rotation steps (SECPE_CONJ included) whose Galois keys a library-built bootstrap needs, ascending with

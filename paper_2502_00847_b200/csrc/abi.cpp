@@ -101,6 +101,75 @@ static void set_out(secpe_ct *out, const CtView &v) {
     out->level = v.level;
     out->scale = v.scale;
 }
+// CUDA-graph cache around a data-independent plan `run` writing vout: replay the graph captured for `key`
+// if there is one, else run eagerly and capture on the key's second sighting (a caller allocating fresh
+// buffers every call would otherwise pay a capture per call); at most kMaxGraphs graphs, oldest evicted.
+// keys / aux: library-owned device memory the kernels read (destroying it drops the graph).
+template <class F>
+static void graphed(Ctx &c, bool graphable, const std::string &key, const void *keys, const void *aux, CtView &vout,
+                    F run) {
+    graphable = graphable && c.use_graphs && !c.log_on && !c.prof.on && c.st != nullptr && c.st != cudaStreamLegacy &&
+                c.st != cudaStreamPerThread;
+    auto git = graphable ? c.graphs.find(key) : c.graphs.end();
+    if (git != c.graphs.end() && git->second.exec) {
+        CUDA_CHECK(cudaGraphLaunch(git->second.exec, c.st));
+        const Counters &d = git->second.cnt;
+        c.cnt.ntt_limbs += d.ntt_limbs, c.cnt.keyswitch += d.keyswitch, c.cnt.rescale += d.rescale;
+        c.cnt.rotate += d.rotate, c.cnt.mulct += d.mulct, c.cnt.mulconst += d.mulconst;
+        c.cnt.launches += d.launches, c.cnt.sign += d.sign;
+        vout.scale = git->second.out_scale;
+        return;
+    }
+    run();
+    if (!graphable) return;
+    if (++c.graph_seen[key] < 2) {
+        if (c.graph_seen.size() > 4 * Ctx::kMaxGraphs) c.graph_seen.clear();
+        return;
+    }
+    if ((int)c.graphs.size() >= Ctx::kMaxGraphs && !c.graph_order.empty()) {
+        CUDA_CHECK(cudaStreamSynchronize(c.st));  // the evicted graph may still be running
+        auto old = c.graphs.find(c.graph_order.front());
+        if (old != c.graphs.end()) {
+            if (old->second.exec) cudaGraphExecDestroy(old->second.exec);
+            c.graphs.erase(old);
+        }
+        c.graph_order.erase(c.graph_order.begin());
+    }
+    const Counters before = c.cnt;
+    cudaGraph_t graph;
+    CUDA_CHECK(cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal));
+    try {
+        run();
+    } catch (...) {
+        cudaStreamEndCapture(c.st, &graph);
+        throw;
+    }
+    CUDA_CHECK(cudaStreamEndCapture(c.st, &graph));
+    Ctx::Graph G;
+    CUDA_CHECK(cudaGraphInstantiate(&G.exec, graph, 0));
+    CUDA_CHECK(cudaGraphDestroy(graph));
+    CUDA_CHECK(cudaGraphUpload(G.exec, c.st));  // pay the one-time upload now, not on the first replay
+    G.keys = keys;
+    G.aux = aux;
+    G.cnt.ntt_limbs = c.cnt.ntt_limbs - before.ntt_limbs;
+    G.cnt.keyswitch = c.cnt.keyswitch - before.keyswitch;
+    G.cnt.rescale = c.cnt.rescale - before.rescale;
+    G.cnt.rotate = c.cnt.rotate - before.rotate;
+    G.cnt.mulct = c.cnt.mulct - before.mulct;
+    G.cnt.mulconst = c.cnt.mulconst - before.mulconst;
+    G.cnt.launches = c.cnt.launches - before.launches;
+    G.cnt.sign = c.cnt.sign - before.sign;
+    c.cnt = before;  // the capture executed nothing
+    G.out_scale = vout.scale;
+    c.graphs[key] = G;
+    c.graph_order.push_back(key);
+    c.graph_seen.erase(key);
+}
+static std::string dkey(double x) {
+    u64 b;
+    std::memcpy(&b, &x, 8);
+    return std::to_string(b);
+}
 static SignCfg sign_cfg(const secpe_sign_cfg *cfg) {
     REQUIRE(cfg && cfg->n_stages > 0 && cfg->degrees && cfg->coeffs, SECPE_EINVAL, "bad sign config");
     SignCfg s;
@@ -515,6 +584,7 @@ int secpe_boot_create(secpe_ctx *ctx, int32_t level, double K, int32_t r, int32_
         REQUIRE(ctx && out && in_scale > 0, SECPE_EINVAL, "null argument");
         auto h = std::make_unique<secpe_boot>();
         h->b.reset(boot_setup(ctx->c, level, K, r, n1, n2, in_scale));
+        ctx->c.live_boots.insert(h->b.get());
         *out = h.release();
     });
 }
@@ -527,7 +597,17 @@ int secpe_boot_get_cfg(const secpe_boot *boot, secpe_boot_cfg *cfg) {
                               b.stc_re, b.stc_im, b.stc_scale};
     });
 }
-void secpe_boot_destroy(secpe_boot *boot) { delete boot; }
+// Synchronises the owning context's stream and drops every CUDA graph that reads this material.
+void secpe_boot_destroy(secpe_boot *boot) {
+    if (!boot) return;
+    if (boot->b && boot->b->ctx) {
+        Ctx &c = *boot->b->ctx;
+        if (c.st) cudaStreamSynchronize(c.st);
+        c.drop_graphs(boot->b.get());
+        c.live_boots.erase(boot->b.get());
+    }
+    delete boot;
+}
 int secpe_boot_export(secpe_ctx *ctx, const secpe_boot *boot, int32_t which, uint64_t *host_out, size_t n_words) {
     return guard([&] {
         REQUIRE(ctx && boot && boot->b && host_out && which >= 0 && which < 4, SECPE_EINVAL, "bad argument");
@@ -567,14 +647,18 @@ static void check_fft_keys(const Ctx &c, const secpe_keys *keys, const FftBootCf
     REQUIRE(keys->k->gk.count(galois_elt(c, kConjStep)), SECPE_ENOKEY, "no conjugation key");
 }
 static void bootstrap_fft_views(Ctx &c, const secpe_keys *keys, const secpe_ct *in, const FftBootCfg &b,
-                                secpe_ct *out) {
+                                secpe_ct *out, const void *material = nullptr) {
     REQUIRE(b.level < c.nq && b.level - fft_boot_depth(b) >= 0, SECPE_ELEVEL, "not enough levels for a bootstrap");
     CtView vi = view_of(c, in);
     REQUIRE(vi.level == 0, SECPE_EINVAL, "bootstrap takes a level-0 ciphertext");
     REQUIRE(out->data != in->data, SECPE_EINVAL, "out must not alias in");
     check_fft_keys(c, keys, b);
     CtView vo = compact_view(c, out->data, 1, b.level - fft_boot_depth(b), 0.0);
-    run_bootstrap_fft(c, *keys->k, vi, b, vo);
+    // library-built material (stable device memory): CUDA graph as secpe_enc_argmax
+    char k[192];
+    snprintf(k, sizeof k, "boot/%p/%p/%s/%p/%p", (void *)vi.data, (void *)vo.data, dkey(vi.scale).c_str(), material,
+             (const void *)keys);
+    graphed(c, material != nullptr, k, keys, material, vo, [&] { run_bootstrap_fft(c, *keys->k, vi, b, vo); });
     set_out(out, vo);
 }
 static FftBootCfg fft_cfg_of(const Ctx &c, const secpe_boot_fft_cfg *cfg) {
@@ -602,7 +686,7 @@ int secpe_bootstrap_fft(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *
 // N4 (R38): argmax with bootstrapping, one ciphertext after another
 static void argmax_boot_views(Ctx &c, const secpe_keys *keys, const secpe_ct *in, int n_in, const secpe_layout *layout,
                               const secpe_sign_cfg *scfg, const FftBootCfg &b, double boot_scale, int prompt_cts,
-                              secpe_ct *out) {
+                              secpe_ct *out, const void *material = nullptr) {
     REQUIRE(keys && in && out && n_in >= 1 && boot_scale > 0, SECPE_EINVAL, "null argument");
     REQUIRE(prompt_cts >= 1 && n_in % prompt_cts == 0, SECPE_EINVAL, "n_in must be a multiple of prompt_cts");
     Layout lay = layout_of(c, layout);
@@ -615,7 +699,16 @@ static void argmax_boot_views(Ctx &c, const secpe_keys *keys, const secpe_ct *in
         for (int j = 0; j < n_in; j++) REQUIRE(out[i].data != in[j].data, SECPE_EINVAL, "out must not alias in");
     const int ol = argmax_boot_level(lay, sc, b, vin.level);
     CtView vout = batch_out(c, out, n_out, ol, c.scale, outb);
-    run_argmax_boot(c, *keys->k, vin, lay, sc, b, boot_scale, prompt_cts, vout);
+    char k[256];
+    snprintf(k, sizeof k, "argmax_boot/%p/%p/%d/%d/%d/%s/%d/%d/%d/%d/%s/%p/%p/", (void *)vin.data, (void *)vout.data,
+             n_in, prompt_cts, vin.level, dkey(vin.scale).c_str(), lay.queries, lay.prompts, lay.classes, lay.block,
+             dkey(boot_scale).c_str(), material, (const void *)keys);
+    std::string key = k;
+    for (auto &stg : sc.stages)
+        for (double x : stg) key += dkey(x) + ",";
+    // graphable only on the caller's own (unstaged) buffers and library-built material
+    graphed(c, material != nullptr && !inb.p && !outb.p, key, keys, material, vout,
+            [&] { run_argmax_boot(c, *keys->k, vin, lay, sc, b, boot_scale, prompt_cts, vout); });
     batch_out_finish(c, out, n_out, vout, outb);
 }
 int secpe_argmax_boot_info(secpe_ctx *ctx, const secpe_layout *layout, const secpe_sign_cfg *cfg,
@@ -630,7 +723,8 @@ int secpe_enc_argmax_boot(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct
                           const secpe_boot *boot, double boot_scale, secpe_ct *out) {
     return guard([&] {
         REQUIRE(ctx && boot && boot->b && boot->b->fft, SECPE_EINVAL, "needs factorised bootstrap material");
-        argmax_boot_views(ctx->c, keys, in, n_in, layout, cfg, boot->b->fcfg, boot_scale, prompt_cts, out);
+        argmax_boot_views(ctx->c, keys, in, n_in, layout, cfg, boot->b->fcfg, boot_scale, prompt_cts, out,
+                          boot->b.get());
     });
 }
 int secpe_enc_argmax_boot_cfg(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n_in,
@@ -648,6 +742,7 @@ int secpe_boot_create_fft(secpe_ctx *ctx, int32_t level, double K, int32_t r, co
         auto h = std::make_unique<secpe_boot>();
         h->b.reset(boot_setup_fft(ctx->c, level, K, r, std::vector<int>(groups, groups + n_groups), in_scale,
                                   bsgs != 0));
+        ctx->c.live_boots.insert(h->b.get());
         *out = h.release();
     });
 }
@@ -689,7 +784,7 @@ int secpe_bootstrap_boot(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct 
     }
     return guard([&] {
         REQUIRE(ctx && keys && in && out && out->data && boot && boot->b, SECPE_EINVAL, "null argument");
-        bootstrap_fft_views(ctx->c, keys, in, boot->b->fcfg, out);
+        bootstrap_fft_views(ctx->c, keys, in, boot->b->fcfg, out, boot->b.get());
     });
 }
 static const LtStage &boot_stage(const FftBootCfg &f, int kind, int idx, int &lv) {
@@ -837,79 +932,13 @@ int secpe_argmax_info(secpe_ctx *ctx, const secpe_layout *layout, const secpe_si
 // fills the mask cache); the legacy / per-thread default streams cannot be captured: eager there.
 static void argmax_views(Ctx &c, const secpe_keys *keys, const CtView &vin, const Layout &lay, const SignCfg &sc,
                          CtView &vout, bool buffers_fixed) {
-    const bool graphable = c.use_graphs && buffers_fixed && !c.log_on && !c.prof.on && c.st != nullptr &&
-                           c.st != cudaStreamLegacy && c.st != cudaStreamPerThread;
-    std::string key;
-    if (graphable) {
-        char b[256];
-        u64 sb;
-        std::memcpy(&sb, &vin.scale, 8);
-        snprintf(b, sizeof b, "%p/%p/%d/%d/%016llx/%d/%d/%d/%d/%p/", (void *)vin.data, (void *)vout.data, vin.n,
-                 vin.level, (unsigned long long)sb, lay.queries, lay.prompts, lay.classes, lay.block,
-                 (const void *)keys);
-        key = b;
-        for (auto &stg : sc.stages)
-            for (double x : stg) {
-                u64 xb;
-                std::memcpy(&xb, &x, 8);
-                key += std::to_string(xb) + ",";
-            }
-    }
-    auto git = graphable ? c.graphs.find(key) : c.graphs.end();
-    if (git != c.graphs.end() && git->second.exec) {
-        CUDA_CHECK(cudaGraphLaunch(git->second.exec, c.st));
-        const Counters &d = git->second.cnt;
-        c.cnt.ntt_limbs += d.ntt_limbs, c.cnt.keyswitch += d.keyswitch, c.cnt.rescale += d.rescale;
-        c.cnt.rotate += d.rotate, c.cnt.mulct += d.mulct, c.cnt.mulconst += d.mulconst;
-        c.cnt.launches += d.launches, c.cnt.sign += d.sign;
-        vout.scale = git->second.out_scale;
-        return;
-    }
-    run_argmax(c, *keys->k, vin, lay, sc, vout);
-    if (!graphable) return;
-    // capture only buffers seen twice (a caller allocating fresh buffers every call would otherwise pay a
-    // capture per call and grow the cache); keep at most kMaxGraphs graphs
-    if (++c.graph_seen[key] < 2) {
-        if (c.graph_seen.size() > 4 * Ctx::kMaxGraphs) c.graph_seen.clear();
-        return;
-    }
-    if ((int)c.graphs.size() >= Ctx::kMaxGraphs && !c.graph_order.empty()) {
-        CUDA_CHECK(cudaStreamSynchronize(c.st));  // the evicted graph may still be running
-        auto old = c.graphs.find(c.graph_order.front());
-        if (old != c.graphs.end()) {
-            if (old->second.exec) cudaGraphExecDestroy(old->second.exec);
-            c.graphs.erase(old);
-        }
-        c.graph_order.erase(c.graph_order.begin());
-    }
-    const Counters before = c.cnt;
-    cudaGraph_t graph;
-    CUDA_CHECK(cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal));
-    try {
-        run_argmax(c, *keys->k, vin, lay, sc, vout);
-    } catch (...) {
-        cudaStreamEndCapture(c.st, &graph);
-        throw;
-    }
-    CUDA_CHECK(cudaStreamEndCapture(c.st, &graph));
-    Ctx::Graph G;
-    CUDA_CHECK(cudaGraphInstantiate(&G.exec, graph, 0));
-    CUDA_CHECK(cudaGraphDestroy(graph));
-    CUDA_CHECK(cudaGraphUpload(G.exec, c.st));  // pay the one-time upload now, not on the first replay
-    G.keys = keys;
-    G.cnt.ntt_limbs = c.cnt.ntt_limbs - before.ntt_limbs;
-    G.cnt.keyswitch = c.cnt.keyswitch - before.keyswitch;
-    G.cnt.rescale = c.cnt.rescale - before.rescale;
-    G.cnt.rotate = c.cnt.rotate - before.rotate;
-    G.cnt.mulct = c.cnt.mulct - before.mulct;
-    G.cnt.mulconst = c.cnt.mulconst - before.mulconst;
-    G.cnt.launches = c.cnt.launches - before.launches;
-    G.cnt.sign = c.cnt.sign - before.sign;
-    c.cnt = before;  // the capture executed nothing
-    G.out_scale = vout.scale;
-    c.graphs[key] = G;
-    c.graph_order.push_back(key);
-    c.graph_seen.erase(key);
+    char b[256];
+    snprintf(b, sizeof b, "%p/%p/%d/%d/%s/%d/%d/%d/%d/%p/", (void *)vin.data, (void *)vout.data, vin.n, vin.level,
+             dkey(vin.scale).c_str(), lay.queries, lay.prompts, lay.classes, lay.block, (const void *)keys);
+    std::string key = b;
+    for (auto &stg : sc.stages)
+        for (double x : stg) key += dkey(x) + ",";
+    graphed(c, buffers_fixed, key, keys, nullptr, vout, [&] { run_argmax(c, *keys->k, vin, lay, sc, vout); });
 }
 
 int secpe_enc_argmax(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n_in,

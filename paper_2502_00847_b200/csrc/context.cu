@@ -345,7 +345,7 @@ void Ctx::build_tc_groups(LevelConsts &lc, int l) {
 // ---------------------------------------------------------------------------------------------
 void Ctx::drop_graphs(const void *keys) {
     for (auto it = graphs.begin(); it != graphs.end();) {
-        if (it->second.keys == keys) {
+        if (it->second.keys == keys || it->second.aux == keys) {
             if (it->second.exec) cudaGraphExecDestroy(it->second.exec);
             graph_order.erase(std::remove(graph_order.begin(), graph_order.end(), it->first), graph_order.end());
             it = graphs.erase(it);
@@ -357,6 +357,7 @@ void Ctx::drop_graphs(const void *keys) {
 
 Ctx::~Ctx() {
     for (Keys *k : live_keys) k->owner = nullptr;  // keys may outlive the context
+    for (BootSetup *b : live_boots) b->ctx = nullptr;
     if (st) cudaStreamSynchronize(st);
     for (auto &g : graphs)
         if (g.second.exec) cudaGraphExecDestroy(g.second.exec);

@@ -11,6 +11,8 @@
 #include "kernels.h"
 
 // RAII device buffer (stream-ordered allocation on the context stream)
+struct BootSetup;
+
 struct DevBuf {
     u64 *p = nullptr;
     size_t words = 0;
@@ -141,12 +143,14 @@ struct Ctx {
         Counters cnt;
         double out_scale = 0;
         const void *keys = nullptr;  // evaluation keys whose device memory the graph's kernels read
+        const void *aux = nullptr;   // other library-owned device memory it reads (bootstrap material)
     };
     std::map<std::string, Graph> graphs;
     std::map<std::string, int> graph_seen;  // eager calls per key: capture on the second sighting only
     std::vector<std::string> graph_order;   // capture order (the oldest graph is evicted beyond kMaxGraphs)
     static constexpr int kMaxGraphs = 16;
     std::set<Keys *> live_keys;          // keys generated on this context (owner back-pointers)
+    std::set<BootSetup *> live_boots;    // bootstrap material built on this context (likewise)
     void drop_graphs(const void *keys);  // destroy every graph that reads these keys
     bool use_graphs = true;
     // host-buffer argmax pipeline (secpe_enc_argmax_host): two device staging slots per direction and a
@@ -275,7 +279,7 @@ void run_argmax_boot(Ctx &c, const Keys &k, const CtView &in, const Layout &lay,
 // library-built bootstrapping material (secpe_boot_create): the EvalMod polynomial and the four encoded
 // matrices, NTT form, [n2][n1][limbs][N] each
 struct BootSetup {
-    const Ctx *ctx = nullptr;
+    Ctx *ctx = nullptr;  // owner (graph cache); nulled when the context goes first
     bool fft = false;
     BootCfg cfg;
     DevBuf cts_re, cts_im, stc_re, stc_im;

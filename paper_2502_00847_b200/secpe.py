@@ -530,11 +530,13 @@ class Context:
                                          1 if bsgs else 0, ctypes.byref(h)))
         return Boot(self, h)
 
-    def bootstrap_boot(self, keys, a, boot):
-        """secpe_bootstrap_boot: bootstrap with library-built material of either kind."""
+    def bootstrap_boot(self, keys, a, boot, out=None):
+        """secpe_bootstrap_boot: bootstrap with library-built material of either kind (a CUDA graph is captured
+        and replayed on a non-default stream when the same buffers come back)."""
         rl = ctypes.c_int32(0)
         depth = lib().secpe_boot_levels(boot.h, ctypes.byref(rl))
-        out = self._out(max(rl.value - depth, 0))
+        if out is None:
+            out = self._out(max(rl.value - depth, 0))
         ca, co = a.c(), out.c()
         _chk(lib().secpe_bootstrap_boot(self.h, keys.h, ctypes.byref(ca), boot.h, ctypes.byref(co)))
         out.level, out.scale = co.level, co.scale

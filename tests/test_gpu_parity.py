@@ -1264,3 +1264,35 @@ def test_bsgs_split_rejects_gaps():
     D = {0: np.ones(n), 2: np.ones(n), 6: np.ones(n)}
     with pytest.raises(ValueError):
         plan.bsgs_split(D, n)
+
+
+@pytest.mark.gpu
+def test_bootstrap_graph_replay_and_material_destroy(S):
+    """secpe_bootstrap_boot on a non-default stream with the same buffers: eager first, captured CUDA graph
+    replayed afterwards -- word for word the eager result; destroying the material drops the graph, so new
+    material (possibly at the same address) is used, not the old graph."""
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        g = S.Context(synth.PARAM_SETS["boot"], stream=stream.cuda_stream)
+        b = g.boot_create_fft(g.L, 16, 7, [4, 4, 3], g.scale, bsgs=True)
+        kg = g.keygen(9, b.steps(), h=64)
+        z = np.random.default_rng(2).uniform(-1, 1, g.N // 2)
+        c0 = g.new_ct(0)
+        g.encrypt_coeffs(kg, g.encode(z, g.scale), 0, g.scale, 3, out=c0)
+        c0.level, c0.scale = 0, g.scale
+        out = g.new_ct(g.L - (2 * 3 + 6 + 7))
+        g.bootstrap_boot(kg, c0, b, out=out)
+        stream.synchronize()
+        first = out.t.cpu().numpy().copy()
+        for _ in range(3):
+            out.t.zero_()
+            g.bootstrap_boot(kg, c0, b, out=out)
+            stream.synchronize()
+            assert np.array_equal(out.t.cpu().numpy(), first)
+        assert np.abs(g.decrypt(kg, out) - z).max() < 2 ** -12
+        del b
+        b2 = g.boot_create_fft(g.L, 16, 7, [4, 4, 3], g.scale, bsgs=True)   # same shapes, fresh material
+        for _ in range(3):
+            g.bootstrap_boot(kg, c0, b2, out=out)
+            stream.synchronize()
+        assert np.abs(g.decrypt(kg, out) - z).max() < 2 ** -12
