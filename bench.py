@@ -210,11 +210,10 @@ def micro_configs(stream, reps=5):
                                   "hoisted": True,
                                   "not_hoisted": {"ms_per_15_keys": ms, "rotations_per_s": 15 * R / (ms / 1000)}}
     del ctx, keys, a, b, r, o
-    out["N3_bootstrap"] = bootstrap_bench(stream, t_ms)
-    out["N4_argmax_k16"] = argmax_k16_bench(stream, t_ms)
-    out["N4_argmax_n256"] = argmax_boot_bench(stream, t_ms, "argmax_n256", 8, 6.0)
-    out["N4_clip_80x1000"] = clip_bench(stream, t_ms)
-    return out
+    nxt = {"N3_bootstrap": bootstrap_bench(stream, t_ms), "N4_argmax_k16": argmax_k16_bench(stream, t_ms),
+           "N4_argmax_n256": argmax_boot_bench(stream, t_ms, "argmax_n256", 8, 6.0),
+           "N4_clip_80x1000": clip_bench(stream, t_ms)}
+    return out, nxt
 
 
 def bootstrap_bench(stream, t_ms):
@@ -573,7 +572,9 @@ def run_secpe(a):
         "clocks": clk,
     }
     if ws == 1 and not a.no_micro:
-        line["configs_1_to_3"] = micro_configs(stream)
+        # BASELINE configs[1]-[3] and the SURVEY 8(f) rows built beyond the hot path (N3 bootstrapping, N4
+        # argmax with bootstrapping), each with its own parity tests
+        line["configs_1_to_3"], line["next_rows"] = micro_configs(stream)
     if ws == 1 and not a.no_cpu_baseline:
         dt, q, cores = oracle_argmax_once()
         line["cpu_baseline"] = {"value": q / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
