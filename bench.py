@@ -281,6 +281,16 @@ def bootstrap_bench(stream, t_ms):
     breakdown = {"keyswitch_share": prof["keyswitch"]["ms"] / tot, "rescale_share": prof["rescale"]["ms"] / tot,
                  "ntt_share": prof["ntt"]["ms"] / tot, "profiled_ms": tot, "key_switches": cnt["keyswitch"],
                  "ntt_limbs": cnt["ntt_limbs"], "launches": cnt["launches"]}
+    # throughput: 8 ciphertexts through one plan (secpe_bootstrap_boot_batch)
+    B = 8
+    cb = secpe.Ct(c0.t.repeat(B, 1, 1, 1), 0, ctx.scale)
+    rb = [ctx.new_ct(ctx.L - (2 * len(groups) + 6 + r), B)]
+
+    def batch():
+        rb[0] = ctx.bootstrap_boot(keys, cb, boot, out=rb[0])
+    ms_b = t_ms(batch)
+    out["N=2^16_fft_batch8"] = {"ms_per_call": ms_b, "ciphertexts": B, "bootstraps_per_s": B / (ms_b / 1000),
+                                "max_abs_err": float(abs(ctx.decrypt(keys, rb[0], B - 1) - z).max())}
     out["N=2^16_fft"] = {"breakdown": breakdown, "ms_per_bootstrap": ms, "logn": ctx.logn, "slots": ctx.N // 2, "level_in": 0,
                          "raised_to": ctx.L, "level_out": res[0].level, "galois_keys": len(steps),
                          "max_abs_err": err, "setup_s": setup_s,

@@ -322,6 +322,11 @@ int secpe_boot_create_fft(secpe_ctx *ctx, int32_t level, double K, int32_t r, co
  * unstaged (contiguous) input and output batches. */
 int secpe_bootstrap_boot(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, const secpe_boot *boot,
                          secpe_ct *out);
+/* A batch of n level-0 ciphertexts (one level and scale) through one bootstrap plan (every key and
+ * transform plaintext read once per op for the batch; one ciphertext does not fill the GPU): in / out
+ * host[n] as secpe_enc_argmax; factorised material only; CUDA graph as above on unstaged buffers. */
+int secpe_bootstrap_boot_batch(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n,
+                               const secpe_boot *boot, secpe_ct *out);
 /* Rotation steps (SECPE_CONJ included) whose Galois keys a library-built bootstrap needs, ascending with
  * SECPE_CONJ last; returns their count, writes min(count, cap) of them to steps (may be null). */
 int32_t secpe_boot_steps(const secpe_boot *boot, int32_t *steps, int32_t cap);

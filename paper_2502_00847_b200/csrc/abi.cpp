@@ -787,6 +787,29 @@ int secpe_bootstrap_boot(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct 
         bootstrap_fft_views(ctx->c, keys, in, boot->b->fcfg, out, boot->b.get());
     });
 }
+int secpe_bootstrap_boot_batch(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n,
+                               const secpe_boot *boot, secpe_ct *out) {
+    return guard([&] {
+        REQUIRE(ctx && keys && in && out && n >= 1 && boot && boot->b && boot->b->fft, SECPE_EINVAL,
+                "needs factorised bootstrap material");
+        Ctx &c = ctx->c;
+        const FftBootCfg &b = boot->b->fcfg;
+        REQUIRE(b.level < c.nq && b.level - fft_boot_depth(b) >= 0, SECPE_ELEVEL, "not enough levels");
+        DevBuf inb, outb;
+        CtView vin = batch_in(c, in, n, inb);
+        REQUIRE(vin.level == 0, SECPE_EINVAL, "bootstrap takes level-0 ciphertexts");
+        for (int i = 0; i < n; i++)
+            for (int j = 0; j < n; j++) REQUIRE(out[i].data != in[j].data, SECPE_EINVAL, "out must not alias in");
+        check_fft_keys(c, keys, b);
+        CtView vout = batch_out(c, out, n, b.level - fft_boot_depth(b), 0.0, outb);
+        char k[192];
+        snprintf(k, sizeof k, "bootb/%p/%p/%d/%s/%p/%p", (void *)vin.data, (void *)vout.data, n, dkey(vin.scale).c_str(),
+                 (const void *)boot->b.get(), (const void *)keys);
+        graphed(c, !inb.p && !outb.p, k, keys, boot->b.get(), vout,
+                [&] { run_bootstrap_fft(c, *keys->k, vin, b, vout); });
+        batch_out_finish(c, out, n, vout, outb);
+    });
+}
 static const LtStage &boot_stage(const FftBootCfg &f, int kind, int idx, int &lv) {
     const int mc = (int)f.cts.size(), base = f.level - mc - 6 - f.r;
     REQUIRE(kind >= 0 && kind < 4, SECPE_EINVAL, "stage kind");

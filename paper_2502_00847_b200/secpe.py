@@ -115,6 +115,8 @@ SIGS = {
     "secpe_bootstrap_boot": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), vp, ctypes.POINTER(CCt)]),
     "secpe_boot_levels": (ctypes.c_int32, [vp, i32p]),
     "secpe_boot_steps": (ctypes.c_int32, [vp, i32p, ctypes.c_int32]),
+    "secpe_bootstrap_boot_batch": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, vp,
+                                                  ctypes.POINTER(CCt)]),
     "secpe_argmax_boot_info": (ctypes.c_int, [vp, ctypes.POINTER(Layout), ctypes.POINTER(SignCfg), vp,
                                               ctypes.c_int32, i32p]),
     "secpe_enc_argmax_boot": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.c_int32,
@@ -535,6 +537,15 @@ class Context:
         and replayed on a non-default stream when the same buffers come back)."""
         rl = ctypes.c_int32(0)
         depth = lib().secpe_boot_levels(boot.h, ctypes.byref(rl))
+        if a.n > 1:  # secpe_bootstrap_boot_batch: one plan for the batch
+            ol = max(rl.value - depth, 0)
+            if out is None:
+                out = self.new_ct(ol, a.n)
+            ins = (CCt * a.n)(*[a.c(i) for i in range(a.n)])
+            outs = (CCt * a.n)(*[CCt(ctypes.cast(out.t[i].data_ptr(), u64p), ol, 0.0) for i in range(a.n)])
+            _chk(lib().secpe_bootstrap_boot_batch(self.h, keys.h, ins, a.n, boot.h, outs))
+            out.level, out.scale = outs[0].level, outs[0].scale
+            return out
         if out is None:
             out = self._out(max(rl.value - depth, 0))
         ca, co = a.c(), out.c()

@@ -1296,3 +1296,22 @@ def test_bootstrap_graph_replay_and_material_destroy(S):
             g.bootstrap_boot(kg, c0, b2, out=out)
             stream.synchronize()
         assert np.abs(g.decrypt(kg, out) - z).max() < 2 ** -12
+
+
+@pytest.mark.gpu
+def test_bootstrap_batch_equals_single(S):
+    """secpe_bootstrap_boot_batch: three ciphertexts through one plan give, word for word, the three
+    single-ciphertext bootstraps."""
+    P = pair(S, "boot")
+    g = P.gpu
+    b = g.boot_create_fft(g.L, 16, 7, [4, 4, 3], g.scale, bsgs=True)
+    kg = g.keygen(11, b.steps(), h=64)
+    zs = [np.random.default_rng(30 + i).uniform(-1, 1, g.N // 2) for i in range(3)]
+    cts = [g.encrypt(kg, z, 0, g.scale, 40 + i) for i, z in enumerate(zs)]
+    batch = S.Ct(torch.cat([c.t for c in cts]), 0, g.scale)
+    out = g.bootstrap_boot(kg, batch, b)
+    for i, c in enumerate(cts):
+        one = g.bootstrap_boot(kg, c, b)
+        assert one.level == out.level and one.scale == out.scale
+        assert torch.equal(one.t[0], out.t[i])
+        assert np.abs(g.decrypt(kg, out, i) - zs[i]).max() < 2 ** -12
