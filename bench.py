@@ -82,9 +82,19 @@ def dist_env():
 # ------------------------------------------------------------------------------------------------
 # reference arm / cpu baseline: the CPU oracle as it stands
 # ------------------------------------------------------------------------------------------------
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 class OracleArgmax:
     """The CPU oracle's full argmax of ONE configs[4] ciphertext (2048 queries); keys and the input are
-    built once, run() times plan.argmax only.  Returns (seconds, queries, threads)."""
+    built once, run() times plan.argmax only.  Returns (seconds, queries, threads actually used)."""
 
     def __init__(self, seed_base=1):
         import synth
@@ -100,10 +110,44 @@ class OracleArgmax:
         self.ct = self.ev.encrypt(self.keys, plan.pack(scores, self.lay, prm.N // 2), prm.scale, 11)
 
     def run(self):
+        from oracle import ckks
+        threads = ckks.lib().o_set_threads(0)  # the OpenMP team size the oracle's parallel loops run with
         t0 = time.perf_counter()
         self.plan.argmax(self.ev, self.keys, self.ct, self.lay, self.st)
         dt = time.perf_counter() - t0
-        return dt, self.lay["queries"], int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+        return dt, self.lay["queries"], threads
+
+    def h1_seconds(self, threads):
+        """Oracle time of the circuit's first stage (H1: log2 P = 3 rotations + additions at the top level, the
+        key-switch-bound op the whole circuit is made of) with `threads` OpenMP threads."""
+        from oracle import ckks
+        lib = ckks.lib()
+        prev = lib.o_set_threads(0)
+        used = lib.o_set_threads(threads)
+        try:
+            y = self.ct
+            t0 = time.perf_counter()
+            for t in range(3):
+                y = self.ev.add(y, self.ev.rot(self.keys, y, self.lay["classes"] << t))
+            return time.perf_counter() - t0, used
+        finally:
+            lib.o_set_threads(prev)
+
+
+def cpu_baseline_line(ora, dt, q, cores):
+    """the oracle on all host cores (one full ciphertext) and single-threaded.  The
+    single-thread figure is the all-core value scaled by the single/all-core time ratio measured on the H1
+    sample (a full single-thread ciphertext would take minutes)."""
+    t1, _ = ora.h1_seconds(1)
+    tn, used = ora.h1_seconds(cores)
+    v = q / dt
+    return {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+            "logical_cpus": os.cpu_count(),
+            "sample": "1 ciphertext of the same workload (2048 queries, full argmax circuit) on %d OpenMP threads, "
+                      "%.1f s" % (cores, dt),
+            "single_thread_value": v * tn / t1,
+            "single_thread_sample": "H1 stage (3 top-level rotations) timed on 1 thread (%.2f s) and on %d threads "
+                                    "(%.2f s); single-thread value = all-core value x %.3f" % (t1, used, tn, tn / t1)}
 
 
 def oracle_argmax_once(seed_base=1):
@@ -135,7 +179,8 @@ def run_reference(a):
             "steps_requested": a.steps, "warmup": a.warmup, "ms_per_step": 1000 * T / n, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64 (RNS residues)", "data": "synthetic",
             "config": {"workload": WORKLOAD, "batch_per_step": 1},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model(), "logical_cpus": os.cpu_count()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -189,7 +234,15 @@ def micro_configs(stream, reps=5):
     a.scale = b.scale = ctx.scale
     o = ctx.new_ct(ctx.L - 1, B)
     ms = t_ms(lambda: ctx.mul_relin_rescale(keys, a, b, out=o))
-    out["configs[2]_mul_relin_rescale"] = {"ms_per_batch": ms, "batch": B, "ops_per_s": B / (ms / 1000)}
+    # algorithmic bytes per op (SURVEY 8(d) cfg 3): inputs 2 x 2 x (L+1) limbs, output 2 L limbs, the
+    # relinearisation key (dnum x 2 x (L+1+k) limbs) once per batch
+    limb = ctx.N * 8
+    dnum = -(-ctx.nq // ctx.alpha)
+    key_limbs = dnum * 2 * (ctx.nq + ctx.np_)
+    b2 = (4 * ctx.nq + 2 * (ctx.nq - 1) + key_limbs / B) * limb
+    gb2 = B * b2 / (ms / 1000) / 1e9
+    out["configs[2]_mul_relin_rescale"] = {"ms_per_batch": ms, "batch": B, "ops_per_s": B / (ms / 1000),
+                                           "alg_bytes_per_op": b2, "alg_gbs": gb2, "frac_of_hbm": gb2 / peak}
     R = 128
     r = ctx.new_ct(ctx.L, R)
     for i in range(R):
@@ -206,9 +259,15 @@ def micro_configs(stream, reps=5):
         outs[0] = ctx.rotate_hoisted(keys, r, steps)
     ms_h = t_ms(hoisted)
     outs[0] = None
+    # per rotation (SURVEY 8(d) cfg 4): input 2 (L+1) limbs + output 2 (L+1) limbs + the Galois key / R
+    b3 = (4 * ctx.nq + key_limbs / R) * limb
+    gb3 = 15 * R * b3 / (ms_h / 1000) / 1e9
+    gb3n = 15 * R * b3 / (ms / 1000) / 1e9
     out["configs[3]_rotation"] = {"ms_per_15_keys": ms_h, "cts": R, "rotations_per_s": 15 * R / (ms_h / 1000),
-                                  "hoisted": True,
-                                  "not_hoisted": {"ms_per_15_keys": ms, "rotations_per_s": 15 * R / (ms / 1000)}}
+                                  "hoisted": True, "alg_bytes_per_rotation": b3, "alg_gbs": gb3,
+                                  "frac_of_hbm": gb3 / peak,
+                                  "not_hoisted": {"ms_per_15_keys": ms, "rotations_per_s": 15 * R / (ms / 1000),
+                                                  "alg_gbs": gb3n, "frac_of_hbm": gb3n / peak}}
     del ctx, keys, a, b, r, o
     nxt = {"N3_bootstrap": bootstrap_bench(stream, t_ms), "N4_argmax_k16": argmax_k16_bench(stream, t_ms),
            "N4_argmax_n256": argmax_boot_bench(stream, t_ms, "argmax_n256", 8, 6.0),
@@ -281,16 +340,22 @@ def bootstrap_bench(stream, t_ms):
     breakdown = {"keyswitch_share": prof["keyswitch"]["ms"] / tot, "rescale_share": prof["rescale"]["ms"] / tot,
                  "ntt_share": prof["ntt"]["ms"] / tot, "profiled_ms": tot, "key_switches": cnt["keyswitch"],
                  "ntt_limbs": cnt["ntt_limbs"], "launches": cnt["launches"]}
-    # throughput: 8 ciphertexts through one plan (secpe_bootstrap_boot_batch)
+    # throughput: 8 distinct ciphertexts through one plan (secpe_bootstrap_boot_batch); every output checked
     B = 8
-    cb = secpe.Ct(c0.t.repeat(B, 1, 1, 1), 0, ctx.scale)
+    zb = [synth.rng(4100 + i).uniform(-1, 1, ctx.N // 2) for i in range(B)]
+    cb = ctx.new_ct(0, B)
+    for i in range(B):
+        ctx.encrypt_coeffs(keys, ctx.encode(zb[i], ctx.scale), 0, ctx.scale, 90 + i,
+                           out=secpe.Ct(cb.t[i:i + 1], 0, ctx.scale))
+    cb.level, cb.scale = 0, ctx.scale
     rb = [ctx.new_ct(ctx.L - (2 * len(groups) + 6 + r), B)]
 
     def batch():
         rb[0] = ctx.bootstrap_boot(keys, cb, boot, out=rb[0])
     ms_b = t_ms(batch)
+    errs = [float(abs(ctx.decrypt(keys, rb[0], i) - zb[i]).max()) for i in range(B)]
     out["N=2^16_fft_batch8"] = {"ms_per_call": ms_b, "ciphertexts": B, "bootstraps_per_s": B / (ms_b / 1000),
-                                "max_abs_err": float(abs(ctx.decrypt(keys, rb[0], B - 1) - z).max())}
+                                "max_abs_err": max(errs), "inputs": "8 distinct ciphertexts, every output decrypted"}
     out["N=2^16_fft"] = {"breakdown": breakdown, "ms_per_bootstrap": ms, "logn": ctx.logn, "slots": ctx.N // 2, "level_in": 0,
                          "raised_to": ctx.L, "level_out": res[0].level, "galois_keys": len(steps),
                          "max_abs_err": err, "setup_s": setup_s,
@@ -572,6 +637,10 @@ def run_secpe(a):
                                           if ntt_int["ms"] > 0 else "none: every prime of Q u P is < 2^46 (R24)"),
                      "keyswitch": {"achieved": ks_ach, "frac": ks_ach / peak, "share_of_step": ks["ms"] / ms_prof,
                                    "unit": "GB/s"},
+                     # the same figures as flat fields (nested objects are not kept by every reader)
+                     "keyswitch_achieved_gbs": ks_ach, "keyswitch_frac": ks_ach / peak,
+                     "keyswitch_share_of_step": ks["ms"] / ms_prof,
+                     "fp64_pipe_frac": fp64_ach / fp64_peak,
                      "rescale_share_of_step": prof["rescale"]["ms"] / ms_prof},
         "stage_share_of_step": {k[6:]: v["ms"] / ms_prof for k, v in prof.items() if k.startswith("stage_")},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h_in.numel() * 8),
@@ -585,11 +654,18 @@ def run_secpe(a):
         # BASELINE configs[1]-[3] and the SURVEY 8(f) rows built beyond the hot path (N3 bootstrapping, N4
         # argmax with bootstrapping), each with its own parity tests
         line["configs_1_to_3"], line["next_rows"] = micro_configs(stream)
+        c = line["configs_1_to_3"]
+        rf = line["roofline"]
+        rf["configs1_ntt_gbs"] = c["configs[1]_ntt"]["alg_gbs"]
+        rf["configs1_ntt_frac"] = c["configs[1]_ntt"]["frac_of_hbm"]
+        rf["configs2_mul_relin_rescale_gbs"] = c["configs[2]_mul_relin_rescale"]["alg_gbs"]
+        rf["configs2_mul_relin_rescale_frac"] = c["configs[2]_mul_relin_rescale"]["frac_of_hbm"]
+        rf["configs3_rotation_gbs"] = c["configs[3]_rotation"]["alg_gbs"]
+        rf["configs3_rotation_frac"] = c["configs[3]_rotation"]["frac_of_hbm"]
     if ws == 1 and not a.no_cpu_baseline:
-        dt, q, cores = oracle_argmax_once()
-        line["cpu_baseline"] = {"value": q / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-                                "sample": "1 ciphertext of the same workload (2048 queries, full argmax circuit), "
-                                          "%.1f s" % dt}
+        ora = OracleArgmax()
+        dt, q, cores = ora.run()
+        line["cpu_baseline"] = cpu_baseline_line(ora, dt, q, cores)
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()

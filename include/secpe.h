@@ -114,18 +114,30 @@ int secpe_ctx_info(const secpe_ctx *ctx, uint64_t *primes_out, uint64_t *psi_out
 size_t secpe_ct_bytes(const secpe_ctx *ctx, int32_t level);
 
 /* ---- keys (client) ---------------------------------------------------------------------
- * All randomness comes from counter-based SplitMix64 streams of `seed` (reading R6):
- * ternary secret, public key, relinearisation key (s^2) and one Galois key per distinct
- * rotation step in rot_steps (host[n_rot]; >0 RotL, <0 RotR).  Hybrid digits (reading R7). */
-int secpe_keygen(secpe_ctx *ctx, uint64_t seed, const int32_t *rot_steps, int32_t n_rot,
+ * Randomness (reading R6): a 256-bit master seed keys ChaCha20 keystreams.  The secret material (the
+ * secret s, every Gaussian error) is drawn under derive(seed, DOM_SK), the public uniform polynomials
+ * (pk.a, every switching key's a) under derive(seed, DOM_PK) -- so the public and evaluation keys
+ * reveal nothing about the stream the secret came from -- and encryption randomness (v, e0, e1) under
+ * derive(encryption seed, DOM_ENC); derive(K, d) = first 32 bytes of ChaCha20 block 0 of key K, nonce d.
+ * seed == NULL: 32 bytes of OS entropy (getrandom(2)) -- the production mode.  A seed built by
+ * secpe_seed_from_u64 is TEST-ONLY (deterministic, 64 bits of entropy at most): parity tests and
+ * benchmarks use it so the oracle can regenerate the same keys. */
+typedef struct {
+    uint8_t bytes[32];
+} secpe_seed;
+/* TEST-ONLY deterministic seed: bytes = little-endian u64 followed by 24 zero bytes. */
+void secpe_seed_from_u64(uint64_t s, secpe_seed *out);
+/* Ternary secret, public key, relinearisation key (s^2) and one Galois key per distinct rotation step in
+ * rot_steps (host[n_rot]; >0 RotL, <0 RotR).  Hybrid digits (reading R7). */
+int secpe_keygen(secpe_ctx *ctx, const secpe_seed *seed, const int32_t *rot_steps, int32_t n_rot,
                  secpe_keys **out);
 /* As secpe_keygen with a sparse ternary secret of Hamming weight `hamming` (reading R36, the secret
- * bootstrapping uses to keep |I| and the EvalMod range K small): draw x_ctr = SplitMix64(seed, tag 1)
+ * bootstrapping uses to keep |I| and the EvalMod range K small): draw x_ctr from the secret's stream
  * for ctr = 0, 1, ...; the top log_n bits pick a coefficient; a still-zero one becomes -1 (x odd) or
  * +1; stop at `hamming` nonzeros.  hamming = 0: the uniform ternary secret of secpe_keygen.
  * SECPE_EINVAL: hamming outside [0, N]. */
-int secpe_keygen_sparse(secpe_ctx *ctx, uint64_t seed, int32_t hamming, const int32_t *rot_steps, int32_t n_rot,
-                        secpe_keys **out);
+int secpe_keygen_sparse(secpe_ctx *ctx, const secpe_seed *seed, int32_t hamming, const int32_t *rot_steps,
+                        int32_t n_rot, secpe_keys **out);
 /* Frees the key material.  Synchronises the owning context's stream and destroys every CUDA graph
  * secpe_enc_argmax captured with these keys (a later keys object at the same address never replays
  * them).  Keys may be destroyed before or after their context; null is a no-op. */
@@ -144,11 +156,12 @@ int secpe_key_export(const secpe_ctx *ctx, const secpe_keys *keys, int32_t which
  * m_k = round_half_away((2 scale / N) Re sum_j z_j zeta^{-5^j k}); host out int64[N]. */
 int secpe_encode(secpe_ctx *ctx, const double *slots, size_t n, double scale, int64_t *coeffs_out);
 /* Encrypt the integer plaintext host coeffs[N] at `level` with the public key; out->data must
- * hold secpe_ct_bytes(level); out->level/scale are set. */
+ * hold secpe_ct_bytes(level); out->level/scale are set.  seed: the encryption randomness's master seed
+ * (NULL: OS entropy; never reuse one for two messages). */
 int secpe_encrypt_coeffs(secpe_ctx *ctx, const secpe_keys *keys, const int64_t *coeffs,
-                         int32_t level, double scale, uint64_t seed, secpe_ct *out);
+                         int32_t level, double scale, const secpe_seed *seed, secpe_ct *out);
 int secpe_encrypt(secpe_ctx *ctx, const secpe_keys *keys, const double *slots, size_t n,
-                  int32_t level, double scale, uint64_t seed, secpe_ct *out);
+                  int32_t level, double scale, const secpe_seed *seed, secpe_ct *out);
 /* host out uint64[level+1][N]: residues of c0 + c1 s in coefficient form (synchronises). */
 int secpe_decrypt_residues(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *ct,
                            uint64_t *host_out);
@@ -185,10 +198,10 @@ int secpe_drop(secpe_ctx *ctx, const secpe_ct *a, int32_t level, secpe_ct *out);
  * rescale.  Same level required; out scale = scale_a * scale_b.  out must not alias. */
 int secpe_mul_relin(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *a, const secpe_ct *b,
                     secpe_ct *out);
-/* a (x) b relinearised and rescaled in ONE step for a batch of n pairs (the form the argmax circuit
- * uses, reading R11b): the ModDown by P and the division by q_l are a single floor division by
- * B = P q_l (fast base conversion from {q_l} u P).  Not bit-identical to secpe_mul_relin followed by
- * secpe_rescale (different rounding, error <= n_p + 1 per coefficient).  a[i], b[i]: same level
+/* a (x) b relinearised and rescaled in ONE pass for a batch of n pairs (the form the argmax circuit
+ * uses): the ModDown conversion (R11) and the rescale conversion (R12) share one INTT/NTT round trip
+ * (ks.cu rr_conv_kernel + the NTT's rescale epilogue).  Bit-identical to secpe_mul_relin followed by
+ * secpe_rescale (tests/test_gpu_parity.py test_ops_bit_exact_toy).  a[i], b[i]: same level
  * l >= 1 and scale within the batch; out[i]: level l - 1, scale (S_a S_b) / q_l, sized
  * secpe_ct_bytes(l - 1), must not alias.  Contiguous batches (data[i] = data[0] + i * ct words)
  * are used in place; others are staged.  The relinearisation key is streamed once per batch. */
@@ -324,7 +337,9 @@ int secpe_bootstrap_boot(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct 
                          secpe_ct *out);
 /* A batch of n level-0 ciphertexts (one level and scale) through one bootstrap plan (every key and
  * transform plaintext read once per op for the batch; one ciphertext does not fill the GPU): in / out
- * host[n] as secpe_enc_argmax; factorised material only; CUDA graph as above on unstaged buffers. */
+ * host[n] as secpe_enc_argmax; factorised material only (SECPE_EINVAL otherwise: loop over
+ * secpe_bootstrap_boot for dense material); no output may overlap any input (byte ranges checked);
+ * CUDA graph as above on unstaged buffers. */
 int secpe_bootstrap_boot_batch(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n,
                                const secpe_boot *boot, secpe_ct *out);
 /* Rotation steps (SECPE_CONJ included) whose Galois keys a library-built bootstrap needs, ascending with
@@ -375,7 +390,11 @@ int secpe_rotate(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int
 
 /* ---- SecPE circuits --------------------------------------------------------------------- */
 /* Composite Sign (Eq. 3-4) with the fixed BSGS plan of reading R13;
- * out level = in level - sum ceil(log2(d+1)); out scale = target_scale. */
+ * out level = in level - secpe_sign_depth(cfg); out scale = target_scale. */
+/* Levels the plan of reading R13 consumes: the sum over stages of 2 (degree 3), 3 (degree 7) or 5
+ * (degree 15, Paterson-Stockmeyer: x, x^2, x^3, x^4, x^8 then two giant products); 13 for (7, 15, 15).
+ * Returns < 0 (SECPE_EINVAL) for an unsupported configuration. */
+int32_t secpe_sign_depth(const secpe_sign_cfg *cfg);
 int secpe_sign_poly(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in,
                     const secpe_sign_cfg *cfg, double target_scale, secpe_ct *out);
 /* Level and scale of secpe_enc_argmax's outputs for inputs at in_level. */
@@ -389,8 +408,9 @@ int secpe_argmax_info(secpe_ctx *ctx, const secpe_layout *layout, const secpe_si
  * concurrent sub-batches on context-owned streams.  On a non-default context stream the call is
  * captured as a CUDA graph the second time the same (buffers, level, layout, Sign, keys) are seen and
  * replayed from the third time on (at most 16 graphs per context, oldest evicted; secpe_keys_destroy
- * drops the graphs of its keys).  No secret key is taken or needed.
- * Errors: SECPE_EINVAL (null arguments, n_in < 1, mixed levels/scales), SECPE_ELAYOUT, SECPE_ELEVEL
+ * drops the graphs of its keys).  No secret key is taken or needed.  No output ciphertext may overlap
+ * any input ciphertext (the two sub-batches run concurrently; checked on the byte ranges).
+ * Errors: SECPE_EINVAL (null arguments, n_in < 1, mixed levels/scales, overlapping in/out), SECPE_ELAYOUT, SECPE_ELEVEL
  * (not enough levels, e.g. K = 16 with the (7,15,15) Sign at L = 29), SECPE_ENOKEY, SECPE_ECUDA. */
 int secpe_enc_argmax(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, int32_t n_in,
                      const secpe_layout *layout, const secpe_sign_cfg *cfg, secpe_ct *out);

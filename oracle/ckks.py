@@ -34,7 +34,35 @@ _SRC = os.path.join(_HERE, "ckks_oracle.c")
 
 u64p = ctypes.POINTER(ctypes.c_uint64)
 i64p = ctypes.POINTER(ctypes.c_int64)
+u32p = ctypes.POINTER(ctypes.c_uint32)
 intp = ctypes.POINTER(ctypes.c_int)
+
+
+def seed_key(seed):
+    """256-bit master seed as 8 little-endian uint32 words (DESIGN.md R6): 32 bytes are taken as they are;
+    an integer 0 <= seed < 2^64 is the TEST-ONLY deterministic mode, bytes = LE64(seed) followed by 24 zeros."""
+    if isinstance(seed, (bytes, bytearray)):
+        if len(seed) != 32:
+            raise ValueError("a seed is 32 bytes")
+        return np.frombuffer(bytes(seed), dtype="<u4").astype(np.uint32)
+    seed = int(seed)
+    if not 0 <= seed < 1 << 64:
+        raise ValueError("integer seeds are 64-bit")
+    return np.array([seed & 0xFFFFFFFF, seed >> 32, 0, 0, 0, 0, 0, 0], dtype=np.uint32)
+
+
+def chacha20_block(key, counter, nonce):
+    """One ChaCha20 block (16 uint32 words) of the oracle core."""
+    out = np.zeros(16, dtype=np.uint32)
+    k = np.ascontiguousarray(key, dtype=np.uint32)
+    lib().o_chacha20_block(k.ctypes.data_as(u32p), counter, nonce, out.ctypes.data_as(u32p))
+    return out
+
+
+def object_key(master, tag):
+    out = np.zeros(8, dtype=np.uint32)
+    lib().o_object_key(master.ctypes.data_as(u32p), tag, out.ctypes.data_as(u32p))
+    return out
 
 
 def build():
@@ -57,6 +85,7 @@ def lib():
         L = ctypes.CDLL(_SO)
         U, I = ctypes.c_uint64, ctypes.c_int
         sig = {
+            "o_set_threads": (I, [I]),
             "o_is_prime": (I, [U]),
             "o_gen_primes": (I, [I, I, U, I, u64p, I, u64p]),
             "o_find_psi": (U, [U, I]),
@@ -67,17 +96,21 @@ def lib():
             "o_ntt_naive": (None, [u64p, u64p, I, U, U]),
             "o_ntt_limbs": (None, [u64p, I, I, u64p, u64p, intp]),
             "o_intt_limbs": (None, [u64p, I, I, u64p, u64p, intp]),
-            "o_draw": (U, [U, U, U]),
+            "o_chacha20_block": (None, [u32p, U, U, u32p]),
+            "o_derive": (None, [u32p, U, u32p]),
+            "o_object_key": (None, [u32p, U, u32p]),
+            "o_encrypt_key": (None, [u32p, u32p]),
+            "o_draw": (U, [u32p, U, U]),
             "o_tag": (U, [U, U, U]),
-            "o_uniform": (U, [U, U, U, U, I, U]),
-            "o_sample_uniform": (None, [U, U, I, I, u64p, intp, u64p]),
-            "o_sample_ternary": (None, [U, U, I, i64p]),
-            "o_sample_sparse": (None, [U, U, I, I, i64p]),
-            "o_sample_gauss": (None, [U, U, I, u64p, I, i64p]),
+            "o_uniform": (U, [u32p, U, U, U, I, U]),
+            "o_sample_uniform": (None, [u32p, U, I, I, u64p, intp, u64p]),
+            "o_sample_ternary": (None, [u32p, U, I, i64p]),
+            "o_sample_sparse": (None, [u32p, U, I, I, i64p]),
+            "o_sample_gauss": (None, [u32p, U, I, u64p, I, i64p]),
             "o_int_to_ntt": (None, [ctypes.c_void_p, i64p, I, intp, u64p]),
-            "o_keygen_pk": (None, [ctypes.c_void_p, U, u64p, u64p, I, u64p]),
-            "o_keygen_swk": (None, [ctypes.c_void_p, U, U, u64p, u64p, u64p, I, u64p]),
-            "o_encrypt": (None, [ctypes.c_void_p, U, u64p, i64p, I, u64p, I, u64p]),
+            "o_keygen_pk": (None, [ctypes.c_void_p, u32p, u64p, u64p, I, u64p]),
+            "o_keygen_swk": (None, [ctypes.c_void_p, u32p, U, u64p, u64p, u64p, I, u64p]),
+            "o_encrypt": (None, [ctypes.c_void_p, u32p, u64p, i64p, I, u64p, I, u64p]),
             "o_decrypt_residues": (None, [ctypes.c_void_p, u64p, u64p, I, u64p]),
             "o_add": (None, [ctypes.c_void_p, u64p, u64p, I, I, u64p]),
             "o_sub": (None, [ctypes.c_void_p, u64p, u64p, I, I, u64p]),
@@ -370,39 +403,43 @@ class Oracle:
         N, ne = prm.N, prm.nq + prm.np_
         k = Keys()
         k.seed = seed
+        master = seed_key(seed)
+        mk = master.ctypes.data_as(u32p)
+        ks = object_key(master, L.o_tag(1, 0, 0))
         s = np.zeros(N, dtype=np.int64)
         if h:
             if not 0 < h <= N:
                 raise ValueError("Hamming weight out of range")
-            L.o_sample_sparse(seed, L.o_tag(1, 0, 0), prm.logn, h, P(s))
+            L.o_sample_sparse(ks.ctypes.data_as(u32p), L.o_tag(1, 0, 0), prm.logn, h, P(s))
         else:
-            L.o_sample_ternary(seed, L.o_tag(1, 0, 0), prm.logn, P(s))
+            L.o_sample_ternary(ks.ctypes.data_as(u32p), L.o_tag(1, 0, 0), prm.logn, P(s))
         k.s = s
         k.s_ntt = np.zeros((ne, N), dtype=np.uint64)
         L.o_int_to_ntt(prm.cptr, P(s), ne, P(np.arange(ne, dtype=np.int32)), P(k.s_ntt))
         k.pk = np.zeros((2, prm.nq, N), dtype=np.uint64)
-        L.o_keygen_pk(prm.cptr, seed, P(k.s_ntt), P(prm.cdt), len(prm.cdt), P(k.pk))
+        L.o_keygen_pk(prm.cptr, mk, P(k.s_ntt), P(prm.cdt), len(prm.cdt), P(k.pk))
         # relinearisation key: s' = s^2
         s2 = np.zeros((prm.nq, N), dtype=np.uint64)
         for t in range(prm.nq):
             q = prm.primes[t]
             lib().o_mul_vec(P(np.ascontiguousarray(k.s_ntt[t])), P(np.ascontiguousarray(k.s_ntt[t])), N, q, P(s2[t]))
-        k.rlk = self._swk(seed, 0, k.s_ntt, s2)
+        k.rlk = self._swk(master, 0, k.s_ntt, s2)
         k.gk = {}
         for st in rot_steps:
             g = galois_elt(prm, st)
             if g in k.gk:
                 continue
             sg = self.automorph_poly(k.s_ntt[: prm.nq], g)
-            k.gk[g] = self._swk(seed, g, k.s_ntt, sg)
+            k.gk[g] = self._swk(master, g, k.s_ntt, sg)
         return k
 
-    def _swk(self, seed, g, s_ntt, sp_ntt):
+    def _swk(self, master, g, s_ntt, sp_ntt):
         prm = self.prm
         beta = prm.beta(prm.L)
         out = np.zeros((beta, 2, prm.nq + prm.np_, prm.N), dtype=np.uint64)
         sp = np.ascontiguousarray(sp_ntt, dtype=np.uint64)
-        lib().o_keygen_swk(prm.cptr, seed, g, P(s_ntt), P(sp), P(prm.cdt), len(prm.cdt), P(out))
+        lib().o_keygen_swk(prm.cptr, master.ctypes.data_as(u32p), g, P(s_ntt), P(sp), P(prm.cdt), len(prm.cdt),
+                           P(out))
         return out
 
     def automorph_poly(self, poly_ntt, g):
@@ -418,7 +455,8 @@ class Oracle:
         prm = self.prm
         m = np.ascontiguousarray(m, dtype=np.int64)
         ct = np.zeros((2, level + 1, prm.N), dtype=np.uint64)
-        lib().o_encrypt(prm.cptr, seed, P(keys.pk), P(m), level, P(prm.cdt), len(prm.cdt), P(ct))
+        lib().o_encrypt(prm.cptr, seed_key(seed).ctypes.data_as(u32p), P(keys.pk), P(m), level, P(prm.cdt),
+                        len(prm.cdt), P(ct))
         return Ct(ct, scale)
 
     def encrypt(self, keys, z, scale, seed, level=None):

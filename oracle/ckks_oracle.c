@@ -16,7 +16,7 @@
  *     order), psi = the smallest primitive 2N-th root of unity mod q;
  *     computed as  twist by psi^k  ->  textbook radix-2 cyclic DFT with omega = psi^2
  *     ->  read out in bit-reversed order;
- *   - sampler: counter-based SplitMix64 streams (DESIGN.md "sampler" reading);
+ *   - sampler: ChaCha20 keystreams keyed by keys derived from a 256-bit master seed (R6);
  *   - key switching: hybrid, consecutive alpha-prime digits, ModDown without
  *     rounding correction (readings R10/R11);
  *   - rescale: round-half-up division by the last prime (R12);
@@ -25,6 +25,7 @@
  * Parallelism: plain `omp parallel for` over independent limbs only; every
  * per-limb computation is sequential and identical with or without OpenMP.
  */
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -32,6 +33,19 @@
 typedef uint64_t u64;
 typedef int64_t i64;
 typedef unsigned __int128 u128;
+
+/* thread control for the timed CPU baseline (bench.py): n > 0 sets the OpenMP team size; returns the
+ * number of threads a parallel region actually runs with */
+int o_set_threads(int n) {
+    if (n > 0) omp_set_num_threads(n);
+    int t = 1;
+#pragma omp parallel
+    {
+#pragma omp single
+        t = omp_get_num_threads();
+    }
+    return t;
+}
 
 /* ------------------------------------------------------------------ */
 /* O-2 modular arithmetic: residues in [0,q), plain % reduction        */
@@ -219,43 +233,90 @@ void o_intt_limbs(u64 *a, int logn, int nl, const u64 *primes, const u64 *psis, 
 }
 
 /* ------------------------------------------------------------------ */
-/* O-6 sampler: counter-based SplitMix64 streams (R6)        */
+/* O-6 sampler: ChaCha20 keystreams (R6)                     */
 /* ------------------------------------------------------------------ */
-#define GAMMA 0x9E3779B97F4A7C15ULL
-static inline u64 mix64(u64 z) {
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-    return z ^ (z >> 31);
+typedef uint32_t u32;
+static inline u32 rotl32(u32 x, int r) { return (x << r) | (x >> (32 - r)); }
+#define QR(a, b, c, d)                          \
+    a += b; d ^= a; d = rotl32(d, 16);          \
+    c += d; b ^= c; b = rotl32(b, 12);          \
+    a += b; d ^= a; d = rotl32(d, 8);           \
+    c += d; b ^= c; b = rotl32(b, 7);
+/* the ChaCha20 block function (Bernstein's layout: words 12-13 a 64-bit block counter, 14-15 a 64-bit
+ * nonce): 20 rounds on the state, then the input state added word by word */
+void o_chacha20_block(const u32 *key, u64 counter, u64 nonce, u32 *out) {
+    u32 x[16], in[16] = {0x61707865u, 0x3320646eu, 0x79622d32u, 0x6b206574u};
+    for (int i = 0; i < 8; i++) in[4 + i] = key[i];
+    in[12] = (u32)counter; in[13] = (u32)(counter >> 32);
+    in[14] = (u32)nonce; in[15] = (u32)(nonce >> 32);
+    for (int i = 0; i < 16; i++) x[i] = in[i];
+    for (int r = 0; r < 10; r++) {
+        QR(x[0], x[4], x[8], x[12]) QR(x[1], x[5], x[9], x[13])
+        QR(x[2], x[6], x[10], x[14]) QR(x[3], x[7], x[11], x[15])
+        QR(x[0], x[5], x[10], x[15]) QR(x[1], x[6], x[11], x[12])
+        QR(x[2], x[7], x[8], x[13]) QR(x[3], x[4], x[9], x[14])
+    }
+    for (int i = 0; i < 16; i++) out[i] = x[i] + in[i];
 }
-/* stream for (seed, tag); the ctr-th output of SplitMix64 started at state s0 is mix(s0 + (ctr+1)*GAMMA) */
-u64 o_draw(u64 seed, u64 tag, u64 ctr) {
-    u64 s0 = mix64(seed ^ mix64(tag + GAMMA));
-    return mix64(s0 + (ctr + 1) * GAMMA);
+/* key derivation: the first 8 words of the block (master, counter 0, nonce domain) */
+void o_derive(const u32 *master, u64 domain, u32 *out) {
+    u32 w[16];
+    o_chacha20_block(master, 0, domain, w);
+    for (int i = 0; i < 8; i++) out[i] = w[i];
+}
+/* stream (key, tag): draw ctr is the 64-bit word (w[2j], w[2j+1]) of block ctr / 8, j = ctr mod 8 */
+u64 o_draw(const u32 *key, u64 tag, u64 ctr) {
+    u32 w[16];
+    o_chacha20_block(key, ctr >> 3, tag, w);
+    int j = (int)(ctr & 7);
+    return (u64)w[2 * j] | ((u64)w[2 * j + 1] << 32);
+}
+/* the same draws with the last block kept (sequential callers) */
+typedef struct { const u32 *key; u64 tag, blk; u32 w[16]; } OStream;
+static void os_init(OStream *s, const u32 *key, u64 tag) { s->key = key; s->tag = tag; s->blk = ~(u64)0; }
+static u64 os_draw(OStream *s, u64 ctr) {
+    if ((ctr >> 3) != s->blk) { s->blk = ctr >> 3; o_chacha20_block(s->key, s->blk, s->tag, s->w); }
+    int j = (int)(ctr & 7);
+    return (u64)s->w[2 * j] | ((u64)s->w[2 * j + 1] << 32);
 }
 /* object tags */
 u64 o_tag(u64 kind, u64 g, u64 j) { return (kind << 48) ^ (g << 8) ^ j; }
+/* key domains (nonces of o_derive): secret material (s, e), public material (the uniform a), encryption */
+#define DOM_SK 0x5345435045534B31ULL
+#define DOM_PK 0x5345435045504B31ULL
+#define DOM_ENC 0x5345435045454E31ULL
+static int kind_public(u64 tag) { u64 k = tag >> 48; return k == 2 || k == 4; }
 
-/* uniform residue mod q for prime index t, coefficient k: floor(X*q / 2^128), X = two draws */
-u64 o_uniform(u64 seed, u64 tag, u64 t, u64 k, int logn, u64 q) {
-    u64 ctr = 2 * ((t << logn) + k);
-    u64 xh = o_draw(seed, tag, ctr), xl = o_draw(seed, tag, ctr + 1);
+/* uniform residue mod q for prime index t, coefficient k: floor(X*q / 2^128), X = draws 2c || 2c+1 */
+static u64 uniform_from(u64 xh, u64 xl, u64 q) {
     u128 p1 = (u128)xl * q;
     u128 p2 = (u128)xh * q + (u64)(p1 >> 64);
     return (u64)(p2 >> 64);
 }
+u64 o_uniform(const u32 *key, u64 tag, u64 t, u64 k, int logn, u64 q) {
+    u64 ctr = 2 * ((t << logn) + k);
+    return uniform_from(o_draw(key, tag, ctr), o_draw(key, tag, ctr + 1), q);
+}
 /* uniform polynomial, sampled directly in the NTT domain, limbs [nl][N] for primes pid[] */
-void o_sample_uniform(u64 seed, u64 tag, int logn, int nl, const u64 *primes, const int *pid, u64 *out) {
+void o_sample_uniform(const u32 *key, u64 tag, int logn, int nl, const u64 *primes, const int *pid, u64 *out) {
     u64 n = (u64)1 << logn;
 #pragma omp parallel for
-    for (int l = 0; l < nl; l++)
-        for (u64 k = 0; k < n; k++)
-            out[(u64)l * n + k] = o_uniform(seed, tag, (u64)pid[l], k, logn, primes[pid[l]]);
+    for (int l = 0; l < nl; l++) {
+        OStream st;
+        os_init(&st, key, tag);
+        for (u64 k = 0; k < n; k++) {
+            u64 ctr = 2 * (((u64)pid[l] << logn) + k);
+            out[(u64)l * n + k] = uniform_from(os_draw(&st, ctr), os_draw(&st, ctr + 1), primes[pid[l]]);
+        }
+    }
 }
 /* ternary: v = floor(x*3 / 2^64) in {0,1,2} -> {0, 1, -1} */
-void o_sample_ternary(u64 seed, u64 tag, int logn, i64 *out) {
+void o_sample_ternary(const u32 *key, u64 tag, int logn, i64 *out) {
     u64 n = (u64)1 << logn;
+    OStream st;
+    os_init(&st, key, tag);
     for (u64 k = 0; k < n; k++) {
-        u64 x = o_draw(seed, tag, k);
+        u64 x = os_draw(&st, k);
         u64 v = (u64)(((u128)x * 3) >> 64);
         out[k] = v == 0 ? 0 : (v == 1 ? 1 : -1);
     }
@@ -263,10 +324,12 @@ void o_sample_ternary(u64 seed, u64 tag, int logn, i64 *out) {
 /* sparse ternary secret of Hamming weight h (reading R36, bootstrapping's sparse secret): draw
  * x_ctr for ctr = 0, 1, ...; position = top logn bits of x; if that coefficient is still 0 it becomes
  * -1 when x is odd, else +1; stop after h nonzeros.  out must be zeroed; h <= N. */
-void o_sample_sparse(u64 seed, u64 tag, int logn, int h, i64 *out) {
+void o_sample_sparse(const u32 *key, u64 tag, int logn, int h, i64 *out) {
     int cnt = 0;
+    OStream st;
+    os_init(&st, key, tag);
     for (u64 ctr = 0; cnt < h; ctr++) {
-        u64 x = o_draw(seed, tag, ctr);
+        u64 x = os_draw(&st, ctr);
         u64 pos = x >> (64 - logn);
         if (out[pos] == 0) {
             out[pos] = (x & 1) ? -1 : 1;
@@ -275,10 +338,12 @@ void o_sample_sparse(u64 seed, u64 tag, int logn, int h, i64 *out) {
     }
 }
 /* discrete Gaussian via CDT: sign = top bit, u = low 63 bits, |e| = min{m : u < T[m]} */
-void o_sample_gauss(u64 seed, u64 tag, int logn, const u64 *cdt, int ncdt, i64 *out) {
+void o_sample_gauss(const u32 *key, u64 tag, int logn, const u64 *cdt, int ncdt, i64 *out) {
     u64 n = (u64)1 << logn;
+    OStream st;
+    os_init(&st, key, tag);
     for (u64 k = 0; k < n; k++) {
-        u64 x = o_draw(seed, tag, k);
+        u64 x = os_draw(&st, k);
         u64 u = x & 0x7FFFFFFFFFFFFFFFULL;
         i64 m = 0;
         while (m < ncdt - 1 && u >= cdt[m]) m++;
@@ -318,14 +383,22 @@ static int *ids_range(int a, int cnt) {
 }
 
 /* O-7 public key: pk = (-a s + e, a) over Q_L, a uniform (NTT domain), e Gaussian */
-void o_keygen_pk(const OCtx *c, u64 seed, const u64 *s_ntt, const u64 *cdt, int ncdt, u64 *pk) {
+/* the key of object `tag`'s stream under the 256-bit master seed: public-material objects (the uniform
+ * a of pk and of every switching key) use derive(master, DOM_PK), all others derive(master, DOM_SK) */
+void o_object_key(const u32 *master, u64 tag, u32 *out) { o_derive(master, kind_public(tag) ? DOM_PK : DOM_SK, out); }
+void o_encrypt_key(const u32 *master, u32 *out) { o_derive(master, DOM_ENC, out); }
+
+void o_keygen_pk(const OCtx *c, const u32 *master, const u64 *s_ntt, const u64 *cdt, int ncdt, u64 *pk) {
     u64 n = NN(c);
     int nq = c->nq;
     int *pid = ids_range(0, nq);
     u64 *a = pk + (u64)nq * n;
-    o_sample_uniform(seed, o_tag(2, 0, 0), c->logn, nq, c->primes, pid, a);
+    u32 kp[8], ks[8];
+    o_object_key(master, o_tag(2, 0, 0), kp);
+    o_object_key(master, o_tag(3, 0, 0), ks);
+    o_sample_uniform(kp, o_tag(2, 0, 0), c->logn, nq, c->primes, pid, a);
     i64 *e = (i64 *)malloc(n * sizeof(i64));
-    o_sample_gauss(seed, o_tag(3, 0, 0), c->logn, cdt, ncdt, e);
+    o_sample_gauss(ks, o_tag(3, 0, 0), c->logn, cdt, ncdt, e);
     u64 *en = (u64 *)malloc((u64)nq * n * sizeof(u64));
     o_int_to_ntt(c, e, nq, pid, en);
     for (int l = 0; l < nq; l++) {
@@ -346,8 +419,11 @@ void o_keygen_pk(const OCtx *c, u64 seed, const u64 *s_ntt, const u64 *cdt, int 
  *   P-limb   : b_j = -a_j s + e_j
  * layout out[j][0 = b, 1 = a][nq+np][N].  g = Galois element (0 for relinearization).
  */
-void o_keygen_swk(const OCtx *c, u64 seed, u64 g, const u64 *s_ntt, const u64 *sp_ntt,
+void o_keygen_swk(const OCtx *c, const u32 *master, u64 g, const u64 *s_ntt, const u64 *sp_ntt,
                   const u64 *cdt, int ncdt, u64 *out) {
+    u32 kp[8], ks[8];
+    o_object_key(master, o_tag(4, g, 0), kp);
+    o_object_key(master, o_tag(5, g, 0), ks);
     u64 n = NN(c);
     int nq = c->nq, np = c->np, ne = nq + np;
     int beta = (nq + c->alpha - 1) / c->alpha;
@@ -357,8 +433,8 @@ void o_keygen_swk(const OCtx *c, u64 seed, u64 g, const u64 *s_ntt, const u64 *s
     for (int j = 0; j < beta; j++) {
         u64 *b = out + (u64)j * 2 * ne * n;
         u64 *a = b + (u64)ne * n;
-        o_sample_uniform(seed, o_tag(4, g, (u64)j), c->logn, ne, c->primes, pid, a);
-        o_sample_gauss(seed, o_tag(5, g, (u64)j), c->logn, cdt, ncdt, e);
+        o_sample_uniform(kp, o_tag(4, g, (u64)j), c->logn, ne, c->primes, pid, a);
+        o_sample_gauss(ks, o_tag(5, g, (u64)j), c->logn, cdt, ncdt, e);
         o_int_to_ntt(c, e, ne, pid, en);
         for (int t = 0; t < ne; t++) {
             u64 q = c->primes[t];
@@ -377,8 +453,10 @@ void o_keygen_swk(const OCtx *c, u64 seed, u64 g, const u64 *s_ntt, const u64 *s
 }
 
 /* O-8 encryption at level `level` with the public key: ct = (v pk0 + e0 + m, v pk1 + e1) */
-void o_encrypt(const OCtx *c, u64 seed, const u64 *pk, const i64 *m, int level,
+void o_encrypt(const OCtx *c, const u32 *master, const u64 *pk, const i64 *m, int level,
                const u64 *cdt, int ncdt, u64 *ct) {
+    u32 ke[8];
+    o_encrypt_key(master, ke);
     u64 n = NN(c);
     int nl = level + 1, nq = c->nq;
     int *pid = ids_range(0, nl);
@@ -387,11 +465,11 @@ void o_encrypt(const OCtx *c, u64 seed, const u64 *pk, const i64 *m, int level,
     u64 *e0 = (u64 *)malloc((u64)nl * n * sizeof(u64));
     u64 *e1 = (u64 *)malloc((u64)nl * n * sizeof(u64));
     u64 *mn = (u64 *)malloc((u64)nl * n * sizeof(u64));
-    o_sample_ternary(seed, o_tag(6, 0, 0), c->logn, tmp);
+    o_sample_ternary(ke, o_tag(6, 0, 0), c->logn, tmp);
     o_int_to_ntt(c, tmp, nl, pid, vn);
-    o_sample_gauss(seed, o_tag(7, 0, 0), c->logn, cdt, ncdt, tmp);
+    o_sample_gauss(ke, o_tag(7, 0, 0), c->logn, cdt, ncdt, tmp);
     o_int_to_ntt(c, tmp, nl, pid, e0);
-    o_sample_gauss(seed, o_tag(8, 0, 0), c->logn, cdt, ncdt, tmp);
+    o_sample_gauss(ke, o_tag(8, 0, 0), c->logn, cdt, ncdt, tmp);
     o_int_to_ntt(c, tmp, nl, pid, e1);
     o_int_to_ntt(c, m, nl, pid, mn);
     for (int l = 0; l < nl; l++) {

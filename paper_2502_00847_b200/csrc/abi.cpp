@@ -9,8 +9,8 @@
 #include "../../include/secpe.h"
 #include "context.h"
 
-Keys *keygen(Ctx &c, u64 seed, const int *rot, int n_rot, int h);
-void encrypt_coeffs(Ctx &c, const Keys &k, const i64 *coeffs, int level, u64 seed, u64 *ct);
+Keys *keygen(Ctx &c, const Key256 &master, const int *rot, int n_rot, int h);
+void encrypt_coeffs(Ctx &c, const Keys &k, const i64 *coeffs, int level, const Key256 &master, u64 *ct);
 void decrypt_residues(Ctx &c, const Keys &k, const CtView &ct, u64 *host_out);
 void decrypt_slots(Ctx &c, const Keys &k, const CtView &ct, double *slots, size_t n);
 
@@ -52,6 +52,15 @@ static CtView view_of(const Ctx &c, const secpe_ct *ct) {
 }
 // A batch of n caller ciphertexts as one CtView: the caller's memory when the batch is contiguous
 // (data[i] = data[0] + i * ct_words), else a staged copy (`stage` receives the buffer).
+// the byte ranges [data, data + words) of the n_out outputs must not overlap those of the n_in inputs
+// (an output batch larger than the input batch can overlap it without sharing a start pointer)
+static void no_overlap(const secpe_ct *in, int n_in, long in_words, const secpe_ct *out, int n_out, long out_words) {
+    for (int i = 0; i < n_out; i++)
+        for (int j = 0; j < n_in; j++) {
+            const uint64_t *o0 = out[i].data, *o1 = o0 + out_words, *i0 = in[j].data, *i1 = i0 + in_words;
+            REQUIRE(o1 <= i0 || i1 <= o0, SECPE_EINVAL, "out must not overlap in");
+        }
+}
 static CtView batch_in(Ctx &c, const secpe_ct *in, int n, DevBuf &stage) {
     REQUIRE(in && n >= 1, SECPE_EINVAL, "empty batch");
     const int lv = in[0].level;
@@ -282,17 +291,31 @@ size_t secpe_ct_bytes(const secpe_ctx *ctx, int32_t level) {
     return (size_t)ctx->c.ct_words(level) * 8;
 }
 
-int secpe_keygen(secpe_ctx *ctx, uint64_t seed, const int32_t *rot_steps, int32_t n_rot, secpe_keys **out) {
+// the 256-bit master seed (null: OS entropy), reading R6
+static Key256 master_key(const secpe_seed *seed) {
+    if (!seed) return os_entropy_key();
+    Key256 k;
+    for (int i = 0; i < 8; i++)
+        k.w[i] = (uint32_t)seed->bytes[4 * i] | ((uint32_t)seed->bytes[4 * i + 1] << 8) |
+                 ((uint32_t)seed->bytes[4 * i + 2] << 16) | ((uint32_t)seed->bytes[4 * i + 3] << 24);
+    return k;
+}
+void secpe_seed_from_u64(uint64_t s, secpe_seed *out) {
+    if (!out) return;
+    for (int i = 0; i < 32; i++) out->bytes[i] = i < 8 ? (uint8_t)(s >> (8 * i)) : 0;
+}
+int secpe_keygen(secpe_ctx *ctx, const secpe_seed *seed, const int32_t *rot_steps, int32_t n_rot, secpe_keys **out) {
     return secpe_keygen_sparse(ctx, seed, 0, rot_steps, n_rot, out);
 }
-int secpe_keygen_sparse(secpe_ctx *ctx, uint64_t seed, int32_t hamming, const int32_t *rot_steps, int32_t n_rot,
+int secpe_keygen_sparse(secpe_ctx *ctx, const secpe_seed *seed, int32_t hamming, const int32_t *rot_steps,
+                        int32_t n_rot,
                         secpe_keys **out) {
     return guard([&] {
         REQUIRE(ctx && out && (n_rot == 0 || rot_steps), SECPE_EINVAL, "null argument");
         REQUIRE(ctx->c.np >= 1, SECPE_EINVAL, "key generation needs at least one special prime");
         REQUIRE(hamming >= 0 && hamming <= ctx->c.N, SECPE_EINVAL, "Hamming weight out of range");
         auto h = std::make_unique<secpe_keys>();
-        h->k = keygen(ctx->c, seed, rot_steps, n_rot, hamming);
+        h->k = keygen(ctx->c, master_key(seed), rot_steps, n_rot, hamming);
         h->k->owner = &ctx->c;
         ctx->c.live_keys.insert(h->k);
         *out = h.release();
@@ -339,23 +362,23 @@ int secpe_encode(secpe_ctx *ctx, const double *slots, size_t n, double scale, in
     });
 }
 int secpe_encrypt_coeffs(secpe_ctx *ctx, const secpe_keys *keys, const int64_t *coeffs, int32_t level, double scale,
-                         uint64_t seed, secpe_ct *out) {
+                         const secpe_seed *seed, secpe_ct *out) {
     return guard([&] {
         REQUIRE(ctx && keys && coeffs && out && out->data, SECPE_EINVAL, "null argument");
         REQUIRE(level >= 0 && level < ctx->c.nq, SECPE_EINVAL, "level out of range");
-        encrypt_coeffs(ctx->c, *keys->k, coeffs, level, seed, out->data);
+        encrypt_coeffs(ctx->c, *keys->k, coeffs, level, master_key(seed), out->data);
         out->level = level;
         out->scale = scale;
     });
 }
 int secpe_encrypt(secpe_ctx *ctx, const secpe_keys *keys, const double *slots, size_t n, int32_t level, double scale,
-                  uint64_t seed, secpe_ct *out) {
+                  const secpe_seed *seed, secpe_ct *out) {
     return guard([&] {
         REQUIRE(ctx && keys && out && out->data && (n == 0 || slots), SECPE_EINVAL, "null argument");
         REQUIRE(level >= 0 && level < ctx->c.nq, SECPE_EINVAL, "level out of range");
         std::vector<i64> m(ctx->c.N);
         encode_int(ctx->c, slots, n, scale, m.data());
-        encrypt_coeffs(ctx->c, *keys->k, m.data(), level, seed, out->data);
+        encrypt_coeffs(ctx->c, *keys->k, m.data(), level, master_key(seed), out->data);
         out->level = level;
         out->scale = scale;
     });
@@ -798,8 +821,7 @@ int secpe_bootstrap_boot_batch(secpe_ctx *ctx, const secpe_keys *keys, const sec
         DevBuf inb, outb;
         CtView vin = batch_in(c, in, n, inb);
         REQUIRE(vin.level == 0, SECPE_EINVAL, "bootstrap takes level-0 ciphertexts");
-        for (int i = 0; i < n; i++)
-            for (int j = 0; j < n; j++) REQUIRE(out[i].data != in[j].data, SECPE_EINVAL, "out must not alias in");
+        no_overlap(in, n, c.ct_words(0), out, n, c.ct_words(b.level - fft_boot_depth(b)));
         check_fft_keys(c, keys, b);
         CtView vout = batch_out(c, out, n, b.level - fft_boot_depth(b), 0.0, outb);
         char k[192];
@@ -938,6 +960,11 @@ int secpe_sign_poly(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in, 
         set_out(out, vo);
     });
 }
+int32_t secpe_sign_depth(const secpe_sign_cfg *cfg) {
+    int32_t d = -1;
+    const int rc = guard([&] { d = sign_depth(sign_cfg(cfg)); });
+    return rc == SECPE_OK ? d : rc;
+}
 int secpe_argmax_info(secpe_ctx *ctx, const secpe_layout *layout, const secpe_sign_cfg *cfg, int32_t in_level,
                       int32_t *out_level, double *out_scale) {
     return guard([&] {
@@ -980,6 +1007,7 @@ int secpe_enc_argmax(secpe_ctx *ctx, const secpe_keys *keys, const secpe_ct *in,
         const int ol = lv - argmax_depth(lay, sc);
         REQUIRE(ol >= 0, SECPE_ELEVEL, "not enough levels for the argmax circuit");
         const long cw = c.ct_words(lv), ow = c.ct_words(ol);
+        no_overlap(in, n_in, cw, out, n_in, ow);
         // batch view: reuse the caller's memory if the inputs are laid out contiguously
         bool contiguous = true;
         for (int i = 1; i < n_in; i++) contiguous &= in[i].data == in[0].data + (long)i * cw;

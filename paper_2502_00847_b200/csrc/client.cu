@@ -2,7 +2,8 @@
 // :143 Step 4; readings R6/R7 of DESIGN.md).
 //
 // Object tags (kind << 48 ^ g << 8 ^ j): 1 secret, 2 pk.a, 3 pk.e, 4 swk.a, 5 swk.e (g = Galois
-// element, 0 for relinearisation; j = digit), 6 enc.v, 7 enc.e0, 8 enc.e1.
+// element, 0 for relinearisation; j = digit), 6 enc.v, 7 enc.e0, 8 enc.e1; each drawn from a ChaCha20
+// stream under a key derived from the caller's 256-bit seed (sample.cu, reading R6).
 #include <cstring>
 
 #include "context.h"
@@ -12,15 +13,16 @@ static inline LimbMap allmap(const Ctx &c) { return LimbMap{c.nprimes(), c.nq, 0
 static inline LimbMap qmap(int nl) { return LimbMap{nl, nl, 0, 0}; }
 
 // small signed polynomial (ternary / Gaussian) -> NTT residues on lm.nl limbs
-static void small_to_ntt(Ctx &c, u64 seed, u64 tg, int kind, u64 *out, LimbMap lm) {
+static void small_to_ntt(Ctx &c, const Key256 &key, u64 tg, int kind, u64 *out, LimbMap lm) {
     DevBuf m(c.N, c.st);
-    k_sample_small(c.logn, seed, tg, kind, (i64 *)m.p, c.st);
+    k_sample_small(c.logn, key, tg, kind, (i64 *)m.p, c.st);
     k_int_to_rows(c.tab, c.logn, (const i64 *)m.p, out, lm, c.st);
     ev_ntt(c, RowsArg{out, 2L * lm.nl * c.N, (long)lm.nl * c.N}, 1, lm, false);
 }
 
 // switching key for s' (NTT, nq limbs): out[j][0 = b, 1 = a][nq + np][N]
-static void gen_swk(Ctx &c, const Keys &k, u64 seed, u64 g, const u64 *sp, DevBuf &out) {
+static void gen_swk(Ctx &c, const Keys &k, const Key256 &master, u64 g, const u64 *sp, DevBuf &out) {
+    const Key256 kp = object_key(master, tag(4, g, 0)), ks = object_key(master, tag(5, g, 0));
     const int P = c.nprimes(), bt = c.beta(c.L());
     const long N = c.N;
     out = DevBuf((size_t)bt * 2 * P * N, c.st);
@@ -35,8 +37,8 @@ static void gen_swk(Ctx &c, const Keys &k, u64 seed, u64 g, const u64 *sp, DevBu
     for (int j = 0; j < bt; j++) {
         u64 *b = out.p + (size_t)j * 2 * P * N;
         u64 *a = b + (size_t)P * N;
-        k_sample_uniform(c.tab, c.logn, seed, tag(4, g, j), a, allmap(c), c.st);
-        small_to_ntt(c, seed, tag(5, g, j), 1, e.p, allmap(c));
+        k_sample_uniform(c.tab, c.logn, kp, tag(4, g, j), a, allmap(c), c.st);
+        small_to_ntt(c, ks, tag(5, g, j), 1, e.p, allmap(c));
         LimbConst gad{};
         for (int t = j * c.alpha; t < std::min((j + 1) * c.alpha, c.nq); t++) {
             gad.c[t] = Pt[t];
@@ -46,36 +48,37 @@ static void gen_swk(Ctx &c, const Keys &k, u64 seed, u64 g, const u64 *sp, DevBu
     }
 }
 
-Keys *keygen(Ctx &c, u64 seed, const int *rot, int n_rot, int h) {
+Keys *keygen(Ctx &c, const Key256 &master, const int *rot, int n_rot, int h) {
+    const Key256 ksk = object_key(master, tag(1, 0, 0)), kpk = object_key(master, tag(2, 0, 0));
     auto k = std::make_unique<Keys>();
     const int P = c.nprimes();
     const long N = c.N;
     k->s = DevBuf((size_t)P * N, c.st);
     if (h > 0) {  // sparse secret (R36), sampled on the host
         std::vector<i64> sh(N);
-        h_sample_sparse(seed, tag(1, 0, 0), c.logn, h, sh.data());
+        h_sample_sparse(ksk, tag(1, 0, 0), c.logn, h, sh.data());
         DevBuf m(N, c.st);
         CUDA_CHECK(cudaMemcpyAsync(m.p, sh.data(), N * 8, cudaMemcpyHostToDevice, c.st));
         k_int_to_rows(c.tab, c.logn, (const i64 *)m.p, k->s.p, allmap(c), c.st);
         ev_ntt(c, RowsArg{k->s.p, 2L * P * N, (long)P * N}, 1, allmap(c), false);
         CUDA_CHECK(cudaStreamSynchronize(c.st));  // sh is host memory of this frame
     } else {
-        small_to_ntt(c, seed, tag(1, 0, 0), 0, k->s.p, allmap(c));
+        small_to_ntt(c, ksk, tag(1, 0, 0), 0, k->s.p, allmap(c));
     }
     // public key (-a s + e, a) over Q_L
     k->pk = DevBuf(2L * c.nq * N, c.st);
     {
         u64 *a = k->pk.p + (size_t)c.nq * N;
-        k_sample_uniform(c.tab, c.logn, seed, tag(2, 0, 0), a, qmap(c.nq), c.st);
+        k_sample_uniform(c.tab, c.logn, kpk, tag(2, 0, 0), a, qmap(c.nq), c.st);
         DevBuf e((size_t)c.nq * N, c.st);
-        small_to_ntt(c, seed, tag(3, 0, 0), 1, e.p, qmap(c.nq));
+        small_to_ntt(c, ksk, tag(3, 0, 0), 1, e.p, qmap(c.nq));
         k_key_combine(c.tab, c.logn, a, k->s.p, e.p, nullptr, nullptr, k->pk.p, qmap(c.nq), c.st);
     }
     // relinearisation key: s' = s^2
     {
         DevBuf s2((size_t)c.nq * N, c.st);
         k_square(c.tab, c.logn, k->s.p, s2.p, qmap(c.nq), c.st);
-        gen_swk(c, *k, seed, 0, s2.p, k->rlk);
+        gen_swk(c, *k, master, 0, s2.p, k->rlk);
     }
     // Galois keys: s' = sigma_g(s)
     for (int i = 0; i < n_rot; i++) {
@@ -85,7 +88,7 @@ Keys *keygen(Ctx &c, u64 seed, const int *rot, int n_rot, int h) {
         k_automorph(c.logn, CRows{k->s.p, 2L * P * N, (long)P * N}, RowsArg{sg.p, 2L * c.nq * N, (long)c.nq * N}, 1,
                     c.nq, g, c.st);
         DevBuf key;
-        gen_swk(c, *k, seed, g, sg.p, key);
+        gen_swk(c, *k, master, g, sg.p, key);
         k->gk.emplace(g, std::move(key));
     }
     CUDA_CHECK(cudaStreamSynchronize(c.st));
@@ -93,7 +96,8 @@ Keys *keygen(Ctx &c, u64 seed, const int *rot, int n_rot, int h) {
 }
 
 // ct = (v pk0 + e0 + m, v pk1 + e1) at `level`; coeffs = integer plaintext (host)
-void encrypt_coeffs(Ctx &c, const Keys &k, const i64 *coeffs, int level, u64 seed, u64 *ct) {
+void encrypt_coeffs(Ctx &c, const Keys &k, const i64 *coeffs, int level, const Key256 &master, u64 *ct) {
+    const Key256 ke = derive_key(master, DOM_ENC);
     const int nl = level + 1;
     const long N = c.N;
     DevBuf mi(N, c.st), m((size_t)nl * N, c.st), v((size_t)nl * N, c.st), e0((size_t)nl * N, c.st),
@@ -101,9 +105,9 @@ void encrypt_coeffs(Ctx &c, const Keys &k, const i64 *coeffs, int level, u64 see
     CUDA_CHECK(cudaMemcpyAsync(mi.p, coeffs, N * 8, cudaMemcpyHostToDevice, c.st));
     k_int_to_rows(c.tab, c.logn, (const i64 *)mi.p, m.p, qmap(nl), c.st);
     ev_ntt(c, RowsArg{m.p, 2L * nl * N, (long)nl * N}, 1, qmap(nl), false);
-    small_to_ntt(c, seed, tag(6, 0, 0), 0, v.p, qmap(nl));
-    small_to_ntt(c, seed, tag(7, 0, 0), 1, e0.p, qmap(nl));
-    small_to_ntt(c, seed, tag(8, 0, 0), 1, e1.p, qmap(nl));
+    small_to_ntt(c, ke, tag(6, 0, 0), 0, v.p, qmap(nl));
+    small_to_ntt(c, ke, tag(7, 0, 0), 1, e0.p, qmap(nl));
+    small_to_ntt(c, ke, tag(8, 0, 0), 1, e1.p, qmap(nl));
     k_encrypt_combine(c.tab, c.logn, v.p, k.pk.p, (long)c.nq * N, e0.p, e1.p, m.p, ct, nl, c.st);
     CUDA_CHECK(cudaStreamSynchronize(c.st));  // coeffs is caller host memory
 }

@@ -188,7 +188,7 @@ void ev_rescale_lin(Ctx &c, const CtView &x1, i64 C1, const CtView *x2, i64 C2, 
 }
 
 // ModUp + key inner product (R10): acc[ct][b][ne][N] over Q_level u P (NTT form).  d01/d01s: optional
-// tensor (d0, d1) rows whose [P] multiple is added on the Q limbs (R11b).
+// tensor (d0, d1) rows whose [P] multiple is added on the Q limbs (the [P] d term lets the ModDown and the rescale share one conversion).
 // ten != nullptr: relinearisation of the tensor of ten->a, ten->b formed on the fly (d unused): the
 // INTT's first pass multiplies a1 b1, the inner product forms d0, d1 (+ C x) and adds [P] d_b.
 // ModUp of d (or of the tensor's d2 = a1 b1): ext[c][j][e] in NTT form, exts = beta (nl + np) N per ct

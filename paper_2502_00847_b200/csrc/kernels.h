@@ -124,7 +124,7 @@ void k_ks_inner(const Tab &tab, int logn, const u64 *d, long d_ct_stride, const 
                 const u64 *key, int nq_total, int np, u64 *acc, long acc_ct_stride, int n_ct, int nl,
                 int alpha, cudaStream_t st, const TensorSrc *ten = nullptr, const u64 *pmod = nullptr,
                 u64 galois = 1);  // galois > 1: read sigma_g(X_j) (NTT-domain gather; hoisted rotation, R29)
-// ModDown conversion (R11, R11b): T[c][b][i] = sum_{s < ns} y_s [B/s]_{q_i} mod q_i for i < nt, with
+// ModDown conversion (R11): T[c][b][i] = sum_{s < ns} y_s [B/s]_{q_i} mod q_i for i < nt, with
 // y_s = acc[c][b][row0 + s] (coefficient form, already times (B/s)^{-1}); hatpk[s * hstride + i]
 // split-30 packed
 void k_moddown_conv(const Tab &tab, int logn, const u64 *acc, long acc_ct_stride, int ne, int row0, int ns, u64 *T,
@@ -136,12 +136,21 @@ void k_rr_conv(const Tab &tab, int logn, const u64 *acc, long acc_ct_stride, int
                cudaStream_t st);
 
 // ---- sampling / keys (sample.cu) ----------------------------------------------------------------
+// ChaCha20 keys (reading R6): a 256-bit master seed, keys derived per material domain
+struct Key256 {
+    uint32_t w[8];
+};
+constexpr u64 DOM_SK = 0x5345435045534B31ULL, DOM_PK = 0x5345435045504B31ULL, DOM_ENC = 0x5345435045454E31ULL;
+Key256 derive_key(const Key256 &master, u64 domain);
+Key256 object_key(const Key256 &master, u64 tag);  // DOM_PK for tags of kind 2, 4 (the uniform a), else DOM_SK
+Key256 os_entropy_key();                             // 32 bytes from getrandom(2)
 // uniform residues in the NTT domain: out[l][k] for prime ids map (formula lm), counter layout per R6
-void k_sample_uniform(const Tab &tab, int logn, u64 seed, u64 tag, u64 *out, LimbMap lm, cudaStream_t st);
+// (N must be a multiple of 1024)
+void k_sample_uniform(const Tab &tab, int logn, const Key256 &key, u64 tag, u64 *out, LimbMap lm, cudaStream_t st);
 // signed small polynomial: kind 0 ternary, 1 Gaussian (cdt in constant memory)
-void k_sample_small(int logn, u64 seed, u64 tag, int kind, i64 *out, cudaStream_t st);
+void k_sample_small(int logn, const Key256 &key, u64 tag, int kind, i64 *out, cudaStream_t st);
 // host: sparse ternary secret of Hamming weight h (reading R36), out[N]
-void h_sample_sparse(u64 seed, u64 tag, int logn, int h, i64 *out);
+void h_sample_sparse(const Key256 &key, u64 tag, int logn, int h, i64 *out);
 void set_cdt(const u64 *cdt, int n);
 // residues of a signed int64 polynomial: out[l][k] = m[k] mod q_l (coefficient form)
 void k_int_to_rows(const Tab &tab, int logn, const i64 *m, u64 *out, LimbMap lm, cudaStream_t st);

@@ -392,7 +392,7 @@ __global__ void ks_inner_kernel(Tab tab, int logn, const u64 *__restrict__ d, lo
     }
 }
 
-// ModDown conversion (R11 / R11b).  grid: x = coefficient chunks (two per thread), y = ct * 2 + b.
+// ModDown conversion (R11).  grid: x = coefficient chunks (two per thread), y = ct * 2 + b.
 // Sources: ns rows starting at row0 of each acc polynomial (already holding [r_s (B/s)^{-1}]_s: the
 // factor is folded into the INTT); targets: q_0..q_{nt-1}.  Packed constants [B/s]_{q_i} at
 // hatpk[s * hstride + i], staged in shared memory as sc[i][s] (NS words per i).

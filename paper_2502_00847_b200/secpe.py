@@ -51,6 +51,26 @@ class CBootCfg(ctypes.Structure):
 CONJ = -(2 ** 31)  # SECPE_CONJ: the rotation step meaning slot conjugation
 
 
+class CSeed(ctypes.Structure):
+    """secpe_seed: 256-bit master seed (reading R6)."""
+    _fields_ = [("bytes", ctypes.c_uint8 * 32)]
+
+
+def seed_arg(seed):
+    """None -> NULL (the library draws 32 bytes of OS entropy: production mode); 32 bytes -> that seed; an
+    integer -> secpe_seed_from_u64 (TEST-ONLY deterministic mode, what the parity tests and the bench use)."""
+    if seed is None:
+        return None
+    s = CSeed()
+    if isinstance(seed, (bytes, bytearray)):
+        if len(seed) != 32:
+            raise ValueError("a seed is 32 bytes")
+        ctypes.memmove(s.bytes, bytes(seed), 32)
+    else:
+        lib().secpe_seed_from_u64(int(seed), ctypes.byref(s))
+    return ctypes.byref(s)
+
+
 class Layout(ctypes.Structure):
     _fields_ = [("queries", ctypes.c_int32), ("prompts", ctypes.c_int32), ("classes", ctypes.c_int32),
                 ("block", ctypes.c_int32)]
@@ -69,15 +89,17 @@ SIGS = {
     "secpe_sync": (ctypes.c_int, [vp]),
     "secpe_ctx_info": (ctypes.c_int, [vp, u64p, u64p]),
     "secpe_ct_bytes": (ctypes.c_size_t, [vp, ctypes.c_int32]),
-    "secpe_keygen": (ctypes.c_int, [vp, ctypes.c_uint64, i32p, ctypes.c_int32, ctypes.POINTER(vp)]),
-    "secpe_keygen_sparse": (ctypes.c_int, [vp, ctypes.c_uint64, ctypes.c_int32, i32p, ctypes.c_int32, ctypes.POINTER(vp)]),
+    "secpe_seed_from_u64": (None, [ctypes.c_uint64, ctypes.POINTER(CSeed)]),
+    "secpe_keygen": (ctypes.c_int, [vp, ctypes.POINTER(CSeed), i32p, ctypes.c_int32, ctypes.POINTER(vp)]),
+    "secpe_keygen_sparse": (ctypes.c_int, [vp, ctypes.POINTER(CSeed), ctypes.c_int32, i32p, ctypes.c_int32,
+                                           ctypes.POINTER(vp)]),
     "secpe_keys_destroy": (None, [vp]),
     "secpe_key_export": (ctypes.c_int, [vp, vp, ctypes.c_int32, ctypes.c_uint64, u64p, ctypes.c_size_t]),
     "secpe_encode": (ctypes.c_int, [vp, f64p, ctypes.c_size_t, ctypes.c_double, i64p]),
-    "secpe_encrypt_coeffs": (ctypes.c_int, [vp, vp, i64p, ctypes.c_int32, ctypes.c_double, ctypes.c_uint64,
+    "secpe_encrypt_coeffs": (ctypes.c_int, [vp, vp, i64p, ctypes.c_int32, ctypes.c_double, ctypes.POINTER(CSeed),
                                             ctypes.POINTER(CCt)]),
     "secpe_encrypt": (ctypes.c_int, [vp, vp, f64p, ctypes.c_size_t, ctypes.c_int32, ctypes.c_double,
-                                     ctypes.c_uint64, ctypes.POINTER(CCt)]),
+                                     ctypes.POINTER(CSeed), ctypes.POINTER(CCt)]),
     "secpe_decrypt_residues": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), u64p]),
     "secpe_decrypt": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), f64p, ctypes.c_size_t]),
     "secpe_ntt": (ctypes.c_int, [vp, u64p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
@@ -134,6 +156,7 @@ SIGS = {
     "secpe_rotate": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.POINTER(CCt)]),
     "secpe_sign_poly": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.POINTER(SignCfg), ctypes.c_double,
                                        ctypes.POINTER(CCt)]),
+    "secpe_sign_depth": (ctypes.c_int32, [ctypes.POINTER(SignCfg)]),
     "secpe_argmax_info": (ctypes.c_int, [vp, ctypes.POINTER(Layout), ctypes.POINTER(SignCfg), ctypes.c_int32,
                                          i32p, f64p]),
     "secpe_enc_argmax": (ctypes.c_int, [vp, vp, ctypes.POINTER(CCt), ctypes.c_int32, ctypes.POINTER(Layout),
@@ -228,8 +251,8 @@ def layout(d):
 
 
 class Keys:
-    def __init__(self, ctx, handle):
-        self.ctx, self.h = ctx, handle
+    def __init__(self, ctx, handle, fft):
+        self.ctx, self.h, self.fft = ctx, handle, fft
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:
@@ -359,7 +382,8 @@ class Context:
         """secpe_keygen (h = 0) / secpe_keygen_sparse (Hamming weight h, reading R36)."""
         r = np.array(list(rot_steps) or [0], dtype=np.int32)
         kh = vp()
-        _chk(lib().secpe_keygen_sparse(self.h, seed, h, r.ctypes.data_as(i32p), len(rot_steps), ctypes.byref(kh)))
+        _chk(lib().secpe_keygen_sparse(self.h, seed_arg(seed), h, r.ctypes.data_as(i32p), len(rot_steps),
+                                       ctypes.byref(kh)))
         return Keys(self, kh)
 
     def encode(self, slots, scale):
@@ -372,7 +396,7 @@ class Context:
         m = np.ascontiguousarray(coeffs, dtype=np.int64)
         ct = out if out is not None else self.new_ct(level)
         cc = CCt(ctypes.cast(ct.t.data_ptr(), u64p), level, scale)
-        _chk(lib().secpe_encrypt_coeffs(self.h, keys.h, m.ctypes.data_as(i64p), level, scale, seed,
+        _chk(lib().secpe_encrypt_coeffs(self.h, keys.h, m.ctypes.data_as(i64p), level, scale, seed_arg(seed),
                                         ctypes.byref(cc)))
         ct.level, ct.scale = level, scale
         return ct
@@ -381,7 +405,7 @@ class Context:
         z = np.ascontiguousarray(slots, dtype=np.float64)
         ct = self.new_ct(level)
         cc = ct.c()
-        _chk(lib().secpe_encrypt(self.h, keys.h, z.ctypes.data_as(f64p), len(z), level, scale, seed,
+        _chk(lib().secpe_encrypt(self.h, keys.h, z.ctypes.data_as(f64p), len(z), level, scale, seed_arg(seed),
                                  ctypes.byref(cc)))
         ct.level, ct.scale = level, scale
         return ct
@@ -465,7 +489,7 @@ class Context:
         return (CCt * ct.n)(*[ct.c(i) for i in range(ct.n)])
 
     def mul_relin_rescale(self, keys, a, b, out=None):
-        """Batched a (x) b relinearised and rescaled in one step (reading R11b); a, b batch Cts."""
+        """Batched a (x) b relinearised and rescaled in one pass (bit-identical to mul_relin + rescale); a, b batch Cts."""
         if out is None:
             out = self.new_ct(a.level - 1, a.n)
         ca, cb = self._batch(a), self._batch(b)
@@ -522,7 +546,7 @@ class Context:
         """secpe_boot_create: library-built bootstrapping material (readings R34, R35)."""
         h = vp()
         _chk(lib().secpe_boot_create(self.h, level, K, r, n1, n2, in_scale, ctypes.byref(h)))
-        return Boot(self, h)
+        return Boot(self, h, fft=False)
 
     def boot_create_fft(self, level, K, r, groups, in_scale, bsgs=False):
         """secpe_boot_create_fft: library-built factorised material (reading R37; bsgs: R39 form)."""
@@ -530,14 +554,23 @@ class Context:
         h = vp()
         _chk(lib().secpe_boot_create_fft(self.h, level, K, r, g.ctypes.data_as(i32p), len(g), in_scale,
                                          1 if bsgs else 0, ctypes.byref(h)))
-        return Boot(self, h)
+        return Boot(self, h, fft=True)
 
     def bootstrap_boot(self, keys, a, boot, out=None):
         """secpe_bootstrap_boot: bootstrap with library-built material of either kind (a CUDA graph is captured
         and replayed on a non-default stream when the same buffers come back)."""
         rl = ctypes.c_int32(0)
         depth = lib().secpe_boot_levels(boot.h, ctypes.byref(rl))
-        if a.n > 1:  # secpe_bootstrap_boot_batch: one plan for the batch
+        if a.n > 1 and not boot.fft:  # dense material (secpe_boot_create): one ciphertext per call
+            ol = max(rl.value - depth, 0)
+            if out is None:
+                out = self.new_ct(ol, a.n)
+            for i in range(a.n):
+                ca, co = a.c(i), CCt(ctypes.cast(out.t[i].data_ptr(), u64p), ol, 0.0)
+                _chk(lib().secpe_bootstrap_boot(self.h, keys.h, ctypes.byref(ca), boot.h, ctypes.byref(co)))
+            out.level, out.scale = co.level, co.scale
+            return out
+        if a.n > 1:  # secpe_bootstrap_boot_batch (factorised material): one plan for the batch
             ol = max(rl.value - depth, 0)
             if out is None:
                 out = self.new_ct(ol, a.n)
@@ -676,7 +709,8 @@ class Context:
     # ---- SecPE circuits ---------------------------------------------------------------------------
     def sign_poly(self, keys, a, stages, target_scale):
         cfg = sign_cfg(stages)
-        depth = sum(int(np.ceil(np.log2(len(c)))) for c in stages)
+        depth = lib().secpe_sign_depth(ctypes.byref(cfg))
+        _chk(depth if depth < 0 else 0)
         out = self._out(a.level - depth)
         ca, co = a.c(), out.c()
         _chk(lib().secpe_sign_poly(self.h, keys.h, ctypes.byref(ca), ctypes.byref(cfg), target_scale,

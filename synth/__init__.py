@@ -47,6 +47,12 @@ PARAM_SETS = {
     # the same with two more bootstrap levels, for four stage groups (3/4/4/4: fewer key switches per group)
     "boot_argmax16_g4": dict(logn=16, q=[("below", 60, 1), ("nearest", 45, 16), ("nearest", 50, 21)],
                              p=[("below", 60, 7)], alpha=7, log_scale=45),
+    # N = 2^12 analogues of the four-group chains (groups 2/3/3/3: depth 21): a standalone bootstrap chain and
+    # boot_argmax16_g4's structure on the small ring (word-for-word parity of the bench's four-group plans)
+    "boot_g4": dict(logn=12, q=[("below", 60, 1), ("nearest", 50, 22)], p=[("below", 60, 7)],
+                    alpha=7, log_scale=50),
+    "boot_argmax_g4": dict(logn=12, q=[("below", 60, 1), ("nearest", 45, 16), ("nearest", 50, 21)],
+                           p=[("below", 60, 7)], alpha=7, log_scale=45),
     # the paper's ring (N = 2^16, 32768 slots) with the factorised transforms (R37, groups 5/5/5: depth 20)
     "boot16": dict(logn=16, q=[("below", 60, 1), ("nearest", 50, 22)], p=[("below", 60, 7)],
                    alpha=7, log_scale=50),

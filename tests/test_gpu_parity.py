@@ -91,18 +91,40 @@ def test_ntt_bit_exact(S, name, n_polys, first, n_limbs):
     assert np.array_equal(t.cpu().numpy(), x)
 
 
-def test_ntt_edge_inputs(S):
-    P = pair(S, "toy")
+@pytest.mark.parametrize("name,first,n_limbs", [
+    ("toy", 0, 9),        # 40-bit chain + 50-bit special (integer rows)
+    ("argmax", 0, 40),    # configs[4]: 45-bit chain + 46-bit special primes (exact-FP64 rows, |v| <= 13 q < 2^51)
+    ("ntt", 0, 24),       # configs[1]: 60-bit primes (integer rows, Harvey bounds near 2^62)
+])
+def test_ntt_edge_inputs(S, name, first, n_limbs):
+    """Worst-case magnitudes for the lazy butterflies: all-(q-1), all-zero, alternating q-1 / 0 and
+    (q-1)/2 inputs, forward against the oracle's NTT on sampled limbs (incl. the first and last), and the
+    inverse of an all-(q-1) NTT-domain input against the oracle's INTT."""
+    P = pair(S, name)
     prm = P.prm
-    for fill in ("zero", "max"):
-        x = np.zeros((1, 8, prm.N), dtype=np.uint64)
+    primes = prm.primes[first:first + n_limbs]
+    qv = np.array(primes, dtype=np.uint64)[None, :, None]
+    check = sorted({0, n_limbs - 1, n_limbs // 2, 1 % n_limbs})
+    for fill in ("zero", "max", "alt", "half"):
+        x = np.zeros((1, n_limbs, prm.N), dtype=np.uint64)
         if fill == "max":
-            x[:] = np.array(prm.q, dtype=np.uint64)[None, :, None] - np.uint64(1)
+            x[:] = qv - np.uint64(1)
+        elif fill == "alt":
+            x[:, :, ::2] = (qv - np.uint64(1))[:, :, :1]
+        elif fill == "half":
+            x[:] = (qv - np.uint64(1)) // np.uint64(2)
         t = torch.from_numpy(x.copy()).cuda()
-        P.gpu.ntt(t, 0, 8)
+        P.gpu.ntt(t, first, n_limbs)
         got = t.cpu().numpy()
-        for l in range(8):
-            assert np.array_equal(got[0, l], ckks.ntt(x[0, l], prm.q[l], prm.psi[l], prm.logn))
+        for l in check:
+            assert np.array_equal(got[0, l], ckks.ntt(x[0, l], primes[l], prm.psi[first + l], prm.logn)), (fill, l)
+    x = np.zeros((1, n_limbs, prm.N), dtype=np.uint64)
+    x[:] = qv - np.uint64(1)
+    t = torch.from_numpy(x.copy()).cuda()
+    P.gpu.ntt(t, first, n_limbs, inverse=True)
+    got = t.cpu().numpy()
+    for l in check:
+        assert np.array_equal(got[0, l], ckks.intt(x[0, l], primes[l], prm.psi[first + l], prm.logn)), ("inv", l)
 
 
 def test_keys_bit_exact(S):
@@ -967,16 +989,17 @@ def test_bootstrap_n16_refreshes(S):
 
 @pytest.mark.gpu
 @pytest.mark.slow
-def test_argmax_boot_k16_bit_exact(S):
+@pytest.mark.parametrize("pname,groups", [("boot_argmax", [4, 4, 3]), ("boot_argmax_g4", [2, 3, 3, 3])])
+def test_argmax_boot_k16_bit_exact(S, pname, groups):
     """N4 (reading R38): secpe_enc_argmax_boot_cfg with K = 16 (16 queries per ciphertext at N = 2^12, four
     bootstraps) is word for word the oracle's argmax_boot with the same op list, and every label is exact
-    above the Sign margin."""
-    P = pair(S, "boot_argmax")
+    above the Sign margin.  Three stage groups, and four groups on a chain built like bench.py's
+    boot_argmax16_g4 (two more bootstrap levels)."""
+    P = pair(S, pname)
     prm, g = P.prm, P.gpu
     ev = ckks.Oracle(prm)
     lay = synth.LAYOUTS["boot_k16"]
     st = load_sign("sign_7_15_15.json")
-    groups = [4, 4, 3]
     rot = plan.argmax_rotations(lay) + plan.fft_boot_rotations(prm.N, groups)
     seed = synth.KEY_SEED_BASE + 37
     ko, kg = ev.keygen(seed, rot, h=64), g.keygen(seed, rot, h=64)
@@ -1198,14 +1221,14 @@ def test_argmax_boot_clip_prompt_groups_bit_exact(S):
 
 @pytest.mark.gpu
 @pytest.mark.slow
-def test_bootstrap_n16_bit_exact(S):
-    """N3 at full size (N = 2^16, 32768 slots, groups 5/5/5 in baby-step giant-step form, 39 Galois keys): the
-    GPU bootstrap with the oracle's encoded material is word for word the oracle's (about two minutes of oracle
-    time), same op list, refresh within 2^-11."""
+@pytest.mark.parametrize("groups", [[5, 5, 5], [4, 5, 6]])
+def test_bootstrap_n16_bit_exact(S, groups):
+    """N3 at full size (N = 2^16, 32768 slots, groups 5/5/5 and bench.py's 4/5/6, in baby-step giant-step form):
+    the GPU bootstrap with the oracle's encoded material is word for word the oracle's (about two minutes of
+    oracle time each), same op list, refresh within 2^-11."""
     P = pair(S, "boot16")
     prm, g = P.prm, P.gpu
     ev = ckks.Oracle(prm)
-    groups = [5, 5, 5]
     rot = plan.fft_boot_rotations(prm.N, groups, bsgs=True)
     seed = synth.KEY_SEED_BASE + 47
     ko, kg = ev.keygen(seed, rot, h=64), g.keygen(seed, rot, h=64)
@@ -1315,3 +1338,154 @@ def test_bootstrap_batch_equals_single(S):
         assert one.level == out.level and one.scale == out.scale
         assert torch.equal(one.t[0], out.t[i])
         assert np.abs(g.decrypt(kg, out, i) - zs[i]).max() < 2 ** -12
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_bootstrap_fft_bsgs_four_groups_bit_exact(S):
+    """R37 + R39 with four stage groups (2/3/3/3 at N = 2^12, the shape of bench.py's 3/4/4/4 at N = 2^16):
+    word for word the oracle's bootstrap with the same op list; the library-built material bootstraps within
+    2^-12 and its rotation steps are the oracle's."""
+    P = pair(S, "boot_g4")
+    prm, g = P.prm, P.gpu
+    ev = ckks.Oracle(prm)
+    groups = [2, 3, 3, 3]
+    rot = plan.fft_boot_rotations(prm.N, groups, bsgs=True)
+    seed = synth.KEY_SEED_BASE + 53
+    ko, kg = ev.keygen(seed, rot, h=64), g.keygen(seed, rot, h=64)
+    cfg = plan.fft_boot_config(ev, prm.scale, prm.L, 16, 7, groups, bsgs=True)
+    z = np.random.default_rng(23).uniform(-1, 1, prm.N // 2)
+    ct = ev.encrypt(ko, z, prm.scale, 37, level=0)
+    ev.log.clear()
+    want = plan.bootstrap_fft(ev, ko, ct, cfg)
+    olog = list(ev.log)
+    g.oplog(enable=True, clear=True)
+    got = g.bootstrap_fft(kg, P.up(ct), cfg["level"], cfg["K"], cfg["r"], cfg["poly"],
+                          [_dev_stage(t) for t in cfg["cts"]], _dev_stage(cfg["cts_im"]),
+                          [_dev_stage(t) for t in cfg["stc"]], _dev_stage(cfg["stc_im"]))
+    glog = g.oplog(enable=False, clear=True)
+    assert glog == olog
+    assert got.level == want.level == prm.L - plan.fft_boot_depth(groups, 7) and got.scale == want.scale
+    assert np.array_equal(P.down(got), want.data)
+    assert np.abs(g.decrypt(kg, got) - z).max() < 2 ** -12
+    b = g.boot_create_fft(prm.L, 16, 7, groups, prm.scale, bsgs=True)
+    assert b.steps() == rot
+    out = g.bootstrap_boot(kg, P.up(ct), b)
+    assert np.abs(g.decrypt(kg, out) - z).max() < 2 ** -12
+
+
+@pytest.mark.gpu
+def test_bootstrap_batch_stream_capture_replay(S):
+    """secpe_bootstrap_boot_batch on a non-default stream with the same buffers called four times (eager,
+    capture, replay, replay) on three DISTINCT ciphertexts: every output, every time, equals the
+    single-ciphertext bootstrap of its own input word for word (a per-ciphertext stride or graph-replay bug
+    would show up here)."""
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        g = S.Context(synth.PARAM_SETS["boot"], stream=stream.cuda_stream)
+        groups = [4, 4, 3]
+        b = g.boot_create_fft(g.L, 16, 7, groups, g.scale, bsgs=True)
+        kg = g.keygen(13, b.steps(), h=64)
+        n = 3
+        zs = [np.random.default_rng(60 + i).uniform(-1, 1, g.N // 2) for i in range(n)]
+        cb = g.new_ct(0, n)
+        for i, z in enumerate(zs):
+            g.encrypt_coeffs(kg, g.encode(z, g.scale), 0, g.scale, 50 + i, out=S.Ct(cb.t[i:i + 1], 0, g.scale))
+        cb.level, cb.scale = 0, g.scale
+        ol = g.L - plan.fft_boot_depth(groups, 7)
+        singles = []
+        for i in range(n):
+            o1 = g.bootstrap_boot(kg, S.Ct(cb.t[i:i + 1].clone(), 0, g.scale), b)
+            stream.synchronize()
+            singles.append(o1.t[0].cpu().numpy().copy())
+        out = g.new_ct(ol, n)
+        for rep in range(4):
+            out.t.zero_()
+            g.bootstrap_boot(kg, cb, b, out=out)
+            stream.synchronize()
+            got = out.t.cpu().numpy()
+            for i in range(n):
+                assert np.array_equal(got[i], singles[i]), (rep, i)
+        for i in range(n):
+            assert np.abs(g.decrypt(kg, out, i) - zs[i]).max() < 2 ** -12
+
+
+@pytest.mark.gpu
+def test_batch_overlap_rejected(S):
+    """An output batch that overlaps the input batch without sharing a start pointer is rejected (byte-range
+    check) by secpe_bootstrap_boot_batch and secpe_enc_argmax."""
+    g = S.Context(synth.PARAM_SETS["boot"])
+    b = g.boot_create_fft(g.L, 16, 7, [4, 4, 3], g.scale, bsgs=True)
+    kg = g.keygen(15, b.steps(), h=64)
+    cb = g.new_ct(0, 2)
+    cb.level, cb.scale = 0, g.scale
+    ol = g.L - plan.fft_boot_depth([4, 4, 3], 7)
+    words0 = cb.t[0].numel()
+    big = torch.zeros(2 * g.new_ct(ol, 1).t[0].numel() + 2 * words0, dtype=torch.uint64, device="cuda")
+    ins = big[words0: 3 * words0].view(2, *cb.t.shape[1:])      # inputs start one ciphertext into the buffer
+    outs = big[:2 * g.new_ct(ol, 1).t[0].numel()].view(2, *g.new_ct(ol, 1).t.shape[1:])
+    with pytest.raises(S.SecpeError):
+        g.bootstrap_boot(kg, S.Ct(ins, 0, g.scale), b, out=S.Ct(outs, ol, g.scale))
+    P = pair(S, "toy_argmax")
+    gp = P.gpu
+    lay = synth.LAYOUTS["toy"]
+    st = load_sign("sign_f1_f1.json")
+    kk = gp.keygen(17, plan.argmax_rotations(lay))
+    x = gp.new_ct(gp.L, 2)
+    x.level, x.scale = gp.L, gp.scale
+    ol2, _ = gp.argmax_info(lay, st, gp.L)
+    o = S.Ct(x.t.view(-1)[x.t[0].numel() // 2:][: 2 * gp.new_ct(ol2, 1).t[0].numel()].view(
+        2, *gp.new_ct(ol2, 1).t.shape[1:]), ol2, gp.scale)
+    with pytest.raises(S.SecpeError):
+        gp.enc_argmax(kk, x, lay, st, out=o)
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_argmax_boot_bench_config_n16(S):
+    """bench.py's N4 row exactly: boot_argmax16_g4 chain, four stage groups 3/4/4/4, K = 16, 8 distinct
+    ciphertexts per call (256 queries each).  Every label above the Sign margin is exact for every
+    ciphertext, and ciphertext 5 of the batch equals its single-ciphertext run word for word (property check:
+    the oracle cannot run this size; test_argmax_boot_k16_bit_exact pins the four-group plan at N = 2^12)."""
+    g = S.Context(synth.PARAM_SETS["boot_argmax16_g4"])
+    lay = synth.LAYOUTS["argmax_k16"]
+    st = load_sign("sign_7_15_15.json")
+    bs = 2.0 ** 50
+    groups = [3, 4, 4, 4]
+    b = g.boot_create_fft(g.L, 16, 7, groups, bs, bsgs=True)
+    assert g.L - plan.fft_boot_depth(groups, 7) == 16
+    kg = g.keygen(synth.KEY_SEED_BASE + 39, sorted(set(plan.argmax_rotations(lay))) + b.steps(), h=64)
+    B = 8
+    scs = [synth.softmax_scores(47 + i, lay["queries"], lay["prompts"], lay["classes"]) for i in range(B)]
+    cts = [g.encrypt(kg, plan.pack(sc, lay, g.N // 2), 16, g.scale, 49 + i) for i, sc in enumerate(scs)]
+    batch = S.Ct(torch.cat([c.t for c in cts]), 16, g.scale)
+    out = g.enc_argmax_boot(kg, batch, lay, st, b, bs)
+    one = g.enc_argmax_boot(kg, cts[5], lay, st, b, bs)
+    assert one.level == out.level and one.scale == out.scale
+    assert torch.equal(one.t[0], out.t[5])
+    for i, scores in enumerate(scs):
+        dec = g.decrypt(kg, out, i)
+        mean = scores.mean(axis=1)
+        srt = np.sort(mean, axis=1)
+        ok = srt[:, -1] - srt[:, -2] >= 2.0 ** -7
+        assert ok.sum() >= 180
+        assert (S.labels(dec, lay)[ok] == plan.true_labels(scores)[ok]).all(), i
+
+
+@pytest.mark.gpu
+def test_keygen_os_entropy_and_seed_modes(S):
+    """Reading R6: seed=None draws the 256-bit master seed from OS entropy (two unseeded keygens differ and
+    still decrypt); an explicit 32-byte seed is deterministic and equals the oracle's keys; the integer
+    (test-only) mode is the 32-byte seed LE64(s) || 0^24."""
+    P = pair(S, "toy")
+    g, ev = P.gpu, ckks.Oracle(P.prm)
+    k1, k2 = g.keygen(None), g.keygen(None)
+    assert not np.array_equal(k1.export(0), k2.export(0))
+    z = np.random.default_rng(4).uniform(-1, 1, g.N // 2)
+    for k in (k1, k2):
+        assert np.abs(g.decrypt(k, g.encrypt(k, z, g.L, g.scale, None)) - z).max() < 2 ** -20
+    raw = bytes(range(7, 39))
+    kb, ko = g.keygen(raw), ev.keygen(raw)
+    assert np.array_equal(kb.export(0), ko.s_ntt) and np.array_equal(kb.export(1), ko.pk)
+    s = 0x0123456789ABCDEF
+    assert np.array_equal(g.keygen(s).export(0), g.keygen(s.to_bytes(8, "little") + bytes(24)).export(0))

@@ -16,7 +16,8 @@ import mpmath
 import synth
 from oracle import ckks, plan
 
-GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_examples.json")))
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = json.load(open(os.path.join(HERE, "golden", "paper_examples.json")))
 
 
 @pytest.fixture(scope="module")
@@ -123,22 +124,56 @@ def test_ntt_roundtrip_and_convolution(toy):
 # ---------------------------------------------------------------------------------------------
 # O-6 sampler
 # ---------------------------------------------------------------------------------------------
-def test_splitmix_stream_matches_sequential_generator():
-    # the counter form equals the sequential SplitMix64 recurrence started at s0
-    M = (1 << 64) - 1
-    G = 0x9E3779B97F4A7C15
+CHACHA = json.load(open(os.path.join(HERE, "golden", "chacha20.json")))
 
-    def mix(z):
-        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
-        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
-        return z ^ (z >> 31)
 
-    seed, tag = 12345, ckks.lib().o_tag(4, 5, 2)
-    assert tag == (4 << 48) ^ (5 << 8) ^ 2
-    state = mix(seed ^ mix((tag + G) & M))
-    for ctr in range(6):
-        state = (state + G) & M
-        assert ckks.lib().o_draw(seed, tag, ctr) == mix(state)
+def _keystream(key_words, counter, nonce, nbytes=64):
+    """Independent ChaCha20 (the `cryptography` package): its 16-byte nonce is state words 12-15."""
+    from cryptography.hazmat.primitives.ciphers import Cipher, algorithms
+    iv = int(counter).to_bytes(8, "little") + int(nonce).to_bytes(8, "little")
+    key = np.asarray(key_words, dtype="<u4").tobytes()
+    return Cipher(algorithms.ChaCha20(key, iv), mode=None).encryptor().update(bytes(nbytes))
+
+
+def test_chacha20_block_vectors():
+    """R6 sampler core: the oracle's ChaCha20 block equals the RFC 7539 test vectors
+    (tests/golden/chacha20.json) and an independent implementation on random keys/counters/nonces."""
+    for v in CHACHA["vectors"]:
+        key = np.frombuffer(bytes.fromhex(v["key_hex"]), dtype="<u4")
+        got = ckks.chacha20_block(key, v["counter"], v["nonce"]).astype("<u4").tobytes()
+        assert got.hex() == v["block_hex"], v["source"]
+    rng = np.random.default_rng(5)
+    for _ in range(8):
+        key = rng.integers(0, 1 << 32, 8, dtype=np.uint64).astype(np.uint32)
+        ctr, nonce = int(rng.integers(0, 1 << 63)), int(rng.integers(0, 1 << 63))
+        got = ckks.chacha20_block(key, ctr, nonce).astype("<u4").tobytes()
+        assert got == _keystream(key, ctr, nonce)
+
+
+def test_chacha_streams_and_key_domains():
+    """draw ctr = 64-bit word ctr mod 8 of block ctr / 8 of the object's stream (nonce = tag); object keys are
+    the first 32 bytes of block 0 under the master seed with nonce DOM_SK (secret material: s, e; tags 1, 3, 5),
+    DOM_PK (public material: the uniform a of pk / switching keys; tags 2, 4) or DOM_ENC (encryption)."""
+    L = ckks.lib()
+    master = ckks.seed_key(0x1234567890ABCDEF)
+    assert list(master[:2]) == [0x90ABCDEF, 0x12345678] and not master[2:].any()
+    assert np.array_equal(ckks.seed_key(bytes(range(32))), np.frombuffer(bytes(range(32)), dtype="<u4"))
+    doms = {1: 0x5345435045534B31, 3: 0x5345435045534B31, 5: 0x5345435045534B31,
+            2: 0x5345435045504B31, 4: 0x5345435045504B31}
+    for kind, dom in doms.items():
+        tag = L.o_tag(kind, 5, 2)
+        assert tag == (kind << 48) ^ (5 << 8) ^ 2
+        k = ckks.object_key(master, tag)
+        assert k.astype("<u4").tobytes() == _keystream(master, 0, dom)[:32], kind
+        ks = _keystream(k, 0, tag, 128)
+        for ctr in range(16):
+            want = int.from_bytes(ks[8 * ctr: 8 * ctr + 8], "little")
+            assert L.o_draw(k.ctypes.data_as(ckks.u32p), tag, ctr) == want
+    ke = np.zeros(8, dtype=np.uint32)
+    L.o_encrypt_key(master.ctypes.data_as(ckks.u32p), ke.ctypes.data_as(ckks.u32p))
+    assert ke.astype("<u4").tobytes() == _keystream(master, 0, 0x5345435045454E31)[:32]
+    # public and secret material never share a stream key
+    assert not np.array_equal(ckks.object_key(master, L.o_tag(1, 0, 0)), ckks.object_key(master, L.o_tag(2, 0, 0)))
 
 
 def test_cdt_table_mpmath():
@@ -157,13 +192,15 @@ def test_cdt_table_mpmath():
 def test_sampler_moments(toy):
     L = ckks.lib()
     n = 1 << 16
+    k7 = ckks.seed_key(7)
+    K = k7.ctypes.data_as(ckks.u32p)
     t = np.zeros(n, dtype=np.int64)
-    L.o_sample_ternary(7, 99, 16, ckks.P(t))
+    L.o_sample_ternary(K, 99, 16, ckks.P(t))
     counts = np.bincount(t + 1, minlength=3)
     chi2 = ((counts - n / 3) ** 2 / (n / 3)).sum()
     assert set(np.unique(t)) <= {-1, 0, 1} and chi2 < 20
     e = np.zeros(n, dtype=np.int64)
-    L.o_sample_gauss(7, 98, 16, ckks.P(toy.cdt), len(toy.cdt), ckks.P(e))
+    L.o_sample_gauss(K, 98, 16, ckks.P(toy.cdt), len(toy.cdt), ckks.P(e))
     assert abs(e.mean()) < 0.05 and abs(e.std() - 3.2) < 0.05 and np.abs(e).max() <= 19
     # exact discrete Gaussian pmf vs histogram (chi^2 over |e| <= 8)
     rho = np.exp(-np.arange(-19, 20) ** 2 / (2 * 3.2 ** 2))
@@ -173,7 +210,7 @@ def test_sampler_moments(toy):
     assert ((hist - exp) ** 2 / exp).sum() < 60
     # uniform mod q: mean and bucket chi^2
     q = toy.primes[0]
-    u = np.array([L.o_uniform(3, 5, 0, k, 12, q) for k in range(4096)], dtype=np.float64)
+    u = np.array([L.o_uniform(K, 5, 0, k, 12, q) for k in range(4096)], dtype=np.float64)
     assert u.max() < q and abs(u.mean() / q - 0.5) < 0.02
     h = np.histogram(u / q, bins=16, range=(0, 1))[0]
     assert ((h - 256) ** 2 / 256).sum() < 45
@@ -194,8 +231,10 @@ def test_switching_key_gadget_identity(tiny):
     L = ckks.lib()
     N, ne = prm.N, prm.nq + prm.np_
     # the secret itself: ternary stream, NTT by definition
+    master = ckks.seed_key(11)
+    ks = ckks.object_key(master, L.o_tag(1, 0, 0))
     s = np.zeros(N, dtype=np.int64)
-    L.o_sample_ternary(11, L.o_tag(1, 0, 0), prm.logn, ckks.P(s))
+    L.o_sample_ternary(ks.ctypes.data_as(ckks.u32p), L.o_tag(1, 0, 0), prm.logn, ckks.P(s))
     for t in range(ne):
         q = prm.primes[t]
         assert [int(v) for v in keys.s_ntt[t]] == ntt_def([int(x) % q for x in s], q, prm.psi[t], prm.logn)
@@ -204,7 +243,9 @@ def test_switching_key_gadget_identity(tiny):
         P_ *= p
     for j in range(prm.beta(prm.L)):
         e = np.zeros(N, dtype=np.int64)
-        L.o_sample_gauss(11, L.o_tag(5, 0, j), prm.logn, ckks.P(prm.cdt), len(prm.cdt), ckks.P(e))
+        ke = ckks.object_key(master, L.o_tag(5, 0, j))
+        L.o_sample_gauss(ke.ctypes.data_as(ckks.u32p), L.o_tag(5, 0, j), prm.logn, ckks.P(prm.cdt), len(prm.cdt),
+                         ckks.P(e))
         for t in range(ne):
             q = prm.primes[t]
             en = ntt_def([int(x) % q for x in e], q, prm.psi[t], prm.logn)
@@ -567,7 +608,51 @@ def test_paper_layout_and_op_law():
         if n <= 4:
             assert calls["sign"] == int(math.log2(n)) + 1
             assert mir.counts["ROT"] == int(math.log2(n)) + 1
-    assert GOLD["op_law"]["sign_ops"] == int(math.log2(GOLD["op_law"]["n"])) + 1
+
+
+def _count_argmax_boot(n, prompts):
+    """Sign calls, ROT ops and refreshes of plan.argmax_boot on the plaintext mirror (the op list the oracle
+    and the library both run), with a mirror bootstrap that returns its input at the post-bootstrap level."""
+    prm = ckks.Params(synth.PARAM_SETS["boot_argmax"])
+    st = json.load(open(os.path.join(HERE, "..", "data", "sign_7_15_15.json")))["coeffs"]
+    st = [list(map(float, c)) for c in st]
+    mir = ckks.Mirror(prm)
+    lay = dict(queries=1, prompts=prompts, classes=n, block=2 * n * prompts)
+    out_level = prm.L - plan.fft_boot_depth([4, 4, 3], 7)
+    calls = {"sign": 0, "boot": 0}
+    orig = plan.sign
+
+    def counting(ev, keys, x, stages, s):
+        calls["sign"] += 1
+        return orig(ev, keys, x, stages, s)
+
+    def boot(c):
+        calls["boot"] += 1
+        assert c.level == 0
+        return ckks.MirrorCt(c.v.copy(), out_level, c.scale)
+    z = np.zeros(prm.N // 2)
+    z[: n * prompts] = np.linspace(0, 1, n * prompts)
+    plan.sign = counting
+    try:
+        plan.argmax_boot(mir, None, ckks.MirrorCt(z, 16, prm.scale), lay, st, boot, 2.0 ** 50)
+    finally:
+        plan.sign = orig
+    return calls["sign"], mir.counts.get("ROT", 0), calls["boot"]
+
+
+@pytest.mark.parametrize("n,prompts", [(2, 1), (16, 1), (256, 1), (16, 8), (256, 2)])
+def test_op_law_counts(n, prompts):
+    """PAPER.md:419 (Sec. 4.5): Algorithm 1 on a length-n input needs (log n + 1) Sign operations and
+    (log n + 1) rotations; n = 256 -> 9 Sign, 9 rotations.  Counted through the planned circuit
+    (plan.argmax_boot on the mirror, refreshes included where the level budget runs out); the prompt
+    aggregation adds log2 P rotations on top."""
+    signs, rots, boots = _count_argmax_boot(n, prompts)
+    ln = int(math.log2(n))
+    assert signs == ln + 1
+    assert rots == ln + 1 + int(math.log2(prompts))
+    if n == 256 and prompts == 1:
+        assert (signs, rots) == (GOLD["op_law"]["sign_ops"], GOLD["op_law"]["rotations"])
+    assert boots >= (1 if n >= 16 else 0)
 
 
 def test_argmax_mirror_examples():
@@ -676,22 +761,15 @@ def boot_tiny():
 def test_sparse_secret(boot_tiny):
     """R36: the sparse secret has exactly h nonzeros, all +-1, is a function of the seed alone, and its first
     nonzero sits where the first draw's top log N bits point (the sampler's definition, recomputed here
-    from SplitMix64)."""
+    with an independent ChaCha20)."""
     prm, ev, keys = boot_tiny
     s = keys.s
     assert np.count_nonzero(s) == BOOT_TINY["h"] and set(np.unique(s)) <= {-1, 0, 1}
     assert np.array_equal(ev.keygen(7, (), h=BOOT_TINY["h"]).s, s)
     assert not np.array_equal(ev.keygen(8, (), h=BOOT_TINY["h"]).s, s)
-    M = (1 << 64) - 1
-    G = 0x9E3779B97F4A7C15
-
-    def mix(z):
-        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
-        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
-        return z ^ (z >> 31)
     tag = 1 << 48
-    s0 = mix(7 ^ mix((tag + G) & M))
-    x = mix((s0 + G) & M)
+    k = ckks.object_key(ckks.seed_key(7), tag)
+    x = int.from_bytes(_keystream(k, 0, tag)[:8], "little")
     assert s[x >> (64 - prm.logn)] == (-1 if x & 1 else 1)
 
 
