@@ -251,8 +251,8 @@ def layout(d):
 
 
 class Keys:
-    def __init__(self, ctx, handle, fft):
-        self.ctx, self.h, self.fft = ctx, handle, fft
+    def __init__(self, ctx, handle):
+        self.ctx, self.h = ctx, handle
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:
@@ -272,8 +272,8 @@ class Keys:
 class Boot:
     """secpe_boot handle: library-built bootstrapping material (device memory owned by the library)."""
 
-    def __init__(self, ctx, handle):
-        self.ctx, self.h = ctx, handle
+    def __init__(self, ctx, handle, fft):
+        self.ctx, self.h, self.fft = ctx, handle, fft
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:
