@@ -446,6 +446,11 @@ int secpe_oplog_clear(secpe_ctx *ctx);
  * out[3k], ciphertexts in out[3k+2]).  Returns SECPE_EINVAL when n_out < 12. */
 int secpe_profile_begin(secpe_ctx *ctx);
 int secpe_profile_end(secpe_ctx *ctx, double *out, int32_t n_out);
+/* Development switch of the N = 2^16 exact-FP64 NTT implementation (process-wide; SECPE_NTT_FUSED sets the
+ * initial value): 0 = the two-pass kernels everywhere, 1 = the persistent TMA-pipelined single-launch kernel
+ * (ntt_fused.cu) for every exact-FP64 run, 2 (default) = the fused kernel for plain transforms of >= 1024
+ * limb rows only.  Both give identical words.  mode < 0 queries.  Returns the previous mode. */
+int32_t secpe_ntt_mode(int32_t mode);
 /* host counts[8]: NTT limb-transforms, key switches, rescales, rotations, ct-ct products,
  * constant products, kernel launches, Sign evaluations. */
 int secpe_opcounts(secpe_ctx *ctx, int64_t *counts, int32_t reset);

@@ -17,7 +17,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-ffp-contract=off",
          "-Xptxas", "-warn-spills"]
-SOURCES = ["ntt.cu", "ops.cu", "ks.cu", "bconv_tc.cu", "sample.cu", "context.cu", "eval.cu", "plan.cu", "client.cu",
+SOURCES = ["ntt.cu", "ntt_fused.cu", "ops.cu", "ks.cu", "bconv_tc.cu", "sample.cu", "context.cu", "eval.cu", "plan.cu", "client.cu",
            "encode.cpp", "boot.cpp", "abi.cpp"]
 
 

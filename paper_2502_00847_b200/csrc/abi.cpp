@@ -3,6 +3,8 @@
 // thread-local message (secpe_last_error).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -1137,18 +1139,24 @@ int secpe_profile_end(secpe_ctx *ctx, double *out, int32_t n_out) {
         CUDA_CHECK(cudaStreamSynchronize(ctx->c.st));
         p.on = false;
         for (int i = 0; i < n_out; i++) out[i] = 0;
+        // development: SECPE_PROF_DUMP=<file> appends every span (kind, units, bytes, ms)
+        const char *dump = getenv("SECPE_PROF_DUMP");
+        FILE *df = dump ? fopen(dump, "a") : nullptr;
         for (const auto &s : p.spans) {
-            if (3 * s.kind + 2 >= n_out) continue;  // stage spans (kinds 4..8) only when asked for
             float ms = 0;
             CUDA_CHECK(cudaEventElapsedTime(&ms, p.pool[s.a], p.pool[s.b]));
+            if (df) fprintf(df, "%d %.1f %.0f %.6f\n", s.kind, (double)s.units, s.bytes, ms);
+            if (3 * s.kind + 2 >= n_out) continue;  // stage spans (kinds 4..8) only when asked for
             out[3 * s.kind + 0] += ms;
             out[3 * s.kind + 1] += s.bytes;
             out[3 * s.kind + 2] += (double)s.units;
         }
+        if (df) fclose(df);
         p.spans.clear();
         p.used = 0;
     });
 }
+int32_t secpe_ntt_mode(int32_t mode) { return ntt_fused_mode(mode); }
 int secpe_opcounts(secpe_ctx *ctx, int64_t *counts, int32_t reset) {
     return guard([&] {
         REQUIRE(ctx && counts, SECPE_EINVAL, "null argument");

@@ -78,6 +78,9 @@ struct Tab {
     const double *qd;  // [P] (double) q and RN(1 / q): no per-CTA int->double conversion or division
     const double *qinv;
     int ntt_cluster;   // host-visible: single-pass cluster NTT for 0 none, 1 FP rows, 2 all rows (SECPE_NTT_CLUSTER)
+    // [P][N] {w, RN(w RN(1/q))} as doubles for the exact-FP64 rows (fused kernel, ntt_fused.cu); integer rows:
+    // the same pointer as tw2 / itw2 ({w, Shoup companion})
+    const ulonglong2 *twp = nullptr, *itwp = nullptr;
 };
 
 // limb l of a polynomial -> global prime index

@@ -461,6 +461,36 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
     }
     for (int i = 0; i < P && i < 64; i++)
         if (primes[i] < (1ULL << 46)) tab.fp_mask |= 1ULL << i;
+    // {w, w/q} pair tables of the exact-FP64 rows for the fused NTT (its row-tile stages read one 16-byte pair
+    // per twiddle instead of forming w/q with a DMUL); integer rows keep their {w, w'} tables
+    tab.twp = tab.tw2;
+    tab.itwp = tab.itw2;
+    if (tab.fp_mask) {
+        std::vector<u64> tp(2 * (size_t)P * N), itp(2 * (size_t)P * N);
+        for (int i = 0; i < P; i++) {
+            const size_t o = 2 * (size_t)i * N;
+            if (primes[i] < (1ULL << 46)) {
+                const double qinv = 1.0 / (double)primes[i];
+                for (long k = 0; k < N; k++) {
+                    double w, iw;
+                    std::memcpy(&w, &tw[o + k], 8);
+                    std::memcpy(&iw, &itw[o + k], 8);
+                    const double wq = w * qinv, iwq = iw * qinv;
+                    std::memcpy(&tp[o + 2 * k], &w, 8);
+                    std::memcpy(&tp[o + 2 * k + 1], &wq, 8);
+                    std::memcpy(&itp[o + 2 * k], &iw, 8);
+                    std::memcpy(&itp[o + 2 * k + 1], &iwq, 8);
+                }
+            } else {
+                std::copy(tw.begin() + o, tw.begin() + o + 2 * N, tp.begin() + o);
+                std::copy(itw.begin() + o, itw.begin() + o + 2 * N, itp.begin() + o);
+            }
+        }
+        d_twp = upload(tp, st);
+        d_itwp = upload(itp, st);
+        tab.twp = reinterpret_cast<const ulonglong2 *>(d_twp.p);
+        tab.itwp = reinterpret_cast<const ulonglong2 *>(d_itwp.p);
+    }
 
     // ModDown constants: P = prod p
     std::vector<u64> vihp(std::max(np, 1)), vihpsh(std::max(np, 1)), vhatp((size_t)std::max(np, 1) * nq),

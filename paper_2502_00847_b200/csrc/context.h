@@ -114,7 +114,7 @@ struct Ctx {
     std::vector<u64> primes, psi;  // q_0..q_L, p_0..p_{k-1}
     cudaStream_t st = nullptr;
     // tables
-    DevBuf d_q, d_br0, d_br1, d_tw, d_itw, d_ninv, d_ninvsh, d_qd, d_qinv;
+    DevBuf d_q, d_br0, d_br1, d_tw, d_itw, d_ninv, d_ninvsh, d_qd, d_qinv, d_twp, d_itwp;
     Tab tab{};
     // ModDown constants
     DevBuf ihp, ihp_sh, hat_p, pinv, pinv_sh;  // hat_p split-30 packed

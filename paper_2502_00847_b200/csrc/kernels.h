@@ -73,6 +73,13 @@ struct NttSeg {
 void ntt_segments(const Tab &tab, int logn, const NttSeg *segs, int nseg, bool inverse, cudaStream_t st);
 void ntt_inverse(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
                  const NttFusion &f = NttFusion());
+// persistent TMA-pipelined single-launch transform (ntt_fused.cu, N = 2^16, exact-FP64 rows) of limbs
+// [limb0, limb0 + nsub) of n_polys polynomials; returns false when it does not apply (caller falls back to
+// the two-pass kernels).  SECPE_NTT_FUSED=0 disables it.
+bool ntt_fused_enabled();
+int ntt_fused_mode(int mode);  // sets SECPE_NTT_FUSED's mode (mode < 0: query); returns the previous one
+bool ntt_fused_run(const Tab &tab, int logn, RowsArg d, int n_polys, LimbMap lm, int limb0, int nsub, bool fp,
+                   bool inverse, const NttFusion &f, cudaStream_t st);
 
 void k_addsub(const Tab &tab, int logn, CRows a, CRows b, RowsArg out, int n_polys, LimbMap lm,
               bool sub, cudaStream_t st);

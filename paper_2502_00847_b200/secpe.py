@@ -168,6 +168,7 @@ SIGS = {
     "secpe_oplog_get": (ctypes.c_int64, [vp, ctypes.c_char_p, ctypes.c_size_t]),
     "secpe_oplog_clear": (ctypes.c_int, [vp]),
     "secpe_opcounts": (ctypes.c_int, [vp, i64p, ctypes.c_int32]),
+    "secpe_ntt_mode": (ctypes.c_int32, [ctypes.c_int32]),
     "secpe_profile_begin": (ctypes.c_int, [vp]),
     "secpe_profile_end": (ctypes.c_int, [vp, f64p, ctypes.c_int32]),
 }
@@ -193,6 +194,11 @@ def lib():
 
 class SecpeError(RuntimeError):
     pass
+
+
+def ntt_mode(mode=-1):
+    """secpe_ntt_mode: development switch of the N = 2^16 FP64-row NTT (0 two-pass, 1 fused, 2 auto)."""
+    return lib().secpe_ntt_mode(mode)
 
 
 def _chk(code):

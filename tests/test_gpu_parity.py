@@ -1489,3 +1489,56 @@ def test_keygen_os_entropy_and_seed_modes(S):
     assert np.array_equal(kb.export(0), ko.s_ntt) and np.array_equal(kb.export(1), ko.pk)
     s = 0x0123456789ABCDEF
     assert np.array_equal(g.keygen(s).export(0), g.keygen(s.to_bytes(8, "little") + bytes(24)).export(0))
+
+
+@pytest.mark.gpu
+def test_fused_ntt_matches_two_pass_and_oracle(S):
+    """The persistent TMA-pipelined NTT (ntt_fused.cu, secpe_ntt_mode 1) against the two-pass kernels (mode 0) on
+    the configs[4] exact-FP64 rows: plain forward / inverse transforms of ragged shapes (1 .. 1856 limb rows,
+    offset limbs, special primes, worst-case all-(q-1) input) give identical words and equal the oracle on
+    sampled limbs; the fused prologues / epilogues (relinearise-and-rescale, rescale, rotation, whole argmax)
+    give identical ciphertexts."""
+    P = pair(S, "argmax")
+    prm, g = P.prm, P.gpu
+    prev = S.ntt_mode(-1)
+    try:
+        for n_polys, first, n_limbs in ((1, 3, 1), (3, 0, 7), (2, 25, 15), (64, 1, 29)):
+            primes = prm.primes[first:first + n_limbs]
+            x = synth.uniform_residues(300 + n_polys, primes, n_polys, prm.logn)
+            if n_polys == 3:
+                x[1] = np.array(primes, dtype=np.uint64)[:, None] - np.uint64(1)
+            outs = {}
+            for mode in (0, 1):
+                S.ntt_mode(mode)
+                t = torch.from_numpy(x.copy()).cuda()
+                g.ntt(t, first, n_limbs)
+                f = t.cpu().numpy()
+                g.ntt(t, first, n_limbs, inverse=True)
+                outs[mode] = (f, t.cpu().numpy())
+            assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+            assert np.array_equal(outs[1][1], x)
+            pi, l = n_polys - 1, n_limbs - 1
+            assert np.array_equal(outs[1][0][pi, l], ckks.ntt(x[pi, l], primes[l], prm.psi[first + l], prm.logn))
+        # fused prologue / epilogue modes inside the evaluator: word-for-word equal under both implementations
+        lay = synth.LAYOUTS["argmax_k2"]
+        st = load_sign("sign_7_15_15.json")
+        kg = g.keygen(synth.KEY_SEED_BASE + 61, plan.argmax_rotations(lay))
+        cts = []
+        for i in range(2):
+            sc = synth.softmax_scores(600 + i, lay["queries"], lay["prompts"], lay["classes"])
+            cts.append(g.encrypt(kg, plan.pack(sc, lay, g.N // 2), g.L, g.scale, 610 + i))
+        res = {}
+        for mode in (0, 1):
+            S.ntt_mode(mode)
+            a, b = cts
+            m = g.mul_relin_rescale(kg, a, b)
+            r = g.rotate(kg, a, 2)
+            rs = g.rescale(a)
+            batch = S.Ct(torch.cat([c.t for c in cts]), g.L, g.scale)
+            am = g.enc_argmax(kg, batch, lay, st)
+            torch.cuda.synchronize()
+            res[mode] = [x.t.cpu().numpy() for x in (m, r, rs, am)]
+        for u, v in zip(res[0], res[1]):
+            assert np.array_equal(u, v)
+    finally:
+        S.ntt_mode(prev)
