@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
     pdl_wait();  // TMEM, constants and the B matrix above do not depend on the previous kernel
     if ((int)blockIdx.x < ntiles) fetch(blockIdx.x);
     int it = 0;
+    u64 rrv = 0;  // fused ModDown + rescale: r of this thread's coefficient
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
         const long k0 = (long)tile * TC_M;
 #pragma unroll
@@ -150,90 +151,109 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
         }
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         if (tile + (int)gridDim.x < ntiles) fetch(tile + gridDim.x);  // overlaps the epilogue below
-        // epilogue: 8 int32 byte-plane sums per target -> value < 2^80 -> reduced with an FP64 quotient
-        // V = lo + hi 2^32 with lo, hi < 2^48; k = floor(V / t) from doubles is off by at most one, so
-        // r = V - k t (exact, mod 2^64) lies in [-t, 2t) and two corrections make it canonical.
-        auto tld = [&](int t, uint32_t (&g)[8]) {
-            const uint32_t lane_base = tmem + ((uint32_t)(32 * lq) << 16);
-            if (planes == 8) {
-                asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                             : "=r"(g[0]), "=r"(g[1]), "=r"(g[2]), "=r"(g[3]), "=r"(g[4]), "=r"(g[5]), "=r"(g[6]),
-                               "=r"(g[7])
-                             : "r"(lane_base + (uint32_t)(8 * t)));
-            } else {
-                const uint32_t a6 = lane_base + (uint32_t)(6 * t);
-                asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n"
-                             : "=r"(g[0]), "=r"(g[1]) : "r"(a6));
-                asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n"
-                             : "=r"(g[2]), "=r"(g[3]) : "r"(a6 + 2));
-                asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n"
-                             : "=r"(g[4]), "=r"(g[5]) : "r"(a6 + 4));
-                g[6] = g[7] = 0;
-            }
+        // epilogue: per target, the byte-plane sums G_b (< 96 * 255^2 < 2^23) -> V = sum_b G_b 256^b -> V mod t.
+        // 6 planes (targets < 2^46): V < 2^64 is one u64 (three wide multiply-adds + two 32-bit adds on the
+        // high word); 8 planes: V = lo + hi 2^32 with lo, hi < 2^47.  The quotient k = rint(V / t) comes from
+        // FP64 (V as a double: two exact conversions and one FMA; k = fma(V, 1/t, 1.5 2^52) - its low word
+        // is k, k < 2^21), r = V - k t is exact mod 2^64 and lies in (-t, t): one conditional add of t.
+        // Each warp takes a contiguous block of targets so two targets' planes come in with one or two
+        // TMEM loads (12 or 16 consecutive columns).
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * lq) << 16);
+        auto v6 = [](const uint32_t *g) -> u64 {
+            u64 v = (u64)g[0] + (u64)g[1] * 256u;
+            v += (u64)g[2] * 65536u;
+            v += (u64)g[3] * 16777216u;
+            return v + ((u64)(g[4] + g[5] * 256u) << 32);
         };
-        auto tld_wait = [] { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); };
-        // 6-plane epilogue (constants < 2^48): the same quotient reduction with the two zero planes
-        // dropped (hi = G4 + G5 2^8 < 2^32 is a plain 32-bit value)
-        auto reduce6 = [&](const uint32_t (&g)[8], int t) -> u64 {
+        auto to_d = [](u64 x) -> double {  // exact for x < 2^52
+            return __dsub_rn(__longlong_as_double((long long)(x | 0x4330000000000000ULL)), 4503599627370496.0);
+        };
+        // V given as lo + hi 2^32 (hi < 2^32 for 6 planes, < 2^47 for 8), V mod 2^64 = vw.  6 planes: V < 2^64
+        // and t > 2^40, so k < 2^24 (32-bit product); 8 planes: V < 2^79, k < 2^39 (64-bit product)
+        auto reduce = [&](u64 lo, u64 hi, u64 vw, int t, bool wide) -> u64 {
             const u64 q = sq[t];
-            const u64 lo = (u64)g[0] + ((u64)g[1] << 8) + ((u64)g[2] << 16) + ((u64)g[3] << 24);
-            const uint32_t hi = g[4] + (g[5] << 8);
-            const double two52 = 4503599627370496.0;
-            const double lod = __dsub_rn(__longlong_as_double((long long)(lo | 0x4330000000000000ULL)), two52);
-            const double hid = __dsub_rn(__hiloint2double(0x43300000, (int)hi), two52);
-            const double vd = __fma_rn(hid, 4294967296.0, lod);
-            const double kd = floor(__dmul_rn(vd, sqinv[t]));
-            const u64 k = (u64)__double_as_longlong(__dadd_rn(kd, two52)) & ((1ULL << 52) - 1);
-            long long r = (long long)(lo + ((u64)hi << 32) - k * q);
-            if (r < 0) r += (long long)q;
-            if ((u64)r >= q) r -= (long long)q;
-            return (u64)r;
+            const double vd = __fma_rn(to_d(hi), 4294967296.0, to_d(lo));
+            const double kb = __fma_rn(vd, sqinv[t], 6755399441055744.0);  // k + 1.5 2^52
+            const u64 kq = wide ? ((u64)__double_as_longlong(kb) & ((1ULL << 51) - 1)) * q
+                                : (u64)(uint32_t)__double_as_longlong(kb) * q;
+            const long long r = (long long)(vw - kq);
+            return (u64)(r + ((r >> 63) & (long long)q));
         };
-        auto reduce_g = [&](const uint32_t (&g)[8], u64 q, double qinv) -> u64 {
-            const u64 lo = (u64)g[0] + ((u64)g[1] << 8) + ((u64)g[2] << 16) + ((u64)g[3] << 24);
-            const u64 hi = (u64)g[4] + ((u64)g[5] << 8) + ((u64)g[6] << 16) + ((u64)g[7] << 24);
-            const double two52 = 4503599627370496.0;
-            const double lod = __dsub_rn(__longlong_as_double((long long)(lo | 0x4330000000000000ULL)), two52);
-            const double hid = __dsub_rn(__longlong_as_double((long long)(hi | 0x4330000000000000ULL)), two52);
-            const double vd = __fma_rn(hid, 4294967296.0, lod);
-            const double kd = floor(__dmul_rn(vd, qinv));
-            const u64 k = (u64)__double_as_longlong(__dadd_rn(kd, two52)) & ((1ULL << 52) - 1);
-            long long r = (long long)(lo + (hi << 32) - k * q);
-            if (r < 0) r += (long long)q;
-            if ((u64)r >= q) r -= (long long)q;
-            return (u64)r;
+        auto emit = [&](u64 z, int t) {
+            if (a.rr) z = addmod(z, csub(mul_shoup(rrv, spm[t], spmsh[t], sq[t]), sq[t]), sq[t]);
+            dst[soff[t] + k0 + m] = z;
         };
-        int t0 = 0;
-        u64 r = 0;
         if (a.rr) {
             // fused ModDown + rescale prelude (target 0 = q_l): Y_l = (xc - T_l) P^{-1}, r = [Y_l + floor(q_l/2)]
             const u64 ql = sq[0];
             uint32_t g[8];
-            tld(0, g);
-            tld_wait();
-            const u64 tl = planes == 6 ? reduce6(g, 0) : reduce_g(g, ql, sqinv[0]);
-            const u64 xc = src[(long)(-1) * N + k0 + m];
-            r = csub(mul_shoup(submod(xc, tl, ql), a.pinv_l, a.pinv_l_sh, ql) + (ql >> 1), ql);
-            t0 = 1;
-        }
-        // two targets per TMEM wait: both loads are in flight together
-        for (int t = t0 + tpar; t < nt; t += 8) {
-            const int t2 = t + 4;
-            uint32_t g[8], h[8];
-            tld(t, g);
-            if (t2 < nt) tld(t2, h);
-            tld_wait();
-            {
-                const u64 q = sq[t];
-                u64 z = planes == 6 ? reduce6(g, t) : reduce_g(g, q, sqinv[t]);
-                if (a.rr) z = addmod(z, csub(mul_shoup(r, spm[t], spmsh[t], q), q), q);
-                dst[soff[t] + k0 + m] = z;
+            if (planes == 6) {
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                             : "=r"(g[0]), "=r"(g[1]), "=r"(g[2]), "=r"(g[3]) : "r"(lane_base));
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n"
+                             : "=r"(g[4]), "=r"(g[5]) : "r"(lane_base + 4));
+            } else {
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                             : "=r"(g[0]), "=r"(g[1]), "=r"(g[2]), "=r"(g[3]), "=r"(g[4]), "=r"(g[5]), "=r"(g[6]),
+                               "=r"(g[7])
+                             : "r"(lane_base));
             }
-            if (t2 < nt) {
-                const u64 q = sq[t2];
-                u64 z = planes == 6 ? reduce6(h, t2) : reduce_g(h, q, sqinv[t2]);
-                if (a.rr) z = addmod(z, csub(mul_shoup(r, spm[t2], spmsh[t2], q), q), q);
-                dst[soff[t2] + k0 + m] = z;
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            u64 tl;
+            if (planes == 6) {
+                const u64 v = v6(g);
+                tl = reduce(v & 0xFFFFFFFFULL, v >> 32, v, 0, false);
+            } else {
+                const u64 lo = (u64)g[0] + (u64)g[1] * 256u + (u64)g[2] * 65536u + (u64)g[3] * 16777216u;
+                const u64 hi = (u64)g[4] + (u64)g[5] * 256u + (u64)g[6] * 65536u + (u64)g[7] * 16777216u;
+                tl = reduce(lo, hi, lo + (hi << 32), 0, true);
+            }
+            const u64 xc = src[(long)(-1) * N + k0 + m];
+            rrv = csub(mul_shoup(submod(xc, tl, ql), a.pinv_l, a.pinv_l_sh, ql) + (ql >> 1), ql);
+        }
+        const int t0 = a.rr ? 1 : 0;
+        const int per = (nt - t0 + 3) >> 2;  // targets per warp group (contiguous)
+        const int tb = t0 + tpar * per, te = min(nt, tb + per);
+        if (planes == 6) {
+            for (int t = tb; t < te; t += 2) {
+                uint32_t g[12];
+                const uint32_t c = lane_base + (uint32_t)(6 * t);
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                             : "=r"(g[0]), "=r"(g[1]), "=r"(g[2]), "=r"(g[3]), "=r"(g[4]), "=r"(g[5]), "=r"(g[6]),
+                               "=r"(g[7])
+                             : "r"(c));
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                             : "=r"(g[8]), "=r"(g[9]), "=r"(g[10]), "=r"(g[11]) : "r"(c + 8));
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                {
+                    const u64 v = v6(g);
+                    emit(reduce(v & 0xFFFFFFFFULL, v >> 32, v, t, false), t);
+                }
+                if (t + 1 < te) {
+                    const u64 v = v6(g + 6);
+                    emit(reduce(v & 0xFFFFFFFFULL, v >> 32, v, t + 1, false), t + 1);
+                }
+            }
+        } else {
+            for (int t = tb; t < te; t += 2) {
+                uint32_t g[16];
+                const uint32_t c = lane_base + (uint32_t)(8 * t);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                    "[%16];\n"
+                    : "=r"(g[0]), "=r"(g[1]), "=r"(g[2]), "=r"(g[3]), "=r"(g[4]), "=r"(g[5]), "=r"(g[6]), "=r"(g[7]),
+                      "=r"(g[8]), "=r"(g[9]), "=r"(g[10]), "=r"(g[11]), "=r"(g[12]), "=r"(g[13]), "=r"(g[14]),
+                      "=r"(g[15])
+                    : "r"(c));
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    if (h == 1 && t + 1 >= te) break;
+                    const uint32_t *x = g + 8 * h;
+                    const u64 lo = (u64)x[0] + (u64)x[1] * 256u + (u64)x[2] * 65536u + (u64)x[3] * 16777216u;
+                    const u64 hi = (u64)x[4] + (u64)x[5] * 256u + (u64)x[6] * 65536u + (u64)x[7] * 16777216u;
+                    emit(reduce(lo, hi, lo + (hi << 32), t + h, true), t + h);
+                }
             }
         }
         asm volatile("tcgen05.fence::before_thread_sync;\n");

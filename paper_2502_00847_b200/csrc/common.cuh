@@ -81,6 +81,9 @@ struct Tab {
     // [P][N] {w, RN(w RN(1/q))} as doubles for the exact-FP64 rows (fused kernel, ntt_fused.cu); integer rows:
     // the same pointer as tw2 / itw2 ({w, Shoup companion})
     const ulonglong2 *twp = nullptr, *itwp = nullptr;
+    // host-visible: bit i set when 2^46 <= prime i < 2^52 / 3.5 (~50-bit rows: exact-FP64 NTT with reductions,
+    // ntt_core.cuh FpB; dense double twiddle tables like the FpA rows)
+    u64 fpb_mask = 0;
 };
 
 // limb l of a polynomial -> global prime index

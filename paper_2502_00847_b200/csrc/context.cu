@@ -390,6 +390,12 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
         const char *c = getenv("SECPE_NTT_CLUSTER");
         ntt_cluster = c ? atoi(c) : 0;
     }
+    // ~50-bit rows on the exact-FP64 NTT with reductions (FpB) for N >= 2^15: measured at N = 2^16 +14 %
+    // batched bootstraps (53.9 -> 61.7 per s), +8 % K = 16 argmax with bootstrapping; at N = 2^12 (64-thread
+    // CTAs, latency-bound) the integer path is faster.  SECPE_NO_FPB=1 keeps them on the integer Shoup NTT
+    const char *nofpb = getenv("SECPE_NO_FPB");
+    const bool use_fpb = !(nofpb && atoi(nofpb) == 1) && logn_ >= 15;
+    constexpr u64 FPB_TABLE_LIMIT = 1286742750677284ULL;  // floor(2^52 / 3.5), ntt_core.cuh FPB_LIMIT
     logn = logn_;
     N = 1L << logn;
     nq = nq_;
@@ -422,8 +428,8 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
         for (long k = 0; k < N; k++) {
             const unsigned b = brv((unsigned)k, logn);
             const size_t o = (size_t)i * N + k;
-            if (qi < (1ULL << 46)) {
-                // exact-FP64 butterflies (ntt.cu FpA): dense doubles w in the first N words of the
+            if (qi < (1ULL << 46) || (use_fpb && i < 64 && qi < FPB_TABLE_LIMIT)) {
+                // exact-FP64 butterflies (ntt_core.cuh FpA / FpB): dense doubles w in the first N words of the
                 // prime's 2N-word region
                 const double w = (double)pw[b], iw = (double)ipw[b];
                 std::memcpy(&tw[2 * (size_t)i * N + k], &w, 8);
@@ -459,8 +465,12 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
         tab.qd = reinterpret_cast<const double *>(d_qd.p);
         tab.qinv = reinterpret_cast<const double *>(d_qinv.p);
     }
-    for (int i = 0; i < P && i < 64; i++)
-        if (primes[i] < (1ULL << 46)) tab.fp_mask |= 1ULL << i;
+    for (int i = 0; i < P && i < 64; i++) {
+        if (primes[i] < (1ULL << 46))
+            tab.fp_mask |= 1ULL << i;
+        else if (use_fpb && primes[i] < FPB_TABLE_LIMIT)
+            tab.fpb_mask |= 1ULL << i;
+    }
     // {w, w/q} pair tables of the exact-FP64 rows for the fused NTT (its row-tile stages read one 16-byte pair
     // per twiddle instead of forming w/q with a DMUL); integer rows keep their {w, w'} tables
     tab.twp = tab.tw2;
@@ -469,7 +479,7 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
         std::vector<u64> tp(2 * (size_t)P * N), itp(2 * (size_t)P * N);
         for (int i = 0; i < P; i++) {
             const size_t o = 2 * (size_t)i * N;
-            if (primes[i] < (1ULL << 46)) {
+            if (primes[i] < (1ULL << 46) || (i < 64 && ((tab.fpb_mask >> i) & 1))) {
                 const double qinv = 1.0 / (double)primes[i];
                 for (long k = 0; k < N; k++) {
                     double w, iw;

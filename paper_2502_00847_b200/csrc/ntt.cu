@@ -691,22 +691,38 @@ void launch_contig_a(const PassArgs &a0, int n_polys, cudaStream_t st) {
     dim3 grid((unsigned)((1L << (LOGN - CF::S)) / CF::CG), n_polys * a.nsub);
     launch_pdl(ntt_contig<LOGN, INV, IO, A>, grid, dim3(CT), st, a);
 }
-// one launch per run of consecutive limbs of the same prime class (bit i of tab.fp_mask: prime i < 2^46)
-inline bool limb_fp(const PassArgs &a, int limb) {
-    const int p = prime_of(a.lm, limb);
-    return p < 64 && ((a.tab.fp_mask >> p) & 1);
+// one launch per run of consecutive limbs of the same prime class: 0 exact FP64 (tab.fp_mask: q < 2^46, FpA),
+// 1 exact FP64 with reductions (tab.fpb_mask: ~50-bit q, FpB), 2 integer Shoup (IntA)
+enum { CLS_FPA = 0, CLS_FPB = 1, CLS_INT = 2 };
+inline int prime_cls(const Tab &t, int p) {
+    if (p < 64 && ((t.fp_mask >> p) & 1)) return CLS_FPA;
+    if (p < 64 && ((t.fpb_mask >> p) & 1)) return CLS_FPB;
+    return CLS_INT;
+}
+inline int limb_cls(const PassArgs &a, int limb) { return prime_cls(a.tab, prime_of(a.lm, limb)); }
+// calls f(policy) with a value of the arithmetic policy of class cls
+template <class F>
+void with_policy(int cls, F f) {
+    if (cls == CLS_FPA)
+        f(FpA{});
+    else if (cls == CLS_FPB)
+        f(FpB{});
+    else
+        f(IntA{});
 }
 thread_local const NttProfHook *g_hook = nullptr;
 
-// calls launch(a, fp) once per run of same-class limbs; `passes` = launches per limb transform that
-// this call makes (2: one of the two passes, 1: single-pass cluster kernel) for the profiling hook
+// calls launch(a, cls) once per run of same-class limbs; `passes` = launches per limb transform that
+// this call makes (2: one of the two passes, 1: single-pass cluster kernel) for the profiling hook (which
+// sees the FP64 classes as one)
 template <class F>
 void for_runs(const PassArgs &a0, int n_polys, int passes, long N, F launch) {
     int l = 0;
     while (l < a0.lm.nl) {
-        const bool fp = limb_fp(a0, l);
+        const int cls = limb_cls(a0, l);
+        const bool fp = cls != CLS_INT;
         int e = l + 1;
-        while (e < a0.lm.nl && limb_fp(a0, e) == fp) e++;
+        while (e < a0.lm.nl && limb_cls(a0, e) == cls) e++;
         PassArgs a = a0;
         a.limb0 = l;
         a.nsub = e - l;
@@ -714,27 +730,21 @@ void for_runs(const PassArgs &a0, int n_polys, int passes, long N, F launch) {
         const double limbs = (double)n_polys * a.nsub / passes;
         const double bytes = 16.0 * limbs * (double)N;  // N words read + written once per transform
         if (g_hook) g_hook->mark(g_hook->ctx, 0, fp, bytes, limbs);
-        launch(a, fp);
+        launch(a, cls);
         if (g_hook) g_hook->mark(g_hook->ctx, 1, fp, bytes, limbs);
         l = e;
     }
 }
 template <int LOGN, bool INV, int IN>
 void launch_strided(const PassArgs &a0, int n_polys, cudaStream_t st) {
-    for_runs(a0, n_polys, 2, 1L << LOGN, [&](const PassArgs &a, bool fp) {
-        if (fp)
-            launch_strided_a<LOGN, INV, IN, FpA>(a, n_polys, st);
-        else
-            launch_strided_a<LOGN, INV, IN, IntA>(a, n_polys, st);
+    for_runs(a0, n_polys, 2, 1L << LOGN, [&](const PassArgs &a, int cls) {
+        with_policy(cls, [&](auto pol) { launch_strided_a<LOGN, INV, IN, decltype(pol)>(a, n_polys, st); });
     });
 }
 template <int LOGN, bool INV, int IO>
 void launch_contig(const PassArgs &a0, int n_polys, cudaStream_t st) {
-    for_runs(a0, n_polys, 2, 1L << LOGN, [&](const PassArgs &a, bool fp) {
-        if (fp)
-            launch_contig_a<LOGN, INV, IO, FpA>(a, n_polys, st);
-        else
-            launch_contig_a<LOGN, INV, IO, IntA>(a, n_polys, st);
+    for_runs(a0, n_polys, 2, 1L << LOGN, [&](const PassArgs &a, int cls) {
+        with_policy(cls, [&](auto pol) { launch_contig_a<LOGN, INV, IO, decltype(pol)>(a, n_polys, st); });
     });
 }
 
@@ -784,27 +794,22 @@ void launch_cluster_a(const PassArgs &a, int n_polys, cudaStream_t st) {
 template <int LOGN, bool INV, int IN, int OUT>
 void launch_cluster_or_split(const PassArgs &a0, int n_polys, cudaStream_t st) {
     const int mode = cluster_mode(a0);
-    for_runs(a0, n_polys, 1, 1L << LOGN, [&](const PassArgs &a, bool fp) {
-        if (fp && mode >= 1) {
+    for_runs(a0, n_polys, 1, 1L << LOGN, [&](const PassArgs &a, int cls) {
+        if (cls == CLS_FPA && mode >= 1) {
             launch_cluster_a<LOGN, INV, IN, OUT, FpA>(a, n_polys, st);
-        } else if (!fp && mode >= 2) {
+        } else if (cls == CLS_INT && mode >= 2) {
             launch_cluster_a<LOGN, INV, IN, OUT, IntA>(a, n_polys, st);
-        } else if (!INV) {
-            if (fp) {
-                launch_strided_a<LOGN, false, IN, FpA>(a, n_polys, st);
-                launch_contig_a<LOGN, false, OUT, FpA>(a, n_polys, st);
-            } else {
-                launch_strided_a<LOGN, false, IN, IntA>(a, n_polys, st);
-                launch_contig_a<LOGN, false, OUT, IntA>(a, n_polys, st);
-            }
         } else {
-            if (fp) {
-                launch_contig_a<LOGN, true, IN, FpA>(a, n_polys, st);
-                launch_strided_a<LOGN, true, IN_PLAIN, FpA>(a, n_polys, st);
-            } else {
-                launch_contig_a<LOGN, true, IN, IntA>(a, n_polys, st);
-                launch_strided_a<LOGN, true, IN_PLAIN, IntA>(a, n_polys, st);
-            }
+            with_policy(cls, [&](auto pol) {
+                using A = decltype(pol);
+                if (!INV) {
+                    launch_strided_a<LOGN, false, IN, A>(a, n_polys, st);
+                    launch_contig_a<LOGN, false, OUT, A>(a, n_polys, st);
+                } else {
+                    launch_contig_a<LOGN, true, IN, A>(a, n_polys, st);
+                    launch_strided_a<LOGN, true, IN_PLAIN, A>(a, n_polys, st);
+                }
+            });
         }
         LAUNCH_CHECK();
     });
@@ -849,12 +854,10 @@ void run_chunk(const PassArgs &a, int rows, bool inverse, cudaStream_t st) {
     if constexpr (LOGN == 16) {
         if (cluster_mode(a) == 0 && ntt_fused_enabled()) {
             // one persistent TMA-pipelined launch per run of exact-FP64 rows (ntt_fused.cu)
-            for_runs(a, rows, 1, 1L << LOGN, [&](const PassArgs &r, bool fp) {
-                if (ntt_fused_run(r.tab, LOGN, r.d, rows, r.lm, r.limb0, r.nsub, fp, inverse, r.f, st)) return;
-                if (fp)
-                    two_pass_run_a<LOGN, FpA>(r, rows, inverse, st);
-                else
-                    two_pass_run_a<LOGN, IntA>(r, rows, inverse, st);
+            for_runs(a, rows, 1, 1L << LOGN, [&](const PassArgs &r, int cls) {
+                if (ntt_fused_run(r.tab, LOGN, r.d, rows, r.lm, r.limb0, r.nsub, cls == CLS_FPA, inverse, r.f, st))
+                    return;
+                with_policy(cls, [&](auto pol) { two_pass_run_a<LOGN, decltype(pol)>(r, rows, inverse, st); });
             });
             return;
         }
@@ -937,29 +940,25 @@ template <int LOGN>
 void run_segs(const Tab &tab, const NttSeg *segs, int nseg, bool inverse, cudaStream_t st) {
     struct Run {
         Seg g;
-        bool fp;
+        int cls;
         int rows;
     };
     std::vector<Run> runs;
     for (int i = 0; i < nseg; i++) {
         const NttSeg &x = segs[i];
         if (x.n_polys <= 0 || x.lm.nl <= 0) continue;
-        auto isfp = [&](int l) {
-            const int p = prime_of(x.lm, l);
-            return p < 64 && ((tab.fp_mask >> p) & 1);
-        };
         int l = 0;
         while (l < x.lm.nl) {
-            const bool fp = isfp(l);
+            const int cls = prime_cls(tab, prime_of(x.lm, l));
             int e = l + 1;
-            while (e < x.lm.nl && isfp(e) == fp) e++;
-            runs.push_back(Run{Seg{x.d, x.lm, l, e - l, 0}, fp, x.n_polys * (e - l)});
+            while (e < x.lm.nl && prime_cls(tab, prime_of(x.lm, e)) == cls) e++;
+            runs.push_back(Run{Seg{x.d, x.lm, l, e - l, 0}, cls, x.n_polys * (e - l)});
             l = e;
         }
     }
     constexpr long N = 1L << LOGN;
-    for (int cls = 0; cls < 2; cls++) {
-        const bool fp = cls == 0;
+    for (int cls = 0; cls < 3; cls++) {
+        const bool fp = cls != CLS_INT;
         PassArgs a{};
         a.tab = tab;
         a.nseg = 0;
@@ -971,21 +970,20 @@ void run_segs(const Tab &tab, const NttSeg *segs, int nseg, bool inverse, cudaSt
             for (int pass = 0; pass < 2; pass++) {
                 if (g_hook) g_hook->mark(g_hook->ctx, 0, fp, bytes, rows / 2.0);
                 const bool first = pass == 0;
-                if (!inverse) {
-                    if (first)
-                        fp ? launch_strided_a<LOGN, false, IN_PLAIN, FpA>(a, 1, st)
-                           : launch_strided_a<LOGN, false, IN_PLAIN, IntA>(a, 1, st);
-                    else
-                        fp ? launch_contig_a<LOGN, false, OUT_PLAIN, FpA>(a, 1, st)
-                           : launch_contig_a<LOGN, false, OUT_PLAIN, IntA>(a, 1, st);
-                } else {
-                    if (first)
-                        fp ? launch_contig_a<LOGN, true, IN_PLAIN, FpA>(a, 1, st)
-                           : launch_contig_a<LOGN, true, IN_PLAIN, IntA>(a, 1, st);
-                    else
-                        fp ? launch_strided_a<LOGN, true, IN_PLAIN, FpA>(a, 1, st)
-                           : launch_strided_a<LOGN, true, IN_PLAIN, IntA>(a, 1, st);
-                }
+                with_policy(cls, [&](auto pol) {
+                    using A = decltype(pol);
+                    if (!inverse) {
+                        if (first)
+                            launch_strided_a<LOGN, false, IN_PLAIN, A>(a, 1, st);
+                        else
+                            launch_contig_a<LOGN, false, OUT_PLAIN, A>(a, 1, st);
+                    } else {
+                        if (first)
+                            launch_contig_a<LOGN, true, IN_PLAIN, A>(a, 1, st);
+                        else
+                            launch_strided_a<LOGN, true, IN_PLAIN, A>(a, 1, st);
+                    }
+                });
                 LAUNCH_CHECK();
                 if (g_hook) g_hook->mark(g_hook->ctx, 1, fp, bytes, rows / 2.0);
             }
@@ -993,7 +991,7 @@ void run_segs(const Tab &tab, const NttSeg *segs, int nseg, bool inverse, cudaSt
             rows = 0;
         };
         for (auto &r : runs) {
-            if (r.fp != fp) continue;
+            if (r.cls != cls) continue;
             if (a.nseg == MAXSEG) flush();
             r.g.row0 = rows;
             a.seg[a.nseg++] = r.g;

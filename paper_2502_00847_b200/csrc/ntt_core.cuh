@@ -199,6 +199,39 @@ struct FpA {
     }
 };
 
+// Exact FP64 path for the ~50-bit primes (2^46 <= q < 2^52 / 3.5 ~ 2^50.19: the bootstrap chains' 50-bit primes,
+// the paper's ~49-bit primes).  Same exact product as FpA, but its input may reach 3.5 q ~ 2^52, so the quotient
+// estimate is off by up to 1.37 and |mm| <= 1.37 q (still exact: |r + pl| < 2^52).  Bounds need reductions:
+// forward CT folds X to [-q/2, q/2] on every other stage (the CORR stages, as IntA), so |v| <= 3.24 q; the
+// inverse GS folds the sum on every stage (|v| <= 1.37 q).  red(x) = x - rint(x / q) q with rint by fma + the
+// 1.5 2^52 magic; k <= 4, so k q is exact and one fma gives the exact remainder.
+struct FpB : FpA {
+    static __device__ __forceinline__ double redB(double x, const PrimeC &P) {
+        const double k = __dsub_rn(__fma_rn(x, P.qinv, FP_MAGIC), FP_MAGIC);
+        return __fma_rn(-k, P.qd, x);
+    }
+    template <bool CORR>
+    static __device__ __forceinline__ void ct(u64 &x, u64 &y, ulonglong2 w, const PrimeC &P) {
+        double X = D(x);
+        if (CORR) X = redB(X, P);
+        const double T = mm(D(y), D(w.x), D(w.y), P.qd);
+        x = B(__dadd_rn(X, T));
+        y = B(__dsub_rn(X, T));
+    }
+    template <bool RED>
+    static __device__ __forceinline__ void gs(u64 &x, u64 &y, ulonglong2 w, const PrimeC &P) {
+        const double X = D(x), Y = D(y);
+        y = B(mm(__dsub_rn(X, Y), D(w.x), D(w.y), P.qd));
+        x = B(redB(__dadd_rn(X, Y), P));
+    }
+    // |mm| <= 1.37 q: a full canonicalisation
+    static __device__ __forceinline__ u64 out_scaled(u64 x, u64 k, u64, const PrimeC &P) {
+        const double kd = D(in(k, P)), kq = __dmul_rn(kd, P.qinv);
+        return canon(mm(D(x), kd, kq, P.qd), P);
+    }
+};
+constexpr u64 FPB_LIMIT = 1286742750677284ULL;  // floor(2^52 / 3.5)
+
 // [C]_q for a signed constant |C| < 2^62 (R9 constants), with the prime's Barrett constants
 __device__ __forceinline__ u64 smod_dev(i64 C, u64 q, u64 br0, u64 br1) {
     const u64 m = barrett128(U128{(u64)(C < 0 ? -C : C), 0}, q, br0, br1);

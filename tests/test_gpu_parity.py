@@ -72,6 +72,7 @@ def test_context_tables(S):
     ("toy", 1, 0, 8), ("toy", 3, 2, 5), ("toy", 2, 8, 1),       # ragged batch, offset limbs, special prime
     ("ntt", 2, 0, 24), ("ntt", 1, 13, 11),                       # configs[1] primes at N = 2^16
     ("argmax", 1, 25, 13),                                       # q tail + special primes
+    ("boot16", 3, 0, 30),                                        # 60-bit + 50-bit (FpB) + 60-bit rows
 ])
 def test_ntt_bit_exact(S, name, n_polys, first, n_limbs):
     P = pair(S, name)
@@ -95,6 +96,8 @@ def test_ntt_bit_exact(S, name, n_polys, first, n_limbs):
     ("toy", 0, 9),        # 40-bit chain + 50-bit special (integer rows)
     ("argmax", 0, 40),    # configs[4]: 45-bit chain + 46-bit special primes (exact-FP64 rows, |v| <= 13 q < 2^51)
     ("ntt", 0, 24),       # configs[1]: 60-bit primes (integer rows, Harvey bounds near 2^62)
+    ("boot16", 0, 30),    # bootstrap chain at N = 2^16: 60-bit q0 + 22 x 50-bit (exact-FP64 rows with reductions,
+                          # FpB, |v| <= 3.24 q ~ 2^51.9) + 7 x 60-bit special primes
 ])
 def test_ntt_edge_inputs(S, name, first, n_limbs):
     """Worst-case magnitudes for the lazy butterflies: all-(q-1), all-zero, alternating q-1 / 0 and
