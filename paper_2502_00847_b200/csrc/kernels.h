@@ -78,7 +78,7 @@ void ntt_inverse(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm
 // the two-pass kernels).  SECPE_NTT_FUSED=0 disables it.
 bool ntt_fused_enabled();
 int ntt_fused_mode(int mode);  // sets SECPE_NTT_FUSED's mode (mode < 0: query); returns the previous one
-bool ntt_fused_run(const Tab &tab, int logn, RowsArg d, int n_polys, LimbMap lm, int limb0, int nsub, bool fp,
+bool ntt_fused_run(const Tab &tab, int logn, RowsArg d, int n_polys, LimbMap lm, int limb0, int nsub, int cls,
                    bool inverse, const NttFusion &f, cudaStream_t st);
 
 void k_addsub(const Tab &tab, int logn, CRows a, CRows b, RowsArg out, int n_polys, LimbMap lm,

@@ -180,6 +180,42 @@ __device__ __forceinline__ void tensor1_fp(u64 a0, u64 a1, u64 b0, u64 b1, bool 
     d2 = fpt::canon(e2, qd, qinv);
 }
 
+// the same tensor left as exact doubles (|e| <= 4.5 q < 2^49, not canonicalised): the FP64 key inner product
+// below multiplies them directly
+__device__ __forceinline__ void tensor1_fp_raw(u64 a0, u64 a1, u64 b0, u64 b1, bool lin, u64 x0, u64 x1, u64 c,
+                                               bool lin2, u64 y0, u64 y1, u64 c2, double qd, double qinv, double &e0,
+                                               double &e1, double &e2, bool p2, u64 u0, u64 u1, u64 w0, u64 w1) {
+    const double A0 = fpt::d(a0), A1 = fpt::d(a1), B0 = fpt::d(b0), B1 = fpt::d(b1);
+    const double B0q = __dmul_rn(B0, qinv), B1q = __dmul_rn(B1, qinv);
+    e0 = fpt::mm(A0, B0, B0q, qd);
+    e1 = __dadd_rn(fpt::mm(A0, B1, B1q, qd), fpt::mm(A1, B0, B0q, qd));
+    e2 = fpt::mm(A1, B1, B1q, qd);
+    if (p2) {
+        const double U0 = fpt::d(u0), U1 = fpt::d(u1), W0 = fpt::d(w0), W1 = fpt::d(w1);
+        const double W0q = __dmul_rn(W0, qinv), W1q = __dmul_rn(W1, qinv);
+        e0 = __dadd_rn(e0, fpt::mm(U0, W0, W0q, qd));
+        e1 = __dadd_rn(e1, __dadd_rn(fpt::mm(U0, W1, W1q, qd), fpt::mm(U1, W0, W0q, qd)));
+        e2 = __dadd_rn(e2, fpt::mm(U1, W1, W1q, qd));
+    }
+    if (lin) {
+        const double C = fpt::d(c), Cq = __dmul_rn(C, qinv);
+        e0 = __dadd_rn(e0, fpt::mm(fpt::d(x0), C, Cq, qd));
+        e1 = __dadd_rn(e1, fpt::mm(fpt::d(x1), C, Cq, qd));
+    }
+    if (lin2) {
+        const double C = fpt::d(c2), Cq = __dmul_rn(C, qinv);
+        e0 = __dadd_rn(e0, fpt::mm(fpt::d(y0), C, Cq, qd));
+        e1 = __dadd_rn(e1, fpt::mm(fpt::d(y1), C, Cq, qd));
+    }
+}
+// canonical residue of an exact double |v| <= 4 q (four FP64 operations, the sign fix on the integer pipe)
+__device__ __forceinline__ u64 fp_canon4(double v, u64 q, double qd, double qinv) {
+    const double k = __dsub_rn(__fma_rn(v, qinv, fpt::MAGIC), fpt::MAGIC);
+    const double r = __fma_rn(-k, qd, v);
+    const long long ri = __double_as_longlong(__dadd_rn(r, fpt::MAGIC)) - __double_as_longlong(fpt::MAGIC);
+    return (u64)(ri + ((ri >> 63) & (long long)q));
+}
+
 // one coefficient of the tensor: (d0, d1, d2) mod q, with the optional linear term C x
 __device__ __forceinline__ void tensor1(u64 a0, u64 a1, u64 b0, u64 b1, bool lin, u64 x0, u64 x1, u64 c, u64 csh,
                                         bool lin2, u64 y0, u64 y1, u64 c2, u64 c2sh, u64 q, u64 r0, u64 r1, u64 &d0,
@@ -234,8 +270,28 @@ __global__ void __launch_bounds__(TPB, 3) ks_inner_vec_kernel(Tab tab, int logn,
     pdl_wait();
     KsIn<MAXB> cur, nxt;
     ks_load<MAXB>(cur, 0, d, ds, ext, exts, e, jd, ne, beta, N, kx, swap);
+    const bool fp = q < (1ULL << 46);
+    const double qd = tab.qd[pr], qinv = tab.qinv[pr];
     for (int c = 0; c < n_ct; c++) {
         if (c + 1 < n_ct) ks_load<MAXB>(nxt, c + 1, d, ds, ext, exts, e, jd, ne, beta, N, kx, swap);
+        if (fp) {
+            // exact-FP64 products (as ks_inner_ten1_kernel): |sum of beta terms| <= 3 q -> canonical
+            double s0 = 0, t0 = 0, s1 = 0, t1 = 0;
+#pragma unroll
+            for (int j = 0; j < MAXB; j++)
+                if (j < beta) {
+                    const double X = fpt::d(cur.x[j].x), Y = fpt::d(cur.x[j].y);
+                    const double B0 = fpt::d(kb[j].x), B1 = fpt::d(kb[j].y), A0 = fpt::d(ka[j].x), A1 = fpt::d(ka[j].y);
+                    s0 = __dadd_rn(s0, fpt::mm(X, B0, __dmul_rn(B0, qinv), qd));
+                    t0 = __dadd_rn(t0, fpt::mm(Y, B1, __dmul_rn(B1, qinv), qd));
+                    s1 = __dadd_rn(s1, fpt::mm(X, A0, __dmul_rn(A0, qinv), qd));
+                    t1 = __dadd_rn(t1, fpt::mm(Y, A1, __dmul_rn(A1, qinv), qd));
+                }
+            stv2(acc + c * accs + (long)e * N + k, fp_canon4(s0, q, qd, qinv), fp_canon4(t0, q, qd, qinv));
+            stv2(acc + c * accs + (long)(ne + e) * N + k, fp_canon4(s1, q, qd, qinv), fp_canon4(t1, q, qd, qinv));
+            cur = nxt;
+            continue;
+        }
         U128 s0{0, 0}, s1{0, 0}, t0{0, 0}, t1{0, 0};  // (poly 0, poly 1) x (coefficient k, k + 1)
 #pragma unroll
         for (int j = 0; j < MAXB; j++)
@@ -309,6 +365,31 @@ __global__ void __launch_bounds__(TPB, KS_TEN1_MINB) ks_inner_ten1_kernel(Tab ta
         }
     };
     auto compute = [&](int c, In &in) {
+        if (q < (1ULL << 46)) {
+            // exact-FP64 products on the FP64 pipe (the integer path's 128-bit MACs and Barrett reductions are
+            // its dominant instructions): sum_j mm(x_j, key_j) [+ mm(d_b, [P])] -> |s| <= 3 q -> canonical
+            double e0 = 0, e1 = 0, e2 = 0;
+            if (qrow)
+                tensor1_fp_raw(in.a0, in.a1, in.b0, in.b1, lin, in.x0, in.x1, cc, lin2, in.y0, in.y1, c2, qd, qinv, e0,
+                               e1, e2, p2, in.u0, in.u1, in.w0, in.w1);
+            double s0 = 0, s1 = 0;
+#pragma unroll
+            for (int j = 0; j < MAXB; j++)
+                if (j < beta) {
+                    const double X = j == jd ? e2 : fpt::d(in.x[j]);
+                    const double KB = fpt::d(kb[j]), KA = fpt::d(ka[j]);
+                    s0 = __dadd_rn(s0, fpt::mm(X, KB, __dmul_rn(KB, qinv), qd));
+                    s1 = __dadd_rn(s1, fpt::mm(X, KA, __dmul_rn(KA, qinv), qd));
+                }
+            if (qrow) {
+                const double PM = fpt::d(pm), PMq = __dmul_rn(PM, qinv);
+                s0 = __dadd_rn(s0, fpt::mm(e0, PM, PMq, qd));
+                s1 = __dadd_rn(s1, fpt::mm(e1, PM, PMq, qd));
+            }
+            acc[c * accs + (long)e * N + k] = fp_canon4(s0, q, qd, qinv);
+            acc[c * accs + (long)(ne + e) * N + k] = fp_canon4(s1, q, qd, qinv);
+            return;
+        }
         u64 d0 = 0, d1 = 0;
         if (qrow) {
             u64 d2;
@@ -340,6 +421,158 @@ __global__ void __launch_bounds__(TPB, KS_TEN1_MINB) ks_inner_ten1_kernel(Tab ta
         In A;
         load(c, A);
         compute(c, A);
+    }
+}
+
+// The same relinearise-and-rescale inner product with the ciphertext inputs staged by bulk asynchronous
+// copies (cp.async.bulk, one 2 KB row slice per input array and ciphertext) into a KB_STAGES-deep shared
+// memory ring: thread 0 issues the copies of ciphertext c + KB_STAGES while the block computes c, so the
+// loads of the next ciphertexts are in flight during the arithmetic (the per-thread version waits on each
+// ciphertext's loads).  Identical integers: the arithmetic is ks_inner_ten1_kernel's, reading its operands
+// from shared memory.
+#ifndef KB_STAGES
+#define KB_STAGES 3
+#endif
+constexpr int KB_MAXARR = 14;  // ext digits (<= 4) + a0 a1 b0 b1 + x0 x1 + y0 y1 + u0 u1 w0 w1
+__device__ __forceinline__ uint32_t ks_su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+template <int MAXB>
+__global__ void __launch_bounds__(TPB, 2) ks_inner_ten1_bulk_kernel(Tab tab, int logn, const u64 *__restrict__ ext,
+                                                                  long exts, const u64 *__restrict__ key,
+                                                                  int nq_total, int np, u64 *__restrict__ acc,
+                                                                  long accs, int n_ct, int nl, int alpha, int beta,
+                                                                  TensorSrc ten, const u64 *__restrict__ pmod,
+                                                                  int narr_max) {
+    extern __shared__ __align__(16) u64 kbuf[];  // [KB_STAGES][narr_max][TPB]
+    __shared__ __align__(8) uint64_t kfull[KB_STAGES];
+    const int e = blockIdx.y, tid = threadIdx.x;
+    const long N = 1L << logn;
+    const long k0 = (long)blockIdx.x * TPB, k = k0 + tid;
+    const int ne = nl + np, nk = nq_total + np;
+    const int pr = e < nl ? e : nq_total + (e - nl);
+    const u64 q = tab.q[pr], r0 = tab.br0[pr], r1 = tab.br1[pr];
+    u64 kb[MAXB], ka[MAXB];
+#pragma unroll
+    for (int j = 0; j < MAXB; j++)
+        if (j < beta) {
+            kb[j] = __ldg(key + (((long)j * 2 + 0) * nk + pr) * N + k);
+            ka[j] = __ldg(key + (((long)j * 2 + 1) * nk + pr) * N + k);
+        }
+    const int jd = e < nl ? e / alpha : -1;
+    const bool qrow = e < nl;
+    const u64 pm = qrow ? pmod[e] : 0;
+    const bool lin = ten.x.p != nullptr, lin2 = ten.x2.p != nullptr, p2 = ten.a2.p != nullptr;
+    const u64 cc = lin && qrow ? ten.C.c[e] : 0, ccsh = lin && qrow ? ten.C.csh[e] : 0;
+    const u64 c2 = lin2 && qrow ? ten.C2.c[e] : 0, c2sh = lin2 && qrow ? ten.C2.csh[e] : 0;
+    const double qd = tab.qd[pr], qinv = tab.qinv[pr];
+    const long o0 = e * N + k0;
+    // this row's input slices: slot -> (base, per-ciphertext stride); ext digits first (slot j = digit j)
+    const int next_ = qrow ? beta - 1 : beta;
+    const int narr = next_ + (qrow ? 4 + (lin ? 2 : 0) + (lin2 ? 2 : 0) + (p2 ? 4 : 0) : 0);
+    auto slot_src = [&](int i, int c) -> const u64 * {
+        if (i < next_) {
+            const int j = (qrow && i >= jd) ? i + 1 : i;
+            return ext + c * exts + ((long)j * ne + e) * N + k0;
+        }
+        int t = i - next_;
+        if (t < 4) {
+            const CRows &r = t < 2 ? ten.a : ten.b;
+            return r.p + c * r.cs + (t & 1) * r.ps + o0;
+        }
+        t -= 4;
+        if (lin) {
+            if (t < 2) return ten.x.p + c * ten.x.cs + t * ten.x.ps + o0;
+            t -= 2;
+        }
+        if (lin2) {
+            if (t < 2) return ten.x2.p + c * ten.x2.cs + t * ten.x2.ps + o0;
+            t -= 2;
+        }
+        const CRows &r = t < 2 ? ten.a2 : ten.b2;
+        return r.p + c * r.cs + (t & 1) * r.ps + o0;
+    };
+    auto issue = [&](int c) {
+        const int st = c % KB_STAGES;
+        const uint32_t bar = ks_su32(&kfull[st]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(narr * TPB * 8)
+                     : "memory");
+        for (int i = 0; i < narr; i++)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             ks_su32(kbuf + ((long)st * narr_max + i) * TPB)),
+                         "l"(slot_src(i, c)), "r"(TPB * 8), "r"(bar)
+                         : "memory");
+    };
+    if (tid == 0) {
+        for (int st = 0; st < KB_STAGES; st++)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ks_su32(&kfull[st])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    pdl_wait();  // the key words above are not produced by the previous kernel; the inputs are
+    if (tid == 0)
+        for (int c = 0; c < KB_STAGES && c < n_ct; c++) issue(c);
+    for (int c = 0; c < n_ct; c++) {
+        const int st = c % KB_STAGES;
+        {
+            const uint32_t bar = ks_su32(&kfull[st]), par = (c / KB_STAGES) & 1;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tKBW%=:\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                "@!p bra KBW%=;\n\t}" ::"r"(bar),
+                "r"(par)
+                : "memory");
+        }
+        const u64 *sl = kbuf + (long)st * narr_max * TPB + tid;
+        u64 x[MAXB];
+#pragma unroll
+        for (int j = 0; j < MAXB; j++)
+            if (j < beta && j != jd) x[j] = sl[(qrow && j > jd ? j - 1 : j) * TPB];
+        u64 d0 = 0, d1 = 0;
+        if (qrow) {
+            const u64 *tp = sl + next_ * TPB;
+            const u64 a0 = tp[0], a1 = tp[TPB], b0 = tp[2 * TPB], b1 = tp[3 * TPB];
+            int t = 4;
+            u64 x0 = 0, x1 = 0, y0 = 0, y1 = 0, u0 = 0, u1 = 0, w0 = 0, w1 = 0;
+            if (lin) {
+                x0 = tp[t * TPB];
+                x1 = tp[(t + 1) * TPB];
+                t += 2;
+            }
+            if (lin2) {
+                y0 = tp[t * TPB];
+                y1 = tp[(t + 1) * TPB];
+                t += 2;
+            }
+            if (p2) {
+                u0 = tp[t * TPB];
+                u1 = tp[(t + 1) * TPB];
+                w0 = tp[(t + 2) * TPB];
+                w1 = tp[(t + 3) * TPB];
+            }
+            u64 d2;
+            if (q < (1ULL << 46))
+                tensor1_fp(a0, a1, b0, b1, lin, x0, x1, cc, lin2, y0, y1, c2, qd, qinv, d0, d1, d2, p2, u0, u1, w0, w1);
+            else
+                tensor1(a0, a1, b0, b1, lin, x0, x1, cc, ccsh, lin2, y0, y1, c2, c2sh, q, r0, r1, d0, d1, d2, p2, u0,
+                        u1, w0, w1);
+#pragma unroll
+            for (int j = 0; j < MAXB; j++)
+                if (j == jd) x[j] = d2;
+        }
+        U128 s0{0, 0}, s1{0, 0};
+#pragma unroll
+        for (int j = 0; j < MAXB; j++)
+            if (j < beta) {
+                mac_wide(s0, x[j], kb[j]);
+                mac_wide(s1, x[j], ka[j]);
+            }
+        if (qrow) {
+            mac_wide(s0, d0, pm);
+            mac_wide(s1, d1, pm);
+        }
+        acc[c * accs + (long)e * N + k] = barrett128(s0, q, r0, r1);
+        acc[c * accs + (long)(ne + e) * N + k] = barrett128(s1, q, r0, r1);
+        __syncthreads();  // every thread is done with stage st
+        if (tid == 0 && c + KB_STAGES < n_ct) issue(c + KB_STAGES);
     }
 }
 
@@ -560,9 +793,27 @@ void k_ks_inner(const Tab &tab, int logn, const u64 *d, long ds, const u64 *ext,
     const dim3 g2(chunks2(logn), nl + np), g1(chunks(logn), nl + np);
     static const TensorSrc none{};
     const TensorSrc &T = ten ? *ten : none;
+    // bulk-staged relinearisation inner product (ks_inner_ten1_bulk_kernel): slices per ciphertext
+    const int narr_max = ten ? std::max(beta, beta - 1 + 4 + (T.x.p ? 2 : 0) + (T.x2.p ? 2 : 0) + (T.a2.p ? 4 : 0)) : 0;
+    const size_t kb_smem = (size_t)KB_STAGES * narr_max * TPB * 8;
+    static int kb_mode = -1;
+    if (kb_mode < 0) {
+        const char *e = getenv("SECPE_KS_BULK");  // development switch: 0 = per-thread loads
+        kb_mode = e ? atoi(e) : 0;  // measured slower than the per-thread kernel (profiles/r02_notes.md)
+    }
 #define KSV(B_)                                                                                                   \
     do {                                                                                                          \
-        if (ten)                                                                                                  \
+        if (ten && kb_mode) {                                                                                     \
+            static bool attr = false;                                                                             \
+            if (!attr) {                                                                                          \
+                CUDA_CHECK(cudaFuncSetAttribute(ks_inner_ten1_bulk_kernel<B_>,                                    \
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,                      \
+                                                KB_STAGES * KB_MAXARR * TPB * 8));                                \
+                attr = true;                                                                                      \
+            }                                                                                                     \
+            launch_pdl_k(ks_inner_ten1_bulk_kernel<B_>, g1, dim3(TPB), kb_smem, st, tab, logn, ext, exts, key,    \
+                         nq_total, np, acc, accs, n_ct, nl, alpha, beta, T, pmod, narr_max);                      \
+        } else if (ten)                                                                                           \
             launch_pdl_k(ks_inner_ten1_kernel<B_>, g1, dim3(TPB), 0, st, tab, logn, ext, exts, key, nq_total, np, \
                          acc, accs, n_ct, nl, alpha, beta, T, pmod);                                              \
         else                                                                                                      \

@@ -855,7 +855,7 @@ void run_chunk(const PassArgs &a, int rows, bool inverse, cudaStream_t st) {
         if (cluster_mode(a) == 0 && ntt_fused_enabled()) {
             // one persistent TMA-pipelined launch per run of exact-FP64 rows (ntt_fused.cu)
             for_runs(a, rows, 1, 1L << LOGN, [&](const PassArgs &r, int cls) {
-                if (ntt_fused_run(r.tab, LOGN, r.d, rows, r.lm, r.limb0, r.nsub, cls == CLS_FPA, inverse, r.f, st))
+                if (ntt_fused_run(r.tab, LOGN, r.d, rows, r.lm, r.limb0, r.nsub, cls, inverse, r.f, st))
                     return;
                 with_policy(cls, [&](auto pol) { two_pass_run_a<LOGN, decltype(pol)>(r, rows, inverse, st); });
             });

@@ -758,12 +758,14 @@ bool ntt_fused_enabled() {
 
 // one run of same-class limbs [limb0, limb0 + nsub) of n_polys polynomials; false: not handled (caller
 // falls back to the two-pass kernels)
-bool ntt_fused_run(const Tab &tab, int logn, RowsArg d, int n_polys, LimbMap lm, int limb0, int nsub, bool fp,
+bool ntt_fused_run(const Tab &tab, int logn, RowsArg d, int n_polys, LimbMap lm, int limb0, int nsub, int cls,
                    bool inverse, const NttFusion &f, cudaStream_t st) {
     if (logn != FL || !ntt_fused_enabled()) return false;
-    if (g_fused_mode == 2 && (f.in_mode != IN_PLAIN || f.out_mode != OUT_PLAIN || (long)n_polys * nsub < FT_AUTO_ROWS))
+    if ((g_fused_mode == 2 || (g_fused_mode == 3 && cls == 0)) && (f.in_mode != IN_PLAIN || f.out_mode != OUT_PLAIN || (long)n_polys * nsub < FT_AUTO_ROWS))
         return false;
-    if (!fp) return false;  // integer rows: two-pass kernels (for now)
+    // classes (ntt.cu): 0 exact FP64 (FpA), 1 FP64 with reductions (FpB: two-pass kernels), 2 integer (IntA)
+    if (cls == 1) return false;
+    if (cls == 2 && g_fused_mode < 3) return false;  // integer rows: opt-in (mode 3)
     if ((long)n_polys * nsub > FT_MAXROWS) return false;
     FtArgs a{};
     a.tab = tab;
@@ -793,10 +795,17 @@ bool ntt_fused_run(const Tab &tab, int logn, RowsArg d, int n_polys, LimbMap lm,
     if (!ok) return false;
     a.sync = stream_sync(st);
     a.rows = n_polys * nsub;
-    if (inverse)
-        dispatch_modes<FpA, true>(a, st);
-    else
-        dispatch_modes<FpA, false>(a, st);
+    if (cls == 0) {
+        if (inverse)
+            dispatch_modes<FpA, true>(a, st);
+        else
+            dispatch_modes<FpA, false>(a, st);
+    } else {
+        if (inverse)
+            dispatch_modes<IntA, true>(a, st);
+        else
+            dispatch_modes<IntA, false>(a, st);
+    }
     LAUNCH_CHECK();
     return true;
 }

@@ -16,6 +16,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 SHAPES = [(1, 1, 3), (1, 30, 0), (2, 10, 5), (3, 7, 1), (8, 30, 0), (16, 30, 0), (64, 29, 1), (32, 40, 0)]
+if os.environ.get("AB_PSET") == "ntt":  # configs[1]: 24 x 60-bit primes
+    SHAPES = [(1, 1, 3), (2, 10, 5), (8, 24, 0), (16, 24, 0), (64, 24, 0)]
 
 
 def child(tag):
@@ -25,7 +27,7 @@ def child(tag):
     from paper_2502_00847_b200 import secpe
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    ctx = secpe.Context(synth.PARAM_SETS["argmax"], stream=stream.cuda_stream)
+    ctx = secpe.Context(synth.PARAM_SETS[os.environ.get("AB_PSET", "argmax")], stream=stream.cuda_stream)
     res, outs = {}, {}
     for P, L, first in SHAPES:
         x0 = torch.from_numpy(synth.uniform_residues(11 + P + L, ctx.q[first:first + L] if first + L <= ctx.nq else
@@ -57,10 +59,11 @@ def main():
     import numpy as np
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     # extra args: variant libraries "tag=path/to/libsecpe_x.so" (fused on), compared with the default build
-    runs = [("twopass", {"SECPE_NTT_FUSED": "0"}), ("fused", {"SECPE_NTT_FUSED": "1"})]
+    fm = os.environ.get("AB_MODE", "1")
+    runs = [("twopass", {"SECPE_NTT_FUSED": "0"}), ("fused", {"SECPE_NTT_FUSED": fm})]
     for v in sys.argv[1:] if False else os.environ.get("AB_VARIANTS", "").split():
         tag, lib = v.split("=")
-        runs.append((tag, {"SECPE_NTT_FUSED": "1", "SECPE_LIB": lib}))
+        runs.append((tag, {"SECPE_NTT_FUSED": fm, "SECPE_LIB": lib}))
     res = {}
     for tag, ev in runs:
         env = dict(os.environ, **ev)
