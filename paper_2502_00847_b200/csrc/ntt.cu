@@ -27,6 +27,7 @@
 #include "kernels.h"
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 #include "ntt_core.cuh"
@@ -248,6 +249,42 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, const RowsArg &d,
         const u64 br0 = a.tab.br0[prime], br1 = a.tab.br1[prime];
         const u64 lc1 = IO == IN_LIN ? smod_dev(a.f.C1, q, br0, br1) : 0;
         const u64 lc2 = IO == IN_LIN && a.f.lin == 2 ? smod_dev(a.f.C2, q, br0, br1) : 0;
+        constexpr bool FPX = std::is_same<A, FpA>::value && (IO == IN_MUL || IO == IN_MUL2 || IO == IN_LIN);
+        if (FPX) {
+            // exact-FP64 rows: the fused products as FpA exact products of canonical operands (the sum of up to
+            // two products, |v| <= 1.5 q, enters the GS stages as it is: their bound analysis holds up to 24 q)
+            const double c1d = FpA::D(FpA::in(lc1, P)), c1q = __dmul_rn(c1d, P.qinv);
+            const double c2d = FpA::D(FpA::in(lc2, P)), c2q = __dmul_rn(c2d, P.qinv);
+            auto fd = [&](u64 x) { return FpA::D(FpA::in(x, P)); };
+#pragma unroll 4
+            for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
+                const ulonglong2 x = NTT_LD2(src + i);
+                double r0, r1;
+                if (IO == IN_LIN) {
+                    r0 = FpA::mm(fd(x.x), c1d, c1q, P.qd);
+                    r1 = FpA::mm(fd(x.y), c1d, c1q, P.qd);
+                    if (src2) {
+                        const ulonglong2 y = src2[i];
+                        r0 = __dadd_rn(r0, FpA::mm(fd(y.x), c2d, c2q, P.qd));
+                        r1 = __dadd_rn(r1, FpA::mm(fd(y.y), c2d, c2q, P.qd));
+                    }
+                } else {
+                    const ulonglong2 y = src2[i];
+                    const double y0 = fd(y.x), y1 = fd(y.y);
+                    r0 = FpA::mm(fd(x.x), y0, __dmul_rn(y0, P.qinv), P.qd);
+                    r1 = FpA::mm(fd(x.y), y1, __dmul_rn(y1, P.qinv), P.qd);
+                    if (IO == IN_MUL2) {
+                        const ulonglong2 z = src3[i], w = src4[i];
+                        const double w0 = fd(w.x), w1 = fd(w.y);
+                        r0 = __dadd_rn(r0, FpA::mm(fd(z.x), w0, __dmul_rn(w0, P.qinv), P.qd));
+                        r1 = __dadd_rn(r1, FpA::mm(fd(z.y), w1, __dmul_rn(w1, P.qinv), P.qd));
+                    }
+                }
+                const int e = 2 * i, gg = e / G, r = e % G;
+                sm[gg * PITCH + padr(r)] = FpA::B(r0);
+                sm[gg * PITCH + padr(r + 1)] = FpA::B(r1);
+            }
+        } else
 #pragma unroll 4
         for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
             ulonglong2 x = NTT_LD2(src + i);
@@ -288,9 +325,14 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, const RowsArg &d,
 #pragma unroll
     for (int k = 0; k < NV; k++) v[k] = smg[padr(held<LO1>(tau, k))];
     do_round<S, INV, 1, true, LOGN, A>(v, tau, g, tw, P);
+    // exact-FP64 rows with a fused epilogue: the transform's doubles (|v| <= 13 q) go into the epilogue as they
+    // are and its products are FpA exact products (one canonicalisation per output instead of Shoup / Barrett)
+    constexpr bool FPE = std::is_same<A, FpA>::value && !INV && (IO == OUT_RESCALE || IO == OUT_MODDOWN);
     if (!INV) {
+        if (!FPE) {
 #pragma unroll
-        for (int k = 0; k < NV; k++) v[k] = A::out_fwd(v[k], P);
+            for (int k = 0; k < NV; k++) v[k] = A::out_fwd(v[k], P);
+        }
         // no barrier: each thread rewrites exactly the words it read for round 1
 #pragma unroll
         for (int k = 0; k < NV; k++) smg[padr(held<LO1>(tau, k))] = v[k];
@@ -321,6 +363,56 @@ __device__ __forceinline__ void contig_body(const PassArgs &a, const RowsArg &d,
             kc = a.f.k[limb];
             kcsh = a.f.ksh[limb];
         }
+        if (FPE) {
+            const double kd = FpA::D(FpA::in(kc, P)), kq = __dmul_rn(kd, P.qinv);
+            const double c1d = FpA::D(FpA::in(lc1, P)), c1q = __dmul_rn(c1d, P.qinv);
+            const double c2d = FpA::D(FpA::in(lc2, P)), c2q = __dmul_rn(c2d, P.qinv);
+            auto fd = [&](u64 x) { return FpA::D(FpA::in(x, P)); };
+            // mm result in [-0.75 q, 0.75 q] -> canonical with one conditional add (integer pipe)
+            auto fix = [&](double t) {
+                const i64 r = FpA::to_int(t);
+                return (u64)(r + ((r >> 63) & (i64)q));
+            };
+#pragma unroll 4
+            for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
+                const int e = 2 * i, gg = e / G, r = e % G;
+                const double x0 = FpA::D(sm[gg * PITCH + padr(r)]), x1 = FpA::D(sm[gg * PITCH + padr(r + 1)]);
+                const ulonglong2 c = e1[i];
+                u64 o0, o1;
+                if (IO == OUT_RESCALE) {
+                    // (C1 e1 [+ C2 e1b] + NTT(T)) q_l^{-1}
+                    double c0d = fd(c.x), c1v = fd(c.y);
+                    if (a.f.lin) {
+                        c0d = FpA::mm(c0d, c1d, c1q, P.qd);
+                        c1v = FpA::mm(c1v, c1d, c1q, P.qd);
+                        if (e1b) {
+                            const ulonglong2 y = e1b[i];
+                            c0d = __dadd_rn(c0d, FpA::mm(fd(y.x), c2d, c2q, P.qd));
+                            c1v = __dadd_rn(c1v, FpA::mm(fd(y.y), c2d, c2q, P.qd));
+                        }
+                    }
+                    o0 = fix(FpA::mm(__dadd_rn(c0d, x0), kd, kq, P.qd));
+                    o1 = fix(FpA::mm(__dadd_rn(c1v, x1), kd, kq, P.qd));
+                } else {
+                    // (acc - NTT(T)) P^{-1} (+ addends): |sum| <= 2.75 q -> canonical
+                    double t0 = FpA::mm(__dsub_rn(fd(c.x), x0), kd, kq, P.qd);
+                    double t1 = FpA::mm(__dsub_rn(fd(c.y), x1), kd, kq, P.qd);
+                    if (e2) {
+                        const ulonglong2 d = e2[i];
+                        t0 = __dadd_rn(t0, fd(d.x));
+                        t1 = __dadd_rn(t1, fd(d.y));
+                    }
+                    if (e3) {
+                        const ulonglong2 d = e3[i];
+                        t0 = __dadd_rn(t0, fd(d.x));
+                        t1 = __dadd_rn(t1, fd(d.y));
+                    }
+                    o0 = FpA::canon(t0, P);
+                    o1 = FpA::canon(t1, P);
+                }
+                NTT_ST2(dst + i, make_ulonglong2(o0, o1));
+            }
+        } else
 #pragma unroll 4
         for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
             const int e = 2 * i, gg = e / G, r = e % G;

@@ -687,7 +687,14 @@ FtSync *stream_sync(cudaStream_t st) {
 // extra HBM pass is not hidden (large launches, 3-4 %); inside the argmax step (100-700 rows per launch,
 // fused prologues / epilogues) its pipeline fill and drain cost more than the saved traffic
 int g_fused_mode = -1;
-constexpr int FT_AUTO_ROWS = 1024;
+int ft_auto_rows() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SECPE_NTT_FUSED_ROWS");  // development switch
+        v = e ? atoi(e) : 1024;
+    }
+    return v;
+}
 
 template <class A, bool INV, int IN, int OUT>
 void launch_k(const FtArgs &a, cudaStream_t st) {
@@ -761,7 +768,7 @@ bool ntt_fused_enabled() {
 bool ntt_fused_run(const Tab &tab, int logn, RowsArg d, int n_polys, LimbMap lm, int limb0, int nsub, int cls,
                    bool inverse, const NttFusion &f, cudaStream_t st) {
     if (logn != FL || !ntt_fused_enabled()) return false;
-    if ((g_fused_mode == 2 || (g_fused_mode == 3 && cls == 0)) && (f.in_mode != IN_PLAIN || f.out_mode != OUT_PLAIN || (long)n_polys * nsub < FT_AUTO_ROWS))
+    if ((g_fused_mode == 2 || (g_fused_mode == 3 && cls == 0)) && (f.in_mode != IN_PLAIN || f.out_mode != OUT_PLAIN || (long)n_polys * nsub < ft_auto_rows()))
         return false;
     // classes (ntt.cu): 0 exact FP64 (FpA), 1 FP64 with reductions (FpB: two-pass kernels), 2 integer (IntA)
     if (cls == 1) return false;
