@@ -101,10 +101,21 @@ __device__ __forceinline__ void strided_body(const PassArgs &a, const RowsArg &d
         // the source row is the coefficient-form last limb of the same polynomial
         const u64 *src = a.f.src.p + poly_off(a.f.src.cs, a.f.src.ps, poly) + c;
         const u64 ql = a.tab.q[a.f.lp], hl = ql >> 1, hi = a.f.half[limb], one_sh = a.tab.br1[prime];
+        if (std::is_same<A, FpA>::value && ql < (1ULL << 47)) {
+            // exact-FP64 rows: [floor(q_l/2)]_{q_i} - r as an exact double, |v| < 2^47 (the forward stages need no
+            // reduction of r mod q_i: their bound grows from 4 q instead of q, 16 q < 2^51)
+            const double hd = FpA::D(FpA::in(hi, P));
 #pragma unroll
-        for (int k = 0; k < NV; k++) {
-            const u64 r = csub(src[STRIDE * held<LO0>(tau, k)] + hl, ql);
-            v[k] = A::in(submod(hi, mul_shoup(r, 1, one_sh, q), q), P);
+            for (int k = 0; k < NV; k++) {
+                const u64 r = csub(src[STRIDE * held<LO0>(tau, k)] + hl, ql);
+                v[k] = FpA::B(__dsub_rn(hd, FpA::D(FpA::in(r, P))));
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < NV; k++) {
+                const u64 r = csub(src[STRIDE * held<LO0>(tau, k)] + hl, ql);
+                v[k] = A::in(submod(hi, mul_shoup(r, 1, one_sh, q), q), P);
+            }
         }
     } else if (!INV) {
 #pragma unroll
