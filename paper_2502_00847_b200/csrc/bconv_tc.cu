@@ -300,6 +300,292 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS));
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Pipelined variant (default): one CTA per SM with warp roles, two A stages and two TMEM accumulators,
+// so the staging of tile i + 1 and its MMAs overlap the epilogue of tile i (the round-1 kernel ran the
+// phases of a tile one after another, separated by block barriers).
+//   warps 0-3  : producers -- thread = coefficient row; load the row's sources of the tile, store them
+//                into A[i % 2] (canonical K-major layout), arrive a_full[i % 2]
+//   warp 4     : lane 0 issues the tile's MMAs into accumulator i % 2 and commits to acc_full[i % 2]
+//   warps 5-28 : epilogue, six warps per TMEM lane quarter, each a contiguous block of targets; arrive
+//                acc_empty[i % 2] when done with the accumulator
+// Same integers as bconv_tc_kernel (the same GEMM and epilogue arithmetic).
+// ---------------------------------------------------------------------------------------------
+#ifndef TC2_EPI
+#define TC2_EPI 24  // epilogue warps (a multiple of 4: TMEM lane quarters)
+#endif
+constexpr int TC2_PROD = 128, TC2_EPI_WARPS = TC2_EPI;
+constexpr int TC2_THREADS = TC2_PROD + 32 + 32 * TC2_EPI_WARPS;  // 544
+constexpr int TC2_TMEM_COLS = 512;                                // two accumulators of up to 256 columns
+
+__device__ __forceinline__ void tc2_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tTC2W%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra TC2W%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tc2_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(TC2_THREADS, 1) bconv_tc2_kernel(TcArgs a, int tiles_per_cta) {
+    extern __shared__ __align__(128) uint8_t tsm[];
+    uint8_t *sA0 = tsm;                        // 2 x TC_M * TC_K
+    uint8_t *sB = tsm + 2 * TC_M * TC_K;       // 8 * TC_TMAX * TC_K
+    __shared__ __align__(8) uint64_t a_full[2], acc_full[2], acc_empty[2];
+    __shared__ uint32_t tslot;
+    __shared__ u64 sq[TC_TMAX], spm[TC_TMAX], spmsh[TC_TMAX];
+    __shared__ double sqinv[TC_TMAX];
+    __shared__ long soff[TC_TMAX];
+    __shared__ __align__(16) ulonglong2 spk[TC_TMAX][2];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int p = blockIdx.y;
+    const TcGroup &G = a.groups[a.grouped ? p % a.pdiv : 0];
+    const int nt = G.nt, ns = G.ns;
+    const int ncols = G.ncols, planes = G.planes;
+    const int ksteps = (8 * (ns + (a.const1 ? 1 : 0)) + 31) / 32;
+    const long N = 1L << a.logn;
+    const int ntiles = (int)(N / TC_M);
+    const int tile0 = blockIdx.x * tiles_per_cta;
+    const int T = min(tiles_per_cta, ntiles - tile0);
+
+    if (warp == 4) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tslot)),
+                     "n"(TC2_TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid < nt) {
+        const u64 q = a.tab.q[G.prime[tid]];
+        sq[tid] = q;
+        sqinv[tid] = G.qinv[tid];
+        spm[tid] = G.pmod[tid];
+        spmsh[tid] = G.pmodsh[tid];
+        soff[tid] = (long)G.out_row[tid] << a.logn;
+        spk[tid][0] = make_ulonglong2(q, (u64)0 - q);
+        spk[tid][1] = make_ulonglong2((u64)__double_as_longlong(G.qinv[tid]), (u64)(((long)G.out_row[tid] << a.logn) * 8));
+    }
+    if (tid == 0) {
+        for (int b = 0; b < 2; b++) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&a_full[b])), "r"(TC2_PROD));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&acc_full[b])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&acc_empty[b])),
+                         "r"(TC2_EPI_WARPS));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    {  // B (canonical) and both A stages zeroed (the constant-1 source is written once)
+        const uint4 *gb = reinterpret_cast<const uint4 *>(G.B);
+        uint4 *b4 = reinterpret_cast<uint4 *>(sB);
+        for (int i = tid; i < ncols * TC_K / 16; i += TC2_THREADS) b4[i] = gb[i];
+        uint4 *a4 = reinterpret_cast<uint4 *>(sA0);
+        for (int i = tid; i < 2 * TC_M * TC_K / 16; i += TC2_THREADS) a4[i] = make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+    if (a.const1 && tid < TC_M)
+        for (int b = 0; b < 2; b++) *reinterpret_cast<u64 *>(sA0 + b * TC_M * TC_K + canon(tid, 8 * ns)) = 1;
+    asm volatile("fence.proxy.async.shared::cta;\n");
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tmem = tslot;
+    const u64 *src = a.src + (long)(p / a.pdiv) * a.s_cs + (long)(p % a.pdiv) * a.s_ps + (long)G.src_row0 * N;
+    u64 *dst = a.dst + (long)(p / a.pdiv) * a.d_cs + (long)(p % a.pdiv) * a.d_ps;
+    pdl_wait();  // TMEM, constants and B do not depend on the previous kernel; the sources do
+
+    if (warp < 4) {
+        // ---------------- producers ----------------
+        const int row = tid;
+        for (int i = 0; i < T; i++) {
+            const int b = i & 1;
+            const long k0 = (long)(tile0 + i) * TC_M;
+            u64 v[12];
+#pragma unroll
+            for (int s = 0; s < 12; s++)
+                if (s < ns) v[s] = src[(long)s * N + k0 + row];
+            if (i >= 2) tc2_wait(&acc_full[b], ((i - 2) >> 1) & 1);  // MMAs of tile i - 2 have read A[b]
+            uint8_t *sA = sA0 + b * TC_M * TC_K;
+#pragma unroll
+            for (int s = 0; s < 12; s++)
+                if (s < ns) *reinterpret_cast<u64 *>(sA + canon(row, 8 * s)) = v[s];
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            tc2_arrive(&a_full[b]);
+        }
+    } else if (warp == 4) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            const uint32_t idesc = (2u << 4) | ((uint32_t)(ncols >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+            for (int i = 0; i < T; i++) {
+                const int b = i & 1;
+                tc2_wait(&a_full[b], (i >> 1) & 1);
+                if (i >= 2) tc2_wait(&acc_empty[b], ((i - 2) >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;\n");
+                const uint32_t a0 = smem_u32(sA0 + b * TC_M * TC_K), b0 = smem_u32(sB);
+                const uint32_t acc = tmem + (uint32_t)(b * 256);
+                for (int s = 0; s < ksteps; s++) {
+                    const uint64_t da = smem_desc(a0 + s * 2 * LBO), db = smem_desc(b0 + s * 2 * LBO);
+                    const uint32_t accum = s > 0;
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(acc),
+                        "l"(da), "l"(db), "r"(idesc), "r"(accum));
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                    smem_u32(&acc_full[b])));
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- epilogue ----------------
+        const int ew = warp - 5;                // 0 .. TC2_EPI_WARPS - 1
+        constexpr int TGS = TC2_EPI_WARPS / 4;  // warps per lane quarter
+        const int lq = warp & 3, tg = ew / 4;   // TMEM lane quarter, target block (0 .. TGS - 1)
+        const int m = 32 * lq + lane;
+        const int t0 = a.rr ? 1 : 0;
+        const int per = (nt - t0 + TGS - 1) / TGS;
+        const int tb = t0 + tg * per, te = min(nt, tb + per);
+        for (int i = 0; i < T; i++) {
+            const int b = i & 1;
+            const long k0 = (long)(tile0 + i) * TC_M;
+            tc2_wait(&acc_full[b], (i >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;\n");
+            const uint32_t lane_base = tmem + (uint32_t)(b * 256) + ((uint32_t)(32 * lq) << 16);
+            auto v6 = [](const uint32_t *g) -> u64 {
+                u64 v = (u64)g[0] + (u64)g[1] * 256u;
+                v += (u64)g[2] * 65536u;
+                v += (u64)g[3] * 16777216u;
+                return v + ((u64)(g[4] + g[5] * 256u) << 32);
+            };
+            auto to_d = [](u64 x) -> double {
+                return __dsub_rn(__longlong_as_double((long long)(x | 0x4330000000000000ULL)), 4503599627370496.0);
+            };
+            auto reduce = [&](u64 lo, u64 hi, u64 vw, int t, bool wide) -> u64 {
+                const u64 q = sq[t];
+                const double vd = __fma_rn(to_d(hi), 4294967296.0, to_d(lo));
+                const double kb = __fma_rn(vd, sqinv[t], 6755399441055744.0);
+                const u64 kq = wide ? ((u64)__double_as_longlong(kb) & ((1ULL << 51) - 1)) * q
+                                    : (u64)(uint32_t)__double_as_longlong(kb) * q;
+                const long long r = (long long)(vw - kq);
+                return (u64)(r + ((r >> 63) & (long long)q));
+            };
+            u64 rrv = 0;
+            if (a.rr) {
+                const u64 ql = sq[0];
+                uint32_t g[8];
+                if (planes == 6) {
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                                 : "=r"(g[0]), "=r"(g[1]), "=r"(g[2]), "=r"(g[3]) : "r"(lane_base));
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n"
+                                 : "=r"(g[4]), "=r"(g[5]) : "r"(lane_base + 4));
+                } else {
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                                 : "=r"(g[0]), "=r"(g[1]), "=r"(g[2]), "=r"(g[3]), "=r"(g[4]), "=r"(g[5]), "=r"(g[6]),
+                                   "=r"(g[7])
+                                 : "r"(lane_base));
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                u64 tl;
+                if (planes == 6) {
+                    const u64 v = v6(g);
+                    tl = reduce(v & 0xFFFFFFFFULL, v >> 32, v, 0, false);
+                } else {
+                    const u64 lo = (u64)g[0] + (u64)g[1] * 256u + (u64)g[2] * 65536u + (u64)g[3] * 16777216u;
+                    const u64 hi = (u64)g[4] + (u64)g[5] * 256u + (u64)g[6] * 65536u + (u64)g[7] * 16777216u;
+                    tl = reduce(lo, hi, lo + (hi << 32), 0, true);
+                }
+                const u64 xc = src[(long)(-1) * N + k0 + m];
+                rrv = csub(mul_shoup(submod(xc, tl, ql), a.pinv_l, a.pinv_l_sh, ql) + (ql >> 1), ql);
+            }
+            auto emit = [&](u64 z, int t) {
+                if (a.rr) z = addmod(z, csub(mul_shoup(rrv, spm[t], spmsh[t], sq[t]), sq[t]), sq[t]);
+                dst[soff[t] + k0 + m] = z;
+            };
+            if (planes == 6 && !a.rr) {
+                uint8_t *const obase = reinterpret_cast<uint8_t *>(dst + k0 + m);
+                auto lean = [&](const uint32_t *x, int t) {
+                    const ulonglong2 c0 = spk[t][0], c1 = spk[t][1];
+                    u64 v = (u64)x[0] + (u64)x[1] * 256u;
+                    v += (u64)x[2] * 65536u;
+                    v += (u64)x[3] * 16777216u;
+                    const uint32_t vh = (uint32_t)(v >> 32) + x[4] + x[5] * 256u, vl = (uint32_t)v;
+                    v = ((u64)vh << 32) | vl;
+                    const double vd = __fma_rn(__dsub_rn(__hiloint2double(0x43300000, (int)vh), 4503599627370496.0),
+                                               4294967296.0,
+                                               __dsub_rn(__hiloint2double(0x43300000, (int)vl), 4503599627370496.0));
+                    const uint32_t k = (uint32_t)__double_as_longlong(
+                        __fma_rn(vd, __longlong_as_double((long long)c1.x), 6755399441055744.0));
+                    u64 r = v + (u64)k * c0.y;
+                    if ((int)(r >> 32) < 0) r += c0.x;
+                    *reinterpret_cast<u64 *>(obase + c1.y) = r;
+                };
+                for (int t = tb; t < te; t += 2) {
+                    uint32_t g[12];
+                    const uint32_t c = lane_base + (uint32_t)(6 * t);
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                                 : "=r"(g[0]), "=r"(g[1]), "=r"(g[2]), "=r"(g[3]), "=r"(g[4]), "=r"(g[5]), "=r"(g[6]),
+                                   "=r"(g[7])
+                                 : "r"(c));
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                                 : "=r"(g[8]), "=r"(g[9]), "=r"(g[10]), "=r"(g[11]) : "r"(c + 8));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                    lean(g, t);
+                    if (t + 1 < te) lean(g + 6, t + 1);
+                }
+            } else if (planes == 6) {
+                for (int t = tb; t < te; t += 2) {
+                    uint32_t g[12];
+                    const uint32_t c = lane_base + (uint32_t)(6 * t);
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                                 : "=r"(g[0]), "=r"(g[1]), "=r"(g[2]), "=r"(g[3]), "=r"(g[4]), "=r"(g[5]), "=r"(g[6]),
+                                   "=r"(g[7])
+                                 : "r"(c));
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                                 : "=r"(g[8]), "=r"(g[9]), "=r"(g[10]), "=r"(g[11]) : "r"(c + 8));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                    {
+                        const u64 v = v6(g);
+                        emit(reduce(v & 0xFFFFFFFFULL, v >> 32, v, t, false), t);
+                    }
+                    if (t + 1 < te) {
+                        const u64 v = v6(g + 6);
+                        emit(reduce(v & 0xFFFFFFFFULL, v >> 32, v, t + 1, false), t + 1);
+                    }
+                }
+            } else {
+                for (int t = tb; t < te; t += 2) {
+                    uint32_t g[16];
+                    const uint32_t c = lane_base + (uint32_t)(8 * t);
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                        "[%16];\n"
+                        : "=r"(g[0]), "=r"(g[1]), "=r"(g[2]), "=r"(g[3]), "=r"(g[4]), "=r"(g[5]), "=r"(g[6]), "=r"(g[7]),
+                          "=r"(g[8]), "=r"(g[9]), "=r"(g[10]), "=r"(g[11]), "=r"(g[12]), "=r"(g[13]), "=r"(g[14]),
+                          "=r"(g[15])
+                        : "r"(c));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        if (h == 1 && t + 1 >= te) break;
+                        const uint32_t *x = g + 8 * h;
+                        const u64 lo = (u64)x[0] + (u64)x[1] * 256u + (u64)x[2] * 65536u + (u64)x[3] * 16777216u;
+                        const u64 hi = (u64)x[4] + (u64)x[5] * 256u + (u64)x[6] * 65536u + (u64)x[7] * 16777216u;
+                        emit(reduce(lo, hi, lo + (hi << 32), t + h, true), t + h);
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;\n");
+            __syncwarp();
+            if (lane == 0) tc2_arrive(&acc_empty[b]);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TC2_TMEM_COLS));
+}
+
 }  // namespace
 
 // host: a conversion group's B matrix in canonical layout.  c[s][t] = the constant of source s for
@@ -326,6 +612,27 @@ std::vector<uint8_t> tc_bmatrix(const std::vector<std::vector<u64>> &c, const st
 int tc_smem_bytes() { return 80 * 1024; }
 
 void k_bconv_tc(const TcArgs &a, int n_polys, cudaStream_t st) {
+    static int ver = -1, tpc2 = 0;
+    if (ver < 0) {
+        const char *e = getenv("SECPE_TC_V");  // development switch: 1 = the round-1 kernel layout
+        ver = e ? atoi(e) : 1;  // the pipelined kernel measured slower in the step (profiles/r02_notes.md)
+        const char *t = getenv("SECPE_TC2_TPC");
+        tpc2 = t ? std::max(1, atoi(t)) : 16;
+    }
+    if (ver == 2) {
+        // 2 A stages (24 KB) + B (24 KB); > 114 KB requested so one CTA (512 TMEM columns) per SM
+        constexpr int smem2 = 120 * 1024;
+        static bool attr2 = false;
+        if (!attr2) {
+            CUDA_CHECK(cudaFuncSetAttribute(bconv_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+            attr2 = true;
+        }
+        const int ntiles = (int)((1L << a.logn) / TC_M);
+        const dim3 grid((ntiles + tpc2 - 1) / tpc2, n_polys);
+        launch_pdl_k(bconv_tc2_kernel, grid, dim3(TC2_THREADS), smem2, st, a, tpc2);
+        LAUNCH_CHECK();
+        return;
+    }
     static bool attr = false;
     if (!attr) {
         CUDA_CHECK(cudaFuncSetAttribute(bconv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes()));

@@ -93,7 +93,15 @@ __device__ __forceinline__ void strided_body(const PassArgs &a, const RowsArg &d
     const int c = blockIdx.x * SC + cl;
     u64 *base = d.p + poly_off(d.cs, d.ps, poly) + limb * N + c;
     const u64 q = P.q;
+#if NTT_STRIDED_PAIRS
+    // column stages: 255 twiddles per prime, L1-resident -- the {w, w/q} pair table saves the per-twiddle DMUL
+    using AT = typename std::conditional<std::is_same<A, FpA>::value, PairTw<A>, A>::type;
+    const ulonglong2 *tw = (std::is_same<A, FpA>::value ? (INV ? a.tab.itwp : a.tab.twp) : (INV ? a.tab.itw2 : a.tab.tw2)) +
+                           prime * N;
+#else
+    using AT = A;
     const ulonglong2 *tw = (INV ? a.tab.itw2 : a.tab.tw2) + prime * N;
+#endif
     u64 v[NV];
     constexpr int LO0 = R::lo(0);
     if constexpr (IN == IN_BCAST) {
@@ -124,14 +132,14 @@ __device__ __forceinline__ void strided_body(const PassArgs &a, const RowsArg &d
 #pragma unroll
         for (int k = 0; k < NV; k++) v[k] = base[STRIDE * held<LO0>(tau, k)];  // intermediate representation
     }
-    do_round<S, INV, 0, false, LOGN, A>(v, tau, 0, tw, P);
+    do_round<S, INV, 0, false, LOGN, AT>(v, tau, 0, tw, P);
     if constexpr (R::NR > 1) {
 #pragma unroll
         for (int k = 0; k < NV; k++) sm[held<R::lo(0)>(tau, k) * SC + cl] = v[k];
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < NV; k++) v[k] = sm[held<R::lo(1)>(tau, k) * SC + cl];
-        do_round<S, INV, 1, false, LOGN, A>(v, tau, 0, tw, P);
+        do_round<S, INV, 1, false, LOGN, AT>(v, tau, 0, tw, P);
     }
     static_assert(R::NR <= 2, "strided pass: at most two rounds");
     constexpr int LOL = R::lo(R::NR - 1);

@@ -232,6 +232,20 @@ struct FpB : FpA {
 };
 constexpr u64 FPB_LIMIT = 1286742750677284ULL;  // floor(2^52 / 3.5)
 
+// the arithmetic policy A reading its twiddles as 16-byte {w, w'} pairs (FpA: {w, w/q} of Tab::twp)
+template <class A>
+struct PairTw : A {
+    static constexpr bool PAIRS = false;
+    static __device__ __forceinline__ ulonglong2 twiddle(const ulonglong2 *tw, int i, const PrimeC &) {
+        return __ldg(tw + i);
+    }
+    static __device__ __forceinline__ void twiddle2(const ulonglong2 *, int, const PrimeC &, ulonglong2 &,
+                                                    ulonglong2 &) {}
+};
+#ifndef NTT_STRIDED_PAIRS
+#define NTT_STRIDED_PAIRS 0  // measured: isolated 0.420 vs 0.412 us/limb, in-step neutral (profiles/r02_notes.md)
+#endif
+
 // [C]_q for a signed constant |C| < 2^62 (R9 constants), with the prime's Barrett constants
 __device__ __forceinline__ u64 smod_dev(i64 C, u64 q, u64 br0, u64 br1) {
     const u64 m = barrett128(U128{(u64)(C < 0 ? -C : C), 0}, q, br0, br1);

@@ -27,34 +27,35 @@ PARAM_SETS = {
     "argmax_small": dict(logn=12, q=[("nearest", 45, 30)], p=[("below", 46, 10)],
                          alpha=10, log_scale=45),
     # Bootstrapping (readings R32-R35): q_0 ~ 2^60 over scale 2^50 (R = q_0 / S ~ 2^10),
-    # a 50-bit chain long enough for one bootstrap (8 + r levels) plus a few, 7 special 60-bit primes
-    # (alpha = 7: every digit < P).  boot_tiny: CPU-sized (oracle pins); boot: the smallest ring the
+    # a 50-bit chain long enough for one bootstrap (8 + r levels) plus a few, 8 special primes below 2^50
+    # (alpha = 7: P ~ 2^400 > every 7-prime digit <= 2^360; reading R40: ~50-bit special primes keep every
+    # key-switching row except q_0 on the exact-FP64 NTT).  boot_tiny: CPU-sized (oracle pins); boot: the smallest ring the
     # library takes (N = 2^12, 2048 slots, BSGS 64 x 32).
-    "boot_tiny": dict(logn=8, q=[("below", 60, 1), ("nearest", 50, 18)], p=[("below", 60, 7)],
+    "boot_tiny": dict(logn=8, q=[("below", 60, 1), ("nearest", 50, 18)], p=[("below", 50, 8)],
                       alpha=7, log_scale=50),
-    "boot": dict(logn=12, q=[("below", 60, 1), ("nearest", 50, 20)], p=[("below", 60, 7)],
+    "boot": dict(logn=12, q=[("below", 60, 1), ("nearest", 50, 20)], p=[("below", 50, 8)],
                  alpha=7, log_scale=50),
     # N4 (reading R38): argmax with bootstrapping.  Levels 1..16 are 45-bit primes at the nominal scale 2^45
     # (the Sign polynomials' constants, up to 2^14.8, need Delta_c ~ q <= 2^47); the 19 levels above are
     # 50-bit primes for the bootstrap (ModRaise to the top, EvalMod at scale 2^50).  A refresh lands at
     # level 16: one normalisation, one Max (14 levels), one level left for the next refresh's scale-up.
     "boot_argmax_tiny": dict(logn=8, q=[("below", 60, 1), ("nearest", 45, 16), ("nearest", 50, 17)],
-                             p=[("below", 60, 7)], alpha=7, log_scale=45),
+                             p=[("below", 50, 8)], alpha=7, log_scale=45),
     "boot_argmax": dict(logn=12, q=[("below", 60, 1), ("nearest", 45, 16), ("nearest", 50, 19)],
-                        p=[("below", 60, 7)], alpha=7, log_scale=45),
+                        p=[("below", 50, 8)], alpha=7, log_scale=45),
     "boot_argmax16": dict(logn=16, q=[("below", 60, 1), ("nearest", 45, 16), ("nearest", 50, 19)],
-                          p=[("below", 60, 7)], alpha=7, log_scale=45),
+                          p=[("below", 50, 8)], alpha=7, log_scale=45),
     # the same with two more bootstrap levels, for four stage groups (3/4/4/4: fewer key switches per group)
     "boot_argmax16_g4": dict(logn=16, q=[("below", 60, 1), ("nearest", 45, 16), ("nearest", 50, 21)],
-                             p=[("below", 60, 7)], alpha=7, log_scale=45),
+                             p=[("below", 50, 8)], alpha=7, log_scale=45),
     # N = 2^12 analogues of the four-group chains (groups 2/3/3/3: depth 21): a standalone bootstrap chain and
     # boot_argmax16_g4's structure on the small ring (word-for-word parity of the bench's four-group plans)
-    "boot_g4": dict(logn=12, q=[("below", 60, 1), ("nearest", 50, 22)], p=[("below", 60, 7)],
+    "boot_g4": dict(logn=12, q=[("below", 60, 1), ("nearest", 50, 22)], p=[("below", 50, 8)],
                     alpha=7, log_scale=50),
     "boot_argmax_g4": dict(logn=12, q=[("below", 60, 1), ("nearest", 45, 16), ("nearest", 50, 21)],
-                           p=[("below", 60, 7)], alpha=7, log_scale=45),
+                           p=[("below", 50, 8)], alpha=7, log_scale=45),
     # the paper's ring (N = 2^16, 32768 slots) with the factorised transforms (R37, groups 5/5/5: depth 20)
-    "boot16": dict(logn=16, q=[("below", 60, 1), ("nearest", 50, 22)], p=[("below", 60, 7)],
+    "boot16": dict(logn=16, q=[("below", 60, 1), ("nearest", 50, 22)], p=[("below", 50, 8)],
                    alpha=7, log_scale=50),
     # BASELINE configs[1]: NTT microbench, 24 x 60-bit primes, N = 2^16.
     "ntt": dict(logn=16, q=[("below", 60, 24)], p=[], alpha=8, log_scale=50),
