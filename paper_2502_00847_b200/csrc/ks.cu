@@ -208,7 +208,13 @@ __device__ __forceinline__ void tensor1_fp_raw(u64 a0, u64 a1, u64 b0, u64 b1, b
         e1 = __dadd_rn(e1, fpt::mm(fpt::d(y1), C, Cq, qd));
     }
 }
-// canonical residue of an exact double |v| <= 4 q (four FP64 operations, the sign fix on the integer pipe)
+// Rows whose plain (rotation) key inner products run on the FP64 pipe: q < 2^52 / 3.5.  With canonical inputs
+// the quotient estimate of fpt::mm is off by at most 1 + q / 2^52 <= 1.29, so |mm| <= 1.29 q and beta <= 4
+// products sum to |s| <= 5.2 q < 2^52.5: every partial sum is an exact double, and the canonicalisation's
+// fma(-k, q, s) is exact whatever k.  The relinearisation kernel sums up to six raw tensor products before its
+// [P] product, which for ~50-bit q could pass 2^53: it keeps the FP64 path to q < 2^46.
+constexpr u64 FP_KS_LIMIT = 1286742750677284ULL;
+// canonical residue of an exact double |v| <= 6 q (four FP64 operations, the sign fix on the integer pipe)
 __device__ __forceinline__ u64 fp_canon4(double v, u64 q, double qd, double qinv) {
     const double k = __dsub_rn(__fma_rn(v, qinv, fpt::MAGIC), fpt::MAGIC);
     const double r = __fma_rn(-k, qd, v);
@@ -270,7 +276,9 @@ __global__ void __launch_bounds__(TPB, 3) ks_inner_vec_kernel(Tab tab, int logn,
     pdl_wait();
     KsIn<MAXB> cur, nxt;
     ks_load<MAXB>(cur, 0, d, ds, ext, exts, e, jd, ne, beta, N, kx, swap);
-    const bool fp = q < (1ULL << 46);
+    // exact-FP64 products for q < 2^52 / 3.5 (the FpA and FpB rows): with canonical inputs |mm| <= 0.79 q,
+    // beta <= 4 terms stay below 3.2 q < 2^52 and k = rint(s / q) <= 4 keeps k q exact
+    const bool fp = q < FP_KS_LIMIT;
     const double qd = tab.qd[pr], qinv = tab.qinv[pr];
     for (int c = 0; c < n_ct; c++) {
         if (c + 1 < n_ct) ks_load<MAXB>(nxt, c + 1, d, ds, ext, exts, e, jd, ne, beta, N, kx, swap);

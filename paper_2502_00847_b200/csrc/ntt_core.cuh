@@ -200,11 +200,15 @@ struct FpA {
 };
 
 // Exact FP64 path for the ~50-bit primes (2^46 <= q < 2^52 / 3.5 ~ 2^50.19: the bootstrap chains' 50-bit primes,
-// the paper's ~49-bit primes).  Same exact product as FpA, but its input may reach 3.5 q ~ 2^52, so the quotient
-// estimate is off by up to 1.37 and |mm| <= 1.37 q (still exact: |r + pl| < 2^52).  Bounds need reductions:
-// forward CT folds X to [-q/2, q/2] on every other stage (the CORR stages, as IntA), so |v| <= 3.24 q; the
-// inverse GS folds the sum on every stage (|v| <= 1.37 q).  red(x) = x - rint(x / q) q with rint by fma + the
-// 1.5 2^52 magic; k <= 4, so k q is exact and one fma gives the exact remainder.
+// the paper's ~49-bit primes).  Same exact product as FpA.  With y up to a few q the quotient k = rint(y w / q) is
+// formed as fma(y, w/q, 1.5 2^52) - 1.5 2^52; once |y w / q| passes 2^51 that sum's ulp is 2, so with the w/q
+// rounding |k - y w / q| <= 1 + |y| / 2^52 and |mm| <= q (1 + c 0.287) for |y| = c q (q / 2^52 <= 0.287).  mm
+// stays exact while |r + pl| < 2^53 (pl <= ulp(y w) / 2 <= 2^50).  Bounds, worst case over the stages: forward CT
+// folds X to [-q/2, q/2] on every other stage (the CORR stages, as IntA): outputs settle below 2.8 q after a
+// folding stage and 4.6 q after the next (the multiplied input of 4.6 q gives |mm| <= 2.3 q); inverse GS folds the
+// sum on every stage: |v| <= 2.35 q, differences <= 4.7 q.  Everything stays below 4.7 q < 2^52.4, an exact
+// double integer.  red(x) = x - rint(x / q) q with rint by fma + the 1.5 2^52 magic (k <= 5: one fma gives the
+// exact remainder).
 struct FpB : FpA {
     static __device__ __forceinline__ double redB(double x, const PrimeC &P) {
         const double k = __dsub_rn(__fma_rn(x, P.qinv, FP_MAGIC), FP_MAGIC);
@@ -224,7 +228,7 @@ struct FpB : FpA {
         y = B(mm(__dsub_rn(X, Y), D(w.x), D(w.y), P.qd));
         x = B(redB(__dadd_rn(X, Y), P));
     }
-    // |mm| <= 1.37 q: a full canonicalisation
+    // |mm| <= 2.4 q: a full canonicalisation
     static __device__ __forceinline__ u64 out_scaled(u64 x, u64 k, u64, const PrimeC &P) {
         const double kd = D(in(k, P)), kq = __dmul_rn(kd, P.qinv);
         return canon(mm(D(x), kd, kq, P.qd), P);
