@@ -460,6 +460,85 @@ def argmax_boot_bench(stream, t_ms, lname, B, sigma, pname="boot_argmax16_g4", g
             "labels_exact_above_margin": good / tot, "in_margin_fraction": inm / (B * lay["queries"]),
             "logn": ctx.logn, "chain": pname + ": q0 60 + 16 x 45 + 21 x 50 bit", "groups": list(groups)}
 
+def argmax_accuracy(ctx, keys, out, all_scores, lay):
+    """Client side, outside every timed region: decrypt the step's outputs and decode the labels (argmax over each
+    query's K window slots, reading R19) against the plaintext argmax of the mean scores."""
+    from paper_2502_00847_b200 import secpe
+    n_ok = n_ok_margin = n_margin = n_q = 0
+    for i in range(len(all_scores)):
+        dec = ctx.decrypt(keys, out, i)
+        got = secpe.labels(dec, lay)
+        mean = all_scores[i].mean(axis=1)
+        srt = np.sort(mean, axis=1)
+        above = srt[:, -1] - srt[:, -2] >= 2.0 ** -7  # the Sign margin of the (7,15,15) design
+        truth = np.argmax(mean, axis=1)
+        n_q += len(truth)
+        n_ok += int((got == truth).sum())
+        n_ok_margin += int((got == truth)[above].sum())
+        n_margin += int(above.sum())
+    return {"queries": n_q, "labels_exact": n_ok / n_q, "labels_exact_above_margin": n_ok_margin / max(1, n_margin),
+            "in_margin_fraction": 1.0 - n_margin / n_q,
+            "note": "decrypted one-hot decoded by argmax over each query's window vs argmax of the plaintext "
+                    "mean scores; 'above margin' = top-1 gap >= 2^-7"}
+
+
+def argmax49_bench(stream, B=16, steps=5, warmup=3):
+    """configs[4]'s workload on the paper's prime size (reading R41: 30 x 49-bit chain primes at scale 2^49, 10 x
+    50-bit special primes): every row takes the FP64 NTT with reductions (FpB).  Same batch, layout, circuit and
+    timing as the headline (device time of `steps` steps after `warmup`), plus the NTT's HBM roofline from one
+    profiled step."""
+    import torch
+
+    import synth
+    from paper_2502_00847_b200 import secpe, shard
+    lay = synth.LAYOUTS["argmax_k2"]
+    st = load_sign("sign_7_15_15.json")
+    ctx = secpe.Context(synth.PARAM_SETS["argmax49"], stream=stream.cuda_stream)
+    keys = ctx.keygen(synth.KEY_SEED_BASE + 49, secpe.argmax_rotations(lay))
+    L = ctx.L
+    inp = ctx.new_ct(L, B)
+    all_scores = []
+    for i in range(B):
+        scores = synth.softmax_scores(shard.input_seed(49, i), lay["queries"], lay["prompts"], lay["classes"])
+        all_scores.append(scores)
+        ctx.encrypt_coeffs(keys, ctx.encode(secpe.pack(scores, lay, ctx.N // 2), ctx.scale), L, ctx.scale, 900 + i,
+                           out=secpe.Ct(inp.t[i:i + 1], L, ctx.scale))
+    inp.level, inp.scale = L, ctx.scale
+    ol, _ = ctx.argmax_info(lay, st, L)
+    out = ctx.new_ct(ol, B)
+    for _ in range(warmup):
+        ctx.enc_argmax(keys, inp, lay, st, out=out)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        ctx.enc_argmax(keys, inp, lay, st, out=out)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    ctx.profile_begin()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    ctx.enc_argmax(keys, inp, lay, st, out=out)
+    p1.record(stream)
+    torch.cuda.synchronize()
+    prof = ctx.profile_end()
+    ms_prof = p0.elapsed_time(p1)
+    peak, _ = peaks()
+    ntt, ks = prof["ntt_fp"], prof["keyswitch"]
+    gbs = lambda d: d["bytes"] / (d["ms"] / 1000.0) / 1e9 if d["ms"] > 0 else 0.0
+    r = {"workload": "configs[4] with 30 x 49-bit chain primes nearest 2^49, scale 2^49, 10 x 50-bit special "
+                     "primes (R41; the paper's log Q / L, PAPER.md:327)",
+         "ciphertexts_per_step": B, "ms_per_step": ms, "query_argmax_per_s": lay["queries"] * B / (ms / 1000.0),
+         "ntt_rows": "FpB (FP64 with reductions)" if ntt["ms"] > 0 and prof["ntt_int"]["ms"] == 0 else "mixed",
+         "ntt_gbs": gbs(ntt), "ntt_frac": gbs(ntt) / peak, "ntt_share_of_step": ntt["ms"] / ms_prof,
+         "keyswitch_gbs": gbs(ks), "keyswitch_frac": gbs(ks) / peak,
+         "accuracy": argmax_accuracy(ctx, keys, out, all_scores, lay)}
+    del keys, inp, out, ctx
+    torch.cuda.empty_cache()
+    return r
+
+
 def run_secpe(a):
     import torch
     import torch.distributed as dist
@@ -568,24 +647,7 @@ def run_secpe(a):
     ms_e2e = shard.max_over_ranks(f0.elapsed_time(f1), device="cuda")
     e2e = shard.job_throughput(lay["queries"] * B * a.steps, ws, ms_e2e)
 
-    # client side, outside every timed region: decrypt the step's outputs and decode the labels (argmax
-    # over each query's K window slots, reading R19) against the plaintext argmax of the mean scores
-    n_ok = n_ok_margin = n_margin = n_q = 0
-    for i in range(B):
-        dec = ctx.decrypt(keys, out, i)
-        got = secpe.labels(dec, lay)
-        mean = all_scores[i].mean(axis=1)
-        srt = np.sort(mean, axis=1)
-        above = srt[:, -1] - srt[:, -2] >= 2.0 ** -7  # the Sign margin of the (7,15,15) design
-        truth = np.argmax(mean, axis=1)
-        n_q += len(truth)
-        n_ok += int((got == truth).sum())
-        n_ok_margin += int((got == truth)[above].sum())
-        n_margin += int(above.sum())
-    accuracy = {"queries": n_q, "labels_exact": n_ok / n_q, "labels_exact_above_margin": n_ok_margin / max(1, n_margin),
-                "in_margin_fraction": 1.0 - n_margin / n_q,
-                "note": "decrypted one-hot decoded by argmax over each query's window vs argmax of the plaintext "
-                        "mean scores; 'above margin' = top-1 gap >= 2^-7"}
+    accuracy = argmax_accuracy(ctx, keys, out, all_scores, lay)
 
     if rank != 0:
         if ws > 1:
@@ -662,6 +724,7 @@ def run_secpe(a):
         rf["configs2_mul_relin_rescale_frac"] = c["configs[2]_mul_relin_rescale"]["frac_of_hbm"]
         rf["configs3_rotation_gbs"] = c["configs[3]_rotation"]["alg_gbs"]
         rf["configs3_rotation_frac"] = c["configs[3]_rotation"]["frac_of_hbm"]
+        line["configs4_49bit"] = argmax49_bench(stream)
     if ws == 1 and not a.no_cpu_baseline:
         ora = OracleArgmax()
         dt, q, cores = ora.run()

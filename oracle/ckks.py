@@ -114,8 +114,8 @@ def lib():
             "o_decrypt_residues": (None, [ctypes.c_void_p, u64p, u64p, I, u64p]),
             "o_add": (None, [ctypes.c_void_p, u64p, u64p, I, I, u64p]),
             "o_sub": (None, [ctypes.c_void_p, u64p, u64p, I, I, u64p]),
-            "o_mul_int": (None, [ctypes.c_void_p, u64p, I, ctypes.c_int64, u64p]),
-            "o_add_int": (None, [ctypes.c_void_p, u64p, I, ctypes.c_int64, u64p]),
+            "o_mul_int": (None, [ctypes.c_void_p, u64p, I, ctypes.c_int64, ctypes.c_uint64, u64p]),
+            "o_add_int": (None, [ctypes.c_void_p, u64p, I, ctypes.c_int64, ctypes.c_uint64, u64p]),
             "o_mul_plain": (None, [ctypes.c_void_p, u64p, I, u64p, u64p]),
             "o_tensor": (None, [ctypes.c_void_p, u64p, u64p, I, u64p]),
             "o_keyswitch": (None, [ctypes.c_void_p, u64p, I, u64p, u64p]),
@@ -152,6 +152,19 @@ class _OCtx(ctypes.Structure):
 # ---------------------------------------------------------------------------
 # exact rounding helpers
 # ---------------------------------------------------------------------------
+# Plan constants C = rha(c Delta_c) are integers below 2^120 in magnitude, passed to the C oracle as two words
+# (two's complement 128-bit); with Delta_c ~ q ~ 2^49 the Sign coefficients (up to 2^14.8) give C ~ 2^64.
+CONST_LIMIT = 2 ** 120
+
+
+def wide_int(C):
+    """(c_hi, c_lo) with C = c_hi 2^64 + c_lo, c_lo in [0, 2^64)."""
+    C = int(C)
+    if abs(C) >= CONST_LIMIT:
+        raise OverflowError("constant too large")
+    return C >> 64, C & ((1 << 64) - 1)
+
+
 def round_half_away(x):
     """Exact round-half-away-from-zero of a Python float -> int."""
     a = abs(x)
@@ -505,12 +518,12 @@ class Oracle:
 
     def mul_int_raw(self, a, C):
         out = np.zeros_like(a.data)
-        lib().o_mul_int(self.prm.cptr, P(a.data), a.level + 1, int(C), P(out))
+        lib().o_mul_int(self.prm.cptr, P(a.data), a.level + 1, *wide_int(C), P(out))
         return out
 
     def add_int_raw(self, a, C):
         out = np.zeros_like(a.data)
-        lib().o_add_int(self.prm.cptr, P(a.data), a.level + 1, int(C), P(out))
+        lib().o_add_int(self.prm.cptr, P(a.data), a.level + 1, *wide_int(C), P(out))
         return out
 
     def mul_plain_raw(self, a, pt_ntt):
@@ -743,7 +756,7 @@ class Oracle:
         x = self.drop(x, lv)
         dc = (target_scale * float(self.prm.primes[lv])) / x.scale
         C = round_half_away(c * dc)
-        if abs(C) >= 2 ** 62:
+        if abs(C) >= CONST_LIMIT:
             raise OverflowError("constant too large")
         y = Ct(self.mul_int_raw(x, C), x.scale * dc)
         out = self.rescale(y, target_scale)
@@ -760,7 +773,7 @@ class Oracle:
             x = self.drop(x, lv)
             dc = (target_scale * float(self.prm.primes[lv])) / x.scale
             C = round_half_away(c * dc)
-            if abs(C) >= 2 ** 62:
+            if abs(C) >= CONST_LIMIT:
                 raise OverflowError("constant too large")
             cx = self.mul_int_raw(x, C)
             if acc is None:
@@ -802,7 +815,7 @@ class Oracle:
                 x = self.drop(x, lv)
                 dc = (s * float(self.prm.primes[lv])) / x.scale
                 C = round_half_away(c * dc)
-                if abs(C) >= 2 ** 62:
+                if abs(C) >= CONST_LIMIT:
                     raise OverflowError("constant too large")
                 cx = self.mul_int_raw(x, C)
                 d01 = np.zeros((2, lv + 1, self.prm.N), dtype=np.uint64)

@@ -72,6 +72,15 @@ static inline u64 smod(i64 v, u64 q) {
     return m ? q - m : 0;
 }
 
+/* signed 128-bit integer C = c_hi 2^64 + c_lo (two's complement) -> residue: the plan's constants
+   C = rha(c Delta_c) pass 2^63 once Delta_c ~ q ~ 2^49 and |c| ~ 2^15 (the Sign coefficients) */
+static inline u64 smod_wide(i64 c_hi, u64 c_lo, u64 q) {
+    u128 v = ((u128)(u64)c_hi << 64) | c_lo;
+    if (c_hi >= 0) return (u64)(v % q);
+    u64 m = (u64)((~v + 1) % q); /* |C| mod q */
+    return m ? q - m : 0;
+}
+
 u64 o_mulmod(u64 a, u64 b, u64 q) { return mulmod(a, b, q); }
 u64 o_powmod(u64 a, u64 e, u64 q) { return powmod(a, e, q); }
 
@@ -519,12 +528,13 @@ void o_sub(const OCtx *c, const u64 *a, const u64 *b, int nl, int npoly, u64 *ou
                 out[i] = submod(a[i], b[i], c->primes[l]);
             }
 }
-/* multiply both polynomials by the integer constant C (an integer plaintext with all NTT points = C) */
-void o_mul_int(const OCtx *c, const u64 *a, int nl, i64 C, u64 *out) {
+/* multiply both polynomials by the integer constant C = c_hi 2^64 + c_lo (an integer plaintext with all NTT
+   points = C) */
+void o_mul_int(const OCtx *c, const u64 *a, int nl, i64 c_hi, u64 c_lo, u64 *out) {
     u64 n = NN(c);
     for (int p = 0; p < 2; p++)
         for (int l = 0; l < nl; l++) {
-            u64 q = c->primes[l], cq = smod(C, q);
+            u64 q = c->primes[l], cq = smod_wide(c_hi, c_lo, q);
             for (u64 k = 0; k < n; k++) {
                 u64 i = ((u64)p * nl + l) * n + k;
                 out[i] = mulmod(a[i], cq, q);
@@ -532,11 +542,11 @@ void o_mul_int(const OCtx *c, const u64 *a, int nl, i64 C, u64 *out) {
         }
 }
 /* add the integer constant C to the message: c0 += C (the constant polynomial C has NTT points all = C) */
-void o_add_int(const OCtx *c, const u64 *a, int nl, i64 C, u64 *out) {
+void o_add_int(const OCtx *c, const u64 *a, int nl, i64 c_hi, u64 c_lo, u64 *out) {
     u64 n = NN(c);
     memcpy(out, a, (u64)2 * nl * n * sizeof(u64));
     for (int l = 0; l < nl; l++) {
-        u64 q = c->primes[l], cq = smod(C, q);
+        u64 q = c->primes[l], cq = smod_wide(c_hi, c_lo, q);
         for (u64 k = 0; k < n; k++) out[(u64)l * n + k] = addmod(a[(u64)l * n + k], cq, q);
     }
 }

@@ -17,6 +17,7 @@
 typedef uint64_t u64;
 typedef int64_t i64;
 typedef unsigned __int128 u128;
+typedef __int128 i128;  // plan constants C = rha(c Delta_c), |C| < 2^120 (plan.cu CONST_LIMIT)
 
 #define SECPE_HD __host__ __device__ __forceinline__
 

@@ -58,6 +58,11 @@ u64 h_powmod(u64 a, u64 e, u64 q) {
 }
 u64 h_invmod(u64 a, u64 q) { return h_powmod(a % q, q - 2, q); }
 u64 h_shoup(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
+u64 h_smod128(i128 v, u64 q) {
+    const u128 a = (u128)(v < 0 ? -v : v);
+    const u64 m = (u64)(a % q);
+    return (v < 0 && m) ? q - m : m;
+}
 u64 h_smod(i64 v, u64 q) {
     if (v >= 0) return (u64)v % q;
     u64 m = (u64)(-(v + 1)) % q;  // (|v| - 1) mod q
@@ -392,9 +397,10 @@ void Ctx::build(const u64 *q, int nq_, const u64 *p, int np_, int alpha_, int lo
     }
     // ~50-bit rows on the exact-FP64 NTT with reductions (FpB) for N >= 2^15: measured at N = 2^16 +14 %
     // batched bootstraps (53.9 -> 61.7 per s), +8 % K = 16 argmax with bootstrapping; at N = 2^12 (64-thread
-    // CTAs, latency-bound) the integer path is faster.  SECPE_NO_FPB=1 keeps them on the integer Shoup NTT
-    const char *nofpb = getenv("SECPE_NO_FPB");
-    const bool use_fpb = !(nofpb && atoi(nofpb) == 1) && logn_ >= 15;
+    // CTAs, latency-bound) the integer path is faster.  SECPE_NO_FPB=1 keeps them on the integer Shoup NTT;
+    // SECPE_FPB=1 takes FpB on every ring (the N = 2^12 parity tests of the FpB path), SECPE_FPB=0 on none
+    const char *nofpb = getenv("SECPE_NO_FPB"), *fpb = getenv("SECPE_FPB");
+    const bool use_fpb = fpb ? atoi(fpb) == 1 : !(nofpb && atoi(nofpb) == 1) && logn_ >= 15;
     constexpr u64 FPB_TABLE_LIMIT = 1286742750677284ULL;  // floor(2^52 / 3.5), ntt_core.cuh FPB_LIMIT
     logn = logn_;
     N = 1L << logn;

@@ -191,6 +191,7 @@ u64 h_powmod(u64 a, u64 e, u64 q);
 u64 h_invmod(u64 a, u64 q);
 u64 h_shoup(u64 w, u64 q);
 u64 h_smod(i64 v, u64 q);
+u64 h_smod128(i128 v, u64 q);  // |v| < 2^127
 bool h_is_prime(u64 n);
 int h_gen_primes(int bits, int count, int logn, int mode, const u64 *ex, int nex, u64 *out);
 u64 h_find_psi(u64 q, int logn);
@@ -205,8 +206,8 @@ void ev_ntt(Ctx &c, RowsArg d, int n_polys, LimbMap lm, bool inverse, const NttF
 void ev_ntt_segs(Ctx &c, const std::vector<NttSeg> &segs, bool inverse);
 void ev_copy(Ctx &c, const CtView &a, const CtView &out);
 void ev_addsub(Ctx &c, const CtView &a, const CtView &b, const CtView &out, bool sub);
-void ev_mul_int(Ctx &c, const CtView &a, i64 C, const CtView &out);
-void ev_add_int(Ctx &c, const CtView &a, i64 C, const CtView &out);
+void ev_mul_int(Ctx &c, const CtView &a, i128 C, const CtView &out);
+void ev_add_int(Ctx &c, const CtView &a, i128 C, const CtView &out);
 void ev_rescale(Ctx &c, const CtView &in, const CtView &out);
 void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, const u64 *add,
                   long add_stride, int add_polys, u64 *out, long out_stride, const CRows *add3 = nullptr);
@@ -214,12 +215,12 @@ void ev_mul_relin(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const
 // a (x) b [+ a2 (x) b2] [+ C x] relinearised and rescaled by q_l in one pass (bit-identical to ev_mul_relin
 // then ev_rescale); out at level a.level - 1.  lin_x: optional linear term (nullptr: none), C its constant;
 // a2, b2: optional second product summed into the tensor before the relinearisation (R13b)
-void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const CtView *lin_x, i64 C,
-                          const CtView &out, const CtView *lin_x2 = nullptr, i64 C2 = 0, const CtView *a2 = nullptr,
+void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const CtView *lin_x, i128 C,
+                          const CtView &out, const CtView *lin_x2 = nullptr, i128 C2 = 0, const CtView *a2 = nullptr,
                           const CtView *b2 = nullptr);
-void ev_lincomb(Ctx &c, const CtView &a, i64 C1, const CtView *b, i64 C2, const CtView &out);
+void ev_lincomb(Ctx &c, const CtView &a, i128 C1, const CtView *b, i128 C2, const CtView &out);
 // rescale(C1 x1 + C2 x2) with the constant products fused into the rescale's transforms (x2 optional)
-void ev_rescale_lin(Ctx &c, const CtView &x1, i64 C1, const CtView *x2, i64 C2, const CtView &out);
+void ev_rescale_lin(Ctx &c, const CtView &x1, i128 C1, const CtView *x2, i128 C2, const CtView &out);
 void ev_rotate(Ctx &c, const Keys &k, const CtView &in, int steps, const CtView &out,
                const CtView *add_after = nullptr);  // add_after: out = RotL(in) + add_after (fused)
 void ev_rotate_hoisted(Ctx &c, const Keys &k, const CtView &in, const int *steps, int n_steps, const CtView *outs);
@@ -231,7 +232,7 @@ void ev_linear_transform_bsgs_gen(Ctx &c, const Keys &k, const CtView &in, const
 void ev_linear_transform_bsgs(Ctx &c, const Keys &k, const CtView &in, const u64 *pts, long pt_stride, int n1, int n2,
                               const CtView &out);
 void ev_mul_plain_ntt(Ctx &c, const CtView &a, const u64 *pt, const CtView &out);
-LimbConst limb_const(const Ctx &c, i64 C, int nl);
+LimbConst limb_const(const Ctx &c, i128 C, int nl);
 
 // host encode/decode (encode.cpp)
 void encode_real(const Ctx &c, const double *slots, size_t n, double scale, std::vector<double> &coef);

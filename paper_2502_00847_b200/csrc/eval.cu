@@ -15,11 +15,11 @@ CtView compact_view(const Ctx &c, u64 *data, int n, int level, double scale) {
     return CtView{data, 2L * (level + 1) * c.N, (long)(level + 1) * c.N, n, level, scale};
 }
 
-LimbConst limb_const(const Ctx &c, i64 C, int nl) {
+LimbConst limb_const(const Ctx &c, i128 C, int nl) {
     LimbConst lc{};
     for (int l = 0; l < nl; l++) {
         const u64 q = c.primes[l];
-        lc.c[l] = h_smod(C, q);
+        lc.c[l] = h_smod128(C, q);
         lc.csh[l] = h_shoup(lc.c[l], q);
     }
     return lc;
@@ -83,13 +83,13 @@ void ev_addsub(Ctx &c, const CtView &a, const CtView &b, const CtView &out, bool
     c.cnt.launches++;
 }
 
-void ev_mul_int(Ctx &c, const CtView &a, i64 C, const CtView &out) {
+void ev_mul_int(Ctx &c, const CtView &a, i128 C, const CtView &out) {
     const int nl = out.level + 1;
     k_mul_const(c.tab, c.logn, crows_of(a), rows_of(out), 2 * a.n, qmap(nl), limb_const(c, C, nl), c.st);
     c.cnt.launches++;
 }
 
-void ev_add_int(Ctx &c, const CtView &a, i64 C, const CtView &out) {
+void ev_add_int(Ctx &c, const CtView &a, i128 C, const CtView &out) {
     const int nl = out.level + 1;
     // c0 rows of every ct (poly P = ct: cs = 2 * stride, ps = stride), then copy c1 if out != a
     k_add_const(c.tab, c.logn, CRows{a.data, 2 * a.stride, a.stride}, RowsArg{out.data, 2 * out.stride, out.stride},
@@ -103,7 +103,7 @@ void ev_add_int(Ctx &c, const CtView &a, i64 C, const CtView &out) {
 }
 
 // C1 a + C2 b (b may be null) at out's level (no rescale; the planner rescales the sum once)
-void ev_lincomb(Ctx &c, const CtView &a, i64 C1, const CtView *b, i64 C2, const CtView &out) {
+void ev_lincomb(Ctx &c, const CtView &a, i128 C1, const CtView *b, i128 C2, const CtView &out) {
     const int nl = out.level + 1;
     k_lincomb2(c.tab, c.logn, crows_of(a), b ? crows_of(*b) : CRows{nullptr, 0, 0}, rows_of(out), 2 * a.n, qmap(nl),
                limb_const(c, C1, nl), b ? limb_const(c, C2, nl) : LimbConst{}, c.st);
@@ -151,7 +151,7 @@ void ev_rescale(Ctx &c, const CtView &in, const CtView &out) {
 // Rescale of C1 x1 (+ C2 x2) with the constant products fused in (no intermediate ciphertext): the INTT
 // of the top limb forms C1 x1 + C2 x2 in its first pass, the rescale epilogue forms it per limb.  The
 // same integers as ev_mul_int / ev_lincomb followed by ev_rescale.
-void ev_rescale_lin(Ctx &c, const CtView &x1, i64 C1, const CtView *x2, i64 C2, const CtView &out) {
+void ev_rescale_lin(Ctx &c, const CtView &x1, i128 C1, const CtView *x2, i128 C2, const CtView &out) {
     const size_t pa = c.prof_begin(2);
     const int l = out.level + 1;
     if (l < 1) throw SecpeError{-2, "rescale: no level left"};
@@ -337,8 +337,8 @@ static void ks_moddown(Ctx &c, DevBuf &acc, int n, int level, const u64 *add, lo
 // Y_b = (x_b - ModDownConv(x_b)) P^{-1} and its rescale is (Y_b + half - [r]) q_l^{-1}; both
 // corrections are computed in the coefficient domain (k_rr_conv) and removed by ONE forward NTT whose
 // epilogue forms (x_i - NTT(T_i)) (P q_l)^{-1}.  This saves the rescale's own INTT/NTT round trip.
-void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const CtView *lin_x, i64 C,
-                          const CtView &out, const CtView *lin_x2, i64 C2, const CtView *a2, const CtView *b2) {
+void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &b, const CtView *lin_x, i128 C,
+                          const CtView &out, const CtView *lin_x2, i128 C2, const CtView *a2, const CtView *b2) {
     const int l = a.level, nl = l + 1;
     if (l < 1) throw SecpeError{-2, "mul_relin_rescale: no level left"};
     if (b.level != l || out.level != l - 1) throw SecpeError{-1, "mul_relin_rescale: levels"};

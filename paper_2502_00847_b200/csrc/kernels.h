@@ -49,7 +49,7 @@ struct NttFusion {
     // C1 src + C2 src2 instead of src (in_mode 5 on the INTT of the top limb), and the rescale epilogue
     // (out_mode 1) uses C1 e1 + C2 e1b instead of e1; lin = number of terms (0: plain)
     int lin = 0;
-    i64 C1 = 0, C2 = 0;
+    i128 C1 = 0, C2 = 0;
     CRows e1b{nullptr, 0, 0};
     RowsArg out{nullptr, 0, 0};
     const u64 *k = nullptr, *ksh = nullptr;

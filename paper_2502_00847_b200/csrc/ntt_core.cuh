@@ -251,8 +251,9 @@ struct PairTw : A {
 #endif
 
 // [C]_q for a signed constant |C| < 2^62 (R9 constants), with the prime's Barrett constants
-__device__ __forceinline__ u64 smod_dev(i64 C, u64 q, u64 br0, u64 br1) {
-    const u64 m = barrett128(U128{(u64)(C < 0 ? -C : C), 0}, q, br0, br1);
+__device__ __forceinline__ u64 smod_dev(i128 C, u64 q, u64 br0, u64 br1) {
+    const u128 a = (u128)(C < 0 ? -C : C);  // |C| < 2^120: within barrett128's 2^125
+    const u64 m = barrett128(U128{(u64)a, (u64)(a >> 64)}, q, br0, br1);
     return (C < 0 && m) ? q - m : m;
 }
 

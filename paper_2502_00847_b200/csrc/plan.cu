@@ -82,9 +82,7 @@ struct Ev {
         if (lv < 1) throw SecpeError{-2, "mul_const: no level left"};
         Val xd = drop(x, lv);
         const double dc = (St * q(lv)) / x.scale();
-        const double Cd = round_half_away(cval * dc);
-        if (!(std::fabs(Cd) < 4611686018427387904.0)) throw SecpeError{-6, "constant exceeds 2^62"};
-        const i64 C = (i64)Cd;
+        const i128 C = const_of(round_half_away(cval * dc));
         Val out = fresh(Lt, St);
         if (SECPE_FUSE_LIN) {
             ev_rescale_lin(c, xd.v, C, nullptr, 0, out.v);  // C x rescaled, the product fused in
@@ -94,20 +92,35 @@ struct Ev {
             ev_rescale(c, tmp.v, out.v);
         }
         c.cnt.mulconst += n;
-        c.log("MULC", lv, Lt, St, std::to_string((long long)C));
+        c.log("MULC", lv, Lt, St, int_str(C));
         return out;
     }
     // integer constant C = rha(c Delta), Delta = (S_t q_l) / S_x (R9)
-    i64 lin_const(double cval, double St, int lv, double Sx) {
+    i128 lin_const(double cval, double St, int lv, double Sx) {
         const double dc = (St * q(lv)) / Sx;
-        const double Cd = round_half_away(cval * dc);
-        if (!(std::fabs(Cd) < 4611686018427387904.0)) throw SecpeError{-6, "constant exceeds 2^62"};
-        return (i64)Cd;
+        return const_of(round_half_away(cval * dc));
+    }
+    // the integer value of an integer-valued double, |C| < 2^120 (with Delta_c ~ q ~ 2^49 the Sign coefficients,
+    // up to 2^14.8, give C ~ 2^64; the conversion of an integer-valued double is exact)
+    static i128 const_of(double Cd) {
+        if (!(std::fabs(Cd) < 1329227995784915872903807060280344576.0)) throw SecpeError{-6, "constant exceeds 2^120"};
+        return (i128)Cd;
+    }
+    static std::string int_str(i128 v) {
+        if (v == 0) return "0";
+        const bool neg = v < 0;
+        u128 a = (u128)(neg ? -v : v);
+        std::string r;
+        while (a) {
+            r.insert(r.begin(), char('0' + (int)(a % 10)));
+            a /= 10;
+        }
+        return neg ? "-" + r : r;
     }
     using Lin = std::vector<std::pair<const Val *, double>>;
-    static std::string join(const std::vector<i64> &v) {
+    static std::string join(const std::vector<i128> &v) {
         std::string r;
-        for (size_t i = 0; i < v.size(); i++) r += (i ? "," : "") + std::to_string((long long)v[i]);
+        for (size_t i = 0; i < v.size(); i++) r += (i ? "," : "") + int_str(v[i]);
         return r;
     }
     // a (x) b [+ sum c x] relinearised and rescaled in one pass; St = NAN: natural scale (S_a S_b) / q_l.
@@ -124,7 +137,7 @@ struct Ev {
         const double s = std::isnan(St) ? (a.scale() * b.scale()) / q(lv) : St;
         Val out = fresh(Lt, s);
         std::vector<Val> xs;
-        std::vector<i64> Cs;
+        std::vector<i128> Cs;
         for (auto &t : lin) {
             xs.push_back(drop(*t.first, lv));
             Cs.push_back(lin_const(t.second, s, lv, t.first->scale()));
@@ -141,7 +154,7 @@ struct Ev {
         if (lv < 1) throw SecpeError{-2, "lincomb: no level left"};
         if (terms.empty() || terms.size() > 2) throw SecpeError{-1, "lincomb: one or two terms"};
         std::vector<Val> xs;
-        std::vector<i64> Cs;
+        std::vector<i128> Cs;
         for (auto &t : terms) {
             xs.push_back(drop(*t.first, lv));
             Cs.push_back(lin_const(t.second, St, lv, t.first->scale()));
@@ -191,12 +204,10 @@ struct Ev {
         return out;
     }
     Val add_const(const Val &x, double cval) {
-        const double Cd = round_half_away(cval * x.scale());
-        if (!(std::fabs(Cd) < 4611686018427387904.0)) throw SecpeError{-6, "constant exceeds 2^62"};
-        const i64 C = (i64)Cd;
+        const i128 C = const_of(round_half_away(cval * x.scale()));
         Val out = fresh(x.level(), x.scale());
         ev_add_int(c, x.v, C, out.v);
-        c.log("ADDC", x.level(), x.level(), x.scale(), std::to_string((long long)C));
+        c.log("ADDC", x.level(), x.level(), x.scale(), int_str(C));
         return out;
     }
 

@@ -57,6 +57,11 @@ PARAM_SETS = {
     # the paper's ring (N = 2^16, 32768 slots) with the factorised transforms (R37, groups 5/5/5: depth 20)
     "boot16": dict(logn=16, q=[("below", 60, 1), ("nearest", 50, 22)], p=[("below", 50, 8)],
                    alpha=7, log_scale=50),
+    # configs[4] at the paper's prime size (log Q = 1763 over L = 35 levels, ~49-bit primes; reading
+    # R41): 30 chain primes nearest 2^49 at scale 2^49, 10 special primes below 2^50 (P ~ 2^500 > every 10-prime
+    # digit ~ 2^490); every row of Q u P takes the FP64 NTT with reductions (FpB) at N >= 2^15
+    "argmax49": dict(logn=16, q=[("nearest", 49, 30)], p=[("below", 50, 10)], alpha=10, log_scale=49),
+    "argmax_small49": dict(logn=12, q=[("nearest", 49, 30)], p=[("below", 50, 10)], alpha=10, log_scale=49),
     # BASELINE configs[1]: NTT microbench, 24 x 60-bit primes, N = 2^16.
     "ntt": dict(logn=16, q=[("below", 60, 24)], p=[], alpha=8, log_scale=50),
     # BASELINE configs[2]/[3]: 24 x 60-bit q, dnum = 3 -> alpha = 8, 8 special 60-bit primes, scale 2^50.

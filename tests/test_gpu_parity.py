@@ -373,6 +373,29 @@ def test_argmax_small_ring_bit_exact(S):
     run_argmax_pair(S, "argmax_small", "argmax_small_k2", "sign_7_15_15.json", 5001, n_ct=2, oracle_cts=2)
 
 
+@pytest.mark.parametrize("fpb", ["0", "1"])
+def test_argmax_small49_bit_exact(S, monkeypatch, fpb):
+    """configs[4]'s circuit on 49-bit primes at scale 2^49 (reading R41, the paper's prime size): plan constants
+    pass 2^63 (wide constants); with SECPE_FPB=1 every row of Q u P takes the FP64 NTT with reductions (FpB) that
+    N >= 2^15 uses by default, with 0 the integer NTT -- both word for word against the oracle, identical op
+    logs."""
+    monkeypatch.setenv("SECPE_FPB", fpb)
+    _pairs.pop("argmax_small49", None)
+    try:
+        run_argmax_pair(S, "argmax_small49", "argmax_small_k2", "sign_7_15_15.json", 5101, n_ct=2, oracle_cts=1)
+        P = pair(S, "argmax_small49")
+        assert max(P.prm.q + P.prm.p) >= 2 ** 46  # FpB-class rows
+    finally:
+        _pairs.pop("argmax_small49", None)
+
+
+@pytest.mark.slow
+def test_argmax49_full(S):
+    """configs[4] at 49-bit primes (R41) at full size (N = 2^16, FpB rows by default), batch of 2: ciphertext 0
+    bit-exact against the oracle, every label exact above the margin."""
+    run_argmax_pair(S, "argmax49", "argmax_k2", "sign_7_15_15.json", 1000 * 5 + 11, n_ct=2, oracle_cts=1)
+
+
 @pytest.mark.slow
 def test_argmax_config5_full(S):
     """BASELINE configs[4] at full size (N = 2^16, 30 limbs, 2048 queries x P=8 x K=2), batch of 2 as bench:

@@ -331,6 +331,30 @@ def test_keyswitch_bigint_bound(tiny):
             assert abs(_centered(x, Q)) < 2 ** 20
 
 
+def test_wide_constants_big_int(tiny):
+    """Constant products and additions with |C| >= 2^63 (reading R41: C = rha(c Delta_c) ~ 2^64 at 49-bit
+    primes): every residue equals Python's big-int a C mod q and (a + C) mod q; wide_int splits into two's
+    complement words; constants at the 2^120 limit raise."""
+    prm, ev = tiny, ckks.Oracle(tiny)
+    rng = np.random.default_rng(41)
+    nl = prm.L + 1
+    a = ckks.Ct(np.stack([np.stack([rng.integers(0, q, prm.N).astype(np.uint64) for q in prm.q[:nl]])
+                          for _ in range(2)]), prm.scale)
+    for C in (2 ** 64 + 12345, -(2 ** 64) - 7, 2 ** 100 - 3, -(2 ** 119), 2 ** 63, -(2 ** 63) - 1, 5, -5):
+        hi, lo = ckks.wide_int(C)
+        assert hi * 2 ** 64 + lo == C and 0 <= lo < 2 ** 64 and -(2 ** 63) <= hi < 2 ** 63
+        m = ev.mul_int_raw(a, C)
+        s = ev.add_int_raw(a, C)
+        for l, q in enumerate(prm.q[:nl]):
+            for k in (0, 1, prm.N - 1):
+                for p_ in (0, 1):
+                    assert int(m[p_, l, k]) == int(a.data[p_, l, k]) * C % q
+                assert int(s[0, l, k]) == (int(a.data[0, l, k]) + C) % q
+                assert int(s[1, l, k]) == int(a.data[1, l, k])
+    with pytest.raises(OverflowError):
+        ev.mul_int_raw(a, 2 ** 120)
+
+
 def test_ops_against_slots(toy):
     ev = ckks.Oracle(toy)
     keys = ev.keygen(5, [1, -1, 3])
