@@ -45,17 +45,21 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+constexpr double TC_MAGIC = 6755399441055744.0;  // 1.5 2^52
+constexpr double TC_TWO52 = 4503599627370496.0;
+
 __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
     extern __shared__ __align__(128) uint8_t tsm[];
     uint8_t *sA = tsm;                      // TC_M * TC_K
     uint8_t *sB = tsm + TC_M * TC_K;        // 8 * TC_TMAX * TC_K
+    uint8_t *sR = sB + 8 * TC_TMAX * TC_K;  // TC_M * TC_K: the r source of the fused ModDown + rescale, zero elsewhere
     __shared__ __align__(8) uint64_t mbar;
     __shared__ uint32_t tslot;
     // per-target constants staged once per CTA: prime, output row offset, 1/q, [P]_{q_t} (+ Shoup)
     __shared__ u64 sq[TC_TMAX], spm[TC_TMAX], spmsh[TC_TMAX];
     __shared__ double sqinv[TC_TMAX];
     __shared__ long soff[TC_TMAX];
-    // the same per-target constants packed for the 6-plane epilogue: {q, -q, 1/q, byte offset of the row}
+    // the same per-target constants packed for the 6-plane epilogue: {q, -q, 2^16/q, byte offset of the row}
     __shared__ __align__(16) ulonglong2 spk[TC_TMAX][2];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int p = blockIdx.y;
@@ -64,6 +68,9 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
     const int ncols = G.ncols, planes = G.planes;  // MMA N (multiple of 16), byte planes per target
     const int ksteps = (8 * ns + 31) / 32;
     const long N = 1L << a.logn;
+    // fused ModDown + rescale with r as a third source: a second MMA adds r [P]_{q_i} once r is known, so every
+    // target's epilogue is the plain conversion epilogue
+    const bool rr2 = a.rr && G.rslot >= 0;
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tslot)),
@@ -78,21 +85,27 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
         spmsh[tid] = G.pmodsh[tid];
         soff[tid] = (long)G.out_row[tid] << a.logn;
         spk[tid][0] = make_ulonglong2(q, (u64)0 - q);
-        spk[tid][1] = make_ulonglong2((u64)__double_as_longlong(G.qinv[tid]), (u64)(((long)G.out_row[tid] << a.logn) * 8));
+        spk[tid][1] = make_ulonglong2((u64)__double_as_longlong(G.qinv[tid] * 65536.0),
+                                      (u64)(((long)G.out_row[tid] << a.logn) * 8));
     }
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar)));
         asm volatile("fence.mbarrier_init.release.cluster;\n");
     }
-    {  // B (canonical, 8 ntp rows x TC_K bytes) and a zeroed A (the constant-1 source written once)
+    {  // B (canonical, 8 ntp rows x TC_K bytes) and a zeroed A (the constant-1 source written once) and R
         const uint4 *gb = reinterpret_cast<const uint4 *>(G.B);
         uint4 *b4 = reinterpret_cast<uint4 *>(sB);
         for (int i = tid; i < ncols * TC_K / 16; i += TC_THREADS) b4[i] = gb[i];
         uint4 *a4 = reinterpret_cast<uint4 *>(sA);
         for (int i = tid; i < TC_M * TC_K / 16; i += TC_THREADS) a4[i] = make_uint4(0, 0, 0, 0);
+        if (rr2) {
+            uint4 *r4 = reinterpret_cast<uint4 *>(sR);
+            for (int i = tid; i < TC_M * TC_K / 16; i += TC_THREADS) r4[i] = make_uint4(0, 0, 0, 0);
+        }
     }
     __syncthreads();
     if (a.const1 && tid < TC_M) *reinterpret_cast<u64 *>(sA + canon(tid, 8 * G.ns)) = 1;
+    asm volatile("fence.proxy.async.shared::cta;\n");
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
@@ -106,7 +119,9 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
     // staging: thread (row, half) holds sources s = half, half + 2, ... of coefficient row; the next
     // tile's values are loaded into registers before the current tile's epilogue
     const int srow = tid & (TC_M - 1), shalf = tid >> 7;  // 4 threads per coefficient row
-    u64 pre[3];
+    u64 pre[3], prexc = 0;
+    // rr: the coefficient-form row x_l the prelude needs, fetched with the sources (warps 0-3: m == srow)
+    const bool xc_here = a.rr && (!rr2 || tpar == 0);
     auto fetch = [&](int tile) {
         const long k0 = (long)tile * TC_M;
 #pragma unroll
@@ -114,12 +129,25 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
             const int s = shalf + 4 * u;
             if (s < G.ns) pre[u] = src[(long)s * N + k0 + srow];
         }
+        if (xc_here) prexc = src[(long)(-1) * N + k0 + m];
     };
     pdl_wait();  // TMEM, constants and the B matrix above do not depend on the previous kernel
     if ((int)blockIdx.x < ntiles) fetch(blockIdx.x);
-    int it = 0;
+    uint32_t phase = 0;  // mbarrier phase (one or two MMA commits per tile)
+    auto mma_wait = [&]() {
+        uint32_t done = 0;
+        const uint32_t mb = smem_u32(&mbar);
+        while (!done)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}\n"
+                : "=r"(done)
+                : "r"(mb), "r"(phase));
+        phase ^= 1;
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+    };
     u64 rrv = 0;  // fused ModDown + rescale: r of this thread's coefficient
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long k0 = (long)tile * TC_M;
 #pragma unroll
         for (int u = 0; u < 3; u++) {
@@ -143,25 +171,10 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                 smem_u32(&mbar)));
         }
-        {
-            uint32_t done = 0;
-            const uint32_t mb = smem_u32(&mbar), par = it & 1;
-            while (!done)
-                asm volatile(
-                    "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-                    "selp.u32 %0, 1, 0, p;\n\t}\n"
-                    : "=r"(done)
-                    : "r"(mb), "r"(par));
-        }
-        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        mma_wait();
+        const u64 xc = prexc;
         if (tile + (int)gridDim.x < ntiles) fetch(tile + gridDim.x);  // overlaps the epilogue below
         // epilogue: per target, the byte-plane sums G_b (< 96 * 255^2 < 2^23) -> V = sum_b G_b 256^b -> V mod t.
-        // 6 planes (targets < 2^46): V < 2^64 is one u64 (three wide multiply-adds + two 32-bit adds on the
-        // high word); 8 planes: V = lo + hi 2^32 with lo, hi < 2^47.  The quotient k = rint(V / t) comes from
-        // FP64 (V as a double: two exact conversions and one FMA; k = fma(V, 1/t, 1.5 2^52) - its low word
-        // is k, k < 2^21), r = V - k t is exact mod 2^64 and lies in (-t, t): one conditional add of t.
-        // Each warp takes a contiguous block of targets so two targets' planes come in with one or two
-        // TMEM loads (12 or 16 consecutive columns).
         const uint32_t lane_base = tmem + ((uint32_t)(32 * lq) << 16);
         auto v6 = [](const uint32_t *g) -> u64 {
             u64 v = (u64)g[0] + (u64)g[1] * 256u;
@@ -170,24 +183,24 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
             return v + ((u64)(g[4] + g[5] * 256u) << 32);
         };
         auto to_d = [](u64 x) -> double {  // exact for x < 2^52
-            return __dsub_rn(__longlong_as_double((long long)(x | 0x4330000000000000ULL)), 4503599627370496.0);
+            return __dsub_rn(__longlong_as_double((long long)(x | 0x4330000000000000ULL)), TC_TWO52);
         };
         // V given as lo + hi 2^32 (hi < 2^32 for 6 planes, < 2^47 for 8), V mod 2^64 = vw.  6 planes: V < 2^64
         // and t > 2^40, so k < 2^24 (32-bit product); 8 planes: V < 2^79, k < 2^39 (64-bit product)
         auto reduce = [&](u64 lo, u64 hi, u64 vw, int t, bool wide) -> u64 {
             const u64 q = sq[t];
             const double vd = __fma_rn(to_d(hi), 4294967296.0, to_d(lo));
-            const double kb = __fma_rn(vd, sqinv[t], 6755399441055744.0);  // k + 1.5 2^52
+            const double kb = __fma_rn(vd, sqinv[t], TC_MAGIC);  // k + 1.5 2^52
             const u64 kq = wide ? ((u64)__double_as_longlong(kb) & ((1ULL << 51) - 1)) * q
                                 : (u64)(uint32_t)__double_as_longlong(kb) * q;
             const long long r = (long long)(vw - kq);
             return (u64)(r + ((r >> 63) & (long long)q));
         };
         auto emit = [&](u64 z, int t) {
-            if (a.rr) z = addmod(z, csub(mul_shoup(rrv, spm[t], spmsh[t], sq[t]), sq[t]), sq[t]);
+            if (a.rr && !rr2) z = addmod(z, csub(mul_shoup(rrv, spm[t], spmsh[t], sq[t]), sq[t]), sq[t]);
             dst[soff[t] + k0 + m] = z;
         };
-        if (a.rr) {
+        if (a.rr && xc_here) {
             // fused ModDown + rescale prelude (target 0 = q_l): Y_l = (xc - T_l) P^{-1}, r = [Y_l + floor(q_l/2)]
             const u64 ql = sq[0];
             uint32_t g[8];
@@ -212,30 +225,55 @@ __global__ void __launch_bounds__(TC_THREADS) bconv_tc_kernel(TcArgs a) {
                 const u64 hi = (u64)g[4] + (u64)g[5] * 256u + (u64)g[6] * 65536u + (u64)g[7] * 16777216u;
                 tl = reduce(lo, hi, lo + (hi << 32), 0, true);
             }
-            const u64 xc = src[(long)(-1) * N + k0 + m];
             rrv = csub(mul_shoup(submod(xc, tl, ql), a.pinv_l, a.pinv_l_sh, ql) + (ql >> 1), ql);
+            if (rr2) *reinterpret_cast<u64 *>(sR + canon(m, 8 * G.rslot)) = rrv;
+        }
+        if (rr2) {
+            // second MMA: the accumulators += r [P]_{q_i} (the K-step of sR holding r; its other bytes are zero)
+            asm volatile("fence.proxy.async.shared::cta;\n");
+            asm volatile("tcgen05.fence::before_thread_sync;\n");
+            __syncthreads();
+            asm volatile("tcgen05.fence::after_thread_sync;\n");
+            if (tid == 0) {
+                const int ks = (8 * G.rslot) / 32;
+                const uint64_t da = smem_desc(smem_u32(sR) + ks * 2 * LBO), db = smem_desc(smem_u32(sB) + ks * 2 * LBO);
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+                    "l"(da), "l"(db), "r"(idesc), "r"(1));
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                    smem_u32(&mbar)));
+            }
+            mma_wait();
         }
         const int t0 = a.rr ? 1 : 0;
         const int per = (nt - t0 + 3) >> 2;  // targets per warp group (contiguous)
         const int tb = t0 + tpar * per, te = min(nt, tb + per);
-        if (planes == 6 && !a.rr) {
-            // lean path: V = sum G_b 256^b < 2^64 (three wide multiply-adds + the high word), k = rint(V / q) from
-            // FP64 (low word of fma(V, 1/q, 1.5 2^52)), r = V + k (-q) (two multiply-adds), one predicated add
+        if (planes == 6 && (!a.rr || rr2)) {
+            // lean path: A = G0 + 256 G1, B = G2 + 256 G3, C = G4 + 256 G5 (each < 2^31), V = A + B 2^16 + C 2^32
+            // (< 2^61: V < 96 * 255 t).  k = rint((V - A) / t) = rint((C 2^16 + B) * RN(2^16 / t)) from one FP64
+            // product (A / t < 2^-13), so V - k t lies in (-t/2 - 1, t/2 + 2^32): one conditional add of t.  V - k t
+            // is formed exactly mod 2^64 from the two 32-bit words of V and k (-t).
             uint8_t *const obase = reinterpret_cast<uint8_t *>(dst + k0 + m);
             auto lean = [&](const uint32_t *x, int t) {
                 const ulonglong2 c0 = spk[t][0], c1 = spk[t][1];
-                u64 v = (u64)x[0] + (u64)x[1] * 256u;
-                v += (u64)x[2] * 65536u;
-                v += (u64)x[3] * 16777216u;
-                const uint32_t vh = (uint32_t)(v >> 32) + x[4] + x[5] * 256u, vl = (uint32_t)v;
-                v = ((u64)vh << 32) | vl;
-                const double vd = __fma_rn(__dsub_rn(__hiloint2double(0x43300000, (int)vh), 4503599627370496.0),
-                                           4294967296.0,
-                                           __dsub_rn(__hiloint2double(0x43300000, (int)vl), 4503599627370496.0));
-                const uint32_t k = (uint32_t)__double_as_longlong(
-                    __fma_rn(vd, __longlong_as_double((long long)c1.x), 6755399441055744.0));
-                u64 r = v + (u64)k * c0.y;
-                if ((int)(r >> 32) < 0) r += c0.x;
+                const uint32_t A = x[0] + (x[1] << 8), B = x[2] + (x[3] << 8), C = x[4] + (x[5] << 8);
+                const double cb = __fma_rn(__dsub_rn(__hiloint2double(0x43300000, (int)C), TC_TWO52), 65536.0,
+                                           __dsub_rn(__hiloint2double(0x43300000, (int)B), TC_TWO52));
+                const uint32_t k =
+                    (uint32_t)__double_as_longlong(__fma_rn(cb, __longlong_as_double((long long)c1.x), TC_MAGIC));
+                uint32_t lo, hi;
+                asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
+                    : "=r"(lo), "=r"(hi)
+                    : "r"(A), "r"(B << 16), "r"(C), "r"(B >> 16));
+                u64 r = (((u64)hi << 32) | lo) + (u64)k * c0.y;
+                asm("{\n\t.reg .pred p;\n\t.reg .u32 rl, rh, tl, th;\n\t"
+                    "mov.b64 {rl, rh}, %0;\n\tmov.b64 {tl, th}, %1;\n\t"
+                    "setp.lt.s32 p, rh, 0;\n\t"
+                    "@p add.cc.u32 rl, rl, tl;\n\t@p addc.u32 rh, rh, th;\n\t"
+                    "mov.b64 %0, {rl, rh};\n\t}"
+                    : "+l"(r)
+                    : "l"(c0.x));  // + t when negative (predicated, 3 instructions)
                 *reinterpret_cast<u64 *>(obase + c1.y) = r;
             };
             for (int t = tb; t < te; t += 2) {

@@ -213,6 +213,9 @@ void Ctx::log(const char *kind, int lin, int lout, double s, const std::string &
 #ifndef SECPE_TC_PLANES6
 #define SECPE_TC_PLANES6 1  // development switch: 0 = 8 byte planes and the integer epilogue everywhere
 #endif
+#ifndef SECPE_TC_RSLOT
+#define SECPE_TC_RSLOT 1  // development switch: 0 = the fused ModDown + rescale adds r [P]_{q_i} per output
+#endif
 void Ctx::build_tc_groups(LevelConsts &lc, int l) {
     const int nl = l + 1, ne = nl + np, bt = beta(l);
     auto pid = [&](int e) { return e < nl ? e : nq + (e - nl); };
@@ -220,7 +223,7 @@ void Ctx::build_tc_groups(LevelConsts &lc, int l) {
     std::vector<std::vector<uint8_t>> Bs;
     bool ok = np >= 1 && np + 1 <= 12;
     auto add = [&](TcGroup g, const std::vector<std::vector<u64>> &c, const std::vector<u64> &tp) {
-        if (g.ns + 1 > 12 || g.nt > TC_TMAX) ok = false;
+        if (g.ns + 1 > 12 || (int)c.size() > 12 || g.nt > TC_TMAX) ok = false;
         if (!ok) return;
         // 6 byte planes suffice when every constant (< target prime) is < 2^48
         bool small = true;
@@ -279,7 +282,11 @@ void Ctx::build_tc_groups(LevelConsts &lc, int l) {
         g.ns = np;
         g.src_row0 = l + 1;
         std::vector<u64> tp;
-        std::vector<std::vector<u64>> c(np + 1);
+        // with a free source slot, r [P]_{q_i} is a third source (slot np + 1) that a second MMA adds once r is
+        // known (bconv_tc_kernel); else the epilogue adds it per output
+        const bool rs = np + 2 <= 12 && SECPE_TC_RSLOT;
+        std::vector<std::vector<u64>> c(np + (rs ? 2 : 1));
+        g.rslot = rs ? np + 1 : -1;
         if (l >= 1 && l + 1 <= TC_TMAX) {
             const u64 ql = primes[l];
             g.prime[0] = l;
@@ -287,6 +294,7 @@ void Ctx::build_tc_groups(LevelConsts &lc, int l) {
             tp.push_back(ql);
             for (int p = 0; p < np; p++) c[p].push_back(Phat(p, ql));
             c[np].push_back(0);
+            if (rs) c[np + 1].push_back(0);
             for (int i = 0; i < l; i++) {
                 const u64 qi = primes[i];
                 g.prime[1 + i] = i;
@@ -297,11 +305,12 @@ void Ctx::build_tc_groups(LevelConsts &lc, int l) {
                 for (int p = 0; p < np; p++) c[p].push_back(Phat(p, qi));
                 const u64 ph = h_mulmod(Pmod(qi), (ql >> 1) % qi, qi);
                 c[np].push_back(ph ? qi - ph : 0);
+                if (rs) c[np + 1].push_back(Pmod(qi));
             }
             g.nt = l + 1;
             add(g, c, tp);
         } else {
-            add(g, std::vector<std::vector<u64>>(np + 1), tp);  // empty placeholder (never launched)
+            add(g, std::vector<std::vector<u64>>(c.size()), tp);  // empty placeholder (never launched)
         }
     }
     // plain ModDown (rotations): sources y_p, targets q_0..q_l

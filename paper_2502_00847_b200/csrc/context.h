@@ -40,6 +40,7 @@ struct TcGroup {
     double qinv[TC_TMAX];    // RN(1 / q_t) for the FP64 quotient of the epilogue
     int planes;              // byte planes per target: 6 when every target prime is < 2^46, else 8
     int ncols;               // MMA N = TMEM columns used (multiple of 16, <= 256)
+    int rslot = -1;          // fused ModDown + rescale: source slot of r (added by a second MMA), -1 = none
 };
 struct TcArgs {
     const u64 *src;
