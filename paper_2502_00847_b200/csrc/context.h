@@ -205,6 +205,7 @@ double round_half_away(double x);
 CtView compact_view(const Ctx &c, u64 *data, int n, int level, double scale);
 void ev_ntt(Ctx &c, RowsArg d, int n_polys, LimbMap lm, bool inverse, const NttFusion &f = NttFusion());
 void ev_ntt_segs(Ctx &c, const std::vector<NttSeg> &segs, bool inverse);
+void ev_ntt_segs_pass1(Ctx &c, const std::vector<NttSeg> &segs);
 void ev_copy(Ctx &c, const CtView &a, const CtView &out);
 void ev_addsub(Ctx &c, const CtView &a, const CtView &b, const CtView &out, bool sub);
 void ev_mul_int(Ctx &c, const CtView &a, i128 C, const CtView &out);

@@ -71,6 +71,17 @@ void ev_ntt_segs(Ctx &c, const std::vector<NttSeg> &segs, bool inverse) {
     c.cnt.launches += 2;
 }
 
+// the first forward pass of the segments only (the fused ModUp pass 2 + key inner product completes them)
+void ev_ntt_segs_pass1(Ctx &c, const std::vector<NttSeg> &segs) {
+    NttSpans spans{&c};
+    const NttProfHook hook{&spans, ntt_mark};
+    if (c.prof.on) ntt_set_prof_hook(&hook);
+    ntt_segments_pass1(c.tab, c.logn, segs.data(), (int)segs.size(), c.st);
+    if (c.prof.on) ntt_set_prof_hook(nullptr);
+    for (auto &g : segs) c.cnt.ntt_limbs += (long long)g.n_polys * g.lm.nl;
+    c.cnt.launches += 1;
+}
+
 void ev_copy(Ctx &c, const CtView &a, const CtView &out) {
     k_copy_rows(c.logn, crows_of(a), rows_of(out), 2 * a.n, out.level + 1, c.st);
     c.cnt.launches++;
@@ -193,7 +204,7 @@ void ev_rescale_lin(Ctx &c, const CtView &x1, i128 C1, const CtView *x2, i128 C2
 // INTT's first pass multiplies a1 b1, the inner product forms d0, d1 (+ C x) and adds [P] d_b.
 // ModUp of d (or of the tensor's d2 = a1 b1): ext[c][j][e] in NTT form, exts = beta (nl + np) N per ct
 static void ks_modup(Ctx &c, const u64 *d, long d_stride, int n, int level, DevBuf &ext,
-                     const TensorSrc *ten = nullptr) {
+                     const TensorSrc *ten = nullptr, bool pass1_only = false) {
     const long N = c.N;
     const int nl = level + 1, np = c.np, ne = nl + np, bt = c.beta(level);
     const LevelConsts &lc = c.level(level);
@@ -247,8 +258,29 @@ static void ks_modup(Ctx &c, const u64 *d, long d_stride, int n, int level, DevB
                                   LimbMap{nl - i1, nl - i1, i1, 0}});
     }
     segs.push_back(NttSeg{RowsArg{ext.p + (long)nl * N, 2L * ne * N, (long)ne * N}, n * bt, LimbMap{np, 0, 0, c.nq}});
-    ev_ntt_segs(c, segs, false);
+    if (pass1_only) {
+        ev_ntt_segs_pass1(c, segs);
+    } else {
+        ev_ntt_segs(c, segs, false);
+    }
     c.cnt.launches += 1;
+}
+
+// Every row of Q_level u P on the exact-FP64 NTT (FpA, q < 2^46): the relinearisation's ModUp second forward pass
+// and key inner product run as one kernel (ntt_ks_inner).  SECPE_KS_FUSE=0 keeps the separate kernels.
+static bool ks_fuse_ok(const Ctx &c, int level) {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("SECPE_KS_FUSE");
+        on = e ? atoi(e) : 1;
+    }
+    if (!on || c.beta(level) > 4) return false;
+    const int nl = level + 1;
+    for (int i = 0; i < nl; i++)
+        if (i >= 64 || !((c.tab.fp_mask >> i) & 1)) return false;
+    for (int p = 0; p < c.np; p++)
+        if (c.nq + p >= 64 || !((c.tab.fp_mask >> (c.nq + p)) & 1)) return false;
+    return true;
 }
 
 // 3. inner product of the ModUp digits with the switching key (galois > 1: of sigma_g of the digits)
@@ -266,6 +298,16 @@ static void ks_inner(Ctx &c, const u64 *d, long d_stride, int n, int level, cons
 static void ks_modup_inner(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, DevBuf &acc,
                            const TensorSrc *ten = nullptr) {
     DevBuf ext;
+    if (ten && ks_fuse_ok(c, level)) {
+        ks_modup(c, d, d_stride, n, level, ext, ten, true);
+        const long N = c.N;
+        const int nl = level + 1, ne = nl + c.np, bt = c.beta(level);
+        acc = DevBuf((size_t)n * 2L * ne * N, c.st);
+        KsFuse f{ext.p, (long)bt * ne * N, key, acc.p, 2L * ne * N, n, nl, c.np, c.nq, c.alpha, bt, *ten, c.pmod.p};
+        ntt_ks_inner(c.tab, c.logn, f, c.st);
+        c.cnt.launches += 1;
+        return;
+    }
     ks_modup(c, d, d_stride, n, level, ext, ten);
     ks_inner(c, d, d_stride, n, level, key, ext, acc, ten);
 }

@@ -131,6 +131,24 @@ void k_ks_inner(const Tab &tab, int logn, const u64 *d, long d_ct_stride, const 
                 const u64 *key, int nq_total, int np, u64 *acc, long acc_ct_stride, int n_ct, int nl,
                 int alpha, cudaStream_t st, const TensorSrc *ten = nullptr, const u64 *pmod = nullptr,
                 u64 galois = 1);  // galois > 1: read sigma_g(X_j) (NTT-domain gather; hoisted rotation, R29)
+// Fused ModUp forward pass 2 + relinearise-and-rescale key inner product (every row of Q_l u P exact-FP64,
+// q < 2^46): ext[c][j][e] holds the ModUp digits after the FIRST forward pass (ntt_segments_pass1); for every
+// (ciphertext, row e, tile) the kernel runs the second pass of each digit j with e outside I_j and multiplies the
+// raw transform with key_j[b][e] on the fly, then adds the tensor terms of the Q rows (d2 = a1 b1 (+ a2_1 b2_1)
+// for the own digit, [P] d_b) exactly as k_ks_inner with ten -- the digits never return to HBM in NTT form.
+struct KsFuse {
+    const u64 *ext;
+    long exts;
+    const u64 *key;  // [beta][2][nq_total + np][N]
+    u64 *acc;        // [n_ct][2][nl + np][N]
+    long accs;
+    int n_ct, nl, np, nq_total, alpha, beta;
+    TensorSrc ten;
+    const u64 *pmod;  // [P]_{q_e} per Q row
+};
+void ntt_ks_inner(const Tab &tab, int logn, const KsFuse &f, cudaStream_t st);
+// ntt_segments' first forward pass only (the fused kernel above runs the second)
+void ntt_segments_pass1(const Tab &tab, int logn, const NttSeg *segs, int nseg, cudaStream_t st);
 // ModDown conversion (R11): T[c][b][i] = sum_{s < ns} y_s [B/s]_{q_i} mod q_i for i < nt, with
 // y_s = acc[c][b][row0 + s] (coefficient form, already times (B/s)^{-1}); hatpk[s * hstride + i]
 // split-30 packed

@@ -31,6 +31,14 @@
 #include <cstdlib>
 
 #include "ntt_core.cuh"
+#include "fpk.cuh"
+
+#ifndef NTT_KSI_MINB
+#define NTT_KSI_MINB 3  // resident CTAs per SM of the fused ModUp pass 2 + key inner product kernel
+#endif
+#ifndef NTT_KSI_PREFETCH
+#define NTT_KSI_PREFETCH 1  // per digit: L2 prefetch of its key tiles and the next digit's tile (all tiles at kernel start: evicted before use, slower)
+#endif
 
 namespace {
 
@@ -490,6 +498,142 @@ __global__ void __launch_bounds__(CT, MinB<A>::v) ntt_contig(PassArgs a) {
     locate(a, blockIdx.y, d, poly, limb, prime);
     const PrimeC P = prime_consts(a.tab, prime);
     contig_body<LOGN, INV, IO, A>(a, d, sm, poly, limb, prime, P);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Fused ModUp forward pass 2 + relinearise-and-rescale key inner product (R10/R11 key switching, every row
+// exact-FP64).  CTA = (row e, ciphertext c, tile of CG G words): for each digit j with e outside I_j, the tile of
+// ext[c][j][e] (after the first forward pass) runs stages S..LOGN-1 (the contiguous pass) and lands in shared
+// memory as raw transform doubles (|v| <= 13 q, as the FPE epilogues); each word is multiplied with the key words
+// key_j[0/1][e] (FpA exact products, |mm| <= 0.75 q).  The partial sums stay exact doubles and are parked in the
+// acc rows between digits (the same thread re-reads its own words: L2-resident); the Q rows then add the
+// tensor's terms (d2 = a1 b1 (+ a2_1 b2_1) with the own digit's key, [P] d0 / [P] d1) and every output is
+// canonicalised once.  At most beta + 1 <= 5 terms: |s| <= 3.75 q, an exact double.  The same canonical
+// residues as ks_inner_ten1_kernel (sums of exact products mod q), so the key-switch integers are unchanged.
+// Rows are ordered e-major (ciphertexts of one row adjacent) so a key tile is read from HBM once per batch.
+// ---------------------------------------------------------------------------------------------
+template <int LOGN>
+__global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab, KsFuse f) {
+    using CF = ContigCfg<LOGN>;
+    constexpr int S = CF::S, G = CF::G, TPG = CF::TPG, CG = CF::CG, PITCH = CF::PITCH;
+    constexpr long N = 1L << LOGN;
+    using R = Rnd<S, false>;
+    constexpr int LO0 = R::lo(0), LO1 = R::lo(1);
+    // two padded tiles: the next digit's tile is copied in (cp.async) while the current one is transformed
+    extern __shared__ __align__(16) u64 ksi_sm[];  // [CG * PITCH]
+    const int e = blockIdx.y / f.n_ct, c = blockIdx.y % f.n_ct;
+    const int ne = f.nl + f.np, nk = f.nq_total + f.np;
+    const bool qrow = e < f.nl;
+    const int pr = qrow ? e : f.nq_total + (e - f.nl);
+    const int jd = qrow ? e / f.alpha : -1;
+    const PrimeC P = prime_consts(tab, pr);
+    const double qd = P.qd, qinv = P.qinv;
+    const long boff = (long)blockIdx.x * CG * G;
+    const ulonglong2 *tw = tab.tw2 + pr * N;
+    const int gl = threadIdx.x / TPG, tau = threadIdx.x % TPG;
+    const int g = blockIdx.x * CG + gl;
+    ulonglong2 *acc0 = reinterpret_cast<ulonglong2 *>(f.acc + c * f.accs + (long)e * N + boff);
+    ulonglong2 *acc1 = reinterpret_cast<ulonglong2 *>(f.acc + c * f.accs + (long)(ne + e) * N + boff);
+    const u64 *keyrow = f.key + (long)pr * N + boff;  // key_j[b] row of this prime: + (2 j + b) nk N
+    auto fx = [](u64 x) { return fpt::d(x); };
+#if NTT_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+    const int ndig = qrow ? f.beta - 1 : f.beta;
+    auto next_digit = [&](int j) {
+        for (j = j + 1; j < f.beta; j++)
+            if (j != jd) return j;
+        return -1;
+    };
+    const long lo = (long)threadIdx.x * 16;  // this thread's 128-byte line of a tile (L2 prefetches)
+    u64 *const sm = ksi_sm, *const smg = sm + gl * PITCH;
+    int nd = 0;
+    for (int j = next_digit(-1); j >= 0; j = next_digit(j)) {
+        const bool fin = nd == ndig - 1 && !qrow;  // the last term of a special row: canonicalise
+#if NTT_KSI_PREFETCH
+        {
+            // this digit's key tiles and the next digit's transform tile into L2 while the rounds run
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(keyrow + (long)(2 * j) * nk * N + lo));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(keyrow + (long)(2 * j + 1) * nk * N + lo));
+            const int jn = next_digit(j);
+            if (jn >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(f.ext + c * f.exts + ((long)jn * ne + e) * N + boff + lo));
+        }
+#endif
+        const u64 *src = f.ext + c * f.exts + ((long)j * ne + e) * N + boff + gl * G;
+        u64 v[NV];
+#pragma unroll
+        for (int k = 0; k < NV; k++) v[k] = NTT_LD(src + held<LO0>(tau, k));  // first-pass representation
+        do_round<S, false, 0, true, LOGN, FpA>(v, tau, g, tw, P);
+#pragma unroll
+        for (int k = 0; k < NV; k++) smg[padr(held<LO0>(tau, k))] = v[k];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < NV; k++) v[k] = smg[padr(held<LO1>(tau, k))];
+        do_round<S, false, 1, true, LOGN, FpA>(v, tau, g, tw, P);
+        // no barrier: each thread rewrites exactly the words it read for round 1
+#pragma unroll
+        for (int k = 0; k < NV; k++) smg[padr(held<LO1>(tau, k))] = v[k];
+        __syncthreads();
+        const ulonglong2 *kb = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * j) * nk * N);
+        const ulonglong2 *ka = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * j + 1) * nk * N);
+#pragma unroll 4
+        for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
+            const int el = 2 * i, gg = el / G, r = el % G;
+            const double x0 = FpA::D(sm[gg * PITCH + padr(r)]), x1 = FpA::D(sm[gg * PITCH + padr(r + 1)]);
+            const ulonglong2 KB = __ldg(kb + i), KA = __ldg(ka + i);
+            const double B0 = fx(KB.x), B1 = fx(KB.y), A0 = fx(KA.x), A1 = fx(KA.y);
+            double s00 = fpt::mm(x0, B0, __dmul_rn(B0, qinv), qd), s01 = fpt::mm(x1, B1, __dmul_rn(B1, qinv), qd);
+            double s10 = fpt::mm(x0, A0, __dmul_rn(A0, qinv), qd), s11 = fpt::mm(x1, A1, __dmul_rn(A1, qinv), qd);
+            if (nd > 0) {
+                const ulonglong2 p0 = acc0[i], p1 = acc1[i];
+                s00 = __dadd_rn(s00, FpA::D(p0.x));
+                s01 = __dadd_rn(s01, FpA::D(p0.y));
+                s10 = __dadd_rn(s10, FpA::D(p1.x));
+                s11 = __dadd_rn(s11, FpA::D(p1.y));
+            }
+            if (fin) {
+                acc0[i] = make_ulonglong2(fp_canon4(s00, P.q, qd, qinv), fp_canon4(s01, P.q, qd, qinv));
+                acc1[i] = make_ulonglong2(fp_canon4(s10, P.q, qd, qinv), fp_canon4(s11, P.q, qd, qinv));
+            } else {
+                acc0[i] = make_ulonglong2(FpA::B(s00), FpA::B(s01));
+                acc1[i] = make_ulonglong2(FpA::B(s10), FpA::B(s11));
+            }
+        }
+        __syncthreads();  // the next digit's round 0 rewrites the shared tile
+        nd++;
+    }
+    if (!qrow) return;
+    // Q rows: the tensor (formed on the fly, tensor1_fp_raw) -- d2 with the own digit's key, [P] d0 / [P] d1
+    const TensorSrc &T = f.ten;
+    const bool lin = T.x.p != nullptr, lin2 = T.x2.p != nullptr, p2 = T.a2.p != nullptr;
+    const u64 cc = lin ? T.C.c[e] : 0, c2 = lin2 ? T.C2.c[e] : 0;
+    const double PM = fx(f.pmod[e]), PMq = __dmul_rn(PM, qinv);
+    const ulonglong2 *kb = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * jd) * nk * N);
+    const ulonglong2 *ka = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * jd + 1) * nk * N);
+    const long o = (long)e * N + boff;
+    auto row1 = [&](const CRows &r, int poly) { return r.p + c * r.cs + poly * r.ps + o; };
+    const u64 *a0p = row1(T.a, 0), *a1p = row1(T.a, 1), *b0p = row1(T.b, 0), *b1p = row1(T.b, 1);
+    const u64 *kb1 = reinterpret_cast<const u64 *>(kb), *ka1 = reinterpret_cast<const u64 *>(ka);
+    u64 *o0p = reinterpret_cast<u64 *>(acc0), *o1p = reinterpret_cast<u64 *>(acc1);
+#pragma unroll 2
+    for (int i = threadIdx.x; i < CG * G; i += CT) {
+        const u64 x0 = lin ? row1(T.x, 0)[i] : 0, x1 = lin ? row1(T.x, 1)[i] : 0;
+        const u64 y0 = lin2 ? row1(T.x2, 0)[i] : 0, y1 = lin2 ? row1(T.x2, 1)[i] : 0;
+        const u64 u0 = p2 ? row1(T.a2, 0)[i] : 0, u1 = p2 ? row1(T.a2, 1)[i] : 0;
+        const u64 w0 = p2 ? row1(T.b2, 0)[i] : 0, w1 = p2 ? row1(T.b2, 1)[i] : 0;
+        double e0, e1, e2;
+        tensor1_fp_raw(a0p[i], a1p[i], b0p[i], b1p[i], lin, x0, x1, cc, lin2, y0, y1, c2, qd, qinv, e0, e1, e2, p2, u0,
+                       u1, w0, w1);
+        const double KBd = fx(__ldg(kb1 + i)), KAd = fx(__ldg(ka1 + i));
+        double s0 = __dadd_rn(fpt::mm(e2, KBd, __dmul_rn(KBd, qinv), qd), fpt::mm(e0, PM, PMq, qd));
+        double s1 = __dadd_rn(fpt::mm(e2, KAd, __dmul_rn(KAd, qinv), qd), fpt::mm(e1, PM, PMq, qd));
+        if (nd > 0) {
+            s0 = __dadd_rn(s0, FpA::D(o0p[i]));
+            s1 = __dadd_rn(s1, FpA::D(o1p[i]));
+        }
+        o0p[i] = fp_canon4(s0, P.q, qd, qinv);
+        o1p[i] = fp_canon4(s1, P.q, qd, qinv);
+    }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1048,7 +1192,7 @@ namespace {
 // several independent plain forward transforms in as few launches as possible (MAXSEG row ranges per
 // launch, one launch pair per prime class)
 template <int LOGN>
-void run_segs(const Tab &tab, const NttSeg *segs, int nseg, bool inverse, cudaStream_t st) {
+void run_segs(const Tab &tab, const NttSeg *segs, int nseg, bool inverse, cudaStream_t st, bool pass1_only = false) {
     struct Run {
         Seg g;
         int cls;
@@ -1078,7 +1222,7 @@ void run_segs(const Tab &tab, const NttSeg *segs, int nseg, bool inverse, cudaSt
             if (!a.nseg) return;
             a.nsub = rows;  // grid rows (n_polys = 1 below)
             const double bytes = 16.0 * rows * (double)N / 2;
-            for (int pass = 0; pass < 2; pass++) {
+            for (int pass = 0; pass < (pass1_only ? 1 : 2); pass++) {
                 if (g_hook) g_hook->mark(g_hook->ctx, 0, fp, bytes, rows / 2.0);
                 const bool first = pass == 0;
                 with_policy(cls, [&](auto pol) {
@@ -1122,6 +1266,58 @@ void ntt_segments(const Tab &tab, int logn, const NttSeg *segs, int nseg, bool i
         case 16: run_segs<16>(tab, segs, nseg, inverse, st); break;
         default: throw SecpeError{-1, "NTT: log N must be in [12, 16]"};
     }
+}
+
+void ntt_segments_pass1(const Tab &tab, int logn, const NttSeg *segs, int nseg, cudaStream_t st) {
+    switch (logn) {
+        case 12: run_segs<12>(tab, segs, nseg, false, st, true); break;
+        case 13: run_segs<13>(tab, segs, nseg, false, st, true); break;
+        case 14: run_segs<14>(tab, segs, nseg, false, st, true); break;
+        case 15: run_segs<15>(tab, segs, nseg, false, st, true); break;
+        case 16: run_segs<16>(tab, segs, nseg, false, st, true); break;
+        default: throw SecpeError{-1, "NTT: log N must be in [12, 16]"};
+    }
+}
+
+namespace {
+template <int LOGN>
+void launch_ks_inner(const Tab &tab, const KsFuse &f, cudaStream_t st) {
+    using CF = ContigCfg<LOGN>;
+    const int ne = f.nl + f.np;
+    const dim3 grid((unsigned)((1L << LOGN) / (CF::CG * CF::G)), (unsigned)(ne * f.n_ct));
+    auto kern = ntt_ks_inner_kernel<LOGN>;
+    const int smem = CF::CG * CF::PITCH * 8;
+    static bool done = false;
+    if (!done) {
+        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        max_smem_carveout(kern);
+        done = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(CT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = NTT_PDL;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, tab, f));
+}
+}  // namespace
+
+void ntt_ks_inner(const Tab &tab, int logn, const KsFuse &f, cudaStream_t st) {
+    if (f.n_ct <= 0) return;
+    switch (logn) {
+        case 12: launch_ks_inner<12>(tab, f, st); break;
+        case 13: launch_ks_inner<13>(tab, f, st); break;
+        case 14: launch_ks_inner<14>(tab, f, st); break;
+        case 15: launch_ks_inner<15>(tab, f, st); break;
+        case 16: launch_ks_inner<16>(tab, f, st); break;
+        default: throw SecpeError{-1, "NTT: log N must be in [12, 16]"};
+    }
+    LAUNCH_CHECK();
 }
 
 void ntt_forward(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
