@@ -443,7 +443,10 @@ int secpe_oplog_clear(secpe_ctx *ctx);
  * batch; rescale: 2(l+1) + 2l limbs per ciphertext), out[3k+2] units (limb transforms per launch,
  * summed / ciphertexts).  With n_out >= 27 also the argmax circuit stages as kinds 4..8 (H1
  * aggregation, H2 mask, H3 duplication, H4 QuickMax incl. its Sign, H6 final Sign + 1; ms in
- * out[3k], ciphertexts in out[3k+2]).  Returns SECPE_EINVAL when n_out < 12. */
+ * out[3k], ciphertexts in out[3k+2]).  With n_out >= 30 also kind 9: the operand bytes the fused
+ * prologues / epilogues of the FP64-row NTT launches read on top of their transforms (tensor factors,
+ * rescale and ModDown operands, addends; out[28]), timed over the same launches (out[27]).
+ * Returns SECPE_EINVAL when n_out < 12. */
 int secpe_profile_begin(secpe_ctx *ctx);
 int secpe_profile_end(secpe_ctx *ctx, double *out, int32_t n_out);
 /* Development switch of the N = 2^16 exact-FP64 NTT implementation (process-wide; SECPE_NTT_FUSED sets the

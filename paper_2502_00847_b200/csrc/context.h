@@ -81,7 +81,8 @@ struct Prof {
     struct Span {
         size_t a, b;
         int kind;      // 0 NTT launch on FP64 rows, 1 key switch, 2 rescale, 3 NTT launch on integer rows,
-                       // 4..8 argmax stages H1, H2, H3, H4, H6
+                       // 4..8 argmax stages H1, H2, H3, H4, H6, 9 fused operand bytes of kind-0 launches (same
+                       // events as their kind-0 span)
         double bytes;  // algorithmic bytes of the span
         double units;
     };

@@ -32,12 +32,21 @@ struct NttSpans {
     Ctx *c;
     size_t open = 0;
 };
-void ntt_mark(void *p, int phase, bool fp, double bytes, double limbs) {
+void ntt_mark(void *p, int phase, bool fp, double bytes, double limbs, double opbytes) {
     NttSpans &s = *static_cast<NttSpans *>(p);
-    if (phase == 0)
+    if (phase == 0) {
         s.open = s.c->prof_begin(fp ? 0 : 3);
-    else
+    } else {
         s.c->prof_end(s.open, fp ? 0 : 3, bytes, limbs);
+        // the fused operands as a second span over the same two events (kind 9: FP64 rows)
+        if (fp && opbytes > 0 && s.c->prof.on) {
+            Prof::Span sp = s.c->prof.spans.back();
+            sp.kind = 9;
+            sp.bytes = opbytes;
+            sp.units = 0;
+            s.c->prof.spans.push_back(sp);
+        }
+    }
 }
 }  // namespace
 
@@ -304,7 +313,11 @@ static void ks_modup_inner(Ctx &c, const u64 *d, long d_stride, int n, int level
         const int nl = level + 1, ne = nl + c.np, bt = c.beta(level);
         acc = DevBuf((size_t)n * 2L * ne * N, c.st);
         KsFuse f{ext.p, (long)bt * ne * N, key, acc.p, 2L * ne * N, n, nl, c.np, c.nq, c.alpha, bt, *ten, c.pmod.p};
+        NttSpans spans{&c};
+        const NttProfHook hook{&spans, ntt_mark};
+        if (c.prof.on) ntt_set_prof_hook(&hook);
         ntt_ks_inner(c.tab, c.logn, f, c.st);
+        if (c.prof.on) ntt_set_prof_hook(nullptr);
         c.cnt.launches += 1;
         return;
     }

@@ -60,7 +60,9 @@ void ntt_forward(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm
 // with the row class of the launch (FP64 or integer rows) and its algorithmic bytes; thread-local
 struct NttProfHook {
     void *ctx;
-    void (*mark)(void *ctx, int phase, bool fp, double bytes, double limbs);
+    // bytes: the transform's 16 N per limb transform (split over its passes); opbytes: the operand limbs the fused
+    // prologue / epilogue of this launch reads on top (tensor factors, rescale / ModDown operands, addends)
+    void (*mark)(void *ctx, int phase, bool fp, double bytes, double limbs, double opbytes);
 };
 void ntt_set_prof_hook(const NttProfHook *h);
 // several independent plain in-place transforms (each: n_polys polynomials of lm.nl limbs in d) batched

@@ -970,8 +970,21 @@ thread_local const NttProfHook *g_hook = nullptr;
 // calls launch(a, cls) once per run of same-class limbs; `passes` = launches per limb transform that
 // this call makes (2: one of the two passes, 1: single-pass cluster kernel) for the profiling hook (which
 // sees the FP64 classes as one)
+// operand limbs the fused modes of a launch read per limb on top of the transform's own input (prologue: the
+// inverse's first pass; epilogue: the forward's last pass)
+inline double prologue_limbs(const NttFusion &f) {
+    if (f.in_mode == IN_MUL) return 1;
+    if (f.in_mode == IN_MUL2) return 3;
+    if (f.in_mode == IN_LIN) return f.lin == 2 ? 1 : 0;
+    return 0;
+}
+inline double epilogue_limbs(const NttFusion &f) {
+    if (f.out_mode == OUT_RESCALE) return 1 + (f.lin == 2 ? 1 : 0);
+    if (f.out_mode == OUT_MODDOWN) return 1 + 0.5 * (f.e2.p ? f.e2_polys : 0) + (f.e3.p ? 1 : 0);
+    return 0;
+}
 template <class F>
-void for_runs(const PassArgs &a0, int n_polys, int passes, long N, F launch) {
+void for_runs(const PassArgs &a0, int n_polys, int passes, long N, F launch, double op_limbs = 0) {
     int l = 0;
     while (l < a0.lm.nl) {
         const int cls = limb_cls(a0, l);
@@ -984,9 +997,10 @@ void for_runs(const PassArgs &a0, int n_polys, int passes, long N, F launch) {
         // per launch: its share of the limb transforms (a two-pass transform counts half in each pass)
         const double limbs = (double)n_polys * a.nsub / passes;
         const double bytes = 16.0 * limbs * (double)N;  // N words read + written once per transform
-        if (g_hook) g_hook->mark(g_hook->ctx, 0, fp, bytes, limbs);
+        const double opb = 8.0 * op_limbs * (double)n_polys * a.nsub * (double)N;
+        if (g_hook) g_hook->mark(g_hook->ctx, 0, fp, bytes, limbs, opb);
         launch(a, cls);
-        if (g_hook) g_hook->mark(g_hook->ctx, 1, fp, bytes, limbs);
+        if (g_hook) g_hook->mark(g_hook->ctx, 1, fp, bytes, limbs, opb);
         l = e;
     }
 }
@@ -998,9 +1012,12 @@ void launch_strided(const PassArgs &a0, int n_polys, cudaStream_t st) {
 }
 template <int LOGN, bool INV, int IO>
 void launch_contig(const PassArgs &a0, int n_polys, cudaStream_t st) {
-    for_runs(a0, n_polys, 2, 1L << LOGN, [&](const PassArgs &a, int cls) {
-        with_policy(cls, [&](auto pol) { launch_contig_a<LOGN, INV, IO, decltype(pol)>(a, n_polys, st); });
-    });
+    for_runs(
+        a0, n_polys, 2, 1L << LOGN,
+        [&](const PassArgs &a, int cls) {
+            with_policy(cls, [&](auto pol) { launch_contig_a<LOGN, INV, IO, decltype(pol)>(a, n_polys, st); });
+        },
+        INV ? prologue_limbs(a0.f) : epilogue_limbs(a0.f));
 }
 
 template <int LOGN>
@@ -1109,11 +1126,14 @@ void run_chunk(const PassArgs &a, int rows, bool inverse, cudaStream_t st) {
     if constexpr (LOGN == 16) {
         if (cluster_mode(a) == 0 && ntt_fused_enabled()) {
             // one persistent TMA-pipelined launch per run of exact-FP64 rows (ntt_fused.cu)
-            for_runs(a, rows, 1, 1L << LOGN, [&](const PassArgs &r, int cls) {
-                if (ntt_fused_run(r.tab, LOGN, r.d, rows, r.lm, r.limb0, r.nsub, cls, inverse, r.f, st))
-                    return;
-                with_policy(cls, [&](auto pol) { two_pass_run_a<LOGN, decltype(pol)>(r, rows, inverse, st); });
-            });
+            for_runs(
+                a, rows, 1, 1L << LOGN,
+                [&](const PassArgs &r, int cls) {
+                    if (ntt_fused_run(r.tab, LOGN, r.d, rows, r.lm, r.limb0, r.nsub, cls, inverse, r.f, st))
+                        return;
+                    with_policy(cls, [&](auto pol) { two_pass_run_a<LOGN, decltype(pol)>(r, rows, inverse, st); });
+                },
+                inverse ? prologue_limbs(f) : epilogue_limbs(f));
             return;
         }
         if (cluster_mode(a) > 0 && !f.lin) {  // (fused constant products: two-pass kernels only)
@@ -1223,7 +1243,7 @@ void run_segs(const Tab &tab, const NttSeg *segs, int nseg, bool inverse, cudaSt
             a.nsub = rows;  // grid rows (n_polys = 1 below)
             const double bytes = 16.0 * rows * (double)N / 2;
             for (int pass = 0; pass < (pass1_only ? 1 : 2); pass++) {
-                if (g_hook) g_hook->mark(g_hook->ctx, 0, fp, bytes, rows / 2.0);
+                if (g_hook) g_hook->mark(g_hook->ctx, 0, fp, bytes, rows / 2.0, 0.0);
                 const bool first = pass == 0;
                 with_policy(cls, [&](auto pol) {
                     using A = decltype(pol);
@@ -1240,7 +1260,7 @@ void run_segs(const Tab &tab, const NttSeg *segs, int nseg, bool inverse, cudaSt
                     }
                 });
                 LAUNCH_CHECK();
-                if (g_hook) g_hook->mark(g_hook->ctx, 1, fp, bytes, rows / 2.0);
+                if (g_hook) g_hook->mark(g_hook->ctx, 1, fp, bytes, rows / 2.0, 0.0);
             }
             a.nseg = 0;
             rows = 0;
@@ -1309,6 +1329,17 @@ void launch_ks_inner(const Tab &tab, const KsFuse &f, cudaStream_t st) {
 
 void ntt_ks_inner(const Tab &tab, int logn, const KsFuse &f, cudaStream_t st) {
     if (f.n_ct <= 0) return;
+    // profiling: the second half of every digit row's transform (8 N per limb) plus the operands the fused inner
+    // product reads and writes (key once per batch, tensor inputs of the Q rows, the acc rows)
+    const double N = (double)(1L << logn);
+    const int ne = f.nl + f.np;
+    double drows = 0;
+    for (int e = 0; e < ne; e++) drows += e < f.nl ? f.beta - 1 : f.beta;
+    drows *= f.n_ct;
+    const TensorSrc &T = f.ten;
+    const int tin = 4 + (T.x.p ? 2 : 0) + (T.x2.p ? 2 : 0) + (T.a2.p ? 4 : 0);
+    const double opb = 8.0 * N * (2.0 * f.beta * ne + (double)f.n_ct * (tin * f.nl + 2.0 * ne));
+    if (g_hook) g_hook->mark(g_hook->ctx, 0, true, 8.0 * N * drows, drows / 2, opb);
     switch (logn) {
         case 12: launch_ks_inner<12>(tab, f, st); break;
         case 13: launch_ks_inner<13>(tab, f, st); break;
@@ -1318,6 +1349,7 @@ void ntt_ks_inner(const Tab &tab, int logn, const KsFuse &f, cudaStream_t st) {
         default: throw SecpeError{-1, "NTT: log N must be in [12, 16]"};
     }
     LAUNCH_CHECK();
+    if (g_hook) g_hook->mark(g_hook->ctx, 1, true, 8.0 * N * drows, drows / 2, opb);
 }
 
 void ntt_forward(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,

@@ -774,11 +774,12 @@ class Context:
         _chk(lib().secpe_profile_begin(self.h))
 
     def profile_end(self):
-        o = np.zeros(27, dtype=np.float64)
-        _chk(lib().secpe_profile_end(self.h, o.ctypes.data_as(f64p), 27))
+        o = np.zeros(30, dtype=np.float64)
+        _chk(lib().secpe_profile_end(self.h, o.ctypes.data_as(f64p), 30))
         r = {}
         for k, name in enumerate(("ntt_fp", "keyswitch", "rescale", "ntt_int", "stage_H1_aggregate", "stage_H2_mask",
-                                  "stage_H3_duplicate", "stage_H4_quickmax", "stage_H6_final_sign")):
+                                  "stage_H3_duplicate", "stage_H4_quickmax", "stage_H6_final_sign",
+                                  "ntt_fp_operands")):
             r[name] = dict(ms=float(o[3 * k]), bytes=float(o[3 * k + 1]), units=float(o[3 * k + 2]))
         r["ntt"] = {f: r["ntt_fp"][f] + r["ntt_int"][f] for f in ("ms", "bytes", "units")}
         return r

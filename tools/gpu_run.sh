@@ -1,8 +1,5 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python -m pytest tests -q -m gpu -x -k "ks_config or small_ring or config5_full" > gpurun_out/t8.log 2>&1; echo rc=$? >> gpurun_out/t8.log
-for i in 1 2 3; do
-for cfg in "1 libsecpe.so" "1 libsecpe_ksinp.so" "0 libsecpe.so"; do set -- $cfg
-ms=$(SECPE_LIB=paper_2502_00847_b200/$2 SECPE_KS_FUSE=$1 SECPE_BATCH=16 timeout 300 python tools/microbench.py argmax --reps 6 2>/dev/null | grep ms_per_batch | tr -dc '0-9.')
-echo "fuse=$1 $2 $ms" >> gpurun_out/ab8.log
+for i in 1 2; do for lib in libsecpe.so libsecpe_nors.so libsecpe_head.so; do
+r=$(SECPE_LIB=paper_2502_00847_b200/$lib timeout 300 python tools/argmax49_probe.py 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step'],2))")
+echo "49bit $lib $r" >> gpurun_out/ab10.log
 done; done
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:ntt_ks_inner -s 20 -c 1 python tools/relin_bench.py > gpurun_out/ncu_ksi8.log 2>&1
