@@ -36,6 +36,10 @@
 #ifndef NTT_KSI_MINB
 #define NTT_KSI_MINB 3  // resident CTAs per SM of the fused ModUp pass 2 + key inner product kernel
 #endif
+#ifndef KSI_CPB
+#define KSI_CPB 1  // ciphertexts per CTA of the fused kernel (2: one key load serves two tiles -- measured slower: partial sums
+                   // spill from L2 to DRAM, 71.8 vs 68.0 ms per argmax step)
+#endif
 #ifndef NTT_KSI_PREFETCH
 #define NTT_KSI_PREFETCH 1  // per digit: L2 prefetch of its key tiles and the next digit's tile (all tiles at kernel start: evicted before use, slower)
 #endif
@@ -519,9 +523,11 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
     constexpr long N = 1L << LOGN;
     using R = Rnd<S, false>;
     constexpr int LO0 = R::lo(0), LO1 = R::lo(1);
-    // two padded tiles: the next digit's tile is copied in (cp.async) while the current one is transformed
-    extern __shared__ __align__(16) u64 ksi_sm[];  // [CG * PITCH]
-    const int e = blockIdx.y / f.n_ct, c = blockIdx.y % f.n_ct;
+    // KSI_CPB ciphertexts per CTA (one padded tile each): every key word loaded serves all of them
+    extern __shared__ __align__(16) u64 ksi_sm[];  // [KSI_CPB][CG * PITCH]
+    const int ncg = (f.n_ct + KSI_CPB - 1) / KSI_CPB;
+    const int e = blockIdx.y / ncg, c0 = (blockIdx.y % ncg) * KSI_CPB;
+    const int nc = min(KSI_CPB, f.n_ct - c0);
     const int ne = f.nl + f.np, nk = f.nq_total + f.np;
     const bool qrow = e < f.nl;
     const int pr = qrow ? e : f.nq_total + (e - f.nl);
@@ -532,8 +538,9 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
     const ulonglong2 *tw = tab.tw2 + pr * N;
     const int gl = threadIdx.x / TPG, tau = threadIdx.x % TPG;
     const int g = blockIdx.x * CG + gl;
-    ulonglong2 *acc0 = reinterpret_cast<ulonglong2 *>(f.acc + c * f.accs + (long)e * N + boff);
-    ulonglong2 *acc1 = reinterpret_cast<ulonglong2 *>(f.acc + c * f.accs + (long)(ne + e) * N + boff);
+    // acc rows of ciphertext c0 + u: b = 0 at accb(u), b = 1 at accb(u) + ne N
+    auto accb = [&](int u) { return f.acc + (c0 + u) * f.accs + (long)e * N + boff; };
+    const long a1off = (long)ne * N;
     const u64 *keyrow = f.key + (long)pr * N + boff;  // key_j[b] row of this prime: + (2 j + b) nk N
     auto fx = [](u64 x) { return fpt::d(x); };
 #if NTT_PDL
@@ -546,60 +553,71 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
         return -1;
     };
     const long lo = (long)threadIdx.x * 16;  // this thread's 128-byte line of a tile (L2 prefetches)
-    u64 *const sm = ksi_sm, *const smg = sm + gl * PITCH;
     int nd = 0;
     for (int j = next_digit(-1); j >= 0; j = next_digit(j)) {
         const bool fin = nd == ndig - 1 && !qrow;  // the last term of a special row: canonicalise
 #if NTT_KSI_PREFETCH
-        {
-            // this digit's key tiles and the next digit's transform tile into L2 while the rounds run
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(keyrow + (long)(2 * j) * nk * N + lo));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(keyrow + (long)(2 * j + 1) * nk * N + lo));
-            const int jn = next_digit(j);
-            if (jn >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(f.ext + c * f.exts + ((long)jn * ne + e) * N + boff + lo));
-        }
+        // this digit's key tiles into L2 while the rounds run
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(keyrow + (long)(2 * j) * nk * N + lo));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(keyrow + (long)(2 * j + 1) * nk * N + lo));
 #endif
-        const u64 *src = f.ext + c * f.exts + ((long)j * ne + e) * N + boff + gl * G;
-        u64 v[NV];
+#pragma unroll 1
+        for (int u = 0; u < nc; u++) {
+            u64 *const smg = ksi_sm + u * CG * PITCH + gl * PITCH;
+            const u64 *src = f.ext + (c0 + u) * f.exts + ((long)j * ne + e) * N + boff + gl * G;
+            // opaque copy of the twiddle pointer: the twiddle loads stay inside the loop (hoisting them out of it
+            // keeps 30 twiddle pairs live across the rounds and spills)
+            const ulonglong2 *twu;
+            asm volatile("mov.b64 %0, %1;" : "=l"(twu) : "l"(tw));
+            u64 v[NV];
 #pragma unroll
-        for (int k = 0; k < NV; k++) v[k] = NTT_LD(src + held<LO0>(tau, k));  // first-pass representation
-        do_round<S, false, 0, true, LOGN, FpA>(v, tau, g, tw, P);
+            for (int k = 0; k < NV; k++) v[k] = NTT_LD(src + held<LO0>(tau, k));  // first-pass representation
+            do_round<S, false, 0, true, LOGN, FpA>(v, tau, g, twu, P);
 #pragma unroll
-        for (int k = 0; k < NV; k++) smg[padr(held<LO0>(tau, k))] = v[k];
-        __syncthreads();
+            for (int k = 0; k < NV; k++) smg[padr(held<LO0>(tau, k))] = v[k];
+            __syncthreads();
 #pragma unroll
-        for (int k = 0; k < NV; k++) v[k] = smg[padr(held<LO1>(tau, k))];
-        do_round<S, false, 1, true, LOGN, FpA>(v, tau, g, tw, P);
-        // no barrier: each thread rewrites exactly the words it read for round 1
+            for (int k = 0; k < NV; k++) v[k] = smg[padr(held<LO1>(tau, k))];
+            do_round<S, false, 1, true, LOGN, FpA>(v, tau, g, twu, P);
+            // no barrier: each thread rewrites exactly the words it read for round 1
 #pragma unroll
-        for (int k = 0; k < NV; k++) smg[padr(held<LO1>(tau, k))] = v[k];
+            for (int k = 0; k < NV; k++) smg[padr(held<LO1>(tau, k))] = v[k];
+        }
         __syncthreads();
         const ulonglong2 *kb = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * j) * nk * N);
         const ulonglong2 *ka = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * j + 1) * nk * N);
-#pragma unroll 4
+#pragma unroll 1
         for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
             const int el = 2 * i, gg = el / G, r = el % G;
-            const double x0 = FpA::D(sm[gg * PITCH + padr(r)]), x1 = FpA::D(sm[gg * PITCH + padr(r + 1)]);
             const ulonglong2 KB = __ldg(kb + i), KA = __ldg(ka + i);
             const double B0 = fx(KB.x), B1 = fx(KB.y), A0 = fx(KA.x), A1 = fx(KA.y);
-            double s00 = fpt::mm(x0, B0, __dmul_rn(B0, qinv), qd), s01 = fpt::mm(x1, B1, __dmul_rn(B1, qinv), qd);
-            double s10 = fpt::mm(x0, A0, __dmul_rn(A0, qinv), qd), s11 = fpt::mm(x1, A1, __dmul_rn(A1, qinv), qd);
-            if (nd > 0) {
-                const ulonglong2 p0 = acc0[i], p1 = acc1[i];
-                s00 = __dadd_rn(s00, FpA::D(p0.x));
-                s01 = __dadd_rn(s01, FpA::D(p0.y));
-                s10 = __dadd_rn(s10, FpA::D(p1.x));
-                s11 = __dadd_rn(s11, FpA::D(p1.y));
-            }
-            if (fin) {
-                acc0[i] = make_ulonglong2(fp_canon4(s00, P.q, qd, qinv), fp_canon4(s01, P.q, qd, qinv));
-                acc1[i] = make_ulonglong2(fp_canon4(s10, P.q, qd, qinv), fp_canon4(s11, P.q, qd, qinv));
-            } else {
-                acc0[i] = make_ulonglong2(FpA::B(s00), FpA::B(s01));
-                acc1[i] = make_ulonglong2(FpA::B(s10), FpA::B(s11));
+            const double B0q = __dmul_rn(B0, qinv), B1q = __dmul_rn(B1, qinv), A0q = __dmul_rn(A0, qinv),
+                         A1q = __dmul_rn(A1, qinv);
+#pragma unroll
+            for (int u = 0; u < KSI_CPB; u++) {
+                if (u >= nc) break;
+                const u64 *sm = ksi_sm + u * CG * PITCH;
+                const double x0 = FpA::D(sm[gg * PITCH + padr(r)]), x1 = FpA::D(sm[gg * PITCH + padr(r + 1)]);
+                double s00 = fpt::mm(x0, B0, B0q, qd), s01 = fpt::mm(x1, B1, B1q, qd);
+                double s10 = fpt::mm(x0, A0, A0q, qd), s11 = fpt::mm(x1, A1, A1q, qd);
+                ulonglong2 *acc0 = reinterpret_cast<ulonglong2 *>(accb(u)), *acc1 = reinterpret_cast<ulonglong2 *>(accb(u) + a1off);
+                if (nd > 0) {
+                    const ulonglong2 p0 = acc0[i], p1 = acc1[i];
+                    s00 = __dadd_rn(s00, FpA::D(p0.x));
+                    s01 = __dadd_rn(s01, FpA::D(p0.y));
+                    s10 = __dadd_rn(s10, FpA::D(p1.x));
+                    s11 = __dadd_rn(s11, FpA::D(p1.y));
+                }
+                if (fin) {
+                    acc0[i] = make_ulonglong2(fp_canon4(s00, P.q, qd, qinv), fp_canon4(s01, P.q, qd, qinv));
+                    acc1[i] = make_ulonglong2(fp_canon4(s10, P.q, qd, qinv), fp_canon4(s11, P.q, qd, qinv));
+                } else {
+                    acc0[i] = make_ulonglong2(FpA::B(s00), FpA::B(s01));
+                    acc1[i] = make_ulonglong2(FpA::B(s10), FpA::B(s11));
+                }
             }
         }
-        __syncthreads();  // the next digit's round 0 rewrites the shared tile
+        __syncthreads();  // the next digit's round 0 rewrites the shared tiles
         nd++;
     }
     if (!qrow) return;
@@ -608,31 +626,33 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
     const bool lin = T.x.p != nullptr, lin2 = T.x2.p != nullptr, p2 = T.a2.p != nullptr;
     const u64 cc = lin ? T.C.c[e] : 0, c2 = lin2 ? T.C2.c[e] : 0;
     const double PM = fx(f.pmod[e]), PMq = __dmul_rn(PM, qinv);
-    const ulonglong2 *kb = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * jd) * nk * N);
-    const ulonglong2 *ka = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * jd + 1) * nk * N);
+    const u64 *kb1 = keyrow + (long)(2 * jd) * nk * N, *ka1 = keyrow + (long)(2 * jd + 1) * nk * N;
     const long o = (long)e * N + boff;
-    auto row1 = [&](const CRows &r, int poly) { return r.p + c * r.cs + poly * r.ps + o; };
-    const u64 *a0p = row1(T.a, 0), *a1p = row1(T.a, 1), *b0p = row1(T.b, 0), *b1p = row1(T.b, 1);
-    const u64 *kb1 = reinterpret_cast<const u64 *>(kb), *ka1 = reinterpret_cast<const u64 *>(ka);
-    u64 *o0p = reinterpret_cast<u64 *>(acc0), *o1p = reinterpret_cast<u64 *>(acc1);
-#pragma unroll 2
+#pragma unroll 1
     for (int i = threadIdx.x; i < CG * G; i += CT) {
-        const u64 x0 = lin ? row1(T.x, 0)[i] : 0, x1 = lin ? row1(T.x, 1)[i] : 0;
-        const u64 y0 = lin2 ? row1(T.x2, 0)[i] : 0, y1 = lin2 ? row1(T.x2, 1)[i] : 0;
-        const u64 u0 = p2 ? row1(T.a2, 0)[i] : 0, u1 = p2 ? row1(T.a2, 1)[i] : 0;
-        const u64 w0 = p2 ? row1(T.b2, 0)[i] : 0, w1 = p2 ? row1(T.b2, 1)[i] : 0;
-        double e0, e1, e2;
-        tensor1_fp_raw(a0p[i], a1p[i], b0p[i], b1p[i], lin, x0, x1, cc, lin2, y0, y1, c2, qd, qinv, e0, e1, e2, p2, u0,
-                       u1, w0, w1);
         const double KBd = fx(__ldg(kb1 + i)), KAd = fx(__ldg(ka1 + i));
-        double s0 = __dadd_rn(fpt::mm(e2, KBd, __dmul_rn(KBd, qinv), qd), fpt::mm(e0, PM, PMq, qd));
-        double s1 = __dadd_rn(fpt::mm(e2, KAd, __dmul_rn(KAd, qinv), qd), fpt::mm(e1, PM, PMq, qd));
-        if (nd > 0) {
-            s0 = __dadd_rn(s0, FpA::D(o0p[i]));
-            s1 = __dadd_rn(s1, FpA::D(o1p[i]));
+        const double KBq = __dmul_rn(KBd, qinv), KAq = __dmul_rn(KAd, qinv);
+#pragma unroll 1
+        for (int u = 0; u < nc; u++) {
+            const int c = c0 + u;
+            auto at = [&](const CRows &rr, int poly) { return rr.p[c * rr.cs + poly * rr.ps + o + i]; };
+            const u64 x0 = lin ? at(T.x, 0) : 0, x1 = lin ? at(T.x, 1) : 0;
+            const u64 y0 = lin2 ? at(T.x2, 0) : 0, y1 = lin2 ? at(T.x2, 1) : 0;
+            const u64 u0 = p2 ? at(T.a2, 0) : 0, u1 = p2 ? at(T.a2, 1) : 0;
+            const u64 w0 = p2 ? at(T.b2, 0) : 0, w1 = p2 ? at(T.b2, 1) : 0;
+            double e0, e1, e2;
+            tensor1_fp_raw(at(T.a, 0), at(T.a, 1), at(T.b, 0), at(T.b, 1), lin, x0, x1, cc, lin2, y0, y1, c2, qd, qinv, e0,
+                           e1, e2, p2, u0, u1, w0, w1);
+            double s0 = __dadd_rn(fpt::mm(e2, KBd, KBq, qd), fpt::mm(e0, PM, PMq, qd));
+            double s1 = __dadd_rn(fpt::mm(e2, KAd, KAq, qd), fpt::mm(e1, PM, PMq, qd));
+            u64 *o0p = accb(u), *o1p = accb(u) + a1off;
+            if (nd > 0) {
+                s0 = __dadd_rn(s0, FpA::D(o0p[i]));
+                s1 = __dadd_rn(s1, FpA::D(o1p[i]));
+            }
+            o0p[i] = fp_canon4(s0, P.q, qd, qinv);
+            o1p[i] = fp_canon4(s1, P.q, qd, qinv);
         }
-        o0p[i] = fp_canon4(s0, P.q, qd, qinv);
-        o1p[i] = fp_canon4(s1, P.q, qd, qinv);
     }
 }
 
@@ -1304,9 +1324,9 @@ template <int LOGN>
 void launch_ks_inner(const Tab &tab, const KsFuse &f, cudaStream_t st) {
     using CF = ContigCfg<LOGN>;
     const int ne = f.nl + f.np;
-    const dim3 grid((unsigned)((1L << LOGN) / (CF::CG * CF::G)), (unsigned)(ne * f.n_ct));
+    const dim3 grid((unsigned)((1L << LOGN) / (CF::CG * CF::G)), (unsigned)(ne * ((f.n_ct + KSI_CPB - 1) / KSI_CPB)));
     auto kern = ntt_ks_inner_kernel<LOGN>;
-    const int smem = CF::CG * CF::PITCH * 8;
+    const int smem = KSI_CPB * CF::CG * CF::PITCH * 8;
     static bool done = false;
     if (!done) {
         CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

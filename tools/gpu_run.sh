@@ -1,5 +1,8 @@
 cd $GRAFT_REPO_ROOT
-for i in 1 2; do for lib in libsecpe.so libsecpe_nors.so libsecpe_head.so; do
-r=$(SECPE_LIB=paper_2502_00847_b200/$lib timeout 300 python tools/argmax49_probe.py 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step'],2))")
-echo "49bit $lib $r" >> gpurun_out/ab10.log
+timeout 600 python -m pytest tests -q -m gpu -x -k "ks_config or small_ring or config5 or digit_counts or other_ring" > gpurun_out/t11.log 2>&1; echo rc=$? >> gpurun_out/t11.log
+for i in 1 2 3; do
+for cfg in "1 libsecpe.so" "1 libsecpe_cpb1.so" "0 libsecpe.so"; do set -- $cfg
+ms=$(SECPE_LIB=paper_2502_00847_b200/$2 SECPE_KS_FUSE=$1 SECPE_BATCH=16 timeout 300 python tools/microbench.py argmax --reps 6 2>/dev/null | grep ms_per_batch | tr -dc '0-9.')
+echo "fuse=$1 $2 $ms" >> gpurun_out/ab11.log
 done; done
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:ntt_ks_inner -s 20 -c 1 python tools/relin_bench.py > gpurun_out/ncu_ksi11.log 2>&1
