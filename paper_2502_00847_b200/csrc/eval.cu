@@ -275,8 +275,9 @@ static void ks_modup(Ctx &c, const u64 *d, long d_stride, int n, int level, DevB
     c.cnt.launches += 1;
 }
 
-// Every row of Q_level u P on the exact-FP64 NTT (FpA, q < 2^46): the relinearisation's ModUp second forward pass
-// and key inner product run as one kernel (ntt_ks_inner).  SECPE_KS_FUSE=0 keeps the separate kernels.
+// Every row of Q_level u P on the exact-FP64 NTT (FpA, q < 2^46): a key switch's ModUp second forward pass and key
+// inner product (relinearisation or plain) run as one kernel (ntt_ks_inner).  SECPE_KS_FUSE=0 keeps the separate
+// kernels.
 static bool ks_fuse_ok(const Ctx &c, int level) {
     static int on = -1;
     if (on < 0) {
@@ -307,12 +308,13 @@ static void ks_inner(Ctx &c, const u64 *d, long d_stride, int n, int level, cons
 static void ks_modup_inner(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, DevBuf &acc,
                            const TensorSrc *ten = nullptr) {
     DevBuf ext;
-    if (ten && ks_fuse_ok(c, level)) {
+    if (ks_fuse_ok(c, level)) {
         ks_modup(c, d, d_stride, n, level, ext, ten, true);
         const long N = c.N;
         const int nl = level + 1, ne = nl + c.np, bt = c.beta(level);
         acc = DevBuf((size_t)n * 2L * ne * N, c.st);
-        KsFuse f{ext.p, (long)bt * ne * N, key, acc.p, 2L * ne * N, n, nl, c.np, c.nq, c.alpha, bt, *ten, c.pmod.p};
+        KsFuse f{ext.p, (long)bt * ne * N, key, acc.p, 2L * ne * N, n, nl, c.np, c.nq, c.alpha, bt,
+                 ten ? *ten : TensorSrc{}, c.pmod.p, d, d_stride};
         NttSpans spans{&c};
         const NttProfHook hook{&spans, ntt_mark};
         if (c.prof.on) ntt_set_prof_hook(&hook);

@@ -133,7 +133,7 @@ void k_ks_inner(const Tab &tab, int logn, const u64 *d, long d_ct_stride, const 
                 const u64 *key, int nq_total, int np, u64 *acc, long acc_ct_stride, int n_ct, int nl,
                 int alpha, cudaStream_t st, const TensorSrc *ten = nullptr, const u64 *pmod = nullptr,
                 u64 galois = 1);  // galois > 1: read sigma_g(X_j) (NTT-domain gather; hoisted rotation, R29)
-// Fused ModUp forward pass 2 + relinearise-and-rescale key inner product (every row of Q_l u P exact-FP64,
+// Fused ModUp forward pass 2 + key inner product (relinearise-and-rescale or plain; every row of Q_l u P exact-FP64,
 // q < 2^46): ext[c][j][e] holds the ModUp digits after the FIRST forward pass (ntt_segments_pass1); for every
 // (ciphertext, row e, tile) the kernel runs the second pass of each digit j with e outside I_j and multiplies the
 // raw transform with key_j[b][e] on the fly, then adds the tensor terms of the Q rows (d2 = a1 b1 (+ a2_1 b2_1)
@@ -145,8 +145,10 @@ struct KsFuse {
     u64 *acc;        // [n_ct][2][nl + np][N]
     long accs;
     int n_ct, nl, np, nq_total, alpha, beta;
-    TensorSrc ten;
+    TensorSrc ten;    // ten.a.p == nullptr: plain key switch of d (rotations), no tensor / [P] terms
     const u64 *pmod;  // [P]_{q_e} per Q row
+    const u64 *d;     // plain key switch: the switched polynomial in NTT form, ct c row e at d + c d_stride + e N
+    long d_stride;
 };
 void ntt_ks_inner(const Tab &tab, int logn, const KsFuse &f, cudaStream_t st);
 // ntt_segments' first forward pass only (the fused kernel above runs the second)

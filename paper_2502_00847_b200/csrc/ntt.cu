@@ -621,6 +621,34 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
         nd++;
     }
     if (!qrow) return;
+    if (!f.ten.a.p) {
+        // plain key switch: the own digit's term is d_e (NTT form) times its key
+        const ulonglong2 *kb = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * jd) * nk * N);
+        const ulonglong2 *ka = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * jd + 1) * nk * N);
+#pragma unroll 1
+        for (int u = 0; u < nc; u++) {
+            const ulonglong2 *dp = reinterpret_cast<const ulonglong2 *>(f.d + (c0 + u) * f.d_stride + (long)e * N + boff);
+            ulonglong2 *acc0 = reinterpret_cast<ulonglong2 *>(accb(u)), *acc1 = reinterpret_cast<ulonglong2 *>(accb(u) + a1off);
+#pragma unroll 2
+            for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
+                const ulonglong2 X = dp[i], KB = __ldg(kb + i), KA = __ldg(ka + i);
+                const double x0 = fx(X.x), x1 = fx(X.y);
+                const double B0 = fx(KB.x), B1 = fx(KB.y), A0 = fx(KA.x), A1 = fx(KA.y);
+                double s00 = fpt::mm(x0, B0, __dmul_rn(B0, qinv), qd), s01 = fpt::mm(x1, B1, __dmul_rn(B1, qinv), qd);
+                double s10 = fpt::mm(x0, A0, __dmul_rn(A0, qinv), qd), s11 = fpt::mm(x1, A1, __dmul_rn(A1, qinv), qd);
+                if (nd > 0) {
+                    const ulonglong2 p0 = acc0[i], p1 = acc1[i];
+                    s00 = __dadd_rn(s00, FpA::D(p0.x));
+                    s01 = __dadd_rn(s01, FpA::D(p0.y));
+                    s10 = __dadd_rn(s10, FpA::D(p1.x));
+                    s11 = __dadd_rn(s11, FpA::D(p1.y));
+                }
+                acc0[i] = make_ulonglong2(fp_canon4(s00, P.q, qd, qinv), fp_canon4(s01, P.q, qd, qinv));
+                acc1[i] = make_ulonglong2(fp_canon4(s10, P.q, qd, qinv), fp_canon4(s11, P.q, qd, qinv));
+            }
+        }
+        return;
+    }
     // Q rows: the tensor (formed on the fly, tensor1_fp_raw) -- d2 with the own digit's key, [P] d0 / [P] d1
     const TensorSrc &T = f.ten;
     const bool lin = T.x.p != nullptr, lin2 = T.x2.p != nullptr, p2 = T.a2.p != nullptr;
@@ -1357,7 +1385,7 @@ void ntt_ks_inner(const Tab &tab, int logn, const KsFuse &f, cudaStream_t st) {
     for (int e = 0; e < ne; e++) drows += e < f.nl ? f.beta - 1 : f.beta;
     drows *= f.n_ct;
     const TensorSrc &T = f.ten;
-    const int tin = 4 + (T.x.p ? 2 : 0) + (T.x2.p ? 2 : 0) + (T.a2.p ? 4 : 0);
+    const int tin = T.a.p ? 4 + (T.x.p ? 2 : 0) + (T.x2.p ? 2 : 0) + (T.a2.p ? 4 : 0) : 1;
     const double opb = 8.0 * N * (2.0 * f.beta * ne + (double)f.n_ct * (tin * f.nl + 2.0 * ne));
     if (g_hook) g_hook->mark(g_hook->ctx, 0, true, 8.0 * N * drows, drows / 2, opb);
     switch (logn) {

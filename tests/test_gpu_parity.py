@@ -711,6 +711,32 @@ def test_key_switching_digit_counts(S, alpha):
     assert np.array_equal(r.t[0].cpu().numpy(), ev.rotate_raw(ko, a, 3).data)
 
 
+@pytest.mark.parametrize("alpha", [2, 4, 8])
+def test_fused_keyswitch_digit_counts(S, alpha):
+    """The fused ModUp second pass + relinearisation key inner product (ntt_ks_inner_kernel: every row of Q u P an
+    exact-FP64 row, 45-bit chain + 46-bit special primes) at dnum = 4, 2, 1 and at two levels (full and a ragged last
+    digit), word for word against the oracle; the rotation path (separate kernels) on the same keys."""
+    desc = dict(logn=12, q=[("nearest", 45, 8)], p=[("below", 46, max(2, alpha // 2))], alpha=alpha, log_scale=45)
+    prm = ckks.Params(desc)
+    assert all(q < (1 << 46) for q in list(prm.q) + list(prm.p))
+    g = S.Context(desc)
+    ev = ckks.Oracle(prm)
+    seed = synth.KEY_SEED_BASE + 14
+    ko, kg = ev.keygen(seed, [3]), g.keygen(seed, [3])
+    a = ev.encrypt(ko, synth.uniform_slots(9, prm.N // 2), prm.scale, 1)
+    b = ev.encrypt(ko, synth.uniform_slots(10, prm.N // 2), prm.scale, 2)
+    for drop in (0, 3):
+        ao, bo = (a, b) if drop == 0 else (ev.drop(a, a.level - drop), ev.drop(b, b.level - drop))
+        ga = S.Ct(torch.from_numpy(ao.data[None].copy()).cuda(), ao.level, ao.scale)
+        gb = S.Ct(torch.from_numpy(bo.data[None].copy()).cuda(), bo.level, bo.scale)
+        out = g.mul_relin_rescale(kg, ga, gb)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.t[0].cpu().numpy(), ev.rescale(ev.mul_relin(ko, ao, bo)).data), drop
+    r = g.rotate(kg, S.Ct(torch.from_numpy(a.data[None].copy()).cuda(), a.level, a.scale), 3)
+    torch.cuda.synchronize()
+    assert np.array_equal(r.t[0].cpu().numpy(), ev.rotate_raw(ko, a, 3).data)
+
+
 @pytest.mark.parametrize("name,steps,level_drop", [
     ("toy", [0, 1, 2, 5, -3], 0),
     ("argmax", [0, 1, 3, 2048, -7, 16], 12),
