@@ -278,6 +278,9 @@ static void ks_modup(Ctx &c, const u64 *d, long d_stride, int n, int level, DevB
 // Every row of Q_level u P on the exact-FP64 NTT (FpA, q < 2^46): a key switch's ModUp second forward pass and key
 // inner product (relinearisation or plain) run as one kernel (ntt_ks_inner).  SECPE_KS_FUSE=0 keeps the separate
 // kernels.
+#ifndef SECPE_KS_FUSE_INTT
+#define SECPE_KS_FUSE_INTT 1  // the fused kernel also runs the ModDown INTT's first pass on its rows
+#endif
 static bool ks_fuse_ok(const Ctx &c, int level) {
     static int on = -1;
     if (on < 0) {
@@ -305,8 +308,10 @@ static void ks_inner(Ctx &c, const u64 *d, long d_stride, int n, int level, cons
     c.cnt.launches += 1;
 }
 
-static void ks_modup_inner(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, DevBuf &acc,
-                           const TensorSrc *ten = nullptr) {
+// returns true when the fused kernel ran; then rows >= intt_row0 (if >= 0) of acc already hold the first pass of their
+// inverse NTT (finish with ev_intt_last)
+static bool ks_modup_inner(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, DevBuf &acc,
+                           const TensorSrc *ten = nullptr, int intt_row0 = -1) {
     DevBuf ext;
     if (ks_fuse_ok(c, level)) {
         ks_modup(c, d, d_stride, n, level, ext, ten, true);
@@ -314,23 +319,35 @@ static void ks_modup_inner(Ctx &c, const u64 *d, long d_stride, int n, int level
         const int nl = level + 1, ne = nl + c.np, bt = c.beta(level);
         acc = DevBuf((size_t)n * 2L * ne * N, c.st);
         KsFuse f{ext.p, (long)bt * ne * N, key, acc.p, 2L * ne * N, n, nl, c.np, c.nq, c.alpha, bt,
-                 ten ? *ten : TensorSrc{}, c.pmod.p, d, d_stride};
+                 ten ? *ten : TensorSrc{}, c.pmod.p, d, d_stride, SECPE_KS_FUSE_INTT ? intt_row0 : -1};
         NttSpans spans{&c};
         const NttProfHook hook{&spans, ntt_mark};
         if (c.prof.on) ntt_set_prof_hook(&hook);
         ntt_ks_inner(c.tab, c.logn, f, c.st);
         if (c.prof.on) ntt_set_prof_hook(nullptr);
         c.cnt.launches += 1;
-        return;
+        return SECPE_KS_FUSE_INTT && intt_row0 >= 0;
     }
     ks_modup(c, d, d_stride, n, level, ext, ten);
     ks_inner(c, d, d_stride, n, level, key, ext, acc, ten);
+    return false;
+}
+
+// the inverse NTT's last pass only (the first ran inside the fused key-switch kernel)
+static void ev_intt_last(Ctx &c, RowsArg d, int n_polys, LimbMap lm, const NttFusion &f) {
+    NttSpans spans{&c};
+    const NttProfHook hook{&spans, ntt_mark};
+    if (c.prof.on) ntt_set_prof_hook(&hook);
+    ntt_inverse_last_pass(c.tab, c.logn, d, n_polys, lm, c.st, f);
+    if (c.prof.on) ntt_set_prof_hook(nullptr);
+    c.cnt.ntt_limbs += (long long)n_polys * lm.nl;
+    c.cnt.launches += 1;
 }
 
 // Hybrid key switching of d (NTT form; ct c at d + c * d_stride, level limbs), result added to
 // `add` (add_polys of 2 polynomials; compact, ct stride add_stride) and written compact to out.
 static void ks_moddown(Ctx &c, DevBuf &acc, int n, int level, const u64 *add, long add_stride, int add_polys,
-                       u64 *out, long out_stride, const CRows *add3 = nullptr);
+                       u64 *out, long out_stride, const CRows *add3 = nullptr, bool intt_pre = false);
 
 void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, const u64 *add,
                   long add_stride, int add_polys, u64 *out, long out_stride, const CRows *add3) {
@@ -338,8 +355,8 @@ void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u
     const int nl = level + 1, np = c.np, ne = nl + np, bt = c.beta(level);
     const size_t pa = c.prof_begin(1);
     DevBuf acc;
-    ks_modup_inner(c, d, d_stride, n, level, key, acc);
-    ks_moddown(c, acc, n, level, add, add_stride, add_polys, out, out_stride, add3);
+    const bool pre = ks_modup_inner(c, d, d_stride, n, level, key, acc, nullptr, level + 1);
+    ks_moddown(c, acc, n, level, add, add_stride, add_polys, out, out_stride, add3, pre);
     c.cnt.keyswitch += n;
     // algorithmic bytes: input limbs + output limbs per ciphertext + the key once per batch
     c.prof_end(pa, 1, 8.0 * N * ((double)n * (nl + 2 * nl + add_polys * nl) + 2.0 * bt * ne), n);
@@ -347,7 +364,7 @@ void ev_keyswitch(Ctx &c, const u64 *d, long d_stride, int n, int level, const u
 
 // ModDown of acc (R11) with the addend fused into the final NTT's epilogue; result compact in out
 static void ks_moddown(Ctx &c, DevBuf &acc, int n, int level, const u64 *add, long add_stride, int add_polys,
-                       u64 *out, long out_stride, const CRows *add3) {
+                       u64 *out, long out_stride, const CRows *add3, bool intt_pre) {
     const long N = c.N;
     const int nl = level + 1, np = c.np, ne = nl + np, bt = c.beta(level);
     const long accs = 2L * ne * N;
@@ -356,7 +373,10 @@ static void ks_moddown(Ctx &c, DevBuf &acc, int n, int level, const u64 *add, lo
     NttFusion f4;
     f4.k = c.ihp_ninv.p;
     f4.ksh = c.ihp_ninv_sh.p;
-    ev_ntt(c, RowsArg{acc.p + (long)nl * N, accs, (long)ne * N}, 2 * n, LimbMap{np, 0, 0, c.nq}, true, f4);
+    if (intt_pre)
+        ev_intt_last(c, RowsArg{acc.p + (long)nl * N, accs, (long)ne * N}, 2 * n, LimbMap{np, 0, 0, c.nq}, f4);
+    else
+        ev_ntt(c, RowsArg{acc.p + (long)nl * N, accs, (long)ne * N}, 2 * n, LimbMap{np, 0, 0, c.nq}, true, f4);
     const long Ts = 2L * nl * N;
     DevBuf T((size_t)n * Ts, c.st);
     const LevelConsts &lc = c.level(level);
@@ -423,13 +443,16 @@ void ev_mul_relin_rescale(Ctx &c, const Keys &k, const CtView &a, const CtView &
     }
     const size_t pa = c.prof_begin(1);
     DevBuf acc;
-    ks_modup_inner(c, nullptr, 0, n, l, k.rlk.p, acc, &ten);
+    const bool pre = ks_modup_inner(c, nullptr, 0, n, l, k.rlk.p, acc, &ten, l);
     const long accs = 2L * ne * N;
     // INTT of the B rows (q_l row, then the special rows: contiguous rows l .. ne-1) with (B/s)^{-1} folded
     NttFusion f4;
     f4.k = lc.rr_fold.p;
     f4.ksh = lc.rr_fold_sh.p;
-    ev_ntt(c, RowsArg{acc.p + (long)l * N, accs, (long)ne * N}, 2 * n, LimbMap{np + 1, 1, l, c.nq}, true, f4);
+    if (pre)
+        ev_intt_last(c, RowsArg{acc.p + (long)l * N, accs, (long)ne * N}, 2 * n, LimbMap{np + 1, 1, l, c.nq}, f4);
+    else
+        ev_ntt(c, RowsArg{acc.p + (long)l * N, accs, (long)ne * N}, 2 * n, LimbMap{np + 1, 1, l, c.nq}, true, f4);
     const long Ts = 2L * l * N;
     DevBuf T((size_t)n * Ts, c.st);
     if (c.use_tc && lc.tc_ok) {

@@ -149,8 +149,13 @@ struct KsFuse {
     const u64 *pmod;  // [P]_{q_e} per Q row
     const u64 *d;     // plain key switch: the switched polynomial in NTT form, ct c row e at d + c d_stride + e N
     long d_stride;
+    int intt_row0;    // >= 0: rows e >= intt_row0 (the ModDown's INTT rows) also get the inverse NTT's first pass,
+                      // in place (finish them with ntt_inverse_last_pass); -1: none
 };
 void ntt_ks_inner(const Tab &tab, int logn, const KsFuse &f, cudaStream_t st);
+// the inverse NTT's last pass only (its first pass already ran, e.g. inside ntt_ks_inner): f.k / f.ksh factors
+void ntt_inverse_last_pass(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
+                           const NttFusion &f);
 // ntt_segments' first forward pass only (the fused kernel above runs the second)
 void ntt_segments_pass1(const Tab &tab, int logn, const NttSeg *segs, int nseg, cudaStream_t st);
 // ModDown conversion (R11): T[c][b][i] = sum_{s < ns} y_s [B/s]_{q_i} mod q_i for i < nt, with

@@ -516,6 +516,50 @@ __global__ void __launch_bounds__(CT, MinB<A>::v) ntt_contig(PassArgs a) {
 // residues as ks_inner_ten1_kernel (sums of exact products mod q), so the key-switch integers are unchanged.
 // Rows are ordered e-major (ciphertexts of one row adjacent) so a key tile is read from HBM once per batch.
 // ---------------------------------------------------------------------------------------------
+// the ModDown's INTT rows (e >= f.intt_row0): the inverse NTT's first pass (GS stages LOGN-1..S, the contiguous pass
+// with a plain input) on the tile this CTA just finished (canonical, L2-resident), written back in place in the
+// inverse's intermediate representation -- the same words the separate first-pass launch would write
+template <int LOGN>
+__device__ __forceinline__ void ksi_intt_rows(const Tab &tab, const KsFuse &f, int e, int pr, const PrimeC &P, long boff,
+                                              int c0, int nc, long a1off, u64 *sm) {
+    if (f.intt_row0 < 0 || e < f.intt_row0) return;
+    using CF = ContigCfg<LOGN>;
+    constexpr int S = CF::S, G = CF::G, TPG = CF::TPG, CG = CF::CG, PITCH = CF::PITCH;
+    constexpr long N = 1L << LOGN;
+    using R = Rnd<S, true>;
+    constexpr int LO0 = R::lo(0), LO1 = R::lo(1);
+    const ulonglong2 *itw = tab.itw2 + pr * N;
+    const int gl = threadIdx.x / TPG, tau = threadIdx.x % TPG;
+    const int g = blockIdx.x * CG + gl;
+    u64 *smg = sm + gl * PITCH;
+    for (int u = 0; u < nc; u++)
+        for (int b = 0; b < 2; b++) {
+            u64 *row = f.acc + (c0 + u) * f.accs + (long)e * N + boff + b * a1off;
+            __syncthreads();  // this CTA's writes of the row (and the shared tile's previous use) are complete
+            const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(row);
+            for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
+                const ulonglong2 x = src[i];
+                const int el = 2 * i, gg = el / G, r = el % G;
+                sm[gg * PITCH + padr(r)] = FpA::in(x.x, P);
+                sm[gg * PITCH + padr(r + 1)] = FpA::in(x.y, P);
+            }
+            __syncthreads();
+            u64 v[NV];
+#pragma unroll
+            for (int k = 0; k < NV; k++) v[k] = smg[padr(held<LO0>(tau, k))];
+            do_round<S, true, 0, true, LOGN, FpA>(v, tau, g, itw, P);
+#pragma unroll
+            for (int k = 0; k < NV; k++) smg[padr(held<LO0>(tau, k))] = v[k];
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < NV; k++) v[k] = smg[padr(held<LO1>(tau, k))];
+            do_round<S, true, 1, true, LOGN, FpA>(v, tau, g, itw, P);
+            u64 *dst = row + gl * G;
+#pragma unroll
+            for (int k = 0; k < NV; k++) NTT_ST(dst + held<LO1>(tau, k), v[k]);
+        }
+}
+
 template <int LOGN>
 __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab, KsFuse f) {
     using CF = ContigCfg<LOGN>;
@@ -620,7 +664,10 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
         __syncthreads();  // the next digit's round 0 rewrites the shared tiles
         nd++;
     }
-    if (!qrow) return;
+    if (!qrow) {
+        ksi_intt_rows<LOGN>(tab, f, e, pr, P, boff, c0, nc, a1off, ksi_sm);
+        return;
+    }
     if (!f.ten.a.p) {
         // plain key switch: the own digit's term is d_e (NTT form) times its key
         const ulonglong2 *kb = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * jd) * nk * N);
@@ -647,6 +694,7 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
                 acc1[i] = make_ulonglong2(fp_canon4(s10, P.q, qd, qinv), fp_canon4(s11, P.q, qd, qinv));
             }
         }
+        ksi_intt_rows<LOGN>(tab, f, e, pr, P, boff, c0, nc, a1off, ksi_sm);
         return;
     }
     // Q rows: the tensor (formed on the fly, tensor1_fp_raw) -- d2 with the own digit's key, [P] d0 / [P] d1
@@ -682,6 +730,7 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
             o1p[i] = fp_canon4(s1, P.q, qd, qinv);
         }
     }
+    ksi_intt_rows<LOGN>(tab, f, e, pr, P, boff, c0, nc, a1off, ksi_sm);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1336,6 +1385,21 @@ void ntt_segments(const Tab &tab, int logn, const NttSeg *segs, int nseg, bool i
     }
 }
 
+void ntt_inverse_last_pass(const Tab &tab, int logn, RowsArg data, int n_polys, LimbMap lm, cudaStream_t st,
+                           const NttFusion &f) {
+    if (n_polys <= 0 || lm.nl <= 0) return;
+    const PassArgs a{data, lm, tab, f, 0, lm.nl, 0};
+    switch (logn) {
+        case 12: launch_strided<12, true, IN_PLAIN>(a, n_polys, st); break;
+        case 13: launch_strided<13, true, IN_PLAIN>(a, n_polys, st); break;
+        case 14: launch_strided<14, true, IN_PLAIN>(a, n_polys, st); break;
+        case 15: launch_strided<15, true, IN_PLAIN>(a, n_polys, st); break;
+        case 16: launch_strided<16, true, IN_PLAIN>(a, n_polys, st); break;
+        default: throw SecpeError{-1, "NTT: log N must be in [12, 16]"};
+    }
+    LAUNCH_CHECK();
+}
+
 void ntt_segments_pass1(const Tab &tab, int logn, const NttSeg *segs, int nseg, cudaStream_t st) {
     switch (logn) {
         case 12: run_segs<12>(tab, segs, nseg, false, st, true); break;
@@ -1386,6 +1450,8 @@ void ntt_ks_inner(const Tab &tab, int logn, const KsFuse &f, cudaStream_t st) {
     drows *= f.n_ct;
     const TensorSrc &T = f.ten;
     const int tin = T.a.p ? 4 + (T.x.p ? 2 : 0) + (T.x2.p ? 2 : 0) + (T.a2.p ? 4 : 0) : 1;
+    // the ModDown's INTT rows get the inverse's first pass here too: half a transform each, 2 polys per ciphertext
+    if (f.intt_row0 >= 0) drows += 2.0 * f.n_ct * (ne - f.intt_row0);
     const double opb = 8.0 * N * (2.0 * f.beta * ne + (double)f.n_ct * (tin * f.nl + 2.0 * ne));
     if (g_hook) g_hook->mark(g_hook->ctx, 0, true, 8.0 * N * drows, drows / 2, opb);
     switch (logn) {
