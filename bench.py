@@ -667,12 +667,13 @@ def run_secpe(a):
     ops = prof.get("ntt_fp_operands", {"bytes": 0.0})
     ach_t, ks_ach = gbs(ntt), gbs(ks)
     ach = (ntt["bytes"] + ops["bytes"]) / (ntt["ms"] / 1000.0) / 1e9 if ntt["ms"] > 0 else 0.0
-    traffic, tsrc = None, None
+    traffic, tsrc, t_over_a = None, None, None
     tp = os.path.join(ROOT, "profiles", "ntt_traffic.json")
     if os.path.exists(tp):
         try:
             tj = json.load(open(tp))
             traffic, tsrc = tj["dram_bytes_per_limb_transform"], tj.get("source")
+            t_over_a = tj.get("traffic_over_algorithmic")
         except Exception:
             traffic = None
     # FP64-pipe roof of the same kernels: (N/2) log2 N butterflies per limb transform, 8 FP64-pipe
@@ -693,7 +694,7 @@ def run_secpe(a):
         "roofline": {"bound": "hbm", "kernel": "ntt on the 45-bit (FP64) rows: every forward/inverse launch in the "
                                                 "profiled region (%.0f limb transforms per step)" % (ntt["units"] / a.steps),
                      "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
-                     "traffic_source": tsrc, "peak_source": peak_src,
+                     "traffic_source": tsrc, "traffic_over_algorithmic": t_over_a, "peak_source": peak_src,
                      "algorithmic_bytes": "per launch: 16 N per limb transform (split over its passes) + the operand "
                                           "limbs of its fused prologue / epilogue (%.1f MB per step of the %.1f MB)" % (
                                               ops["bytes"] / a.steps / 1e6,
