@@ -403,7 +403,8 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) bconv_tc2_kernel(TcArgs a, int
         spmsh[tid] = G.pmodsh[tid];
         soff[tid] = (long)G.out_row[tid] << a.logn;
         spk[tid][0] = make_ulonglong2(q, (u64)0 - q);
-        spk[tid][1] = make_ulonglong2((u64)__double_as_longlong(G.qinv[tid]), (u64)(((long)G.out_row[tid] << a.logn) * 8));
+        spk[tid][1] = make_ulonglong2((u64)__double_as_longlong(G.qinv[tid] * 65536.0),
+                                      (u64)(((long)G.out_row[tid] << a.logn) * 8));
     }
     if (tid == 0) {
         for (int b = 0; b < 2; b++) {
@@ -542,20 +543,25 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) bconv_tc2_kernel(TcArgs a, int
             };
             if (planes == 6 && !a.rr) {
                 uint8_t *const obase = reinterpret_cast<uint8_t *>(dst + k0 + m);
-                auto lean = [&](const uint32_t *x, int t) {
+                auto lean = [&](const uint32_t *x, int t) {  // bconv_tc_kernel's lean epilogue (same integers)
                     const ulonglong2 c0 = spk[t][0], c1 = spk[t][1];
-                    u64 v = (u64)x[0] + (u64)x[1] * 256u;
-                    v += (u64)x[2] * 65536u;
-                    v += (u64)x[3] * 16777216u;
-                    const uint32_t vh = (uint32_t)(v >> 32) + x[4] + x[5] * 256u, vl = (uint32_t)v;
-                    v = ((u64)vh << 32) | vl;
-                    const double vd = __fma_rn(__dsub_rn(__hiloint2double(0x43300000, (int)vh), 4503599627370496.0),
-                                               4294967296.0,
-                                               __dsub_rn(__hiloint2double(0x43300000, (int)vl), 4503599627370496.0));
-                    const uint32_t k = (uint32_t)__double_as_longlong(
-                        __fma_rn(vd, __longlong_as_double((long long)c1.x), 6755399441055744.0));
-                    u64 r = v + (u64)k * c0.y;
-                    if ((int)(r >> 32) < 0) r += c0.x;
+                    const uint32_t A = x[0] + (x[1] << 8), B = x[2] + (x[3] << 8), C = x[4] + (x[5] << 8);
+                    const double cb = __fma_rn(__dsub_rn(__hiloint2double(0x43300000, (int)C), TC_TWO52), 65536.0,
+                                               __dsub_rn(__hiloint2double(0x43300000, (int)B), TC_TWO52));
+                    const uint32_t k =
+                        (uint32_t)__double_as_longlong(__fma_rn(cb, __longlong_as_double((long long)c1.x), TC_MAGIC));
+                    uint32_t lo, hi;
+                    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
+                        : "=r"(lo), "=r"(hi)
+                        : "r"(A), "r"(B << 16), "r"(C), "r"(B >> 16));
+                    u64 r = (((u64)hi << 32) | lo) + (u64)k * c0.y;
+                    asm("{\n\t.reg .pred p;\n\t.reg .u32 rl, rh, tl, th;\n\t"
+                        "mov.b64 {rl, rh}, %0;\n\tmov.b64 {tl, th}, %1;\n\t"
+                        "setp.lt.s32 p, rh, 0;\n\t"
+                        "@p add.cc.u32 rl, rl, tl;\n\t@p addc.u32 rh, rh, th;\n\t"
+                        "mov.b64 %0, {rl, rh};\n\t}"
+                        : "+l"(r)
+                        : "l"(c0.x));
                     *reinterpret_cast<u64 *>(obase + c1.y) = r;
                 };
                 for (int t = tb; t < te; t += 2) {
@@ -657,7 +663,7 @@ void k_bconv_tc(const TcArgs &a, int n_polys, cudaStream_t st) {
         const char *t = getenv("SECPE_TC2_TPC");
         tpc2 = t ? std::max(1, atoi(t)) : 16;
     }
-    if (ver == 2) {
+    if (ver == 2 && !a.rr) {  // (the fused ModDown + rescale keeps the second-MMA kernel below)
         // 2 A stages (24 KB) + B (24 KB); > 114 KB requested so one CTA (512 TMEM columns) per SM
         constexpr int smem2 = 120 * 1024;
         static bool attr2 = false;
