@@ -40,6 +40,13 @@
 #define KSI_CPB 1  // ciphertexts per CTA of the fused kernel (2: one key load serves two tiles -- measured slower: partial sums
                    // spill from L2 to DRAM, 71.8 vs 68.0 ms per argmax step)
 #endif
+#ifndef KSI_DPB
+#define KSI_DPB 1  // digits per epilogue pass of the fused kernel (2: two transformed tiles per CTA, one epilogue pass --
+                   // kernel -8 % alone, but the argmax step +1.4 % (the second tile costs residency next to the other stream))
+#endif
+#ifndef KSI_PAIR_MIN_BETA
+#define KSI_PAIR_MIN_BETA 3  // digit pairs from this many digits on (fewer: one tile, more resident CTAs)
+#endif
 #ifndef NTT_KSI_PREFETCH
 #define NTT_KSI_PREFETCH 1  // per digit: L2 prefetch of its key tiles and the next digit's tile (all tiles at kernel start: evicted before use, slower)
 #endif
@@ -601,6 +608,87 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
     };
     const long lo = (long)threadIdx.x * 16;  // this thread's 128-byte line of a tile (L2 prefetches)
     int nd = 0;
+    if (KSI_DPB == 2 && f.pairs) {
+    // digits in pairs: both tiles transformed into their own shared buffers, then ONE epilogue pass multiplies both
+    // with their keys (twice the independent loads per iteration, half the partial-sum round trips)
+    static_assert(KSI_DPB != 2 || KSI_CPB == 1, "digit pairs: one ciphertext per CTA");
+    for (int ja = next_digit(-1); ja >= 0;) {
+        const int jb0 = next_digit(ja), ng = jb0 >= 0 ? 2 : 1, jn = jb0 >= 0 ? next_digit(jb0) : -1;
+        const bool fin = jn < 0 && !qrow;  // the last terms of a special row: canonicalise
+#pragma unroll 1
+        for (int h = 0; h < ng; h++) {
+            const int j = h ? jb0 : ja;
+#if NTT_KSI_PREFETCH
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(keyrow + (long)(2 * j) * nk * N + lo));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(keyrow + (long)(2 * j + 1) * nk * N + lo));
+#endif
+            u64 *const smg = ksi_sm + h * CG * PITCH + gl * PITCH;
+            const u64 *src = f.ext + c0 * f.exts + ((long)j * ne + e) * N + boff + gl * G;
+            const ulonglong2 *twu;
+            asm volatile("mov.b64 %0, %1;" : "=l"(twu) : "l"(tw));
+            u64 v[NV];
+#pragma unroll
+            for (int k = 0; k < NV; k++) v[k] = NTT_LD(src + held<LO0>(tau, k));  // first-pass representation
+            do_round<S, false, 0, true, LOGN, FpA>(v, tau, g, twu, P);
+#pragma unroll
+            for (int k = 0; k < NV; k++) smg[padr(held<LO0>(tau, k))] = v[k];
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < NV; k++) v[k] = smg[padr(held<LO1>(tau, k))];
+            do_round<S, false, 1, true, LOGN, FpA>(v, tau, g, twu, P);
+#pragma unroll
+            for (int k = 0; k < NV; k++) smg[padr(held<LO1>(tau, k))] = v[k];
+        }
+        __syncthreads();
+        const int jb = ng > 1 ? jb0 : ja;
+        const ulonglong2 *kba = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * ja) * nk * N);
+        const ulonglong2 *kaa = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * ja + 1) * nk * N);
+        const ulonglong2 *kbb = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * jb) * nk * N);
+        const ulonglong2 *kab = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * jb + 1) * nk * N);
+        ulonglong2 *acc0 = reinterpret_cast<ulonglong2 *>(accb(0)), *acc1 = reinterpret_cast<ulonglong2 *>(accb(0) + a1off);
+        const u64 *smb = ksi_sm + CG * PITCH;
+#pragma unroll 2
+        for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
+            const int el = 2 * i, gg = el / G, r = el % G;
+            const ulonglong2 KB = __ldg(kba + i), KA = __ldg(kaa + i);
+            const double x0 = FpA::D(ksi_sm[gg * PITCH + padr(r)]), x1 = FpA::D(ksi_sm[gg * PITCH + padr(r + 1)]);
+            double s00, s01, s10, s11;
+            {
+                const double B0 = fx(KB.x), B1 = fx(KB.y), A0 = fx(KA.x), A1 = fx(KA.y);
+                s00 = fpt::mm(x0, B0, __dmul_rn(B0, qinv), qd);
+                s01 = fpt::mm(x1, B1, __dmul_rn(B1, qinv), qd);
+                s10 = fpt::mm(x0, A0, __dmul_rn(A0, qinv), qd);
+                s11 = fpt::mm(x1, A1, __dmul_rn(A1, qinv), qd);
+            }
+            if (ng > 1) {
+                const ulonglong2 KB2 = __ldg(kbb + i), KA2 = __ldg(kab + i);
+                const double y0 = FpA::D(smb[gg * PITCH + padr(r)]), y1 = FpA::D(smb[gg * PITCH + padr(r + 1)]);
+                const double B0 = fx(KB2.x), B1 = fx(KB2.y), A0 = fx(KA2.x), A1 = fx(KA2.y);
+                s00 = __dadd_rn(s00, fpt::mm(y0, B0, __dmul_rn(B0, qinv), qd));
+                s01 = __dadd_rn(s01, fpt::mm(y1, B1, __dmul_rn(B1, qinv), qd));
+                s10 = __dadd_rn(s10, fpt::mm(y0, A0, __dmul_rn(A0, qinv), qd));
+                s11 = __dadd_rn(s11, fpt::mm(y1, A1, __dmul_rn(A1, qinv), qd));
+            }
+            if (nd > 0) {
+                const ulonglong2 p0 = acc0[i], p1 = acc1[i];
+                s00 = __dadd_rn(s00, FpA::D(p0.x));
+                s01 = __dadd_rn(s01, FpA::D(p0.y));
+                s10 = __dadd_rn(s10, FpA::D(p1.x));
+                s11 = __dadd_rn(s11, FpA::D(p1.y));
+            }
+            if (fin) {
+                acc0[i] = make_ulonglong2(fp_canon4(s00, P.q, qd, qinv), fp_canon4(s01, P.q, qd, qinv));
+                acc1[i] = make_ulonglong2(fp_canon4(s10, P.q, qd, qinv), fp_canon4(s11, P.q, qd, qinv));
+            } else {
+                acc0[i] = make_ulonglong2(FpA::B(s00), FpA::B(s01));
+                acc1[i] = make_ulonglong2(FpA::B(s10), FpA::B(s11));
+            }
+        }
+        __syncthreads();  // the next pair's round 0 rewrites the shared tiles
+        nd += ng;
+        ja = jn;
+    }
+    } else {
     for (int j = next_digit(-1); j >= 0; j = next_digit(j)) {
         const bool fin = nd == ndig - 1 && !qrow;  // the last term of a special row: canonicalise
 #if NTT_KSI_PREFETCH
@@ -666,6 +754,7 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
         }
         __syncthreads();  // the next digit's round 0 rewrites the shared tiles
         nd++;
+    }
     }
     if (!qrow) {
         ksi_intt_rows<LOGN>(tab, f, e, pr, P, boff, c0, nc, a1off, ksi_sm);
@@ -1421,10 +1510,12 @@ void launch_ks_inner(const Tab &tab, const KsFuse &f, cudaStream_t st) {
     const int ne = f.nl + f.np;
     const dim3 grid((unsigned)((1L << LOGN) / (CF::CG * CF::G)), (unsigned)(ne * ((f.n_ct + KSI_CPB - 1) / KSI_CPB)));
     auto kern = ntt_ks_inner_kernel<LOGN>;
-    const int smem = KSI_CPB * CF::CG * CF::PITCH * 8;
+    // digit pairs only where rows have three or more digits (a second tile costs residency; measured in the step)
+    const int smem = (f.pairs ? 2 : KSI_CPB) * CF::CG * CF::PITCH * 8;
     static bool done = false;
     if (!done) {
-        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        std::max(2, KSI_CPB) * CF::CG * CF::PITCH * 8));
         max_smem_carveout(kern);
         done = true;
     }
@@ -1442,8 +1533,10 @@ void launch_ks_inner(const Tab &tab, const KsFuse &f, cudaStream_t st) {
 }
 }  // namespace
 
-void ntt_ks_inner(const Tab &tab, int logn, const KsFuse &f, cudaStream_t st) {
-    if (f.n_ct <= 0) return;
+void ntt_ks_inner(const Tab &tab, int logn, const KsFuse &f0, cudaStream_t st) {
+    if (f0.n_ct <= 0) return;
+    KsFuse f = f0;
+    f.pairs = KSI_DPB == 2 && KSI_CPB == 1 && f.beta >= KSI_PAIR_MIN_BETA;
     // profiling: the second half of every digit row's transform (8 N per limb) plus the operands the fused inner
     // product reads and writes (key once per batch, tensor inputs of the Q rows, the acc rows)
     const double N = (double)(1L << logn);
