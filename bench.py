@@ -691,8 +691,10 @@ def run_secpe(a):
                    "l2": "inputs larger than L2 (%.0f MB ciphertexts + %.0f MB keys per rank)" % (
                        B * inp.t[0].numel() * 8 / 1e6,
                        (len(steps_rot) + 1) * -(-ctx.nq // ctx.alpha) * 2 * (ctx.nq + ctx.np_) * ctx.N * 8 / 1e6)},
-        "roofline": {"bound": "hbm", "kernel": "ntt on the 45-bit (FP64) rows: every forward/inverse launch in the "
-                                                "profiled region (%.0f limb transforms per step)" % (ntt["units"] / a.steps),
+        "roofline": {"bound": "hbm", "kernel": "ntt family on the 45-bit (FP64) rows: every forward/inverse launch in the "
+                                                "profiled region incl. the fused ModUp pass 2 + key inner product "
+                                                "(ntt_ks_inner_kernel) and the fused prologues/epilogues (%.0f limb "
+                                                "transforms per step)" % (ntt["units"] / a.steps),
                      "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
                      "traffic_source": tsrc, "traffic_over_algorithmic": t_over_a, "peak_source": peak_src,
                      "algorithmic_bytes": "per launch: 16 N per limb transform (split over its passes) + the operand "
