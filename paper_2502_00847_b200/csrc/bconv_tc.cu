@@ -686,7 +686,8 @@ void k_bconv_tc(const TcArgs &a, int n_polys, cudaStream_t st) {
     static int tiles_per_cta = 0;
     if (!tiles_per_cta) {
         const char *e = getenv("SECPE_TC_TPC");  // development switch
-        tiles_per_cta = e ? atoi(e) : 8;  // measured 4: 78.6, 8: 77.6, 16: 77.6 ms per argmax step
+        tiles_per_cta = e ? atoi(e) : 16;  // measured (round 2) 4: 78.6, 8: 77.6, 16: 77.6; (session 3) 4: 68.0,
+                                           // 8: 66.8, 16: 66.5, 32: 66.5, 64: 69.5 ms per argmax step
         if (tiles_per_cta < 1) tiles_per_cta = 1;
     }
     const dim3 grid((ntiles + tiles_per_cta - 1) / tiles_per_cta, n_polys);

@@ -33,6 +33,9 @@
 #include "ntt_core.cuh"
 #include "fpk.cuh"
 
+#ifndef NTT_WAVE_PREFETCH_INV
+#define NTT_WAVE_PREFETCH_INV 0  // the same next-wave L2 prefetch in the inverse's last (strided) pass
+#endif
 #ifndef NTT_KSI_MINB
 #define NTT_KSI_MINB 3  // resident CTAs per SM of the fused ModUp pass 2 + key inner product kernel
 #endif
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(SC *(1 << (LOGN / 2 - RB)), MinB<A>::v) ntt_st
     asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
 #if NTT_WAVE_PREFETCH
-    if (!INV && IN == IN_PLAIN && a.wave > 0) {
+    if ((!INV || NTT_WAVE_PREFETCH_INV) && IN == IN_PLAIN && a.wave > 0) {
         // the tile a CTA of the next wave will read: one 128-byte row segment per thread into L2
         constexpr int S = LOGN / 2;
         constexpr long N = 1L << LOGN;
