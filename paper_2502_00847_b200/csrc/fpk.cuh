@@ -71,4 +71,31 @@ __device__ __forceinline__ u64 fp_canon4(double v, u64 q, double qd, double qinv
 }
 
 
+// one coefficient of the tensor: (d0, d1, d2) mod q, with the optional linear term C x
+__device__ __forceinline__ void tensor1(u64 a0, u64 a1, u64 b0, u64 b1, bool lin, u64 x0, u64 x1, u64 c, u64 csh,
+                                        bool lin2, u64 y0, u64 y1, u64 c2, u64 c2sh, u64 q, u64 r0, u64 r1, u64 &d0,
+                                        u64 &d1, u64 &d2, bool p2 = false, u64 u0 = 0, u64 u1 = 0, u64 w0 = 0,
+                                        u64 w1 = 0) {
+    U128 t0 = mul_wide(a0, b0), t2 = mul_wide(a1, b1);
+    U128 t = mul_wide(a0, b1);
+    mac_wide(t, a1, b0);
+    if (p2) {  // second product (R13b); four 120-bit products stay below the Barrett bound 2^125
+        mac_wide(t0, u0, w0);
+        mac_wide(t2, u1, w1);
+        mac_wide(t, u0, w1);
+        mac_wide(t, u1, w0);
+    }
+    d0 = barrett128(t0, q, r0, r1);
+    d1 = barrett128(t, q, r0, r1);
+    d2 = barrett128(t2, q, r0, r1);
+    if (lin) {
+        d0 = addmod(d0, mul_shoup(x0, c, csh, q), q);
+        d1 = addmod(d1, mul_shoup(x1, c, csh, q), q);
+    }
+    if (lin2) {
+        d0 = addmod(d0, mul_shoup(y0, c2, c2sh, q), q);
+        d1 = addmod(d1, mul_shoup(y1, c2, c2sh, q), q);
+    }
+}
+
 }  // namespace

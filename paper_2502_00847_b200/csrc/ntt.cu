@@ -43,13 +43,6 @@
 #define KSI_CPB 1  // ciphertexts per CTA of the fused kernel (2: one key load serves two tiles -- measured slower: partial sums
                    // spill from L2 to DRAM, 71.8 vs 68.0 ms per argmax step)
 #endif
-#ifndef KSI_DPB
-#define KSI_DPB 1  // digits per epilogue pass of the fused kernel (2: two transformed tiles per CTA, one epilogue pass --
-                   // kernel -8 % alone, but the argmax step +1.4 % (the second tile costs residency next to the other stream))
-#endif
-#ifndef KSI_PAIR_MIN_BETA
-#define KSI_PAIR_MIN_BETA 3  // digit pairs from this many digits on (fewer: one tile, more resident CTAs)
-#endif
 #ifndef NTT_KSI_PREFETCH
 #define NTT_KSI_PREFETCH 1  // per digit: L2 prefetch of its key tiles and the next digit's tile (all tiles at kernel start: evicted before use, slower)
 #endif
@@ -529,7 +522,7 @@ __global__ void __launch_bounds__(CT, MinB<A>::v) ntt_contig(PassArgs a) {
 // the ModDown's INTT rows (e >= f.intt_row0): the inverse NTT's first pass (GS stages LOGN-1..S, the contiguous pass
 // with a plain input) on the tile this CTA just finished (canonical, L2-resident), written back in place in the
 // inverse's intermediate representation -- the same words the separate first-pass launch would write
-template <int LOGN>
+template <int LOGN, class A>
 __device__ __forceinline__ void ksi_intt_rows(const Tab &tab, const KsFuse &f, int e, int pr, const PrimeC &P, long boff,
                                               int c0, int nc, long a1off, u64 *sm) {
     if (f.intt_row0 < 0 || e < f.intt_row0) return;
@@ -550,20 +543,20 @@ __device__ __forceinline__ void ksi_intt_rows(const Tab &tab, const KsFuse &f, i
             for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
                 const ulonglong2 x = src[i];
                 const int el = 2 * i, gg = el / G, r = el % G;
-                sm[gg * PITCH + padr(r)] = FpA::in(x.x, P);
-                sm[gg * PITCH + padr(r + 1)] = FpA::in(x.y, P);
+                sm[gg * PITCH + padr(r)] = A::in(x.x, P);
+                sm[gg * PITCH + padr(r + 1)] = A::in(x.y, P);
             }
             __syncthreads();
             u64 v[NV];
 #pragma unroll
             for (int k = 0; k < NV; k++) v[k] = smg[padr(held<LO0>(tau, k))];
-            do_round<S, true, 0, true, LOGN, FpA>(v, tau, g, itw, P);
+            do_round<S, true, 0, true, LOGN, A>(v, tau, g, itw, P);
 #pragma unroll
             for (int k = 0; k < NV; k++) smg[padr(held<LO0>(tau, k))] = v[k];
             __syncthreads();
 #pragma unroll
             for (int k = 0; k < NV; k++) v[k] = smg[padr(held<LO1>(tau, k))];
-            do_round<S, true, 1, true, LOGN, FpA>(v, tau, g, itw, P);
+            do_round<S, true, 1, true, LOGN, A>(v, tau, g, itw, P);
             u64 *dst = row + gl * G;
 #pragma unroll
             for (int k = 0; k < NV; k++) NTT_ST(dst + held<LO1>(tau, k), v[k]);
@@ -573,8 +566,12 @@ __device__ __forceinline__ void ksi_intt_rows(const Tab &tab, const KsFuse &f, i
 // iterations of the digit epilogue in flight per thread: their key and partial-sum loads overlap (1 exposes every
 // load's latency: measured 497 vs 442 us per launch at 8 ciphertexts)
 constexpr int ksi_epi_unroll = KSI_CPB == 1 ? 4 : 1;
-template <int LOGN>
+template <int LOGN, class A>
 __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab, KsFuse f) {
+    // A = FpA (q < 2^46: raw transform doubles |v| <= 13 q go into the products, partial sums unreduced) or FpB
+    // (~50-bit rows: every transform value centred first, |y| <= q/2 + 1, products |mm| <= 1.29 q, partial sums
+    // centred per digit, the tensor formed canonically on the integer pipe) -- every sum stays below 2^52
+    constexpr bool FB = std::is_same<A, FpB>::value;
     using CF = ContigCfg<LOGN>;
     constexpr int S = CF::S, G = CF::G, TPG = CF::TPG, CG = CF::CG, PITCH = CF::PITCH;
     constexpr long N = 1L << LOGN;
@@ -591,6 +588,8 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
     const int jd = qrow ? e / f.alpha : -1;
     const PrimeC P = prime_consts(tab, pr);
     const double qd = P.qd, qinv = P.qinv;
+    // centred residue of an exact double |v| < 2^52.5: |result| <= q/2 (+1)
+    auto cen = [&](double v) { return __fma_rn(-__dsub_rn(__fma_rn(v, qinv, FP_MAGIC), FP_MAGIC), qd, v); };
     const long boff = (long)blockIdx.x * CG * G;
     const ulonglong2 *tw = tab.tw2 + pr * N;
     const int gl = threadIdx.x / TPG, tau = threadIdx.x % TPG;
@@ -611,87 +610,7 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
     };
     const long lo = (long)threadIdx.x * 16;  // this thread's 128-byte line of a tile (L2 prefetches)
     int nd = 0;
-    if (KSI_DPB == 2 && f.pairs) {
-    // digits in pairs: both tiles transformed into their own shared buffers, then ONE epilogue pass multiplies both
-    // with their keys (twice the independent loads per iteration, half the partial-sum round trips)
-    static_assert(KSI_DPB != 2 || KSI_CPB == 1, "digit pairs: one ciphertext per CTA");
-    for (int ja = next_digit(-1); ja >= 0;) {
-        const int jb0 = next_digit(ja), ng = jb0 >= 0 ? 2 : 1, jn = jb0 >= 0 ? next_digit(jb0) : -1;
-        const bool fin = jn < 0 && !qrow;  // the last terms of a special row: canonicalise
-#pragma unroll 1
-        for (int h = 0; h < ng; h++) {
-            const int j = h ? jb0 : ja;
-#if NTT_KSI_PREFETCH
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(keyrow + (long)(2 * j) * nk * N + lo));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(keyrow + (long)(2 * j + 1) * nk * N + lo));
-#endif
-            u64 *const smg = ksi_sm + h * CG * PITCH + gl * PITCH;
-            const u64 *src = f.ext + c0 * f.exts + ((long)j * ne + e) * N + boff + gl * G;
-            const ulonglong2 *twu;
-            asm volatile("mov.b64 %0, %1;" : "=l"(twu) : "l"(tw));
-            u64 v[NV];
-#pragma unroll
-            for (int k = 0; k < NV; k++) v[k] = NTT_LD(src + held<LO0>(tau, k));  // first-pass representation
-            do_round<S, false, 0, true, LOGN, FpA>(v, tau, g, twu, P);
-#pragma unroll
-            for (int k = 0; k < NV; k++) smg[padr(held<LO0>(tau, k))] = v[k];
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < NV; k++) v[k] = smg[padr(held<LO1>(tau, k))];
-            do_round<S, false, 1, true, LOGN, FpA>(v, tau, g, twu, P);
-#pragma unroll
-            for (int k = 0; k < NV; k++) smg[padr(held<LO1>(tau, k))] = v[k];
-        }
-        __syncthreads();
-        const int jb = ng > 1 ? jb0 : ja;
-        const ulonglong2 *kba = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * ja) * nk * N);
-        const ulonglong2 *kaa = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * ja + 1) * nk * N);
-        const ulonglong2 *kbb = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * jb) * nk * N);
-        const ulonglong2 *kab = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * jb + 1) * nk * N);
-        ulonglong2 *acc0 = reinterpret_cast<ulonglong2 *>(accb(0)), *acc1 = reinterpret_cast<ulonglong2 *>(accb(0) + a1off);
-        const u64 *smb = ksi_sm + CG * PITCH;
-#pragma unroll 2
-        for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
-            const int el = 2 * i, gg = el / G, r = el % G;
-            const ulonglong2 KB = __ldg(kba + i), KA = __ldg(kaa + i);
-            const double x0 = FpA::D(ksi_sm[gg * PITCH + padr(r)]), x1 = FpA::D(ksi_sm[gg * PITCH + padr(r + 1)]);
-            double s00, s01, s10, s11;
-            {
-                const double B0 = fx(KB.x), B1 = fx(KB.y), A0 = fx(KA.x), A1 = fx(KA.y);
-                s00 = fpt::mm(x0, B0, __dmul_rn(B0, qinv), qd);
-                s01 = fpt::mm(x1, B1, __dmul_rn(B1, qinv), qd);
-                s10 = fpt::mm(x0, A0, __dmul_rn(A0, qinv), qd);
-                s11 = fpt::mm(x1, A1, __dmul_rn(A1, qinv), qd);
-            }
-            if (ng > 1) {
-                const ulonglong2 KB2 = __ldg(kbb + i), KA2 = __ldg(kab + i);
-                const double y0 = FpA::D(smb[gg * PITCH + padr(r)]), y1 = FpA::D(smb[gg * PITCH + padr(r + 1)]);
-                const double B0 = fx(KB2.x), B1 = fx(KB2.y), A0 = fx(KA2.x), A1 = fx(KA2.y);
-                s00 = __dadd_rn(s00, fpt::mm(y0, B0, __dmul_rn(B0, qinv), qd));
-                s01 = __dadd_rn(s01, fpt::mm(y1, B1, __dmul_rn(B1, qinv), qd));
-                s10 = __dadd_rn(s10, fpt::mm(y0, A0, __dmul_rn(A0, qinv), qd));
-                s11 = __dadd_rn(s11, fpt::mm(y1, A1, __dmul_rn(A1, qinv), qd));
-            }
-            if (nd > 0) {
-                const ulonglong2 p0 = acc0[i], p1 = acc1[i];
-                s00 = __dadd_rn(s00, FpA::D(p0.x));
-                s01 = __dadd_rn(s01, FpA::D(p0.y));
-                s10 = __dadd_rn(s10, FpA::D(p1.x));
-                s11 = __dadd_rn(s11, FpA::D(p1.y));
-            }
-            if (fin) {
-                acc0[i] = make_ulonglong2(fp_canon4(s00, P.q, qd, qinv), fp_canon4(s01, P.q, qd, qinv));
-                acc1[i] = make_ulonglong2(fp_canon4(s10, P.q, qd, qinv), fp_canon4(s11, P.q, qd, qinv));
-            } else {
-                acc0[i] = make_ulonglong2(FpA::B(s00), FpA::B(s01));
-                acc1[i] = make_ulonglong2(FpA::B(s10), FpA::B(s11));
-            }
-        }
-        __syncthreads();  // the next pair's round 0 rewrites the shared tiles
-        nd += ng;
-        ja = jn;
-    }
-    } else {
+    {
     for (int j = next_digit(-1); j >= 0; j = next_digit(j)) {
         const bool fin = nd == ndig - 1 && !qrow;  // the last term of a special row: canonicalise
 #if NTT_KSI_PREFETCH
@@ -710,13 +629,13 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
             u64 v[NV];
 #pragma unroll
             for (int k = 0; k < NV; k++) v[k] = NTT_LD(src + held<LO0>(tau, k));  // first-pass representation
-            do_round<S, false, 0, true, LOGN, FpA>(v, tau, g, twu, P);
+            do_round<S, false, 0, true, LOGN, A>(v, tau, g, twu, P);
 #pragma unroll
             for (int k = 0; k < NV; k++) smg[padr(held<LO0>(tau, k))] = v[k];
             __syncthreads();
 #pragma unroll
             for (int k = 0; k < NV; k++) v[k] = smg[padr(held<LO1>(tau, k))];
-            do_round<S, false, 1, true, LOGN, FpA>(v, tau, g, twu, P);
+            do_round<S, false, 1, true, LOGN, A>(v, tau, g, twu, P);
             // no barrier: each thread rewrites exactly the words it read for round 1
 #pragma unroll
             for (int k = 0; k < NV; k++) smg[padr(held<LO1>(tau, k))] = v[k];
@@ -735,7 +654,11 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
             for (int u = 0; u < KSI_CPB; u++) {
                 if (u >= nc) break;
                 const u64 *sm = ksi_sm + u * CG * PITCH;
-                const double x0 = FpA::D(sm[gg * PITCH + padr(r)]), x1 = FpA::D(sm[gg * PITCH + padr(r + 1)]);
+                double x0 = FpA::D(sm[gg * PITCH + padr(r)]), x1 = FpA::D(sm[gg * PITCH + padr(r + 1)]);
+                if (FB) {
+                    x0 = cen(x0);
+                    x1 = cen(x1);
+                }
                 double s00 = fpt::mm(x0, B0, B0q, qd), s01 = fpt::mm(x1, B1, B1q, qd);
                 double s10 = fpt::mm(x0, A0, A0q, qd), s11 = fpt::mm(x1, A1, A1q, qd);
                 ulonglong2 *acc0 = reinterpret_cast<ulonglong2 *>(accb(u)), *acc1 = reinterpret_cast<ulonglong2 *>(accb(u) + a1off);
@@ -749,6 +672,9 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
                 if (fin) {
                     acc0[i] = make_ulonglong2(fp_canon4(s00, P.q, qd, qinv), fp_canon4(s01, P.q, qd, qinv));
                     acc1[i] = make_ulonglong2(fp_canon4(s10, P.q, qd, qinv), fp_canon4(s11, P.q, qd, qinv));
+                } else if (FB) {
+                    acc0[i] = make_ulonglong2(FpA::B(cen(s00)), FpA::B(cen(s01)));
+                    acc1[i] = make_ulonglong2(FpA::B(cen(s10)), FpA::B(cen(s11)));
                 } else {
                     acc0[i] = make_ulonglong2(FpA::B(s00), FpA::B(s01));
                     acc1[i] = make_ulonglong2(FpA::B(s10), FpA::B(s11));
@@ -760,7 +686,7 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
     }
     }
     if (!qrow) {
-        ksi_intt_rows<LOGN>(tab, f, e, pr, P, boff, c0, nc, a1off, ksi_sm);
+        ksi_intt_rows<LOGN, A>(tab, f, e, pr, P, boff, c0, nc, a1off, ksi_sm);
         return;
     }
     if (!f.ten.a.p) {
@@ -789,13 +715,14 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
                 acc1[i] = make_ulonglong2(fp_canon4(s10, P.q, qd, qinv), fp_canon4(s11, P.q, qd, qinv));
             }
         }
-        ksi_intt_rows<LOGN>(tab, f, e, pr, P, boff, c0, nc, a1off, ksi_sm);
+        ksi_intt_rows<LOGN, A>(tab, f, e, pr, P, boff, c0, nc, a1off, ksi_sm);
         return;
     }
     // Q rows: the tensor (formed on the fly, tensor1_fp_raw) -- d2 with the own digit's key, [P] d0 / [P] d1
     const TensorSrc &T = f.ten;
     const bool lin = T.x.p != nullptr, lin2 = T.x2.p != nullptr, p2 = T.a2.p != nullptr;
     const u64 cc = lin ? T.C.c[e] : 0, c2 = lin2 ? T.C2.c[e] : 0;
+    const u64 ccsh = lin ? T.C.csh[e] : 0, c2sh = lin2 ? T.C2.csh[e] : 0, br0 = tab.br0[pr], br1 = tab.br1[pr];
     const double PM = fx(f.pmod[e]), PMq = __dmul_rn(PM, qinv);
     const u64 *kb1 = keyrow + (long)(2 * jd) * nk * N, *ka1 = keyrow + (long)(2 * jd + 1) * nk * N;
     const long o = (long)e * N + boff;
@@ -812,8 +739,19 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
             const u64 u0 = p2 ? at(T.a2, 0) : 0, u1 = p2 ? at(T.a2, 1) : 0;
             const u64 w0 = p2 ? at(T.b2, 0) : 0, w1 = p2 ? at(T.b2, 1) : 0;
             double e0, e1, e2;
-            tensor1_fp_raw(at(T.a, 0), at(T.a, 1), at(T.b, 0), at(T.b, 1), lin, x0, x1, cc, lin2, y0, y1, c2, qd, qinv, e0,
-                           e1, e2, p2, u0, u1, w0, w1);
+            if (FB) {
+                // ~50-bit rows: up to six raw products could pass 2^53, so the tensor is formed canonically (128-bit
+                // MACs + Barrett, the integer kernels' arithmetic)
+                u64 d0, d1, d2;
+                tensor1(at(T.a, 0), at(T.a, 1), at(T.b, 0), at(T.b, 1), lin, x0, x1, cc, ccsh, lin2, y0, y1, c2, c2sh, P.q,
+                        br0, br1, d0, d1, d2, p2, u0, u1, w0, w1);
+                e0 = fx(d0);
+                e1 = fx(d1);
+                e2 = fx(d2);
+            } else {
+                tensor1_fp_raw(at(T.a, 0), at(T.a, 1), at(T.b, 0), at(T.b, 1), lin, x0, x1, cc, lin2, y0, y1, c2, qd, qinv,
+                               e0, e1, e2, p2, u0, u1, w0, w1);
+            }
             double s0 = __dadd_rn(fpt::mm(e2, KBd, KBq, qd), fpt::mm(e0, PM, PMq, qd));
             double s1 = __dadd_rn(fpt::mm(e2, KAd, KAq, qd), fpt::mm(e1, PM, PMq, qd));
             u64 *o0p = accb(u), *o1p = accb(u) + a1off;
@@ -825,7 +763,7 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
             o1p[i] = fp_canon4(s1, P.q, qd, qinv);
         }
     }
-    ksi_intt_rows<LOGN>(tab, f, e, pr, P, boff, c0, nc, a1off, ksi_sm);
+    ksi_intt_rows<LOGN, A>(tab, f, e, pr, P, boff, c0, nc, a1off, ksi_sm);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1512,15 +1450,13 @@ void launch_ks_inner(const Tab &tab, const KsFuse &f, cudaStream_t st) {
     using CF = ContigCfg<LOGN>;
     const int ne = f.nl + f.np;
     const dim3 grid((unsigned)((1L << LOGN) / (CF::CG * CF::G)), (unsigned)(ne * ((f.n_ct + KSI_CPB - 1) / KSI_CPB)));
-    auto kern = ntt_ks_inner_kernel<LOGN>;
-    // digit pairs only where rows have three or more digits (a second tile costs residency; measured in the step)
-    const int smem = (f.pairs ? 2 : KSI_CPB) * CF::CG * CF::PITCH * 8;
-    static bool done = false;
-    if (!done) {
-        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        std::max(2, KSI_CPB) * CF::CG * CF::PITCH * 8));
-        max_smem_carveout(kern);
-        done = true;
+    auto kern = f.fpb ? ntt_ks_inner_kernel<LOGN, FpB> : ntt_ks_inner_kernel<LOGN, FpA>;
+    const int smem = KSI_CPB * CF::CG * CF::PITCH * 8;
+    static bool done[2] = {false, false};
+    if (!done[f.fpb]) {
+        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        done[f.fpb] = true;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
@@ -1539,7 +1475,6 @@ void launch_ks_inner(const Tab &tab, const KsFuse &f, cudaStream_t st) {
 void ntt_ks_inner(const Tab &tab, int logn, const KsFuse &f0, cudaStream_t st) {
     if (f0.n_ct <= 0) return;
     KsFuse f = f0;
-    f.pairs = KSI_DPB == 2 && KSI_CPB == 1 && f.beta >= KSI_PAIR_MIN_BETA;
     // profiling: the second half of every digit row's transform (8 N per limb) plus the operands the fused inner
     // product reads and writes (key once per batch, tensor inputs of the Q rows, the acc rows)
     const double N = (double)(1L << logn);
