@@ -281,25 +281,24 @@ static void ks_modup(Ctx &c, const u64 *d, long d_stride, int n, int level, DevB
 #ifndef SECPE_KS_FUSE_INTT
 #define SECPE_KS_FUSE_INTT 1  // the fused kernel also runs the ModDown INTT's first pass on its rows
 #endif
-// returns 0: separate kernels; 1: fused, every row FpA (q < 2^46); 2: fused, every row FpB (~50-bit, N >= 2^15)
-static int ks_fuse_ok(const Ctx &c, int level) {
+// SECPE_KS_FUSE: 2 (default) fused ModUp pass 2 + key inner product when every row of Q_level u P is an exact-FP64
+// row (FpA or FpB); 1 on every level (integer rows too: bit-exact, measured slower -- configs[2] 4234 -> 3766 ops/s,
+// single N = 2^16 bootstrap 28.2 -> 30.9 ms); 3 only when every row is FpA; 0 never
+static bool ks_fuse_ok(const Ctx &c, int level) {
     static int on = -1;
     if (on < 0) {
         const char *e = getenv("SECPE_KS_FUSE");
-        on = e ? atoi(e) : 1;
+        on = e ? atoi(e) : 2;
     }
-    if (!on || c.beta(level) > 4) return 0;
+    if (!on || c.beta(level) > 4) return false;
+    if (on == 1) return true;
     const int nl = level + 1;
-    auto all = [&](u64 mask) {
-        for (int i = 0; i < nl; i++)
-            if (i >= 64 || !((mask >> i) & 1)) return false;
-        for (int p = 0; p < c.np; p++)
-            if (c.nq + p >= 64 || !((mask >> (c.nq + p)) & 1)) return false;
-        return true;
-    };
-    if (all(c.tab.fp_mask)) return 1;
-    if (all(c.tab.fpb_mask) && on != 2) return 2;  // SECPE_KS_FUSE=2: exact-FP64 (q < 2^46) rows only
-    return 0;
+    const u64 mask = on == 3 ? c.tab.fp_mask : (c.tab.fp_mask | c.tab.fpb_mask);
+    for (int i = 0; i < nl; i++)
+        if (i >= 64 || !((mask >> i) & 1)) return false;
+    for (int p = 0; p < c.np; p++)
+        if (c.nq + p >= 64 || !((mask >> (c.nq + p)) & 1)) return false;
+    return true;
 }
 
 // 3. inner product of the ModUp digits with the switching key (galois > 1: of sigma_g of the digits)
@@ -319,13 +318,13 @@ static void ks_inner(Ctx &c, const u64 *d, long d_stride, int n, int level, cons
 static bool ks_modup_inner(Ctx &c, const u64 *d, long d_stride, int n, int level, const u64 *key, DevBuf &acc,
                            const TensorSrc *ten = nullptr, int intt_row0 = -1) {
     DevBuf ext;
-    if (const int fz = ks_fuse_ok(c, level)) {
+    if (ks_fuse_ok(c, level)) {
         ks_modup(c, d, d_stride, n, level, ext, ten, true);
         const long N = c.N;
         const int nl = level + 1, ne = nl + c.np, bt = c.beta(level);
         acc = DevBuf((size_t)n * 2L * ne * N, c.st);
         KsFuse f{ext.p, (long)bt * ne * N, key, acc.p, 2L * ne * N, n, nl, c.np, c.nq, c.alpha, bt,
-                 ten ? *ten : TensorSrc{}, c.pmod.p, d, d_stride, SECPE_KS_FUSE_INTT ? intt_row0 : -1, fz == 2};
+                 ten ? *ten : TensorSrc{}, c.pmod.p, d, d_stride, SECPE_KS_FUSE_INTT ? intt_row0 : -1};
         NttSpans spans{&c};
         const NttProfHook hook{&spans, ntt_mark};
         if (c.prof.on) ntt_set_prof_hook(&hook);

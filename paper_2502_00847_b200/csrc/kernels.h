@@ -151,7 +151,7 @@ struct KsFuse {
     long d_stride;
     int intt_row0;    // >= 0: rows e >= intt_row0 (the ModDown's INTT rows) also get the inverse NTT's first pass,
                       // in place (finish them with ntt_inverse_last_pass); -1: none
-    int fpb = 0;      // 1: every row is a ~50-bit exact-FP64 row (FpB policy), 0: every row FpA (q < 2^46)
+    int e0 = 0, e1 = 0;  // set by ntt_ks_inner: the launch's rows (one run of one prime class: FpA, FpB or integer)
 };
 void ntt_ks_inner(const Tab &tab, int logn, const KsFuse &f, cudaStream_t st);
 // the inverse NTT's last pass only (its first pass already ran, e.g. inside ntt_ks_inner): f.k / f.ksh factors

@@ -567,20 +567,23 @@ __device__ __forceinline__ void ksi_intt_rows(const Tab &tab, const KsFuse &f, i
 // load's latency: measured 497 vs 442 us per launch at 8 ciphertexts)
 constexpr int ksi_epi_unroll = KSI_CPB == 1 ? 4 : 1;
 template <int LOGN, class A>
-__global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab, KsFuse f) {
-    // A = FpA (q < 2^46: raw transform doubles |v| <= 13 q go into the products, partial sums unreduced) or FpB
-    // (~50-bit rows: every transform value centred first, |y| <= q/2 + 1, products |mm| <= 1.29 q, partial sums
-    // centred per digit, the tensor formed canonically on the integer pipe) -- every sum stays below 2^52
+__device__ __forceinline__ void ksi_body(const Tab &tab, const KsFuse &f) {
+    // A = the row's policy.  FpA (q < 2^46): raw transform doubles |v| <= 13 q go into the products, partial sums
+    // unreduced.  FpB (~50-bit rows): every transform value centred first, |y| <= q/2 + 1, products |mm| <= 1.29 q,
+    // partial sums centred per digit, the tensor formed canonically on the integer pipe -- every sum < 2^52.
+    // IntA (larger primes): the transform canonicalised, 128-bit products (+ the parked canonical partial sum) and
+    // one Barrett reduction per digit, the integer tensor -- the arithmetic of ks_inner_ten1_kernel's integer path.
     constexpr bool FB = std::is_same<A, FpB>::value;
+    constexpr bool IA = std::is_same<A, IntA>::value;
+    extern __shared__ __align__(16) u64 ksi_sm[];  // [KSI_CPB][CG * PITCH]
     using CF = ContigCfg<LOGN>;
     constexpr int S = CF::S, G = CF::G, TPG = CF::TPG, CG = CF::CG, PITCH = CF::PITCH;
     constexpr long N = 1L << LOGN;
     using R = Rnd<S, false>;
     constexpr int LO0 = R::lo(0), LO1 = R::lo(1);
     // KSI_CPB ciphertexts per CTA (one padded tile each): every key word loaded serves all of them
-    extern __shared__ __align__(16) u64 ksi_sm[];  // [KSI_CPB][CG * PITCH]
     const int ncg = (f.n_ct + KSI_CPB - 1) / KSI_CPB;
-    const int e = blockIdx.y / ncg, c0 = (blockIdx.y % ncg) * KSI_CPB;
+    const int e = f.e0 + blockIdx.y / ncg, c0 = (blockIdx.y % ncg) * KSI_CPB;
     const int nc = min(KSI_CPB, f.n_ct - c0);
     const int ne = f.nl + f.np, nk = f.nq_total + f.np;
     const bool qrow = e < f.nl;
@@ -643,6 +646,31 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
         __syncthreads();
         const ulonglong2 *kb = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * j) * nk * N);
         const ulonglong2 *ka = reinterpret_cast<const ulonglong2 *>(keyrow + (long)(2 * j + 1) * nk * N);
+        if constexpr (IA) {
+            const u64 r0 = tab.br0[pr], r1 = tab.br1[pr];
+#pragma unroll 2
+            for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
+                const int el = 2 * i, gg = el / G, r = el % G;
+                const ulonglong2 KB = __ldg(kb + i), KA = __ldg(ka + i);
+#pragma unroll
+                for (int u = 0; u < KSI_CPB; u++) {
+                    if (u >= nc) break;
+                    const u64 *sm = ksi_sm + u * CG * PITCH;
+                    const u64 x0 = IntA::out_fwd(sm[gg * PITCH + padr(r)], P), x1 = IntA::out_fwd(sm[gg * PITCH + padr(r + 1)], P);
+                    U128 t00 = mul_wide(x0, KB.x), t01 = mul_wide(x1, KB.y), t10 = mul_wide(x0, KA.x), t11 = mul_wide(x1, KA.y);
+                    ulonglong2 *acc0 = reinterpret_cast<ulonglong2 *>(accb(u)), *acc1 = reinterpret_cast<ulonglong2 *>(accb(u) + a1off);
+                    if (nd > 0) {
+                        const ulonglong2 p0 = acc0[i], p1 = acc1[i];
+                        add_wide(t00, U128{p0.x, 0});
+                        add_wide(t01, U128{p0.y, 0});
+                        add_wide(t10, U128{p1.x, 0});
+                        add_wide(t11, U128{p1.y, 0});
+                    }
+                    acc0[i] = make_ulonglong2(barrett128(t00, P.q, r0, r1), barrett128(t01, P.q, r0, r1));
+                    acc1[i] = make_ulonglong2(barrett128(t10, P.q, r0, r1), barrett128(t11, P.q, r0, r1));
+                }
+            }
+        } else
 #pragma unroll (ksi_epi_unroll)
         for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
             const int el = 2 * i, gg = el / G, r = el % G;
@@ -697,6 +725,24 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
         for (int u = 0; u < nc; u++) {
             const ulonglong2 *dp = reinterpret_cast<const ulonglong2 *>(f.d + (c0 + u) * f.d_stride + (long)e * N + boff);
             ulonglong2 *acc0 = reinterpret_cast<ulonglong2 *>(accb(u)), *acc1 = reinterpret_cast<ulonglong2 *>(accb(u) + a1off);
+            if constexpr (IA) {
+                const u64 r0 = tab.br0[pr], r1 = tab.br1[pr];
+#pragma unroll 2
+                for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
+                    const ulonglong2 X = dp[i], KB = __ldg(kb + i), KA = __ldg(ka + i);
+                    U128 t00 = mul_wide(X.x, KB.x), t01 = mul_wide(X.y, KB.y), t10 = mul_wide(X.x, KA.x),
+                         t11 = mul_wide(X.y, KA.y);
+                    if (nd > 0) {
+                        const ulonglong2 p0 = acc0[i], p1 = acc1[i];
+                        add_wide(t00, U128{p0.x, 0});
+                        add_wide(t01, U128{p0.y, 0});
+                        add_wide(t10, U128{p1.x, 0});
+                        add_wide(t11, U128{p1.y, 0});
+                    }
+                    acc0[i] = make_ulonglong2(barrett128(t00, P.q, r0, r1), barrett128(t01, P.q, r0, r1));
+                    acc1[i] = make_ulonglong2(barrett128(t10, P.q, r0, r1), barrett128(t11, P.q, r0, r1));
+                }
+            } else
 #pragma unroll 2
             for (int i = threadIdx.x; i < CG * G / 2; i += CT) {
                 const ulonglong2 X = dp[i], KB = __ldg(kb + i), KA = __ldg(ka + i);
@@ -738,6 +784,23 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
             const u64 y0 = lin2 ? at(T.x2, 0) : 0, y1 = lin2 ? at(T.x2, 1) : 0;
             const u64 u0 = p2 ? at(T.a2, 0) : 0, u1 = p2 ? at(T.a2, 1) : 0;
             const u64 w0 = p2 ? at(T.b2, 0) : 0, w1 = p2 ? at(T.b2, 1) : 0;
+            if constexpr (IA) {
+                u64 d0, d1, d2;
+                tensor1(at(T.a, 0), at(T.a, 1), at(T.b, 0), at(T.b, 1), lin, x0, x1, cc, ccsh, lin2, y0, y1, c2, c2sh, P.q,
+                        br0, br1, d0, d1, d2, p2, u0, u1, w0, w1);
+                const u64 KBw = __ldg(kb1 + i), KAw = __ldg(ka1 + i), pm = f.pmod[e];
+                U128 t0 = mul_wide(d2, KBw), t1 = mul_wide(d2, KAw);
+                mac_wide(t0, d0, pm);
+                mac_wide(t1, d1, pm);
+                u64 *o0p = accb(u), *o1p = accb(u) + a1off;
+                if (nd > 0) {
+                    add_wide(t0, U128{o0p[i], 0});
+                    add_wide(t1, U128{o1p[i], 0});
+                }
+                o0p[i] = barrett128(t0, P.q, br0, br1);
+                o1p[i] = barrett128(t1, P.q, br0, br1);
+                continue;
+            }
             double e0, e1, e2;
             if (FB) {
                 // ~50-bit rows: up to six raw products could pass 2^53, so the tensor is formed canonically (128-bit
@@ -764,6 +827,21 @@ __global__ void __launch_bounds__(CT, NTT_KSI_MINB) ntt_ks_inner_kernel(Tab tab,
         }
     }
     ksi_intt_rows<LOGN, A>(tab, f, e, pr, P, boff, c0, nc, a1off, ksi_sm);
+}
+
+// one launch per run of rows of one class (the ModUp digits of a level can mix the ~50-bit FpB rows with a 60-bit q_0,
+// as the bootstrapping chains do): rows [f.e0, f.e1) of the level, each CTA with its class's policy
+template <class A>
+struct KsiMinB {
+    static constexpr int v = NTT_KSI_MINB;
+};
+template <>
+struct KsiMinB<IntA> {
+    static constexpr int v = 2;  // 128-bit products and Barrett reductions: 80 registers spill
+};
+template <int LOGN, class A>
+__global__ void __launch_bounds__(CT, KsiMinB<A>::v) ntt_ks_inner_kernel(Tab tab, KsFuse f) {
+    ksi_body<LOGN, A>(tab, f);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1445,18 +1523,18 @@ void ntt_segments_pass1(const Tab &tab, int logn, const NttSeg *segs, int nseg, 
 }
 
 namespace {
-template <int LOGN>
-void launch_ks_inner(const Tab &tab, const KsFuse &f, cudaStream_t st) {
+template <int LOGN, class A>
+void launch_ks_inner_a(const Tab &tab, const KsFuse &f, cudaStream_t st) {
     using CF = ContigCfg<LOGN>;
-    const int ne = f.nl + f.np;
-    const dim3 grid((unsigned)((1L << LOGN) / (CF::CG * CF::G)), (unsigned)(ne * ((f.n_ct + KSI_CPB - 1) / KSI_CPB)));
-    auto kern = f.fpb ? ntt_ks_inner_kernel<LOGN, FpB> : ntt_ks_inner_kernel<LOGN, FpA>;
+    const dim3 grid((unsigned)((1L << LOGN) / (CF::CG * CF::G)),
+                    (unsigned)((f.e1 - f.e0) * ((f.n_ct + KSI_CPB - 1) / KSI_CPB)));
+    auto kern = ntt_ks_inner_kernel<LOGN, A>;
     const int smem = KSI_CPB * CF::CG * CF::PITCH * 8;
-    static bool done[2] = {false, false};
-    if (!done[f.fpb]) {
+    static bool done = false;
+    if (!done) {
         CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        done[f.fpb] = true;
+        done = true;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
@@ -1469,6 +1547,31 @@ void launch_ks_inner(const Tab &tab, const KsFuse &f, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, tab, f));
+}
+template <int LOGN>
+void launch_ks_inner(const Tab &tab, const KsFuse &f0, cudaStream_t st) {
+    // rows e of the level in order (Q rows 0..nl-1, then the special rows), split into runs of one prime class
+    const int ne = f0.nl + f0.np;
+    auto cls_of = [&](int e) {
+        const int pr = e < f0.nl ? e : f0.nq_total + (e - f0.nl);
+        return prime_cls(tab, pr);
+    };
+    int e0 = 0;
+    while (e0 < ne) {
+        const int cls = cls_of(e0);
+        int e1 = e0 + 1;
+        while (e1 < ne && cls_of(e1) == cls) e1++;
+        KsFuse f = f0;
+        f.e0 = e0;
+        f.e1 = e1;
+        if (cls == CLS_FPA)
+            launch_ks_inner_a<LOGN, FpA>(tab, f, st);
+        else if (cls == CLS_FPB)
+            launch_ks_inner_a<LOGN, FpB>(tab, f, st);
+        else
+            launch_ks_inner_a<LOGN, IntA>(tab, f, st);
+        e0 = e1;
+    }
 }
 }  // namespace
 
