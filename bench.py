@@ -92,6 +92,14 @@ def cpu_model():
     return "unknown"
 
 
+def workload_config(B, ws, queries, ct_words, n_rot, nq, np_, alpha, N):
+    """`config` of the JSON line (both arms print the same dict for the same --batch / world size)."""
+    return {"workload": WORKLOAD, "ciphertexts_per_rank_per_step": B, "queries_per_ciphertext": queries,
+            "parallelism": "ciphertexts sharded over ranks (replicated keys)" if ws > 1 else "single GPU",
+            "l2": "inputs larger than L2 (%.0f MB ciphertexts + %.0f MB keys per rank)" % (
+                B * ct_words * 8 / 1e6, (n_rot + 1) * -(-nq // alpha) * 2 * (nq + np_) * N * 8 / 1e6)}
+
+
 class OracleArgmax:
     """The CPU oracle's full argmax of ONE configs[4] ciphertext (2048 queries); keys and the input are
     built once, run() times plan.argmax only.  Returns (seconds, queries, threads actually used)."""
@@ -154,6 +162,9 @@ def oracle_argmax_once(seed_base=1):
     return OracleArgmax(seed_base).run()
 
 
+REF_CAP_S = 600.0  # safety cap on the reference arm's timed region (a default-sized run never reaches it)
+
+
 def run_reference(a):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -161,24 +172,27 @@ def run_reference(a):
     ora = OracleArgmax()
     for _ in range(a.warmup if a.ref_warmup else 0):
         ora.run()
-    # each step is one full ciphertext (2048 queries); the timed steps are capped at ~150 s of CPU work so
-    # the arm finishes within a few minutes whatever --steps asks for
+    # each step is one full ciphertext of the workload (2048 queries, ~13 s on 16 cores): --steps 20 ends in
+    # about 4.5 minutes.  The cap only guards against a much slower host or a very large --steps.
     times, q, cores = [], 0, 1
     for _ in range(a.steps):
         dt, q, cores = ora.run()
         times.append(dt)
-        if sum(times) > 150.0:
+        if sum(times) > REF_CAP_S:
             break
     n = len(times)
     T = sum(times)
     v = q * n / T
     sample = ("1 ciphertext (2048 queries x P=8 x K=2, full argmax circuit) per step, %d of %d requested steps "
-              "timed (capped at ~150 s); warm-up steps %s" % (n, a.steps, "run" if a.ref_warmup else
-                                                              "skipped (CPU oracle has no warm-up state)"))
+              "timed%s; warm-up steps %s" % (n, a.steps, "" if n == a.steps else " (capped at %.0f s)" % REF_CAP_S,
+                                             "run" if a.ref_warmup else "skipped (CPU oracle has no warm-up state)"))
+    prm, lay = ora.ev.prm, ora.lay
+    cfg = workload_config(a.batch, ws, lay["queries"], 2 * prm.nq * prm.N, len(ora.plan.argmax_rotations(lay)),
+                          prm.nq, prm.np_, prm.alpha, prm.N)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": n,
             "steps_requested": a.steps, "warmup": a.warmup, "ms_per_step": 1000 * T / n, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64 (RNS residues)", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "batch_per_step": 1},
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64 (RNS residues mod 45/60-bit primes)", "data": "synthetic",
+            "config": cfg,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
                              "cpu_model": cpu_model(), "logical_cpus": os.cpu_count()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -686,11 +700,8 @@ def run_secpe(a):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u64 (RNS residues mod 45/60-bit primes)", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "ciphertexts_per_rank_per_step": B, "queries_per_ciphertext": lay["queries"],
-                   "parallelism": "ciphertexts sharded over ranks (replicated keys)" if ws > 1 else "single GPU",
-                   "l2": "inputs larger than L2 (%.0f MB ciphertexts + %.0f MB keys per rank)" % (
-                       B * inp.t[0].numel() * 8 / 1e6,
-                       (len(steps_rot) + 1) * -(-ctx.nq // ctx.alpha) * 2 * (ctx.nq + ctx.np_) * ctx.N * 8 / 1e6)},
+        "config": workload_config(B, ws, lay["queries"], inp.t[0].numel(), len(steps_rot), ctx.nq, ctx.np_,
+                                  ctx.alpha, ctx.N),
         "roofline": {"bound": "hbm", "kernel": "ntt family on the 45-bit (FP64) rows: every forward/inverse launch in the "
                                                 "profiled region incl. the fused ModUp pass 2 + key inner product "
                                                 "(ntt_ks_inner_kernel) and the fused prologues/epilogues (%.0f limb "
