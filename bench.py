@@ -565,7 +565,10 @@ def run_secpe(a):
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if ws > 1:
+    # NCCL plumbing (barriers + max-over-ranks) for N > 1; SECPE_DIST_SINGLE=1 runs the same path with one rank
+    # (the 1-GPU box's check that the torchrun / NCCL code path executes)
+    use_dist = ws > 1 or (os.environ.get("SECPE_DIST_SINGLE") == "1" and "MASTER_ADDR" in os.environ)
+    if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     build.build()
     stream = torch.cuda.Stream()
@@ -609,7 +612,7 @@ def run_secpe(a):
         torch.cuda.profiler.stop()
         print(json.dumps({"ncu_step": True, "batch": B, "launches": ctx.opcounts(reset=True)["launches"]}))
         return
-    if ws > 1:
+    if use_dist:
         dist.barrier()
     clocks = Clocks(local)
     clocks.start()
@@ -624,7 +627,7 @@ def run_secpe(a):
     counts = ctx.opcounts(reset=True)
     clk = clocks.stop()
     ms = shard.max_over_ranks(e0.elapsed_time(e1), device="cuda")  # slowest rank's device time
-    if ws > 1:
+    if use_dist:
         dist.barrier()
     # roofline: the same K steps again with CUDA events recorded on the launching stream around every
     # NTT / key-switch / rescale span (kept out of the headline timing above)
@@ -648,7 +651,7 @@ def run_secpe(a):
     for _ in range(max(4, a.warmup)):  # both staging slots captured and replayed once
         ctx.enc_argmax_host(keys, h_in, L, ctx.scale, lay, st, h_out=h_out, chunk=B)
     torch.cuda.synchronize()
-    if ws > 1:
+    if use_dist:
         dist.barrier()
     fe = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
     f0, f1 = fe[0], fe[-1]
@@ -667,7 +670,7 @@ def run_secpe(a):
     accuracy = argmax_accuracy(ctx, keys, out, all_scores, lay)
 
     if rank != 0:
-        if ws > 1:
+        if use_dist:
             dist.barrier()
             dist.destroy_process_group()
         return
@@ -757,7 +760,7 @@ def run_secpe(a):
         dt, q, cores = ora.run()
         line["cpu_baseline"] = cpu_baseline_line(ora, dt, q, cores)
     print(json.dumps(line), flush=True)
-    if ws > 1:
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
 

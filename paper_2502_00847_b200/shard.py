@@ -28,7 +28,7 @@ def input_seed(config_index, global_ct):
 
 def max_over_ranks(value, device="cpu"):
     """Max of a per-rank float (the job time of a weak-scaling step is the slowest rank's)."""
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+    if not (dist.is_available() and dist.is_initialized()):
         return float(value)
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
