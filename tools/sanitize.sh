@@ -7,6 +7,8 @@ mkdir -p gpurun_out
 CS=/usr/local/cuda/bin/compute-sanitizer
 # the torchrun / NCCL code path of bench.py with one rank (init, barriers, max-over-ranks all-reduce)
 SECPE_DIST_SINGLE=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 1 --steps 5 --warmup 3 --no-micro --no-cpu-baseline > gpurun_out/nccl1.log 2>&1; echo rc=$? >> gpurun_out/nccl1.log
+# configs[1] NTT launches (60-bit rows, IntA): integer-pipe utilisation for DESIGN section 6
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:ntt --launch-skip 8 -c 6 -o gpurun_out/c1_ntt python tools/microbench.py ntt --reps 2 > gpurun_out/c1_ncu.log 2>&1; echo rc=$? >> gpurun_out/c1_ncu.log
 K="test_ntt_bit_exact or test_ops_bit_exact_toy or test_argmax_small_ring_bit_exact or test_argmax_small49_bit_exact or test_key_switching_digit_counts or test_fused_keyswitch_digit_counts or test_rotate_hoisted_bit_exact or test_empty_inputs or test_cluster_ntt_path or test_fused_ntt_matches_two_pass_and_oracle or test_integer_base_conversion_fallback"
 timeout 1200 $CS --tool memcheck --error-exitcode 9 --log-file gpurun_out/san_mem_smoke.txt python __graft_entry__.py smoke > gpurun_out/san_mem_smoke.log 2>&1; echo rc=$? >> gpurun_out/san_mem_smoke.log
 timeout 1500 $CS --tool memcheck --error-exitcode 9 --log-file gpurun_out/san_mem_tests.txt python -m pytest tests/test_gpu_parity.py -q -x -m gpu -k "$K" > gpurun_out/san_mem_tests.log 2>&1; echo rc=$? >> gpurun_out/san_mem_tests.log
