@@ -92,6 +92,12 @@ def cpu_model():
     return "unknown"
 
 
+# 60-bit (IntA) NTT: warp instructions per N = 2^16 limb transform, mean of forward (384.98 M + 452.20 M) and inverse
+# (395.97 M + 465.96 M) over 1536 rows -- ncu smsp__inst_executed.sum, profiles/r02_ncu_configs1_ntt_summary.txt
+INTA_WARP_INSTR_PER_LIMB = (384.98e6 + 452.20e6 + 395.97e6 + 465.96e6) / 2 / 1536
+SM_MAX_MHZ = 1965.0  # B200 max SM clock (MEASURED_PEAKS.json sm_max_mhz)
+
+
 def workload_config(B, ws, queries, ct_words, n_rot, nq, np_, alpha, N):
     """`config` of the JSON line (both arms print the same dict for the same --batch / world size)."""
     return {"workload": WORKLOAD, "ciphertexts_per_rank_per_step": B, "queries_per_ciphertext": queries,
@@ -232,7 +238,17 @@ def micro_configs(stream, reps=5):
     gbs = 2 * 16 * ctx.N * 64 * 24 / (ms / 1000) / 1e9
     out["configs[1]_ntt"] = {"ms_round_trip": ms, "limb_transforms_per_s": 2 * 64 * 24 / (ms / 1000),
                              "alg_gbs": gbs, "frac_of_hbm": gbs / peak,
-                             "note": "60-bit primes: integer Shoup path (FMA-pipe bound, quarter-rate IMAD.WIDE)"}
+                             # the 60-bit rows are bound by the integer instruction stream, not HBM:
+                             # issue-slot roofline = warp instructions per limb transform (ncu smsp__inst_executed.sum of
+                             # the four IntA passes / 1536 rows, profiles/r02_ncu_configs1_ntt_summary.txt) x transforms/s
+                             # over 148 SMs x 4 schedulers x 1 warp instruction per clock at the max SM clock
+                             "bound": "alu", "warp_instr_per_limb_transform": INTA_WARP_INSTR_PER_LIMB,
+                             "alu_achieved_ginstr_s": INTA_WARP_INSTR_PER_LIMB * 2 * 64 * 24 / (ms / 1000) / 1e9,
+                             "alu_peak_ginstr_s": 148 * 4 * SM_MAX_MHZ * 1e6 / 1e9,
+                             "frac_of_issue_slots": INTA_WARP_INSTR_PER_LIMB * 2 * 64 * 24 / (ms / 1000)
+                                                    / (148 * 4 * SM_MAX_MHZ * 1e6),
+                             "note": "60-bit primes: integer Shoup path; ncu: ALU pipe 46-56 %, FMA pipe 23-28 %, issue "
+                                     "51-60 %, DRAM 27-31 % of peak"}
     del ctx, x
     ctx = secpe.Context(synth.PARAM_SETS["ks"], stream=stream.cuda_stream)
     keys = ctx.keygen(synth.KEY_SEED_BASE + 3, [1 << k for k in range(15)])
@@ -750,6 +766,8 @@ def run_secpe(a):
         rf = line["roofline"]
         rf["configs1_ntt_gbs"] = c["configs[1]_ntt"]["alg_gbs"]
         rf["configs1_ntt_frac"] = c["configs[1]_ntt"]["frac_of_hbm"]
+        rf["configs1_ntt_bound"] = "alu"
+        rf["configs1_ntt_issue_slot_frac"] = c["configs[1]_ntt"]["frac_of_issue_slots"]
         rf["configs2_mul_relin_rescale_gbs"] = c["configs[2]_mul_relin_rescale"]["alg_gbs"]
         rf["configs2_mul_relin_rescale_frac"] = c["configs[2]_mul_relin_rescale"]["frac_of_hbm"]
         rf["configs3_rotation_gbs"] = c["configs[3]_rotation"]["alg_gbs"]
