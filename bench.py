@@ -700,13 +700,18 @@ def run_secpe(a):
     ops = prof.get("ntt_fp_operands", {"bytes": 0.0})
     ach_t, ks_ach = gbs(ntt), gbs(ks)
     ach = (ntt["bytes"] + ops["bytes"]) / (ntt["ms"] / 1000.0) / 1e9 if ntt["ms"] > 0 else 0.0
-    traffic, tsrc, t_over_a = None, None, None
+    traffic, tsrc, t_over_a, step_dram = None, None, None, {}
     tp = os.path.join(ROOT, "profiles", "ntt_traffic.json")
     if os.path.exists(tp):
         try:
             tj = json.load(open(tp))
             traffic, tsrc = tj["dram_bytes_per_limb_transform"], tj.get("source")
             t_over_a = tj.get("traffic_over_algorithmic")
+            # every launch of the step: the real DRAM bytes (same ncu list) over the measured step time
+            if tj.get("step_ciphertexts") == B and tj.get("step_dram_bytes"):
+                step_dram = {"step_dram_bytes": tj["step_dram_bytes"],
+                             "step_dram_gbs": tj["step_dram_bytes"] / (ms / a.steps / 1000.0) / 1e9,
+                             "step_dram_source": tj.get("step_source")}
         except Exception:
             traffic = None
     # FP64-pipe roof of the same kernels: (N/2) log2 N butterflies per limb transform, 8 FP64-pipe
@@ -749,7 +754,9 @@ def run_secpe(a):
                      "keyswitch_achieved_gbs": ks_ach, "keyswitch_frac": ks_ach / peak,
                      "keyswitch_share_of_step": ks["ms"] / ms_prof,
                      "fp64_pipe_frac": fp64_ach / fp64_peak,
-                     "rescale_share_of_step": prof["rescale"]["ms"] / ms_prof},
+                     "rescale_share_of_step": prof["rescale"]["ms"] / ms_prof,
+                     # whole step: real DRAM bytes of all its launches (ncu) over the measured step time
+                     **({**step_dram, "step_dram_frac": step_dram["step_dram_gbs"] / peak} if step_dram else {})},
         "stage_share_of_step": {k[6:]: v["ms"] / ms_prof for k, v in prof.items() if k.startswith("stage_")},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h_in.numel() * 8),
                 "d2h_bytes_per_step": int(h_out.numel() * 8)},
